@@ -1,0 +1,132 @@
+/*
+ * pauliprop_gpu.h -- C-ABI of the B200 Pauli-propagation engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (SURVEY.md section 8b).  Each entry point replaces one call of the
+ * reference's C++ operator/gate API (namespace pauliprop):
+ *
+ *   pp_create / pp_destroy      Engine::Engine(const EngineConfig&), ~Engine
+ *                               (reference include/pauliprop/engine.hpp:131-139,
+ *                                src/engine.cpp:167-190)
+ *   pp_set_initial              Engine::set_initial  (engine.hpp:145-146,
+ *                                engine.cpp:196-205)
+ *   pp_apply_gate               Engine::apply_gate   (engine.hpp:150,
+ *                                engine.cpp:277-316), including the per-gate
+ *                                truncation at cadence 0 (engine.cpp:313-315)
+ *   pp_apply_gates              a run of Engine::apply_gate calls in order
+ *                                (the inner loop of run_circuit,
+ *                                engine.cpp:414-418); lets the engine fuse
+ *                                runs of Clifford gates bit-exactly
+ *   pp_truncate_now             Engine::truncate_now (engine.cpp:318-351)
+ *   pp_term_count               Engine::term_count   (engine.cpp:353-357)
+ *   pp_global_max               Engine::global_max   (engine.hpp:158)
+ *   pp_expectation_zero_state   Engine::expectation_zero_state
+ *                                (engine.cpp:359-361, sparse_operator.cpp:89-97)
+ *   pp_coefficient              Engine::coefficient  (engine.cpp:363-366)
+ *   pp_export                   Engine::merged       (engine.cpp:375-386),
+ *                                returned sorted by key
+ *   pp_take_counters            Engine::take_counters (engine.hpp:171-178)
+ *
+ * Pauli strings cross this boundary in the reference's own packed layout
+ * (pauli_string.hpp:28-38): 4 x uint64 per string, site i in bits
+ * (2i, 2i+1) counted from the least significant end of word i/32,
+ * I=00 X=01 Y=10 Z=11, unused high bits zero.  Gate trig is computed on the
+ * host exactly as Gate::Gate does (circuit.cpp:89-93) and passed in.
+ *
+ * Return codes map onto the reference's exceptions:
+ *   0 ok
+ *   2 invalid argument   (std::invalid_argument)
+ *   3 numerical          (pauliprop::NumericalError, engine.cpp:333-339)
+ *   4 resource           (pauliprop::ResourceLimitError, engine.cpp:269-273,
+ *                         or device memory exhausted -> std::bad_alloc)
+ *   5 internal CUDA error (std::runtime_error)
+ * pp_last_error() returns the message of the last failure on the engine.
+ *
+ * Threading: one caller thread per engine, like the reference Engine
+ * (not re-entrant).  All entry points are synchronous with respect to the
+ * results they return.
+ */
+#ifndef PAULIPROP_GPU_H
+#define PAULIPROP_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PP_OK 0
+#define PP_ERR_INVALID 2
+#define PP_ERR_NUMERICAL 3
+#define PP_ERR_RESOURCE 4
+#define PP_ERR_INTERNAL 5
+
+#define PP_CADENCE_GATE 0
+#define PP_CADENCE_LAYER 1
+
+/* pp_config.flags */
+#define PP_FLAG_NO_CLIFFORD_FUSION 1u /* apply Clifford gates one by one */
+
+typedef struct pp_engine pp_engine;
+
+/* EngineConfig (engine.hpp:99-106) minus the thread pool: worker_count is
+ * kept for ledger accounting only -- results never depend on it
+ * (test_engine.cpp:211-258). */
+typedef struct {
+  int n;               /* qubits, 1..128 */
+  double epsilon0;     /* relative truncation threshold, >= 0 */
+  int cadence;         /* PP_CADENCE_GATE or PP_CADENCE_LAYER */
+  uint64_t max_terms;  /* 0 = unlimited */
+  uint32_t workers;    /* logical workers (ledger only) */
+  int device;          /* CUDA device ordinal */
+  uint32_t flags;      /* PP_FLAG_* */
+  double mem_fraction; /* share of free device memory the engine may use (0 = default 0.9) */
+} pp_config;
+
+/* Gate (circuit.hpp:46-54): generator in the packed layout + host trig. */
+typedef struct {
+  uint64_t words[4];
+  double theta;
+  double cos_theta;
+  double sin_theta;
+} pp_gate;
+
+/* Engine::Counters (engine.hpp:171-178), nanoseconds split by phase. */
+typedef struct {
+  uint64_t removed;
+  uint64_t batches_sent;
+  uint64_t records_sent;
+  uint64_t gates;
+  uint64_t branch_ns;   /* branch+merge kernels (generate+apply) */
+  uint64_t exchange_ns; /* regroup / reshuffle after Clifford runs */
+  uint64_t truncate_ns; /* max-reduce + truncation */
+  uint64_t other_ns;
+} pp_counters;
+
+int pp_create(const pp_config* config, pp_engine** out);
+void pp_destroy(pp_engine* engine);
+int pp_set_initial(pp_engine* engine, const uint64_t* words, const double* coeffs, size_t count);
+int pp_apply_gate(pp_engine* engine, const pp_gate* gate);
+int pp_apply_gates(pp_engine* engine, const pp_gate* gates, size_t count);
+int pp_truncate_now(pp_engine* engine);
+int pp_term_count(const pp_engine* engine, uint64_t* out);
+int pp_global_max(const pp_engine* engine, double* out);
+int pp_expectation_zero_state(pp_engine* engine, double* out);
+int pp_coefficient(pp_engine* engine, const uint64_t* words, double* out);
+/* Copies every live term, sorted ascending by the packed words (word 3 most
+ * significant).  cap = capacity of words (4*cap uint64) and coeffs. */
+int pp_export(pp_engine* engine, uint64_t* words, double* coeffs, uint64_t cap, uint64_t* count);
+int pp_take_counters(pp_engine* engine, pp_counters* out);
+const char* pp_last_error(const pp_engine* engine);
+
+/* Device time (ms) of the branch+merge kernel launches since the last call,
+ * with the algorithmic bytes they moved; for the roofline in bench.py. */
+int pp_take_kernel_stats(pp_engine* engine, double* branch_ms, double* branch_bytes,
+                         uint64_t* branch_launches, uint64_t* total_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PAULIPROP_GPU_H */

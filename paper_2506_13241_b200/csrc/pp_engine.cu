@@ -1,0 +1,931 @@
+// pp_engine.cu -- host orchestration of the B200 Pauli-propagation engine
+// and its C-ABI (include/pauliprop_gpu.h).
+//
+// One engine owns one CUDA device's share of the operator: a z-grouped
+// arena store (pp_kernels.cuh) plus the regroup machinery (pp_regroup.cuh).
+// The per-gate sequence mirrors Engine::apply_gate (engine.cpp:277-316):
+//   branch (+ merge)  ->  budget check  ->  [per-gate cadence] truncate
+// and truncate_now mirrors engine.cpp:318-351 (global max, NaN/Inf check,
+// threshold epsilon0 * gmax, remove |c| <= threshold).
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pauliprop_gpu.h"
+#include "pp_regroup.cuh"
+
+namespace ppgpu {
+
+struct EngineError : std::runtime_error {
+  int code;
+  EngineError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PP_CUDA(x)                                                                                  \
+  do {                                                                                              \
+    cudaError_t e_ = (x);                                                                           \
+    if (e_ != cudaSuccess) {                                                                        \
+      if (e_ == cudaErrorMemoryAllocation) {                                                        \
+        cudaGetLastError();                                                                         \
+        throw EngineError(PP_ERR_RESOURCE, std::string("device memory exhausted: ") + #x);          \
+      }                                                                                             \
+      throw EngineError(PP_ERR_INTERNAL, std::string(cudaGetErrorString(e_)) + " at " + #x);       \
+    }                                                                                               \
+  } while (0)
+
+using Clock = std::chrono::steady_clock;
+static uint64_t ns_since(Clock::time_point t) {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t).count();
+}
+
+__global__ void k_reset_stats(DevStats* st, unsigned long long bump) {
+  DevStats s;
+  memset(&s, 0, sizeof(s));
+  s.bump = bump;
+  s.gmin_bits = 0x7ff0000000000000ull;
+  *st = s;
+}
+
+// ---------------------------------------------------------------------------
+// interleaved (reference) <-> plane conversion on the host
+// ---------------------------------------------------------------------------
+static inline uint64_t compact_even(uint64_t v) {
+  v &= 0x5555555555555555ull;
+  v = (v | (v >> 1)) & 0x3333333333333333ull;
+  v = (v | (v >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v >> 4)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v >> 8)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v >> 16)) & 0x00000000FFFFFFFFull;
+  return v;
+}
+static inline uint64_t spread_even(uint64_t v) {
+  v &= 0xFFFFFFFFull;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+// words[4] -> x[2], z[2]  (x = lo ^ hi, z = hi per site)
+static void words_to_planes(const uint64_t* w, uint64_t* x, uint64_t* z) {
+  for (int pw = 0; pw < 2; ++pw) {
+    uint64_t lo = compact_even(w[2 * pw]) | (compact_even(w[2 * pw + 1]) << 32);
+    uint64_t hi = compact_even(w[2 * pw] >> 1) | (compact_even(w[2 * pw + 1] >> 1) << 32);
+    x[pw] = lo ^ hi;
+    z[pw] = hi;
+  }
+}
+static void planes_to_words(const uint64_t* x, const uint64_t* z, uint64_t* w) {
+  for (int pw = 0; pw < 2; ++pw) {
+    uint64_t hi = z[pw], lo = x[pw] ^ z[pw];
+    w[2 * pw] = spread_even(lo) | (spread_even(hi) << 1);
+    w[2 * pw + 1] = spread_even(lo >> 32) | (spread_even(hi >> 32) << 1);
+  }
+}
+
+static inline bool is_clifford(const pp_gate& g) {
+  return g.cos_theta == 0.0 && (g.sin_theta == 1.0 || g.sin_theta == -1.0);
+}
+
+// ---------------------------------------------------------------------------
+// device buffer helper
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    release();
+    size_t nb = std::max<size_t>(b, 256);
+    PP_CUDA(cudaMalloc(&p, nb));
+    bytes = nb;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() { release(); }
+};
+
+class EngineBase {
+ public:
+  virtual ~EngineBase() = default;
+  virtual void set_initial(const uint64_t* words, const double* c, size_t count) = 0;
+  virtual void apply_gates(const pp_gate* gates, size_t count) = 0;
+  virtual void truncate_now() = 0;
+  virtual uint64_t term_count() const = 0;
+  virtual double global_max() const = 0;
+  virtual double expectation() = 0;
+  virtual double coefficient(const uint64_t* words) = 0;
+  virtual uint64_t export_terms(uint64_t* words, double* c, uint64_t cap) = 0;
+  virtual pp_counters take_counters() = 0;
+  virtual void take_kernel_stats(double* ms, double* bytes, uint64_t* launches, uint64_t* total) = 0;
+};
+
+template <int W>
+class EngineImpl final : public EngineBase {
+ public:
+  explicit EngineImpl(const pp_config& cfg) : cfg_(cfg) {
+    PP_CUDA(cudaSetDevice(cfg.device));
+    PP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    PP_CUDA(cudaMalloc(&d_stats_, sizeof(DevStats)));
+    PP_CUDA(cudaMallocHost(&h_stats_, sizeof(DevStats)));
+    PP_CUDA(cudaEventCreate(&ev0_));
+    PP_CUDA(cudaEventCreate(&ev1_));
+    PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(BranchSmem<W>)));
+    PP_CUDA(cudaFuncSetAttribute(k_sort_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(SortSmem<W>)));
+    PP_CUDA(cudaFuncSetAttribute(k_sort_big<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)big_sort_smem()));
+    keep_zeros_ = cfg.cadence == PP_CADENCE_LAYER;
+    seed_ = 0x5eed5eed12345678ull;
+  }
+  ~EngineImpl() override {
+    cudaStreamSynchronize(stream_);
+    cudaEventDestroy(ev0_);
+    cudaEventDestroy(ev1_);
+    cudaFree(d_stats_);
+    cudaFreeHost(h_stats_);
+    cudaStreamDestroy(stream_);
+  }
+
+  // ---------------------------------------------------------------- set_initial
+  void set_initial(const uint64_t* words, const double* c, size_t count) override {
+    // Engine::set_initial (engine.cpp:196-205): clear, then upsert in order.
+    using K = std::array<uint64_t, 2 * W>;  // z (msw first) then x (msw first)
+    std::map<K, double> terms;
+    for (size_t i = 0; i < count; ++i) {
+      uint64_t x[2], z[2];
+      words_to_planes(words + 4 * i, x, z);
+      if (W == 1 && (x[1] | z[1])) throw EngineError(PP_ERR_INVALID, "term has sites beyond the engine width");
+      K k;
+      for (int j = 0; j < W; ++j) {
+        k[j] = z[W - 1 - j];
+        k[W + j] = x[W - 1 - j];
+      }
+      auto it = terms.find(k);
+      if (it == terms.end()) terms.emplace(k, c[i]);
+      else it->second += c[i];
+    }
+    const uint64_t n = terms.size();
+    std::vector<uint64_t> hx(W * std::max<uint64_t>(n, 1)), hz;
+    std::vector<double> hc(std::max<uint64_t>(n, 1));
+    std::vector<uint64_t> goff, gz;
+    std::vector<uint32_t> gcnt;
+    std::vector<double> gmx, gmn;
+    std::vector<uint32_t> gfl;
+    uint64_t i = 0;
+    double gmax = 0.0;
+    K prev{};
+    bool first = true;
+    for (auto& [k, v] : terms) {
+      bool newg = first;
+      for (int j = 0; j < W && !newg; ++j) newg = k[j] != prev[j];
+      if (newg) {
+        goff.push_back(i);
+        gcnt.push_back(0);
+        for (int j = 0; j < W; ++j) gz.push_back(k[W - 1 - j]);
+        gmx.push_back(0.0);
+        gmn.push_back(INFINITY);
+        gfl.push_back(0);
+      }
+      first = false;
+      prev = k;
+      for (int j = 0; j < W; ++j) hx[j * n + i] = k[2 * W - 1 - j];
+      hc[i] = v;
+      gcnt.back()++;
+      double av = std::fabs(v);
+      gmx.back() = std::max(gmx.back(), av);
+      gmn.back() = std::min(gmn.back(), av);
+      if (!std::isfinite(v)) gfl.back() = 1;
+      gmax = std::max(gmax, av);  // global_max_abs (sparse_operator.cpp:130-134)
+      ++i;
+    }
+    const uint32_t G = (uint32_t)gcnt.size();
+    // fresh buffers
+    cur_ = 0;
+    ensure_arena(0, std::max<uint64_t>(1u << 16, 4 * n));
+    ensure_groups(0, std::max<uint32_t>(G, 1024));
+    gcur_ = 0;
+    G_ = G;
+    if (n) {
+      ArenaView<W> a = aview(0);
+      for (int j = 0; j < W; ++j)
+        PP_CUDA(cudaMemcpyAsync(a.x[j], hx.data() + j * n, n * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemcpyAsync(a.c, hc.data(), n * 8, cudaMemcpyHostToDevice, stream_));
+    }
+    if (G) {
+      GroupView<W> g = gview(0);
+      std::vector<uint64_t> zt(G);
+      for (int j = 0; j < W; ++j) {
+        for (uint32_t q = 0; q < G; ++q) zt[q] = gz[q * W + j];
+        PP_CUDA(cudaMemcpyAsync(g.z[j], zt.data(), G * 8, cudaMemcpyHostToDevice, stream_));
+      }
+      PP_CUDA(cudaMemcpyAsync(g.off, goff.data(), G * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemcpyAsync(g.cnt, gcnt.data(), G * 4, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemcpyAsync(g.cap, gcnt.data(), G * 4, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemcpyAsync(g.gmax, gmx.data(), G * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemcpyAsync(g.gmin, gmn.data(), G * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemcpyAsync(g.flags, gfl.data(), G * 4, cudaMemcpyHostToDevice, stream_));
+    }
+    PP_CUDA(cudaStreamSynchronize(stream_));
+    bump_ = n;
+    live_ = n;
+    gmax_ = gmax;
+    counters_ = pp_counters{};
+    gates_applied_ = 0;
+  }
+
+  // ---------------------------------------------------------------- gates
+  void apply_gates(const pp_gate* gates, size_t count) override {
+    size_t i = 0;
+    while (i < count) {
+      if (fusion_allowed() && is_clifford(gates[i])) {
+        size_t j = i;
+        while (j < count && is_clifford(gates[j])) ++j;
+        apply_clifford_run(gates + i, j - i);
+        i = j;
+      } else {
+        apply_one(gates[i]);
+        ++i;
+      }
+    }
+  }
+
+  void truncate_now() override {
+    auto t0 = Clock::now();
+    reduce();
+    do_truncate();
+    counters_.truncate_ns += ns_since(t0);
+  }
+
+  uint64_t term_count() const override { return live_; }
+  double global_max() const override { return gmax_; }
+
+  double expectation() override {
+    // expectation_zero_state (sparse_operator.cpp:89-97): sum over strings
+    // with no X/Y.  Summed on the host in ascending z order with Neumaier
+    // compensation, so the value is deterministic.
+    if (G_ == 0) return 0.0;
+    diag_z_.ensure((size_t)G_ * W * 8);
+    diag_c_.ensure((size_t)G_ * 8);
+    reset_stats(bump_);
+    k_diag<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, aview(cur_), diag_z_.as<uint64_t>(),
+                                                 diag_c_.as<double>(), d_stats_);
+    ++launches_;
+    fetch_stats();
+    uint64_t nd = h_stats_->diag_count;
+    std::vector<uint64_t> z(nd * W);
+    std::vector<double> c(nd);
+    if (nd) {
+      PP_CUDA(cudaMemcpy(z.data(), diag_z_.p, nd * W * 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(cudaMemcpy(c.data(), diag_c_.p, nd * 8, cudaMemcpyDeviceToHost));
+    }
+    std::vector<uint64_t> order(nd);
+    for (uint64_t i = 0; i < nd; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+      for (int k = W - 1; k >= 0; --k)
+        if (z[a * W + k] != z[b * W + k]) return z[a * W + k] < z[b * W + k];
+      return false;
+    });
+    double s = 0.0, comp = 0.0;
+    for (uint64_t i : order) {
+      double v = c[i];
+      double t = s + v;
+      if (std::fabs(s) >= std::fabs(v)) comp += (s - t) + v;
+      else comp += (v - t) + s;
+      s = t;
+    }
+    return s + comp;
+  }
+
+  double coefficient(const uint64_t* words) override {
+    uint64_t x[2], z[2];
+    words_to_planes(words, x, z);
+    if (W == 1 && (x[1] | z[1])) return 0.0;
+    if (G_ == 0) return 0.0;
+    GroupView<W> g = gview(gcur_);
+    std::vector<uint64_t> gz(G_);
+    std::vector<uint32_t> match(G_, 1);
+    for (int k = 0; k < W; ++k) {
+      PP_CUDA(cudaMemcpy(gz.data(), g.z[k], G_ * 8, cudaMemcpyDeviceToHost));
+      for (uint32_t i = 0; i < G_; ++i) match[i] &= gz[i] == z[k];
+    }
+    for (uint32_t i = 0; i < G_; ++i) {
+      if (!match[i]) continue;
+      uint64_t off;
+      uint32_t cnt;
+      PP_CUDA(cudaMemcpy(&off, g.off + i, 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(cudaMemcpy(&cnt, g.cnt + i, 4, cudaMemcpyDeviceToHost));
+      if (!cnt) continue;
+      ArenaView<W> a = aview(cur_);
+      std::vector<uint64_t> xs(cnt * W);
+      std::vector<double> cs(cnt);
+      for (int k = 0; k < W; ++k)
+        PP_CUDA(cudaMemcpy(xs.data() + k * cnt, a.x[k] + off, cnt * 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(cudaMemcpy(cs.data(), a.c + off, cnt * 8, cudaMemcpyDeviceToHost));
+      for (uint32_t e = 0; e < cnt; ++e) {
+        bool eq = true;
+        for (int k = 0; k < W; ++k) eq &= xs[k * cnt + e] == x[k];
+        if (eq) return cs[e];
+      }
+    }
+    return 0.0;
+  }
+
+  uint64_t export_terms(uint64_t* words, double* c, uint64_t cap) override {
+    if (live_ > cap) throw EngineError(PP_ERR_INVALID, "export capacity too small");
+    compact();  // one contiguous live range in the current arena
+    const uint64_t n = live_;
+    std::vector<uint64_t> xs(n * W), zs;
+    std::vector<double> cs(n);
+    std::vector<uint64_t> goff(G_), gz(G_ * W);
+    std::vector<uint32_t> gcnt(G_);
+    if (n) {
+      ArenaView<W> a = aview(cur_);
+      for (int k = 0; k < W; ++k)
+        PP_CUDA(cudaMemcpy(xs.data() + k * n, a.x[k], n * 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(cudaMemcpy(cs.data(), a.c, n * 8, cudaMemcpyDeviceToHost));
+    }
+    if (G_) {
+      GroupView<W> g = gview(gcur_);
+      PP_CUDA(cudaMemcpy(goff.data(), g.off, G_ * 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(cudaMemcpy(gcnt.data(), g.cnt, G_ * 4, cudaMemcpyDeviceToHost));
+      for (int k = 0; k < W; ++k)
+        PP_CUDA(cudaMemcpy(gz.data() + k * G_, g.z[k], G_ * 8, cudaMemcpyDeviceToHost));
+    }
+    std::vector<std::array<uint64_t, 4>> out;
+    std::vector<double> outc;
+    out.reserve(n);
+    outc.reserve(n);
+    for (uint32_t gi = 0; gi < G_; ++gi) {
+      uint64_t zz[2] = {gz[gi], W == 2 ? gz[G_ + gi] : 0};
+      for (uint32_t e = 0; e < gcnt[gi]; ++e) {
+        uint64_t p = goff[gi] + e;
+        uint64_t xx[2] = {xs[p], W == 2 ? xs[n + p] : 0};
+        std::array<uint64_t, 4> w;
+        planes_to_words(xx, zz, w.data());
+        out.push_back(w);
+        outc.push_back(cs[p]);
+      }
+    }
+    std::vector<uint64_t> order(out.size());
+    for (uint64_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+      for (int k = 3; k >= 0; --k)
+        if (out[a][k] != out[b][k]) return out[a][k] < out[b][k];
+      return false;
+    });
+    for (uint64_t i = 0; i < order.size(); ++i) {
+      std::memcpy(words + 4 * i, out[order[i]].data(), 32);
+      c[i] = outc[order[i]];
+    }
+    return order.size();
+  }
+
+  pp_counters take_counters() override {
+    pp_counters out = counters_;
+    counters_ = pp_counters{};
+    return out;
+  }
+
+  void take_kernel_stats(double* ms, double* bytes, uint64_t* launches, uint64_t* total) override {
+    *ms = branch_ms_;
+    *bytes = branch_bytes_;
+    *launches = branch_launches_;
+    *total = launches_;
+    branch_ms_ = branch_bytes_ = 0.0;
+    branch_launches_ = launches_ = 0;
+  }
+
+ private:
+  static constexpr size_t R = 8 * W + 8;  // bytes per string in the arena
+
+  static size_t big_sort_smem() { return std::max(sizeof(SortSmem<W>), sizeof(MergeSmem<W>)); }
+  static uint32_t blocks(uint64_t n) { return (uint32_t)((n + kCta - 1) / kCta); }
+
+  bool fusion_allowed() const {
+    if (cfg_.flags & PP_FLAG_NO_CLIFFORD_FUSION) return false;
+    // a fused run never exceeds |O|, but the reference's transient count
+    // inside a Clifford gate can reach 2|O| before truncation
+    return cfg_.max_terms == 0 || 2 * live_ <= cfg_.max_terms;
+  }
+
+  // ----- buffers
+  struct Arena {
+    DevBuf buf;
+    uint64_t cap = 0;
+  };
+  struct Groups {
+    DevBuf buf;
+    uint32_t cap = 0;
+  };
+  ArenaView<W> aview(int i) const {
+    ArenaView<W> v;
+    uint64_t* b = arena_[i].buf.template as<uint64_t>();
+    for (int k = 0; k < W; ++k) v.x[k] = b + k * arena_[i].cap;
+    v.c = reinterpret_cast<double*>(b + W * arena_[i].cap);
+    return v;
+  }
+  GroupView<W> gview(int i) const {
+    GroupView<W> v;
+    const uint64_t C = groups_[i].cap;
+    char* b = groups_[i].buf.template as<char>();
+    for (int k = 0; k < W; ++k) v.z[k] = reinterpret_cast<uint64_t*>(b) + k * C;
+    char* p = b + W * C * 8;
+    v.off = reinterpret_cast<uint64_t*>(p);
+    p += C * 8;
+    v.gmax = reinterpret_cast<double*>(p);
+    p += C * 8;
+    v.gmin = reinterpret_cast<double*>(p);
+    p += C * 8;
+    v.cnt = reinterpret_cast<uint32_t*>(p);
+    p += C * 4;
+    v.cap = reinterpret_cast<uint32_t*>(p);
+    p += C * 4;
+    v.flags = reinterpret_cast<uint32_t*>(p);
+    return v;
+  }
+  void ensure_arena(int i, uint64_t cap) {
+    if (arena_[i].cap >= cap) return;
+    arena_[i].buf.release();
+    arena_[i].cap = 0;
+    arena_[i].buf.ensure(cap * R);
+    arena_[i].cap = cap;
+  }
+  void ensure_groups(int i, uint32_t cap) {
+    if (groups_[i].cap >= cap) return;
+    groups_[i].buf.release();
+    groups_[i].cap = 0;
+    groups_[i].buf.ensure((size_t)cap * (8 * W + 8 + 8 + 8 + 4 + 4 + 4));
+    groups_[i].cap = cap;
+  }
+
+  void reset_stats(unsigned long long bump) {
+    k_reset_stats<<<1, 1, 0, stream_>>>(d_stats_, bump);
+    ++launches_;
+  }
+  void fetch_stats() {
+    PP_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, sizeof(DevStats), cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaStreamSynchronize(stream_));
+  }
+
+  // ----- garbage collection: compact the current arena into the other one
+  void gc_into_other(uint64_t new_cap) {
+    const int o = 1 - cur_;
+    ensure_arena(o, new_cap);
+    reset_stats(0);
+    if (G_) {
+      k_gc<W><<<G_, kCta, 0, stream_>>>(gview(gcur_), aview(cur_), aview(o), d_stats_);
+      ++launches_;
+    }
+    fetch_stats();
+    bump_ = h_stats_->bump;
+    cur_ = o;
+  }
+  void compact() {
+    uint64_t cap = std::max<uint64_t>(arena_[cur_].cap, live_ + 1);
+    gc_into_other(cap);
+  }
+  void ensure_space(uint64_t need) {
+    if (bump_ + need <= arena_[cur_].cap) return;
+    uint64_t target = (uint64_t)((live_ + need) * 1.5) + (1u << 16);
+    target = std::max<uint64_t>(target, arena_[cur_].cap);
+    gc_into_other(target);
+    if (bump_ + need > arena_[cur_].cap) throw EngineError(PP_ERR_INTERNAL, "arena sizing failed");
+  }
+
+  // ----- reductions / truncation
+  void reduce() {
+    reset_stats(bump_);
+    if (G_) {
+      k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, d_stats_);
+      ++launches_;
+    }
+    fetch_stats();
+    live_ = h_stats_->live;
+    red_gmax_ = __builtin_bit_cast(double, h_stats_->gmax_bits);
+    red_gmin_ = __builtin_bit_cast(double, h_stats_->gmin_bits);
+    red_nonfinite_ = h_stats_->nonfinite;
+  }
+  void do_truncate() {
+    if (red_nonfinite_) {
+      throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient at layer " + std::to_string(layer_) +
+                                              ", gate " + std::to_string(gates_applied_) +
+                                              ", |O|=" + std::to_string(live_));
+    }
+    gmax_ = red_gmax_;
+    const double T = cfg_.epsilon0 * gmax_;  // engine.cpp:345
+    if (G_ && red_gmin_ <= T) {
+      reset_stats(bump_);
+      k_truncate<W><<<G_, kCta, 0, stream_>>>(gview(gcur_), aview(cur_), T, d_stats_);
+      ++launches_;
+      fetch_stats();
+      counters_.removed += h_stats_->removed;
+      live_ -= h_stats_->removed;
+    }
+  }
+  void post_gate() {
+    ++gates_applied_;
+    ++counters_.gates;
+    auto t0 = Clock::now();
+    reduce();
+    if (cfg_.max_terms && live_ > cfg_.max_terms) {  // check_budget, engine.cpp:266-275
+      throw EngineError(PP_ERR_RESOURCE, "term budget exhausted: |O|=" + std::to_string(live_) +
+                                             " exceeds max_terms=" + std::to_string(cfg_.max_terms) +
+                                             " at gate " + std::to_string(gates_applied_));
+    }
+    if (cfg_.cadence == PP_CADENCE_GATE) do_truncate();
+    counters_.truncate_ns += ns_since(t0);
+  }
+
+  // ----- one gate
+  void apply_one(const pp_gate& gate) {
+    uint64_t jx[2], jz[2];
+    words_to_planes(gate.words, jx, jz);
+    if (W == 1 && (jx[1] | jz[1])) throw EngineError(PP_ERR_INVALID, "generator has sites beyond the engine width");
+    auto t0 = Clock::now();
+    int nx = __builtin_popcountll(jx[0]) + (W == 2 ? __builtin_popcountll(jx[1]) : 0);
+    bool zfree = (jz[0] | (W == 2 ? jz[1] : 0)) == 0;
+    if (nx == 0 && zfree) {
+      // identity generator: commutes with everything, no records
+    } else if (zfree && nx == 1) {
+      branch_x(jx, gate.cos_theta, gate.sin_theta);
+    } else {
+      GateProducer<W> p;
+      for (int k = 0; k < W; ++k) {
+        p.jx.w[k] = jx[k];
+        p.jz.w[k] = jz[k];
+      }
+      p.cosv = gate.cos_theta;
+      p.sinv = gate.sin_theta;
+      regroup(p);
+      counters_.records_sent += h_records_;
+    }
+    counters_.branch_ns += ns_since(t0);
+    if (h_records_) counters_.batches_sent += 1;
+    h_records_ = 0;
+    post_gate();
+  }
+
+  void branch_x(const uint64_t* jx, double cosv, double sinv) {
+    if (G_ == 0) return;
+    Plane<W> px;
+    int wq = 0;
+    uint64_t mq = 0;
+    for (int k = 0; k < W; ++k) {
+      px.w[k] = jx[k];
+      if (jx[k]) {
+        wq = k;
+        mq = jx[k];
+      }
+    }
+    ensure_list(G_);
+    reset_stats(bump_);
+    k_select_x<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, px, list_.as<uint32_t>(), d_stats_);
+    ++launches_;
+    fetch_stats();
+    const uint32_t n_aff = h_stats_->n_aff;
+    const uint64_t aff = h_stats_->aff_elems;
+    if (n_aff == 0) return;
+    ensure_space(2 * aff);
+    reset_stats(bump_);
+    PP_CUDA(cudaEventRecord(ev0_, stream_));
+    k_branch_x<W><<<n_aff, kCta, sizeof(BranchSmem<W>), stream_>>>(gview(gcur_), aview(cur_), list_.as<uint32_t>(),
+                                                                    wq, mq, cosv, sinv, keep_zeros_, d_stats_);
+    PP_CUDA(cudaEventRecord(ev1_, stream_));
+    ++launches_;
+    ++branch_launches_;
+    fetch_stats();
+    PP_CUDA(cudaGetLastError());
+    float ms = 0.f;
+    PP_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    branch_ms_ += ms;
+    branch_bytes_ += (double)(aff + h_stats_->out_elems) * R;
+    bump_ = h_stats_->bump;
+    h_records_ = h_stats_->records;
+    counters_.records_sent += h_stats_->records;
+    counters_.removed += h_stats_->removed;
+  }
+
+  void ensure_list(uint32_t n) { list_.ensure((size_t)std::max<uint32_t>(n, 1) * 4); }
+
+  // ----- fused Clifford run
+  void apply_clifford_run(const pp_gate* gates, size_t count) {
+    auto t0 = Clock::now();
+    std::vector<uint64_t> gx(count * W), gz(count * W);
+    std::vector<double> gs(count);
+    for (size_t i = 0; i < count; ++i) {
+      uint64_t jx[2], jz[2];
+      words_to_planes(gates[i].words, jx, jz);
+      if (W == 1 && (jx[1] | jz[1])) throw EngineError(PP_ERR_INVALID, "generator has sites beyond the engine width");
+      for (int k = 0; k < W; ++k) {
+        gx[i * W + k] = jx[k];
+        gz[i * W + k] = jz[k];
+      }
+      gs[i] = gates[i].sin_theta;
+    }
+    cliff_.ensure(count * (2 * W + 1) * 8);
+    uint64_t* dgx = cliff_.as<uint64_t>();
+    uint64_t* dgz = dgx + count * W;
+    double* dgs = reinterpret_cast<double*>(dgz + count * W);
+    PP_CUDA(cudaMemcpyAsync(dgx, gx.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(dgz, gz.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(dgs, gs.data(), count * 8, cudaMemcpyHostToDevice, stream_));
+    CliffordProducer<W> p{dgx, dgz, dgs, (int)count};
+    if (G_) regroup(p);
+    // Clifford gates zero each moved parent and re-insert it at I xor J;
+    // absent a partner pair the reference removes one zero per record.
+    counters_.records_sent += h_records_;
+    counters_.removed += h_records_;
+    counters_.batches_sent += h_records_ ? count : 0;
+    h_records_ = 0;
+    counters_.exchange_ns += ns_since(t0);
+    gates_applied_ += count;
+    counters_.gates += count;
+    auto t1 = Clock::now();
+    reduce();
+    if (cfg_.cadence == PP_CADENCE_GATE) do_truncate();
+    counters_.truncate_ns += ns_since(t1);
+  }
+
+  // ----- regroup: records -> new z-grouped store
+  template <class P>
+  void regroup(const P& prod) {
+    const int maxrec = P::kMaxRec;
+    const uint64_t live = live_;
+    if (G_ == 0 || live == 0) return;
+    const uint64_t max_items = (uint64_t)G_ + live / kItem + 1;
+    items_.ensure(max_items * sizeof(Item));
+    rec_slot_.ensure(live * maxrec * 4);
+    uint64_t records_upper = live * maxrec;
+    uint64_t tc = 1024;
+    while (tc < 2 * std::min<uint64_t>(records_upper, 4ull * G_ + 1024)) tc <<= 1;
+    uint64_t tc_max = 1024;
+    while (tc_max < 2 * records_upper) tc_max <<= 1;
+    const int o = 1 - cur_;
+    for (int attempt = 0;; ++attempt) {
+      if (attempt > 8) throw EngineError(PP_ERR_INTERNAL, "regroup: hash table retries exhausted");
+      table_.ensure(tc * (8 + 8 * W + 4 + 4));
+      HashTable<W> t = tview(tc);
+      PP_CUDA(cudaMemsetAsync(t.fp, 0, tc * 8, stream_));
+      PP_CUDA(cudaMemsetAsync(t.count, 0, tc * 4, stream_));
+      reset_stats(bump_);
+      k_make_items<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, items_.as<Item>(), maxrec, d_stats_);
+      ++launches_;
+      fetch_stats();
+      const uint64_t n_items = h_stats_->items;
+      k_insert<W, P><<<(uint32_t)n_items, kCta, 0, stream_>>>(items_.as<Item>(), gview(gcur_), aview(cur_), prod, t,
+                                                              rec_slot_.as<uint32_t>(), seed_,
+                                                              (uint32_t)std::min<uint64_t>(tc / 2, 0xffffffffu),
+                                                              d_stats_);
+      ++launches_;
+      fetch_stats();
+      PP_CUDA(cudaGetLastError());
+      if (h_stats_->overflow) {
+        if (tc >= tc_max) throw EngineError(PP_ERR_INTERNAL, "regroup: hash table overflow");
+        tc = std::min(tc_max, tc * 4);
+        continue;
+      }
+      const uint32_t distinct = h_stats_->distinct;
+      const unsigned long long records = h_stats_->records;
+      // deterministic ids and offsets from slot order
+      const uint64_t ntiles = (tc + kScanTile - 1) / kScanTile;
+      scan_tmp_.ensure((ntiles + 1) * 8);
+      scan_gid_.ensure(tc * 8);
+      scan_off_.ensure(tc * 8);
+      device_scan(t.count, tc, 1, scan_gid_.as<unsigned long long>(), ntiles);
+      device_scan(t.count, tc, 0, scan_off_.as<unsigned long long>(), ntiles);
+      unsigned long long total = 0;
+      PP_CUDA(cudaMemcpyAsync(&total, scan_tmp_.as<unsigned long long>() + ntiles, 8, cudaMemcpyDeviceToHost,
+                              stream_));
+      PP_CUDA(cudaStreamSynchronize(stream_));
+      ensure_groups(1 - gcur_, std::max<uint32_t>(distinct, 1024));
+      ensure_arena(o, std::max<uint64_t>(total + (1u << 16), (uint64_t)(total * 1.5)));
+      k_table_emit<W><<<(uint32_t)((tc + kCta - 1) / kCta), kCta, 0, stream_>>>(
+          t, scan_gid_.as<unsigned long long>(), scan_off_.as<unsigned long long>(), gview(1 - gcur_), 0);
+      ++launches_;
+      reset_stats(0);
+      k_scatter<W, P><<<(uint32_t)n_items, kCta, 0, stream_>>>(items_.as<Item>(), gview(gcur_), aview(cur_), prod, t,
+                                                               rec_slot_.as<uint32_t>(), gview(1 - gcur_), aview(o),
+                                                               d_stats_);
+      ++launches_;
+      fetch_stats();
+      PP_CUDA(cudaGetLastError());
+      if (h_stats_->collision) {
+        seed_ = mix64(seed_ + 1);
+        continue;
+      }
+      // sort inside groups; the source arena is free now and serves as
+      // scratch for the big-group merge passes
+      ensure_arena(cur_, total + 1);
+      reset_stats(0);
+      k_sort_small<W><<<distinct, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o), keep_zeros_,
+                                                                         d_stats_);
+      k_sort_big<W><<<distinct, kCta, big_sort_smem(), stream_>>>(gview(1 - gcur_), aview(o), aview(cur_),
+                                                                  keep_zeros_, d_stats_);
+      launches_ += 2;
+      fetch_stats();
+      PP_CUDA(cudaGetLastError());
+      counters_.removed += h_stats_->removed;
+      h_records_ = records;
+      cur_ = o;
+      gcur_ = 1 - gcur_;
+      G_ = distinct;
+      bump_ = total;
+      return;
+    }
+  }
+
+  HashTable<W> tview(uint64_t tc) const {
+    HashTable<W> t;
+    char* b = table_.as<char>();
+    t.fp = reinterpret_cast<unsigned long long*>(b);
+    uint64_t* zb = reinterpret_cast<uint64_t*>(b + tc * 8);
+    for (int k = 0; k < W; ++k) t.z[k] = zb + k * tc;
+    t.count = reinterpret_cast<uint32_t*>(b + tc * 8 + tc * 8 * W);
+    t.gid = t.count + tc;
+    t.mask = tc - 1;
+    return t;
+  }
+
+  // exclusive scan of in[0..n) (or of in != 0) into out; total at
+  // scan_tmp_[ntiles]
+  void device_scan(const uint32_t* in, uint64_t n, int as_flag, unsigned long long* out, uint64_t ntiles) {
+    unsigned long long* sums = scan_tmp_.as<unsigned long long>();
+    k_scan_tiles<<<(uint32_t)ntiles, kCta, 0, stream_>>>(in, n, as_flag, sums);
+    k_scan_sums<<<1, kCta, 0, stream_>>>(sums, ntiles);
+    k_scan_apply<<<(uint32_t)ntiles, kCta, 0, stream_>>>(in, n, as_flag, sums, out);
+    launches_ += 3;
+  }
+
+  pp_config cfg_;
+  cudaStream_t stream_ = nullptr;
+  DevStats* d_stats_ = nullptr;
+  DevStats* h_stats_ = nullptr;
+  cudaEvent_t ev0_, ev1_;
+  Arena arena_[2];
+  Groups groups_[2];
+  DevBuf list_, items_, rec_slot_, table_, scan_tmp_, scan_gid_, scan_off_, diag_z_, diag_c_, cliff_;
+  int cur_ = 0, gcur_ = 0;
+  uint32_t G_ = 0;
+  uint64_t bump_ = 0, live_ = 0;
+  double gmax_ = 0.0, red_gmax_ = 0.0, red_gmin_ = 0.0;
+  uint32_t red_nonfinite_ = 0;
+  int keep_zeros_ = 0;
+  unsigned long long seed_;
+  unsigned long long h_records_ = 0;
+  pp_counters counters_{};
+  uint64_t gates_applied_ = 0;
+  int layer_ = 0;
+  double branch_ms_ = 0.0, branch_bytes_ = 0.0;
+  uint64_t branch_launches_ = 0, launches_ = 0;
+};
+
+}  // namespace ppgpu
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+struct pp_engine {
+  std::unique_ptr<ppgpu::EngineBase> impl;
+  std::string error;
+};
+
+namespace {
+thread_local std::string g_create_error;
+
+template <class F>
+int guarded(pp_engine* e, F&& f) {
+  try {
+    f();
+    return PP_OK;
+  } catch (const ppgpu::EngineError& x) {
+    if (e) e->error = x.what();
+    return x.code;
+  } catch (const std::bad_alloc&) {
+    if (e) e->error = "host memory exhausted";
+    return PP_ERR_RESOURCE;
+  } catch (const std::exception& x) {
+    if (e) e->error = x.what();
+    return PP_ERR_INTERNAL;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int pp_create(const pp_config* config, pp_engine** out) {
+  if (!config || !out) return PP_ERR_INVALID;
+  *out = nullptr;
+  if (config->n < 1 || config->n > 128) {
+    g_create_error = "qubit count out of range";
+    return PP_ERR_INVALID;
+  }
+  if (!(config->epsilon0 >= 0)) {
+    g_create_error = "epsilon0 must be >= 0";
+    return PP_ERR_INVALID;
+  }
+  if (config->cadence != PP_CADENCE_GATE && config->cadence != PP_CADENCE_LAYER) {
+    g_create_error = "bad cadence";
+    return PP_ERR_INVALID;
+  }
+  auto e = std::make_unique<pp_engine>();
+  int rc = guarded(e.get(), [&] {
+    int ndev = 0;
+    cudaError_t err = cudaGetDeviceCount(&ndev);
+    if (err != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw ppgpu::EngineError(PP_ERR_INTERNAL, "no CUDA device available (the engine has no CPU fallback)");
+    }
+    if (config->device < 0 || config->device >= ndev) throw ppgpu::EngineError(PP_ERR_INVALID, "bad device ordinal");
+    if (config->n <= 64) e->impl = std::make_unique<ppgpu::EngineImpl<1>>(*config);
+    else e->impl = std::make_unique<ppgpu::EngineImpl<2>>(*config);
+  });
+  if (rc) {
+    g_create_error = e->error;
+    return rc;
+  }
+  *out = e.release();
+  return PP_OK;
+}
+
+void pp_destroy(pp_engine* e) { delete e; }
+
+int pp_set_initial(pp_engine* e, const uint64_t* words, const double* coeffs, size_t count) {
+  if (!e) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->set_initial(words, coeffs, count); });
+}
+
+int pp_apply_gate(pp_engine* e, const pp_gate* gate) {
+  if (!e || !gate) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->apply_gates(gate, 1); });
+}
+
+int pp_apply_gates(pp_engine* e, const pp_gate* gates, size_t count) {
+  if (!e || (!gates && count)) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->apply_gates(gates, count); });
+}
+
+int pp_truncate_now(pp_engine* e) {
+  if (!e) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->truncate_now(); });
+}
+
+int pp_term_count(const pp_engine* e, uint64_t* out) {
+  if (!e || !out) return PP_ERR_INVALID;
+  *out = e->impl->term_count();
+  return PP_OK;
+}
+
+int pp_global_max(const pp_engine* e, double* out) {
+  if (!e || !out) return PP_ERR_INVALID;
+  *out = e->impl->global_max();
+  return PP_OK;
+}
+
+int pp_expectation_zero_state(pp_engine* e, double* out) {
+  if (!e || !out) return PP_ERR_INVALID;
+  return guarded(e, [&] { *out = e->impl->expectation(); });
+}
+
+int pp_coefficient(pp_engine* e, const uint64_t* words, double* out) {
+  if (!e || !words || !out) return PP_ERR_INVALID;
+  return guarded(e, [&] { *out = e->impl->coefficient(words); });
+}
+
+int pp_export(pp_engine* e, uint64_t* words, double* coeffs, uint64_t cap, uint64_t* count) {
+  if (!e || !count) return PP_ERR_INVALID;
+  return guarded(e, [&] { *count = e->impl->export_terms(words, coeffs, cap); });
+}
+
+int pp_take_counters(pp_engine* e, pp_counters* out) {
+  if (!e || !out) return PP_ERR_INVALID;
+  *out = e->impl->take_counters();
+  return PP_OK;
+}
+
+int pp_take_kernel_stats(pp_engine* e, double* branch_ms, double* branch_bytes, uint64_t* branch_launches,
+                         uint64_t* total_launches) {
+  if (!e) return PP_ERR_INVALID;
+  e->impl->take_kernel_stats(branch_ms, branch_bytes, branch_launches, total_launches);
+  return PP_OK;
+}
+
+const char* pp_last_error(const pp_engine* e) { return e ? e->error.c_str() : g_create_error.c_str(); }
+
+}  // extern "C"

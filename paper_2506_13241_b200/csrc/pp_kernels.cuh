@@ -1,0 +1,525 @@
+// pp_kernels.cuh -- sm_100a kernels of the Pauli-propagation hot path.
+//
+// Store layout: the operator is a set of
+// z-groups.  Every string of a group shares its z-plane, which is stored
+// once in the group table; the strings themselves live in an arena as
+// structure-of-arrays x-plane words + fp64 coefficient (8W+8 bytes/string),
+// sorted ascending by x inside each group's region.
+//
+// Why z-groups: an Rx gate on qubit q (generator X_q) anticommutes with a
+// string iff z_q = 1 and its partner flips only x_q (SURVEY.md section 0,
+// fact 2), so a z-group is either untouched by the gate or entirely
+// branched, and all children stay inside their group.  The branch+merge of
+// one gate therefore reads and writes only the affected groups.
+//
+// All coefficient arithmetic uses __dmul_rn/__dadd_rn (no FMA contraction)
+// so results are bit-identical to the reference's scalar C++ (engine.cpp:
+// 223-226, term_map.hpp:77-79).
+#pragma once
+
+#include "pp_common.cuh"
+
+namespace ppgpu {
+
+template <int W>
+struct ArenaView {
+  uint64_t* x[W];
+  double* c;
+};
+
+template <int W>
+struct GroupView {
+  uint64_t* z[W];
+  uint64_t* off;
+  uint32_t* cnt;
+  uint32_t* cap;
+  double* gmax;
+  double* gmin;
+  uint32_t* flags;  // bit0: non-finite coefficient present
+};
+
+struct DevStats {
+  unsigned long long bump;         // bump pointer of the target arena
+  unsigned long long live;         // sum of group counts
+  unsigned long long records;      // nonzero sin-branch records (records_sent)
+  unsigned long long removed;      // stored strings dropped (zero or truncated)
+  unsigned long long gmax_bits;    // max |c| as bits
+  unsigned long long gmin_bits;    // min over groups of their min |c|
+  unsigned long long aff_elems;    // strings in affected groups
+  unsigned long long items;        // regroup work items
+  unsigned long long rec_total;    // regroup record slots reserved
+  unsigned long long scratch_bump; // scratch allocation for big sorts
+  unsigned long long diag_count;   // diagonal strings found
+  unsigned long long out_elems;    // strings written by branch kernels
+  unsigned int nonfinite;
+  unsigned int n_aff;
+  unsigned int overflow;
+  unsigned int collision;
+  unsigned int distinct;
+  unsigned int pad;
+};
+
+template <int W>
+__device__ __forceinline__ Plane<W> load_plane(uint64_t* const (&p)[W], uint64_t i) {
+  Plane<W> r;
+#pragma unroll
+  for (int k = 0; k < W; ++k) r.w[k] = p[k][i];
+  return r;
+}
+template <int W>
+__device__ __forceinline__ void store_plane(uint64_t* const (&p)[W], uint64_t i, const Plane<W>& v) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) p[k][i] = v.w[k];
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory key arrays (SoA: one array per plane word, bank friendly)
+// ---------------------------------------------------------------------------
+template <int W>
+__device__ __forceinline__ Plane<W> sk_load(const uint64_t* base, uint32_t stride, uint32_t i) {
+  Plane<W> r;
+#pragma unroll
+  for (int k = 0; k < W; ++k) r.w[k] = base[k * stride + i];
+  return r;
+}
+template <int W>
+__device__ __forceinline__ void sk_store(uint64_t* base, uint32_t stride, uint32_t i, const Plane<W>& v) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) base[k * stride + i] = v.w[k];
+}
+// first index in [0, n) with key >= k
+template <int W>
+__device__ __forceinline__ uint32_t sk_lower_bound(const uint64_t* base, uint32_t stride, uint32_t n,
+                                                   const Plane<W>& k) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (plane_lt<W>(sk_load<W>(base, stride, mid), k)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+// first index in [0, n) with key > k
+template <int W>
+__device__ __forceinline__ uint32_t sk_upper_bound(const uint64_t* base, uint32_t stride, uint32_t n,
+                                                   const Plane<W>& k) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (!plane_lt<W>(k, sk_load<W>(base, stride, mid))) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// group selection for an X-type gate
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void k_select_x(GroupView<W> g, uint32_t G, Plane<W> jx, uint32_t* list, DevStats* st) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool take = false;
+  uint32_t c = 0;
+  if (i < G) {
+    c = g.cnt[i];
+    if (c) take = plane_parity_and<W>(load_plane<W>(g.z, i), jx);
+  }
+  unsigned mask = __ballot_sync(0xffffffffu, take);
+  if (!mask) return;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  unsigned long long sum = warp_sum64(take ? c : 0);
+  if (lane == 0) {
+    base = atomicAdd(&st->n_aff, __popc(mask));
+    atomicAdd(&st->aff_elems, sum);
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (take) list[base + __popc(mask & ((1u << lane) - 1))] = i;
+}
+
+// ---------------------------------------------------------------------------
+// K_branch: Rx branch + merge of one affected z-group (one CTA per group).
+//
+// For the group S (sorted by x) and the gate X_q every string branches:
+//   parent   x        -> cos * c                 (engine.cpp:223)
+//   child    x ^ e_q  -> (+-sin) * c_parent       (engine.cpp:224-227)
+// with sign + for a Z at q (x_q = 0) and - for a Y (x_q = 1)
+// (record_sign, engine.cpp:67-73 with the phase table of
+// pauli_string.cpp:28-34).  A child landing on an existing string is added
+// to its scaled value (TermMap::add, term_map.hpp:77-79); each key gets at
+// most one child, so the sum is a single two-operand rounding.
+//
+// The output is the sorted merge of three sorted streams read from S:
+//   A  = S                      (all strings, scaled by cos)
+//   T0 = { x | e_q : x_q = 0 }  (children of Z-parents, keys with bit q set)
+//   T1 = { x &~e_q : x_q = 1 }  (children of Y-parents, keys with bit q clear)
+// T0 and T1 are disjoint, and a T key equal to an A key is a partner pair.
+// The CTA streams the three views through shared-memory buffers, merging
+// every round all buffered keys <= kmax (the smallest last-buffered key of
+// the streams that still have input), then compacts and writes them.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kBufCap = 2 * kCta;      // per-stream buffer
+constexpr uint32_t kRefill = kCta;          // refill threshold
+constexpr uint32_t kSlots = 3 * kBufCap;    // output slots per round
+
+template <int W>
+struct BranchSmem {
+  uint64_t key[3][W * kBufCap];
+  double val[3][kBufCap];
+  uint64_t skey[W * kSlots];
+  double sval[kSlots];
+  uint8_t semit[kSlots];
+  uint32_t scan[40];
+  uint32_t cnt[3];
+  uint32_t pos[3];
+  uint32_t m[3];
+  uint32_t all_done;
+};
+
+template <int W>
+__global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> ar, const uint32_t* list,
+                                                    int wq, uint64_t mq, double cosv, double sinv,
+                                                    int keep_zeros, DevStats* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  const uint32_t gid = list[blockIdx.x];
+  const uint32_t n = g.cnt[gid];
+  const uint64_t src = g.off[gid];
+  __shared__ unsigned long long dst_s;
+  if (tid == 0) {
+    dst_s = atomicAdd(&st->bump, 2ull * n);
+    sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0;
+    sm.pos[0] = sm.pos[1] = sm.pos[2] = 0;
+  }
+  __syncthreads();
+  const uint64_t dst = dst_s;
+  const double nsin = -sinv;
+
+  uint32_t out_n = 0;
+  double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  uint32_t nonfinite = 0;
+  unsigned long long records = 0, removed = 0;
+
+  for (;;) {
+    // ---- refill the three stream buffers --------------------------------
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+      while (sm.cnt[s] < kRefill && sm.pos[s] < n) {
+        uint32_t p = sm.pos[s] + tid;
+        bool ok = false;
+        Plane<W> key;
+        double v = 0.0;
+        if (p < n) {
+          key = load_plane<W>(ar.x, src + p);
+          v = ar.c[src + p];
+          uint32_t cls = (key.w[wq] & mq) ? 1u : 0u;
+          ok = (s == 0) || (s == 1 && cls == 0) || (s == 2 && cls == 1);
+          if (s) key.w[wq] ^= mq;
+        }
+        uint32_t total;
+        uint32_t o = block_excl_scan(ok ? 1u : 0u, sm.scan, &total);
+        if (ok) {
+          uint32_t d = sm.cnt[s] + o;
+          sk_store<W>(sm.key[s], kBufCap, d, key);
+          sm.val[s][d] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          sm.cnt[s] += total;
+          sm.pos[s] += kCta;
+        }
+        __syncthreads();
+      }
+    }
+    // ---- choose kmax and the consumed prefix of every stream ------------
+    if (tid < 3) {
+      Plane<W> kmax = plane_max<W>();
+      bool bounded = false;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        if (sm.pos[s] < n) {  // stream still has unread input
+          Plane<W> last = sk_load<W>(sm.key[s], kBufCap, sm.cnt[s] - 1);
+          if (!bounded || plane_lt<W>(last, kmax)) kmax = last;
+          bounded = true;
+        }
+      }
+      uint32_t s = tid;
+      sm.m[s] = bounded ? sk_upper_bound<W>(sm.key[s], kBufCap, sm.cnt[s], kmax) : sm.cnt[s];
+    }
+    __syncthreads();
+    const uint32_t mA = sm.m[0], m0 = sm.m[1], m1 = sm.m[2];
+    const uint32_t total = mA + m0 + m1;
+    for (uint32_t i = tid; i < total; i += kCta) sm.semit[i] = 0;
+    __syncthreads();
+    // ---- A: scaled parents, plus the partner child if present -------------
+    for (uint32_t i = tid; i < mA; i += kCta) {
+      Plane<W> k = sk_load<W>(sm.key[0], kBufCap, i);
+      double c = sm.val[0][i];
+      uint32_t l0 = sk_lower_bound<W>(sm.key[1], kBufCap, m0, k);
+      uint32_t l1 = sk_lower_bound<W>(sm.key[2], kBufCap, m1, k);
+      uint32_t rank = i + l0 + l1;
+      double v = __dmul_rn(c, cosv);
+      if (k.w[wq] & mq) {  // bit q set: partner child comes from a Z-parent (T0)
+        if (l0 < m0 && plane_eq<W>(sk_load<W>(sm.key[1], kBufCap, l0), k)) {
+          double d = __dmul_rn(sinv, sm.val[1][l0]);
+          if (d != 0.0) v = __dadd_rn(v, d);
+        }
+      } else {
+        if (l1 < m1 && plane_eq<W>(sk_load<W>(sm.key[2], kBufCap, l1), k)) {
+          double d = __dmul_rn(nsin, sm.val[2][l1]);
+          if (d != 0.0) v = __dadd_rn(v, d);
+        }
+      }
+      bool emit = keep_zeros || v != 0.0;
+      if (!emit) ++removed;
+      sk_store<W>(sm.skey, kSlots, rank, k);
+      sm.sval[rank] = v;
+      sm.semit[rank] = emit;
+    }
+    // ---- T0 / T1: children; emitted on their own when no partner exists ---
+    for (uint32_t j = tid; j < m0 + m1; j += kCta) {
+      const bool t0 = j < m0;
+      const uint32_t jj = t0 ? j : j - m0;
+      const int s = t0 ? 1 : 2;
+      Plane<W> k = sk_load<W>(sm.key[s], kBufCap, jj);
+      double d = __dmul_rn(t0 ? sinv : nsin, sm.val[s][jj]);
+      if (d != 0.0) ++records;
+      uint32_t la = sk_lower_bound<W>(sm.key[0], kBufCap, mA, k);
+      if (la < mA && plane_eq<W>(sk_load<W>(sm.key[0], kBufCap, la), k)) continue;  // partner
+      if (d == 0.0) continue;  // engine.cpp:226: no record for a zero increment
+      uint32_t lo = t0 ? sk_lower_bound<W>(sm.key[2], kBufCap, m1, k) : sk_lower_bound<W>(sm.key[1], kBufCap, m0, k);
+      uint32_t rank = jj + la + lo;
+      sk_store<W>(sm.skey, kSlots, rank, k);
+      sm.sval[rank] = d;
+      sm.semit[rank] = 1;
+    }
+    __syncthreads();
+    // ---- compact the slots and stream them out ----------------------------
+    for (uint32_t base = 0; base < total; base += kCta) {
+      uint32_t s = base + tid;
+      bool e = s < total && sm.semit[s];
+      uint32_t tot;
+      uint32_t o = block_excl_scan(e ? 1u : 0u, sm.scan, &tot);
+      if (e) {
+        double v = sm.sval[s];
+        uint64_t d = dst + out_n + o;
+        store_plane<W>(ar.x, d, sk_load<W>(sm.skey, kSlots, s));
+        ar.c[d] = v;
+        double av = fabs(v);
+        if (!(av <= 1.7976931348623157e308)) nonfinite = 1;  // NaN or Inf
+        vmax = fmax(vmax, av);
+        vmin = fmin(vmin, av);
+      }
+      out_n += tot;
+    }
+    // ---- drop the consumed prefixes --------------------------------------
+    uint32_t rem[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) rem[s] = sm.cnt[s] - sm.m[s];
+    Plane<W> tk[3][kBufCap / kCta];
+    double tv[3][kBufCap / kCta];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+#pragma unroll
+      for (uint32_t r = 0; r < kBufCap / kCta; ++r) {
+        uint32_t i = tid + r * kCta;
+        if (i < rem[s]) {
+          tk[s][r] = sk_load<W>(sm.key[s], kBufCap, sm.m[s] + i);
+          tv[s][r] = sm.val[s][sm.m[s] + i];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+#pragma unroll
+      for (uint32_t r = 0; r < kBufCap / kCta; ++r) {
+        uint32_t i = tid + r * kCta;
+        if (i < rem[s]) {
+          sk_store<W>(sm.key[s], kBufCap, i, tk[s][r]);
+          sm.val[s][i] = tv[s][r];
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      bool done = true;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        sm.cnt[s] = rem[s];
+        done &= (rem[s] == 0 && sm.pos[s] >= n);
+      }
+      sm.all_done = done;
+    }
+    __syncthreads();
+    if (sm.all_done) break;
+  }
+
+  // ---- per-group statistics ---------------------------------------------
+  vmax = warp_max(vmax);
+  vmin = warp_min(vmin);
+  records = warp_sum64(records);
+  removed = warp_sum64(removed);
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  __shared__ double red_max[kWarps], red_min[kWarps];
+  __shared__ unsigned long long red_rec[kWarps], red_rem[kWarps];
+  __shared__ uint32_t red_nf[kWarps];
+  const uint32_t lane = tid & 31, warp = tid >> 5;
+  if (lane == 0) {
+    red_max[warp] = vmax;
+    red_min[warp] = vmin;
+    red_rec[warp] = records;
+    red_rem[warp] = removed;
+    red_nf[warp] = nonfinite;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (uint32_t w = 1; w < kWarps; ++w) {
+      vmax = fmax(vmax, red_max[w]);
+      vmin = fmin(vmin, red_min[w]);
+      records += red_rec[w];
+      removed += red_rem[w];
+      nonfinite |= red_nf[w];
+    }
+    g.off[gid] = dst;
+    g.cnt[gid] = out_n;
+    g.cap[gid] = 2 * n;
+    g.gmax[gid] = out_n ? vmax : 0.0;
+    g.gmin[gid] = out_n ? vmin : __longlong_as_double(0x7ff0000000000000ll);
+    g.flags[gid] = nonfinite;
+    atomicAdd(&st->records, records);
+    atomicAdd(&st->removed, removed);
+    atomicAdd(&st->out_elems, (unsigned long long)out_n);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// group-level reductions: live count, max |c|, min over group minima, NaN
+// (truncate_now's first pass, engine.cpp:321-343, at group granularity)
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void k_reduce(GroupView<W> g, uint32_t G, DevStats* st) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long live = 0;
+  double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
+  uint32_t nf = 0;
+  if (i < G) {
+    uint32_t c = g.cnt[i];
+    if (c) {
+      live = c;
+      mx = g.gmax[i];
+      mn = g.gmin[i];
+      nf = g.flags[i] & 1u;
+    }
+  }
+  live = warp_sum64(live);
+  mx = warp_max(mx);
+  mn = warp_min(mn);
+  nf = __any_sync(0xffffffffu, nf);
+  if ((threadIdx.x & 31) == 0) {
+    if (live) atomicAdd(&st->live, live);
+    atomic_max_nonneg(reinterpret_cast<double*>(&st->gmax_bits), mx);
+    atomic_min_nonneg(reinterpret_cast<double*>(&st->gmin_bits), mn);
+    if (nf) atomicOr(&st->nonfinite, 1u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// truncation: remove |c| <= T inside every group whose min |c| <= T
+// (TermMap::remove_below, term_map.cpp:105-144; strict <= so exact zeros
+// and -0.0 always go).  In-place streaming compaction, one CTA per group.
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, ArenaView<W> ar, double T, DevStats* st) {
+  const uint32_t gid = blockIdx.x;
+  const uint32_t n = g.cnt[gid];
+  if (n == 0 || !(g.gmin[gid] <= T)) return;
+  const uint64_t off = g.off[gid];
+  __shared__ uint32_t scan[40];
+  const uint32_t tid = threadIdx.x;
+  uint32_t w = 0;
+  double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);
+  for (uint32_t base = 0; base < n; base += kCta) {
+    uint32_t p = base + tid;
+    bool keep = false;
+    Plane<W> k;
+    double v = 0.0;
+    if (p < n) {
+      k = load_plane<W>(ar.x, off + p);
+      v = ar.c[off + p];
+      keep = !(fabs(v) <= T);
+    }
+    uint32_t tot;
+    uint32_t o = block_excl_scan(keep ? 1u : 0u, scan, &tot);  // syncs: all reads done
+    if (keep) {
+      store_plane<W>(ar.x, off + w + o, k);
+      ar.c[off + w + o] = v;
+      vmax = fmax(vmax, fabs(v));
+      vmin = fmin(vmin, fabs(v));
+    }
+    w += tot;
+    __syncthreads();
+  }
+  vmax = warp_max(vmax);
+  vmin = warp_min(vmin);
+  __shared__ double rmx[kWarps], rmn[kWarps];
+  if ((tid & 31) == 0) {
+    rmx[tid >> 5] = vmax;
+    rmn[tid >> 5] = vmin;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (uint32_t i = 1; i < kWarps; ++i) {
+      vmax = fmax(vmax, rmx[i]);
+      vmin = fmin(vmin, rmn[i]);
+    }
+    g.cnt[gid] = w;
+    g.gmax[gid] = w ? vmax : 0.0;
+    g.gmin[gid] = w ? vmin : __longlong_as_double(0x7ff0000000000000ll);
+    atomicAdd(&st->removed, (unsigned long long)(n - w));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// diagonal strings (x == 0 is the smallest key of a group, so it can only be
+// the first element): <0|O|0> terms (sparse_operator.cpp:32-36, 89-97)
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void k_diag(GroupView<W> g, uint32_t G, ArenaView<W> ar, uint64_t* out_z, double* out_c,
+                       DevStats* st) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G || g.cnt[i] == 0) return;
+  uint64_t o = g.off[i];
+  if (!plane_zero<W>(load_plane<W>(ar.x, o))) return;
+  unsigned long long d = atomicAdd(&st->diag_count, 1ull);
+#pragma unroll
+  for (int k = 0; k < W; ++k) out_z[d * W + k] = g.z[k][i];
+  out_c[d] = ar.c[o];
+}
+
+// ---------------------------------------------------------------------------
+// compaction of the arena into the other buffer (garbage collection)
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(kCta) k_gc(GroupView<W> g, ArenaView<W> src, ArenaView<W> dst, DevStats* st) {
+  const uint32_t gid = blockIdx.x;
+  const uint32_t n = g.cnt[gid];
+  __shared__ unsigned long long d_s;
+  const uint64_t so = g.off[gid];
+  if (threadIdx.x == 0) d_s = n ? atomicAdd(&st->bump, (unsigned long long)n) : 0ull;
+  __syncthreads();
+  const uint64_t d = d_s;
+  for (uint32_t p = threadIdx.x; p < n; p += kCta) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) dst.x[k][d + p] = src.x[k][so + p];
+    dst.c[d + p] = src.c[so + p];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g.off[gid] = d;
+    g.cap[gid] = n;
+  }
+}
+
+}  // namespace ppgpu

@@ -1,0 +1,640 @@
+// pp_regroup.cuh -- rebuilding the z-grouped store after gates that move
+// strings between z-groups.
+//
+// Used for (a) a run of Clifford gates fused into one signed permutation of
+// the strings (cos = 0, |sin| = 1: every anticommuting string moves to
+// I xor J with coefficient (+-sin) c, exactly -- SURVEY.md section 0 fact 6;
+// a permutation never merges, so the reference's per-gate passes and the
+// fused map give identical sets), and (b) any gate whose generator carries a
+// Z or Y (its children change z-group).
+//
+// Pipeline (all passes recompute the per-string records from the source
+// arena, so no record buffer is materialised):
+//   insert  -- hash every record's new z-plane into an open-addressing table
+//              of (fingerprint, z, count); remember the slot per record
+//   scan    -- prefix sums over the table give deterministic group ids and
+//              arena offsets
+//   scatter -- every record goes to its group's region
+//   sort    -- each group's region is sorted by x; equal keys (a parent and
+//              the child landing on it, at most two per key) are summed,
+//              zeros dropped (TermMap::add + remove_below semantics)
+#pragma once
+
+#include "pp_kernels.cuh"
+
+namespace ppgpu {
+
+constexpr uint32_t kItem = 2048;  // strings per regroup work item
+
+struct Item {
+  uint32_t g;
+  uint32_t start;
+  uint32_t len;
+  uint32_t pad;
+  unsigned long long rbase;
+};
+
+template <int W>
+struct Record {
+  Plane<W> x, z;
+  double c;
+};
+
+// (a) fused run of Clifford gates.  Gate planes live in device memory.
+template <int W>
+struct CliffordProducer {
+  static constexpr int kMaxRec = 1;
+  const uint64_t* gx;  // [ng][W]
+  const uint64_t* gz;  // [ng][W]
+  const double* gsin;  // [ng], +-1
+  int ng;
+  __device__ __forceinline__ int emit(Plane<W> x, Plane<W> z, double c, Record<W>* out, uint32_t* nrec) const {
+    uint32_t moved = 0;
+    for (int i = 0; i < ng; ++i) {
+      Plane<W> jx, jz;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        jx.w[k] = gx[i * W + k];
+        jz.w[k] = gz[i * W + k];
+      }
+      if (plane_parity_and<W>(x, jz) ^ plane_parity_and<W>(z, jx)) {
+        int b = phase_mod4<W>(x, z, jx, jz);
+        double f = b == 1 ? gsin[i] : -gsin[i];  // record_sign * sin (engine.cpp:224)
+        c = __dmul_rn(f, c);                     // exact: |f| == 1
+        x = plane_xor<W>(x, jx);
+        z = plane_xor<W>(z, jz);
+        moved += (c != 0.0);
+      }
+    }
+    out[0].x = x;
+    out[0].z = z;
+    out[0].c = c;
+    *nrec = moved;
+    return 1;
+  }
+};
+
+// (b) one general gate: parent scaled by cos when it anticommutes, plus the
+// child (I xor J, (+-sin) c) when the increment is nonzero (engine.cpp:
+// 218-245).
+template <int W>
+struct GateProducer {
+  static constexpr int kMaxRec = 2;
+  Plane<W> jx, jz;
+  double cosv, sinv;
+  __device__ __forceinline__ int emit(Plane<W> x, Plane<W> z, double c, Record<W>* out, uint32_t* nrec) const {
+    out[0].x = x;
+    out[0].z = z;
+    *nrec = 0;
+    if (!(plane_parity_and<W>(x, jz) ^ plane_parity_and<W>(z, jx))) {
+      out[0].c = c;
+      return 1;
+    }
+    int b = phase_mod4<W>(x, z, jx, jz);
+    out[0].c = __dmul_rn(c, cosv);
+    double d = __dmul_rn(b == 1 ? sinv : -sinv, c);
+    if (d == 0.0) return 1;
+    out[1].x = plane_xor<W>(x, jx);
+    out[1].z = plane_xor<W>(z, jz);
+    out[1].c = d;
+    *nrec = 1;
+    return 2;
+  }
+};
+
+template <int W>
+struct HashTable {
+  unsigned long long* fp;  // 0 = empty
+  uint64_t* z[W];
+  uint32_t* count;
+  uint32_t* gid;
+  unsigned long long mask;
+};
+
+// work items: chunks of <= kItem strings of one group
+template <int W>
+__global__ void k_make_items(GroupView<W> g, uint32_t G, Item* items, int maxrec, DevStats* st) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G) return;
+  uint32_t n = g.cnt[i];
+  if (!n) return;
+  uint32_t nch = (n + kItem - 1) / kItem;
+  unsigned long long base = atomicAdd(&st->items, (unsigned long long)nch);
+  unsigned long long rb = atomicAdd(&st->rec_total, (unsigned long long)n * maxrec);
+  for (uint32_t k = 0; k < nch; ++k) {
+    Item it;
+    it.g = i;
+    it.start = k * kItem;
+    it.len = min(kItem, n - k * kItem);
+    it.pad = 0;
+    it.rbase = rb + (unsigned long long)k * kItem * maxrec;
+    items[base + k] = it;
+  }
+}
+
+template <int W>
+__device__ __forceinline__ unsigned long long z_fingerprint(const Plane<W>& z, unsigned long long seed) {
+  unsigned long long f = plane_hash<W>(z, seed);
+  return f ? f : 1ull;
+}
+
+template <int W, class P>
+__global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W> g, ArenaView<W> src, P prod,
+                                                 HashTable<W> t, uint32_t* rec_slot, unsigned long long seed,
+                                                 uint32_t max_distinct, DevStats* st) {
+  const Item it = items[blockIdx.x];
+  const uint64_t off = g.off[it.g] + it.start;
+  const Plane<W> z = load_plane<W>(g.z, it.g);
+  unsigned long long records = 0;
+  for (uint32_t i = threadIdx.x; i < it.len; i += kCta) {
+    Record<W> rec[P::kMaxRec];
+    uint32_t nr = 0;
+    int nrec = prod.emit(load_plane<W>(src.x, off + i), z, src.c[off + i], rec, &nr);
+    records += nr;
+#pragma unroll
+    for (int r = 0; r < P::kMaxRec; ++r) {
+      uint32_t slot_out = 0xffffffffu;
+      if (r < nrec) {
+        unsigned long long f = z_fingerprint<W>(rec[r].z, seed);
+        unsigned long long s = f & t.mask;
+        for (unsigned long long probe = 0;; ++probe) {
+          unsigned long long cur = t.fp[s];
+          if (cur == 0) {
+            cur = atomicCAS(&t.fp[s], 0ull, f);
+            if (cur == 0) {
+              uint32_t d = atomicAdd(&st->distinct, 1u);
+              if (d >= max_distinct) atomicOr(&st->overflow, 1u);
+              store_plane<W>(t.z, s, rec[r].z);
+              cur = f;
+            }
+          }
+          if (cur == f) break;
+          s = (s + 1) & t.mask;
+          if (probe > t.mask) {
+            atomicOr(&st->overflow, 1u);
+            break;
+          }
+        }
+        atomicAdd(&t.count[s], 1u);
+        slot_out = (uint32_t)s;
+      }
+      rec_slot[it.rbase + (unsigned long long)i * P::kMaxRec + r] = slot_out;
+    }
+  }
+  records = warp_sum64(records);
+  if ((threadIdx.x & 31) == 0 && records) atomicAdd(&st->records, records);
+}
+
+// --------------------------- device-wide exclusive scan over uint32 -> u64
+constexpr uint32_t kScanPer = 8;
+constexpr uint32_t kScanTile = kCta * kScanPer;
+
+__global__ void __launch_bounds__(kCta) k_scan_tiles(const uint32_t* in, unsigned long long n, int as_flag,
+                                                     unsigned long long* tile_sums) {
+  __shared__ unsigned long long red[kWarps];
+  unsigned long long b = (unsigned long long)blockIdx.x * kScanTile;
+  unsigned long long s = 0;
+  for (uint32_t k = 0; k < kScanPer; ++k) {
+    unsigned long long i = b + k * kCta + threadIdx.x;
+    if (i < n) {
+      uint32_t v = in[i];
+      s += as_flag ? (v != 0) : v;
+    }
+  }
+  s = warp_sum64(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (uint32_t w = 0; w < kWarps; ++w) t += red[w];
+    tile_sums[blockIdx.x] = t;
+  }
+}
+
+// single CTA: exclusive scan of tile sums in place, total at [ntiles]
+__global__ void __launch_bounds__(kCta) k_scan_sums(unsigned long long* sums, unsigned long long ntiles) {
+  __shared__ unsigned long long carry_s;
+  __shared__ unsigned long long wsum[kWarps];
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (unsigned long long base = 0; base < ntiles; base += kCta) {
+    unsigned long long i = base + threadIdx.x;
+    unsigned long long v = i < ntiles ? sums[i] : 0;
+    unsigned long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long nb = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= (uint32_t)o) inc += nb;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    unsigned long long wpre = 0, tot = 0;
+    for (uint32_t w = 0; w < kWarps; ++w) {
+      if (w < warp) wpre += wsum[w];
+      tot += wsum[w];
+    }
+    unsigned long long carry = carry_s;
+    if (i < ntiles) sums[i] = carry + wpre + inc - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[ntiles] = carry_s;
+}
+
+__global__ void __launch_bounds__(kCta) k_scan_apply(const uint32_t* in, unsigned long long n, int as_flag,
+                                                     const unsigned long long* tile_sums, unsigned long long* out) {
+  __shared__ unsigned long long wsum[kWarps];
+  __shared__ unsigned long long carry_s;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = tile_sums[blockIdx.x];
+  __syncthreads();
+  unsigned long long b = (unsigned long long)blockIdx.x * kScanTile;
+  for (uint32_t k = 0; k < kScanPer; ++k) {
+    unsigned long long i = b + k * kCta + threadIdx.x;
+    unsigned long long v = 0;
+    if (i < n) {
+      uint32_t x = in[i];
+      v = as_flag ? (x != 0) : x;
+    }
+    unsigned long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long nb = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= (uint32_t)o) inc += nb;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    unsigned long long wpre = 0, tot = 0;
+    for (uint32_t w = 0; w < kWarps; ++w) {
+      if (w < warp) wpre += wsum[w];
+      tot += wsum[w];
+    }
+    unsigned long long carry = carry_s;
+    if (i < n) out[i] = carry + wpre + inc - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + tot;
+    __syncthreads();
+  }
+}
+
+// new group table from the hash table (slot order => deterministic ids)
+template <int W>
+__global__ void k_table_emit(HashTable<W> t, const unsigned long long* gid_scan, const unsigned long long* off_scan,
+                             GroupView<W> ng, uint64_t arena_base) {
+  unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > t.mask) return;
+  uint32_t c = t.count[s];
+  if (!c) return;
+  uint32_t gid = (uint32_t)gid_scan[s];
+  t.gid[s] = gid;
+#pragma unroll
+  for (int k = 0; k < W; ++k) ng.z[k][gid] = t.z[k][s];
+  ng.off[gid] = arena_base + off_scan[s];
+  ng.cap[gid] = c;
+  ng.cnt[gid] = 0;  // scatter cursor
+  ng.flags[gid] = 0;
+}
+
+template <int W, class P>
+__global__ void __launch_bounds__(kCta) k_scatter(const Item* items, GroupView<W> g, ArenaView<W> src, P prod,
+                                                  HashTable<W> t, const uint32_t* rec_slot, GroupView<W> ng,
+                                                  ArenaView<W> dst, DevStats* st) {
+  const Item it = items[blockIdx.x];
+  const uint64_t off = g.off[it.g] + it.start;
+  const Plane<W> z = load_plane<W>(g.z, it.g);
+  for (uint32_t i = threadIdx.x; i < it.len; i += kCta) {
+    Record<W> rec[P::kMaxRec];
+    uint32_t nr;
+    int nrec = prod.emit(load_plane<W>(src.x, off + i), z, src.c[off + i], rec, &nr);
+#pragma unroll
+    for (int r = 0; r < P::kMaxRec; ++r) {
+      if (r >= nrec) break;
+      uint32_t s = rec_slot[it.rbase + (unsigned long long)i * P::kMaxRec + r];
+      if (!plane_eq<W>(load_plane<W>(t.z, s), rec[r].z)) {  // 64-bit fingerprint collision
+        atomicOr(&st->collision, 1u);
+        continue;
+      }
+      uint32_t gid = t.gid[s];
+      uint64_t pos = ng.off[gid] + atomicAdd(&ng.cnt[gid], 1u);
+      store_plane<W>(dst.x, pos, rec[r].x);
+      dst.c[pos] = rec[r].c;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-group sort by x + pair combine + zero drop
+// ---------------------------------------------------------------------------
+constexpr uint32_t kSortSmall = 2048;
+
+template <int W>
+struct SortSmem {
+  uint64_t key[W * kSortSmall];
+  double val[kSortSmall];
+  uint32_t scan[40];
+};
+
+// bitonic sort of smem [0, npow2) (npow2 power of two, padded with max keys)
+template <int W>
+__device__ void smem_bitonic(uint64_t* key, double* val, uint32_t stride, uint32_t npow2) {
+  for (uint32_t size = 2; size <= npow2; size <<= 1) {
+    for (uint32_t j = size >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = threadIdx.x; t < (npow2 >> 1); t += blockDim.x) {
+        uint32_t i = 2 * j * (t / j) + (t % j);
+        uint32_t l = i + j;
+        bool up = ((i & size) == 0);
+        Plane<W> a = sk_load<W>(key, stride, i), b = sk_load<W>(key, stride, l);
+        bool swap = up ? plane_lt<W>(b, a) : plane_lt<W>(a, b);
+        if (swap) {
+          sk_store<W>(key, stride, i, b);
+          sk_store<W>(key, stride, l, a);
+          double tv = val[i];
+          val[i] = val[l];
+          val[l] = tv;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// combine adjacent equal keys of a sorted sequence, drop zeros (unless
+// keep_zeros), stream to dst; accessor functions read the sorted input.
+// Returns the number written; accumulates stats.  `in_key/in_val` are the
+// sorted input (global or shared), `dst` the output region (may alias the
+// input when writes never overtake reads, which holds for in-place use).
+template <int W, class GetK, class GetV>
+__device__ uint32_t combine_stream(uint32_t n, GetK getk, GetV getv, ArenaView<W> ar, uint64_t dst, int keep_zeros,
+                                   uint32_t* scan, double& vmax, double& vmin, uint32_t& nonfinite,
+                                   unsigned long long& removed) {
+  uint32_t w = 0;
+  for (uint32_t base = 0; base < n; base += kCta) {
+    uint32_t p = base + threadIdx.x;
+    bool e = false;
+    Plane<W> k;
+    double v = 0.0;
+    if (p < n) {
+      k = getk(p);
+      bool head = (p == 0) || !plane_eq<W>(getk(p - 1), k);
+      if (head) {
+        v = getv(p);
+        if (p + 1 < n && plane_eq<W>(getk(p + 1), k)) v = __dadd_rn(v, getv(p + 1));
+        e = keep_zeros || v != 0.0;
+        if (!e) ++removed;
+      }
+    }
+    uint32_t tot;
+    uint32_t o = block_excl_scan(e ? 1u : 0u, scan, &tot);
+    if (e) {
+      store_plane<W>(ar.x, dst + w + o, k);
+      ar.c[dst + w + o] = v;
+      double av = fabs(v);
+      if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
+      vmax = fmax(vmax, av);
+      vmin = fmin(vmin, av);
+    }
+    w += tot;
+    __syncthreads();
+  }
+  return w;
+}
+
+template <int W>
+__device__ void finish_group_stats(GroupView<W> g, uint32_t gid, uint32_t count, double vmax, double vmin,
+                                   uint32_t nonfinite, unsigned long long removed, DevStats* st) {
+  __shared__ double rmx[kWarps], rmn[kWarps];
+  __shared__ unsigned long long rrm[kWarps];
+  __shared__ uint32_t rnf[kWarps];
+  vmax = warp_max(vmax);
+  vmin = warp_min(vmin);
+  removed = warp_sum64(removed);
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  const uint32_t tid = threadIdx.x;
+  if ((tid & 31) == 0) {
+    rmx[tid >> 5] = vmax;
+    rmn[tid >> 5] = vmin;
+    rrm[tid >> 5] = removed;
+    rnf[tid >> 5] = nonfinite;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (uint32_t i = 1; i < kWarps; ++i) {
+      vmax = fmax(vmax, rmx[i]);
+      vmin = fmin(vmin, rmn[i]);
+      removed += rrm[i];
+      nonfinite |= rnf[i];
+    }
+    g.cnt[gid] = count;
+    g.gmax[gid] = count ? vmax : 0.0;
+    g.gmin[gid] = count ? vmin : __longlong_as_double(0x7ff0000000000000ll);
+    g.flags[gid] = nonfinite;
+    if (removed) atomicAdd(&st->removed, removed);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W> ar, int keep_zeros, DevStats* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem<W>& sm = *reinterpret_cast<SortSmem<W>*>(smem_raw);
+  const uint32_t gid = blockIdx.x;
+  const uint32_t n = g.cnt[gid];
+  if (n > kSortSmall) return;
+  const uint64_t off = g.off[gid];
+  uint32_t np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  for (uint32_t i = threadIdx.x; i < np2; i += kCta) {
+    if (i < n) {
+      sk_store<W>(sm.key, kSortSmall, i, load_plane<W>(ar.x, off + i));
+      sm.val[i] = ar.c[off + i];
+    } else {
+      sk_store<W>(sm.key, kSortSmall, i, plane_max<W>());
+      sm.val[i] = 0.0;
+    }
+  }
+  __syncthreads();
+  if (np2 > 1) smem_bitonic<W>(sm.key, sm.val, kSortSmall, np2);
+  double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);
+  uint32_t nf = 0;
+  unsigned long long removed = 0;
+  auto getk = [&](uint32_t p) { return sk_load<W>(sm.key, kSortSmall, p); };
+  auto getv = [&](uint32_t p) { return sm.val[p]; };
+  uint32_t w = combine_stream<W>(n, getk, getv, ar, off, keep_zeros, sm.scan, vmax, vmin, nf, removed);
+  finish_group_stats<W>(g, gid, w, vmax, vmin, nf, removed, st);
+}
+
+// two-run merge of sorted runs a=[0,na) and b=[0,nb) (global) into out,
+// stable (ties: a first), one CTA, buffered through shared memory.
+template <int W>
+struct MergeSmem {
+  uint64_t key[2][W * kBufCap];
+  double val[2][kBufCap];
+  uint64_t okey[W * 2 * kBufCap];
+  double oval[2 * kBufCap];
+  uint32_t cnt[2], pos[2], m[2];
+};
+
+template <int W>
+__device__ void cta_merge_runs(MergeSmem<W>& sm, ArenaView<W> ar, uint64_t a, uint32_t na, uint64_t b, uint32_t nb,
+                               ArenaView<W> out, uint64_t o) {
+  const uint32_t tid = threadIdx.x;
+  const uint64_t srcb[2] = {a, b};
+  const uint32_t len[2] = {na, nb};
+  if (tid == 0) {
+    sm.cnt[0] = sm.cnt[1] = 0;
+    sm.pos[0] = sm.pos[1] = 0;
+  }
+  __syncthreads();
+  uint64_t written = 0;
+  for (;;) {
+    for (int s = 0; s < 2; ++s) {
+      while (sm.cnt[s] < kRefill && sm.pos[s] < len[s]) {
+        uint32_t take = min(kCta, len[s] - sm.pos[s]);
+        if (tid < take) {
+          uint64_t p = srcb[s] + sm.pos[s] + tid;
+          sk_store<W>(sm.key[s], kBufCap, sm.cnt[s] + tid, load_plane<W>(ar.x, p));
+          sm.val[s][sm.cnt[s] + tid] = ar.c[p];
+        }
+        __syncthreads();
+        if (tid == 0) {
+          sm.cnt[s] += take;
+          sm.pos[s] += take;
+        }
+        __syncthreads();
+      }
+    }
+    if (tid < 2) {
+      Plane<W> kmax = plane_max<W>();
+      bool bounded = false;
+      for (int s = 0; s < 2; ++s) {
+        if (sm.pos[s] < len[s]) {
+          Plane<W> last = sk_load<W>(sm.key[s], kBufCap, sm.cnt[s] - 1);
+          if (!bounded || plane_lt<W>(last, kmax)) kmax = last;
+          bounded = true;
+        }
+      }
+      sm.m[tid] = bounded ? sk_upper_bound<W>(sm.key[tid], kBufCap, sm.cnt[tid], kmax) : sm.cnt[tid];
+    }
+    __syncthreads();
+    const uint32_t ma = sm.m[0], mb = sm.m[1];
+    for (uint32_t i = tid; i < ma + mb; i += kCta) {
+      bool isa = i < ma;
+      uint32_t j = isa ? i : i - ma;
+      Plane<W> k = sk_load<W>(sm.key[isa ? 0 : 1], kBufCap, j);
+      uint32_t r = isa ? j + sk_lower_bound<W>(sm.key[1], kBufCap, mb, k)
+                       : j + sk_upper_bound<W>(sm.key[0], kBufCap, ma, k);
+      sk_store<W>(sm.okey, 2 * kBufCap, r, k);
+      sm.oval[r] = sm.val[isa ? 0 : 1][j];
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < ma + mb; i += kCta) {
+      store_plane<W>(out.x, o + written + i, sk_load<W>(sm.okey, 2 * kBufCap, i));
+      out.c[o + written + i] = sm.oval[i];
+    }
+    written += ma + mb;
+    // shift remaining
+    uint32_t rem[2] = {sm.cnt[0] - ma, sm.cnt[1] - mb};
+    Plane<W> tk[2][kBufCap / kCta];
+    double tv[2][kBufCap / kCta];
+    for (int s = 0; s < 2; ++s)
+      for (uint32_t r = 0; r < kBufCap / kCta; ++r) {
+        uint32_t i = tid + r * kCta;
+        if (i < rem[s]) {
+          tk[s][r] = sk_load<W>(sm.key[s], kBufCap, sm.m[s] + i);
+          tv[s][r] = sm.val[s][sm.m[s] + i];
+        }
+      }
+    __syncthreads();
+    for (int s = 0; s < 2; ++s)
+      for (uint32_t r = 0; r < kBufCap / kCta; ++r) {
+        uint32_t i = tid + r * kCta;
+        if (i < rem[s]) {
+          sk_store<W>(sm.key[s], kBufCap, i, tk[s][r]);
+          sm.val[s][i] = tv[s][r];
+        }
+      }
+    __syncthreads();
+    bool done = rem[0] == 0 && rem[1] == 0 && sm.pos[0] >= len[0] && sm.pos[1] >= len[1];
+    if (tid == 0) {
+      sm.cnt[0] = rem[0];
+      sm.cnt[1] = rem[1];
+    }
+    __syncthreads();
+    if (done) break;
+  }
+}
+
+// big groups (> kSortSmall): chunk bitonic sorts, then log2 merge passes
+// ping-ponging between the group's region and a scratch region, then the
+// combine pass back into the region.  One CTA per group.
+template <int W>
+__global__ void __launch_bounds__(kCta) k_sort_big(GroupView<W> g, ArenaView<W> ar, ArenaView<W> scratch,
+                                                   int keep_zeros, DevStats* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t gid = blockIdx.x;
+  const uint32_t n = g.cnt[gid];
+  if (n <= kSortSmall) return;
+  const uint64_t off = g.off[gid];
+  __shared__ unsigned long long so_s;
+  if (threadIdx.x == 0) so_s = atomicAdd(&st->scratch_bump, (unsigned long long)n);
+  __syncthreads();
+  const uint64_t so = so_s;
+  {
+    SortSmem<W>& sm = *reinterpret_cast<SortSmem<W>*>(smem_raw);
+    for (uint32_t c0 = 0; c0 < n; c0 += kSortSmall) {
+      uint32_t len = min(kSortSmall, n - c0);
+      for (uint32_t i = threadIdx.x; i < kSortSmall; i += kCta) {
+        if (i < len) {
+          sk_store<W>(sm.key, kSortSmall, i, load_plane<W>(ar.x, off + c0 + i));
+          sm.val[i] = ar.c[off + c0 + i];
+        } else {
+          sk_store<W>(sm.key, kSortSmall, i, plane_max<W>());
+          sm.val[i] = 0.0;
+        }
+      }
+      __syncthreads();
+      smem_bitonic<W>(sm.key, sm.val, kSortSmall, kSortSmall);
+      for (uint32_t i = threadIdx.x; i < len; i += kCta) {
+        store_plane<W>(ar.x, off + c0 + i, sk_load<W>(sm.key, kSortSmall, i));
+        ar.c[off + c0 + i] = sm.val[i];
+      }
+      __syncthreads();
+    }
+  }
+  MergeSmem<W>& mm = *reinterpret_cast<MergeSmem<W>*>(smem_raw);
+  bool in_region = true;
+  for (uint32_t run = kSortSmall; run < n; run <<= 1) {
+    ArenaView<W> from = in_region ? ar : scratch;
+    ArenaView<W> to = in_region ? scratch : ar;
+    uint64_t fo = in_region ? off : so, to_o = in_region ? so : off;
+    for (uint32_t s0 = 0; s0 < n; s0 += 2 * run) {
+      uint32_t na = min(run, n - s0);
+      uint32_t nb = (s0 + run < n) ? min(run, n - s0 - run) : 0;
+      if (nb == 0) {
+        for (uint32_t i = threadIdx.x; i < na; i += kCta) {
+          store_plane<W>(to.x, to_o + s0 + i, load_plane<W>(from.x, fo + s0 + i));
+          to.c[to_o + s0 + i] = from.c[fo + s0 + i];
+        }
+        __syncthreads();
+      } else {
+        // cta_merge_runs reads from a single arena view; both runs are in `from`
+        cta_merge_runs<W>(mm, from, fo + s0, na, fo + s0 + run, nb, to, to_o + s0);
+      }
+    }
+    in_region = !in_region;
+    __syncthreads();
+  }
+  __shared__ uint32_t scan[40];
+  double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);
+  uint32_t nf = 0;
+  unsigned long long removed = 0;
+  ArenaView<W> fin = in_region ? ar : scratch;
+  uint64_t fo = in_region ? off : so;
+  auto getk = [&](uint32_t p) { return load_plane<W>(fin.x, fo + p); };
+  auto getv = [&](uint32_t p) { return fin.c[fo + p]; };
+  uint32_t w = combine_stream<W>(n, getk, getv, ar, off, keep_zeros, scan, vmax, vmin, nf, removed);
+  finish_group_stats<W>(g, gid, w, vmax, vmin, nf, removed, st);
+}
+
+}  // namespace ppgpu

@@ -1,0 +1,234 @@
+"""Parity of the CUDA path (through the C-ABI / pybind engine) against the
+oracle restatement (oracle/pp_oracle.c), bit-exact for string sets and
+coefficients (BASELINE.json north_star tolerance
+1e-12 relative applies to <Z>, which is summed in a different order)."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import assert_same_terms, gate_tuples
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_close(a, b, tol=1e-12):
+    return abs(a - b) <= tol * max(1.0, abs(b))
+
+
+def random_words(rng, n):
+    w = np.zeros(4, np.uint64)
+    for site in range(n):
+        w[site // 32] |= np.uint64(int(rng.integers(4))) << np.uint64(2 * (site % 32))
+    return w
+
+
+def run_both(pp, O, n, layers, initial, eps=0.0, cadence="gate", steps=None, check_each=True, fuse=True):
+    """layers: list of lists of product Gates (forward order)."""
+    words = np.stack([w for w, _ in initial]).astype(np.uint64)
+    coeffs = np.array([c for _, c in initial], np.float64)
+    eng = pp.Engine(n, eps, cadence, fuse_clifford=fuse)
+    eng.set_initial(words, coeffs)
+    ora = O.OracleEngine(n, eps, 1 if cadence == "layer" else 0)
+    ora.set_initial(words, coeffs)
+    circ_layers = layers
+    L = len(circ_layers)
+    for t in range(1, L + 1):
+        layer = circ_layers[L - t]
+        eng.apply_gates(list(reversed(layer)))
+        for g in reversed(gate_tuples(layer)):
+            ora.apply_gate(*g)
+        if cadence == "layer":
+            eng.truncate_now()
+            ora.truncate_now()
+        ctr = eng.take_counters()
+        octr = ora.take_counters()
+        if check_each or t == L:
+            w, c = eng.export()
+            ow, oc = ora.export()
+            assert_same_terms(w, c, ow, oc, f"layer {t}")
+            assert eng.term_count() == ora.term_count()
+            assert rel_close(eng.expectation_zero_state(), ora.expectation())
+            assert eng.global_max() == ora.global_max()
+            assert ctr["records_sent"] == octr["records_sent"], (ctr, octr)
+    return eng, ora
+
+
+def test_single_qubit_rotation_signs(pp, O):
+    # test_engine.cpp:77-91: X under Z(theta) -> cos X, record (Y, -sin)
+    theta = 0.81
+    eng = pp.Engine(1, 0.0)
+    eng.set_initial(O.site_word(0, 1)[None], np.array([1.0]))
+    g = pp.Gate(pp.PauliString("Z0", 1), theta)
+    eng.apply_gate(g)
+    assert eng.coefficient(pp.PauliString("X0", 1)) == math.cos(theta) * 1.0
+    assert eng.coefficient(pp.PauliString("Y0", 1)) == -math.sin(theta) * 1.0
+    assert eng.term_count() == 2
+
+
+def test_rx_signs_match_oracle(pp, O):
+    # Rx on Z and Y: c'_Y = cos c_Y + sin c_Z ; c'_Z = cos c_Z - sin c_Y
+    for init in (["Z0"], ["Y0"], ["Z0", "Y0"]):
+        terms = [(np.asarray(pp.PauliString(l, 1).words), 0.5 + i) for i, l in enumerate(init)]
+        layers = [[pp.Gate(pp.PauliString("X0", 1), 0.3)]]
+        run_both(pp, O, 1, layers, terms)
+
+
+def test_commuting_and_theta_zero(pp, O):
+    # test_engine.cpp:93-120
+    terms = [(np.asarray(pp.PauliString("Z2 Z0", 3).words), 0.5), (np.asarray(pp.PauliString("Z1", 3).words), -0.25)]
+    run_both(pp, O, 3, [[pp.Gate(pp.PauliString("Z2", 3), 1.1)]], terms)
+    run_both(pp, O, 3, [[pp.Gate(pp.PauliString("X0", 3), 0.0)]], terms)
+    run_both(pp, O, 3, [[pp.Gate(pp.PauliString("X1", 3), "0.5pi")]], terms)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("eps,cadence", [(0.0, "gate"), (1e-3, "gate"), (1e-2, "layer")])
+def test_random_circuits(pp, O, seed, eps, cadence):
+    # test_engine.cpp:148-175 / acceptance criterion 3 (random generators of
+    # any weight, radian angles in [-3, 3])
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 11))
+    layers = []
+    for _ in range(int(rng.integers(1, 4))):
+        layer = []
+        for _ in range(int(rng.integers(1, 8))):
+            layer.append(pp.Gate(pp.PauliString.from_words(random_words(rng, n)), float(rng.uniform(-3, 3))))
+        layers.append(layer)
+    site = int(rng.integers(n))
+    run_both(pp, O, n, layers, [(O.site_word(site, 3), 1.0)], eps, cadence)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_x_and_zz_circuits_many_terms(pp, O, seed):
+    # kicked-Ising-like gates (Rx + Rzz, some Clifford) on a random initial sum
+    rng = np.random.default_rng(77 + seed)
+    n = [5, 12, 40, 64, 65, 127][seed]
+    init = [(random_words(rng, n), float(rng.uniform(-1, 1))) for _ in range(200)]
+    layer = []
+    for q in range(n):
+        layer.append(pp.Gate(pp.PauliString(f"X{q}", n), float(rng.uniform(-3, 3))))
+    for q in range(n - 1):
+        ang = "-0.5pi" if rng.random() < 0.7 else float(rng.uniform(-3, 3))
+        layer.append(pp.Gate(pp.PauliString(f"Z{q} Z{q + 1}", n), ang))
+    run_both(pp, O, n, [layer, layer], init, 1e-4)
+
+
+def test_duplicate_and_zero_initial_terms(pp, O):
+    n = 4
+    a = np.asarray(pp.PauliString("Z0 X1", n).words)
+    b = np.asarray(pp.PauliString("Y2", n).words)
+    init = [(a, 0.5), (b, 0.0), (a, 0.25), (b, 1e-30), (a, -0.75)]
+    layers = [[pp.Gate(pp.PauliString("X0", n), 0.4), pp.Gate(pp.PauliString("Z1 Z2", n), 0.7)]]
+    for cad in ("gate", "layer"):
+        run_both(pp, O, n, layers, init, 0.0, cad)
+
+
+def test_identity_generator_and_empty_operator(pp, O):
+    n = 3
+    layers = [[pp.Gate(pp.PauliString("III", n), 0.5), pp.Gate(pp.PauliString("X1", n), 0.5)]]
+    run_both(pp, O, n, layers, [(O.site_word(1, 3), 1.0)])
+    eng = pp.Engine(n, 0.0)
+    eng.set_initial(np.zeros((0, 4), np.uint64), np.zeros(0))
+    eng.apply_gate(layers[0][1])
+    assert eng.term_count() == 0
+    assert eng.expectation_zero_state() == 0.0
+
+
+def _kicked(pp, geom, thx, layers):
+    return pp.build_kicked_ising(geom, thx, "-0.5pi", layers)
+
+
+def test_heavy_hex_config1_bitexact(pp, O):
+    # BASELINE config 1: theta_h = pi/4, eps0 = 0, Z62, 5 steps (2,146,372 strings)
+    geom = pp.heavy_hex_127()
+    circ = _kicked(pp, geom, "0.25pi", 5)
+    eng, ora = run_both(pp, O, 127, list(circ.layers), [(O.site_word(62, 3), 1.0)], 0.0, "gate")
+    assert eng.term_count() == 2146372
+
+
+def test_table1_rows(pp, O):
+    # PAPER.md Table I / acceptance_main.cpp:99-109
+    geom = pp.heavy_hex_127()
+    exact = [-0.95105651629515, 0.90450849718747, -0.9423841865631, 0.97436799430396, -0.95315824248965]
+    tol = [1e-11, 1e-11, 1e-11, 1e-10, 1e-10]
+    eng = pp.Engine(127, 0.0)
+    eng.set_initial(O.site_word(62, 3)[None], np.array([1.0]))
+    rows = eng.run_circuit(_kicked(pp, geom, "0.9pi", 5))
+    for r, v, t in zip(rows, exact, tol):
+        assert abs(r["observable"] - v) < t
+    eng = pp.Engine(127, 1e-5)
+    eng.set_initial(O.site_word(62, 3)[None], np.array([1.0]))
+    rows = eng.run_circuit(_kicked(pp, geom, "0.9pi", 5))
+    assert abs(rows[3]["observable"] - 0.97438562148434) < 1e-9
+    assert abs(rows[4]["observable"] - -0.95311531321393) < 1e-9
+
+
+def test_clifford_regimes(pp, O):
+    # acceptance_main.cpp:417-453: theta_x = 0 and pi/2 keep |O| = 1
+    geom = pp.heavy_hex_127()
+    for thx in ("0pi", "0.5pi"):
+        eng = pp.Engine(127, 0.0)
+        eng.set_initial(O.site_word(62, 3)[None], np.array([1.0]))
+        rows = eng.run_circuit(_kicked(pp, geom, thx, 20))
+        assert all(r["term_count"] == 1 for r in rows)
+        if thx == "0pi":
+            assert all(r["observable"] == 1.0 for r in rows)
+
+
+def test_chain_config0_bitexact(pp, O):
+    # BASELINE config 0 prefix: n = 64 chain, theta_h = 0.3 rad, eps0 = 0
+    text = "\n".join(f"{i} {i + 1} {i % 2}" for i in range(63))
+    geom = pp.load_geometry(text)
+    circ = pp.build_kicked_ising(geom, 0.3, "-0.5pi", 7)
+    eng, _ = run_both(pp, O, 64, list(circ.layers), [(O.site_word(32, 3), 1.0)], 0.0, "gate", check_each=False)
+    assert eng.term_count() == 613470
+
+
+def test_truncated_heavy_hex_bitexact(pp, O):
+    geom = pp.heavy_hex_127()
+    circ = _kicked(pp, geom, "0.25pi", 7)
+    run_both(pp, O, 127, list(circ.layers), [(O.site_word(62, 3), 1.0)], 1e-4, "gate", check_each=True)
+
+
+def test_non_clifford_zz_config4_shape(pp, O):
+    # BASELINE config 4 shape: theta_J = -pi/2 + 0.2 (Rzz branches), sum Z_i / 127
+    geom = pp.heavy_hex_127()
+    circ = pp.build_kicked_ising(geom, 0.4, -math.pi / 2 + 0.2, 3)
+    init = [(O.site_word(q, 3), 1.0 / 127) for q in range(127)]
+    run_both(pp, O, 127, list(circ.layers), init, 1e-4, "gate")
+
+
+def test_budget_and_nan(pp, O):
+    geom = pp.heavy_hex_127()
+    with pytest.raises(pp.ResourceLimitError):
+        pp.simulate(_kicked(pp, geom, "0.25pi", 6), observable="Z62", max_terms=100)
+    eng = pp.Engine(2, 0.0)
+    eng.set_initial(O.site_word(0, 3)[None], np.array([math.inf]))
+    with pytest.raises(pp.NumericalError):
+        eng.apply_gate(pp.Gate(pp.PauliString("X0", 2), 0.3))
+
+
+def test_simulate_reference_smoke_values(pp):
+    # tests/python/test_smoke.py:59-66 of the reference
+    geom = pp.heavy_hex_127()
+    rows = pp.simulate(pp.build_kicked_ising(geom, "0.9pi", "-0.5pi", layers=1), observable="Z62", workers=2)
+    assert len(rows) == 1
+    assert rows[0]["observable"] == pytest.approx(math.cos(0.9 * math.pi), abs=1e-12)
+    assert rows[0]["term_count"] == 2
+
+
+def test_fusion_matches_unfused(pp, O):
+    geom = pp.heavy_hex_127()
+    circ = _kicked(pp, geom, "0.25pi", 4)
+    a = pp.Engine(127, 0.0, fuse_clifford=True)
+    b = pp.Engine(127, 0.0, fuse_clifford=False)
+    for e in (a, b):
+        e.set_initial(O.site_word(62, 3)[None], np.array([1.0]))
+    ra, rb = a.run_circuit(circ), b.run_circuit(circ)
+    wa, ca = a.export()
+    wb, cb = b.export()
+    assert_same_terms(wa, ca, wb, cb, "fused vs unfused")
+    for x, y in zip(ra, rb):
+        for k in ("term_count", "removed", "records_sent"):
+            assert x[k] == y[k], (k, x, y)
