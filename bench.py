@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark of the Heisenberg-picture Pauli-propagation hot path on B200.
+
+Metric (BASELINE.json): Pauli-string terms processed per second per gate
+layer = string-gates/s, where one string-gate is one live string entering
+one gate.  Sum over gates of |O_in| / time.
+
+Workload (default, BASELINE.json configs[1]): 127-qubit heavy-hex kicked
+Ising, theta_h = pi/4, theta_J = -pi/2 (Clifford ZZ), O0 = Z62, eps0 = 0,
+5 Trotter steps (final |O| = 2,146,372).  One bench step = one full
+propagation of that circuit from O0 (1,355 gates), readout after every
+layer, exactly what the reference's run_circuit does.
+
+  value -- device-timed (CUDA events on the engine's stream), state created
+           on the device, string-gates/s
+  e2e   -- the public API call a user makes (simulate(...)), host circuit
+           in, ledger rows out, wall-clocked around the call
+  cpu_baseline -- the reference engine compiled from its own sources
+           (oracle/_ref), on this box's host cores
+
+``--impl reference`` times the reference CPU engine on the same workload.
+Under torchrun (N > 1) every rank runs an independent replica (weak
+scaling; the sharded exchange is not built yet -- DESIGN.md section 6).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (geometry, n, theta_x, theta_zz, observable site, eps0, layers)
+    "config1": ("heavy_hex", 127, "0.25pi", "-0.5pi", 62, 0.0, 5),
+    "config0_t8": ("chain64", 64, 0.3, "-0.5pi", 32, 0.0, 8),
+    "config0_t9": ("chain64", 64, 0.3, "-0.5pi", 32, 0.0, 9),
+    "config2_pi4_eps1e-4_t8": ("heavy_hex", 127, "0.25pi", "-0.5pi", 62, 1e-4, 8),
+}
+
+
+def chain_text(n):
+    return "\n".join(f"{i} {i + 1} {i % 2}" for i in range(n - 1))
+
+
+def build_circuit(pp, wl):
+    geom_kind, n, thx, thzz, site, eps, layers = wl
+    geom = pp.heavy_hex_127() if geom_kind == "heavy_hex" else pp.load_geometry(chain_text(64))
+    return pp.build_kicked_ising(geom, thx, thzz, layers)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def string_gates(pp, circ, wl):
+    """Exact sum over gates of |O_in| for the workload (one counted run,
+    outside every timed region)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    n, site, eps = wl[1], wl[4], wl[5]
+    eng = pp.Engine(n, eps)
+    w = np.zeros((1, 4), np.uint64)
+    w[0, site // 32] = np.uint64(3) << np.uint64(2 * (site % 32))
+    eng.set_initial(w, np.array([1.0]))
+    total = 0
+    L = circ.num_layers()
+    for t in range(1, L + 1):
+        layer = circ.layers[L - t]
+        for g in reversed(layer):
+            total += eng.term_count()
+            eng.apply_gate(g)
+    return total, eng.term_count()
+
+
+def cpu_reference_time(wl, steps, warmup, threads):
+    """Reference CPU engine (oracle/_ref, compiled from the reference's own
+    sources) on the same workload; returns (seconds per step list, string_gates)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import oracle as O
+    geom_kind, n, thx, thzz, site, eps, layers = wl
+    if geom_kind == "heavy_hex":
+        edges, cols = O.ref_heavy_hex()
+        text = "\n".join(f"{a} {b} {c}" for (a, b), c in zip(edges, cols))
+    else:
+        text = chain_text(64)
+    words, is_zz = O.ref_kicked_layer(text)
+
+    def ang(v):
+        if isinstance(v, str):
+            return float(v[:-2]), 1
+        return float(v), 0
+    ax, az = ang(thx), ang(thzz)
+    gates = [(words[i], az[0] if is_zz[i] else ax[0], az[1] if is_zz[i] else ax[1]) for i in range(len(is_zz))]
+    init = np.zeros((1, 4), np.uint64)
+    init[0, site // 32] = np.uint64(3) << np.uint64(2 * (site % 32))
+    times, sg = [], 0.0
+    for i in range(warmup + steps):
+        r = O.RefEngine(n, eps, workers=threads, threads=threads)
+        r.set_initial(init, [1.0])
+        sec, sg = r.time_circuit(gates, layers)
+        if i >= warmup:
+            times.append(sec)
+        del r
+    return times, sg
+
+
+def run_reference_arm(args, wl, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    times, sg = cpu_reference_time(wl, args.steps, args.warmup, threads)
+    per = sorted(times)[len(times) // 2]
+    value = sg / per
+    line = {
+        "metric": "string_gates_per_s", "value": value, "unit": "string-gates/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic circuit)",
+        "impl": "reference",
+        "config": {"workload": args.workload, "string_gates_per_step": sg},
+        "cpu_baseline": {"value": value, "unit": "string-gates/s", "cores": threads, "kind": "reference",
+                         "sample": f"full {args.workload} propagation per step (reference engine, "
+                                   f"{threads} workers/threads, median of {len(times)})"},
+        "e2e": {"value": value, "unit": "string-gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config1", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, wl, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2506_13241_b200 as pp
+
+    circ = build_circuit(pp, wl)
+    n, site, eps = wl[1], wl[4], wl[5]
+    sg, final_terms = string_gates(pp, circ, wl)
+    init = np.zeros((1, 4), np.uint64)
+    init[0, site // 32] = np.uint64(3) << np.uint64(2 * (site % 32))
+
+    # ---------------- device-resident value: CUDA events on the engine stream
+    eng = pp.Engine(n, eps, device=local)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=local)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")  # > 126 MB L2
+
+    def one_step():
+        eng.set_initial(init, np.array([1.0]))
+        rows = eng.run_circuit(circ)
+        return rows
+
+    for _ in range(args.warmup):
+        one_step()
+    eng.kernel_stats()
+    ms = []
+    rows = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rows = one_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+    ks = eng.kernel_stats()
+    assert rows[-1]["term_count"] == final_terms
+    total_ms = sum(ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = sg * world / (ms_per_step / 1e3)
+
+    # ---------------- e2e through the public API (simulate), wall clock
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = pp.simulate(circ, observable=f"Z{site}", epsilon0=eps)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_times.append(t1 - t0)
+    assert out[-1]["term_count"] == final_terms
+    e2e_s = sum(e2e_times) / len(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = sg * world / e2e_s
+    L = circ.num_layers()
+    n_zz_runs = L
+    h2d = 40 + n_zz_runs * 144 * (16 * (1 if n <= 64 else 2) + 8)  # initial term + Clifford-run gate planes
+    d2h = L * (8 * 40)  # per-layer ledger scalars and diagonal readout
+
+    peak, peak_kind = load_peaks()
+    achieved = ks["branch_bytes"] / (ks["branch_ms"] / 1e3) / 1e9 if ks["branch_ms"] > 0 else 0.0
+    launches_per_step = ks["launches"] / args.steps
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "branch_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(args.workload)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            times, csg = cpu_reference_time(wl, 1, 1, threads)
+            cpu = {"value": csg / times[0], "unit": "string-gates/s", "cores": threads, "kind": "reference",
+                   "sample": f"one full {args.workload} propagation (reference engine compiled from its "
+                             f"sources, {threads} workers/threads, after 1 warm-up run)"}
+        except Exception as exc:  # the reference build travels as oracle/_ref
+            cpu = {"value": None, "unit": "string-gates/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "string_gates_per_s", "value": value, "unit": "string-gates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic kicked-Ising circuit, BASELINE config)",
+            "config": {"workload": args.workload, "string_gates_per_step": sg, "final_terms": final_terms,
+                       "layers": L, "gates_per_step": circ.total_gates(),
+                       "l2": "flushed (512 MB write) between timed steps",
+                       "parallelism": f"replicas x{world}"},
+            "e2e": {"value": e2e_value, "unit": "string-gates/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "api": "simulate()"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "kernel": "k_branch_x", "peak_kind": peak_kind,
+                         "bytes_model": "touched: (strings read + strings written) x (8W+8) B per launch",
+                         "branch_ms_per_step": ks["branch_ms"] / args.steps,
+                         "branch_launches_per_step": ks["branch_launches"] / args.steps},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

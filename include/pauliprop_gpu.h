@@ -125,6 +125,10 @@ const char* pp_last_error(const pp_engine* engine);
 int pp_take_kernel_stats(pp_engine* engine, double* branch_ms, double* branch_bytes,
                          uint64_t* branch_launches, uint64_t* total_launches);
 
+/* The CUDA stream (cudaStream_t) the engine launches on, so callers can
+ * bracket work with their own events. */
+void* pp_stream(const pp_engine* engine);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,13 @@ static uint64_t ns_since(Clock::time_point t) {
   return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t).count();
 }
 
+__global__ void k_clear_cumulative(DevStats* st) {
+  st->records = 0;
+  st->removed = 0;
+  st->out_elems = 0;
+  st->aff_total = 0;
+}
+
 __global__ void k_reset_stats(DevStats* st, unsigned long long bump) {
   DevStats s;
   memset(&s, 0, sizeof(s));
@@ -126,13 +133,14 @@ class EngineBase {
   virtual void set_initial(const uint64_t* words, const double* c, size_t count) = 0;
   virtual void apply_gates(const pp_gate* gates, size_t count) = 0;
   virtual void truncate_now() = 0;
-  virtual uint64_t term_count() const = 0;
-  virtual double global_max() const = 0;
+  virtual uint64_t term_count() = 0;
+  virtual double global_max() = 0;
   virtual double expectation() = 0;
   virtual double coefficient(const uint64_t* words) = 0;
   virtual uint64_t export_terms(uint64_t* words, double* c, uint64_t cap) = 0;
   virtual pp_counters take_counters() = 0;
   virtual void take_kernel_stats(double* ms, double* bytes, uint64_t* launches, uint64_t* total) = 0;
+  virtual void* stream() const = 0;
 };
 
 template <int W>
@@ -242,9 +250,12 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(cudaMemcpyAsync(g.gmin, gmn.data(), G * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemcpyAsync(g.flags, gfl.data(), G * 4, cudaMemcpyHostToDevice, stream_));
     }
+    reset_stats(n);
     PP_CUDA(cudaStreamSynchronize(stream_));
-    bump_ = n;
-    live_ = n;
+    bump_ = bump_bound_ = n;
+    live_ = live_bound_ = n;
+    dirty_ = false;
+    truncated_since_sync_ = false;
     gmax_ = gmax;
     counters_ = pp_counters{};
     gates_applied_ = 0;
@@ -268,18 +279,25 @@ class EngineImpl final : public EngineBase {
 
   void truncate_now() override {
     auto t0 = Clock::now();
-    reduce();
-    do_truncate();
+    epilogue(/*do_truncate=*/true, /*check_budget=*/false);
+    sync_state();
     counters_.truncate_ns += ns_since(t0);
   }
 
-  uint64_t term_count() const override { return live_; }
-  double global_max() const override { return gmax_; }
+  uint64_t term_count() override {
+    sync_state();
+    return live_;
+  }
+  double global_max() override {
+    sync_state();
+    return gmax_;
+  }
 
   double expectation() override {
     // expectation_zero_state (sparse_operator.cpp:89-97): sum over strings
     // with no X/Y.  Summed on the host in ascending z order with Neumaier
     // compensation, so the value is deterministic.
+    sync_state();
     if (G_ == 0) return 0.0;
     diag_z_.ensure((size_t)G_ * W * 8);
     diag_c_.ensure((size_t)G_ * 8);
@@ -314,6 +332,7 @@ class EngineImpl final : public EngineBase {
   }
 
   double coefficient(const uint64_t* words) override {
+    sync_state();
     uint64_t x[2], z[2];
     words_to_planes(words, x, z);
     if (W == 1 && (x[1] | z[1])) return 0.0;
@@ -348,6 +367,7 @@ class EngineImpl final : public EngineBase {
   }
 
   uint64_t export_terms(uint64_t* words, double* c, uint64_t cap) override {
+    sync_state();
     if (live_ > cap) throw EngineError(PP_ERR_INVALID, "export capacity too small");
     compact();  // one contiguous live range in the current arena
     const uint64_t n = live_;
@@ -397,13 +417,17 @@ class EngineImpl final : public EngineBase {
     return order.size();
   }
 
+  void* stream() const override { return (void*)stream_; }
+
   pp_counters take_counters() override {
+    sync_state();
     pp_counters out = counters_;
     counters_ = pp_counters{};
     return out;
   }
 
   void take_kernel_stats(double* ms, double* bytes, uint64_t* launches, uint64_t* total) override {
+    sync_state();
     *ms = branch_ms_;
     *bytes = branch_bytes_;
     *launches = branch_launches_;
@@ -486,6 +510,7 @@ class EngineImpl final : public EngineBase {
 
   // ----- garbage collection: compact the current arena into the other one
   void gc_into_other(uint64_t new_cap) {
+    sync_state();
     const int o = 1 - cur_;
     ensure_arena(o, new_cap);
     reset_stats(0);
@@ -494,64 +519,87 @@ class EngineImpl final : public EngineBase {
       ++launches_;
     }
     fetch_stats();
-    bump_ = h_stats_->bump;
+    bump_ = bump_bound_ = h_stats_->bump;
     cur_ = o;
   }
   void compact() {
+    sync_state();
     uint64_t cap = std::max<uint64_t>(arena_[cur_].cap, live_ + 1);
     gc_into_other(cap);
   }
-  void ensure_space(uint64_t need) {
-    if (bump_ + need <= arena_[cur_].cap) return;
-    uint64_t target = (uint64_t)((live_ + need) * 1.5) + (1u << 16);
-    target = std::max<uint64_t>(target, arena_[cur_].cap);
+  // Room for one more X-type gate: the gate writes at most 2 * |O| strings.
+  // Uses the host's upper bounds first; synchronises (and compacts) only
+  // when the bound does not fit.
+  void ensure_branch_space() {
+    if (bump_bound_ + 2 * live_bound_ <= arena_[cur_].cap) return;
+    sync_state();
+    if (bump_ + 2 * live_ <= arena_[cur_].cap) return;
+    uint64_t target = std::max<uint64_t>((uint64_t)(live_ * 6) + (1u << 20), arena_[cur_].cap);
     gc_into_other(target);
-    if (bump_ + need > arena_[cur_].cap) throw EngineError(PP_ERR_INTERNAL, "arena sizing failed");
+    if (bump_ + 2 * live_ > arena_[cur_].cap) throw EngineError(PP_ERR_INTERNAL, "arena sizing failed");
   }
 
-  // ----- reductions / truncation
-  void reduce() {
-    reset_stats(bump_);
+  // ----- per-gate epilogue and host synchronisation
+  // Budget check, NaN check and truncation run on the device (k_truncate),
+  // so consecutive gates need no host round trip; the host synchronises only
+  // when it needs exact sizes (sync_state).
+  void epilogue(bool do_truncate, bool check_budget) {
+    k_gate_reset<<<1, 1, 0, stream_>>>(d_stats_);
     if (G_) {
       k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, d_stats_);
-      ++launches_;
+      k_truncate<W><<<std::min<uint32_t>(G_, persistent_grid()), kCta, 0, stream_>>>(
+          gview(gcur_), G_, aview(cur_), cfg_.epsilon0, do_truncate ? 1 : 0, check_budget ? cfg_.max_terms : 0,
+          gates_applied_, d_stats_);
+      launches_ += 2;
     }
-    fetch_stats();
-    live_ = h_stats_->live;
-    red_gmax_ = __builtin_bit_cast(double, h_stats_->gmax_bits);
-    red_gmin_ = __builtin_bit_cast(double, h_stats_->gmin_bits);
-    red_nonfinite_ = h_stats_->nonfinite;
-  }
-  void do_truncate() {
-    if (red_nonfinite_) {
-      throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient at layer " + std::to_string(layer_) +
-                                              ", gate " + std::to_string(gates_applied_) +
-                                              ", |O|=" + std::to_string(live_));
-    }
-    gmax_ = red_gmax_;
-    const double T = cfg_.epsilon0 * gmax_;  // engine.cpp:345
-    if (G_ && red_gmin_ <= T) {
-      reset_stats(bump_);
-      k_truncate<W><<<G_, kCta, 0, stream_>>>(gview(gcur_), aview(cur_), T, d_stats_);
-      ++launches_;
-      fetch_stats();
-      counters_.removed += h_stats_->removed;
-      live_ -= h_stats_->removed;
-    }
+    ++launches_;
+    if (do_truncate) truncated_since_sync_ = true;
+    dirty_ = true;
   }
   void post_gate() {
     ++gates_applied_;
     ++counters_.gates;
-    auto t0 = Clock::now();
-    reduce();
-    if (cfg_.max_terms && live_ > cfg_.max_terms) {  // check_budget, engine.cpp:266-275
-      throw EngineError(PP_ERR_RESOURCE, "term budget exhausted: |O|=" + std::to_string(live_) +
-                                             " exceeds max_terms=" + std::to_string(cfg_.max_terms) +
-                                             " at gate " + std::to_string(gates_applied_));
-    }
-    if (cfg_.cadence == PP_CADENCE_GATE) do_truncate();
-    counters_.truncate_ns += ns_since(t0);
+    epilogue(cfg_.cadence == PP_CADENCE_GATE, true);
   }
+  void sync_state() {
+    if (!dirty_) return;
+    k_gate_reset<<<1, 1, 0, stream_>>>(d_stats_);
+    if (G_) k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, d_stats_);
+    launches_ += 2;
+    fetch_stats();
+    PP_CUDA(cudaGetLastError());
+    const DevStats& st = *h_stats_;
+    counters_.records_sent += st.records;
+    counters_.removed += st.removed;
+    if (st.err_budget) {
+      dirty_ = false;
+      throw EngineError(PP_ERR_RESOURCE, "term budget exhausted: |O|=" + std::to_string(st.err_live) +
+                                             " exceeds max_terms=" + std::to_string(cfg_.max_terms) + " at gate " +
+                                             std::to_string(st.err_gate + 1));
+    }
+    if (st.err_numerical) {
+      dirty_ = false;
+      throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient at gate " + std::to_string(st.err_gate + 1) +
+                                              ", |O|=" + std::to_string(st.err_live));
+    }
+    live_ = live_bound_ = st.live;
+    bump_ = bump_bound_ = st.bump;
+    if (truncated_since_sync_) gmax_ = __builtin_bit_cast(double, st.last_gmax_bits);
+    truncated_since_sync_ = false;
+    // harvest branch-kernel timings
+    for (auto& pr : pending_events_) {
+      float ms = 0.f;
+      PP_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      branch_ms_ += ms;
+      free_events_.push_back(pr);
+    }
+    pending_events_.clear();
+    branch_bytes_ += (double)(st.aff_total + st.out_elems) * R;
+    k_clear_cumulative<<<1, 1, 0, stream_>>>(d_stats_);
+    ++launches_;
+    dirty_ = false;
+  }
+  uint32_t persistent_grid() const { return 148u * 8u; }
 
   // ----- one gate
   void apply_one(const pp_gate& gate) {
@@ -577,7 +625,7 @@ class EngineImpl final : public EngineBase {
       counters_.records_sent += h_records_;
     }
     counters_.branch_ns += ns_since(t0);
-    if (h_records_) counters_.batches_sent += 1;
+    counters_.batches_sent += 1;
     h_records_ = 0;
     post_gate();
   }
@@ -595,31 +643,32 @@ class EngineImpl final : public EngineBase {
       }
     }
     ensure_list(G_);
-    reset_stats(bump_);
+    ensure_branch_space();
+    k_gate_reset<<<1, 1, 0, stream_>>>(d_stats_);
     k_select_x<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, px, list_.as<uint32_t>(), d_stats_);
-    ++launches_;
-    fetch_stats();
-    const uint32_t n_aff = h_stats_->n_aff;
-    const uint64_t aff = h_stats_->aff_elems;
-    if (n_aff == 0) return;
-    ensure_space(2 * aff);
-    reset_stats(bump_);
-    PP_CUDA(cudaEventRecord(ev0_, stream_));
-    k_branch_x<W><<<n_aff, kCta, sizeof(BranchSmem<W>), stream_>>>(gview(gcur_), aview(cur_), list_.as<uint32_t>(),
-                                                                    wq, mq, cosv, sinv, keep_zeros_, d_stats_);
-    PP_CUDA(cudaEventRecord(ev1_, stream_));
-    ++launches_;
+    std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
+    PP_CUDA(cudaEventRecord(ev.first, stream_));
+    k_branch_x<W><<<std::min<uint32_t>(G_, branch_grid_), kCta, sizeof(BranchSmem<W>), stream_>>>(
+        gview(gcur_), aview(cur_), list_.as<uint32_t>(), wq, mq, cosv, sinv, keep_zeros_, d_stats_);
+    PP_CUDA(cudaEventRecord(ev.second, stream_));
+    pending_events_.push_back(ev);
+    launches_ += 3;
     ++branch_launches_;
-    fetch_stats();
-    PP_CUDA(cudaGetLastError());
-    float ms = 0.f;
-    PP_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
-    branch_ms_ += ms;
-    branch_bytes_ += (double)(aff + h_stats_->out_elems) * R;
-    bump_ = h_stats_->bump;
-    h_records_ = h_stats_->records;
-    counters_.records_sent += h_stats_->records;
-    counters_.removed += h_stats_->removed;
+    bump_bound_ += 2 * live_bound_;
+    live_bound_ *= 2;
+    dirty_ = true;
+  }
+
+  std::pair<cudaEvent_t, cudaEvent_t> take_event_pair() {
+    if (!free_events_.empty()) {
+      auto e = free_events_.back();
+      free_events_.pop_back();
+      return e;
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    PP_CUDA(cudaEventCreate(&e.first));
+    PP_CUDA(cudaEventCreate(&e.second));
+    return e;
   }
 
   void ensure_list(uint32_t n) { list_.ensure((size_t)std::max<uint32_t>(n, 1) * 4); }
@@ -658,8 +707,7 @@ class EngineImpl final : public EngineBase {
     gates_applied_ += count;
     counters_.gates += count;
     auto t1 = Clock::now();
-    reduce();
-    if (cfg_.cadence == PP_CADENCE_GATE) do_truncate();
+    epilogue(cfg_.cadence == PP_CADENCE_GATE, false);
     counters_.truncate_ns += ns_since(t1);
   }
 
@@ -667,6 +715,7 @@ class EngineImpl final : public EngineBase {
   template <class P>
   void regroup(const P& prod) {
     const int maxrec = P::kMaxRec;
+    sync_state();
     const uint64_t live = live_;
     if (G_ == 0 || live == 0) return;
     const uint64_t max_items = (uint64_t)G_ + live / kItem + 1;
@@ -746,7 +795,9 @@ class EngineImpl final : public EngineBase {
       cur_ = o;
       gcur_ = 1 - gcur_;
       G_ = distinct;
-      bump_ = total;
+      bump_ = bump_bound_ = total;
+      live_ = live_bound_ = total - h_stats_->removed;
+      reset_stats(bump_);  // cumulative counters were harvested above
       return;
     }
   }
@@ -787,6 +838,10 @@ class EngineImpl final : public EngineBase {
   double gmax_ = 0.0, red_gmax_ = 0.0, red_gmin_ = 0.0;
   uint32_t red_nonfinite_ = 0;
   int keep_zeros_ = 0;
+  uint64_t bump_bound_ = 0, live_bound_ = 0;
+  bool dirty_ = false, truncated_since_sync_ = false;
+  uint32_t branch_grid_ = 148u * 2u;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_events_, free_events_;
   unsigned long long seed_;
   unsigned long long h_records_ = 0;
   pp_counters counters_{};
@@ -888,14 +943,12 @@ int pp_truncate_now(pp_engine* e) {
 
 int pp_term_count(const pp_engine* e, uint64_t* out) {
   if (!e || !out) return PP_ERR_INVALID;
-  *out = e->impl->term_count();
-  return PP_OK;
+  return guarded(const_cast<pp_engine*>(e), [&] { *out = e->impl->term_count(); });
 }
 
 int pp_global_max(const pp_engine* e, double* out) {
   if (!e || !out) return PP_ERR_INVALID;
-  *out = e->impl->global_max();
-  return PP_OK;
+  return guarded(const_cast<pp_engine*>(e), [&] { *out = e->impl->global_max(); });
 }
 
 int pp_expectation_zero_state(pp_engine* e, double* out) {
@@ -925,6 +978,8 @@ int pp_take_kernel_stats(pp_engine* e, double* branch_ms, double* branch_bytes, 
   e->impl->take_kernel_stats(branch_ms, branch_bytes, branch_launches, total_launches);
   return PP_OK;
 }
+
+void* pp_stream(const pp_engine* e) { return e ? e->impl->stream() : nullptr; }
 
 const char* pp_last_error(const pp_engine* e) { return e ? e->error.c_str() : g_create_error.c_str(); }
 

@@ -56,8 +56,28 @@ struct DevStats {
   unsigned int overflow;
   unsigned int collision;
   unsigned int distinct;
+  unsigned int err_budget;         // sticky: term budget exceeded (check_budget)
+  unsigned int err_numerical;      // sticky: NaN/Inf seen by a truncation
   unsigned int pad;
+  unsigned long long err_gate;     // gate index of the first error
+  unsigned long long err_live;     // |O| at the first error
+  unsigned long long last_gmax_bits;  // gmax used by the latest truncation
+  unsigned long long aff_total;    // cumulative strings in affected groups
 };
+
+// Reset of the per-gate fields (cumulative counters and sticky errors stay).
+__global__ void k_gate_reset(DevStats* st) {
+  st->live = 0;
+  st->gmax_bits = 0;
+  st->gmin_bits = 0x7ff0000000000000ull;
+  st->aff_elems = 0;
+  st->n_aff = 0;
+  st->nonfinite = 0;
+}
+
+__device__ __forceinline__ bool engine_failed(const DevStats* st) {
+  return (*(volatile const unsigned int*)&st->err_budget) | (*(volatile const unsigned int*)&st->err_numerical);
+}
 
 template <int W>
 __device__ __forceinline__ Plane<W> load_plane(uint64_t* const (&p)[W], uint64_t i) {
@@ -117,6 +137,7 @@ __device__ __forceinline__ uint32_t sk_upper_bound(const uint64_t* base, uint32_
 // ---------------------------------------------------------------------------
 template <int W>
 __global__ void k_select_x(GroupView<W> g, uint32_t G, Plane<W> jx, uint32_t* list, DevStats* st) {
+  if (engine_failed(st)) return;
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   bool take = false;
   uint32_t c = 0;
@@ -132,6 +153,7 @@ __global__ void k_select_x(GroupView<W> g, uint32_t G, Plane<W> jx, uint32_t* li
   if (lane == 0) {
     base = atomicAdd(&st->n_aff, __popc(mask));
     atomicAdd(&st->aff_elems, sum);
+    atomicAdd(&st->aff_total, sum);
   }
   base = __shfl_sync(0xffffffffu, base, 0);
   if (take) list[base + __popc(mask & ((1u << lane) - 1))] = i;
@@ -183,10 +205,16 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   const uint32_t tid = threadIdx.x;
-  const uint32_t gid = list[blockIdx.x];
+  const uint32_t n_aff = *(volatile uint32_t*)&st->n_aff;
+  for (uint32_t li = blockIdx.x; li < n_aff; li += gridDim.x) {
+  __syncthreads();
+  const uint32_t gid = list[li];
   const uint32_t n = g.cnt[gid];
   const uint64_t src = g.off[gid];
   __shared__ unsigned long long dst_s;
+  __shared__ double red_max[kWarps], red_min[kWarps];
+  __shared__ unsigned long long red_rec[kWarps], red_rem[kWarps];
+  __shared__ uint32_t red_nf[kWarps];
   if (tid == 0) {
     dst_s = atomicAdd(&st->bump, 2ull * n);
     sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0;
@@ -362,9 +390,6 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   records = warp_sum64(records);
   removed = warp_sum64(removed);
   nonfinite = __any_sync(0xffffffffu, nonfinite);
-  __shared__ double red_max[kWarps], red_min[kWarps];
-  __shared__ unsigned long long red_rec[kWarps], red_rem[kWarps];
-  __shared__ uint32_t red_nf[kWarps];
   const uint32_t lane = tid & 31, warp = tid >> 5;
   if (lane == 0) {
     red_max[warp] = vmax;
@@ -392,6 +417,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
     atomicAdd(&st->removed, removed);
     atomicAdd(&st->out_elems, (unsigned long long)out_n);
   }
+  }  // groups of this CTA
 }
 
 // ---------------------------------------------------------------------------
@@ -431,12 +457,10 @@ __global__ void k_reduce(GroupView<W> g, uint32_t G, DevStats* st) {
 // and -0.0 always go).  In-place streaming compaction, one CTA per group.
 // ---------------------------------------------------------------------------
 template <int W>
-__global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, ArenaView<W> ar, double T, DevStats* st) {
-  const uint32_t gid = blockIdx.x;
+__device__ void truncate_group(GroupView<W> g, ArenaView<W> ar, uint32_t gid, double T, DevStats* st,
+                               uint32_t* scan, double* rmx, double* rmn) {
   const uint32_t n = g.cnt[gid];
-  if (n == 0 || !(g.gmin[gid] <= T)) return;
   const uint64_t off = g.off[gid];
-  __shared__ uint32_t scan[40];
   const uint32_t tid = threadIdx.x;
   uint32_t w = 0;
   double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);
@@ -463,7 +487,6 @@ __global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, ArenaView<W> 
   }
   vmax = warp_max(vmax);
   vmin = warp_min(vmin);
-  __shared__ double rmx[kWarps], rmn[kWarps];
   if ((tid & 31) == 0) {
     rmx[tid >> 5] = vmax;
     rmn[tid >> 5] = vmin;
@@ -478,6 +501,47 @@ __global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, ArenaView<W> 
     g.gmax[gid] = w ? vmax : 0.0;
     g.gmin[gid] = w ? vmin : __longlong_as_double(0x7ff0000000000000ll);
     atomicAdd(&st->removed, (unsigned long long)(n - w));
+  }
+  __syncthreads();
+}
+
+// Per-gate epilogue (Engine::apply_gate tail, engine.cpp:309-315 and
+// truncate_now, engine.cpp:318-351), device-side so no host round trip:
+//   budget check on |O| after the apply -> sticky err_budget
+//   [truncate] NaN/Inf -> sticky err_numerical; T = epsilon0 * gmax;
+//              remove |c| <= T in every group whose min |c| <= T.
+// Persistent grid-stride over groups.
+template <int W>
+__global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, uint32_t G, ArenaView<W> ar, double epsilon0,
+                                                   int do_truncate, unsigned long long max_terms,
+                                                   unsigned long long gate_index, DevStats* st) {
+  if (engine_failed(st)) return;
+  const unsigned long long live = *(volatile unsigned long long*)&st->live;
+  if (max_terms && live > max_terms) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && atomicCAS(&st->err_budget, 0u, 1u) == 0u) {
+      st->err_gate = gate_index;
+      st->err_live = live;
+    }
+    return;
+  }
+  if (!do_truncate) return;
+  if (*(volatile unsigned int*)&st->nonfinite) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && atomicCAS(&st->err_numerical, 0u, 1u) == 0u) {
+      st->err_gate = gate_index;
+      st->err_live = live;
+    }
+    return;
+  }
+  const double gmax = __longlong_as_double(*(volatile long long*)&st->gmax_bits);
+  const double gmin = __longlong_as_double(*(volatile long long*)&st->gmin_bits);
+  const double T = epsilon0 * gmax;  // engine.cpp:345, one IEEE product
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->last_gmax_bits = (unsigned long long)__double_as_longlong(gmax);
+  if (!(gmin <= T)) return;
+  __shared__ uint32_t scan[40];
+  __shared__ double rmx[kWarps], rmn[kWarps];
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+    if (g.cnt[gid] == 0 || !(g.gmin[gid] <= T)) continue;  // uniform per CTA
+    truncate_group<W>(g, ar, gid, T, st, scan, rmx, rmn);
   }
 }
 
