@@ -14,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -56,7 +57,7 @@ __global__ void k_reset_stats(DevStats* st, unsigned long long bump) {
   DevStats s;
   memset(&s, 0, sizeof(s));
   s.bump = bump;
-  s.gmin_bits = 0x7ff0000000000000ull;
+  for (int i = 0; i < 3; ++i) s.red[i].gmin_bits = 0x7ff0000000000000ull;
   *st = s;
 }
 
@@ -103,22 +104,77 @@ static inline bool is_clifford(const pp_gate& g) {
 }
 
 // ---------------------------------------------------------------------------
-// device buffer helper
+// device memory: a process-wide caching pool so that creating engines (one
+// per simulate() call, like the reference) does not pay cudaMalloc/cudaFree
+// every time.  Blocks are reused when they fit within 25 % slack.
 // ---------------------------------------------------------------------------
+class DevicePool {
+ public:
+  static DevicePool& get() {
+    static DevicePool p;
+    return p;
+  }
+  void* acquire(size_t bytes, size_t* got) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    bytes = (bytes + kGrain - 1) / kGrain * kGrain;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      auto& fl = free_[dev];
+      auto it = fl.lower_bound(bytes);
+      if (it != fl.end() && it->first <= bytes + bytes / 4) {
+        void* p = it->second;
+        *got = it->first;
+        fl.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      trim(dev);
+      e = cudaMalloc(&p, bytes);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      if (e == cudaErrorMemoryAllocation) throw EngineError(PP_ERR_RESOURCE, "device memory exhausted");
+      throw EngineError(PP_ERR_INTERNAL, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    *got = bytes;
+    return p;
+  }
+  void release(void* p, size_t bytes) {
+    if (!p) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu_);
+    free_[dev].emplace(bytes, p);
+  }
+  void trim(int dev) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto& [b, p] : free_[dev]) cudaFree(p);
+    free_[dev].clear();
+  }
+
+ private:
+  static constexpr size_t kGrain = 1u << 20;
+  std::mutex mu_;
+  std::map<int, std::multimap<size_t, void*>> free_;
+};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   void release() {
-    if (p) cudaFree(p);
+    if (p) DevicePool::get().release(p, bytes);
     p = nullptr;
     bytes = 0;
   }
   void ensure(size_t b) {
     if (b <= bytes) return;
     release();
-    size_t nb = std::max<size_t>(b, 256);
-    PP_CUDA(cudaMalloc(&p, nb));
-    bytes = nb;
+    p = DevicePool::get().acquire(std::max<size_t>(b, 256), &bytes);
   }
   template <class T>
   T* as() const {
@@ -126,6 +182,27 @@ struct DevBuf {
   }
   ~DevBuf() { release(); }
 };
+
+// pinned host mirrors of DevStats, recycled across engines
+static std::mutex g_pinned_mu;
+static std::vector<DevStats*> g_pinned_free;
+static DevStats* pinned_stats() {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      DevStats* p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  DevStats* p = nullptr;
+  PP_CUDA(cudaMallocHost(&p, sizeof(DevStats)));
+  return p;
+}
+static void release_pinned_stats(DevStats* p) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
 
 class EngineBase {
  public:
@@ -149,8 +226,9 @@ class EngineImpl final : public EngineBase {
   explicit EngineImpl(const pp_config& cfg) : cfg_(cfg) {
     PP_CUDA(cudaSetDevice(cfg.device));
     PP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    PP_CUDA(cudaMalloc(&d_stats_, sizeof(DevStats)));
-    PP_CUDA(cudaMallocHost(&h_stats_, sizeof(DevStats)));
+    stats_buf_.ensure(sizeof(DevStats));
+    d_stats_ = stats_buf_.as<DevStats>();
+    h_stats_ = pinned_stats();
     PP_CUDA(cudaEventCreate(&ev0_));
     PP_CUDA(cudaEventCreate(&ev1_));
     PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -166,8 +244,7 @@ class EngineImpl final : public EngineBase {
     cudaStreamSynchronize(stream_);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
-    cudaFree(d_stats_);
-    cudaFreeHost(h_stats_);
+    release_pinned_stats(h_stats_);
     cudaStreamDestroy(stream_);
   }
 
@@ -198,6 +275,7 @@ class EngineImpl final : public EngineBase {
     std::vector<uint32_t> gfl;
     uint64_t i = 0;
     double gmax = 0.0;
+    bool has_zero = false;
     K prev{};
     bool first = true;
     for (auto& [k, v] : terms) {
@@ -220,6 +298,7 @@ class EngineImpl final : public EngineBase {
       gmx.back() = std::max(gmx.back(), av);
       gmn.back() = std::min(gmn.back(), av);
       if (!std::isfinite(v)) gfl.back() = 1;
+      if (v == 0.0) has_zero = true;
       gmax = std::max(gmax, av);  // global_max_abs (sparse_operator.cpp:130-134)
       ++i;
     }
@@ -256,6 +335,9 @@ class EngineImpl final : public EngineBase {
     live_ = live_bound_ = n;
     dirty_ = false;
     truncated_since_sync_ = false;
+    gmax_stale_ = false;
+    may_hold_zeros_ = has_zero || keep_zeros_;
+    eseq_ = bseq_ = 0;
     gmax_ = gmax;
     counters_ = pp_counters{};
     gates_applied_ = 0;
@@ -263,6 +345,10 @@ class EngineImpl final : public EngineBase {
 
   // ---------------------------------------------------------------- gates
   void apply_gates(const pp_gate* gates, size_t count) override {
+    apply_gates_async(gates, count);
+    sync_state();  // errors surface at the call, as Engine::apply_gate throws
+  }
+  void apply_gates_async(const pp_gate* gates, size_t count) {
     size_t i = 0;
     while (i < count) {
       if (fusion_allowed() && is_clifford(gates[i])) {
@@ -544,15 +630,27 @@ class EngineImpl final : public EngineBase {
   // so consecutive gates need no host round trip; the host synchronises only
   // when it needs exact sizes (sync_state).
   void epilogue(bool do_truncate, bool check_budget) {
-    k_gate_reset<<<1, 1, 0, stream_>>>(d_stats_);
-    if (G_) {
-      k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, d_stats_);
-      k_truncate<W><<<std::min<uint32_t>(G_, persistent_grid()), kCta, 0, stream_>>>(
-          gview(gcur_), G_, aview(cur_), cfg_.epsilon0, do_truncate ? 1 : 0, check_budget ? cfg_.max_terms : 0,
-          gates_applied_, d_stats_);
-      launches_ += 2;
+    const bool budget = check_budget && cfg_.max_terms;
+    // With epsilon0 == 0 the threshold is 0: only exact zeros go, and the
+    // branch/regroup kernels never emit zeros (cadence gate), so unless the
+    // store may hold zeros (set_initial) or a budget must be checked the
+    // epilogue is a no-op; NaN/Inf is then caught at the next sync.
+    if (cfg_.epsilon0 == 0.0 && !budget && !may_hold_zeros_) {
+      if (do_truncate) gmax_stale_ = true;
+      dirty_ = true;
+      return;
     }
-    ++launches_;
+    RedSlot* r = &d_stats_->red[eseq_ & 1];
+    RedSlot* rn = &d_stats_->red[(eseq_ + 1) & 1];
+    ++eseq_;
+    if (G_) {
+      k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, r);
+      k_truncate<W><<<std::min<uint32_t>(G_, persistent_grid()), kCta, 0, stream_>>>(
+          gview(gcur_), G_, aview(cur_), cfg_.epsilon0, do_truncate ? 1 : 0, budget ? cfg_.max_terms : 0,
+          gates_applied_, r, rn, d_stats_);
+      launches_ += 2;
+      if (do_truncate) may_hold_zeros_ = false;
+    }
     if (do_truncate) truncated_since_sync_ = true;
     dirty_ = true;
   }
@@ -563,8 +661,8 @@ class EngineImpl final : public EngineBase {
   }
   void sync_state() {
     if (!dirty_) return;
-    k_gate_reset<<<1, 1, 0, stream_>>>(d_stats_);
-    if (G_) k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, d_stats_);
+    k_red_reset<<<1, 1, 0, stream_>>>(&d_stats_->red[2]);
+    if (G_) k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, &d_stats_->red[2]);
     launches_ += 2;
     fetch_stats();
     PP_CUDA(cudaGetLastError());
@@ -582,10 +680,19 @@ class EngineImpl final : public EngineBase {
       throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient at gate " + std::to_string(st.err_gate + 1) +
                                               ", |O|=" + std::to_string(st.err_live));
     }
-    live_ = live_bound_ = st.live;
+    if (st.red[2].nonfinite && gmax_stale_) {
+      dirty_ = false;
+      throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient detected at gate " + std::to_string(gates_applied_) +
+                                              ", |O|=" + std::to_string(st.red[2].live));
+    }
+    live_ = live_bound_ = st.red[2].live;
     bump_ = bump_bound_ = st.bump;
     if (truncated_since_sync_) gmax_ = __builtin_bit_cast(double, st.last_gmax_bits);
+    // epsilon0 == 0 fast path: the skipped truncations would have used the
+    // max after the last gate, which survives its own truncation
+    if (gmax_stale_) gmax_ = __builtin_bit_cast(double, st.red[2].gmax_bits);
     truncated_since_sync_ = false;
+    gmax_stale_ = false;
     // harvest branch-kernel timings
     for (auto& pr : pending_events_) {
       float ms = 0.f;
@@ -644,18 +751,21 @@ class EngineImpl final : public EngineBase {
     }
     ensure_list(G_);
     ensure_branch_space();
-    k_gate_reset<<<1, 1, 0, stream_>>>(d_stats_);
-    k_select_x<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, px, list_.as<uint32_t>(), d_stats_);
+    SelSlot* sel = &d_stats_->sel[bseq_ & 1];
+    SelSlot* sel_next = &d_stats_->sel[(bseq_ + 1) & 1];
+    ++bseq_;
+    k_select_x<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, px, list_.as<uint32_t>(), sel, d_stats_);
     std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
     PP_CUDA(cudaEventRecord(ev.first, stream_));
     k_branch_x<W><<<std::min<uint32_t>(G_, branch_grid_), kCta, sizeof(BranchSmem<W>), stream_>>>(
-        gview(gcur_), aview(cur_), list_.as<uint32_t>(), wq, mq, cosv, sinv, keep_zeros_, d_stats_);
+        gview(gcur_), aview(cur_), list_.as<uint32_t>(), wq, mq, cosv, sinv, keep_zeros_, sel, sel_next, d_stats_);
     PP_CUDA(cudaEventRecord(ev.second, stream_));
     pending_events_.push_back(ev);
-    launches_ += 3;
+    launches_ += 2;
     ++branch_launches_;
     bump_bound_ += 2 * live_bound_;
     live_bound_ *= 2;
+    if (keep_zeros_) may_hold_zeros_ = true;
     dirty_ = true;
   }
 
@@ -798,6 +908,7 @@ class EngineImpl final : public EngineBase {
       bump_ = bump_bound_ = total;
       live_ = live_bound_ = total - h_stats_->removed;
       reset_stats(bump_);  // cumulative counters were harvested above
+      if (keep_zeros_) may_hold_zeros_ = true;
       return;
     }
   }
@@ -831,7 +942,7 @@ class EngineImpl final : public EngineBase {
   cudaEvent_t ev0_, ev1_;
   Arena arena_[2];
   Groups groups_[2];
-  DevBuf list_, items_, rec_slot_, table_, scan_tmp_, scan_gid_, scan_off_, diag_z_, diag_c_, cliff_;
+  DevBuf stats_buf_, list_, items_, rec_slot_, table_, scan_tmp_, scan_gid_, scan_off_, diag_z_, diag_c_, cliff_;
   int cur_ = 0, gcur_ = 0;
   uint32_t G_ = 0;
   uint64_t bump_ = 0, live_ = 0;
@@ -839,7 +950,8 @@ class EngineImpl final : public EngineBase {
   uint32_t red_nonfinite_ = 0;
   int keep_zeros_ = 0;
   uint64_t bump_bound_ = 0, live_bound_ = 0;
-  bool dirty_ = false, truncated_since_sync_ = false;
+  bool dirty_ = false, truncated_since_sync_ = false, gmax_stale_ = false, may_hold_zeros_ = false;
+  uint64_t eseq_ = 0, bseq_ = 0;
   uint32_t branch_grid_ = 148u * 2u;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_events_, free_events_;
   unsigned long long seed_;

@@ -38,21 +38,40 @@ struct GroupView {
   uint32_t* flags;  // bit0: non-finite coefficient present
 };
 
+// Per-gate scratch lives in small slot arrays so consecutive gates need no
+// reset launches: a gate's kernels use slot s and clear slot s^1 for the
+// next gate.
+struct RedSlot {            // group reduction of one epilogue
+  unsigned long long live;
+  unsigned long long gmax_bits;
+  unsigned long long gmin_bits;
+  unsigned int nonfinite;
+  unsigned int pad;
+};
+struct SelSlot {            // affected-group selection of one X-type gate
+  unsigned long long aff_elems;
+  unsigned int n_aff;
+  unsigned int pad;
+};
+
+__device__ __forceinline__ void clear_red(RedSlot* r) {
+  r->live = 0;
+  r->gmax_bits = 0;
+  r->gmin_bits = 0x7ff0000000000000ull;
+  r->nonfinite = 0;
+}
+
 struct DevStats {
+  RedSlot red[3];                  // [0,1]: per-gate epilogues, [2]: host syncs
+  SelSlot sel[2];
   unsigned long long bump;         // bump pointer of the target arena
-  unsigned long long live;         // sum of group counts
   unsigned long long records;      // nonzero sin-branch records (records_sent)
   unsigned long long removed;      // stored strings dropped (zero or truncated)
-  unsigned long long gmax_bits;    // max |c| as bits
-  unsigned long long gmin_bits;    // min over groups of their min |c|
-  unsigned long long aff_elems;    // strings in affected groups
   unsigned long long items;        // regroup work items
   unsigned long long rec_total;    // regroup record slots reserved
   unsigned long long scratch_bump; // scratch allocation for big sorts
   unsigned long long diag_count;   // diagonal strings found
   unsigned long long out_elems;    // strings written by branch kernels
-  unsigned int nonfinite;
-  unsigned int n_aff;
   unsigned int overflow;
   unsigned int collision;
   unsigned int distinct;
@@ -65,15 +84,8 @@ struct DevStats {
   unsigned long long aff_total;    // cumulative strings in affected groups
 };
 
-// Reset of the per-gate fields (cumulative counters and sticky errors stay).
-__global__ void k_gate_reset(DevStats* st) {
-  st->live = 0;
-  st->gmax_bits = 0;
-  st->gmin_bits = 0x7ff0000000000000ull;
-  st->aff_elems = 0;
-  st->n_aff = 0;
-  st->nonfinite = 0;
-}
+// Reset of one reduction slot (cumulative counters and sticky errors stay).
+__global__ void k_red_reset(RedSlot* r) { clear_red(r); }
 
 __device__ __forceinline__ bool engine_failed(const DevStats* st) {
   return (*(volatile const unsigned int*)&st->err_budget) | (*(volatile const unsigned int*)&st->err_numerical);
@@ -136,7 +148,7 @@ __device__ __forceinline__ uint32_t sk_upper_bound(const uint64_t* base, uint32_
 // group selection for an X-type gate
 // ---------------------------------------------------------------------------
 template <int W>
-__global__ void k_select_x(GroupView<W> g, uint32_t G, Plane<W> jx, uint32_t* list, DevStats* st) {
+__global__ void k_select_x(GroupView<W> g, uint32_t G, Plane<W> jx, uint32_t* list, SelSlot* sel, DevStats* st) {
   if (engine_failed(st)) return;
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   bool take = false;
@@ -151,8 +163,8 @@ __global__ void k_select_x(GroupView<W> g, uint32_t G, Plane<W> jx, uint32_t* li
   uint32_t base = 0;
   unsigned long long sum = warp_sum64(take ? c : 0);
   if (lane == 0) {
-    base = atomicAdd(&st->n_aff, __popc(mask));
-    atomicAdd(&st->aff_elems, sum);
+    base = atomicAdd(&sel->n_aff, __popc(mask));
+    atomicAdd(&sel->aff_elems, sum);
     atomicAdd(&st->aff_total, sum);
   }
   base = __shfl_sync(0xffffffffu, base, 0);
@@ -201,11 +213,16 @@ struct BranchSmem {
 template <int W>
 __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> ar, const uint32_t* list,
                                                     int wq, uint64_t mq, double cosv, double sinv,
-                                                    int keep_zeros, DevStats* st) {
+                                                    int keep_zeros, SelSlot* sel, SelSlot* sel_next,
+                                                    DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   const uint32_t tid = threadIdx.x;
-  const uint32_t n_aff = *(volatile uint32_t*)&st->n_aff;
+  const uint32_t n_aff = *(volatile uint32_t*)&sel->n_aff;
+  if (blockIdx.x == 0 && tid == 0) {
+    sel_next->n_aff = 0;
+    sel_next->aff_elems = 0;
+  }
   for (uint32_t li = blockIdx.x; li < n_aff; li += gridDim.x) {
   __syncthreads();
   const uint32_t gid = list[li];
@@ -425,7 +442,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
 // (truncate_now's first pass, engine.cpp:321-343, at group granularity)
 // ---------------------------------------------------------------------------
 template <int W>
-__global__ void k_reduce(GroupView<W> g, uint32_t G, DevStats* st) {
+__global__ void k_reduce(GroupView<W> g, uint32_t G, RedSlot* out) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long live = 0;
   double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
@@ -444,10 +461,10 @@ __global__ void k_reduce(GroupView<W> g, uint32_t G, DevStats* st) {
   mn = warp_min(mn);
   nf = __any_sync(0xffffffffu, nf);
   if ((threadIdx.x & 31) == 0) {
-    if (live) atomicAdd(&st->live, live);
-    atomic_max_nonneg(reinterpret_cast<double*>(&st->gmax_bits), mx);
-    atomic_min_nonneg(reinterpret_cast<double*>(&st->gmin_bits), mn);
-    if (nf) atomicOr(&st->nonfinite, 1u);
+    if (live) atomicAdd(&out->live, live);
+    atomic_max_nonneg(reinterpret_cast<double*>(&out->gmax_bits), mx);
+    atomic_min_nonneg(reinterpret_cast<double*>(&out->gmin_bits), mn);
+    if (nf) atomicOr(&out->nonfinite, 1u);
   }
 }
 
@@ -514,9 +531,11 @@ __device__ void truncate_group(GroupView<W> g, ArenaView<W> ar, uint32_t gid, do
 template <int W>
 __global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, uint32_t G, ArenaView<W> ar, double epsilon0,
                                                    int do_truncate, unsigned long long max_terms,
-                                                   unsigned long long gate_index, DevStats* st) {
+                                                   unsigned long long gate_index, RedSlot* red, RedSlot* red_next,
+                                                   DevStats* st) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) clear_red(red_next);
   if (engine_failed(st)) return;
-  const unsigned long long live = *(volatile unsigned long long*)&st->live;
+  const unsigned long long live = *(volatile unsigned long long*)&red->live;
   if (max_terms && live > max_terms) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && atomicCAS(&st->err_budget, 0u, 1u) == 0u) {
       st->err_gate = gate_index;
@@ -525,15 +544,15 @@ __global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, uint32_t G, A
     return;
   }
   if (!do_truncate) return;
-  if (*(volatile unsigned int*)&st->nonfinite) {
+  if (*(volatile unsigned int*)&red->nonfinite) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && atomicCAS(&st->err_numerical, 0u, 1u) == 0u) {
       st->err_gate = gate_index;
       st->err_live = live;
     }
     return;
   }
-  const double gmax = __longlong_as_double(*(volatile long long*)&st->gmax_bits);
-  const double gmin = __longlong_as_double(*(volatile long long*)&st->gmin_bits);
+  const double gmax = __longlong_as_double(*(volatile long long*)&red->gmax_bits);
+  const double gmin = __longlong_as_double(*(volatile long long*)&red->gmin_bits);
   const double T = epsilon0 * gmax;  // engine.cpp:345, one IEEE product
   if (blockIdx.x == 0 && threadIdx.x == 0) st->last_gmax_bits = (unsigned long long)__double_as_longlong(gmax);
   if (!(gmin <= T)) return;
