@@ -749,19 +749,14 @@ class EngineImpl final : public EngineBase {
         mq = jx[k];
       }
     }
-    ensure_list(G_);
     ensure_branch_space();
-    SelSlot* sel = &d_stats_->sel[bseq_ & 1];
-    SelSlot* sel_next = &d_stats_->sel[(bseq_ + 1) & 1];
-    ++bseq_;
-    k_select_x<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, px, list_.as<uint32_t>(), sel, d_stats_);
     std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
     PP_CUDA(cudaEventRecord(ev.first, stream_));
     k_branch_x<W><<<std::min<uint32_t>(G_, branch_grid_), kCta, sizeof(BranchSmem<W>), stream_>>>(
-        gview(gcur_), aview(cur_), list_.as<uint32_t>(), wq, mq, cosv, sinv, keep_zeros_, sel, sel_next, d_stats_);
+        gview(gcur_), G_, aview(cur_), wq, mq, cosv, sinv, keep_zeros_, d_stats_);
     PP_CUDA(cudaEventRecord(ev.second, stream_));
     pending_events_.push_back(ev);
-    launches_ += 2;
+    launches_ += 1;
     ++branch_launches_;
     bump_bound_ += 2 * live_bound_;
     live_bound_ *= 2;

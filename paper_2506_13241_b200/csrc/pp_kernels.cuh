@@ -210,23 +210,23 @@ struct BranchSmem {
   uint32_t all_done;
 };
 
+// Persistent: CTA b visits groups b, b + gridDim.x, ... and branches those
+// the gate touches (z_q = 1), so selection costs no separate launch.
 template <int W>
-__global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> ar, const uint32_t* list,
+__global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, ArenaView<W> ar,
                                                     int wq, uint64_t mq, double cosv, double sinv,
-                                                    int keep_zeros, SelSlot* sel, SelSlot* sel_next,
-                                                    DevStats* st) {
+                                                    int keep_zeros, DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   const uint32_t tid = threadIdx.x;
-  const uint32_t n_aff = *(volatile uint32_t*)&sel->n_aff;
-  if (blockIdx.x == 0 && tid == 0) {
-    sel_next->n_aff = 0;
-    sel_next->aff_elems = 0;
-  }
-  for (uint32_t li = blockIdx.x; li < n_aff; li += gridDim.x) {
-  __syncthreads();
-  const uint32_t gid = list[li];
+  if (engine_failed(st)) return;
+  unsigned long long aff_elems = 0;
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+  if (!(g.z[wq][gid] & mq)) continue;  // uniform per CTA
   const uint32_t n = g.cnt[gid];
+  if (n == 0) continue;
+  aff_elems += n;
+  __syncthreads();
   const uint64_t src = g.off[gid];
   __shared__ unsigned long long dst_s;
   __shared__ double red_max[kWarps], red_min[kWarps];
@@ -435,6 +435,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
     atomicAdd(&st->out_elems, (unsigned long long)out_n);
   }
   }  // groups of this CTA
+  if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
 }
 
 // ---------------------------------------------------------------------------
