@@ -232,7 +232,7 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaEventCreate(&ev0_));
     PP_CUDA(cudaEventCreate(&ev1_));
     PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(BranchSmem<W>)));
+                                 (int)branch_smem_bytes<W>()));
     PP_CUDA(cudaFuncSetAttribute(k_sort_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(SortSmem<W>)));
     PP_CUDA(cudaFuncSetAttribute(k_sort_big<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -752,7 +752,7 @@ class EngineImpl final : public EngineBase {
     ensure_branch_space();
     std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
     PP_CUDA(cudaEventRecord(ev.first, stream_));
-    k_branch_x<W><<<std::min<uint32_t>(G_, branch_grid_), kCta, sizeof(BranchSmem<W>), stream_>>>(
+    k_branch_x<W><<<std::min<uint32_t>(G_, branch_grid_), kCta, branch_smem_bytes<W>(), stream_>>>(
         gview(gcur_), G_, aview(cur_), wq, mq, cosv, sinv, keep_zeros_, d_stats_);
     PP_CUDA(cudaEventRecord(ev.second, stream_));
     pending_events_.push_back(ev);

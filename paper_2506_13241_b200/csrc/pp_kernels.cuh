@@ -210,42 +210,22 @@ struct BranchSmem {
   uint32_t all_done;
 };
 
-// Persistent: CTA b visits groups b, b + gridDim.x, ... and branches those
-// the gate touches (z_q = 1), so selection costs no separate launch.
+// Three-stream merge over one range S[src, src + n) of a group (a whole
+// block of equal high bits, or a whole group): appends the sorted outputs at
+// dst + out_n.  Buffers: BranchSmem.
 template <int W>
-__global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, ArenaView<W> ar,
-                                                    int wq, uint64_t mq, double cosv, double sinv,
-                                                    int keep_zeros, DevStats* st) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
+__device__ void stream_branch_range(BranchSmem<W>& sm, ArenaView<W> ar, uint64_t src, uint32_t n, uint64_t dst,
+                                    uint32_t& out_n, int wq, uint64_t mq, double cosv, double sinv, int keep_zeros,
+                                    double& vmax, double& vmin, uint32_t& nonfinite, unsigned long long& records,
+                                    unsigned long long& removed) {
   const uint32_t tid = threadIdx.x;
-  if (engine_failed(st)) return;
-  unsigned long long aff_elems = 0;
-  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
-  if (!(g.z[wq][gid] & mq)) continue;  // uniform per CTA
-  const uint32_t n = g.cnt[gid];
-  if (n == 0) continue;
-  aff_elems += n;
+  const double nsin = -sinv;
   __syncthreads();
-  const uint64_t src = g.off[gid];
-  __shared__ unsigned long long dst_s;
-  __shared__ double red_max[kWarps], red_min[kWarps];
-  __shared__ unsigned long long red_rec[kWarps], red_rem[kWarps];
-  __shared__ uint32_t red_nf[kWarps];
   if (tid == 0) {
-    dst_s = atomicAdd(&st->bump, 2ull * n);
     sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0;
     sm.pos[0] = sm.pos[1] = sm.pos[2] = 0;
   }
   __syncthreads();
-  const uint64_t dst = dst_s;
-  const double nsin = -sinv;
-
-  uint32_t out_n = 0;
-  double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-  uint32_t nonfinite = 0;
-  unsigned long long records = 0, removed = 0;
-
   for (;;) {
     // ---- refill the three stream buffers --------------------------------
 #pragma unroll 1
@@ -401,41 +381,362 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, A
     if (sm.all_done) break;
   }
 
-  // ---- per-group statistics ---------------------------------------------
-  vmax = warp_max(vmax);
-  vmin = warp_min(vmin);
-  records = warp_sum64(records);
-  removed = warp_sum64(removed);
-  nonfinite = __any_sync(0xffffffffu, nonfinite);
-  const uint32_t lane = tid & 31, warp = tid >> 5;
-  if (lane == 0) {
-    red_max[warp] = vmax;
-    red_min[warp] = vmin;
-    red_rec[warp] = records;
-    red_rem[warp] = removed;
-    red_nf[warp] = nonfinite;
+}
+
+// ---------------------------------------------------------------------------
+// Segment path.  In a group sorted by x, the gate X_q pairs only strings that
+// agree on every x bit above q ("blocks"); inside a block the class-0 strings
+// (x_q = 0) precede the class-1 strings.  A block's output is the sorted
+// coset list Y = merge(S_0, S_1 &~e_q) followed by Y | e_q.  Whole blocks that
+// fit in one shared-memory segment are processed from a single coalesced
+// load: per-element ranks by binary search inside the block, per-block output
+// bases by a CTA scan, then one compaction and a coalesced store.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kSeg = 1024;
+constexpr uint32_t kVT = kSeg / kCta;
+constexpr uint32_t kNone = 0xffffffffu;
+
+template <int W>
+struct SegSmem {
+  uint64_t key[W * (kSeg + 1)];
+  double val[kSeg];
+  uint32_t blk[kSeg];
+  uint32_t bstart[kSeg + 1];
+  uint32_t bmid[kSeg];
+  uint32_t bpairs[kSeg];
+  uint32_t bobase[kSeg];
+  uint32_t bysz[kSeg];
+  uint64_t okey[W * 2 * kSeg];
+  double oval[2 * kSeg];
+  uint8_t oemit[2 * kSeg];
+  uint32_t scan[40];
+  uint32_t nb, nbc, lc, s2;
+};
+
+template <int W>
+__device__ __forceinline__ bool same_high(const Plane<W>& a, const Plane<W>& b, int wq, uint64_t hmask) {
+  bool eq = true;
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    uint64_t d = a.w[k] ^ b.w[k];
+    if (k > wq) eq &= d == 0;
+    else if (k == wq) eq &= (d & hmask) == 0;
+  }
+  return eq;
+}
+
+// first index in [lo, hi) of smem keys (stride kSeg+1) with key >= k
+template <int W>
+__device__ __forceinline__ uint32_t seg_lower_bound(const uint64_t* key, uint32_t lo, uint32_t hi, const Plane<W>& k) {
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (plane_lt<W>(sk_load<W>(key, kSeg + 1, mid), k)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Processes the complete blocks at the front of S[p, n); returns how many
+// strings were consumed (0: the first block is longer than a segment).
+template <int W>
+__device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, uint32_t p, uint32_t n, uint64_t dst,
+                               uint32_t& out_n, int wq, uint64_t mq, double cosv, double sinv, int keep_zeros,
+                               double& vmax, double& vmin, uint32_t& nonfinite, unsigned long long& records,
+                               unsigned long long& removed) {
+  const uint32_t tid = threadIdx.x;
+  const uint64_t hmask = ~((mq << 1) - 1);  // bits above q in word wq
+  const uint32_t L = min(kSeg, n - p);
+  const uint32_t has_next = (p + L < n) ? 1u : 0u;
+  const double nsin = -sinv;
+  __syncthreads();  // previous users of the shared buffers are done
+  for (uint32_t i = tid; i < L + has_next; i += kCta) {
+    sk_store<W>(sm.key, kSeg + 1, i, load_plane<W>(ar.x, src + p + i));
+    if (i < L) sm.val[i] = ar.c[src + p + i];
+  }
+  __syncthreads();
+  // block starts (blocked arrangement: thread t owns [t*kVT, t*kVT + kVT))
+  uint32_t flags = 0, cnt = 0;
+#pragma unroll
+  for (uint32_t v = 0; v < kVT; ++v) {
+    uint32_t i = tid * kVT + v;
+    bool f = i < L && (i == 0 || !same_high<W>(sk_load<W>(sm.key, kSeg + 1, i - 1), sk_load<W>(sm.key, kSeg + 1, i),
+                                               wq, hmask));
+    flags |= (f ? 1u : 0u) << v;
+    cnt += f;
+  }
+  uint32_t nb;
+  uint32_t run = block_excl_scan(cnt, sm.scan, &nb);
+#pragma unroll
+  for (uint32_t v = 0; v < kVT; ++v) {
+    uint32_t i = tid * kVT + v;
+    if (i >= L) break;
+    if (flags >> v & 1u) sm.bstart[run++] = i;
+    sm.blk[i] = run - 1;
   }
   __syncthreads();
   if (tid == 0) {
-    for (uint32_t w = 1; w < kWarps; ++w) {
-      vmax = fmax(vmax, red_max[w]);
-      vmin = fmin(vmin, red_min[w]);
-      records += red_rec[w];
-      removed += red_rem[w];
-      nonfinite |= red_nf[w];
-    }
-    g.off[gid] = dst;
-    g.cnt[gid] = out_n;
-    g.cap[gid] = 2 * n;
-    g.gmax[gid] = out_n ? vmax : 0.0;
-    g.gmin[gid] = out_n ? vmin : __longlong_as_double(0x7ff0000000000000ll);
-    g.flags[gid] = nonfinite;
-    atomicAdd(&st->records, records);
-    atomicAdd(&st->removed, removed);
-    atomicAdd(&st->out_elems, (unsigned long long)out_n);
+    bool last_complete = !has_next || !same_high<W>(sk_load<W>(sm.key, kSeg + 1, L - 1),
+                                                    sk_load<W>(sm.key, kSeg + 1, L), wq, hmask);
+    uint32_t nbc = last_complete ? nb : nb - 1;
+    uint32_t lc = last_complete ? L : sm.bstart[nb - 1];
+    sm.nbc = nbc;
+    sm.lc = lc;
+    sm.bstart[nbc] = lc;
   }
-  }  // groups of this CTA
+  __syncthreads();
+  const uint32_t nbc = sm.nbc, Lc = sm.lc;
+  if (nbc == 0) return 0;
+  for (uint32_t b = tid; b < nbc; b += kCta) {
+    sm.bmid[b] = sm.bstart[b + 1];
+    sm.bpairs[b] = 0;
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < Lc; i += kCta)
+    if (sm.key[wq * (kSeg + 1) + i] & mq) atomicMin(&sm.bmid[sm.blk[i]], i);
+  __syncthreads();
+  // ranks in the coset list Y of the element's block
+  uint32_t ry[kVT], pidx[kVT];
+#pragma unroll
+  for (uint32_t v = 0; v < kVT; ++v) {
+    uint32_t i = tid * kVT + v;
+    ry[v] = kNone;
+    pidx[v] = kNone;
+    if (i >= Lc) continue;
+    const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1], m = sm.bmid[b];
+    Plane<W> k = sk_load<W>(sm.key, kSeg + 1, i);
+    if (!(k.w[wq] & mq)) {  // class 0: partner x | e_q among [m, be)
+      Plane<W> t = k;
+      t.w[wq] |= mq;
+      uint32_t lb = seg_lower_bound<W>(sm.key, m, be, t);
+      if (lb < be && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), t)) {
+        pidx[v] = lb;
+        atomicAdd(&sm.bpairs[b], 1u);
+      }
+      ry[v] = (i - bs) + (lb - m);
+    } else {  // class 1: partner x &~e_q among [bs, m); a pair is owned by its class-0 member
+      Plane<W> y = k;
+      y.w[wq] &= ~mq;
+      uint32_t lb = seg_lower_bound<W>(sm.key, bs, m, y);
+      if (!(lb < m && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), y))) ry[v] = (i - m) + (lb - bs);
+    }
+  }
+  __syncthreads();
+  // per-block |Y| and output bases (scan over blocks, blocked arrangement)
+  uint32_t bsum = 0, ys[kVT];
+#pragma unroll
+  for (uint32_t v = 0; v < kVT; ++v) {
+    uint32_t b = tid * kVT + v;
+    ys[v] = 0;
+    if (b < nbc) ys[v] = (sm.bstart[b + 1] - sm.bstart[b]) - sm.bpairs[b];
+    bsum += 2 * ys[v];
+  }
+  uint32_t s2;
+  uint32_t ob = block_excl_scan(bsum, sm.scan, &s2);
+#pragma unroll
+  for (uint32_t v = 0; v < kVT; ++v) {
+    uint32_t b = tid * kVT + v;
+    if (b < nbc) {
+      sm.bobase[b] = ob;
+      sm.bysz[b] = ys[v];
+    }
+    ob += 2 * ys[v];
+  }
+  for (uint32_t i = tid; i < s2; i += kCta) sm.oemit[i] = 0;
+  __syncthreads();
+  // values: Rx rule (engine.cpp:218-227 + term_map.hpp:77-79)
+#pragma unroll
+  for (uint32_t v = 0; v < kVT; ++v) {
+    uint32_t i = tid * kVT + v;
+    if (i >= Lc || ry[v] == kNone) continue;
+    const uint32_t b = sm.blk[i];
+    const uint32_t s0 = sm.bobase[b] + ry[v], s1 = s0 + sm.bysz[b];
+    Plane<W> k = sk_load<W>(sm.key, kSeg + 1, i);
+    const double c = sm.val[i];
+    Plane<W> y = k, y1 = k;
+    y.w[wq] &= ~mq;
+    y1.w[wq] |= mq;
+    double v0, v1;
+    bool e0, e1;
+    if (!(k.w[wq] & mq)) {  // class 0 (Z at q): its child y|e_q gets +sin c0
+      const double d1 = __dmul_rn(sinv, c);
+      if (d1 != 0.0) ++records;
+      double s = __dmul_rn(c, cosv);
+      if (pidx[v] != kNone) {
+        const double c1 = sm.val[pidx[v]];
+        const double d0 = __dmul_rn(nsin, c1);  // child of the Y partner lands on y
+        if (d0 != 0.0) {
+          ++records;
+          s = __dadd_rn(s, d0);
+        }
+        double t = __dmul_rn(c1, cosv);
+        if (d1 != 0.0) t = __dadd_rn(t, d1);
+        v1 = t;
+        e1 = keep_zeros || t != 0.0;
+        if (!e1) ++removed;
+      } else {
+        v1 = d1;
+        e1 = d1 != 0.0;
+      }
+      v0 = s;
+      e0 = keep_zeros || s != 0.0;
+      if (!e0) ++removed;
+    } else {  // class 1 (Y at q) without partner: child y gets -sin c1
+      const double d0 = __dmul_rn(nsin, c);
+      if (d0 != 0.0) ++records;
+      v0 = d0;
+      e0 = d0 != 0.0;
+      v1 = __dmul_rn(c, cosv);
+      e1 = keep_zeros || v1 != 0.0;
+      if (!e1) ++removed;
+    }
+    sk_store<W>(sm.okey, 2 * kSeg, s0, y);
+    sm.oval[s0] = v0;
+    sm.oemit[s0] = e0;
+    sk_store<W>(sm.okey, 2 * kSeg, s1, y1);
+    sm.oval[s1] = v1;
+    sm.oemit[s1] = e1;
+  }
+  __syncthreads();
+  for (uint32_t base = 0; base < s2; base += kCta) {
+    uint32_t sl = base + tid;
+    bool e = sl < s2 && sm.oemit[sl];
+    uint32_t tot;
+    uint32_t o = block_excl_scan(e ? 1u : 0u, sm.scan, &tot);
+    if (e) {
+      const double val = sm.oval[sl];
+      const uint64_t d = dst + out_n + o;
+      store_plane<W>(ar.x, d, sk_load<W>(sm.okey, 2 * kSeg, sl));
+      ar.c[d] = val;
+      const double av = fabs(val);
+      if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
+      vmax = fmax(vmax, av);
+      vmin = fmin(vmin, av);
+    }
+    out_n += tot;
+  }
+  return Lc;
+}
+
+// End of the block that starts at p (first index with different high bits),
+// searched cooperatively: 256 probes per round narrow [lo, hi).
+template <int W>
+__device__ uint32_t find_block_end(ArenaView<W> ar, uint64_t src, uint32_t p, uint32_t n, int wq, uint64_t mq,
+                                   uint32_t* scan) {
+  const uint64_t hmask = ~((mq << 1) - 1);
+  const Plane<W> k0 = load_plane<W>(ar.x, src + p);
+  uint32_t lo = p, hi = n;  // x[lo] in the block; answer in (lo, hi]
+  __shared__ uint32_t s_lo, s_hi;
+  while (hi - lo > 1) {
+    const uint32_t span = hi - lo - 1;  // candidates lo+1 .. hi-1
+    const uint32_t step = (span + kCta - 1) / kCta;
+    const uint32_t pos = lo + 1 + threadIdx.x * step;
+    const bool valid = pos < hi;
+    const bool out = valid && !same_high<W>(k0, load_plane<W>(ar.x, src + pos), wq, hmask);
+    if (threadIdx.x == 0) {
+      s_lo = lo;
+      s_hi = hi;
+    }
+    __syncthreads();
+    if (valid && out) atomicMin(&s_hi, pos);
+    if (valid && !out) atomicMax(&s_lo, pos);
+    __syncthreads();
+    lo = s_lo;
+    hi = s_hi;
+    __syncthreads();
+    if (step == 1) break;
+  }
+  (void)scan;
+  return hi;
+}
+
+// Persistent: CTA b visits groups b, b + gridDim.x, ... and branches those
+// the gate touches (z_q = 1), so selection costs no separate launch.  Each
+// group is walked front to back: runs of small blocks go through the
+// shared-memory segment path, a block longer than a segment through the
+// three-stream merge restricted to that block.
+template <int W>
+__global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, ArenaView<W> ar,
+                                                    int wq, uint64_t mq, double cosv, double sinv,
+                                                    int keep_zeros, DevStats* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
+  SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  if (engine_failed(st)) return;
+  unsigned long long aff_elems = 0;
+  __shared__ unsigned long long dst_s;
+  __shared__ double red_max[kWarps], red_min[kWarps];
+  __shared__ unsigned long long red_rec[kWarps], red_rem[kWarps];
+  __shared__ uint32_t red_nf[kWarps];
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+    if (!(g.z[wq][gid] & mq)) continue;  // uniform per CTA
+    const uint32_t n = g.cnt[gid];
+    if (n == 0) continue;
+    aff_elems += n;
+    const uint64_t src = g.off[gid];
+    __syncthreads();
+    if (tid == 0) dst_s = atomicAdd(&st->bump, 2ull * n);
+    __syncthreads();
+    const uint64_t dst = dst_s;
+    uint32_t out_n = 0;
+    double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    uint32_t nonfinite = 0;
+    unsigned long long records = 0, removed = 0;
+    uint32_t p = 0;
+    while (p < n) {
+      uint32_t used = seg_branch<W>(sg, ar, src, p, n, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
+                                    nonfinite, records, removed);
+      if (used) {
+        p += used;
+        continue;
+      }
+      __syncthreads();
+      const uint32_t be = find_block_end<W>(ar, src, p, n, wq, mq, nullptr);
+      stream_branch_range<W>(sm, ar, src + p, be - p, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
+                             nonfinite, records, removed);
+      p = be;
+    }
+    // ---- per-group statistics -------------------------------------------
+    vmax = warp_max(vmax);
+    vmin = warp_min(vmin);
+    records = warp_sum64(records);
+    removed = warp_sum64(removed);
+    nonfinite = __any_sync(0xffffffffu, nonfinite);
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    __syncthreads();
+    if (lane == 0) {
+      red_max[warp] = vmax;
+      red_min[warp] = vmin;
+      red_rec[warp] = records;
+      red_rem[warp] = removed;
+      red_nf[warp] = nonfinite;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (uint32_t w = 1; w < kWarps; ++w) {
+        vmax = fmax(vmax, red_max[w]);
+        vmin = fmin(vmin, red_min[w]);
+        records += red_rec[w];
+        removed += red_rem[w];
+        nonfinite |= red_nf[w];
+      }
+      g.off[gid] = dst;
+      g.cnt[gid] = out_n;
+      g.cap[gid] = 2 * n;
+      g.gmax[gid] = out_n ? vmax : 0.0;
+      g.gmin[gid] = out_n ? vmin : __longlong_as_double(0x7ff0000000000000ll);
+      g.flags[gid] = nonfinite;
+      atomicAdd(&st->records, records);
+      atomicAdd(&st->removed, removed);
+      atomicAdd(&st->out_elems, (unsigned long long)out_n);
+    }
+  }
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
+}
+
+template <int W>
+constexpr size_t branch_smem_bytes() {
+  return sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
 }
 
 // ---------------------------------------------------------------------------
