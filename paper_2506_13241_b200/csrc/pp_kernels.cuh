@@ -406,6 +406,7 @@ struct SegSmem {
   uint32_t bpairs[kSeg];
   uint32_t bobase[kSeg];
   uint32_t bysz[kSeg];
+  uint32_t unp[kSeg + 1];  // exclusive prefix of "unpaired class-1" flags
   uint64_t okey[W * 2 * kSeg];
   double oval[2 * kSeg];
   uint8_t oemit[2 * kSeg];
@@ -494,17 +495,18 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
   for (uint32_t i = tid; i < Lc; i += kCta)
     if (sm.key[wq * (kSeg + 1) + i] & mq) atomicMin(&sm.bmid[sm.blk[i]], i);
   __syncthreads();
-  // ranks in the coset list Y of the element's block
-  uint32_t ry[kVT], pidx[kVT];
+  // partners: a class-0 x pairs with x | e_q, a class-1 x with x &~e_q
+  uint32_t lbv[kVT], pidx[kVT];
+  uint32_t unpaired = 0, ucnt = 0;
 #pragma unroll
   for (uint32_t v = 0; v < kVT; ++v) {
     uint32_t i = tid * kVT + v;
-    ry[v] = kNone;
+    lbv[v] = kNone;
     pidx[v] = kNone;
     if (i >= Lc) continue;
     const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1], m = sm.bmid[b];
     Plane<W> k = sk_load<W>(sm.key, kSeg + 1, i);
-    if (!(k.w[wq] & mq)) {  // class 0: partner x | e_q among [m, be)
+    if (!(k.w[wq] & mq)) {  // class 0: partner among [m, be)
       Plane<W> t = k;
       t.w[wq] |= mq;
       uint32_t lb = seg_lower_bound<W>(sm.key, m, be, t);
@@ -512,15 +514,41 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
         pidx[v] = lb;
         atomicAdd(&sm.bpairs[b], 1u);
       }
-      ry[v] = (i - bs) + (lb - m);
-    } else {  // class 1: partner x &~e_q among [bs, m); a pair is owned by its class-0 member
+      lbv[v] = lb;
+    } else {  // class 1: partner among [bs, m); a pair is owned by its class-0 member
       Plane<W> y = k;
       y.w[wq] &= ~mq;
       uint32_t lb = seg_lower_bound<W>(sm.key, bs, m, y);
-      if (!(lb < m && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), y))) ry[v] = (i - m) + (lb - bs);
+      if (!(lb < m && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), y))) {
+        lbv[v] = lb;
+        unpaired |= 1u << v;
+        ++ucnt;
+      }
     }
   }
+  {
+    uint32_t tot;
+    uint32_t e = block_excl_scan(ucnt, sm.scan, &tot);
+#pragma unroll
+    for (uint32_t v = 0; v < kVT; ++v) {
+      uint32_t i = tid * kVT + v;
+      if (i < Lc) sm.unp[i] = e;
+      e += (unpaired >> v) & 1u;
+    }
+    if (tid == 0) sm.unp[Lc] = tot;
+  }
   __syncthreads();
+  // rank in the coset list Y = #(class-0 keys below) + #(unpaired class-1 keys below)
+  uint32_t ry[kVT];
+#pragma unroll
+  for (uint32_t v = 0; v < kVT; ++v) {
+    uint32_t i = tid * kVT + v;
+    ry[v] = kNone;
+    if (i >= Lc || lbv[v] == kNone) continue;
+    const uint32_t b = sm.blk[i], bs = sm.bstart[b], m = sm.bmid[b];
+    if (!(sm.key[wq * (kSeg + 1) + i] & mq)) ry[v] = (i - bs) + (sm.unp[lbv[v]] - sm.unp[m]);
+    else ry[v] = (lbv[v] - bs) + (sm.unp[i] - sm.unp[m]);
+  }
   // per-block |Y| and output bases (scan over blocks, blocked arrangement)
   uint32_t bsum = 0, ys[kVT];
 #pragma unroll
