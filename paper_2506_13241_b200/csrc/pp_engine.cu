@@ -753,7 +753,9 @@ class EngineImpl final : public EngineBase {
     std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
     PP_CUDA(cudaEventRecord(ev.first, stream_));
     k_branch_x<W><<<std::min<uint32_t>(G_, branch_grid_), kCta, branch_smem_bytes<W>(), stream_>>>(
-        gview(gcur_), G_, aview(cur_), wq, mq, cosv, sinv, keep_zeros_, d_stats_);
+        gview(gcur_), G_, aview(cur_), wq, mq, cosv, sinv, keep_zeros_, gview(gcur_).z[wq],
+        &d_stats_->work[bseq_ & 1], &d_stats_->work[(bseq_ + 1) & 1], d_stats_);
+    ++bseq_;
     PP_CUDA(cudaEventRecord(ev.second, stream_));
     pending_events_.push_back(ev);
     launches_ += 1;

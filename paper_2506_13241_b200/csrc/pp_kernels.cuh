@@ -82,6 +82,7 @@ struct DevStats {
   unsigned long long err_live;     // |O| at the first error
   unsigned long long last_gmax_bits;  // gmax used by the latest truncation
   unsigned long long aff_total;    // cumulative strings in affected groups
+  unsigned int work[2];            // chunk counters of consecutive branch launches
 };
 
 // Reset of one reduction slot (cumulative counters and sticky errors stay).
@@ -677,15 +678,17 @@ __device__ uint32_t find_block_end(ArenaView<W> ar, uint64_t src, uint32_t p, ui
   return hi;
 }
 
-// Persistent: CTA b visits groups b, b + gridDim.x, ... and branches those
-// the gate touches (z_q = 1), so selection costs no separate launch.  Each
+// Persistent: CTAs grab chunks of kCta groups from a counter, select the
+// groups the gate touches (z_q = 1) with one coalesced check, and branch
+// them, so selection costs no separate launch.  Each
 // group is walked front to back: runs of small blocks go through the
 // shared-memory segment path, a block longer than a segment through the
 // three-stream merge restricted to that block.
 template <int W>
 __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, ArenaView<W> ar,
                                                     int wq, uint64_t mq, double cosv, double sinv,
-                                                    int keep_zeros, DevStats* st) {
+                                                    int keep_zeros, const uint64_t* __restrict__ zq,
+                                                    unsigned int* work, unsigned int* work_next, DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
@@ -696,10 +699,30 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, A
   __shared__ double red_max[kWarps], red_min[kWarps];
   __shared__ unsigned long long red_rec[kWarps], red_rem[kWarps];
   __shared__ uint32_t red_nf[kWarps];
-  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
-    if (!(g.z[wq][gid] & mq)) continue;  // uniform per CTA
+  __shared__ uint32_t glist[kCta];
+  __shared__ uint32_t gscan[40];
+  __shared__ uint32_t s_chunk, s_nlist;
+  if (blockIdx.x == 0 && tid == 0) *work_next = 0;  // the next gate's counter
+  for (;;) {
+  // grab the next chunk of kCta groups and select the affected ones in parallel
+  __syncthreads();
+  if (tid == 0) s_chunk = atomicAdd(work, 1u);
+  __syncthreads();
+  const uint32_t g0 = s_chunk * kCta;
+  if (g0 >= G) break;
+  {
+    const uint32_t gi = g0 + tid;
+    const bool take = gi < G && (zq[gi] & mq) && g.cnt[gi] != 0;
+    uint32_t tot;
+    const uint32_t o = block_excl_scan(take ? 1u : 0u, gscan, &tot);
+    if (take) glist[o] = gi;
+    if (tid == 0) s_nlist = tot;
+    __syncthreads();
+  }
+  const uint32_t nlist = s_nlist;
+  for (uint32_t li = 0; li < nlist; ++li) {
+    const uint32_t gid = glist[li];
     const uint32_t n = g.cnt[gid];
-    if (n == 0) continue;
     aff_elems += n;
     const uint64_t src = g.off[gid];
     __syncthreads();
@@ -758,7 +781,8 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, A
       atomicAdd(&st->removed, removed);
       atomicAdd(&st->out_elems, (unsigned long long)out_n);
     }
-  }
+  }  // groups of the chunk
+  }  // chunks
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
 }
 
