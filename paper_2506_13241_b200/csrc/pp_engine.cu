@@ -754,7 +754,8 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaEventRecord(ev.first, stream_));
     k_branch_x<W><<<std::min<uint32_t>(G_, branch_grid_), kCta, branch_smem_bytes<W>(), stream_>>>(
         gview(gcur_), G_, aview(cur_), wq, mq, cosv, sinv, keep_zeros_, gview(gcur_).z[wq],
-        &d_stats_->work[bseq_ & 1], &d_stats_->work[(bseq_ + 1) & 1], d_stats_);
+        &d_stats_->work[bseq_ & 1], &d_stats_->work[(bseq_ + 1) & 1],
+        std::max<uint32_t>(1u, std::min<uint32_t>(kCta, G_ / (4 * branch_grid_))), d_stats_);
     ++bseq_;
     PP_CUDA(cudaEventRecord(ev.second, stream_));
     pending_events_.push_back(ev);

@@ -688,7 +688,8 @@ template <int W>
 __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, ArenaView<W> ar,
                                                     int wq, uint64_t mq, double cosv, double sinv,
                                                     int keep_zeros, const uint64_t* __restrict__ zq,
-                                                    unsigned int* work, unsigned int* work_next, DevStats* st) {
+                                                    unsigned int* work, unsigned int* work_next, uint32_t chunk,
+                                                    DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
@@ -708,11 +709,11 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, A
   __syncthreads();
   if (tid == 0) s_chunk = atomicAdd(work, 1u);
   __syncthreads();
-  const uint32_t g0 = s_chunk * kCta;
+  const uint32_t g0 = s_chunk * chunk;
   if (g0 >= G) break;
   {
     const uint32_t gi = g0 + tid;
-    const bool take = gi < G && (zq[gi] & mq) && g.cnt[gi] != 0;
+    const bool take = tid < chunk && gi < G && (zq[gi] & mq) && g.cnt[gi] != 0;
     uint32_t tot;
     const uint32_t o = block_excl_scan(take ? 1u : 0u, gscan, &tot);
     if (take) glist[o] = gi;
