@@ -620,7 +620,14 @@ class EngineImpl final : public EngineBase {
     if (bump_bound_ + 2 * live_bound_ <= arena_[cur_].cap) return;
     sync_state();
     if (bump_ + 2 * live_ <= arena_[cur_].cap) return;
-    uint64_t target = std::max<uint64_t>((uint64_t)(live_ * 6) + (1u << 20), arena_[cur_].cap);
+    // after compaction the arena must hold |O| + 2|O|; leave more slack when
+    // memory allows so compactions stay rare
+    const uint64_t need = 3 * live_ + 1024;
+    size_t free_b = 0, total_b = 0;
+    PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t afford = (uint64_t)((free_b + arena_[1 - cur_].buf.bytes) * 0.8) / R;
+    uint64_t target = std::max<uint64_t>(need, std::min<uint64_t>(std::max<uint64_t>(live_ * 8, 1ull << 24), afford));
+    target = std::max<uint64_t>(target, std::min<uint64_t>(arena_[cur_].cap, afford));
     gc_into_other(target);
     if (bump_ + 2 * live_ > arena_[cur_].cap) throw EngineError(PP_ERR_INTERNAL, "arena sizing failed");
   }
@@ -644,7 +651,7 @@ class EngineImpl final : public EngineBase {
     RedSlot* rn = &d_stats_->red[(eseq_ + 1) & 1];
     ++eseq_;
     if (G_) {
-      k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, r);
+      k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), G_, r);
       k_truncate<W><<<std::min<uint32_t>(G_, persistent_grid()), kCta, 0, stream_>>>(
           gview(gcur_), G_, aview(cur_), cfg_.epsilon0, do_truncate ? 1 : 0, budget ? cfg_.max_terms : 0,
           gates_applied_, r, rn, d_stats_);
@@ -662,7 +669,7 @@ class EngineImpl final : public EngineBase {
   void sync_state() {
     if (!dirty_) return;
     k_red_reset<<<1, 1, 0, stream_>>>(&d_stats_->red[2]);
-    if (G_) k_reduce<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, &d_stats_->red[2]);
+    if (G_) k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), G_, &d_stats_->red[2]);
     launches_ += 2;
     fetch_stats();
     PP_CUDA(cudaGetLastError());
@@ -707,6 +714,7 @@ class EngineImpl final : public EngineBase {
     dirty_ = false;
   }
   uint32_t persistent_grid() const { return 148u * 8u; }
+  uint32_t reduce_grid() const { return std::max<uint32_t>(1u, std::min<uint32_t>(blocks(G_), 148u * 4u)); }
 
   // ----- one gate
   void apply_one(const pp_gate& gate) {
@@ -781,6 +789,59 @@ class EngineImpl final : public EngineBase {
 
   void ensure_list(uint32_t n) { list_.ensure((size_t)std::max<uint32_t>(n, 1) * 4); }
 
+  // A run of Clifford Z_i Z_j gates (i != j, no X/Y): split into matchings,
+  // then into equal-offset groups, and regroup with ZZRunProducer.
+  bool try_zz_run(const pp_gate* gates, size_t count) {
+    std::vector<std::pair<int, int>> edges(count);
+    std::vector<int> neg(count);
+    for (size_t g = 0; g < count; ++g) {
+      uint64_t jx[2], jz[2];
+      words_to_planes(gates[g].words, jx, jz);
+      if (jx[0] | jx[1]) return false;
+      int sites[3], ns = 0;
+      for (int w = 0; w < 2; ++w)
+        for (uint64_t v = jz[w]; v && ns < 3; v &= v - 1) sites[ns++] = 64 * w + __builtin_ctzll(v);
+      if (ns != 2) return false;
+      edges[g] = {sites[0], sites[1]};
+      neg[g] = gates[g].sin_theta < 0;
+    }
+    // greedy matchings in run order
+    std::vector<std::vector<size_t>> matchings;
+    std::vector<std::vector<uint8_t>> used;
+    for (size_t g = 0; g < count; ++g) {
+      size_t k = 0;
+      for (; k < matchings.size(); ++k)
+        if (!used[k][edges[g].first] && !used[k][edges[g].second]) break;
+      if (k == matchings.size()) {
+        matchings.emplace_back();
+        used.emplace_back(128, 0);
+      }
+      matchings[k].push_back(g);
+      used[k][edges[g].first] = used[k][edges[g].second] = 1;
+    }
+    ZZRunProducer<W> p;
+    p.ng = 0;
+    using T = typename PlaneInt<W>::T;
+    for (auto& mt : matchings) {
+      std::map<int, std::pair<T, T>> by_d;
+      for (size_t g : mt) {
+        int i = edges[g].first, d = edges[g].second - edges[g].first;  // first < second (ascending scan)
+        auto& e = by_d[d];
+        e.first |= (T)1 << i;
+        if (neg[g]) e.second |= (T)1 << i;
+      }
+      for (auto& [d, mm] : by_d) {
+        if (p.ng >= kMaxZZGroups) return false;
+        p.grp[p.ng].m = mm.first;
+        p.grp[p.ng].neg = mm.second;
+        p.grp[p.ng].d = d;
+        ++p.ng;
+      }
+    }
+    regroup(p);
+    return true;
+  }
+
   // ----- fused Clifford run
   void apply_clifford_run(const pp_gate* gates, size_t count) {
     auto t0 = Clock::now();
@@ -796,6 +857,9 @@ class EngineImpl final : public EngineBase {
       }
       gs[i] = gates[i].sin_theta;
     }
+    if (G_ && try_zz_run(gates, count)) {
+      // handled by the bit-parallel ZZ producer
+    } else {
     cliff_.ensure(count * (2 * W + 1) * 8);
     uint64_t* dgx = cliff_.as<uint64_t>();
     uint64_t* dgz = dgx + count * W;
@@ -805,6 +869,7 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaMemcpyAsync(dgs, gs.data(), count * 8, cudaMemcpyHostToDevice, stream_));
     CliffordProducer<W> p{dgx, dgz, dgs, (int)count};
     if (G_) regroup(p);
+    }
     // Clifford gates zero each moved parent and re-insert it at I xor J;
     // absent a partner pair the reference removes one zero per record.
     counters_.records_sent += h_records_;
@@ -831,7 +896,7 @@ class EngineImpl final : public EngineBase {
     rec_slot_.ensure(live * maxrec * 4);
     uint64_t records_upper = live * maxrec;
     uint64_t tc = 1024;
-    while (tc < 2 * std::min<uint64_t>(records_upper, 4ull * G_ + 1024)) tc <<= 1;
+    while (tc < 2 * std::min<uint64_t>(records_upper, std::max<uint64_t>(8ull * G_, live / 4) + 1024)) tc <<= 1;
     uint64_t tc_max = 1024;
     while (tc_max < 2 * records_upper) tc_max <<= 1;
     const int o = 1 - cur_;
@@ -855,7 +920,7 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(cudaGetLastError());
       if (h_stats_->overflow) {
         if (tc >= tc_max) throw EngineError(PP_ERR_INTERNAL, "regroup: hash table overflow");
-        tc = std::min(tc_max, tc * 4);
+        tc = std::min(tc_max, tc * 8);
         continue;
       }
       const uint32_t distinct = h_stats_->distinct;

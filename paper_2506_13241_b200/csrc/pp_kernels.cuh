@@ -797,25 +797,43 @@ constexpr size_t branch_smem_bytes() {
 // (truncate_now's first pass, engine.cpp:321-343, at group granularity)
 // ---------------------------------------------------------------------------
 template <int W>
-__global__ void k_reduce(GroupView<W> g, uint32_t G, RedSlot* out) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kCta) k_reduce(GroupView<W> g, uint32_t G, RedSlot* out) {
+  // grid-stride, then one set of atomics per CTA (same-address atomics from
+  // every warp serialise in L2)
   unsigned long long live = 0;
   double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
   uint32_t nf = 0;
-  if (i < G) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < G; i += gridDim.x * blockDim.x) {
     uint32_t c = g.cnt[i];
     if (c) {
-      live = c;
-      mx = g.gmax[i];
-      mn = g.gmin[i];
-      nf = g.flags[i] & 1u;
+      live += c;
+      mx = fmax(mx, g.gmax[i]);
+      mn = fmin(mn, g.gmin[i]);
+      nf |= g.flags[i] & 1u;
     }
   }
   live = warp_sum64(live);
   mx = warp_max(mx);
   mn = warp_min(mn);
   nf = __any_sync(0xffffffffu, nf);
+  __shared__ unsigned long long sl[kWarps];
+  __shared__ double smx[kWarps], smn[kWarps];
+  __shared__ uint32_t snf[kWarps];
+  const uint32_t w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    sl[w] = live;
+    smx[w] = mx;
+    smn[w] = mn;
+    snf[w] = nf;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 1; k < kWarps; ++k) {
+      live += sl[k];
+      mx = fmax(mx, smx[k]);
+      mn = fmin(mn, smn[k]);
+      nf |= snf[k];
+    }
     if (live) atomicAdd(&out->live, live);
     atomic_max_nonneg(reinterpret_cast<double*>(&out->gmax_bits), mx);
     atomic_min_nonneg(reinterpret_cast<double*>(&out->gmin_bits), mn);

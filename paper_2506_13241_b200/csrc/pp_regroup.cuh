@@ -74,6 +74,80 @@ struct CliffordProducer {
   }
 };
 
+// (a') fused run of Clifford Z_i Z_j gates, bit-parallel.  The run's edges
+// are split on the host into matchings (no shared qubit) and, inside a
+// matching, into groups of equal offset d = j - i; all gates of a group act on
+// disjoint sites, so one group is applied at once:
+//   a  = (x ^ x >> d) & M          anticommuting edges (x_i != x_j), at bit i
+//   zs = the z bit of the x-carrying site (Y there -> record sign +,
+//        X -> -; engine.cpp:67-81 with the phase table)
+//   factor of an edge = sign * sin = -1 iff (zs == 0) xor (sin == -1)
+//   z ^= a | a << d
+// Commuting Clifford rotations compose to the same signed permutation in any
+// order, so regrouping the run is exact.
+constexpr int kMaxZZGroups = 64;  // keeps the kernel parameter block under 4 KB
+
+template <int W>
+struct PlaneInt;
+template <>
+struct PlaneInt<1> {
+  using T = unsigned long long;
+};
+template <>
+struct PlaneInt<2> {
+  using T = unsigned __int128;
+};
+
+template <int W>
+struct ZZGroup {
+  typename PlaneInt<W>::T m;    // bit i set for every edge (i, i + d) of the group
+  typename PlaneInt<W>::T neg;  // edges whose gate has sin = -1
+  int d;
+};
+
+template <int W>
+struct ZZRunProducer {
+  static constexpr int kMaxRec = 1;
+  using T = typename PlaneInt<W>::T;
+  int ng;
+  ZZGroup<W> grp[kMaxZZGroups];
+  __device__ __forceinline__ static T pack(const Plane<W>& p) {
+    if constexpr (W == 1) return p.w[0];
+    else return (T)p.w[0] | ((T)p.w[1] << 64);
+  }
+  __device__ __forceinline__ static Plane<W> unpack(T v) {
+    Plane<W> p;
+    p.w[0] = (uint64_t)v;
+    if constexpr (W == 2) p.w[1] = (uint64_t)(v >> 64);
+    return p;
+  }
+  __device__ __forceinline__ static int popc(T v) {
+    if constexpr (W == 1) return __popcll(v);
+    else return __popcll((uint64_t)v) + __popcll((uint64_t)(v >> 64));
+  }
+  __device__ __forceinline__ int emit(Plane<W> xp, Plane<W> zp, double c, Record<W>* out, uint32_t* nrec) const {
+    const T x = pack(xp);
+    T z = pack(zp);
+    int flips = 0, moved = 0;
+    for (int k = 0; k < ng; ++k) {
+      const T m = grp[k].m;
+      const int d = grp[k].d;
+      const T a = (x ^ (x >> d)) & m;
+      if (!a) continue;
+      const T xi = x & m;
+      const T zs = (xi & z) | (~xi & (z >> d));  // z at the x-carrying site, at bit i
+      flips += popc((~zs ^ grp[k].neg) & a);
+      moved += popc(a);
+      z ^= a | (a << d);
+    }
+    out[0].x = xp;
+    out[0].z = unpack(z);
+    out[0].c = (flips & 1) ? -c : c;  // a product of +-1 factors: exact
+    *nrec = c != 0.0 ? (uint32_t)moved : 0u;
+    return 1;
+  }
+};
+
 // (b) one general gate: parent scaled by cos when it anticommutes, plus the
 // child (I xor J, (+-sin) c) when the increment is nonzero (engine.cpp:
 // 218-245).
