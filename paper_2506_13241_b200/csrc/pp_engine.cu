@@ -11,6 +11,8 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -51,6 +53,7 @@ __global__ void k_clear_cumulative(DevStats* st) {
   st->removed = 0;
   st->out_elems = 0;
   st->aff_total = 0;
+  st->stream_elems = 0;
 }
 
 __global__ void k_reset_stats(DevStats* st, unsigned long long bump) {
@@ -516,6 +519,10 @@ class EngineImpl final : public EngineBase {
     sync_state();
     *ms = branch_ms_;
     *bytes = branch_bytes_;
+    last_stream_frac_ = branch_in_ ? (double)branch_stream_ / (double)branch_in_ : 0.0;
+    if (std::getenv("PP_DEBUG")) std::fprintf(stderr, "[pp] branch strings %llu, via long-block stream path %.3f\n",
+                                              (unsigned long long)branch_in_, last_stream_frac_);
+    branch_in_ = branch_stream_ = 0;
     *launches = branch_launches_;
     *total = launches_;
     branch_ms_ = branch_bytes_ = 0.0;
@@ -709,6 +716,8 @@ class EngineImpl final : public EngineBase {
     }
     pending_events_.clear();
     branch_bytes_ += (double)(st.aff_total + st.out_elems) * R;
+    branch_in_ += st.aff_total;
+    branch_stream_ += st.stream_elems;
     k_clear_cumulative<<<1, 1, 0, stream_>>>(d_stats_);
     ++launches_;
     dirty_ = false;
@@ -1023,6 +1032,10 @@ class EngineImpl final : public EngineBase {
   uint64_t gates_applied_ = 0;
   int layer_ = 0;
   double branch_ms_ = 0.0, branch_bytes_ = 0.0;
+  uint64_t branch_in_ = 0, branch_stream_ = 0;
+ public:
+  double last_stream_frac_ = 0.0;
+ private:
   uint64_t branch_launches_ = 0, launches_ = 0;
 };
 

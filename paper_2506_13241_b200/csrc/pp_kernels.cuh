@@ -83,6 +83,7 @@ struct DevStats {
   unsigned long long last_gmax_bits;  // gmax used by the latest truncation
   unsigned long long aff_total;    // cumulative strings in affected groups
   unsigned int work[2];            // chunk counters of consecutive branch launches
+  unsigned long long stream_elems; // strings branched through the long-block stream path
 };
 
 // Reset of one reduction slot (cumulative counters and sticky errors stay).
@@ -404,10 +405,10 @@ struct SegSmem {
   uint32_t blk[kSeg];
   uint32_t bstart[kSeg + 1];
   uint32_t bmid[kSeg];
-  uint32_t bpairs[kSeg];
   uint32_t bobase[kSeg];
   uint32_t bysz[kSeg];
   uint32_t unp[kSeg + 1];  // exclusive prefix of "unpaired class-1" flags
+  uint32_t prs[kSeg + 1];  // exclusive prefix of "class-0 with partner" flags
   uint64_t okey[W * 2 * kSeg];
   double oval[2 * kSeg];
   uint8_t oemit[2 * kSeg];
@@ -488,17 +489,18 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
   __syncthreads();
   const uint32_t nbc = sm.nbc, Lc = sm.lc;
   if (nbc == 0) return 0;
-  for (uint32_t b = tid; b < nbc; b += kCta) {
-    sm.bmid[b] = sm.bstart[b + 1];
-    sm.bpairs[b] = 0;
-  }
+  for (uint32_t b = tid; b < nbc; b += kCta) sm.bmid[b] = sm.bstart[b + 1];
   __syncthreads();
-  for (uint32_t i = tid; i < Lc; i += kCta)
-    if (sm.key[wq * (kSeg + 1) + i] & mq) atomicMin(&sm.bmid[sm.blk[i]], i);
+  // class-1 strings are contiguous at the end of their block: the first one
+  // (bit q set, predecessor in the block with bit q clear) marks the mid
+  for (uint32_t i = tid; i < Lc; i += kCta) {
+    const uint64_t* kw = sm.key + wq * (kSeg + 1);
+    if ((kw[i] & mq) && (i == sm.bstart[sm.blk[i]] || !(kw[i - 1] & mq))) sm.bmid[sm.blk[i]] = i;
+  }
   __syncthreads();
   // partners: a class-0 x pairs with x | e_q, a class-1 x with x &~e_q
   uint32_t lbv[kVT], pidx[kVT];
-  uint32_t unpaired = 0, ucnt = 0;
+  uint32_t unpaired = 0, ucnt = 0, paired = 0, pcnt = 0;
 #pragma unroll
   for (uint32_t v = 0; v < kVT; ++v) {
     uint32_t i = tid * kVT + v;
@@ -513,7 +515,8 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
       uint32_t lb = seg_lower_bound<W>(sm.key, m, be, t);
       if (lb < be && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), t)) {
         pidx[v] = lb;
-        atomicAdd(&sm.bpairs[b], 1u);
+        paired |= 1u << v;
+        ++pcnt;
       }
       lbv[v] = lb;
     } else {  // class 1: partner among [bs, m); a pair is owned by its class-0 member
@@ -528,15 +531,22 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     }
   }
   {
+    // one scan for both prefixes: pairs in the high half, unpaired in the low
     uint32_t tot;
-    uint32_t e = block_excl_scan(ucnt, sm.scan, &tot);
+    uint32_t e = block_excl_scan((pcnt << 16) | ucnt, sm.scan, &tot);
 #pragma unroll
     for (uint32_t v = 0; v < kVT; ++v) {
       uint32_t i = tid * kVT + v;
-      if (i < Lc) sm.unp[i] = e;
-      e += (unpaired >> v) & 1u;
+      if (i < Lc) {
+        sm.unp[i] = e & 0xffffu;
+        sm.prs[i] = e >> 16;
+      }
+      e += ((unpaired >> v) & 1u) | (((paired >> v) & 1u) << 16);
     }
-    if (tid == 0) sm.unp[Lc] = tot;
+    if (tid == 0) {
+      sm.unp[Lc] = tot & 0xffffu;
+      sm.prs[Lc] = tot >> 16;
+    }
   }
   __syncthreads();
   // rank in the coset list Y = #(class-0 keys below) + #(unpaired class-1 keys below)
@@ -556,7 +566,7 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
   for (uint32_t v = 0; v < kVT; ++v) {
     uint32_t b = tid * kVT + v;
     ys[v] = 0;
-    if (b < nbc) ys[v] = (sm.bstart[b + 1] - sm.bstart[b]) - sm.bpairs[b];
+    if (b < nbc) ys[v] = (sm.bstart[b + 1] - sm.bstart[b]) - (sm.prs[sm.bstart[b + 1]] - sm.prs[sm.bstart[b]]);
     bsum += 2 * ys[v];
   }
   uint32_t s2;
@@ -744,6 +754,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, A
       }
       __syncthreads();
       const uint32_t be = find_block_end<W>(ar, src, p, n, wq, mq, nullptr);
+      if (tid == 0) atomicAdd(&st->stream_elems, (unsigned long long)(be - p));
       stream_branch_range<W>(sm, ar, src + p, be - p, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
                              nonfinite, records, removed);
       p = be;
