@@ -67,6 +67,7 @@ extern "C" {
 
 /* pp_config.flags */
 #define PP_FLAG_NO_CLIFFORD_FUSION 1u /* apply Clifford gates one by one */
+#define PP_FLAG_PROFILE 2u            /* no CUDA graphs; time every branch launch */
 
 typedef struct pp_engine pp_engine;
 

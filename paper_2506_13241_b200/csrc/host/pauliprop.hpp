@@ -167,6 +167,7 @@ struct EngineConfig {
   bool collect_gate_stats = false;
   int device = 0;
   bool fuse_clifford = true;
+  bool profile = false;  // no CUDA graphs, per-launch kernel timing
 };
 
 // Host copy of the operator (what Engine::merged() returns).

@@ -61,7 +61,13 @@ __global__ void k_reset_stats(DevStats* st, unsigned long long bump) {
   memset(&s, 0, sizeof(s));
   s.bump = bump;
   for (int i = 0; i < 3; ++i) s.red[i].gmin_bits = 0x7ff0000000000000ull;
+  s.err_seq = ~0ull;
   *st = s;
+}
+
+__global__ void k_clear_arena_error(DevStats* st) {
+  st->err_arena = 0;
+  st->err_seq = ~0ull;
 }
 
 // ---------------------------------------------------------------------------
@@ -245,6 +251,7 @@ class EngineImpl final : public EngineBase {
   }
   ~EngineImpl() override {
     cudaStreamSynchronize(stream_);
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     release_pinned_stats(h_stats_);
@@ -331,6 +338,7 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(cudaMemcpyAsync(g.gmax, gmx.data(), G * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemcpyAsync(g.gmin, gmn.data(), G * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemcpyAsync(g.flags, gfl.data(), G * 4, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemsetAsync(g.stamp, 0xff, G * 4, stream_));
     }
     reset_stats(n);
     PP_CUDA(cudaStreamSynchronize(stream_));
@@ -359,11 +367,153 @@ class EngineImpl final : public EngineBase {
         while (j < count && is_clifford(gates[j])) ++j;
         apply_clifford_run(gates + i, j - i);
         i = j;
+      } else if (is_x_type(gates[i])) {
+        size_t j = i;
+        while (j < count && is_x_type(gates[j]) && !(fusion_allowed() && is_clifford(gates[j]))) ++j;
+        run_rx(gates + i, j - i);
+        i = j;
       } else {
         apply_one(gates[i]);
         ++i;
       }
     }
+  }
+
+  // single-qubit X generator: the z-group preserving branch kernel applies
+  static bool is_x_type(const pp_gate& g) {
+    uint64_t jx[2], jz[2];
+    words_to_planes(g.words, jx, jz);
+    return (jz[0] | jz[1]) == 0 && __builtin_popcountll(jx[0]) + __builtin_popcountll(jx[1]) == 1;
+  }
+
+  struct RxParam {
+    int wq;
+    uint64_t mq;
+    double cosv, sinv;
+  };
+
+  // A run of X-type gates: launched as one CUDA graph (captured once per
+  // gate list and buffer set, replayed every layer) or as direct launches.
+  // An arena overflow inside the run stops it on the device; the host then
+  // compacts and resumes at the failing gate, whose finished groups carry
+  // its stamp and are skipped.
+  void run_rx(const pp_gate* gates, size_t count) {
+    if (W == 1)
+      for (size_t i = 0; i < count; ++i) {
+        uint64_t jx[2], jz[2];
+        words_to_planes(gates[i].words, jx, jz);
+        if (jx[1]) throw EngineError(PP_ERR_INVALID, "generator has sites beyond the engine width");
+      }
+    auto t0 = Clock::now();
+    std::vector<RxParam> prm(count);
+    for (size_t i = 0; i < count; ++i) {
+      uint64_t jx[2], jz[2];
+      words_to_planes(gates[i].words, jx, jz);
+      prm[i].wq = jx[0] ? 0 : 1;
+      prm[i].mq = jx[0] ? jx[0] : jx[1];
+      prm[i].cosv = gates[i].cos_theta;
+      prm[i].sinv = gates[i].sin_theta;
+    }
+    const bool budget = cfg_.max_terms != 0;
+    const bool epi = !(cfg_.epsilon0 == 0.0 && !budget && !may_hold_zeros_);
+    const bool do_trunc = cfg_.cadence == PP_CADENCE_GATE;
+    const uint64_t seq0 = bseq_;
+    size_t pos = 0;
+    while (pos < count && G_) {
+      sync_state();
+      if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
+      const bool use_graph = pos == 0 && !(cfg_.flags & PP_FLAG_PROFILE);
+      push_scalars(seq0 + pos);
+      if (use_graph) {
+        cudaGraphExec_t exec = rx_graph(prm, epi, do_trunc, budget);
+        std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
+        PP_CUDA(cudaEventRecord(ev.first, stream_));
+        PP_CUDA(cudaGraphLaunch(exec, stream_));
+        PP_CUDA(cudaEventRecord(ev.second, stream_));
+        pending_events_.push_back(ev);
+        launches_ += count * (epi ? 3 : 1);
+      } else {
+        for (size_t i = pos; i < count; ++i) {
+          std::pair<cudaEvent_t, cudaEvent_t> ev;
+          if (cfg_.flags & PP_FLAG_PROFILE) {
+            ev = take_event_pair();
+            PP_CUDA(cudaEventRecord(ev.first, stream_));
+          }
+          launch_branch(prm[i], (uint32_t)(i - pos));
+          if (cfg_.flags & PP_FLAG_PROFILE) {
+            PP_CUDA(cudaEventRecord(ev.second, stream_));
+            pending_events_.push_back(ev);
+          }
+          if (epi) launch_epilogue((uint32_t)(i - pos), do_trunc, budget);
+        }
+      }
+      branch_launches_ += count - pos;
+      if (keep_zeros_) may_hold_zeros_ = true;
+      if (epi && do_trunc) truncated_since_sync_ = true;
+      if (!epi && do_trunc) gmax_stale_ = true;
+      dirty_ = true;
+      sync_state();
+      if (!arena_fault_) break;
+      // resume at the first gate that ran out of room
+      pos = (size_t)(arena_fault_seq_ - seq0);
+      k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
+      ++launches_;
+      arena_fault_ = false;
+      gc_into_other(next_arena_target());
+    }
+    bseq_ = seq0 + count;
+    gates_applied_ += count;
+    counters_.gates += count;
+    counters_.batches_sent += count;
+    counters_.branch_ns += ns_since(t0);
+  }
+
+  void launch_branch(const RxParam& p, uint32_t rel) {
+    k_branch_x<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+        gview(gcur_), aview(cur_), p.wq, p.mq, p.cosv, p.sinv, keep_zeros_, gview(gcur_).z[p.wq],
+        &d_stats_->work[rel & 1], &d_stats_->work[(rel + 1) & 1], rel, d_stats_);
+    ++launches_;
+  }
+
+  cudaGraphExec_t rx_graph(const std::vector<RxParam>& prm, bool epi, bool do_trunc, bool budget) {
+    std::string key;
+    auto put = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
+    GroupView<W> gv = gview(gcur_);
+    ArenaView<W> av = aview(cur_);
+    put(&gv, sizeof(gv));
+    put(&av, sizeof(av));
+    int flags = (epi ? 1 : 0) | (do_trunc ? 2 : 0) | (budget ? 4 : 0) | (keep_zeros_ ? 8 : 0);
+    put(&flags, sizeof(flags));
+    for (const RxParam& p : prm) put(&p, sizeof(p));
+    auto it = graphs_.find(key);
+    if (it != graphs_.end()) return it->second;
+    if (graphs_.size() > 16) {
+      for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+      graphs_.clear();
+    }
+    cudaGraph_t graph;
+    PP_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    const uint64_t saved = launches_;
+    for (size_t i = 0; i < prm.size(); ++i) {
+      launch_branch(prm[i], (uint32_t)i);
+      if (epi) launch_epilogue((uint32_t)i, do_trunc, budget);
+    }
+    launches_ = saved;
+    PP_CUDA(cudaStreamEndCapture(stream_, &graph));
+    cudaGraphExec_t exec;
+    PP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    graphs_.emplace(key, exec);
+    return exec;
+  }
+
+  uint64_t next_arena_target() {
+    const uint64_t need = 3 * live_ + 1024;
+    size_t free_b = 0, total_b = 0;
+    PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t afford = (uint64_t)((free_b + arena_[1 - cur_].buf.bytes) * 0.8) / R;
+    uint64_t target = std::max<uint64_t>(need, std::min<uint64_t>(std::max<uint64_t>(live_ * 8, 1ull << 24), afford));
+    return std::max<uint64_t>(target, std::min<uint64_t>(arena_[cur_].cap, afford));
   }
 
   void truncate_now() override {
@@ -575,6 +725,8 @@ class EngineImpl final : public EngineBase {
     v.cap = reinterpret_cast<uint32_t*>(p);
     p += C * 4;
     v.flags = reinterpret_cast<uint32_t*>(p);
+    p += C * 4;
+    v.stamp = reinterpret_cast<uint32_t*>(p);
     return v;
   }
   void ensure_arena(int i, uint64_t cap) {
@@ -588,7 +740,7 @@ class EngineImpl final : public EngineBase {
     if (groups_[i].cap >= cap) return;
     groups_[i].buf.release();
     groups_[i].cap = 0;
-    groups_[i].buf.ensure((size_t)cap * (8 * W + 8 + 8 + 8 + 4 + 4 + 4));
+    groups_[i].buf.ensure((size_t)cap * (8 * W + 8 + 8 + 8 + 4 + 4 + 4 + 4));
     groups_[i].cap = cap;
   }
 
@@ -620,25 +772,6 @@ class EngineImpl final : public EngineBase {
     uint64_t cap = std::max<uint64_t>(arena_[cur_].cap, live_ + 1);
     gc_into_other(cap);
   }
-  // Room for one more X-type gate: the gate writes at most 2 * |O| strings.
-  // Uses the host's upper bounds first; synchronises (and compacts) only
-  // when the bound does not fit.
-  void ensure_branch_space() {
-    if (bump_bound_ + 2 * live_bound_ <= arena_[cur_].cap) return;
-    sync_state();
-    if (bump_ + 2 * live_ <= arena_[cur_].cap) return;
-    // after compaction the arena must hold |O| + 2|O|; leave more slack when
-    // memory allows so compactions stay rare
-    const uint64_t need = 3 * live_ + 1024;
-    size_t free_b = 0, total_b = 0;
-    PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t afford = (uint64_t)((free_b + arena_[1 - cur_].buf.bytes) * 0.8) / R;
-    uint64_t target = std::max<uint64_t>(need, std::min<uint64_t>(std::max<uint64_t>(live_ * 8, 1ull << 24), afford));
-    target = std::max<uint64_t>(target, std::min<uint64_t>(arena_[cur_].cap, afford));
-    gc_into_other(target);
-    if (bump_ + 2 * live_ > arena_[cur_].cap) throw EngineError(PP_ERR_INTERNAL, "arena sizing failed");
-  }
-
   // ----- per-gate epilogue and host synchronisation
   // Budget check, NaN check and truncation run on the device (k_truncate),
   // so consecutive gates need no host round trip; the host synchronises only
@@ -654,15 +787,9 @@ class EngineImpl final : public EngineBase {
       dirty_ = true;
       return;
     }
-    RedSlot* r = &d_stats_->red[eseq_ & 1];
-    RedSlot* rn = &d_stats_->red[(eseq_ + 1) & 1];
-    ++eseq_;
+    push_scalars(bseq_);
     if (G_) {
-      k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), G_, r);
-      k_truncate<W><<<std::min<uint32_t>(G_, persistent_grid()), kCta, 0, stream_>>>(
-          gview(gcur_), G_, aview(cur_), cfg_.epsilon0, do_truncate ? 1 : 0, budget ? cfg_.max_terms : 0,
-          gates_applied_, r, rn, d_stats_);
-      launches_ += 2;
+      launch_epilogue(0, do_truncate, budget);
       if (do_truncate) may_hold_zeros_ = false;
     }
     if (do_truncate) truncated_since_sync_ = true;
@@ -675,9 +802,10 @@ class EngineImpl final : public EngineBase {
   }
   void sync_state() {
     if (!dirty_) return;
+    push_scalars(bseq_);
     k_red_reset<<<1, 1, 0, stream_>>>(&d_stats_->red[2]);
-    if (G_) k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), G_, &d_stats_->red[2]);
-    launches_ += 2;
+    if (G_) k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, &d_stats_->red[2]);
+    launches_ += 3;
     fetch_stats();
     PP_CUDA(cudaGetLastError());
     const DevStats& st = *h_stats_;
@@ -694,6 +822,8 @@ class EngineImpl final : public EngineBase {
       throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient at gate " + std::to_string(st.err_gate + 1) +
                                               ", |O|=" + std::to_string(st.err_live));
     }
+    arena_fault_ = st.err_arena != 0;
+    arena_fault_seq_ = st.err_seq;
     if (st.red[2].nonfinite && gmax_stale_) {
       dirty_ = false;
       throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient detected at gate " + std::to_string(gates_applied_) +
@@ -723,7 +853,22 @@ class EngineImpl final : public EngineBase {
     dirty_ = false;
   }
   uint32_t persistent_grid() const { return 148u * 8u; }
-  uint32_t reduce_grid() const { return std::max<uint32_t>(1u, std::min<uint32_t>(blocks(G_), 148u * 4u)); }
+
+  void push_scalars(uint64_t seq_base) {
+    k_set_scalars<<<1, 1, 0, stream_>>>(d_stats_, G_, arena_[cur_].cap, seq_base);
+    ++launches_;
+  }
+  // per-gate epilogue kernels for gate `rel` of a launch run (red slots by parity)
+  void launch_epilogue(uint32_t rel, bool do_truncate, bool budget) {
+    RedSlot* r = &d_stats_->red[rel & 1];
+    RedSlot* rn = &d_stats_->red[(rel + 1) & 1];
+    k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, r);
+    k_truncate<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), aview(cur_), cfg_.epsilon0,
+                                                           do_truncate ? 1 : 0, budget ? cfg_.max_terms : 0, rel, r,
+                                                           rn, d_stats_);
+    launches_ += 2;
+  }
+  uint32_t reduce_grid() const { return 148u * 4u; }
 
   // ----- one gate
   void apply_one(const pp_gate& gate) {
@@ -736,7 +881,8 @@ class EngineImpl final : public EngineBase {
     if (nx == 0 && zfree) {
       // identity generator: commutes with everything, no records
     } else if (zfree && nx == 1) {
-      branch_x(jx, gate.cos_theta, gate.sin_theta);
+      run_rx(&gate, 1);
+      return;
     } else {
       GateProducer<W> p;
       for (int k = 0; k < W; ++k) {
@@ -752,36 +898,6 @@ class EngineImpl final : public EngineBase {
     counters_.batches_sent += 1;
     h_records_ = 0;
     post_gate();
-  }
-
-  void branch_x(const uint64_t* jx, double cosv, double sinv) {
-    if (G_ == 0) return;
-    Plane<W> px;
-    int wq = 0;
-    uint64_t mq = 0;
-    for (int k = 0; k < W; ++k) {
-      px.w[k] = jx[k];
-      if (jx[k]) {
-        wq = k;
-        mq = jx[k];
-      }
-    }
-    ensure_branch_space();
-    std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
-    PP_CUDA(cudaEventRecord(ev.first, stream_));
-    k_branch_x<W><<<std::min<uint32_t>(G_, branch_grid_), kCta, branch_smem_bytes<W>(), stream_>>>(
-        gview(gcur_), G_, aview(cur_), wq, mq, cosv, sinv, keep_zeros_, gview(gcur_).z[wq],
-        &d_stats_->work[bseq_ & 1], &d_stats_->work[(bseq_ + 1) & 1],
-        std::max<uint32_t>(1u, std::min<uint32_t>(kCta, G_ / (4 * branch_grid_))), d_stats_);
-    ++bseq_;
-    PP_CUDA(cudaEventRecord(ev.second, stream_));
-    pending_events_.push_back(ev);
-    launches_ += 1;
-    ++branch_launches_;
-    bump_bound_ += 2 * live_bound_;
-    live_bound_ *= 2;
-    if (keep_zeros_) may_hold_zeros_ = true;
-    dirty_ = true;
   }
 
   std::pair<cudaEvent_t, cudaEvent_t> take_event_pair() {
@@ -1024,6 +1140,9 @@ class EngineImpl final : public EngineBase {
   uint64_t bump_bound_ = 0, live_bound_ = 0;
   bool dirty_ = false, truncated_since_sync_ = false, gmax_stale_ = false, may_hold_zeros_ = false;
   uint64_t eseq_ = 0, bseq_ = 0;
+  bool arena_fault_ = false;
+  uint64_t arena_fault_seq_ = 0;
+  std::map<std::string, cudaGraphExec_t> graphs_;
   uint32_t branch_grid_ = 148u * 2u;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_events_, free_events_;
   unsigned long long seed_;

@@ -36,6 +36,7 @@ struct GroupView {
   double* gmax;
   double* gmin;
   uint32_t* flags;  // bit0: non-finite coefficient present
+  uint32_t* stamp;  // sequence number of the last X-type gate applied (makes gates resumable)
 };
 
 // Per-gate scratch lives in small slot arrays so consecutive gates need no
@@ -84,13 +85,30 @@ struct DevStats {
   unsigned long long aff_total;    // cumulative strings in affected groups
   unsigned int work[2];            // chunk counters of consecutive branch launches
   unsigned long long stream_elems; // strings branched through the long-block stream path
+  unsigned long long arena_cap;    // capacity of the current arena (strings)
+  unsigned long long seq_base;     // sequence number of gate 0 of the current launch run
+  unsigned int G_dev;              // group count of the current table
+  unsigned int err_arena;          // sticky: a branch allocation did not fit; run must resume
+  unsigned long long err_seq;      // first gate sequence number that overflowed
 };
+
+// Scalars a launch run reads from device memory, so that a captured CUDA
+// graph can be replayed for every layer.
+__global__ void k_set_scalars(DevStats* st, unsigned int G, unsigned long long cap, unsigned long long seq_base) {
+  st->G_dev = G;
+  st->arena_cap = cap;
+  st->seq_base = seq_base;
+  st->work[0] = st->work[1] = 0;
+  clear_red(&st->red[0]);
+  clear_red(&st->red[1]);
+}
 
 // Reset of one reduction slot (cumulative counters and sticky errors stay).
 __global__ void k_red_reset(RedSlot* r) { clear_red(r); }
 
 __device__ __forceinline__ bool engine_failed(const DevStats* st) {
-  return (*(volatile const unsigned int*)&st->err_budget) | (*(volatile const unsigned int*)&st->err_numerical);
+  return (*(volatile const unsigned int*)&st->err_budget) | (*(volatile const unsigned int*)&st->err_numerical) |
+         (*(volatile const unsigned int*)&st->err_arena);
 }
 
 template <int W>
@@ -695,16 +713,19 @@ __device__ uint32_t find_block_end(ArenaView<W> ar, uint64_t src, uint32_t p, ui
 // shared-memory segment path, a block longer than a segment through the
 // three-stream merge restricted to that block.
 template <int W>
-__global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, ArenaView<W> ar,
-                                                    int wq, uint64_t mq, double cosv, double sinv,
-                                                    int keep_zeros, const uint64_t* __restrict__ zq,
-                                                    unsigned int* work, unsigned int* work_next, uint32_t chunk,
-                                                    DevStats* st) {
+__global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> ar, int wq, uint64_t mq,
+                                                    double cosv, double sinv, int keep_zeros,
+                                                    const uint64_t* __restrict__ zq, unsigned int* work,
+                                                    unsigned int* work_next, uint32_t seq_rel, DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
   const uint32_t tid = threadIdx.x;
   if (engine_failed(st)) return;
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  const unsigned long long cap = *(volatile const unsigned long long*)&st->arena_cap;
+  const uint32_t seq = (uint32_t)(*(volatile const unsigned long long*)&st->seq_base + seq_rel);
+  const uint32_t chunk = max(1u, min(kCta, G / (4u * gridDim.x)));
   unsigned long long aff_elems = 0;
   __shared__ unsigned long long dst_s;
   __shared__ double red_max[kWarps], red_min[kWarps];
@@ -723,7 +744,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, A
   if (g0 >= G) break;
   {
     const uint32_t gi = g0 + tid;
-    const bool take = tid < chunk && gi < G && (zq[gi] & mq) && g.cnt[gi] != 0;
+    const bool take = tid < chunk && gi < G && (zq[gi] & mq) && g.cnt[gi] != 0 && g.stamp[gi] != seq;
     uint32_t tot;
     const uint32_t o = block_excl_scan(take ? 1u : 0u, gscan, &tot);
     if (take) glist[o] = gi;
@@ -734,12 +755,19 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, A
   for (uint32_t li = 0; li < nlist; ++li) {
     const uint32_t gid = glist[li];
     const uint32_t n = g.cnt[gid];
-    aff_elems += n;
     const uint64_t src = g.off[gid];
     __syncthreads();
-    if (tid == 0) dst_s = atomicAdd(&st->bump, 2ull * n);
+    if (tid == 0) {
+      dst_s = atomicAdd(&st->bump, 2ull * n);
+      if (dst_s + 2ull * n > cap) {  // no room: leave the group untouched, the host compacts and resumes
+        atomicOr(&st->err_arena, 1u);
+        atomicMin(&st->err_seq, (unsigned long long)seq);
+      }
+    }
     __syncthreads();
     const uint64_t dst = dst_s;
+    if (dst + 2ull * n > cap) continue;
+    aff_elems += n;
     uint32_t out_n = 0;
     double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     uint32_t nonfinite = 0;
@@ -789,6 +817,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, uint32_t G, A
       g.gmax[gid] = out_n ? vmax : 0.0;
       g.gmin[gid] = out_n ? vmin : __longlong_as_double(0x7ff0000000000000ll);
       g.flags[gid] = nonfinite;
+      g.stamp[gid] = seq;
       atomicAdd(&st->records, records);
       atomicAdd(&st->removed, removed);
       atomicAdd(&st->out_elems, (unsigned long long)out_n);
@@ -808,7 +837,8 @@ constexpr size_t branch_smem_bytes() {
 // (truncate_now's first pass, engine.cpp:321-343, at group granularity)
 // ---------------------------------------------------------------------------
 template <int W>
-__global__ void __launch_bounds__(kCta) k_reduce(GroupView<W> g, uint32_t G, RedSlot* out) {
+__global__ void __launch_bounds__(kCta) k_reduce(GroupView<W> g, const DevStats* st, RedSlot* out) {
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
   // grid-stride, then one set of atomics per CTA (same-address atomics from
   // every warp serialise in L2)
   unsigned long long live = 0;
@@ -913,12 +943,13 @@ __device__ void truncate_group(GroupView<W> g, ArenaView<W> ar, uint32_t gid, do
 //              remove |c| <= T in every group whose min |c| <= T.
 // Persistent grid-stride over groups.
 template <int W>
-__global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, uint32_t G, ArenaView<W> ar, double epsilon0,
+__global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, ArenaView<W> ar, double epsilon0,
                                                    int do_truncate, unsigned long long max_terms,
                                                    unsigned long long gate_index, RedSlot* red, RedSlot* red_next,
                                                    DevStats* st) {
   if (blockIdx.x == 0 && threadIdx.x == 0) clear_red(red_next);
   if (engine_failed(st)) return;
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
   const unsigned long long live = *(volatile unsigned long long*)&red->live;
   if (max_terms && live > max_terms) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && atomicCAS(&st->err_budget, 0u, 1u) == 0u) {

@@ -369,6 +369,7 @@ __global__ void k_table_emit(HashTable<W> t, const unsigned long long* gid_scan,
   ng.cap[gid] = c;
   ng.cnt[gid] = 0;  // scatter cursor
   ng.flags[gid] = 0;
+  ng.stamp[gid] = 0xffffffffu;
 }
 
 template <int W, class P>
