@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
   const unsigned long long cap = *(volatile const unsigned long long*)&st->arena_cap;
   const uint32_t seq = (uint32_t)(*(volatile const unsigned long long*)&st->seq_base + seq_rel);
-  const uint32_t chunk = max(1u, min(kCta, G / (4u * gridDim.x)));
+  const uint32_t chunk = max(1u, min(kCta, (G + gridDim.x - 1) / gridDim.x));  // one selection round when G is small
   unsigned long long aff_elems = 0;
   __shared__ unsigned long long dst_s;
   __shared__ double red_max[kWarps], red_min[kWarps];
