@@ -213,6 +213,9 @@ static void release_pinned_stats(DevStats* p) {
   g_pinned_free.push_back(p);
 }
 
+static std::mutex g_graph_mu;
+static std::map<std::string, cudaGraphExec_t> g_graphs;
+
 class EngineBase {
  public:
   virtual ~EngineBase() = default;
@@ -251,7 +254,6 @@ class EngineImpl final : public EngineBase {
   }
   ~EngineImpl() override {
     cudaStreamSynchronize(stream_);
-    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     release_pinned_stats(h_stats_);
@@ -482,14 +484,24 @@ class EngineImpl final : public EngineBase {
     ArenaView<W> av = aview(cur_);
     put(&gv, sizeof(gv));
     put(&av, sizeof(av));
+    put(&d_stats_, sizeof(d_stats_));
+    put(&cfg_.epsilon0, sizeof(double));
+    put(&cfg_.max_terms, sizeof(uint64_t));
+    int dev = cfg_.device;
+    put(&dev, sizeof(dev));
+    int w = W;
+    put(&w, sizeof(w));
     int flags = (epi ? 1 : 0) | (do_trunc ? 2 : 0) | (budget ? 4 : 0) | (keep_zeros_ ? 8 : 0);
     put(&flags, sizeof(flags));
     for (const RxParam& p : prm) put(&p, sizeof(p));
-    auto it = graphs_.find(key);
-    if (it != graphs_.end()) return it->second;
-    if (graphs_.size() > 16) {
-      for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
-      graphs_.clear();
+    // process-wide cache: engines built one per simulate() call get the same
+    // pooled buffers, so their graphs are identical and reused
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto it = g_graphs.find(key);
+    if (it != g_graphs.end()) return it->second;
+    if (g_graphs.size() > 64) {
+      for (auto& kv : g_graphs) cudaGraphExecDestroy(kv.second);
+      g_graphs.clear();
     }
     cudaGraph_t graph;
     PP_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
@@ -503,7 +515,7 @@ class EngineImpl final : public EngineBase {
     cudaGraphExec_t exec;
     PP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     cudaGraphDestroy(graph);
-    graphs_.emplace(key, exec);
+    g_graphs.emplace(key, exec);
     return exec;
   }
 
@@ -1142,7 +1154,7 @@ class EngineImpl final : public EngineBase {
   uint64_t eseq_ = 0, bseq_ = 0;
   bool arena_fault_ = false;
   uint64_t arena_fault_seq_ = 0;
-  std::map<std::string, cudaGraphExec_t> graphs_;
+
   uint32_t branch_grid_ = 148u * 2u;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_events_, free_events_;
   unsigned long long seed_;
