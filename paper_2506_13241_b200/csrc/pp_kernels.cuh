@@ -653,7 +653,24 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     sm.oval[s1] = v1;
     sm.oemit[s1] = e1;
   }
-  __syncthreads();
+  // every slot emitted (no exact zero, the common case): the slots are the
+  // compacted output already, stream them out coalesced without a scan
+  bool any_hole = false;
+  for (uint32_t i = tid; i < s2; i += kCta) any_hole |= !sm.oemit[i];
+  if (!__syncthreads_or(any_hole)) {
+    for (uint32_t i = tid; i < s2; i += kCta) {
+      const double val = sm.oval[i];
+      const uint64_t d = dst + out_n + i;
+      store_plane<W>(ar.x, d, sk_load<W>(sm.okey, 2 * kSeg, i));
+      ar.c[d] = val;
+      const double av = fabs(val);
+      if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
+      vmax = fmax(vmax, av);
+      vmin = fmin(vmin, av);
+    }
+    out_n += s2;
+    return Lc;
+  }
   for (uint32_t base = 0; base < s2; base += kCta) {
     uint32_t sl = base + tid;
     bool e = sl < s2 && sm.oemit[sl];
