@@ -418,20 +418,21 @@ constexpr uint32_t kNone = 0xffffffffu;
 
 template <int W>
 struct SegSmem {
-  uint64_t key[W * (kSeg + 1)];
+  uint64_t key[W * (kSeg + 1)];  // x planes of the segment (+1 lookahead), SoA
   double val[kSeg];
-  uint32_t blk[kSeg];
-  uint32_t bstart[kSeg + 1];
-  uint32_t bmid[kSeg];
-  uint32_t bobase[kSeg];
-  uint32_t bysz[kSeg];
-  uint32_t unp[kSeg + 1];  // exclusive prefix of "unpaired class-1" flags
-  uint32_t prs[kSeg + 1];  // exclusive prefix of "class-0 with partner" flags
+  alignas(16) uint32_t blk[kSeg];  // block id per string (stored as uint4)
+  uint32_t bstart[kSeg + 1];     // first string of each block (+ end)
+  uint32_t bmid[kSeg];           // first class-1 string of each block
+  uint32_t bobase[kSeg];         // output slot base of each block
+  alignas(16) uint32_t pre[kSeg + 4];  // exclusive prefixes: pairs << 16 | unpaired class-1
+  uint32_t lbv[kSeg];            // partner search result per string
+  uint16_t cpos[2 * kSeg];       // compacted output position per slot
+  alignas(16) uint8_t f[kSeg];   // bit0 block start, bit1 class-0 with partner, bit2 unpaired class-1
   uint64_t okey[W * 2 * kSeg];
   double oval[2 * kSeg];
-  uint8_t oemit[2 * kSeg];
+  alignas(16) uint8_t oemit[2 * kSeg];
   uint32_t scan[40];
-  uint32_t nb, nbc, lc, s2;
+  uint32_t nbc, lc;
 };
 
 template <int W>
@@ -459,6 +460,8 @@ __device__ __forceinline__ uint32_t seg_lower_bound(const uint64_t* key, uint32_
 
 // Processes the complete blocks at the front of S[p, n); returns how many
 // strings were consumed (0: the first block is longer than a segment).
+// Per-string passes are striped (string i on thread i % kCta: conflict-free
+// shared memory); the three scans read flag bytes in a blocked layout.
 template <int W>
 __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, uint32_t p, uint32_t n, uint64_t dst,
                                uint32_t& out_n, int wq, uint64_t mq, double cosv, double sinv, int keep_zeros,
@@ -469,157 +472,143 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
   const uint32_t L = min(kSeg, n - p);
   const uint32_t has_next = (p + L < n) ? 1u : 0u;
   const double nsin = -sinv;
+  const uint64_t* kq = sm.key + wq * (kSeg + 1);  // the plane word holding bit q
   __syncthreads();  // previous users of the shared buffers are done
   for (uint32_t i = tid; i < L + has_next; i += kCta) {
     sk_store<W>(sm.key, kSeg + 1, i, load_plane<W>(ar.x, src + p + i));
     if (i < L) sm.val[i] = ar.c[src + p + i];
   }
   __syncthreads();
-  // block starts (blocked arrangement: thread t owns [t*kVT, t*kVT + kVT))
-  uint32_t flags = 0, cnt = 0;
-#pragma unroll
-  for (uint32_t v = 0; v < kVT; ++v) {
-    uint32_t i = tid * kVT + v;
+  // block starts (string i differs from i-1 above bit q)
+  for (uint32_t i = tid; i < kSeg; i += kCta) {
     bool f = i < L && (i == 0 || !same_high<W>(sk_load<W>(sm.key, kSeg + 1, i - 1), sk_load<W>(sm.key, kSeg + 1, i),
                                                wq, hmask));
-    flags |= (f ? 1u : 0u) << v;
-    cnt += f;
-  }
-  uint32_t nb;
-  uint32_t run = block_excl_scan(cnt, sm.scan, &nb);
-#pragma unroll
-  for (uint32_t v = 0; v < kVT; ++v) {
-    uint32_t i = tid * kVT + v;
-    if (i >= L) break;
-    if (flags >> v & 1u) sm.bstart[run++] = i;
-    sm.blk[i] = run - 1;
+    sm.f[i] = f ? 1 : 0;
   }
   __syncthreads();
-  if (tid == 0) {
-    bool last_complete = !has_next || !same_high<W>(sk_load<W>(sm.key, kSeg + 1, L - 1),
-                                                    sk_load<W>(sm.key, kSeg + 1, L), wq, hmask);
-    uint32_t nbc = last_complete ? nb : nb - 1;
-    uint32_t lc = last_complete ? L : sm.bstart[nb - 1];
-    sm.nbc = nbc;
-    sm.lc = lc;
-    sm.bstart[nbc] = lc;
-  }
-  __syncthreads();
-  const uint32_t nbc = sm.nbc, Lc = sm.lc;
-  if (nbc == 0) return 0;
-  for (uint32_t b = tid; b < nbc; b += kCta) sm.bmid[b] = sm.bstart[b + 1];
-  __syncthreads();
-  // class-1 strings are contiguous at the end of their block: the first one
-  // (bit q set, predecessor in the block with bit q clear) marks the mid
-  for (uint32_t i = tid; i < Lc; i += kCta) {
-    const uint64_t* kw = sm.key + wq * (kSeg + 1);
-    if ((kw[i] & mq) && (i == sm.bstart[sm.blk[i]] || !(kw[i - 1] & mq))) sm.bmid[sm.blk[i]] = i;
-  }
-  __syncthreads();
-  // partners: a class-0 x pairs with x | e_q, a class-1 x with x &~e_q
-  uint32_t lbv[kVT], pidx[kVT];
-  uint32_t unpaired = 0, ucnt = 0, paired = 0, pcnt = 0;
-#pragma unroll
-  for (uint32_t v = 0; v < kVT; ++v) {
-    uint32_t i = tid * kVT + v;
-    lbv[v] = kNone;
-    pidx[v] = kNone;
-    if (i >= Lc) continue;
-    const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1], m = sm.bmid[b];
-    Plane<W> k = sk_load<W>(sm.key, kSeg + 1, i);
-    if (!(k.w[wq] & mq)) {  // class 0: partner among [m, be)
-      Plane<W> t = k;
-      t.w[wq] |= mq;
-      uint32_t lb = seg_lower_bound<W>(sm.key, m, be, t);
-      if (lb < be && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), t)) {
-        pidx[v] = lb;
-        paired |= 1u << v;
-        ++pcnt;
-      }
-      lbv[v] = lb;
-    } else {  // class 1: partner among [bs, m); a pair is owned by its class-0 member
-      Plane<W> y = k;
-      y.w[wq] &= ~mq;
-      uint32_t lb = seg_lower_bound<W>(sm.key, bs, m, y);
-      if (!(lb < m && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), y))) {
-        lbv[v] = lb;
-        unpaired |= 1u << v;
-        ++ucnt;
-      }
-    }
-  }
+  // scan 1 (blocked): block ids and starts
   {
-    // one scan for both prefixes: pairs in the high half, unpaired in the low
-    uint32_t tot;
-    uint32_t e = block_excl_scan((pcnt << 16) | ucnt, sm.scan, &tot);
+    const uint32_t fl = reinterpret_cast<const uint32_t*>(sm.f)[tid];  // bytes 4 tid .. 4 tid + 3
+    uint32_t cnt = __popc(fl & 0x01010101u);
+    uint32_t nb;
+    uint32_t run = block_excl_scan(cnt, sm.scan, &nb);
+    uint32_t ids[kVT];
 #pragma unroll
     for (uint32_t v = 0; v < kVT; ++v) {
-      uint32_t i = tid * kVT + v;
-      if (i < Lc) {
-        sm.unp[i] = e & 0xffffu;
-        sm.prs[i] = e >> 16;
-      }
-      e += ((unpaired >> v) & 1u) | (((paired >> v) & 1u) << 16);
+      const uint32_t i = tid * kVT + v;
+      if ((fl >> (8 * v)) & 1u) sm.bstart[run++] = i;
+      ids[v] = run - 1;
     }
+    reinterpret_cast<uint4*>(sm.blk)[tid] = make_uint4(ids[0], ids[1], ids[2], ids[3]);
+    __syncthreads();
     if (tid == 0) {
-      sm.unp[Lc] = tot & 0xffffu;
-      sm.prs[Lc] = tot >> 16;
+      bool last_complete = !has_next || !same_high<W>(sk_load<W>(sm.key, kSeg + 1, L - 1),
+                                                      sk_load<W>(sm.key, kSeg + 1, L), wq, hmask);
+      uint32_t nbc = last_complete ? nb : nb - 1;
+      uint32_t lc = last_complete ? L : sm.bstart[nb - 1];
+      sm.nbc = nbc;
+      sm.lc = lc;
+      sm.bstart[nbc] = lc;
     }
+    __syncthreads();
+  }
+  const uint32_t nbc = sm.nbc, Lc = sm.lc;
+  if (nbc == 0) return 0;
+  // mid of each block: its first class-1 string (class-1 strings close the block)
+  for (uint32_t b = tid; b < nbc; b += kCta) sm.bmid[b] = sm.bstart[b + 1];
+  __syncthreads();
+  for (uint32_t i = tid; i < Lc; i += kCta)
+    if ((kq[i] & mq) && ((sm.f[i] & 1u) || !(kq[i - 1] & mq))) sm.bmid[sm.blk[i]] = i;
+  __syncthreads();
+  // partners: class-0 x pairs with x | e_q in [mid, end), class-1 x with x &~e_q in [start, mid)
+  for (uint32_t i = tid; i < kSeg; i += kCta) {
+    uint8_t fl = i < kSeg ? sm.f[i] : 0;
+    if (i < Lc) {
+      const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1], m = sm.bmid[b];
+      Plane<W> k = sk_load<W>(sm.key, kSeg + 1, i);
+      if (!(k.w[wq] & mq)) {
+        k.w[wq] |= mq;
+        uint32_t lb = seg_lower_bound<W>(sm.key, m, be, k);
+        if (lb < be && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), k)) fl |= 2;
+        sm.lbv[i] = lb;
+      } else {
+        k.w[wq] &= ~mq;
+        uint32_t lb = seg_lower_bound<W>(sm.key, bs, m, k);
+        if (!(lb < m && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), k))) fl |= 4;
+        sm.lbv[i] = lb;
+      }
+    }
+    sm.f[i] = fl;
   }
   __syncthreads();
-  // rank in the coset list Y = #(class-0 keys below) + #(unpaired class-1 keys below)
-  uint32_t ry[kVT];
+  // scan 2 (blocked): pairs (high half) and unpaired class-1 (low half)
+  {
+    const uint32_t fl = reinterpret_cast<const uint32_t*>(sm.f)[tid];
+    const uint32_t c = (__popc(fl & 0x02020202u) << 16) | __popc(fl & 0x04040404u);
+    uint32_t tot;
+    uint32_t e = block_excl_scan(c, sm.scan, &tot);
+    uint32_t out[kVT];
 #pragma unroll
-  for (uint32_t v = 0; v < kVT; ++v) {
-    uint32_t i = tid * kVT + v;
-    ry[v] = kNone;
-    if (i >= Lc || lbv[v] == kNone) continue;
-    const uint32_t b = sm.blk[i], bs = sm.bstart[b], m = sm.bmid[b];
-    if (!(sm.key[wq * (kSeg + 1) + i] & mq)) ry[v] = (i - bs) + (sm.unp[lbv[v]] - sm.unp[m]);
-    else ry[v] = (lbv[v] - bs) + (sm.unp[i] - sm.unp[m]);
-  }
-  // per-block |Y| and output bases (scan over blocks, blocked arrangement)
-  uint32_t bsum = 0, ys[kVT];
-#pragma unroll
-  for (uint32_t v = 0; v < kVT; ++v) {
-    uint32_t b = tid * kVT + v;
-    ys[v] = 0;
-    if (b < nbc) ys[v] = (sm.bstart[b + 1] - sm.bstart[b]) - (sm.prs[sm.bstart[b + 1]] - sm.prs[sm.bstart[b]]);
-    bsum += 2 * ys[v];
-  }
-  uint32_t s2;
-  uint32_t ob = block_excl_scan(bsum, sm.scan, &s2);
-#pragma unroll
-  for (uint32_t v = 0; v < kVT; ++v) {
-    uint32_t b = tid * kVT + v;
-    if (b < nbc) {
-      sm.bobase[b] = ob;
-      sm.bysz[b] = ys[v];
+    for (uint32_t v = 0; v < kVT; ++v) {
+      out[v] = e;
+      const uint32_t b = (fl >> (8 * v)) & 0xffu;
+      e += (((b >> 1) & 1u) << 16) | ((b >> 2) & 1u);
     }
-    ob += 2 * ys[v];
+    reinterpret_cast<uint4*>(sm.pre)[tid] = make_uint4(out[0], out[1], out[2], out[3]);
+    if (tid == 0) sm.pre[kSeg] = tot;
   }
-  for (uint32_t i = tid; i < s2; i += kCta) sm.oemit[i] = 0;
   __syncthreads();
-  // values: Rx rule (engine.cpp:218-227 + term_map.hpp:77-79)
+  // scan 3 (blocked over blocks): |Y| per block and output bases
+  {
+    uint32_t bsum = 0, ys[kVT];
 #pragma unroll
-  for (uint32_t v = 0; v < kVT; ++v) {
-    uint32_t i = tid * kVT + v;
-    if (i >= Lc || ry[v] == kNone) continue;
-    const uint32_t b = sm.blk[i];
-    const uint32_t s0 = sm.bobase[b] + ry[v], s1 = s0 + sm.bysz[b];
+    for (uint32_t v = 0; v < kVT; ++v) {
+      const uint32_t b = tid * kVT + v;
+      ys[v] = 0;
+      if (b < nbc) {
+        const uint32_t bs = sm.bstart[b], be = sm.bstart[b + 1];
+        ys[v] = (be - bs) - ((sm.pre[be] >> 16) - (sm.pre[bs] >> 16));
+      }
+      bsum += 2 * ys[v];
+    }
+    uint32_t s2;
+    uint32_t ob = block_excl_scan(bsum, sm.scan, &s2);
+#pragma unroll
+    for (uint32_t v = 0; v < kVT; ++v) {
+      const uint32_t b = tid * kVT + v;
+      if (b < nbc) sm.bobase[b] = ob;
+      ob += 2 * ys[v];
+    }
+    if (tid == 0) sm.scan[33] = s2;
+  }
+  __syncthreads();
+  const uint32_t s2 = sm.scan[33];
+  // values: Rx rule (engine.cpp:218-227 + term_map.hpp:77-79); the owner of
+  // a coset (its class-0 string, or an unpaired class-1 string) fills both
+  // output slots.  Rank in Y = class-0 keys below + unpaired class-1 keys below.
+  for (uint32_t i = tid; i < Lc; i += kCta) {
+    const uint8_t fl = sm.f[i];
     Plane<W> k = sk_load<W>(sm.key, kSeg + 1, i);
+    const bool cls1 = (k.w[wq] & mq) != 0;
+    if (cls1 && !(fl & 4)) continue;  // paired class-1: its class-0 partner owns the coset
+    const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1], m = sm.bmid[b];
+    const uint32_t lb = sm.lbv[i];
+    const uint32_t um = sm.pre[m] & 0xffffu;
+    const uint32_t ry = cls1 ? (lb - bs) + ((sm.pre[i] & 0xffffu) - um) : (i - bs) + ((sm.pre[lb] & 0xffffu) - um);
+    const uint32_t ysz = (be - bs) - ((sm.pre[be] >> 16) - (sm.pre[bs] >> 16));
+    const uint32_t s0 = sm.bobase[b] + ry, s1 = s0 + ysz;
     const double c = sm.val[i];
     Plane<W> y = k, y1 = k;
     y.w[wq] &= ~mq;
     y1.w[wq] |= mq;
     double v0, v1;
     bool e0, e1;
-    if (!(k.w[wq] & mq)) {  // class 0 (Z at q): its child y|e_q gets +sin c0
+    if (!cls1) {  // Z at q: the child y|e_q gets +sin c0
       const double d1 = __dmul_rn(sinv, c);
       if (d1 != 0.0) ++records;
       double s = __dmul_rn(c, cosv);
-      if (pidx[v] != kNone) {
-        const double c1 = sm.val[pidx[v]];
+      if (fl & 2) {
+        const double c1 = sm.val[lb];
         const double d0 = __dmul_rn(nsin, c1);  // child of the Y partner lands on y
         if (d0 != 0.0) {
           ++records;
@@ -637,7 +626,7 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
       v0 = s;
       e0 = keep_zeros || s != 0.0;
       if (!e0) ++removed;
-    } else {  // class 1 (Y at q) without partner: child y gets -sin c1
+    } else {  // Y at q, no partner: the child y gets -sin c1
       const double d0 = __dmul_rn(nsin, c);
       if (d0 != 0.0) ++records;
       v0 = d0;
@@ -653,41 +642,44 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     sm.oval[s1] = v1;
     sm.oemit[s1] = e1;
   }
-  // every slot emitted (no exact zero, the common case): the slots are the
-  // compacted output already, stream them out coalesced without a scan
-  bool any_hole = false;
-  for (uint32_t i = tid; i < s2; i += kCta) any_hole |= !sm.oemit[i];
-  if (!__syncthreads_or(any_hole)) {
-    for (uint32_t i = tid; i < s2; i += kCta) {
-      const double val = sm.oval[i];
-      const uint64_t d = dst + out_n + i;
-      store_plane<W>(ar.x, d, sk_load<W>(sm.okey, 2 * kSeg, i));
-      ar.c[d] = val;
-      const double av = fabs(val);
-      if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
-      vmax = fmax(vmax, av);
-      vmin = fmin(vmin, av);
+  __syncthreads();
+  // compaction: holes are exact zeros (removed strings); one blocked scan
+  // over the emit bytes gives every slot its output position, then a
+  // coalesced store reads the slots in position order
+  constexpr uint32_t kSV = 2 * kSeg / kCta;
+  uint32_t ecnt;
+  {
+    const uint2 eb = reinterpret_cast<const uint2*>(sm.oemit)[tid];  // slots kSV tid .. kSV tid + 7
+    const uint32_t base = tid * kSV;
+    uint32_t m0 = 0;
+#pragma unroll
+    for (uint32_t v = 0; v < kSV; ++v) {
+      const uint32_t byte = v < 4 ? (eb.x >> (8 * v)) & 0xffu : (eb.y >> (8 * (v - 4))) & 0xffu;
+      if (base + v < s2 && byte) m0 |= 1u << v;
     }
-    out_n += s2;
-    return Lc;
-  }
-  for (uint32_t base = 0; base < s2; base += kCta) {
-    uint32_t sl = base + tid;
-    bool e = sl < s2 && sm.oemit[sl];
     uint32_t tot;
-    uint32_t o = block_excl_scan(e ? 1u : 0u, sm.scan, &tot);
-    if (e) {
-      const double val = sm.oval[sl];
-      const uint64_t d = dst + out_n + o;
-      store_plane<W>(ar.x, d, sk_load<W>(sm.okey, 2 * kSeg, sl));
-      ar.c[d] = val;
-      const double av = fabs(val);
-      if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
-      vmax = fmax(vmax, av);
-      vmin = fmin(vmin, av);
+    uint32_t o = block_excl_scan(__popc(m0), sm.scan, &tot);
+    ecnt = tot;
+    if (tot != s2) {
+#pragma unroll
+      for (uint32_t v = 0; v < kSV; ++v)
+        if ((m0 >> v) & 1u) sm.cpos[o++] = (uint16_t)(base + v);
     }
-    out_n += tot;
   }
+  __syncthreads();
+  const bool dense = ecnt == s2;
+  for (uint32_t i = tid; i < ecnt; i += kCta) {
+    const uint32_t sl = dense ? i : sm.cpos[i];
+    const double val = sm.oval[sl];
+    const uint64_t d = dst + out_n + i;
+    store_plane<W>(ar.x, d, sk_load<W>(sm.okey, 2 * kSeg, sl));
+    ar.c[d] = val;
+    const double av = fabs(val);
+    if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
+    vmax = fmax(vmax, av);
+    vmin = fmin(vmin, av);
+  }
+  out_n += ecnt;
   return Lc;
 }
 
