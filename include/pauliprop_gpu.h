@@ -68,6 +68,9 @@ extern "C" {
 /* pp_config.flags */
 #define PP_FLAG_NO_CLIFFORD_FUSION 1u /* apply Clifford gates one by one */
 #define PP_FLAG_PROFILE 2u            /* no CUDA graphs; time every branch launch */
+#define PP_FLAG_EXTERNAL_TRUNCATION 4u /* never truncate or check the budget itself: a
+                                          sharded orchestrator calls pp_truncate_threshold
+                                          with the global threshold */
 
 typedef struct pp_engine pp_engine;
 
@@ -129,6 +132,23 @@ int pp_take_kernel_stats(pp_engine* engine, double* branch_ms, double* branch_by
 /* The CUDA stream (cudaStream_t) the engine launches on, so callers can
  * bracket work with their own events. */
 void* pp_stream(const pp_engine* engine);
+
+/* ---- sharding (one engine per GPU; the orchestrator owns the collectives).
+ * owner(z) = pp_shard_owner: a hash of the string's z-plane.  An Rx gate keeps
+ * z, so it never moves strings between shards; after a Clifford/ZZ run or a
+ * Z/Y-carrying gate, pp_shard_evict removes every z-group owned elsewhere and
+ * returns it as records [x words, z words, coefficient bits] (pp_record_words
+ * words each) grouped by destination rank; the receiver merges them with
+ * pp_shard_ingest (equal keys combine exactly like TermMap::add).  The
+ * reference's distribution is the block-sum map (partition.cpp:53-59) over
+ * in-process workers (engine.hpp:126-130); results never depend on it. */
+int pp_local_stats(pp_engine* engine, double* gmax, uint32_t* nonfinite, uint64_t* count);
+int pp_truncate_threshold(pp_engine* engine, double threshold, uint64_t* removed);
+int pp_record_words(const pp_engine* engine);
+int pp_shard_evict(pp_engine* engine, uint32_t world, uint32_t rank, uint64_t seed, uint64_t* records,
+                   uint64_t cap, uint64_t* counts);
+int pp_shard_ingest(pp_engine* engine, const uint64_t* records, uint64_t count);
+uint32_t pp_shard_owner(const uint64_t* words, int n, uint64_t seed, uint32_t world);
 
 #ifdef __cplusplus
 }

@@ -150,6 +150,8 @@ def _oracle_lib():
         L.ppo_take_counters.argtypes = [_vp, _vp]
         L.ppo_angle.argtypes = [_dbl, _int, _vp, _vp, _vp]
         L.ppo_phase_exponent.argtypes = [_vp, _vp, _int]
+        L.ppo_truncate_threshold.restype = _u64
+        L.ppo_truncate_threshold.argtypes = [_vp, _dbl]
         _olib = L
     return _olib
 
@@ -194,6 +196,9 @@ class OracleEngine:
 
     def truncate_now(self):
         self._check(self.L.ppo_truncate_now(self.h))
+
+    def truncate_threshold(self, threshold):
+        return int(self.L.ppo_truncate_threshold(self.h, float(threshold)))
 
     def _check(self, rc):
         if rc:

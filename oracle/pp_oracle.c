@@ -238,6 +238,14 @@ int ppo_truncate_now(ppo_engine* e) {
   return PPO_OK;
 }
 
+/* remove_below at an explicit threshold (a sharded run's global
+ * epsilon0 * gmax); returns the removed count. */
+uint64_t ppo_truncate_threshold(ppo_engine* e, double threshold) {
+  size_t r = store_remove_below(&e->store, threshold);
+  e->removed += r;
+  return (uint64_t)r;
+}
+
 /* Engine::apply_gate, engine.cpp:277-316, with generate_phase (207-247)
  * and apply_phase (249-264) for a single worker. */
 int ppo_apply_gate(ppo_engine* e, const uint64_t* gen, double cos_t,

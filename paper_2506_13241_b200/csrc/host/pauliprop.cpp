@@ -573,7 +573,8 @@ Engine::Engine(const EngineConfig& config) : config_(config) {
   c.max_terms = config.max_terms;
   c.workers = config.partition.worker_count;
   c.device = config.device;
-  c.flags = (config.fuse_clifford ? 0u : PP_FLAG_NO_CLIFFORD_FUSION) | (config.profile ? PP_FLAG_PROFILE : 0u);
+  c.flags = (config.fuse_clifford ? 0u : PP_FLAG_NO_CLIFFORD_FUSION) | (config.profile ? PP_FLAG_PROFILE : 0u) |
+            (config.external_truncation ? PP_FLAG_EXTERNAL_TRUNCATION : 0u);
   c.mem_fraction = 0.0;
   int rc = pp_create(&c, &handle_);
   if (rc != PP_OK) {

@@ -168,6 +168,7 @@ struct EngineConfig {
   int device = 0;
   bool fuse_clifford = true;
   bool profile = false;  // no CUDA graphs, per-launch kernel timing
+  bool external_truncation = false;  // sharded: the orchestrator truncates with a global threshold
 };
 
 // Host copy of the operator (what Engine::merged() returns).

@@ -230,6 +230,13 @@ class EngineBase {
   virtual pp_counters take_counters() = 0;
   virtual void take_kernel_stats(double* ms, double* bytes, uint64_t* launches, uint64_t* total) = 0;
   virtual void* stream() const = 0;
+  // sharding hooks (multi-GPU orchestration)
+  virtual void local_stats(double* gmax, uint32_t* nonfinite, uint64_t* count) = 0;
+  virtual uint64_t truncate_threshold(double T) = 0;
+  virtual int record_words() const = 0;
+  virtual void shard_evict(uint32_t world, uint32_t rank, uint64_t seed, uint64_t* out, uint64_t cap,
+                           uint64_t* counts) = 0;
+  virtual void shard_ingest(const uint64_t* rec, uint64_t count) = 0;
 };
 
 template <int W>
@@ -416,8 +423,8 @@ class EngineImpl final : public EngineBase {
       prm[i].cosv = gates[i].cos_theta;
       prm[i].sinv = gates[i].sin_theta;
     }
-    const bool budget = cfg_.max_terms != 0;
-    const bool epi = !(cfg_.epsilon0 == 0.0 && !budget && !may_hold_zeros_);
+    const bool budget = cfg_.max_terms != 0 && !external();
+    const bool epi = !external() && !(cfg_.epsilon0 == 0.0 && !budget && !may_hold_zeros_);
     const bool do_trunc = cfg_.cadence == PP_CADENCE_GATE;
     const uint64_t seq0 = bseq_;
     size_t pos = 0;
@@ -452,7 +459,7 @@ class EngineImpl final : public EngineBase {
       branch_launches_ += count - pos;
       if (keep_zeros_) may_hold_zeros_ = true;
       if (epi && do_trunc) truncated_since_sync_ = true;
-      if (!epi && do_trunc) gmax_stale_ = true;
+      if (!epi && do_trunc && !external()) gmax_stale_ = true;
       dirty_ = true;
       sync_state();
       if (!arena_fault_) break;
@@ -670,6 +677,114 @@ class EngineImpl final : public EngineBase {
 
   void* stream() const override { return (void*)stream_; }
 
+  // ---------------------------------------------------------------- sharding
+  void local_stats(double* gmax, uint32_t* nonfinite, uint64_t* count) override {
+    dirty_ = true;
+    sync_state();
+    *gmax = __builtin_bit_cast(double, h_stats_->red[2].gmax_bits);
+    *nonfinite = h_stats_->red[2].nonfinite;
+    *count = live_;
+  }
+
+  uint64_t truncate_threshold(double T) override {
+    sync_state();
+    const uint64_t before = counters_.removed;
+    if (G_) {
+      push_scalars(bseq_);
+      k_truncate_T<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), aview(cur_), T, d_stats_);
+      ++launches_;
+      dirty_ = true;
+      sync_state();
+    }
+    gmax_ = T;  // informational; the orchestrator keeps the global max
+    return counters_.removed - before;
+  }
+
+  int record_words() const override { return 2 * W + 1; }
+
+  void shard_evict(uint32_t world, uint32_t rank, uint64_t seed, uint64_t* out, uint64_t cap,
+                   uint64_t* counts) override {
+    sync_state();
+    for (uint32_t d = 0; d < world; ++d) counts[d] = 0;
+    if (G_ == 0) return;
+    evict_cnt_.ensure(world * 8 * 2);
+    unsigned long long* dcnt = evict_cnt_.as<unsigned long long>();
+    PP_CUDA(cudaMemsetAsync(dcnt, 0, world * 8, stream_));
+    k_evict_count<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, world, rank, seed, dcnt);
+    std::vector<unsigned long long> hc(world);
+    PP_CUDA(cudaMemcpyAsync(hc.data(), dcnt, world * 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaStreamSynchronize(stream_));
+    uint64_t total = 0;
+    std::vector<unsigned long long> off(world);
+    for (uint32_t d = 0; d < world; ++d) {
+      off[d] = total;
+      total += hc[d];
+      counts[d] = hc[d];
+    }
+    if (total > cap) throw EngineError(PP_ERR_INVALID, "evict: output capacity too small");
+    if (total == 0) return;
+    const int rw = 2 * W + 1;
+    evict_buf_.ensure(total * rw * 8);
+    PP_CUDA(cudaMemcpyAsync(dcnt + world, off.data(), world * 8, cudaMemcpyHostToDevice, stream_));
+    k_evict_write<W><<<G_, kCta, 0, stream_>>>(gview(gcur_), aview(cur_), world, rank, seed, dcnt + world,
+                                               evict_buf_.as<uint64_t>());
+    PP_CUDA(cudaMemcpyAsync(out, evict_buf_.p, total * rw * 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaStreamSynchronize(stream_));
+    launches_ += 2;
+    dirty_ = true;
+    sync_state();
+  }
+
+  void shard_ingest(const uint64_t* rec, uint64_t count) override {
+    sync_state();
+    if (count == 0) return;
+    const int rw = 2 * W + 1;
+    if (bump_ + count > arena_[cur_].cap) gc_into_other(std::max<uint64_t>(next_arena_target(), live_ + 2 * count));
+    evict_buf_.ensure(count * rw * 8);
+    PP_CUDA(cudaMemcpyAsync(evict_buf_.p, rec, count * rw * 8, cudaMemcpyHostToDevice, stream_));
+    rec_slot_.ensure(count * 4);
+    uint32_t* flags = rec_slot_.as<uint32_t>();
+    k_run_starts<<<(uint32_t)((count + kCta - 1) / kCta), kCta, 0, stream_>>>(evict_buf_.as<uint64_t>(), count, W, W,
+                                                                                flags);
+    const uint64_t ntiles = (count + kScanTile - 1) / kScanTile;
+    scan_tmp_.ensure((ntiles + 1) * 8);
+    scan_gid_.ensure(count * 8);
+    device_scan(flags, count, 1, scan_gid_.as<unsigned long long>(), ntiles);
+    unsigned long long nruns = 0;
+    PP_CUDA(cudaMemcpyAsync(&nruns, scan_tmp_.as<unsigned long long>() + ntiles, 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaStreamSynchronize(stream_));
+    grow_groups_preserving(G_ + (uint32_t)nruns);
+    k_ingest_append<W><<<(uint32_t)((count + kCta - 1) / kCta), kCta, 0, stream_>>>(
+        evict_buf_.as<uint64_t>(), count, scan_gid_.as<unsigned long long>(), gview(gcur_), G_, aview(cur_), bump_);
+    k_ingest_counts<W><<<blocks(nruns), kCta, 0, stream_>>>(gview(gcur_), G_, (uint32_t)nruns, bump_ + count);
+    launches_ += 3;
+    G_ += (uint32_t)nruns;
+    bump_ += count;
+    live_ += count;
+    bump_bound_ = bump_;
+    live_bound_ = live_;
+    reset_stats(bump_);
+    IdentityProducer<W> p;
+    regroup(p);  // merge groups sharing a z, sort by x, combine equal keys
+    dirty_ = true;
+  }
+
+  void grow_groups_preserving(uint32_t cap) {
+    if (groups_[gcur_].cap >= cap) return;
+    const int o = 1 - gcur_;
+    ensure_groups(o, std::max<uint32_t>(cap, 2 * groups_[gcur_].cap));
+    GroupView<W> a = gview(gcur_), b = gview(o);
+    for (int k = 0; k < W; ++k) PP_CUDA(cudaMemcpyAsync(b.z[k], a.z[k], G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(b.off, a.off, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(b.gmax, a.gmax, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(b.gmin, a.gmin, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(b.cnt, a.cnt, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(b.cap, a.cap, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(b.flags, a.flags, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(b.stamp, a.stamp, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
+    gcur_ = o;
+  }
+
   pp_counters take_counters() override {
     sync_state();
     pp_counters out = counters_;
@@ -788,7 +903,12 @@ class EngineImpl final : public EngineBase {
   // Budget check, NaN check and truncation run on the device (k_truncate),
   // so consecutive gates need no host round trip; the host synchronises only
   // when it needs exact sizes (sync_state).
+  bool external() const { return (cfg_.flags & PP_FLAG_EXTERNAL_TRUNCATION) != 0; }
   void epilogue(bool do_truncate, bool check_budget) {
+    if (external()) {  // the orchestrator truncates with a global threshold
+      dirty_ = true;
+      return;
+    }
     const bool budget = check_budget && cfg_.max_terms;
     // With epsilon0 == 0 the threshold is 0: only exact zeros go, and the
     // branch/regroup kernels never emit zeros (cadence gate), so unless the
@@ -836,7 +956,7 @@ class EngineImpl final : public EngineBase {
     }
     arena_fault_ = st.err_arena != 0;
     arena_fault_seq_ = st.err_seq;
-    if (st.red[2].nonfinite && gmax_stale_) {
+    if (st.red[2].nonfinite && gmax_stale_ && !external()) {
       dirty_ = false;
       throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient detected at gate " + std::to_string(gates_applied_) +
                                               ", |O|=" + std::to_string(st.red[2].live));
@@ -1142,6 +1262,7 @@ class EngineImpl final : public EngineBase {
   cudaEvent_t ev0_, ev1_;
   Arena arena_[2];
   Groups groups_[2];
+  DevBuf evict_cnt_, evict_buf_;
   DevBuf stats_buf_, list_, items_, rec_slot_, table_, scan_tmp_, scan_gid_, scan_off_, diag_z_, diag_c_, cliff_;
   int cur_ = 0, gcur_ = 0;
   uint32_t G_ = 0;
@@ -1299,6 +1420,46 @@ int pp_take_kernel_stats(pp_engine* e, double* branch_ms, double* branch_bytes, 
 }
 
 void* pp_stream(const pp_engine* e) { return e ? e->impl->stream() : nullptr; }
+
+int pp_local_stats(pp_engine* e, double* gmax, uint32_t* nonfinite, uint64_t* count) {
+  if (!e || !gmax || !nonfinite || !count) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->local_stats(gmax, nonfinite, count); });
+}
+
+int pp_truncate_threshold(pp_engine* e, double threshold, uint64_t* removed) {
+  if (!e) return PP_ERR_INVALID;
+  return guarded(e, [&] {
+    uint64_t r = e->impl->truncate_threshold(threshold);
+    if (removed) *removed = r;
+  });
+}
+
+int pp_record_words(const pp_engine* e) { return e ? e->impl->record_words() : 0; }
+
+int pp_shard_evict(pp_engine* e, uint32_t world, uint32_t rank, uint64_t seed, uint64_t* records, uint64_t cap,
+                   uint64_t* counts) {
+  if (!e || !counts || world == 0 || rank >= world) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->shard_evict(world, rank, seed, records, cap, counts); });
+}
+
+int pp_shard_ingest(pp_engine* e, const uint64_t* records, uint64_t count) {
+  if (!e || (!records && count)) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->shard_ingest(records, count); });
+}
+
+uint32_t pp_shard_owner(const uint64_t* words, int n, uint64_t seed, uint32_t world) {
+  uint64_t x[2], z[2];
+  ppgpu::words_to_planes(words, x, z);
+  if (n <= 64) {
+    ppgpu::Plane<1> p;
+    p.w[0] = z[0];
+    return ppgpu::shard_owner<1>(p, seed, world);
+  }
+  ppgpu::Plane<2> p;
+  p.w[0] = z[0];
+  p.w[1] = z[1];
+  return ppgpu::shard_owner<2>(p, seed, world);
+}
 
 const char* pp_last_error(const pp_engine* e) { return e ? e->error.c_str() : g_create_error.c_str(); }
 

@@ -988,6 +988,19 @@ __global__ void __launch_bounds__(kCta) k_truncate(GroupView<W> g, ArenaView<W> 
   }
 }
 
+// truncation at an externally supplied threshold (sharded engines: T comes
+// from epsilon0 times the max over all shards)
+template <int W>
+__global__ void __launch_bounds__(kCta) k_truncate_T(GroupView<W> g, ArenaView<W> ar, double T, DevStats* st) {
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  __shared__ uint32_t scan[40];
+  __shared__ double rmx[kWarps], rmn[kWarps];
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+    if (g.cnt[gid] == 0 || !(g.gmin[gid] <= T)) continue;  // uniform per CTA
+    truncate_group<W>(g, ar, gid, T, st, scan, rmx, rmn);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // diagonal strings (x == 0 is the smallest key of a group, so it can only be
 // the first element): <0|O|0> terms (sparse_operator.cpp:32-36, 89-97)

@@ -148,6 +148,120 @@ struct ZZRunProducer {
   }
 };
 
+// (c) identity: regroup the store as it is (merges groups that share a z,
+// e.g. after strings received from other shards were appended as groups;
+// equal keys are combined by the sort pass).
+template <int W>
+struct IdentityProducer {
+  static constexpr int kMaxRec = 1;
+  __device__ __forceinline__ int emit(Plane<W> x, Plane<W> z, double c, Record<W>* out, uint32_t* nrec) const {
+    out[0].x = x;
+    out[0].z = z;
+    out[0].c = c;
+    *nrec = 0;
+    return 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// sharding (multi-GPU): owner(z) is a hash of the z-plane, so an Rx gate
+// (which keeps z) never moves a string between shards; Clifford/ZZ gates do,
+// and whole z-groups are evicted to their new owner after a regroup.
+// ---------------------------------------------------------------------------
+template <int W>
+__host__ __device__ __forceinline__ uint32_t shard_owner(const Plane<W>& z, uint64_t seed, uint32_t world) {
+  uint64_t h = mix64(z.w[0] ^ seed);
+  if (W == 2) h = mix64(h ^ z.w[W - 1]);
+  return (uint32_t)(h % world);
+}
+
+template <int W>
+__global__ void k_evict_count(GroupView<W> g, uint32_t G, uint32_t world, uint32_t rank, uint64_t seed,
+                              unsigned long long* counts) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G || g.cnt[i] == 0) return;
+  uint32_t d = shard_owner<W>(load_plane<W>(g.z, i), seed, world);
+  if (d != rank) atomicAdd(&counts[d], (unsigned long long)g.cnt[i]);
+}
+
+// writes every string of every group owned elsewhere as a record
+// [x words, z words, coefficient bits] at its destination's cursor, then
+// empties the group
+template <int W>
+__global__ void __launch_bounds__(kCta) k_evict_write(GroupView<W> g, ArenaView<W> ar, uint32_t world, uint32_t rank,
+                                                      uint64_t seed, unsigned long long* cursor, uint64_t* out) {
+  const uint32_t gid = blockIdx.x;
+  const uint32_t n = g.cnt[gid];
+  if (n == 0) return;
+  const Plane<W> z = load_plane<W>(g.z, gid);
+  const uint32_t d = shard_owner<W>(z, seed, world);
+  if (d == rank) return;
+  __shared__ unsigned long long base_s;
+  if (threadIdx.x == 0) base_s = atomicAdd(&cursor[d], (unsigned long long)n);
+  __syncthreads();
+  const uint64_t off = g.off[gid];
+  for (uint32_t i = threadIdx.x; i < n; i += kCta) {
+    uint64_t* r = out + (base_s + i) * (2 * W + 1);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      r[k] = ar.x[k][off + i];
+      r[W + k] = z.w[k];
+    }
+    r[2 * W] = (uint64_t)__double_as_longlong(ar.c[off + i]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) g.cnt[gid] = 0;
+}
+
+// appends received records to the arena as one group per run of equal z
+// (run starts flagged in `start`, group ids from an exclusive scan `gid`)
+template <int W>
+__global__ void k_ingest_append(const uint64_t* rec, uint64_t count, const unsigned long long* gidscan, GroupView<W> g,
+                                uint32_t G0, ArenaView<W> ar, uint64_t base) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t* r = rec + i * (2 * W + 1);
+#pragma unroll
+  for (int k = 0; k < W; ++k) ar.x[k][base + i] = r[k];
+  ar.c[base + i] = __longlong_as_double((long long)r[2 * W]);
+  bool start = i == 0;
+  if (!start) {
+    const uint64_t* q = rec + (i - 1) * (2 * W + 1);
+#pragma unroll
+    for (int k = 0; k < W; ++k) start |= q[W + k] != r[W + k];
+  }
+  if (start) {
+    uint32_t gi = G0 + (uint32_t)gidscan[i];
+#pragma unroll
+    for (int k = 0; k < W; ++k) g.z[k][gi] = r[W + k];
+    g.off[gi] = base + i;
+    g.gmax[gi] = 0.0;
+    g.gmin[gi] = 0.0;
+    g.flags[gi] = 0;
+    g.stamp[gi] = 0xffffffffu;
+  }
+}
+
+// group sizes of the appended runs from consecutive offsets
+template <int W>
+__global__ void k_ingest_counts(GroupView<W> g, uint32_t G0, uint32_t nruns, uint64_t end) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nruns) return;
+  const uint32_t gi = G0 + j;
+  const uint64_t next = j + 1 < nruns ? g.off[gi + 1] : end;
+  g.cnt[gi] = (uint32_t)(next - g.off[gi]);
+  g.cap[gi] = g.cnt[gi];
+}
+
+__global__ void k_run_starts(const uint64_t* rec, uint64_t count, int words, int zoff, uint32_t* flag) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  bool start = i == 0;
+  if (!start)
+    for (int k = 0; k < words; ++k) start |= rec[(i - 1) * (2 * words + 1) + zoff + k] != rec[i * (2 * words + 1) + zoff + k];
+  flag[i] = start ? 1u : 0u;
+}
+
 // (b) one general gate: parent scaled by cos when it anticommutes, plus the
 // child (I xor J, (+-sin) c) when the increment is nonzero (engine.cpp:
 // 218-245).
