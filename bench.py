@@ -192,6 +192,71 @@ def run_reference_arm(args, wl, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, pp, circ, wl, sg, final_terms, init, rank, world, local):
+    """N > 1: the operator is sharded over the ranks by z-plane hash
+    (paper_2506_13241_b200/sharded.py); total work fixed -> strong scaling.
+    Device time per step = CUDA events on this rank's engine stream, max over
+    ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2506_13241_b200.sharded import GpuShard, ShardedEngine, TorchComm
+
+    n, eps = wl[1], wl[5]
+    gloo = dist.new_group(backend="gloo")  # host-staged exchange
+    comm = TorchComm(gloo)
+
+    def one_step():
+        shard = GpuShard(n, eps, "gate", device=local)
+        se = ShardedEngine(shard, n, comm, eps, "gate")
+        stream = torch.cuda.ExternalStream(shard.engine.stream_ptr(), device=local)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        t0 = time.perf_counter()
+        se.set_initial(init, np.array([1.0]))
+        rows = se.run_circuit(circ)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        return rows, e0.elapsed_time(e1), wall, se.exchanged_records
+
+    for _ in range(args.warmup):
+        one_step()
+    ms, walls, moved = [], [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            rows, m, w, mv = one_step()
+            ms.append(m)
+            walls.append(w)
+            moved += mv
+    assert rows[-1]["term_count"] == final_terms
+    t = torch.tensor([sum(ms), sum(walls)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
+    ms_per_step = float(t[0]) / args.steps
+    wall_per_step = float(t[1]) / args.steps
+    mv = torch.tensor([float(moved)], dtype=torch.float64)
+    dist.all_reduce(mv, group=gloo)
+    if rank == 0:
+        line = {
+            "metric": "string_gates_per_s", "value": sg / (ms_per_step / 1e3), "unit": "string-gates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic kicked-Ising circuit, BASELINE config)",
+            "config": {"workload": args.workload, "string_gates_per_step": sg, "final_terms": final_terms,
+                       "parallelism": f"z-hash shards x{world}", "exchange": "host-staged (gloo)",
+                       "records_exchanged_per_step": float(mv[0]) / args.steps},
+            "e2e": {"value": sg / wall_per_step, "unit": "string-gates/s", "h2d_bytes_per_step": 40,
+                    "d2h_bytes_per_step": 8 * 4 * circ.num_layers(), "api": "ShardedEngine.run_circuit"},
+            "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -214,9 +279,14 @@ def main():
     import numpy as np
     import torch
     import torch.distributed as dist
+    if os.environ.get("PP_BENCH_PG") == "gloo":  # test hook: several ranks sharing one GPU
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PP_BENCH_PG") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2506_13241_b200 as pp
 
@@ -225,6 +295,9 @@ def main():
     sg, final_terms = string_gates(pp, circ, wl)
     init = np.zeros((1, 4), np.uint64)
     init[0, site // 32] = np.uint64(3) << np.uint64(2 * (site % 32))
+    if world > 1:
+        run_sharded(args, pp, circ, wl, sg, final_terms, init, rank, world, local)
+        return
 
     # ---------------- device-resident value: CUDA events on the engine stream
     eng = pp.Engine(n, eps, device=local)
