@@ -40,6 +40,7 @@ WORKLOADS = {
     "config1": ("heavy_hex", 127, "0.25pi", "-0.5pi", 62, 0.0, 5),
     "config0_t8": ("chain64", 64, 0.3, "-0.5pi", 32, 0.0, 8),
     "config0_t9": ("chain64", 64, 0.3, "-0.5pi", 32, 0.0, 9),
+    "config0_t10": ("chain64", 64, 0.3, "-0.5pi", 32, 0.0, 10),
     "config2_pi4_eps1e-4_t8": ("heavy_hex", 127, "0.25pi", "-0.5pi", 62, 1e-4, 8),
 }
 

@@ -150,6 +150,10 @@ int pp_shard_evict(pp_engine* engine, uint32_t world, uint32_t rank, uint64_t se
 int pp_shard_ingest(pp_engine* engine, const uint64_t* records, uint64_t count);
 uint32_t pp_shard_owner(const uint64_t* words, int n, uint64_t seed, uint32_t world);
 
+/* Sum of squared coefficients (conserved at epsilon0 = 0; property checks at
+ * sizes the oracle cannot reach). */
+int pp_norm2(pp_engine* engine, double* out);
+
 #ifdef __cplusplus
 }
 #endif

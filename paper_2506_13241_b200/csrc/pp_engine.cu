@@ -237,6 +237,7 @@ class EngineBase {
   virtual void shard_evict(uint32_t world, uint32_t rank, uint64_t seed, uint64_t* out, uint64_t cap,
                            uint64_t* counts) = 0;
   virtual void shard_ingest(const uint64_t* rec, uint64_t count) = 0;
+  virtual double norm2() = 0;
 };
 
 template <int W>
@@ -701,6 +702,20 @@ class EngineImpl final : public EngineBase {
   }
 
   int record_words() const override { return 2 * W + 1; }
+
+  double norm2() override {
+    sync_state();
+    if (G_ == 0) return 0.0;
+    evict_cnt_.ensure(64);
+    double* acc = evict_cnt_.as<double>();
+    PP_CUDA(cudaMemsetAsync(acc, 0, 8, stream_));
+    push_scalars(bseq_);
+    k_norm2<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), aview(cur_), d_stats_, acc);
+    double h = 0.0;
+    PP_CUDA(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaStreamSynchronize(stream_));
+    return h;
+  }
 
   void shard_evict(uint32_t world, uint32_t rank, uint64_t seed, uint64_t* out, uint64_t cap,
                    uint64_t* counts) override {
@@ -1435,6 +1450,11 @@ int pp_truncate_threshold(pp_engine* e, double threshold, uint64_t* removed) {
 }
 
 int pp_record_words(const pp_engine* e) { return e ? e->impl->record_words() : 0; }
+
+int pp_norm2(pp_engine* e, double* out) {
+  if (!e || !out) return PP_ERR_INVALID;
+  return guarded(e, [&] { *out = e->impl->norm2(); });
+}
 
 int pp_shard_evict(pp_engine* e, uint32_t world, uint32_t rank, uint64_t seed, uint64_t* records, uint64_t cap,
                    uint64_t* counts) {

@@ -1001,6 +1001,31 @@ __global__ void __launch_bounds__(kCta) k_truncate_T(GroupView<W> g, ArenaView<W
   }
 }
 
+// sum of c^2 over the store (Frobenius norm^2 / 2^n: conserved exactly at
+// epsilon0 = 0 -- a size-independent property check, test_engine.cpp:260-304)
+template <int W>
+__global__ void __launch_bounds__(kCta) k_norm2(GroupView<W> g, ArenaView<W> ar, const DevStats* st, double* out) {
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  double acc = 0.0;
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+    const uint32_t n = g.cnt[gid];
+    const uint64_t off = g.off[gid];
+    for (uint32_t i = threadIdx.x; i < n; i += kCta) {
+      const double c = ar.c[off + i];
+      acc = fma(c, c, acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[kWarps];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < kWarps; ++w) acc += red[w];
+    atomicAdd(out, acc);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // diagonal strings (x == 0 is the smallest key of a group, so it can only be
 // the first element): <0|O|0> terms (sparse_operator.cpp:32-36, 89-97)
