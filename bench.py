@@ -331,6 +331,9 @@ def main():
     ks = eng.kernel_stats()
     assert rows[-1]["term_count"] == final_terms
     # roofline pass (untimed): no graphs, CUDA events around every branch launch
+    del eng, stream  # its device buffers return to the engine's pool for reuse
+    import gc
+    gc.collect()
     peng = pp.Engine(n, eps, device=local, profile=True)
     peng.set_initial(init, np.array([1.0]))
     peng.kernel_stats()
