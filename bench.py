@@ -412,7 +412,13 @@ def main():
                          "branch_ms_per_step": pks["branch_ms"],
                          "branch_bytes_per_step": pks["branch_bytes"],
                          "branch_launches_per_step": pks["branch_launches"],
-                         "how": "separate untimed pass, CUDA events around each k_branch_x launch"},
+                         "how": "separate untimed pass, CUDA events around each k_branch_x launch",
+                         # SURVEY.md 8d streaming model: R(n) (|O_in| + |O_out|) bytes per
+                         # branching gate ~ 2 R(n) per string-gate, R(n) = 16 ceil(n/64) + 8
+                         "streaming_model": {
+                             "bytes_per_string_gate": 2 * (16 * ((n + 63) // 64) + 8),
+                             "equivalent_GBps": value * 2 * (16 * ((n + 63) // 64) + 8) / 1e9,
+                             "frac": value * 2 * (16 * ((n + 63) // 64) + 8) / 1e9 / peak}},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(round(launches_per_step * args.steps)),
