@@ -253,6 +253,8 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaEventCreate(&ev1_));
     PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)branch_smem_bytes<W>()));
+    PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)branch_smem_bytes<W>()));
     PP_CUDA(cudaFuncSetAttribute(k_sort_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(SortSmem<W>)));
     PP_CUDA(cudaFuncSetAttribute(k_sort_big<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -428,6 +430,48 @@ class EngineImpl final : public EngineBase {
     const bool epi = !external() && !(cfg_.epsilon0 == 0.0 && !budget && !may_hold_zeros_);
     const bool do_trunc = cfg_.cadence == PP_CADENCE_GATE;
     const uint64_t seq0 = bseq_;
+    // epsilon0 = 0 (no global threshold), no budget: the whole run in one
+    // launch, every group through its gates (k_branch_sublayer)
+    if (!epi && count <= (size_t)kMaxSubGates && G_) {
+      SubGates sgates{};
+      sgates.ng = (int)count;
+      for (size_t i = 0; i < count; ++i) {
+        sgates.wq[i] = (int8_t)prm[i].wq;
+        sgates.mq[i] = prm[i].mq;
+        sgates.cosv[i] = prm[i].cosv;
+        sgates.sinv[i] = prm[i].sinv;
+        sgates.any[prm[i].wq] |= prm[i].mq;
+      }
+      for (int attempt = 0;; ++attempt) {
+        sync_state();
+        if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
+        push_scalars(seq0);
+        std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
+        PP_CUDA(cudaEventRecord(ev.first, stream_));
+        k_branch_sublayer<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+            gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_stats_);
+        PP_CUDA(cudaEventRecord(ev.second, stream_));
+        pending_events_.push_back(ev);
+        ++launches_;
+        ++branch_launches_;
+        if (keep_zeros_) may_hold_zeros_ = true;
+        if (do_trunc && !external()) gmax_stale_ = true;
+        dirty_ = true;
+        sync_state();
+        if (!arena_fault_) break;
+        if (attempt > 64) throw EngineError(PP_ERR_RESOURCE, "arena cannot hold the sublayer");
+        k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
+        ++launches_;
+        arena_fault_ = false;
+        gc_into_other(next_arena_target());  // groups resume after their stamps
+      }
+      bseq_ = seq0 + count;
+      gates_applied_ += count;
+      counters_.gates += count;
+      counters_.batches_sent += count;
+      counters_.branch_ns += ns_since(t0);
+      return;
+    }
     size_t pos = 0;
     while (pos < count && G_) {
       sync_state();

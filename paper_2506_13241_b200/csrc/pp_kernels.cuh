@@ -836,6 +836,138 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
 }
 
+// ---------------------------------------------------------------------------
+// K_sublayer: a whole run of X-type gates in ONE launch, for epsilon0 = 0.
+// Under X-type gates z-groups evolve independently; the only coupling
+// between them in the reference is the per-gate global max, and a threshold
+// of 0 * gmax = 0 does not depend on it (exact zeros are dropped as they
+// appear).  So each CTA takes a group and applies every gate of the run that
+// touches it, in order.  g.stamp = sequence number of the last gate applied:
+// after an arena overflow the host compacts and relaunches, and each group
+// resumes after its stamp.
+// ---------------------------------------------------------------------------
+constexpr int kMaxSubGates = 128;
+struct SubGates {
+  int ng;
+  int8_t wq[kMaxSubGates];
+  uint64_t mq[kMaxSubGates];
+  double cosv[kMaxSubGates];
+  double sinv[kMaxSubGates];
+  uint64_t any[2];  // union of the gate masks per plane word
+};
+
+template <int W>
+__global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
+                                                           int keep_zeros, unsigned int* work, DevStats* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
+  SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  if (engine_failed(st)) return;
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  const unsigned long long cap = *(volatile const unsigned long long*)&st->arena_cap;
+  const uint32_t seq0 = (uint32_t)(*(volatile const unsigned long long*)&st->seq_base);
+  __shared__ unsigned long long dst_s;
+  __shared__ uint32_t s_gid, s_fail;
+  __shared__ double red_max[kWarps], red_min[kWarps];
+  __shared__ unsigned long long red_rec[kWarps], red_rem[kWarps];
+  __shared__ uint32_t red_nf[kWarps];
+  unsigned long long aff_elems = 0;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_gid = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t gid = s_gid;
+    if (gid >= G) break;
+    Plane<W> z;
+#pragma unroll
+    for (int k = 0; k < W; ++k) z.w[k] = g.z[k][gid];
+    bool touched = false;
+#pragma unroll
+    for (int k = 0; k < W; ++k) touched |= (z.w[k] & gates.any[k]) != 0;
+    if (!touched || g.cnt[gid] == 0) continue;
+    const uint32_t stamp = g.stamp[gid];
+    int k0 = (stamp - seq0 < (uint32_t)gates.ng) ? (int)(stamp - seq0) + 1 : 0;  // resume after the stamp
+    for (int k = k0; k < gates.ng; ++k) {
+      const int wq = gates.wq[k];
+      const uint64_t mq = gates.mq[k];
+      if (!(z.w[wq] & mq)) continue;
+      const uint32_t n = g.cnt[gid];
+      if (n == 0) break;
+      const uint64_t src = g.off[gid];
+      __syncthreads();
+      if (tid == 0) {
+        dst_s = atomicAdd(&st->bump, 2ull * n);
+        s_fail = dst_s + 2ull * n > cap;
+        if (s_fail) {
+          atomicOr(&st->err_arena, 1u);
+          atomicMin(&st->err_seq, (unsigned long long)(seq0 + k));
+        }
+      }
+      __syncthreads();
+      if (s_fail) break;  // group stays after gate k-1 (its stamp); the host compacts and relaunches
+      const uint64_t dst = dst_s;
+      aff_elems += n;
+      uint32_t out_n = 0;
+      double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);
+      uint32_t nonfinite = 0;
+      unsigned long long records = 0, removed = 0;
+      const double cosv = gates.cosv[k], sinv = gates.sinv[k];
+      uint32_t p = 0;
+      while (p < n) {
+        uint32_t used = seg_branch<W>(sg, ar, src, p, n, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
+                                      nonfinite, records, removed);
+        if (used) {
+          p += used;
+          continue;
+        }
+        __syncthreads();
+        const uint32_t be = find_block_end<W>(ar, src, p, n, wq, mq, nullptr);
+        if (tid == 0) atomicAdd(&st->stream_elems, (unsigned long long)(be - p));
+        stream_branch_range<W>(sm, ar, src + p, be - p, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
+                               nonfinite, records, removed);
+        p = be;
+      }
+      vmax = warp_max(vmax);
+      vmin = warp_min(vmin);
+      records = warp_sum64(records);
+      removed = warp_sum64(removed);
+      nonfinite = __any_sync(0xffffffffu, nonfinite);
+      const uint32_t lane = tid & 31, warp = tid >> 5;
+      __syncthreads();
+      if (lane == 0) {
+        red_max[warp] = vmax;
+        red_min[warp] = vmin;
+        red_rec[warp] = records;
+        red_rem[warp] = removed;
+        red_nf[warp] = nonfinite;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (uint32_t w = 1; w < kWarps; ++w) {
+          vmax = fmax(vmax, red_max[w]);
+          vmin = fmin(vmin, red_min[w]);
+          records += red_rec[w];
+          removed += red_rem[w];
+          nonfinite |= red_nf[w];
+        }
+        g.off[gid] = dst;
+        g.cnt[gid] = out_n;
+        g.cap[gid] = 2 * n;
+        g.gmax[gid] = out_n ? vmax : 0.0;
+        g.gmin[gid] = out_n ? vmin : __longlong_as_double(0x7ff0000000000000ll);
+        g.flags[gid] = nonfinite;
+        g.stamp[gid] = seq0 + k;
+        atomicAdd(&st->records, records);
+        atomicAdd(&st->removed, removed);
+        atomicAdd(&st->out_elems, (unsigned long long)out_n);
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
+}
+
 template <int W>
 constexpr size_t branch_smem_bytes() {
   return sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
