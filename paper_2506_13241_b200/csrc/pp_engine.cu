@@ -432,7 +432,9 @@ class EngineImpl final : public EngineBase {
     const uint64_t seq0 = bseq_;
     // epsilon0 = 0 (no global threshold), no budget: the whole run in one
     // launch, every group through its gates (k_branch_sublayer)
-    if (!epi && count <= (size_t)kMaxSubGates && G_) {
+    const bool no_budget = !budget;
+    const bool independent = no_budget && (external() || !do_trunc || (cfg_.epsilon0 == 0.0 && !may_hold_zeros_));
+    if (independent && count <= (size_t)kMaxSubGates && G_) {
       SubGates sgates{};
       sgates.ng = (int)count;
       for (size_t i = 0; i < count; ++i) {
@@ -449,7 +451,7 @@ class EngineImpl final : public EngineBase {
         std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
         PP_CUDA(cudaEventRecord(ev.first, stream_));
         k_branch_sublayer<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
-            gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_stats_);
+            gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], nullptr, nullptr, d_stats_);
         PP_CUDA(cudaEventRecord(ev.second, stream_));
         pending_events_.push_back(ev);
         ++launches_;
@@ -472,6 +474,9 @@ class EngineImpl final : public EngineBase {
       counters_.branch_ns += ns_since(t0);
       return;
     }
+    if (no_budget && do_trunc && !external() && cfg_.epsilon0 > 0.0 && count <= (size_t)kMaxSubGates && G_ &&
+        !(cfg_.flags & PP_FLAG_PROFILE) && run_rx_speculative(prm, seq0, t0))
+      return;
     size_t pos = 0;
     while (pos < count && G_) {
       sync_state();
@@ -520,6 +525,86 @@ class EngineImpl final : public EngineBase {
     counters_.gates += count;
     counters_.batches_sent += count;
     counters_.branch_ns += ns_since(t0);
+  }
+
+  // epsilon0 > 0, per-gate cadence: the whole run in one launch with
+  // predicted thresholds, verified bit-exactly against epsilon0 * gmax_k.
+  bool run_rx_speculative(const std::vector<RxParam>& prm, uint64_t seq0, Clock::time_point t0) {
+    const size_t count = prm.size();
+    SubGates sgates{};
+    sgates.ng = (int)count;
+    for (size_t i = 0; i < count; ++i) {
+      sgates.wq[i] = (int8_t)prm[i].wq;
+      sgates.mq[i] = prm[i].mq;
+      sgates.cosv[i] = prm[i].cosv;
+      sgates.sinv[i] = prm[i].sinv;
+      sgates.any[prm[i].wq] |= prm[i].mq;
+    }
+    sync_state();
+    std::vector<double> tpred(count, cfg_.epsilon0 * gmax_);
+    spec_buf_.ensure(count * 16 + 64);
+    double* d_tpred = spec_buf_.as<double>();
+    unsigned long long* d_gmax = reinterpret_cast<unsigned long long*>(d_tpred + count);
+    for (int attempt = 0; attempt < 8; ++attempt) {
+      sync_state();
+      if (bump_ + 3 * live_ > arena_[cur_].cap) gc_into_other(std::max<uint64_t>(next_arena_target(), 4 * live_));
+      // snapshot of the group table: the rollback point
+      const size_t gbytes = (size_t)groups_[gcur_].cap * (8 * W + 8 + 8 + 8 + 4 + 4 + 4 + 4);
+      backup_.ensure(gbytes);
+      PP_CUDA(cudaMemcpyAsync(backup_.p, groups_[gcur_].buf.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
+      const uint32_t G_saved = G_;
+      const pp_counters saved = counters_;
+      PP_CUDA(cudaMemcpyAsync(d_tpred, tpred.data(), count * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemsetAsync(d_gmax, 0, count * 8, stream_));
+      push_scalars(seq0);
+      std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
+      PP_CUDA(cudaEventRecord(ev.first, stream_));
+      k_branch_sublayer<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+          gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_tpred, d_gmax, d_stats_);
+      PP_CUDA(cudaEventRecord(ev.second, stream_));
+      pending_events_.push_back(ev);
+      ++launches_;
+      ++branch_launches_;
+      std::vector<unsigned long long> gm(count);
+      PP_CUDA(cudaMemcpyAsync(gm.data(), d_gmax, count * 8, cudaMemcpyDeviceToHost, stream_));
+      dirty_ = true;
+      sync_state();  // harvests counters, reads the arena fault flag
+      bool exact = !arena_fault_;
+      std::vector<double> tobs(count);
+      for (size_t k = 0; k < count; ++k) {
+        tobs[k] = cfg_.epsilon0 * __builtin_bit_cast(double, gm[k]);  // engine.cpp:345
+        if (__builtin_bit_cast(uint64_t, tobs[k]) != __builtin_bit_cast(uint64_t, tpred[k])) exact = false;
+      }
+      if (exact && h_stats_->red[2].nonfinite)
+        throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient in gates " + std::to_string(gates_applied_ + 1) +
+                                                ".." + std::to_string(gates_applied_ + count));
+      if (exact) {
+        gmax_ = __builtin_bit_cast(double, gm[count - 1]);
+        truncated_since_sync_ = false;
+        bseq_ = seq0 + count;
+        gates_applied_ += count;
+        counters_.gates += count;
+        counters_.batches_sent += count;
+        counters_.branch_ns += ns_since(t0);
+        spec_attempts_ += attempt + 1;
+        return true;
+      }
+      // roll back: restore the table (the old regions are untouched)
+      PP_CUDA(cudaMemcpyAsync(groups_[gcur_].buf.p, backup_.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
+      G_ = G_saved;
+      counters_ = saved;
+      if (arena_fault_) {
+        k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
+        ++launches_;
+        arena_fault_ = false;
+      } else {
+        tpred = tobs;
+      }
+      dirty_ = true;
+      sync_state();
+      gc_into_other(std::max<uint64_t>(next_arena_target(), 4 * live_));
+    }
+    return false;  // did not converge: the caller runs the gates one by one
   }
 
   void launch_branch(const RxParam& p, uint32_t rel) {
@@ -1321,7 +1406,8 @@ class EngineImpl final : public EngineBase {
   cudaEvent_t ev0_, ev1_;
   Arena arena_[2];
   Groups groups_[2];
-  DevBuf evict_cnt_, evict_buf_;
+  DevBuf evict_cnt_, evict_buf_, spec_buf_, backup_;
+  uint64_t spec_attempts_ = 0;
   DevBuf stats_buf_, list_, items_, rec_slot_, table_, scan_tmp_, scan_gid_, scan_off_, diag_z_, diag_c_, cliff_;
   int cur_ = 0, gcur_ = 0;
   uint32_t G_ = 0;

@@ -237,7 +237,7 @@ template <int W>
 __device__ void stream_branch_range(BranchSmem<W>& sm, ArenaView<W> ar, uint64_t src, uint32_t n, uint64_t dst,
                                     uint32_t& out_n, int wq, uint64_t mq, double cosv, double sinv, int keep_zeros,
                                     double& vmax, double& vmin, uint32_t& nonfinite, unsigned long long& records,
-                                    unsigned long long& removed) {
+                                    unsigned long long& removed, double tout, double& vall) {
   const uint32_t tid = threadIdx.x;
   const double nsin = -sinv;
   __syncthreads();
@@ -316,7 +316,8 @@ __device__ void stream_branch_range(BranchSmem<W>& sm, ArenaView<W> ar, uint64_t
           if (d != 0.0) v = __dadd_rn(v, d);
         }
       }
-      bool emit = keep_zeros || v != 0.0;
+      vall = fmax(vall, fabs(v));
+      bool emit = tout < 0.0 ? (keep_zeros || v != 0.0) : !(fabs(v) <= tout);  // remove_below: |c| <= T
       if (!emit) ++removed;
       sk_store<W>(sm.skey, kSlots, rank, k);
       sm.sval[rank] = v;
@@ -333,6 +334,11 @@ __device__ void stream_branch_range(BranchSmem<W>& sm, ArenaView<W> ar, uint64_t
       uint32_t la = sk_lower_bound<W>(sm.key[0], kBufCap, mA, k);
       if (la < mA && plane_eq<W>(sk_load<W>(sm.key[0], kBufCap, la), k)) continue;  // partner
       if (d == 0.0) continue;  // engine.cpp:226: no record for a zero increment
+      vall = fmax(vall, fabs(d));
+      if (tout >= 0.0 && fabs(d) <= tout) {  // inserted, then truncated
+        ++removed;
+        continue;
+      }
       uint32_t lo = t0 ? sk_lower_bound<W>(sm.key[2], kBufCap, m1, k) : sk_lower_bound<W>(sm.key[1], kBufCap, m0, k);
       uint32_t rank = jj + la + lo;
       sk_store<W>(sm.skey, kSlots, rank, k);
@@ -466,7 +472,7 @@ template <int W>
 __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, uint32_t p, uint32_t n, uint64_t dst,
                                uint32_t& out_n, int wq, uint64_t mq, double cosv, double sinv, int keep_zeros,
                                double& vmax, double& vmin, uint32_t& nonfinite, unsigned long long& records,
-                               unsigned long long& removed) {
+                               unsigned long long& removed, double tout, double& vall) {
   const uint32_t tid = threadIdx.x;
   const uint64_t hmask = ~((mq << 1) - 1);  // bits above q in word wq
   const uint32_t L = min(kSeg, n - p);
@@ -617,24 +623,27 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
         double t = __dmul_rn(c1, cosv);
         if (d1 != 0.0) t = __dadd_rn(t, d1);
         v1 = t;
-        e1 = keep_zeros || t != 0.0;
+        e1 = tout < 0.0 ? (keep_zeros || t != 0.0) : !(fabs(t) <= tout);
         if (!e1) ++removed;
       } else {
         v1 = d1;
-        e1 = d1 != 0.0;
+        e1 = d1 != 0.0 && !(fabs(d1) <= tout);
+        if (d1 != 0.0 && !e1) ++removed;  // inserted, then truncated
       }
       v0 = s;
-      e0 = keep_zeros || s != 0.0;
+      e0 = tout < 0.0 ? (keep_zeros || s != 0.0) : !(fabs(s) <= tout);
       if (!e0) ++removed;
     } else {  // Y at q, no partner: the child y gets -sin c1
       const double d0 = __dmul_rn(nsin, c);
       if (d0 != 0.0) ++records;
       v0 = d0;
-      e0 = d0 != 0.0;
+      e0 = d0 != 0.0 && !(fabs(d0) <= tout);
+      if (d0 != 0.0 && !e0) ++removed;
       v1 = __dmul_rn(c, cosv);
-      e1 = keep_zeros || v1 != 0.0;
+      e1 = tout < 0.0 ? (keep_zeros || v1 != 0.0) : !(fabs(v1) <= tout);
       if (!e1) ++removed;
     }
+    vall = fmax(vall, fmax(fabs(v0), fabs(v1)));
     sk_store<W>(sm.okey, 2 * kSeg, s0, y);
     sm.oval[s0] = v0;
     sm.oemit[s0] = e0;
@@ -781,10 +790,11 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
     double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     uint32_t nonfinite = 0;
     unsigned long long records = 0, removed = 0;
+    double vall = 0.0;
     uint32_t p = 0;
     while (p < n) {
       uint32_t used = seg_branch<W>(sg, ar, src, p, n, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
-                                    nonfinite, records, removed);
+                                    nonfinite, records, removed, -1.0, vall);
       if (used) {
         p += used;
         continue;
@@ -793,7 +803,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
       const uint32_t be = find_block_end<W>(ar, src, p, n, wq, mq, nullptr);
       if (tid == 0) atomicAdd(&st->stream_elems, (unsigned long long)(be - p));
       stream_branch_range<W>(sm, ar, src + p, be - p, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
-                             nonfinite, records, removed);
+                             nonfinite, records, removed, -1.0, vall);
       p = be;
     }
     // ---- per-group statistics -------------------------------------------
@@ -856,67 +866,218 @@ struct SubGates {
   uint64_t any[2];  // union of the gate masks per plane word
 };
 
+// copy group region [src, src+n) to dst keeping |c| > T (truncation into
+// fresh space, so the source stays intact for a rollback); returns the count
+// and the kept max / min
+template <int W>
+__device__ uint32_t copy_truncated(ArenaView<W> ar, uint64_t src, uint32_t n, uint64_t dst, double T, uint32_t* scan,
+                                   double& vmax, double& vmin) {
+  uint32_t w = 0;
+  for (uint32_t base = 0; base < n; base += kCta) {
+    const uint32_t p = base + threadIdx.x;
+    bool keep = false;
+    Plane<W> k;
+    double v = 0.0;
+    if (p < n) {
+      k = load_plane<W>(ar.x, src + p);
+      v = ar.c[src + p];
+      keep = !(fabs(v) <= T);
+    }
+    uint32_t tot;
+    const uint32_t o = block_excl_scan(keep ? 1u : 0u, scan, &tot);
+    if (keep) {
+      store_plane<W>(ar.x, dst + w + o, k);
+      ar.c[dst + w + o] = v;
+      vmax = fmax(vmax, fabs(v));
+      vmin = fmin(vmin, fabs(v));
+    }
+    w += tot;
+  }
+  return w;
+}
+
+// Block-wide reduction of the per-thread group statistics into shared
+// scalars (result valid in every thread after the call).
+struct GroupStatsSmem {
+  double mx[kWarps], mn[kWarps], all[kWarps];
+  unsigned long long rec[kWarps], rem[kWarps];
+  uint32_t nf[kWarps];
+};
+__device__ __forceinline__ void reduce_group_stats(GroupStatsSmem& r, double& vmax, double& vmin, double& vall,
+                                                   uint32_t& nonfinite, unsigned long long& records,
+                                                   unsigned long long& removed) {
+  vmax = warp_max(vmax);
+  vmin = warp_min(vmin);
+  vall = warp_max(vall);
+  records = warp_sum64(records);
+  removed = warp_sum64(removed);
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    r.mx[warp] = vmax;
+    r.mn[warp] = vmin;
+    r.all[warp] = vall;
+    r.rec[warp] = records;
+    r.rem[warp] = removed;
+    r.nf[warp] = nonfinite;
+  }
+  __syncthreads();
+  vmax = r.mx[0];
+  vmin = r.mn[0];
+  vall = r.all[0];
+  records = r.rec[0];
+  removed = r.rem[0];
+  nonfinite = r.nf[0];
+  for (uint32_t w = 1; w < kWarps; ++w) {
+    vmax = fmax(vmax, r.mx[w]);
+    vmin = fmin(vmin, r.mn[w]);
+    vall = fmax(vall, r.all[w]);
+    records += r.rec[w];
+    removed += r.rem[w];
+    nonfinite |= r.nf[w];
+  }
+  __syncthreads();
+}
+
+// Modes:
+//  tpred == nullptr  (epsilon0 = 0, or per-layer cadence): only groups some
+//    gate touches; no truncation inside the run; resumable via stamps.
+//  tpred != nullptr  (per-gate cadence, epsilon0 > 0, speculative): every
+//    group; gate k truncates with the PREDICTED threshold tpred[k]; the max
+//    |c| after each gate's apply (before its truncation) is max-reduced into
+//    gmax_out[k] over all groups (untouched groups contribute their current
+//    max).  All writes go to fresh arena space, so the host can verify
+//    eps * gmax_out[k] == tpred[k] for every k and otherwise roll the group
+//    table back and rerun with the observed thresholds.
 template <int W>
 __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
-                                                           int keep_zeros, unsigned int* work, DevStats* st) {
+                                                           int keep_zeros, unsigned int* work, const double* tpred,
+                                                           unsigned long long* gmax_out, DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
   const uint32_t tid = threadIdx.x;
   if (engine_failed(st)) return;
+  const bool spec = tpred != nullptr;
   const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
   const unsigned long long cap = *(volatile const unsigned long long*)&st->arena_cap;
   const uint32_t seq0 = (uint32_t)(*(volatile const unsigned long long*)&st->seq_base);
   __shared__ unsigned long long dst_s;
   __shared__ uint32_t s_gid, s_fail;
-  __shared__ double red_max[kWarps], red_min[kWarps];
-  __shared__ unsigned long long red_rec[kWarps], red_rem[kWarps];
-  __shared__ uint32_t red_nf[kWarps];
+  __shared__ GroupStatsSmem gs;
+  __shared__ unsigned long long smax[kMaxSubGates];  // per-CTA per-gate max (bits)
+  __shared__ uint32_t tscan[40];
+  for (int k = tid; k < gates.ng; k += kCta) smax[k] = 0ull;
   unsigned long long aff_elems = 0;
+  bool failed = false;
+  // contribute the group's current max to gates [a, b)
+  auto contribute = [&](int a, int b, double m) {
+    if (!spec || m <= 0.0) return;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+    for (int j = a + (int)tid; j < b; j += kCta) atomicMax(&smax[j], bits);
+  };
+  auto alloc = [&](uint32_t n, int k) -> bool {
+    __syncthreads();
+    if (tid == 0) {
+      dst_s = atomicAdd(&st->bump, (unsigned long long)n);
+      s_fail = dst_s + n > cap;
+      if (s_fail) {
+        atomicOr(&st->err_arena, 1u);
+        atomicMin(&st->err_seq, (unsigned long long)(seq0 + k));
+      }
+    }
+    __syncthreads();
+    return !s_fail;
+  };
   for (;;) {
     __syncthreads();
     if (tid == 0) s_gid = atomicAdd(work, 1u);
     __syncthreads();
     const uint32_t gid = s_gid;
-    if (gid >= G) break;
+    if (gid >= G || failed) break;
     Plane<W> z;
 #pragma unroll
     for (int k = 0; k < W; ++k) z.w[k] = g.z[k][gid];
-    bool touched = false;
+    uint32_t n = g.cnt[gid];
+    if (n == 0) continue;
+    if (!spec) {
+      bool touched = false;
 #pragma unroll
-    for (int k = 0; k < W; ++k) touched |= (z.w[k] & gates.any[k]) != 0;
-    if (!touched || g.cnt[gid] == 0) continue;
-    const uint32_t stamp = g.stamp[gid];
-    int k0 = (stamp - seq0 < (uint32_t)gates.ng) ? (int)(stamp - seq0) + 1 : 0;  // resume after the stamp
-    for (int k = k0; k < gates.ng; ++k) {
-      const int wq = gates.wq[k];
-      const uint64_t mq = gates.mq[k];
-      if (!(z.w[wq] & mq)) continue;
-      const uint32_t n = g.cnt[gid];
-      if (n == 0) break;
-      const uint64_t src = g.off[gid];
-      __syncthreads();
-      if (tid == 0) {
-        dst_s = atomicAdd(&st->bump, 2ull * n);
-        s_fail = dst_s + 2ull * n > cap;
-        if (s_fail) {
-          atomicOr(&st->err_arena, 1u);
-          atomicMin(&st->err_seq, (unsigned long long)(seq0 + k));
+      for (int k = 0; k < W; ++k) touched |= (z.w[k] & gates.any[k]) != 0;
+      if (!touched) continue;
+    }
+    uint64_t src = g.off[gid];
+    uint32_t cap_g = g.cap[gid];
+    double curmax = g.gmax[gid], curmin = g.gmin[gid];
+    uint32_t curnf = g.flags[gid];
+    bool changed = false;
+    int k0 = 0;
+    if (!spec) {
+      const uint32_t stamp = g.stamp[gid];
+      k0 = (stamp - seq0 < (uint32_t)gates.ng) ? (int)(stamp - seq0) + 1 : 0;  // resume after the stamp
+    }
+    int last = -1;  // last gate applied to this group (spec: truncations after it are pending)
+    for (int k = k0; k <= gates.ng; ++k) {
+      const bool end = k == gates.ng;
+      if (!end && !(z.w[gates.wq[k]] & gates.mq[k])) continue;
+      if (spec) {
+        // gates (last, k) did not touch the group: it held its values, each
+        // of those gates' truncations applied to it
+        double tp = -1.0;
+        for (int j = last + 1; j < k; ++j) tp = fmax(tp, tpred[j]);
+        if (n) {
+          int j_empty = k;  // first pending gate whose threshold empties the group
+          for (int j = last + 1; j < k; ++j)
+            if (curmax <= tpred[j]) {
+              j_empty = j;
+              break;
+            }
+          contribute(last + 1, j_empty + 1 < k ? j_empty + 1 : k, curmax);
+          if (j_empty < k) n = 0;
+        }
+        if (n && curmin <= tp) {  // drop what those truncations removed, into fresh space
+          if (!alloc(n, k)) {
+            failed = true;
+            break;
+          }
+          double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
+          const uint32_t w = copy_truncated<W>(ar, src, n, dst_s, tp, tscan, mx, mn);
+          mx = warp_max(mx);
+          mn = warp_min(mn);
+          double dv = 0.0;
+          uint32_t nf0 = 0;
+          unsigned long long r0 = 0, rm = n - w;
+          if (tid != 0) rm = 0;
+          reduce_group_stats(gs, mx, mn, dv, nf0, r0, rm);
+          if (tid == 0 && rm) atomicAdd(&st->removed, rm);
+          src = dst_s;
+          cap_g = n;
+          n = w;
+          curmax = w ? mx : 0.0;
+          curmin = w ? mn : __longlong_as_double(0x7ff0000000000000ll);
+          changed = true;
         }
       }
-      __syncthreads();
-      if (s_fail) break;  // group stays after gate k-1 (its stamp); the host compacts and relaunches
+      if (end || n == 0) break;
+      const int wq = gates.wq[k];
+      const uint64_t mq = gates.mq[k];
+      if (!alloc(2 * n, k)) {
+        failed = true;
+        break;
+      }
       const uint64_t dst = dst_s;
       aff_elems += n;
       uint32_t out_n = 0;
-      double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);
+      double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll), vall = 0.0;
       uint32_t nonfinite = 0;
       unsigned long long records = 0, removed = 0;
       const double cosv = gates.cosv[k], sinv = gates.sinv[k];
+      const double tout = spec ? tpred[k] : -1.0;
       uint32_t p = 0;
       while (p < n) {
         uint32_t used = seg_branch<W>(sg, ar, src, p, n, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
-                                      nonfinite, records, removed);
+                                      nonfinite, records, removed, tout, vall);
         if (used) {
           p += used;
           continue;
@@ -925,46 +1086,54 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
         const uint32_t be = find_block_end<W>(ar, src, p, n, wq, mq, nullptr);
         if (tid == 0) atomicAdd(&st->stream_elems, (unsigned long long)(be - p));
         stream_branch_range<W>(sm, ar, src + p, be - p, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
-                               nonfinite, records, removed);
+                               nonfinite, records, removed, tout, vall);
         p = be;
       }
-      vmax = warp_max(vmax);
-      vmin = warp_min(vmin);
-      records = warp_sum64(records);
-      removed = warp_sum64(removed);
-      nonfinite = __any_sync(0xffffffffu, nonfinite);
-      const uint32_t lane = tid & 31, warp = tid >> 5;
-      __syncthreads();
-      if (lane == 0) {
-        red_max[warp] = vmax;
-        red_min[warp] = vmin;
-        red_rec[warp] = records;
-        red_rem[warp] = removed;
-        red_nf[warp] = nonfinite;
-      }
-      __syncthreads();
+      reduce_group_stats(gs, vmax, vmin, vall, nonfinite, records, removed);
       if (tid == 0) {
-        for (uint32_t w = 1; w < kWarps; ++w) {
-          vmax = fmax(vmax, red_max[w]);
-          vmin = fmin(vmin, red_min[w]);
-          records += red_rec[w];
-          removed += red_rem[w];
-          nonfinite |= red_nf[w];
-        }
-        g.off[gid] = dst;
-        g.cnt[gid] = out_n;
-        g.cap[gid] = 2 * n;
-        g.gmax[gid] = out_n ? vmax : 0.0;
-        g.gmin[gid] = out_n ? vmin : __longlong_as_double(0x7ff0000000000000ll);
-        g.flags[gid] = nonfinite;
-        g.stamp[gid] = seq0 + k;
         atomicAdd(&st->records, records);
         atomicAdd(&st->removed, removed);
         atomicAdd(&st->out_elems, (unsigned long long)out_n);
       }
+      if (spec) {
+        if (tid == 0 && vall > 0.0) atomicMax(&smax[k], (unsigned long long)__double_as_longlong(vall));
+        // gmax as the reference sees it includes a NaN only through the flag
+      }
+      src = dst;
+      cap_g = 2 * n;
+      n = out_n;
+      curmax = out_n ? vmax : 0.0;
+      curmin = out_n ? vmin : __longlong_as_double(0x7ff0000000000000ll);
+      curnf = nonfinite;
+      changed = true;
+      last = k;
+      if (!spec && tid == 0) {  // resumable progress (eps = 0 mode)
+        g.off[gid] = src;
+        g.cnt[gid] = n;
+        g.cap[gid] = cap_g;
+        g.gmax[gid] = curmax;
+        g.gmin[gid] = curmin;
+        g.flags[gid] = curnf;
+        g.stamp[gid] = seq0 + k;
+      }
       __syncthreads();
     }
+    if (failed) break;
+    if (spec && changed && tid == 0) {
+      g.off[gid] = src;
+      g.cnt[gid] = n;
+      g.cap[gid] = cap_g;
+      g.gmax[gid] = curmax;
+      g.gmin[gid] = curmin;
+      g.flags[gid] = curnf;
+    } else if (spec && n == 0 && tid == 0) {
+      g.cnt[gid] = 0;
+    }
   }
+  __syncthreads();
+  if (spec)
+    for (int k = tid; k < gates.ng; k += kCta)
+      if (smax[k]) atomicMax(&gmax_out[k], smax[k]);
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
 }
 
