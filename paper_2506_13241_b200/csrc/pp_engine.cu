@@ -474,8 +474,11 @@ class EngineImpl final : public EngineBase {
       counters_.branch_ns += ns_since(t0);
       return;
     }
-    if (no_budget && do_trunc && !external() && cfg_.epsilon0 > 0.0 && count <= (size_t)kMaxSubGates && G_ &&
-        !(cfg_.flags & PP_FLAG_PROFILE) && run_rx_speculative(prm, seq0, t0))
+    // speculative fused run for epsilon0 > 0 (exact, but two passes per run on
+    // these workloads: opt-in until the first prediction is right more often)
+    static const bool speculate = std::getenv("PP_SPECULATE") != nullptr;
+    if (speculate && no_budget && do_trunc && !external() && cfg_.epsilon0 > 0.0 && count <= (size_t)kMaxSubGates &&
+        G_ && !(cfg_.flags & PP_FLAG_PROFILE) && run_rx_speculative(prm, seq0, t0))
       return;
     size_t pos = 0;
     while (pos < count && G_) {
@@ -545,9 +548,19 @@ class EngineImpl final : public EngineBase {
     spec_buf_.ensure(count * 16 + 64);
     double* d_tpred = spec_buf_.as<double>();
     unsigned long long* d_gmax = reinterpret_cast<unsigned long long*>(d_tpred + count);
+    int faults = 0;
     for (int attempt = 0; attempt < 8; ++attempt) {
       sync_state();
-      if (bump_ + 3 * live_ > arena_[cur_].cap) gc_into_other(std::max<uint64_t>(next_arena_target(), 4 * live_));
+      // every gate application writes fresh space (the pre-run regions are
+      // the rollback point): reserve ~24 |O| when memory allows
+      const uint64_t want = 24 * live_ + (1u << 16);
+      if (bump_ + want > arena_[cur_].cap) {
+        size_t free_b = 0, total_b = 0;
+        PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const uint64_t afford = (uint64_t)((free_b + arena_[1 - cur_].buf.bytes) * 0.8) / R;
+        if (live_ + want > afford && faults > 0) return false;
+        gc_into_other(std::max<uint64_t>(std::min<uint64_t>(live_ + want, afford), next_arena_target()));
+      }
       // snapshot of the group table: the rollback point
       const size_t gbytes = (size_t)groups_[gcur_].cap * (8 * W + 8 + 8 + 8 + 4 + 4 + 4 + 4);
       backup_.ensure(gbytes);
@@ -587,22 +600,45 @@ class EngineImpl final : public EngineBase {
         counters_.batches_sent += count;
         counters_.branch_ns += ns_since(t0);
         spec_attempts_ += attempt + 1;
+        if (std::getenv("PP_DEBUG"))
+          std::fprintf(stderr, "[pp] speculative run of %zu gates accepted after %d attempt(s)\n", count, attempt + 1);
         return true;
       }
       // roll back: restore the table (the old regions are untouched)
       PP_CUDA(cudaMemcpyAsync(groups_[gcur_].buf.p, backup_.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
       G_ = G_saved;
       counters_ = saved;
-      if (arena_fault_) {
+      if (std::getenv("PP_DEBUG")) {
+        size_t first = 0;
+        while (first < count && __builtin_bit_cast(uint64_t, tobs[first]) == __builtin_bit_cast(uint64_t, tpred[first]))
+          ++first;
+        if (first < count)
+          std::fprintf(stderr, "[pp]   gate %zu: predicted %.17g (%016llx) observed %.17g (%016llx) gmax_=%.17g\n", first,
+                       tpred[first], (unsigned long long)__builtin_bit_cast(uint64_t, tpred[first]), tobs[first],
+                       (unsigned long long)gm[first], gmax_);
+      }
+      const bool fault = arena_fault_;
+      if (fault) {
         k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
         ++launches_;
         arena_fault_ = false;
+        if (++faults >= 2) {  // cannot hold a whole speculative run: gates one by one
+          dirty_ = true;
+          sync_state();
+          gc_into_other(next_arena_target());
+          return false;
+        }
       } else {
         tpred = tobs;
       }
       dirty_ = true;
       sync_state();
-      gc_into_other(std::max<uint64_t>(next_arena_target(), 4 * live_));
+      if (std::getenv("PP_DEBUG")) {
+        size_t first = 0;
+        while (first < count && tobs[first] == tpred[first]) ++first;
+        std::fprintf(stderr, "[pp] speculative run of %zu gates: attempt %d rejected (faults %d, first mismatch at %zu)\n",
+                     count, attempt, faults, first);
+      }
     }
     return false;  // did not converge: the caller runs the gates one by one
   }
