@@ -476,7 +476,7 @@ class EngineImpl final : public EngineBase {
     }
     // speculative fused run for epsilon0 > 0 (exact, but two passes per run on
     // these workloads: opt-in until the first prediction is right more often)
-    static const bool speculate = std::getenv("PP_SPECULATE") != nullptr;
+    const bool speculate = std::getenv("PP_SPECULATE") != nullptr;
     if (speculate && no_budget && do_trunc && !external() && cfg_.epsilon0 > 0.0 && count <= (size_t)kMaxSubGates &&
         G_ && !(cfg_.flags & PP_FLAG_PROFILE) && run_rx_speculative(prm, seq0, t0))
       return;

@@ -237,3 +237,13 @@ def test_fusion_matches_unfused(pp, O):
     for x, y in zip(ra, rb):
         for k in ("term_count", "removed", "records_sent"):
             assert x[k] == y[k], (k, x, y)
+
+
+def test_speculative_sublayer_is_exact(pp, O, monkeypatch):
+    # the opt-in fused run for epsilon0 > 0 (predicted thresholds, verified and
+    # rolled back on mismatch) must give the per-gate result bit for bit
+    monkeypatch.setenv("PP_SPECULATE", "1")
+    geom = pp.heavy_hex_127()
+    for thx, eps in (("0.25pi", 1e-4), (0.3, 1e-5)):
+        circ = _kicked(pp, geom, thx, 6)
+        run_both(pp, O, 127, list(circ.layers), [(O.site_word(62, 3), 1.0)], eps, "gate", check_each=True)
