@@ -1331,11 +1331,19 @@ class EngineImpl final : public EngineBase {
     const uint64_t max_items = (uint64_t)G_ + live / kItem + 1;
     items_.ensure(max_items * sizeof(Item));
     rec_slot_.ensure(live * maxrec * 4);
-    uint64_t records_upper = live * maxrec;
+    const uint64_t records_upper = live * maxrec;
+    // small stores: size every buffer by its upper bound so nothing can
+    // overflow, let the kernels read counts from the device, and synchronise
+    // once at the end
+    bool small = records_upper <= (1ull << 22);
     uint64_t tc = 1024;
-    while (tc < 2 * std::min<uint64_t>(records_upper, std::max<uint64_t>(8ull * G_, live / 4) + 1024)) tc <<= 1;
+    if (small) {
+      while (tc < 2 * records_upper + 1024) tc <<= 1;
+    } else {
+      while (tc < 2 * std::min<uint64_t>(records_upper, std::max<uint64_t>(8ull * G_, live / 4) + 1024)) tc <<= 1;
+    }
     uint64_t tc_max = 1024;
-    while (tc_max < 2 * records_upper) tc_max <<= 1;
+    while (tc_max < 2 * records_upper + 1024) tc_max <<= 1;
     const int o = 1 - cur_;
     for (int attempt = 0;; ++attempt) {
       if (attempt > 8) throw EngineError(PP_ERR_INTERNAL, "regroup: hash table retries exhausted");
@@ -1346,22 +1354,27 @@ class EngineImpl final : public EngineBase {
       reset_stats(bump_);
       k_make_items<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, items_.as<Item>(), maxrec, d_stats_);
       ++launches_;
-      fetch_stats();
-      const uint64_t n_items = h_stats_->items;
+      uint64_t n_items = max_items;
+      if (!small) {
+        fetch_stats();
+        n_items = h_stats_->items;
+      }
       k_insert<W, P><<<(uint32_t)n_items, kCta, 0, stream_>>>(items_.as<Item>(), gview(gcur_), aview(cur_), prod, t,
                                                               rec_slot_.as<uint32_t>(), seed_,
                                                               (uint32_t)std::min<uint64_t>(tc / 2, 0xffffffffu),
                                                               d_stats_);
       ++launches_;
-      fetch_stats();
-      PP_CUDA(cudaGetLastError());
-      if (h_stats_->overflow) {
-        if (tc >= tc_max) throw EngineError(PP_ERR_INTERNAL, "regroup: hash table overflow");
-        tc = std::min(tc_max, tc * 8);
-        continue;
+      uint32_t distinct = 0;
+      if (!small) {
+        fetch_stats();
+        PP_CUDA(cudaGetLastError());
+        if (h_stats_->overflow) {
+          if (tc >= tc_max) throw EngineError(PP_ERR_INTERNAL, "regroup: hash table overflow");
+          tc = std::min(tc_max, tc * 8);
+          continue;
+        }
+        distinct = h_stats_->distinct;
       }
-      const uint32_t distinct = h_stats_->distinct;
-      const unsigned long long records = h_stats_->records;
       // deterministic ids and offsets from slot order
       const uint64_t ntiles = (tc + kScanTile - 1) / kScanTile;
       scan_tmp_.ensure((ntiles + 1) * 8);
@@ -1369,39 +1382,53 @@ class EngineImpl final : public EngineBase {
       scan_off_.ensure(tc * 8);
       device_scan(t.count, tc, 1, scan_gid_.as<unsigned long long>(), ntiles);
       device_scan(t.count, tc, 0, scan_off_.as<unsigned long long>(), ntiles);
-      unsigned long long total = 0;
-      PP_CUDA(cudaMemcpyAsync(&total, scan_tmp_.as<unsigned long long>() + ntiles, 8, cudaMemcpyDeviceToHost,
-                              stream_));
-      PP_CUDA(cudaStreamSynchronize(stream_));
-      ensure_groups(1 - gcur_, std::max<uint32_t>(distinct, 1024));
-      ensure_arena(o, std::max<uint64_t>(total + (1u << 16), (uint64_t)(total * 1.5)));
+      PP_CUDA(cudaMemcpyAsync(&d_stats_->scan_total, scan_tmp_.as<unsigned long long>() + ntiles, 8,
+                              cudaMemcpyDeviceToDevice, stream_));
+      uint64_t total_bound = records_upper;
+      uint32_t groups_bound = (uint32_t)std::min<uint64_t>(records_upper, 0xffffffffu);
+      if (!small) {
+        fetch_stats();
+        total_bound = h_stats_->scan_total;
+        groups_bound = distinct;
+      }
+      ensure_groups(1 - gcur_, std::max<uint32_t>(groups_bound, 1024));
+      ensure_arena(o, std::max<uint64_t>(total_bound + (1u << 16), (uint64_t)(total_bound * 1.5)));
       k_table_emit<W><<<(uint32_t)((tc + kCta - 1) / kCta), kCta, 0, stream_>>>(
           t, scan_gid_.as<unsigned long long>(), scan_off_.as<unsigned long long>(), gview(1 - gcur_), 0);
-      ++launches_;
-      reset_stats(0);
       k_scatter<W, P><<<(uint32_t)n_items, kCta, 0, stream_>>>(items_.as<Item>(), gview(gcur_), aview(cur_), prod, t,
                                                                rec_slot_.as<uint32_t>(), gview(1 - gcur_), aview(o),
                                                                d_stats_);
-      ++launches_;
-      fetch_stats();
-      PP_CUDA(cudaGetLastError());
-      if (h_stats_->collision) {
-        seed_ = mix64(seed_ + 1);
-        continue;
+      launches_ += 2;
+      if (!small) {
+        fetch_stats();
+        PP_CUDA(cudaGetLastError());
+        if (h_stats_->collision) {
+          seed_ = mix64(seed_ + 1);
+          continue;
+        }
       }
       // sort inside groups; the source arena is free now and serves as
       // scratch for the big-group merge passes
-      ensure_arena(cur_, total + 1);
-      reset_stats(0);
-      k_sort_small<W><<<distinct, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o), keep_zeros_,
-                                                                         d_stats_);
-      k_sort_big<W><<<distinct, kCta, big_sort_smem(), stream_>>>(gview(1 - gcur_), aview(o), aview(cur_),
-                                                                  keep_zeros_, d_stats_);
+      const bool source_kept = arena_[cur_].cap >= total_bound + 1;
+      ensure_arena(cur_, total_bound + 1);
+      const uint32_t sort_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 16u));
+      k_sort_small<W><<<sort_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o), keep_zeros_,
+                                                                          d_stats_);
+      k_sort_big<W><<<std::min<uint32_t>(sort_grid, 148u * 2u), kCta, big_sort_smem(), stream_>>>(
+          gview(1 - gcur_), aview(o), aview(cur_), keep_zeros_, d_stats_);
       launches_ += 2;
       fetch_stats();
       PP_CUDA(cudaGetLastError());
+      if (small && (h_stats_->overflow || h_stats_->collision)) {  // not expected: redo on the careful path
+        if (!source_kept) throw EngineError(PP_ERR_INTERNAL, "regroup: fingerprint collision after the source was freed");
+        seed_ = mix64(seed_ + 1);
+        small = false;
+        continue;
+      }
+      distinct = h_stats_->distinct;
+      const uint64_t total = h_stats_->scan_total;
       counters_.removed += h_stats_->removed;
-      h_records_ = records;
+      h_records_ = h_stats_->records;
       cur_ = o;
       gcur_ = 1 - gcur_;
       G_ = distinct;

@@ -90,6 +90,7 @@ struct DevStats {
   unsigned int G_dev;              // group count of the current table
   unsigned int err_arena;          // sticky: a branch allocation did not fit; run must resume
   unsigned long long err_seq;      // first gate sequence number that overflowed
+  unsigned long long scan_total;   // regroup: total records (copied from the scan)
 };
 
 // Scalars a launch run reads from device memory, so that a captured CUDA

@@ -330,6 +330,7 @@ template <int W, class P>
 __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W> g, ArenaView<W> src, P prod,
                                                  HashTable<W> t, uint32_t* rec_slot, unsigned long long seed,
                                                  uint32_t max_distinct, DevStats* st) {
+  if (blockIdx.x >= *(volatile const unsigned long long*)&st->items) return;  // grid may be an upper bound
   const Item it = items[blockIdx.x];
   const uint64_t off = g.off[it.g] + it.start;
   const Plane<W> z = load_plane<W>(g.z, it.g);
@@ -490,6 +491,7 @@ template <int W, class P>
 __global__ void __launch_bounds__(kCta) k_scatter(const Item* items, GroupView<W> g, ArenaView<W> src, P prod,
                                                   HashTable<W> t, const uint32_t* rec_slot, GroupView<W> ng,
                                                   ArenaView<W> dst, DevStats* st) {
+  if (blockIdx.x >= *(volatile const unsigned long long*)&st->items) return;
   const Item it = items[blockIdx.x];
   const uint64_t off = g.off[it.g] + it.start;
   const Plane<W> z = load_plane<W>(g.z, it.g);
@@ -627,9 +629,11 @@ template <int W>
 __global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W> ar, int keep_zeros, DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<W>& sm = *reinterpret_cast<SortSmem<W>*>(smem_raw);
-  const uint32_t gid = blockIdx.x;
+  const uint32_t G = *(volatile const unsigned int*)&st->distinct;
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+  __syncthreads();
   const uint32_t n = g.cnt[gid];
-  if (n > kSortSmall) return;
+  if (n > kSortSmall) continue;
   const uint64_t off = g.off[gid];
   uint32_t np2 = 1;
   while (np2 < n) np2 <<= 1;
@@ -651,6 +655,7 @@ __global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W
   auto getv = [&](uint32_t p) { return sm.val[p]; };
   uint32_t w = combine_stream<W>(n, getk, getv, ar, off, keep_zeros, sm.scan, vmax, vmin, nf, removed);
   finish_group_stats<W>(g, gid, w, vmax, vmin, nf, removed, st);
+  }
 }
 
 // two-run merge of sorted runs a=[0,na) and b=[0,nb) (global) into out,
@@ -761,9 +766,11 @@ template <int W>
 __global__ void __launch_bounds__(kCta) k_sort_big(GroupView<W> g, ArenaView<W> ar, ArenaView<W> scratch,
                                                    int keep_zeros, DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const uint32_t gid = blockIdx.x;
+  const uint32_t G = *(volatile const unsigned int*)&st->distinct;
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+  __syncthreads();
   const uint32_t n = g.cnt[gid];
-  if (n <= kSortSmall) return;
+  if (n <= kSortSmall) continue;
   const uint64_t off = g.off[gid];
   __shared__ unsigned long long so_s;
   if (threadIdx.x == 0) so_s = atomicAdd(&st->scratch_bump, (unsigned long long)n);
@@ -824,6 +831,7 @@ __global__ void __launch_bounds__(kCta) k_sort_big(GroupView<W> g, ArenaView<W> 
   auto getv = [&](uint32_t p) { return fin.c[fo + p]; };
   uint32_t w = combine_stream<W>(n, getk, getv, ar, off, keep_zeros, scan, vmax, vmin, nf, removed);
   finish_group_stats<W>(g, gid, w, vmax, vmin, nf, removed, st);
+  }
 }
 
 }  // namespace ppgpu
