@@ -154,6 +154,16 @@ uint32_t pp_shard_owner(const uint64_t* words, int n, uint64_t seed, uint32_t wo
  * sizes the oracle cannot reach). */
 int pp_norm2(pp_engine* engine, double* out);
 
+/* Log-binned coefficient density with a sign split, the reference's
+ * density_histogram (sparse_operator.cpp:150-197, written per layer by
+ * runner.cpp:173-179): edges exp(log(lower) * (1 - b/bins)), lower =
+ * max(epsilon0, 1e-16), x = c / global_max.  Writes exact integer counts per
+ * bin (positive[bins], negative[bins]); the reference's normalized values are
+ * sums of 1/total over those counts.  1 <= bins <= 4096.  PP_ERR_INVALID if
+ * the operator is nonempty and global_max <= 0 (sparse_operator.cpp:156-160). */
+int pp_density_histogram(pp_engine* engine, int bins, double global_max, double epsilon0, uint64_t* positive,
+                         uint64_t* negative);
+
 #ifdef __cplusplus
 }
 #endif

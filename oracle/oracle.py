@@ -152,6 +152,7 @@ def _oracle_lib():
         L.ppo_phase_exponent.argtypes = [_vp, _vp, _int]
         L.ppo_truncate_threshold.restype = _u64
         L.ppo_truncate_threshold.argtypes = [_vp, _dbl]
+        L.ppo_density_histogram.argtypes = [_vp, _int, _dbl, _dbl, _vp, _vp]
         _olib = L
     return _olib
 
@@ -229,6 +230,15 @@ class OracleEngine:
         k = self.L.ppo_export(self.h, w.ctypes.data, c.ctypes.data, n)
         return sort_terms(w[:k], c[:k])
 
+    def density_histogram(self, bins, epsilon0, gmax=None):
+        """Exact per-bin counts (positive, negative) of density_histogram
+        (sparse_operator.cpp:150-197) with x = c / gmax."""
+        g = self.global_max() if gmax is None else gmax
+        pos = np.zeros(bins, np.uint64)
+        neg = np.zeros(bins, np.uint64)
+        self._check(self.L.ppo_density_histogram(self.h, bins, g, epsilon0, pos.ctypes.data, neg.ctypes.data))
+        return pos, neg
+
     def run_layers(self, gates, layers):
         """run_circuit semantics (engine.cpp:394-446) for a circuit of
         identical layers.  gates: list of (words[4], cos, sin) in circuit
@@ -287,6 +297,12 @@ def _ref_lib():
         L.ppref_angle.argtypes = [_dbl, _int, _vp, _vp, _vp]
         L.ppref_heavy_hex.argtypes = [_vp, _vp, _int]
         L.ppref_kicked_layer.argtypes = [ctypes.c_char_p, _vp, _vp, _int]
+        L.ppref_histogram_tsv.argtypes = [_vp, _int, _dbl, ctypes.c_char_p, _u64]
+        L.ppref_histogram_tsv.restype = ctypes.c_int64
+        L.ppref_dump.argtypes = [_vp, ctypes.c_char_p, _u64]
+        L.ppref_dump.restype = ctypes.c_int64
+        L.ppref_load_dump.argtypes = [ctypes.c_char_p, _int, _vp, _vp, _u64]
+        L.ppref_load_dump.restype = ctypes.c_int64
         _rlib = L
     return _rlib
 
@@ -404,9 +420,40 @@ class RefEngine:
         w = np.ascontiguousarray(words, np.uint64)
         return self.L.ppref_coefficient(self.h, w.ctypes.data)
 
+    def _text(self, fn, *args):
+        cap = 1 << 16
+        while True:
+            buf = ctypes.create_string_buffer(cap)
+            r = fn(self.h, *args, buf, cap)
+            if r == -1:
+                raise OracleError(2, self.L.ppref_last_error().decode())
+            if r >= 0:
+                return buf.value.decode()
+            cap = -r
+
+    def histogram_tsv(self, bins, epsilon0):
+        """The reference's density_histogram(...).to_tsv() for this engine."""
+        return self._text(self.L.ppref_histogram_tsv, bins, epsilon0)
+
+    def dump(self):
+        """Concatenated SparseOperator::dump of all shards."""
+        return self._text(self.L.ppref_dump)
+
     def export(self):
         n = self.term_count()
         w = np.zeros((max(n, 1), 4), np.uint64)
         c = np.zeros(max(n, 1))
         k = self.L.ppref_export(self.h, w.ctypes.data, c.ctypes.data, n)
         return sort_terms(w[:k], c[:k])
+
+
+def ref_load_dump(text: str, n: int):
+    """SparseOperator::load_dump of the reference (sorted words, coeffs)."""
+    L = _ref_lib()
+    cap = max(1, text.count("\n") + 1)
+    w = np.zeros((cap, 4), np.uint64)
+    c = np.zeros(cap)
+    k = L.ppref_load_dump(text.encode(), n, w.ctypes.data, c.ctypes.data, cap)
+    if k < 0:
+        raise OracleError(2, L.ppref_last_error().decode())
+    return sort_terms(w[:k], c[:k])

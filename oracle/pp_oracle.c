@@ -337,6 +337,34 @@ int64_t ppo_export(const ppo_engine* e, uint64_t* words, double* c,
   return (int64_t)e->store.size;
 }
 
+/* density_histogram, sparse_operator.cpp:150-197, as exact counts per bin
+ * (the reference sums 1/total per string; the caller normalizes).  Returns
+ * PPO_INVALID for bins < 1 or a nonempty operator with gmax <= 0. */
+int ppo_density_histogram(const ppo_engine* e, int bins, double gmax,
+                          double epsilon0, uint64_t* pos, uint64_t* neg) {
+  if (bins < 1) return PPO_INVALID;
+  if (e->store.size > 0 && !(gmax > 0)) return PPO_INVALID;
+  double lower = epsilon0 > 1e-16 ? epsilon0 : 1e-16;
+  double log_lower = log(lower);
+  for (int b = 0; b < bins; ++b) pos[b] = neg[b] = 0;
+  for (size_t i = 0; i < e->store.size; ++i) {
+    double x = e->store.vals[i] / gmax;
+    double ax = fabs(x);
+    int b;
+    if (ax <= lower) {
+      b = 0;
+    } else if (ax >= 1.0) {
+      b = bins - 1;
+    } else {
+      b = (int)(bins * (1.0 - log(ax) / log_lower));
+      if (b < 0) b = 0;
+      if (b > bins - 1) b = bins - 1;
+    }
+    if (x < 0) neg[b]++; else pos[b]++;
+  }
+  return PPO_OK;
+}
+
 /* Counters since the last call: removed, records, gates. */
 void ppo_take_counters(ppo_engine* e, uint64_t* out3) {
   out3[0] = e->removed;

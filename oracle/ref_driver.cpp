@@ -22,6 +22,7 @@
 #include <cstring>
 #include <exception>
 #include <new>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -302,6 +303,53 @@ int ppref_kicked_layer(const char* geometry_text, uint64_t* words_out,
       is_zz_out[i] = pauli_weight(layer[i].generator) == 2;
     }
     return static_cast<int>(layer.size());
+  } catch (...) {
+    map_exception();
+    return -1;
+  }
+}
+
+// density_histogram(shards, global_max, bins, epsilon0).to_tsv()
+// (sparse_operator.cpp:136-197).  Returns the TSV length, -1 on error, or
+// -(needed + 2) when cap is too small.
+int64_t ppref_histogram_tsv(void* h, int bins, double epsilon0, char* buf, uint64_t cap) {
+  try {
+    const Engine& engine = static_cast<Handle*>(h)->engine;
+    std::string tsv =
+        density_histogram(engine.shards(), engine.global_max(), bins, epsilon0).to_tsv();
+    if (tsv.size() + 1 > cap) return -static_cast<int64_t>(tsv.size() + 3);
+    std::memcpy(buf, tsv.c_str(), tsv.size() + 1);
+    return static_cast<int64_t>(tsv.size());
+  } catch (...) {
+    map_exception();
+    return -1;
+  }
+}
+
+// SparseOperator::dump of every shard in shard order (sparse_operator.cpp:99-106),
+// i.e. the concatenation of the reference's checkpoint shard files.
+int64_t ppref_dump(void* h, char* buf, uint64_t cap) {
+  std::ostringstream out;
+  for (const SparseOperator& shard : static_cast<Handle*>(h)->engine.shards()) shard.dump(out);
+  std::string text = out.str();
+  if (text.size() + 1 > cap) return -static_cast<int64_t>(text.size() + 3);
+  std::memcpy(buf, text.c_str(), text.size() + 1);
+  return static_cast<int64_t>(text.size());
+}
+
+// SparseOperator::load_dump (sparse_operator.cpp:108-122) -> words/coeffs.
+int64_t ppref_load_dump(const char* text, int n, uint64_t* words, double* coeffs, uint64_t cap) {
+  try {
+    std::istringstream in(text);
+    SparseOperator op = SparseOperator::load_dump(in, n);
+    auto keys = op.store().keys();
+    auto values = op.store().values();
+    if (keys.size() > cap) return -1;
+    for (size_t i = 0; i < keys.size(); ++i) {
+      std::memcpy(words + kIndexWords * i, keys[i].words.data(), sizeof(uint64_t) * kIndexWords);
+      coeffs[i] = values[i];
+    }
+    return static_cast<int64_t>(keys.size());
   } catch (...) {
     map_exception();
     return -1;

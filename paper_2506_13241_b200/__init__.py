@@ -32,6 +32,12 @@ PartitionSpec = _impl.PartitionSpec
 PauliString = _impl.PauliString
 ResourceLimitError = _impl.ResourceLimitError
 bfs_ball = _impl.bfs_ball
+dump_operator = _impl.dump_operator
+histogram_from_counts = _impl.histogram_from_counts
+load_dump = _impl.load_dump
+read_checkpoint = _impl.read_checkpoint
+write_checkpoint_manifest = _impl.write_checkpoint_manifest
+write_shard_file = _impl.write_shard_file
 build_kicked_ising = _impl.build_kicked_ising
 commutes = _impl.commutes
 heavy_hex_127 = _impl.heavy_hex_127
@@ -54,7 +60,8 @@ NATIVE_LIBS = (
 __all__ = [
     "Circuit", "Engine", "Gate", "Geometry", "NumericalError", "PartitionSpec",
     "PauliString", "ResourceLimitError", "bfs_ball", "build_kicked_ising",
-    "commutes", "heavy_hex_127", "load_geometry", "load_geometry_file", "owner",
+    "commutes", "dump_operator", "histogram_from_counts", "load_dump", "read_checkpoint",
+    "write_checkpoint_manifest", "write_shard_file", "heavy_hex_127", "load_geometry", "load_geometry_file", "owner",
     "parse_circuit", "parse_pauli_label", "pauli_weight", "phase_exponent",
     "simulate", "string_product", "uniformity_ratio",
 ]

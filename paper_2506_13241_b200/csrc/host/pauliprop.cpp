@@ -10,7 +10,10 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <deque>
+#include <iterator>
+#include <sys/stat.h>
 #include <fstream>
 #include <limits>
 #include <set>
@@ -676,7 +679,10 @@ RunLedger run_circuit(Engine& engine, const Circuit& circuit, const RunOptions& 
   RunLedger ledger;
   const int L = (int)circuit.layers.size();
   engine.take_counters();
-  for (int t = 1; t <= L; ++t) {
+  if (options.start_layer < 0 || options.start_layer > L)
+    throw std::invalid_argument("start_layer " + std::to_string(options.start_layer) + " outside [0, " +
+                                std::to_string(L) + "]");
+  for (int t = options.start_layer + 1; t <= L; ++t) {
     engine.set_layer_context(t);
     const auto& layer = circuit.layers[L - t];
     auto t0 = std::chrono::steady_clock::now();
@@ -707,6 +713,212 @@ RunLedger run_circuit(Engine& engine, const Circuit& circuit, const RunOptions& 
     if (options.on_layer) options.on_layer(row, engine);
   }
   return ledger;
+}
+
+// ------------------------------------------------------------ diagnostics and checkpoints
+static std::string fmt17(double v) {
+  char buf[32];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+
+DensityHistogram histogram_from_counts(int bins, double epsilon0, const std::vector<uint64_t>& pos,
+                                       const std::vector<uint64_t>& neg) {
+  if (bins < 1) throw std::invalid_argument("histogram needs at least 1 bin");
+  if ((int)pos.size() != bins || (int)neg.size() != bins) throw std::invalid_argument("histogram count size");
+  DensityHistogram h;
+  const double lower = std::max(epsilon0, 1e-16);
+  const double log_lower = std::log(lower);
+  h.bin_edges.resize(bins + 1);
+  for (int b = 0; b <= bins; ++b) h.bin_edges[b] = std::exp(log_lower * (1.0 - double(b) / bins));
+  h.bin_edges[bins] = 1.0;
+  h.positive.assign(bins, 0.0);
+  h.negative.assign(bins, 0.0);
+  h.positive_counts = pos;
+  h.negative_counts = neg;
+  uint64_t total = 0;
+  for (int b = 0; b < bins; ++b) total += pos[b] + neg[b];
+  h.total_terms = total;
+  if (total == 0) return h;
+  const double inv_norm = 1.0 / double(total);
+  // same sequence of roundings as the reference's per-string accumulation
+  for (int b = 0; b < bins; ++b) {
+    double sp = 0.0, sn = 0.0;
+    for (uint64_t k = 0; k < pos[b]; ++k) sp += inv_norm;
+    for (uint64_t k = 0; k < neg[b]; ++k) sn += inv_norm;
+    h.positive[b] = sp;
+    h.negative[b] = sn;
+  }
+  return h;
+}
+
+DensityHistogram density_histogram(const Engine& engine, int bins, double epsilon0, double global_max) {
+  if (bins < 1) throw std::invalid_argument("histogram needs at least 1 bin");
+  std::vector<uint64_t> pos(bins), neg(bins);
+  engine.check(pp_density_histogram(engine.handle(), bins, global_max, epsilon0, pos.data(), neg.data()));
+  return histogram_from_counts(bins, epsilon0, pos, neg);
+}
+DensityHistogram density_histogram(const Engine& engine, int bins, double epsilon0) {
+  return density_histogram(engine, bins, epsilon0, engine.global_max());
+}
+
+std::string DensityHistogram::to_tsv() const {
+  std::ostringstream out;
+  out << "bin_low\tbin_high\tsign\tnormalized_count\n";
+  for (size_t b = 0; b + 1 < bin_edges.size(); ++b) {
+    out << fmt17(bin_edges[b]) << '\t' << fmt17(bin_edges[b + 1]) << "\t+\t" << fmt17(positive[b]) << '\n';
+    out << fmt17(bin_edges[b]) << '\t' << fmt17(bin_edges[b + 1]) << "\t-\t" << fmt17(negative[b]) << '\n';
+  }
+  return out.str();
+}
+
+void dump_operator(std::ostream& out, const SparseOperator& op) {
+  for (size_t i = 0; i < op.keys.size(); ++i) out << to_hex(op.keys[i], op.n) << ' ' << fmt17(op.values[i]) << '\n';
+}
+
+static void sort_operator(SparseOperator& op) {
+  std::vector<size_t> idx(op.keys.size());
+  for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+  auto less = [&](size_t a, size_t b) {
+    for (int k = kIndexWords - 1; k >= 0; --k)
+      if (op.keys[a].words[k] != op.keys[b].words[k]) return op.keys[a].words[k] < op.keys[b].words[k];
+    return false;
+  };
+  std::sort(idx.begin(), idx.end(), less);
+  SparseOperator out;
+  out.n = op.n;
+  for (size_t i : idx) {
+    if (!out.keys.empty() && out.keys.back() == op.keys[i]) {
+      out.values.back() += op.values[i];
+      continue;
+    }
+    out.keys.push_back(op.keys[i]);
+    out.values.push_back(op.values[i]);
+  }
+  op = std::move(out);
+}
+
+SparseOperator load_dump(std::istream& in, int n) {
+  SparseOperator op;
+  op.n = n;
+  std::string line;
+  while (std::getline(in, line)) {
+    if (line.empty() || line[0] == '#') continue;
+    std::istringstream ls(line);
+    std::string hex;
+    double value;
+    if (!(ls >> hex >> value)) throw std::invalid_argument("malformed dump line: " + line);
+    op.keys.push_back(from_hex(hex, n));
+    op.values.push_back(value);
+  }
+  sort_operator(op);
+  return op;
+}
+
+static const char kBinMagic[4] = {'P', 'P', 'B', '1'};
+
+void write_shard_file(const std::string& path, const SparseOperator& op, bool binary) {
+  std::ofstream out(path, binary ? std::ios::binary : std::ios::out);
+  if (!out) throw std::runtime_error("cannot write " + path);
+  if (!binary) {
+    dump_operator(out, op);
+  } else {
+    const uint32_t n = (uint32_t)op.n;
+    const uint64_t count = op.keys.size();
+    out.write(kBinMagic, 4);
+    out.write(reinterpret_cast<const char*>(&n), 4);
+    out.write(reinterpret_cast<const char*>(&count), 8);
+    for (const auto& k : op.keys) out.write(reinterpret_cast<const char*>(k.words.data()), 8 * kIndexWords);
+    out.write(reinterpret_cast<const char*>(op.values.data()), 8 * count);
+  }
+  if (!out) throw std::runtime_error("write failed: " + path);
+}
+
+static SparseOperator read_shard_file(const std::string& path, int n) {
+  const bool binary = path.size() > 4 && path.compare(path.size() - 4, 4, ".ppb") == 0;
+  std::ifstream in(path, binary ? std::ios::binary : std::ios::in);
+  if (!in) throw std::invalid_argument("cannot open checkpoint shard " + path);
+  if (!binary) return load_dump(in, n);
+  char magic[4];
+  uint32_t fn = 0;
+  uint64_t count = 0;
+  in.read(magic, 4);
+  in.read(reinterpret_cast<char*>(&fn), 4);
+  in.read(reinterpret_cast<char*>(&count), 8);
+  if (!in || std::memcmp(magic, kBinMagic, 4) != 0) throw std::invalid_argument("not a binary shard: " + path);
+  if ((int)fn != n) throw std::invalid_argument("shard " + path + " width does not match the manifest");
+  SparseOperator op;
+  op.n = n;
+  op.keys.resize(count);
+  op.values.resize(count);
+  for (auto& k : op.keys) in.read(reinterpret_cast<char*>(k.words.data()), 8 * kIndexWords);
+  in.read(reinterpret_cast<char*>(op.values.data()), 8 * count);
+  if (!in) throw std::invalid_argument("truncated binary shard " + path);
+  sort_operator(op);
+  return op;
+}
+
+void write_checkpoint_manifest(const std::string& dir, int layer, int qubits, double epsilon0,
+                               const std::vector<std::pair<std::string, uint64_t>>& files) {
+  std::ofstream mf(dir + "/manifest.json");
+  if (!mf) throw std::runtime_error("cannot write " + dir + "/manifest.json");
+  mf << "{\n  \"schema\": 1,\n  \"layer\": " << layer << ",\n  \"qubits\": " << qubits
+     << ",\n  \"workers\": " << files.size() << ",\n  \"epsilon0\": " << fmt17(epsilon0)
+     << ",\n  \"shard_map\": \"z-plane splitmix hash\",\n  \"files\": [";
+  for (size_t m = 0; m < files.size(); ++m) {
+    mf << (m ? "," : "") << "\n    {\n      \"path\": \"" << files[m].first << "\",\n      \"terms\": "
+       << files[m].second << ",\n      \"worker\": " << m << "\n    }";
+  }
+  mf << "\n  ]\n}\n";
+}
+
+void write_checkpoint(const std::string& dir, const Engine& engine, int layer, bool binary) {
+  for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p (fs::create_directories in runner.cpp:54)
+    if (i == dir.size() || dir[i] == '/') ::mkdir(dir.substr(0, i).c_str(), 0777);
+  SparseOperator op = engine.merged();
+  const std::string name = binary ? "shard_0.ppb" : "shard_0.txt";
+  write_shard_file(dir + "/" + name, op, binary);
+  write_checkpoint_manifest(dir, layer, engine.num_qubits(), engine.config().policy.epsilon0,
+                            {{name, (uint64_t)op.keys.size()}});
+}
+
+// minimal reader for the manifest keys we need (nlohmann's dump(2) layout and ours)
+static bool json_number(const std::string& text, const std::string& key, double* out) {
+  size_t p = text.find("\"" + key + "\"");
+  if (p == std::string::npos) return false;
+  p = text.find(':', p);
+  if (p == std::string::npos) return false;
+  *out = std::strtod(text.c_str() + p + 1, nullptr);
+  return true;
+}
+
+Checkpoint read_checkpoint(const std::string& dir) {
+  std::ifstream mf(dir + "/manifest.json");
+  if (!mf) throw std::invalid_argument("no manifest.json in " + dir);
+  std::string text((std::istreambuf_iterator<char>(mf)), std::istreambuf_iterator<char>());
+  Checkpoint ck;
+  double v = 0;
+  if (!json_number(text, "layer", &v)) throw std::invalid_argument("manifest has no layer");
+  ck.layer = (int)v;
+  if (!json_number(text, "qubits", &v)) throw std::invalid_argument("manifest has no qubits");
+  ck.qubits = (int)v;
+  if (json_number(text, "epsilon0", &v)) ck.epsilon0 = v;
+  ck.op.n = ck.qubits;
+  std::vector<std::string> paths;
+  for (size_t p = text.find("\"path\""); p != std::string::npos; p = text.find("\"path\"", p + 6)) {
+    size_t a = text.find('"', text.find(':', p) + 1);
+    size_t b = text.find('"', a + 1);
+    if (a == std::string::npos || b == std::string::npos) throw std::invalid_argument("malformed manifest");
+    paths.push_back(text.substr(a + 1, b - a - 1));
+  }
+  if (paths.empty()) throw std::invalid_argument("manifest lists no shard files");
+  for (const auto& name : paths) {
+    SparseOperator part = read_shard_file(dir + "/" + name, ck.qubits);
+    ck.op.keys.insert(ck.op.keys.end(), part.keys.begin(), part.keys.end());
+    ck.op.values.insert(ck.op.values.end(), part.values.begin(), part.values.end());
+  }
+  sort_operator(ck.op);
+  return ck;
 }
 
 }  // namespace pauliprop

@@ -215,8 +215,9 @@ class Engine {
   void set_layer_context(int t) { layer_context_ = t; }
   pp_engine* handle() const { return handle_; }
 
+  void check(int rc) const;  // C-ABI return code -> the reference's exception types
+
  private:
-  void check(int rc) const;
   EngineConfig config_;
   pp_engine* handle_ = nullptr;
   int layer_context_ = 0;
@@ -226,10 +227,58 @@ enum class ReadoutMode { ZeroState, TrackedCoefficient };
 
 struct RunOptions {
   ReadoutMode readout = ReadoutMode::ZeroState;
+  // Resume: layers t <= start_layer are already folded into the engine's
+  // operator (loaded from checkpoint_t<start_layer>); propagation continues
+  // at t = start_layer + 1.  The reference writes checkpoints but has no
+  // resume path (runner.cpp:52-77, 180-183).
+  int start_layer = 0;
   PauliString tracked_index;
   std::function<void(const LayerRecord&, const Engine&)> on_layer;
   std::function<void(int t, size_t gate_index, double value)> on_gate_readout;
 };
+
+// ------------------------------------------------------------ diagnostics and checkpoints
+// Coefficient density, log-binned with a sign split (sparse_operator.hpp
+// DensityHistogram, sparse_operator.cpp:150-197).  The GPU counts (exact
+// integers, pp_density_histogram); positive/negative are the reference's
+// normalized values: 1/total summed count times, in the same order of
+// additions, so the TSV is byte-identical.
+struct DensityHistogram {
+  std::vector<double> bin_edges;
+  std::vector<double> positive;
+  std::vector<double> negative;
+  std::vector<uint64_t> positive_counts;
+  std::vector<uint64_t> negative_counts;
+  uint64_t total_terms = 0;
+  std::string to_tsv() const;  // sparse_operator.cpp:136-148
+};
+DensityHistogram histogram_from_counts(int bins, double epsilon0, const std::vector<uint64_t>& positive_counts,
+                                       const std::vector<uint64_t>& negative_counts);
+DensityHistogram density_histogram(const Engine& engine, int bins, double epsilon0);
+DensityHistogram density_histogram(const Engine& engine, int bins, double epsilon0, double global_max);
+
+// Shard dump: one "<hex index> <%.17g coefficient>" line per string
+// (SparseOperator::dump/load_dump, sparse_operator.cpp:99-122).
+void dump_operator(std::ostream& out, const SparseOperator& op);
+SparseOperator load_dump(std::istream& in, int n);
+
+// Checkpoint directory of runner.cpp:52-77: shard_<m>.txt (or the binary
+// shard_<m>.ppb: "PPB1", n, count, count x 4 index words, count doubles) plus
+// manifest.json {schema, layer, qubits, workers, ..., epsilon0, files}.
+// read_checkpoint accepts the reference's own checkpoints (any worker count;
+// duplicate keys across shards are added, which cannot happen for a valid
+// sharding) and ours.
+struct Checkpoint {
+  int layer = 0;
+  int qubits = 0;
+  double epsilon0 = 0.0;
+  SparseOperator op;
+};
+void write_shard_file(const std::string& path, const SparseOperator& op, bool binary);
+void write_checkpoint_manifest(const std::string& dir, int layer, int qubits, double epsilon0,
+                               const std::vector<std::pair<std::string, uint64_t>>& files);
+void write_checkpoint(const std::string& dir, const Engine& engine, int layer, bool binary = false);
+Checkpoint read_checkpoint(const std::string& dir);
 
 // Heisenberg loop of engine.cpp:394-446: layers last to first, gates in
 // reverse order, optional per-layer truncation, readout after truncation.

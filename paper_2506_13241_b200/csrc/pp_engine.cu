@@ -238,6 +238,7 @@ class EngineBase {
                            uint64_t* counts) = 0;
   virtual void shard_ingest(const uint64_t* rec, uint64_t count) = 0;
   virtual double norm2() = 0;
+  virtual void histogram(int bins, double gmax, double epsilon0, uint64_t* pos, uint64_t* neg) = 0;
 };
 
 template <int W>
@@ -880,6 +881,24 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
     return h;
+  }
+
+  void histogram(int bins, double gmax, double epsilon0, uint64_t* pos, uint64_t* neg) override {
+    sync_state();
+    for (int b = 0; b < bins; ++b) pos[b] = neg[b] = 0;
+    if (G_ == 0) return;
+    const double lower = std::max(epsilon0, 1e-16);
+    evict_cnt_.ensure(16 * (size_t)bins);
+    unsigned long long* d = evict_cnt_.as<unsigned long long>();
+    PP_CUDA(cudaMemsetAsync(d, 0, 16 * (size_t)bins, stream_));
+    push_scalars(bseq_);
+    const size_t smem = 8 * (size_t)bins;
+    k_histogram<W><<<persistent_grid(), kCta, smem, stream_>>>(gview(gcur_), aview(cur_), d_stats_, bins, gmax,
+                                                               lower, std::log(lower), d, d + bins);
+    ++launches_;
+    PP_CUDA(cudaMemcpyAsync(pos, d, 8 * (size_t)bins, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaMemcpyAsync(neg, d + bins, 8 * (size_t)bins, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaStreamSynchronize(stream_));
   }
 
   void shard_evict(uint32_t world, uint32_t rank, uint64_t seed, uint64_t* out, uint64_t cap,
@@ -1647,6 +1666,17 @@ int pp_record_words(const pp_engine* e) { return e ? e->impl->record_words() : 0
 int pp_norm2(pp_engine* e, double* out) {
   if (!e || !out) return PP_ERR_INVALID;
   return guarded(e, [&] { *out = e->impl->norm2(); });
+}
+
+int pp_density_histogram(pp_engine* e, int bins, double global_max, double epsilon0, uint64_t* positive,
+                         uint64_t* negative) {
+  if (!e || !positive || !negative || bins < 1 || bins > ppgpu::kMaxHistBins) return PP_ERR_INVALID;
+  return guarded(e, [&] {
+    if (e->impl->term_count() > 0 && !(global_max > 0))
+      throw ppgpu::EngineError(PP_ERR_INVALID,
+                               "density_histogram needs a positive global maximum for a nonempty operator");
+    e->impl->histogram(bins, global_max, epsilon0, positive, negative);
+  });
 }
 
 int pp_shard_evict(pp_engine* e, uint32_t world, uint32_t rank, uint64_t seed, uint64_t* records, uint64_t cap,

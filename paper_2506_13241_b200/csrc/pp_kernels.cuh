@@ -1329,6 +1329,47 @@ __global__ void __launch_bounds__(kCta) k_norm2(GroupView<W> g, ArenaView<W> ar,
 }
 
 // ---------------------------------------------------------------------------
+// log-binned coefficient density with a sign split (sparse_operator.cpp:
+// 150-197): bin 0 holds |c/gmax| <= lower, bin bins-1 holds >= 1, the rest
+// int(bins * (1 - log|x| / log lower)).  Counts are exact integers; the host
+// turns them into the reference's normalized sums.  Reads 8 B per string.
+// ---------------------------------------------------------------------------
+constexpr int kMaxHistBins = 4096;
+
+template <int W>
+__global__ void __launch_bounds__(kCta) k_histogram(GroupView<W> g, ArenaView<W> ar, const DevStats* st, int bins,
+                                                   double gmax, double lower, double log_lower,
+                                                   unsigned long long* pos, unsigned long long* neg) {
+  extern __shared__ unsigned int hist[];  // [2 * bins]: positive then negative
+  for (int b = threadIdx.x; b < 2 * bins; b += kCta) hist[b] = 0;
+  __syncthreads();
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+    const uint32_t n = g.cnt[gid];
+    const uint64_t off = g.off[gid];
+    for (uint32_t i = threadIdx.x; i < n; i += kCta) {
+      const double x = ar.c[off + i] / gmax;
+      const double ax = fabs(x);
+      int b;
+      if (ax <= lower) {
+        b = 0;
+      } else if (ax >= 1.0) {
+        b = bins - 1;
+      } else {
+        b = (int)((double)bins * (1.0 - log(ax) / log_lower));
+        b = b < 0 ? 0 : (b > bins - 1 ? bins - 1 : b);
+      }
+      atomicAdd(&hist[(x < 0 ? bins : 0) + b], 1u);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < bins; b += kCta) {
+    if (hist[b]) atomicAdd(&pos[b], (unsigned long long)hist[b]);
+    if (hist[bins + b]) atomicAdd(&neg[b], (unsigned long long)hist[bins + b]);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // diagonal strings (x == 0 is the smallest key of a group, so it can only be
 // the first element): <0|O|0> terms (sparse_operator.cpp:32-36, 89-97)
 // ---------------------------------------------------------------------------

@@ -18,6 +18,7 @@ threads of one process.  The exchange is host-staged in this version.
 """
 from __future__ import annotations
 
+import os
 import threading
 from typing import List, Sequence
 
@@ -173,6 +174,10 @@ class GpuShard:
     def take_counters(self):
         return self.engine.take_counters()
 
+    def histogram_counts(self, bins, epsilon0, gmax):
+        h = self.engine.density_histogram(bins, epsilon0, gmax)
+        return np.asarray(h["positive_counts"], np.uint64), np.asarray(h["negative_counts"], np.uint64)
+
 
 def _is_local(gate) -> bool:
     """Generators that never change z (a single X): rank-local branch."""
@@ -305,15 +310,61 @@ class ShardedEngine:
         order = np.lexsort((words[:, 0], words[:, 1], words[:, 2], words[:, 3]))
         return words[order], coeffs[order]
 
-    def run_circuit(self, circuit):
-        """run_circuit (engine.cpp:394-446) over the sharded operator."""
+    # -- diagnostics and checkpoints
+    def density_histogram(self, bins, epsilon0=None):
+        """Global density histogram (sparse_operator.cpp:150-197): per-rank
+        device counts summed over ranks, normalized once."""
+        from . import _pauliprop as _impl
+        eps = self.eps if epsilon0 is None else float(epsilon0)
+        pos, neg = self.b.histogram_counts(bins, eps, self.gmax)
+        tot = self.comm.allreduce(np.concatenate([pos, neg]).astype(np.float64), "sum")  # exact below 2^53
+        tot = tot.astype(np.uint64)
+        return _impl.histogram_from_counts(bins, eps, tot[:bins].tolist(), tot[bins:].tolist())
+
+    def write_checkpoint(self, directory, layer, binary=False):
+        """runner.cpp:52-77 layout: every rank writes its own shard file,
+        rank 0 the manifest."""
+        from . import _pauliprop as _impl
+        os.makedirs(directory, exist_ok=True)
+        w, c = self.b.export()
+        name = f"shard_{self.comm.rank}.{'ppb' if binary else 'txt'}"
+        _impl.write_shard_file(os.path.join(directory, name), np.asarray(w), np.asarray(c), self.n, binary)
+        files = self.comm.allgather((name, int(len(c))))
+        if self.comm.rank == 0:
+            _impl.write_checkpoint_manifest(directory, int(layer), self.n, self.eps, files)
+        self.comm.allgather(None)  # the manifest exists once any rank returns
+
+    def load_checkpoint(self, directory):
+        """Loads a checkpoint written by any rank count (or by the
+        reference); each rank keeps the strings it owns.  Returns the layer."""
+        from . import _pauliprop as _impl
+        ck = _impl.read_checkpoint(directory)
+        if ck["qubits"] != self.n:
+            raise ValueError(f"checkpoint has {ck['qubits']} qubits, engine {self.n}")
+        self.set_initial(ck["words"], ck["coeffs"])
+        return int(ck["layer"])
+
+    def run_circuit(self, circuit, start_layer=0, out_dir="", histogram_bins=0, checkpoint_every=0,
+                    binary_checkpoint=False):
+        """run_circuit (engine.cpp:394-446) over the sharded operator, with
+        the runner's per-layer outputs (runner.cpp:173-183) and resume."""
         rows = []
         L = circuit.num_layers()
-        for t in range(1, L + 1):
+        if not 0 <= start_layer <= L:
+            raise ValueError(f"start_layer {start_layer} outside [0, {L}]")
+        for t in range(start_layer + 1, L + 1):
             layer = circuit.layers[L - t]
             self.apply_gates(list(reversed(layer)))
             if not self.per_gate:
                 self.truncate_now()
             rows.append({"t": t, "observable": self.expectation_zero_state(), "term_count": self.term_count(),
                          "global_max": self.gmax})
+            if out_dir and histogram_bins > 0 and self.gmax > 0:
+                h = self.density_histogram(histogram_bins)
+                if self.comm.rank == 0:
+                    os.makedirs(out_dir, exist_ok=True)
+                    with open(os.path.join(out_dir, f"histogram_t{t}.tsv"), "w") as f:
+                        f.write(h["tsv"])
+            if out_dir and checkpoint_every > 0 and t % checkpoint_every == 0:
+                self.write_checkpoint(os.path.join(out_dir, f"checkpoint_t{t}"), t, binary_checkpoint)
         return rows

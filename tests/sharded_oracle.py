@@ -63,3 +63,6 @@ class OracleShard:
 
     def export(self):
         return self.eng.export()
+
+    def histogram_counts(self, bins, epsilon0, gmax):
+        return self.eng.density_histogram(bins, epsilon0, gmax)

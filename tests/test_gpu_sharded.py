@@ -67,3 +67,56 @@ def test_sharded_gpu_matches_single(pp, O, case, world):
             assert a["term_count"] == b["term_count"]
             assert abs(a["observable"] - b["observable"]) <= 1e-12 * max(1.0, abs(b["observable"]))
     assert sum(x[3] for x in res) > 0
+
+
+def test_sharded_gpu_histogram_and_resume(pp, O, tmp_path):
+    """Device histograms summed over 2 ranks equal the single engine's TSV;
+    a 2-rank checkpoint resumes on 3 ranks to the single engine's result."""
+    from paper_2506_13241_b200.sharded import GpuShard, ShardedEngine, ThreadComm
+
+    n, eps, L, k = 127, 1e-4, 5, 3
+    circ = pp.build_kicked_ising(pp.heavy_hex_127(), 0.3, "-0.5pi", L)
+    z62 = O.site_word(62, 3)[None]
+    single = pp.Engine(n, eps, "gate")
+    single.set_initial(z62, [1.0])
+    single.run_circuit(circ)
+    sw, sc = single.export()
+    want = single.density_histogram(32)["tsv"]
+    out = str(tmp_path / "run")
+
+    def run(world, fn):
+        comms = ThreadComm.make(world)
+        res, errs = [None] * world, []
+
+        def main(r):
+            try:
+                res[r] = fn(comms[r])
+            except Exception as exc:  # pragma: no cover
+                errs.append(exc)
+                comms[r].hub.barrier.abort()
+
+        th = [threading.Thread(target=main, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        return res
+
+    def first(comm):
+        se = ShardedEngine(GpuShard(n, eps, "gate"), n, comm, eps, "gate")
+        se.set_initial(z62, [1.0])
+        se.run_circuit(circ, out_dir=out, histogram_bins=32, checkpoint_every=k, binary_checkpoint=True)
+        return se.density_histogram(32)["tsv"]
+
+    assert all(t == want for t in run(2, first))
+
+    def second(comm):
+        se = ShardedEngine(GpuShard(n, eps, "gate"), n, comm, eps, "gate")
+        assert se.load_checkpoint(f"{out}/checkpoint_t{k}") == k
+        se.run_circuit(circ, start_layer=k)
+        return se.export()
+
+    for w, c in run(3, second):
+        assert_same_terms(w, c, sw, sc, "gpu sharded resume 2 -> 3 ranks")

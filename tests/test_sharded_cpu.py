@@ -5,6 +5,7 @@ global sums.  Each rank's local engine is the oracle restatement
 for bit, for any rank count (the reference's worker-independence contract,
 test_engine.cpp:211-258).  Ranks run as threads (ThreadComm) and, for the
 real multi-process path, as world_size-2 gloo processes (TorchComm)."""
+import json
 import math
 import os
 import threading
@@ -149,3 +150,65 @@ def test_sharded_gloo_world2_matches_single(pp, O, tmp_path):
     ow, oc = ora.export()
     assert_same_terms(res["w"], res["c"], ow, oc, "gloo world=2")
     assert int(res["tc"]) == ora.term_count()
+
+
+def _run_threads(world, fn):
+    from paper_2506_13241_b200.sharded import ThreadComm
+    comms = ThreadComm.make(world)
+    results, errors = [None] * world, []
+
+    def main(r):
+        try:
+            results[r] = fn(comms[r])
+        except Exception as exc:  # pragma: no cover
+            errors.append(exc)
+            comms[r].hub.barrier.abort()
+
+    th = [threading.Thread(target=main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errors:
+        raise errors[0]
+    return results
+
+
+def test_sharded_histogram_and_checkpoint_resume(pp, O, tmp_path):
+    """Global histogram = the single engine's (counts summed over ranks);
+    a checkpoint written by 3 ranks resumes on 2 ranks and finishes with the
+    single-engine result bit for bit."""
+    from paper_2506_13241_b200.sharded import ShardedEngine
+    from sharded_oracle import OracleShard
+
+    n, eps, L, k = 127, 1e-4, 4, 2
+    g = pp.load_geometry(ref_geometry_text())
+    circ = pp.build_kicked_ising(g, 0.3, "-0.5pi", L)
+    init = [(O.site_word(62, 3), 1.0)]
+    ora = single_oracle(O, n, circ, init, eps, "gate")
+    ow, oc = ora.export()
+    pos, neg = ora.density_histogram(16, eps)
+    want_tsv = pp.histogram_from_counts(16, eps, pos.tolist(), neg.tolist())["tsv"]
+    out = str(tmp_path / "run")
+
+    def first(comm):
+        se = ShardedEngine(OracleShard(n, eps), n, comm, eps, "gate")
+        se.set_initial(O.site_word(62, 3)[None], [1.0])
+        se.run_circuit(circ, out_dir=out, histogram_bins=16, checkpoint_every=k)
+        return se.density_histogram(16)["tsv"]
+
+    tsvs = _run_threads(3, first)
+    assert all(t == want_tsv for t in tsvs)
+    assert open(os.path.join(out, f"histogram_t{L}.tsv")).read() == want_tsv
+    man = json.load(open(os.path.join(out, f"checkpoint_t{k}", "manifest.json")))
+    assert len(man["files"]) == 3 and man["layer"] == k
+
+    def second(comm):
+        se = ShardedEngine(OracleShard(n, eps), n, comm, eps, "gate")
+        assert se.load_checkpoint(os.path.join(out, f"checkpoint_t{k}")) == k
+        rows = se.run_circuit(circ, start_layer=k)
+        return rows, se.export()
+
+    for rows, (w, c) in _run_threads(2, second):
+        assert [r["t"] for r in rows] == list(range(k + 1, L + 1))
+        assert_same_terms(w, c, ow, oc, "sharded resume 3 -> 2 ranks")

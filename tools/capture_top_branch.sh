@@ -4,7 +4,7 @@
 set -e
 W=$1; OUT=$2
 python tools/profile_run.py $W > gpurun_out/${OUT}_plain.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_branch_x --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:${KRE:-k_branch_x} --csv \
     --log-file gpurun_out/${OUT}_branch_launches.csv python tools/profile_run.py $W > /dev/null 2>&1
 IDX=$(python - "$OUT" <<'PY'
 import csv, sys
@@ -18,5 +18,5 @@ print(max(vals)[1])
 PY
 )
 echo "top launch index $IDX"
-ncu --set full --clock-control none --import-source on -k regex:k_branch_x -s $IDX -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:${KRE:-k_branch_x} -s $IDX -c 1 \
     -o gpurun_out/${OUT} python tools/profile_run.py $W > /dev/null 2>&1
