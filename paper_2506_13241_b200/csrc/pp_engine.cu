@@ -147,7 +147,13 @@ class DevicePool {
     }
     if (e != cudaSuccess) {
       cudaGetLastError();
-      if (e == cudaErrorMemoryAllocation) throw EngineError(PP_ERR_RESOURCE, "device memory exhausted");
+      if (e == cudaErrorMemoryAllocation) {
+        size_t fb = 0, tb = 0;
+        cudaMemGetInfo(&fb, &tb);
+        throw EngineError(PP_ERR_RESOURCE, "device memory exhausted (request " + std::to_string(bytes >> 20) +
+                                               " MiB, free " + std::to_string(fb >> 20) + " MiB of " +
+                                               std::to_string(tb >> 20) + " MiB)");
+      }
       throw EngineError(PP_ERR_INTERNAL, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     }
     *got = bytes;
@@ -260,8 +266,31 @@ class EngineImpl final : public EngineBase {
                                  (int)sizeof(SortSmem<W>)));
     PP_CUDA(cudaFuncSetAttribute(k_sort_big<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)big_sort_smem()));
+    PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    {  // persistent branch grids: every resident CTA slot of the device
+      int sms = 148, occ_x = 1, occ_s = 1;
+      PP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
+      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_branch_x<W>, kCta, branch_smem_bytes<W>()));
+      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_branch_sublayer<W>, kCta,
+                                                            branch_smem_bytes<W>()));
+      branch_grid_ = (uint32_t)(sms * std::max(occ_x, 1));
+      sub_grid_ = (uint32_t)(sms * std::max(occ_s, 1));
+      if (std::getenv("PP_DEBUG"))
+        std::fprintf(stderr, "[pp] W=%d branch CTAs/SM %d, sublayer CTAs/SM %d, smem %zu\n", W, occ_x, occ_s,
+                     branch_smem_bytes<W>());
+    }
     keep_zeros_ = cfg.cadence == PP_CADENCE_LAYER;
     seed_ = 0x5eed5eed12345678ull;
+    // Memory plan: two arenas (current + compaction/regroup target) of at
+    // most arena_max_ strings each, plus ~8 B per string of regroup slots
+    // and a fixed reserve for tables and scratch.
+    size_t free_b = 0, total_b = 0;
+    PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double frac = cfg.mem_fraction > 0 && cfg.mem_fraction <= 1 ? cfg.mem_fraction : 0.92;
+    const double budget = (double)free_b * frac - (double)(3ull << 30);
+    arena_max_ = budget > 0 ? (uint64_t)(budget / (double)(2 * R + 16)) : (1ull << 20);
+    tight_arena_ = std::getenv("PP_TIGHT_ARENA") != nullptr;
   }
   ~EngineImpl() override {
     cudaStreamSynchronize(stream_);
@@ -451,7 +480,7 @@ class EngineImpl final : public EngineBase {
         push_scalars(seq0);
         std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
         PP_CUDA(cudaEventRecord(ev.first, stream_));
-        k_branch_sublayer<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+        k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
             gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], nullptr, nullptr, d_stats_);
         PP_CUDA(cudaEventRecord(ev.second, stream_));
         pending_events_.push_back(ev);
@@ -481,14 +510,24 @@ class EngineImpl final : public EngineBase {
     if (speculate && no_budget && do_trunc && !external() && cfg_.epsilon0 > 0.0 && count <= (size_t)kMaxSubGates &&
         G_ && !(cfg_.flags & PP_FLAG_PROFILE) && run_rx_speculative(prm, seq0, t0))
       return;
+    // per-gate truncation without a budget: deferred (k_thresh / k_flush)
+    const bool lazy = epi && do_trunc && no_budget && !external() && cfg_.epsilon0 > 0.0 && !keep_zeros_ &&
+                      count + 2 <= kLazyWindow && std::getenv("PP_EAGER_TRUNCATION") == nullptr;
+    if (lazy) thr_.ensure(kLazyWindow * sizeof(double));
     size_t pos = 0;
     while (pos < count && G_) {
       sync_state();
       if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
       const bool use_graph = pos == 0 && !(cfg_.flags & PP_FLAG_PROFILE);
       push_scalars(seq0 + pos);
+      if (lazy) {
+        PP_CUDA(cudaMemsetAsync(thr_.p, 0, 2 * sizeof(double), stream_));
+        lazy_open_ = true;
+        lazy_base_ = seq0 + pos;
+        lazy_len_ = (uint32_t)(count - pos);
+      }
       if (use_graph) {
-        cudaGraphExec_t exec = rx_graph(prm, epi, do_trunc, budget);
+        cudaGraphExec_t exec = rx_graph(prm, epi, do_trunc, budget, lazy);
         std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
         PP_CUDA(cudaEventRecord(ev.first, stream_));
         PP_CUDA(cudaGraphLaunch(exec, stream_));
@@ -502,12 +541,12 @@ class EngineImpl final : public EngineBase {
             ev = take_event_pair();
             PP_CUDA(cudaEventRecord(ev.first, stream_));
           }
-          launch_branch(prm[i], (uint32_t)(i - pos));
+          launch_branch(prm[i], (uint32_t)(i - pos), lazy);
           if (cfg_.flags & PP_FLAG_PROFILE) {
             PP_CUDA(cudaEventRecord(ev.second, stream_));
             pending_events_.push_back(ev);
           }
-          if (epi) launch_epilogue((uint32_t)(i - pos), do_trunc, budget);
+          if (epi) launch_epilogue((uint32_t)(i - pos), do_trunc, budget, lazy);
         }
       }
       branch_launches_ += count - pos;
@@ -573,7 +612,7 @@ class EngineImpl final : public EngineBase {
       push_scalars(seq0);
       std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
       PP_CUDA(cudaEventRecord(ev.first, stream_));
-      k_branch_sublayer<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+      k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
           gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_tpred, d_gmax, d_stats_);
       PP_CUDA(cudaEventRecord(ev.second, stream_));
       pending_events_.push_back(ev);
@@ -644,14 +683,15 @@ class EngineImpl final : public EngineBase {
     return false;  // did not converge: the caller runs the gates one by one
   }
 
-  void launch_branch(const RxParam& p, uint32_t rel) {
+  void launch_branch(const RxParam& p, uint32_t rel, bool lazy) {
     k_branch_x<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
         gview(gcur_), aview(cur_), p.wq, p.mq, p.cosv, p.sinv, keep_zeros_, gview(gcur_).z[p.wq],
-        &d_stats_->work[rel & 1], &d_stats_->work[(rel + 1) & 1], rel, d_stats_);
+        &d_stats_->work[rel & 1], &d_stats_->work[(rel + 1) & 1], rel, d_stats_,
+        lazy ? thr_.as<double>() : nullptr);
     ++launches_;
   }
 
-  cudaGraphExec_t rx_graph(const std::vector<RxParam>& prm, bool epi, bool do_trunc, bool budget) {
+  cudaGraphExec_t rx_graph(const std::vector<RxParam>& prm, bool epi, bool do_trunc, bool budget, bool lazy) {
     std::string key;
     auto put = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
     GroupView<W> gv = gview(gcur_);
@@ -665,8 +705,10 @@ class EngineImpl final : public EngineBase {
     put(&dev, sizeof(dev));
     int w = W;
     put(&w, sizeof(w));
-    int flags = (epi ? 1 : 0) | (do_trunc ? 2 : 0) | (budget ? 4 : 0) | (keep_zeros_ ? 8 : 0);
+    int flags = (epi ? 1 : 0) | (do_trunc ? 2 : 0) | (budget ? 4 : 0) | (keep_zeros_ ? 8 : 0) | (lazy ? 16 : 0);
     put(&flags, sizeof(flags));
+    void* thr = thr_.p;
+    put(&thr, sizeof(thr));
     for (const RxParam& p : prm) put(&p, sizeof(p));
     // process-wide cache: engines built one per simulate() call get the same
     // pooled buffers, so their graphs are identical and reused
@@ -681,8 +723,8 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     const uint64_t saved = launches_;
     for (size_t i = 0; i < prm.size(); ++i) {
-      launch_branch(prm[i], (uint32_t)i);
-      if (epi) launch_epilogue((uint32_t)i, do_trunc, budget);
+      launch_branch(prm[i], (uint32_t)i, lazy);
+      if (epi) launch_epilogue((uint32_t)i, do_trunc, budget, lazy);
     }
     launches_ = saved;
     PP_CUDA(cudaStreamEndCapture(stream_, &graph));
@@ -693,13 +735,33 @@ class EngineImpl final : public EngineBase {
     return exec;
   }
 
+  // arena capacity for the next compaction: room to grow ~2x without
+  // another compaction, generous for small states, never above the memory
+  // plan's arena_max_ (the other arena must fit too)
   uint64_t next_arena_target() {
-    const uint64_t need = 3 * live_ + 1024;
-    size_t free_b = 0, total_b = 0;
-    PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t afford = (uint64_t)((free_b + arena_[1 - cur_].buf.bytes) * 0.8) / R;
-    uint64_t target = std::max<uint64_t>(need, std::min<uint64_t>(std::max<uint64_t>(live_ * 8, 1ull << 24), afford));
-    return std::max<uint64_t>(target, std::min<uint64_t>(arena_[cur_].cap, afford));
+    if (tight_arena_) return live_ + live_ / 8 + 1024;  // test hook: exercise overflow and resume
+    const uint64_t lo = live_ + live_ / 8 + (1u << 16);
+    // 8x while two such arenas take at most half the plan, else 3x
+    const uint64_t want = std::max<uint64_t>(3 * live_ + 1024, std::min<uint64_t>(8 * live_, arena_max_ / 2));
+    uint64_t t = std::min<uint64_t>(std::max<uint64_t>(want, arena_[cur_].cap), arena_max_);
+    if (t < lo) {
+      if (lo > arena_max_)
+        throw EngineError(PP_ERR_RESOURCE, "device memory exhausted: " + std::to_string(live_) +
+                                               " live strings exceed the arena plan of " +
+                                               std::to_string(arena_max_) + " strings");
+      t = lo;
+    }
+    return t;
+  }
+
+  // regroup target arena: the exact output plus slack, within the plan
+  uint64_t regroup_arena(uint64_t total) {
+    if (total + 1 > arena_max_)
+      throw EngineError(PP_ERR_RESOURCE, "device memory exhausted: " + std::to_string(total) +
+                                             " strings after regroup exceed the arena plan of " +
+                                             std::to_string(arena_max_) + " strings");
+    if (tight_arena_) return total + 1024;
+    return std::min<uint64_t>(std::max<uint64_t>(total + (1u << 16), total + total / 2), arena_max_);
   }
 
   void truncate_now() override {
@@ -1080,8 +1142,18 @@ class EngineImpl final : public EngineBase {
   }
 
   // ----- garbage collection: compact the current arena into the other one
+  void mem_report(const char* what, uint64_t arg) {
+    if (!std::getenv("PP_DEBUG")) return;
+    size_t fb = 0, tb = 0;
+    cudaMemGetInfo(&fb, &tb);
+    std::fprintf(stderr, "[pp] %s %llu: live %llu bump %llu G %u arenas %llu/%llu (max %llu) free %zu MiB\n", what,
+                 (unsigned long long)arg, (unsigned long long)live_, (unsigned long long)bump_, G_,
+                 (unsigned long long)arena_[cur_].cap, (unsigned long long)arena_[1 - cur_].cap,
+                 (unsigned long long)arena_max_, fb >> 20);
+  }
   void gc_into_other(uint64_t new_cap) {
     sync_state();
+    mem_report("gc ->", new_cap);
     const int o = 1 - cur_;
     ensure_arena(o, new_cap);
     reset_stats(0);
@@ -1133,6 +1205,14 @@ class EngineImpl final : public EngineBase {
   }
   void sync_state() {
     if (!dirty_) return;
+    if (lazy_open_) {  // apply the deferred truncations of the last launch window
+      if (G_) {
+        k_flush<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), aview(cur_), thr_.as<double>(),
+                                                          (uint32_t)lazy_base_, lazy_len_, d_stats_);
+        ++launches_;
+      }
+      lazy_open_ = false;
+    }
     push_scalars(bseq_);
     k_red_reset<<<1, 1, 0, stream_>>>(&d_stats_->red[2]);
     if (G_) k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, &d_stats_->red[2]);
@@ -1190,9 +1270,15 @@ class EngineImpl final : public EngineBase {
     ++launches_;
   }
   // per-gate epilogue kernels for gate `rel` of a launch run (red slots by parity)
-  void launch_epilogue(uint32_t rel, bool do_truncate, bool budget) {
+  void launch_epilogue(uint32_t rel, bool do_truncate, bool budget, bool lazy = false) {
     RedSlot* r = &d_stats_->red[rel & 1];
     RedSlot* rn = &d_stats_->red[(rel + 1) & 1];
+    if (lazy) {  // deferred truncation: exact threshold now, removal at the next touch or flush
+      k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, r, thr_.as<double>(), rel);
+      k_thresh<W><<<1, kCta, 0, stream_>>>(cfg_.epsilon0, rel, r, rn, thr_.as<double>(), d_stats_);
+      launches_ += 2;
+      return;
+    }
     k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, r);
     k_truncate<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), aview(cur_), cfg_.epsilon0,
                                                            do_truncate ? 1 : 0, budget ? cfg_.max_terms : 0, rel, r,
@@ -1347,6 +1433,7 @@ class EngineImpl final : public EngineBase {
     sync_state();
     const uint64_t live = live_;
     if (G_ == 0 || live == 0) return;
+    mem_report("regroup maxrec", maxrec);
     const uint64_t max_items = (uint64_t)G_ + live / kItem + 1;
     items_.ensure(max_items * sizeof(Item));
     rec_slot_.ensure(live * maxrec * 4);
@@ -1359,7 +1446,10 @@ class EngineImpl final : public EngineBase {
     if (small) {
       while (tc < 2 * records_upper + 1024) tc <<= 1;
     } else {
-      while (tc < 2 * std::min<uint64_t>(records_upper, std::max<uint64_t>(8ull * G_, live / 4) + 1024)) tc <<= 1;
+      // distinct output z-groups: learned from the previous regroup; an
+      // overflow retries with a 4x larger table
+      const double est = std::max(2.0, 1.5 * zfactor_) * (double)G_;
+      while ((double)tc < 2.0 * std::min<double>((double)records_upper, est) + 1024) tc <<= 1;
     }
     uint64_t tc_max = 1024;
     while (tc_max < 2 * records_upper + 1024) tc_max <<= 1;
@@ -1389,7 +1479,7 @@ class EngineImpl final : public EngineBase {
         PP_CUDA(cudaGetLastError());
         if (h_stats_->overflow) {
           if (tc >= tc_max) throw EngineError(PP_ERR_INTERNAL, "regroup: hash table overflow");
-          tc = std::min(tc_max, tc * 8);
+          tc = std::min(tc_max, tc * 4);
           continue;
         }
         distinct = h_stats_->distinct;
@@ -1411,7 +1501,7 @@ class EngineImpl final : public EngineBase {
         groups_bound = distinct;
       }
       ensure_groups(1 - gcur_, std::max<uint32_t>(groups_bound, 1024));
-      ensure_arena(o, std::max<uint64_t>(total_bound + (1u << 16), (uint64_t)(total_bound * 1.5)));
+      ensure_arena(o, regroup_arena(total_bound));
       k_table_emit<W><<<(uint32_t)((tc + kCta - 1) / kCta), kCta, 0, stream_>>>(
           t, scan_gid_.as<unsigned long long>(), scan_off_.as<unsigned long long>(), gview(1 - gcur_), 0);
       k_scatter<W, P><<<(uint32_t)n_items, kCta, 0, stream_>>>(items_.as<Item>(), gview(gcur_), aview(cur_), prod, t,
@@ -1429,7 +1519,7 @@ class EngineImpl final : public EngineBase {
       // sort inside groups; the source arena is free now and serves as
       // scratch for the big-group merge passes
       const bool source_kept = arena_[cur_].cap >= total_bound + 1;
-      ensure_arena(cur_, total_bound + 1);
+      ensure_arena(cur_, std::min<uint64_t>(total_bound + 1, arena_max_));
       const uint32_t sort_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 16u));
       k_sort_small<W><<<sort_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o), keep_zeros_,
                                                                           d_stats_);
@@ -1445,6 +1535,7 @@ class EngineImpl final : public EngineBase {
         continue;
       }
       distinct = h_stats_->distinct;
+      zfactor_ = std::max(1.0, (double)distinct / (double)std::max<uint32_t>(G_, 1));
       const uint64_t total = h_stats_->scan_total;
       counters_.removed += h_stats_->removed;
       h_records_ = h_stats_->records;
@@ -1455,6 +1546,16 @@ class EngineImpl final : public EngineBase {
       live_ = live_bound_ = total - h_stats_->removed;
       reset_stats(bump_);  // cumulative counters were harvested above
       if (keep_zeros_) may_hold_zeros_ = true;
+      if ((uint64_t)tc * 48 + live * maxrec * 4 > (64ull << 20)) {
+        // large temporaries go back to the pool, where an allocation that
+        // does not fit can trim them (the arenas need the room)
+        PP_CUDA(cudaStreamSynchronize(stream_));
+        table_.release();
+        scan_gid_.release();
+        scan_off_.release();
+        rec_slot_.release();
+        items_.release();
+      }
       return;
     }
   }
@@ -1494,6 +1595,14 @@ class EngineImpl final : public EngineBase {
   int cur_ = 0, gcur_ = 0;
   uint32_t G_ = 0;
   uint64_t bump_ = 0, live_ = 0;
+  uint64_t arena_max_ = 0;  // per-arena capacity of the memory plan (strings)
+  bool tight_arena_ = false;  // PP_TIGHT_ARENA: minimal arenas (tests of the resume paths)
+  static constexpr size_t kLazyWindow = 4096;  // gates per deferred-truncation window
+  DevBuf thr_;                // thr[j] = max(T_j .. T_now) over the open window
+  bool lazy_open_ = false;
+  uint64_t lazy_base_ = 0;
+  uint32_t lazy_len_ = 0;
+  double zfactor_ = 4.0;     // distinct output groups per input group at the last regroup
   double gmax_ = 0.0, red_gmax_ = 0.0, red_gmin_ = 0.0;
   uint32_t red_nonfinite_ = 0;
   int keep_zeros_ = 0;
@@ -1504,6 +1613,7 @@ class EngineImpl final : public EngineBase {
   uint64_t arena_fault_seq_ = 0;
 
   uint32_t branch_grid_ = 148u * 2u;
+  uint32_t sub_grid_ = 148u * 2u;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_events_, free_events_;
   unsigned long long seed_;
   unsigned long long h_records_ = 0;

@@ -39,6 +39,17 @@ struct GroupView {
   uint32_t* stamp;  // sequence number of the last X-type gate applied (makes gates resumable)
 };
 
+// deferred truncation helpers (see k_thresh): a pending string is held as
+// -0.0 in shared memory (stored values are never zero when truncating per
+// gate), and a group's threshold slot follows from its stamp
+__device__ __forceinline__ bool is_pending(double c) {
+  return __double_as_longlong(c) == (long long)0x8000000000000000ull;
+}
+__device__ __forceinline__ uint32_t pending_index(uint32_t stamp, uint32_t win_base, uint32_t rel) {
+  const uint32_t idx = stamp - win_base;
+  return idx > rel ? 0u : idx;
+}
+
 // Per-gate scratch lives in small slot arrays so consecutive gates need no
 // reset launches: a gate's kernels use slot s and clear slot s^1 for the
 // next gate.
@@ -238,7 +249,7 @@ template <int W>
 __device__ void stream_branch_range(BranchSmem<W>& sm, ArenaView<W> ar, uint64_t src, uint32_t n, uint64_t dst,
                                     uint32_t& out_n, int wq, uint64_t mq, double cosv, double sinv, int keep_zeros,
                                     double& vmax, double& vmin, uint32_t& nonfinite, unsigned long long& records,
-                                    unsigned long long& removed, double tout, double& vall) {
+                                    unsigned long long& removed, double tout, double& vall, double tin = -1.0) {
   const uint32_t tid = threadIdx.x;
   const double nsin = -sinv;
   __syncthreads();
@@ -259,6 +270,7 @@ __device__ void stream_branch_range(BranchSmem<W>& sm, ArenaView<W> ar, uint64_t
         if (p < n) {
           key = load_plane<W>(ar.x, src + p);
           v = ar.c[src + p];
+          if (tin >= 0.0 && fabs(v) <= tin) v = -0.0;  // removed by a deferred truncation
           uint32_t cls = (key.w[wq] & mq) ? 1u : 0u;
           ok = (s == 0) || (s == 1 && cls == 0) || (s == 2 && cls == 1);
           if (s) key.w[wq] ^= mq;
@@ -319,7 +331,9 @@ __device__ void stream_branch_range(BranchSmem<W>& sm, ArenaView<W> ar, uint64_t
       }
       vall = fmax(vall, fabs(v));
       bool emit = tout < 0.0 ? (keep_zeros || v != 0.0) : !(fabs(v) <= tout);  // remove_below: |c| <= T
-      if (!emit) ++removed;
+      const bool pend = tin >= 0.0 && is_pending(c);
+      if (pend) ++removed;  // its deferred removal, counted once
+      if (!emit && !pend) ++removed;
       sk_store<W>(sm.skey, kSlots, rank, k);
       sm.sval[rank] = v;
       sm.semit[rank] = emit;
@@ -465,32 +479,80 @@ __device__ __forceinline__ uint32_t seg_lower_bound(const uint64_t* key, uint32_
   return lo;
 }
 
+// A pack: several small groups of one gate processed as one segment (their
+// strings side by side; a group start is always a block start), so a CTA
+// pays the per-segment passes once per ~kSeg strings instead of once per
+// group.  Built by k_branch_x; seg_branch<W, true> fills the per-group
+// output counts, offsets and statistics.
+constexpr uint32_t kMaxPack = 64;             // groups per pack
+constexpr uint32_t kPackMaxGroup = kSeg / 2;  // larger groups go one by one
+
+struct PackSmem {
+  uint32_t m;                       // groups in the pack
+  uint32_t gstart[kMaxPack + 1];    // first string of each group in the segment (+ end)
+  uint64_t src[kMaxPack];           // arena offset of each group
+  double tin[kMaxPack];             // deferred-truncation threshold per group (-1: none)
+  double mx[kMaxPack], mn[kMaxPack];
+  uint32_t cnt[kMaxPack], ostart[kMaxPack], nf[kMaxPack], gid[kMaxPack];
+};
+
+__device__ __forceinline__ uint32_t pack_group_of(const PackSmem& pk, uint32_t i) {
+  uint32_t lo = 0, hi = pk.m;  // largest k with gstart[k] <= i
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (pk.gstart[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
 // Processes the complete blocks at the front of S[p, n); returns how many
 // strings were consumed (0: the first block is longer than a segment).
+// PACK: the segment is the pack `pk` (all its strings, complete groups).
 // Per-string passes are striped (string i on thread i % kCta: conflict-free
 // shared memory); the three scans read flag bytes in a blocked layout.
-template <int W>
+template <int W, bool PACK = false>
 __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, uint32_t p, uint32_t n, uint64_t dst,
                                uint32_t& out_n, int wq, uint64_t mq, double cosv, double sinv, int keep_zeros,
                                double& vmax, double& vmin, uint32_t& nonfinite, unsigned long long& records,
-                               unsigned long long& removed, double tout, double& vall) {
+                               unsigned long long& removed, double tout, double& vall, double tin = -1.0,
+                               PackSmem* pk = nullptr) {
   const uint32_t tid = threadIdx.x;
   const uint64_t hmask = ~((mq << 1) - 1);  // bits above q in word wq
-  const uint32_t L = min(kSeg, n - p);
-  const uint32_t has_next = (p + L < n) ? 1u : 0u;
+  const uint32_t L = PACK ? pk->gstart[pk->m] : min(kSeg, n - p);
+  const uint32_t has_next = (!PACK && p + L < n) ? 1u : 0u;
+  const bool lazy = PACK ? pk->tin[0] >= 0.0 : tin >= 0.0;  // deferred truncation (uniform per launch)
   const double nsin = -sinv;
   const uint64_t* kq = sm.key + wq * (kSeg + 1);  // the plane word holding bit q
   __syncthreads();  // previous users of the shared buffers are done
   for (uint32_t i = tid; i < L + has_next; i += kCta) {
-    sk_store<W>(sm.key, kSeg + 1, i, load_plane<W>(ar.x, src + p + i));
-    if (i < L) sm.val[i] = ar.c[src + p + i];
+    uint64_t a;
+    double t;
+    if (PACK) {
+      const uint32_t k = pack_group_of(*pk, i);
+      a = pk->src[k] + (i - pk->gstart[k]);
+      t = pk->tin[k];
+    } else {
+      a = src + p + i;
+      t = tin;
+    }
+    sk_store<W>(sm.key, kSeg + 1, i, load_plane<W>(ar.x, a));
+    if (i < L) {
+      double v = ar.c[a];
+      if (t >= 0.0 && fabs(v) <= t) v = -0.0;  // removed by a deferred truncation
+      sm.val[i] = v;
+    }
   }
   __syncthreads();
-  // block starts (string i differs from i-1 above bit q)
+  // block starts (string i differs from i-1 above bit q; every group start)
   for (uint32_t i = tid; i < kSeg; i += kCta) {
     bool f = i < L && (i == 0 || !same_high<W>(sk_load<W>(sm.key, kSeg + 1, i - 1), sk_load<W>(sm.key, kSeg + 1, i),
                                                wq, hmask));
     sm.f[i] = f ? 1 : 0;
+  }
+  if (PACK) {
+    __syncthreads();
+    if (tid < pk->m) sm.f[pk->gstart[tid]] = 1;
   }
   __syncthreads();
   // scan 1 (blocked): block ids and starts
@@ -597,6 +659,11 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     const uint8_t fl = sm.f[i];
     Plane<W> k = sk_load<W>(sm.key, kSeg + 1, i);
     const bool cls1 = (k.w[wq] & mq) != 0;
+    const double c = sm.val[i];
+    // a string removed by a deferred truncation is counted once, here; its
+    // slot then behaves as absent (0 * cos + child == child, no record of 0)
+    const bool pc = lazy && is_pending(c);
+    if (pc) ++removed;
     if (cls1 && !(fl & 4)) continue;  // paired class-1: its class-0 partner owns the coset
     const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1], m = sm.bmid[b];
     const uint32_t lb = sm.lbv[i];
@@ -604,7 +671,6 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     const uint32_t ry = cls1 ? (lb - bs) + ((sm.pre[i] & 0xffffu) - um) : (i - bs) + ((sm.pre[lb] & 0xffffu) - um);
     const uint32_t ysz = (be - bs) - ((sm.pre[be] >> 16) - (sm.pre[bs] >> 16));
     const uint32_t s0 = sm.bobase[b] + ry, s1 = s0 + ysz;
-    const double c = sm.val[i];
     Plane<W> y = k, y1 = k;
     y.w[wq] &= ~mq;
     y1.w[wq] |= mq;
@@ -625,7 +691,7 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
         if (d1 != 0.0) t = __dadd_rn(t, d1);
         v1 = t;
         e1 = tout < 0.0 ? (keep_zeros || t != 0.0) : !(fabs(t) <= tout);
-        if (!e1) ++removed;
+        if (!e1 && !(lazy && is_pending(c1))) ++removed;
       } else {
         v1 = d1;
         e1 = d1 != 0.0 && !(fabs(d1) <= tout);
@@ -633,7 +699,7 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
       }
       v0 = s;
       e0 = tout < 0.0 ? (keep_zeros || s != 0.0) : !(fabs(s) <= tout);
-      if (!e0) ++removed;
+      if (!e0 && !pc) ++removed;
     } else {  // Y at q, no partner: the child y gets -sin c1
       const double d0 = __dmul_rn(nsin, c);
       if (d0 != 0.0) ++records;
@@ -642,7 +708,7 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
       if (d0 != 0.0 && !e0) ++removed;
       v1 = __dmul_rn(c, cosv);
       e1 = tout < 0.0 ? (keep_zeros || v1 != 0.0) : !(fabs(v1) <= tout);
-      if (!e1) ++removed;
+      if (!e1 && !pc) ++removed;
     }
     vall = fmax(vall, fmax(fabs(v0), fabs(v1)));
     sk_store<W>(sm.okey, 2 * kSeg, s0, y);
@@ -684,10 +750,54 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     const uint64_t d = dst + out_n + i;
     store_plane<W>(ar.x, d, sk_load<W>(sm.okey, 2 * kSeg, sl));
     ar.c[d] = val;
-    const double av = fabs(val);
-    if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
-    vmax = fmax(vmax, av);
-    vmin = fmin(vmin, av);
+    if (!PACK) {
+      const double av = fabs(val);
+      if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
+      vmax = fmax(vmax, av);
+      vmin = fmin(vmin, av);
+    }
+  }
+  if (PACK) {
+    // a group's slots and hence its outputs are contiguous: output range of
+    // group k = emitted slots in [bobase of its first block, next group's)
+    const uint32_t m = pk->m;
+    if (tid < m) {
+      const uint32_t sb = sm.bobase[sm.blk[pk->gstart[tid]]];
+      uint32_t lo = 0, hi = ecnt;  // emitted slots below sb
+      if (dense) {
+        lo = sb;
+      } else {
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (sm.cpos[mid] < sb) lo = mid + 1;
+          else hi = mid;
+        }
+      }
+      pk->ostart[tid] = lo;
+    }
+    __syncthreads();
+    // per-group statistics: one warp per group
+    const uint32_t lane = tid & 31;
+    for (uint32_t k = tid >> 5; k < m; k += kWarps) {
+      const uint32_t o0 = pk->ostart[k], o1 = k + 1 < m ? pk->ostart[k + 1] : ecnt;
+      double gx = 0.0, gn = __longlong_as_double(0x7ff0000000000000ll);
+      uint32_t nf = 0;
+      for (uint32_t j = o0 + lane; j < o1; j += 32) {
+        const double av = fabs(sm.oval[dense ? j : sm.cpos[j]]);
+        if (!(av <= 1.7976931348623157e308)) nf = 1;
+        gx = fmax(gx, av);
+        gn = fmin(gn, av);
+      }
+      gx = warp_max(gx);
+      gn = warp_min(gn);
+      nf = __any_sync(0xffffffffu, nf);
+      if (lane == 0) {
+        pk->cnt[k] = o1 - o0;
+        pk->mx[k] = gx;
+        pk->mn[k] = gn;
+        pk->nf[k] = nf;
+      }
+    }
   }
   out_n += ecnt;
   return Lc;
@@ -735,7 +845,8 @@ template <int W>
 __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> ar, int wq, uint64_t mq,
                                                     double cosv, double sinv, int keep_zeros,
                                                     const uint64_t* __restrict__ zq, unsigned int* work,
-                                                    unsigned int* work_next, uint32_t seq_rel, DevStats* st) {
+                                                    unsigned int* work_next, uint32_t seq_rel, DevStats* st,
+                                                    const double* __restrict__ thr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
@@ -743,7 +854,8 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   if (engine_failed(st)) return;
   const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
   const unsigned long long cap = *(volatile const unsigned long long*)&st->arena_cap;
-  const uint32_t seq = (uint32_t)(*(volatile const unsigned long long*)&st->seq_base + seq_rel);
+  const uint32_t seq_base = (uint32_t)*(volatile const unsigned long long*)&st->seq_base;
+  const uint32_t seq = seq_base + seq_rel;
   const uint32_t chunk = max(1u, min(kCta, (G + gridDim.x - 1) / gridDim.x));  // one selection round when G is small
   unsigned long long aff_elems = 0;
   __shared__ unsigned long long dst_s;
@@ -753,6 +865,9 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   __shared__ uint32_t glist[kCta];
   __shared__ uint32_t gscan[40];
   __shared__ uint32_t s_chunk, s_nlist;
+  __shared__ uint32_t s_pp[kCta + 1], s_pfirst[kCta + 1];
+  __shared__ PackSmem pk;
+  unsigned long long pk_records = 0, pk_removed = 0, pk_out = 0;
   if (blockIdx.x == 0 && tid == 0) *work_next = 0;  // the next gate's counter
   for (;;) {
   // grab the next chunk of kCta groups and select the affected ones in parallel
@@ -771,10 +886,86 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
     __syncthreads();
   }
   const uint32_t nlist = s_nlist;
-  for (uint32_t li = 0; li < nlist; ++li) {
+  // ---- groups of at most kPackMaxGroup strings: packs of up to kMaxPack
+  // groups (consecutive in the list) whose start prefix falls in the same
+  // half segment, so a pack holds at most kSeg strings
+  uint32_t nsmall;
+  {
+    const bool in = tid < nlist;
+    const uint32_t gi = in ? glist[tid] : 0u;
+    const uint32_t nt = in ? g.cnt[gi] : 0u;
+    const bool small = in && nt <= kPackMaxGroup;
+    uint32_t tsz;
+    const uint32_t r = block_excl_scan(small ? 1u : 0u, gscan, &nsmall);
+    const uint32_t P = block_excl_scan(small ? nt : 0u, gscan, &tsz);
+    if (small) {
+      glist[r] = gi;
+      s_pp[r] = P;
+    } else if (in) {
+      glist[nsmall + (tid - r)] = gi;  // the larger groups follow, in order
+    }
+    if (tid == 0) s_pp[nsmall] = tsz;
+    __syncthreads();
+    const bool start = tid < nsmall && (tid % kMaxPack == 0 || s_pp[tid] / kPackMaxGroup !=
+                                                                  s_pp[tid - 1] / kPackMaxGroup);
+    uint32_t npk;
+    const uint32_t q = block_excl_scan(start ? 1u : 0u, gscan, &npk);
+    if (start) s_pfirst[q] = tid;
+    if (tid == 0) s_pfirst[npk] = nsmall;
+    __syncthreads();
+    for (uint32_t pj = 0; pj < npk; ++pj) {
+      const uint32_t a = s_pfirst[pj], b = s_pfirst[pj + 1];
+      const uint32_t m = b - a;
+      const uint32_t base = s_pp[a], total = s_pp[b] - base;
+      __syncthreads();  // the previous pack is written back
+      if (tid < m) {
+        const uint32_t gid = glist[a + tid];
+        pk.gid[tid] = gid;
+        pk.gstart[tid] = s_pp[a + tid] - base;
+        pk.src[tid] = g.off[gid];
+        pk.tin[tid] = thr ? thr[pending_index(g.stamp[gid], seq_base, seq_rel)] : -1.0;
+      }
+      if (tid == 0) {
+        pk.m = m;
+        pk.gstart[m] = total;
+        dst_s = atomicAdd(&st->bump, 2ull * total);
+        if (dst_s + 2ull * total > cap) {  // no room: the pack stays untouched, the host compacts and resumes
+          atomicOr(&st->err_arena, 1u);
+          atomicMin(&st->err_seq, (unsigned long long)seq);
+        }
+      }
+      __syncthreads();
+      const uint64_t dst = dst_s;
+      if (dst + 2ull * total > cap) continue;
+      aff_elems += total;
+      uint32_t out_n = 0;
+      double dmax = 0.0, dmin = 0.0, dall = 0.0;
+      uint32_t dnf = 0;
+      seg_branch<W, true>(sg, ar, 0, 0, total, dst, out_n, wq, mq, cosv, sinv, keep_zeros, dmax, dmin, dnf,
+                          pk_records, pk_removed, -1.0, dall, -1.0, &pk);
+      __syncthreads();
+      if (tid < m) {
+        const uint32_t gid = pk.gid[tid];
+        const uint32_t c = pk.cnt[tid];
+        g.off[gid] = dst + pk.ostart[tid];
+        g.cnt[gid] = c;
+        g.cap[gid] = c;
+        g.gmax[gid] = c ? pk.mx[tid] : 0.0;
+        g.gmin[gid] = c ? pk.mn[tid] : __longlong_as_double(0x7ff0000000000000ll);
+        g.flags[gid] = pk.nf[tid];
+        g.stamp[gid] = seq;
+      }
+      pk_out += out_n;
+    }
+  }
+  // ---- larger groups one at a time
+  for (uint32_t li = nsmall; li < nlist; ++li) {
     const uint32_t gid = glist[li];
     const uint32_t n = g.cnt[gid];
     const uint64_t src = g.off[gid];
+    // deferred truncation: thresholds of the gates since this group was last
+    // rewritten (read before this gate overwrites its stamp)
+    const double tin = thr ? thr[pending_index(g.stamp[gid], seq_base, seq_rel)] : -1.0;
     __syncthreads();
     if (tid == 0) {
       dst_s = atomicAdd(&st->bump, 2ull * n);
@@ -795,7 +986,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
     uint32_t p = 0;
     while (p < n) {
       uint32_t used = seg_branch<W>(sg, ar, src, p, n, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
-                                    nonfinite, records, removed, -1.0, vall);
+                                    nonfinite, records, removed, -1.0, vall, tin);
       if (used) {
         p += used;
         continue;
@@ -804,7 +995,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
       const uint32_t be = find_block_end<W>(ar, src, p, n, wq, mq, nullptr);
       if (tid == 0) atomicAdd(&st->stream_elems, (unsigned long long)(be - p));
       stream_branch_range<W>(sm, ar, src + p, be - p, dst, out_n, wq, mq, cosv, sinv, keep_zeros, vmax, vmin,
-                             nonfinite, records, removed, -1.0, vall);
+                             nonfinite, records, removed, -1.0, vall, tin);
       p = be;
     }
     // ---- per-group statistics -------------------------------------------
@@ -845,6 +1036,13 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   }  // groups of the chunk
   }  // chunks
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
+  pk_records = warp_sum64(pk_records);
+  pk_removed = warp_sum64(pk_removed);
+  if ((tid & 31) == 0) {
+    if (pk_records) atomicAdd(&st->records, pk_records);
+    if (pk_removed) atomicAdd(&st->removed, pk_removed);
+  }
+  if (tid == 0 && pk_out) atomicAdd(&st->out_elems, pk_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1148,20 +1346,38 @@ constexpr size_t branch_smem_bytes() {
 // (truncate_now's first pass, engine.cpp:321-343, at group granularity)
 // ---------------------------------------------------------------------------
 template <int W>
-__global__ void __launch_bounds__(kCta) k_reduce(GroupView<W> g, const DevStats* st, RedSlot* out) {
+__global__ void __launch_bounds__(kCta) k_reduce(GroupView<W> g, const DevStats* st, RedSlot* out,
+                                                 const double* __restrict__ thr = nullptr, uint32_t rel = 0) {
   const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  const uint32_t seq_base = (uint32_t)*(volatile const unsigned long long*)&st->seq_base;
   // grid-stride, then one set of atomics per CTA (same-address atomics from
   // every warp serialise in L2)
   unsigned long long live = 0;
   double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
   uint32_t nf = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < G; i += gridDim.x * blockDim.x) {
-    uint32_t c = g.cnt[i];
-    if (c) {
-      live += c;
-      mx = fmax(mx, g.gmax[i]);
-      mn = fmin(mn, g.gmin[i]);
-      nf |= g.flags[i] & 1u;
+  if (thr) {
+    // deferred truncation: a group whose max is pending removal holds no live
+    // string (every other value is smaller).  thr[0] bounds every slot, so
+    // only groups with a max at or below it need their own slot.
+    const double t0 = thr[0];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < G; i += gridDim.x * blockDim.x) {
+      const uint32_t c = g.cnt[i];
+      if (c) {
+        live += c;
+        const double gm = g.gmax[i];
+        if (gm > t0 || gm > thr[pending_index(g.stamp[i], seq_base, rel)]) mx = fmax(mx, gm);
+        nf |= g.flags[i] & 1u;
+      }
+    }
+  } else {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < G; i += gridDim.x * blockDim.x) {
+      const uint32_t c = g.cnt[i];
+      if (c) {
+        live += c;
+        mx = fmax(mx, g.gmax[i]);
+        mn = fmin(mn, g.gmin[i]);
+        nf |= g.flags[i] & 1u;
+      }
     }
   }
   live = warp_sum64(live);
@@ -1300,6 +1516,56 @@ __global__ void __launch_bounds__(kCta) k_truncate_T(GroupView<W> g, ArenaView<W
   for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
     if (g.cnt[gid] == 0 || !(g.gmin[gid] <= T)) continue;  // uniform per CTA
     truncate_group<W>(g, ar, gid, T, st, scan, rmx, rmn);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deferred truncation (epsilon0 > 0, per-gate cadence).  The reference
+// removes |c| <= T_k = epsilon0 * gmax_k from the whole store after every gate
+// k (engine.cpp:318-351).  A string that survives to gate k unchanged is
+// removed at the first k whose T_k >= |c|; since an untouched group's values do
+// not change, it is enough to know, per group, the largest T since the group
+// was last rewritten.  thr[j] = max(T_j .. T_now) for the gates j of the
+// current launch window (j = seq - window base); a group rewritten at gate j
+// reads thr[j], one rewritten before the window reads thr[0].  The next gate
+// that touches the group drops those strings while loading it (they act as
+// absent: 0*cos + child == child, and a zero child is no record), and a flush
+// compacts the rest before anything else reads the store.  The global max per
+// gate skips groups whose max is pending, so T_k is exactly the reference's.
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(kCta) k_thresh(double epsilon0, uint32_t rel, RedSlot* red, RedSlot* red_next,
+                                                 double* thr, DevStats* st) {
+  if (threadIdx.x == 0) clear_red(red_next);
+  if (engine_failed(st)) return;
+  if (*(volatile unsigned int*)&red->nonfinite) {
+    if (threadIdx.x == 0 && atomicCAS(&st->err_numerical, 0u, 1u) == 0u) {
+      st->err_gate = rel;
+      st->err_live = *(volatile unsigned long long*)&red->live;
+    }
+    return;
+  }
+  const double gmax = __longlong_as_double(*(volatile long long*)&red->gmax_bits);
+  const double T = epsilon0 * gmax;  // engine.cpp:345, one IEEE product
+  for (uint32_t j = threadIdx.x; j < rel; j += kCta) thr[j] = fmax(thr[j], T);
+  if (threadIdx.x == 0) {
+    st->last_gmax_bits = (unsigned long long)__double_as_longlong(gmax);
+    thr[rel] = T;
+    thr[rel + 1] = 0.0;  // the next gate's groups are exact when it reduces
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kCta) k_flush(GroupView<W> g, ArenaView<W> ar, const double* __restrict__ thr,
+                                                uint32_t win_base, uint32_t win_len, DevStats* st) {
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  __shared__ uint32_t scan[40];
+  __shared__ double rmx[kWarps], rmn[kWarps];
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+    if (g.cnt[gid] == 0) continue;
+    const double P = thr[pending_index(g.stamp[gid], win_base, win_len)];
+    if (!(g.gmin[gid] <= P)) continue;  // uniform per CTA
+    truncate_group<W>(g, ar, gid, P, st, scan, rmx, rmn);
   }
 }
 

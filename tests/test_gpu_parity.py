@@ -51,6 +51,7 @@ def run_both(pp, O, n, layers, initial, eps=0.0, cadence="gate", steps=None, che
             assert rel_close(eng.expectation_zero_state(), ora.expectation())
             assert eng.global_max() == ora.global_max()
             assert ctr["records_sent"] == octr["records_sent"], (ctr, octr)
+            assert ctr["removed"] == octr["removed"], (ctr, octr)
     return eng, ora
 
 
@@ -247,3 +248,22 @@ def test_speculative_sublayer_is_exact(pp, O, monkeypatch):
     for thx, eps in (("0.25pi", 1e-4), (0.3, 1e-5)):
         circ = _kicked(pp, geom, thx, 6)
         run_both(pp, O, 127, list(circ.layers), [(O.site_word(62, 3), 1.0)], eps, "gate", check_each=True)
+
+
+@pytest.mark.parametrize("mode", ["eager", "deferred", "deferred_tight"])
+def test_deferred_truncation_is_exact(pp, O, monkeypatch, mode):
+    """Per-gate truncation applied lazily (k_thresh/k_flush, the default for
+    epsilon0 > 0) equals the eager per-gate compaction and the oracle: string
+    sets, coefficient bits, records and removed counts per layer, also when
+    the arena overflows mid-run and the run resumes (PP_TIGHT_ARENA)."""
+    if mode == "eager":
+        monkeypatch.setenv("PP_EAGER_TRUNCATION", "1")
+    if mode == "deferred_tight":
+        monkeypatch.setenv("PP_TIGHT_ARENA", "1")
+    geom = pp.heavy_hex_127()
+    for thx, eps in (("0.25pi", 1e-4), (0.3, 1e-5), ("0.9pi", 3e-3)):
+        circ = _kicked(pp, geom, thx, 6)
+        run_both(pp, O, 127, list(circ.layers), [(O.site_word(62, 3), 1.0)], eps, "gate", check_each=True)
+    circ = pp.build_kicked_ising(geom, 0.4, -math.pi / 2 + 0.2, 3)
+    init = [(O.site_word(q, 3), 1.0 / 127) for q in range(127)]
+    run_both(pp, O, 127, list(circ.layers), init, 3e-4, "gate")
