@@ -687,7 +687,7 @@ class EngineImpl final : public EngineBase {
     k_branch_x<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
         gview(gcur_), aview(cur_), p.wq, p.mq, p.cosv, p.sinv, keep_zeros_, gview(gcur_).z[p.wq],
         &d_stats_->work[rel & 1], &d_stats_->work[(rel + 1) & 1], rel, d_stats_,
-        lazy ? thr_.as<double>() : nullptr);
+        lazy ? thr_.as<double>() : nullptr, lazy ? &d_stats_->red[rel & 1] : nullptr);
     ++launches_;
   }
 
@@ -1158,7 +1158,7 @@ class EngineImpl final : public EngineBase {
     ensure_arena(o, new_cap);
     reset_stats(0);
     if (G_) {
-      k_gc<W><<<G_, kCta, 0, stream_>>>(gview(gcur_), aview(cur_), aview(o), d_stats_);
+      k_gc<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), G_, aview(cur_), aview(o), d_stats_);
       ++launches_;
     }
     fetch_stats();
@@ -1273,10 +1273,9 @@ class EngineImpl final : public EngineBase {
   void launch_epilogue(uint32_t rel, bool do_truncate, bool budget, bool lazy = false) {
     RedSlot* r = &d_stats_->red[rel & 1];
     RedSlot* rn = &d_stats_->red[(rel + 1) & 1];
-    if (lazy) {  // deferred truncation: exact threshold now, removal at the next touch or flush
-      k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, r, thr_.as<double>(), rel);
+    if (lazy) {  // deferred truncation: the branch kernel reduced into r; exact threshold now
       k_thresh<W><<<1, kCta, 0, stream_>>>(cfg_.epsilon0, rel, r, rn, thr_.as<double>(), d_stats_);
-      launches_ += 2;
+      ++launches_;
       return;
     }
     k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, r);
@@ -1521,8 +1520,9 @@ class EngineImpl final : public EngineBase {
       const bool source_kept = arena_[cur_].cap >= total_bound + 1;
       ensure_arena(cur_, std::min<uint64_t>(total_bound + 1, arena_max_));
       const uint32_t sort_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 16u));
-      k_sort_small<W><<<sort_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o), keep_zeros_,
-                                                                          d_stats_);
+      const uint32_t small_grid = std::max<uint32_t>(1u, std::min<uint32_t>((groups_bound + kCta - 1) / kCta, 148u * 4u));
+      k_sort_small<W><<<small_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o), keep_zeros_,
+                                                                           d_stats_);
       k_sort_big<W><<<std::min<uint32_t>(sort_grid, 148u * 2u), kCta, big_sort_smem(), stream_>>>(
           gview(1 - gcur_), aview(o), aview(cur_), keep_zeros_, d_stats_);
       launches_ += 2;

@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
                                                     double cosv, double sinv, int keep_zeros,
                                                     const uint64_t* __restrict__ zq, unsigned int* work,
                                                     unsigned int* work_next, uint32_t seq_rel, DevStats* st,
-                                                    const double* __restrict__ thr) {
+                                                    const double* __restrict__ thr, RedSlot* red_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
@@ -868,6 +868,13 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   __shared__ uint32_t s_pp[kCta + 1], s_pfirst[kCta + 1];
   __shared__ PackSmem pk;
   unsigned long long pk_records = 0, pk_removed = 0, pk_out = 0;
+  // fused epilogue reduction (red_out): live count, max |c| over live strings
+  // and the non-finite flag of every group, taken chunk by chunk after the
+  // chunk's groups are rewritten (k_reduce's result, without its launch)
+  unsigned long long r_live = 0;
+  double r_max = 0.0;
+  uint32_t r_nf = 0;
+  const double thr0 = (red_out && thr) ? thr[0] : 0.0;
   if (blockIdx.x == 0 && tid == 0) *work_next = 0;  // the next gate's counter
   for (;;) {
   // grab the next chunk of kCta groups and select the affected ones in parallel
@@ -1034,8 +1041,44 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
       atomicAdd(&st->out_elems, (unsigned long long)out_n);
     }
   }  // groups of the chunk
+  if (red_out) {
+    __syncthreads();  // the chunk's group entries are written
+    const uint32_t gi = g0 + tid;
+    if (tid < chunk && gi < G) {
+      const uint32_t c = g.cnt[gi];
+      if (c) {
+        r_live += c;
+        const double gm = g.gmax[gi];
+        // deferred truncation: a group whose max is pending removal is empty
+        if (!thr || gm > thr0 || gm > thr[pending_index(g.stamp[gi], seq_base, seq_rel)]) r_max = fmax(r_max, gm);
+        r_nf |= g.flags[gi] & 1u;
+      }
+    }
+  }
   }  // chunks
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
+  if (red_out) {
+    r_live = warp_sum64(r_live);
+    r_max = warp_max(r_max);
+    r_nf = __any_sync(0xffffffffu, r_nf);
+    __syncthreads();
+    if ((tid & 31) == 0) {
+      red_rec[tid >> 5] = r_live;
+      red_max[tid >> 5] = r_max;
+      red_nf[tid >> 5] = r_nf;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (uint32_t w = 1; w < kWarps; ++w) {
+        r_live += red_rec[w];
+        r_max = fmax(r_max, red_max[w]);
+        r_nf |= red_nf[w];
+      }
+      if (r_live) atomicAdd(&red_out->live, r_live);
+      atomic_max_nonneg(reinterpret_cast<double*>(&red_out->gmax_bits), r_max);
+      if (r_nf) atomicOr(&red_out->nonfinite, 1u);
+    }
+  }
   pk_records = warp_sum64(pk_records);
   pk_removed = warp_sum64(pk_removed);
   if ((tid & 31) == 0) {
@@ -1656,23 +1699,41 @@ __global__ void k_diag(GroupView<W> g, uint32_t G, ArenaView<W> ar, uint64_t* ou
 // compaction of the arena into the other buffer (garbage collection)
 // ---------------------------------------------------------------------------
 template <int W>
-__global__ void __launch_bounds__(kCta) k_gc(GroupView<W> g, ArenaView<W> src, ArenaView<W> dst, DevStats* st) {
-  const uint32_t gid = blockIdx.x;
-  const uint32_t n = g.cnt[gid];
-  __shared__ unsigned long long d_s;
-  const uint64_t so = g.off[gid];
-  if (threadIdx.x == 0) d_s = n ? atomicAdd(&st->bump, (unsigned long long)n) : 0ull;
-  __syncthreads();
-  const uint64_t d = d_s;
-  for (uint32_t p = threadIdx.x; p < n; p += kCta) {
+__global__ void __launch_bounds__(kCta) k_gc(GroupView<W> g, uint32_t G, ArenaView<W> src, ArenaView<W> dst,
+                                             DevStats* st) {
+  // warp per 32 consecutive groups: one bump allocation per warp batch, then
+  // the warp copies the groups one after another (coalesced per group)
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t base = warp * 32; base < G; base += nw * 32) {
+    const uint32_t gid = base + lane;
+    const uint32_t n = gid < G ? g.cnt[gid] : 0u;
+    const uint64_t so = gid < G ? g.off[gid] : 0ull;
+    uint32_t inc = n;
 #pragma unroll
-    for (int k = 0; k < W; ++k) dst.x[k][d + p] = src.x[k][so + p];
-    dst.c[d + p] = src.c[so + p];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    g.off[gid] = d;
-    g.cap[gid] = n;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    unsigned long long d0 = 0;
+    if (lane == 31 && inc) d0 = atomicAdd(&st->bump, (unsigned long long)inc);
+    d0 = __shfl_sync(0xffffffffu, d0, 31);
+    const uint64_t d = d0 + (inc - n);
+    if (gid < G) {
+      g.off[gid] = n ? d : 0ull;
+      g.cap[gid] = n;
+    }
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t nj = __shfl_sync(0xffffffffu, n, j);
+      if (!nj) continue;
+      const uint64_t sj = __shfl_sync(0xffffffffu, so, j);
+      const uint64_t dj = __shfl_sync(0xffffffffu, d, j);
+      for (uint32_t p = lane; p < nj; p += 32) {
+#pragma unroll
+        for (int k = 0; k < W; ++k) dst.x[k][dj + p] = src.x[k][sj + p];
+        dst.c[dj + p] = src.c[sj + p];
+      }
+    }
   }
 }
 

@@ -520,11 +520,19 @@ __global__ void __launch_bounds__(kCta) k_scatter(const Item* items, GroupView<W
 // ---------------------------------------------------------------------------
 constexpr uint32_t kSortSmall = 2048;
 
+constexpr uint32_t kSortPackGroup = kSortSmall / 2;  // groups up to this size are sorted in packs
+
 template <int W>
 struct SortSmem {
   uint64_t key[W * kSortSmall];
   double val[kSortSmall];
+  uint16_t gk[kSortSmall];     // pack: group of each string (0xffff = padding)
+  uint8_t em[kSortSmall];      // pack: emitted after combining
   uint32_t scan[40];
+  // pack bookkeeping for one chunk of kCta consecutive groups
+  uint32_t plist[kCta], pp[kCta + 1], pfirst[kCta + 1], mlist[kCta];
+  uint32_t gstart[kCta + 1], estart[kCta + 1], pgid[kCta];
+  uint64_t poff[kCta];
 };
 
 // bitonic sort of smem [0, npow2) (npow2 power of two, padded with max keys)
@@ -625,37 +633,211 @@ __device__ void finish_group_stats(GroupView<W> g, uint32_t gid, uint32_t count,
   }
 }
 
+// bitonic sort of (group, x) pairs: a pack of small groups sorts in one pass
+template <int W>
+__device__ void smem_bitonic_pack(uint64_t* key, double* val, uint16_t* gk, uint32_t stride, uint32_t npow2) {
+  for (uint32_t size = 2; size <= npow2; size <<= 1) {
+    for (uint32_t j = size >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = threadIdx.x; t < (npow2 >> 1); t += blockDim.x) {
+        const uint32_t i = 2 * j * (t / j) + (t % j);
+        const uint32_t l = i + j;
+        const bool up = ((i & size) == 0);
+        const uint16_t ga = gk[i], gb = gk[l];
+        const Plane<W> a = sk_load<W>(key, stride, i), b = sk_load<W>(key, stride, l);
+        const bool b_lt_a = gb < ga || (gb == ga && plane_lt<W>(b, a));
+        const bool a_lt_b = ga < gb || (ga == gb && plane_lt<W>(a, b));
+        if (up ? b_lt_a : a_lt_b) {
+          sk_store<W>(key, stride, i, b);
+          sk_store<W>(key, stride, l, a);
+          gk[i] = gb;
+          gk[l] = ga;
+          const double tv = val[i];
+          val[i] = val[l];
+          val[l] = tv;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Sorts groups of <= kSortSmall strings by x and combines equal keys in
+// place.  Each CTA walks chunks of kCta consecutive groups: groups of at most
+// kSortPackGroup strings are sorted together in packs of <= kSortSmall
+// strings (one bitonic pass on (group, x)), larger ones one by one.
 template <int W>
 __global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W> ar, int keep_zeros, DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<W>& sm = *reinterpret_cast<SortSmem<W>*>(smem_raw);
   const uint32_t G = *(volatile const unsigned int*)&st->distinct;
-  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
-  __syncthreads();
-  const uint32_t n = g.cnt[gid];
-  if (n > kSortSmall) continue;
-  const uint64_t off = g.off[gid];
-  uint32_t np2 = 1;
-  while (np2 < n) np2 <<= 1;
-  for (uint32_t i = threadIdx.x; i < np2; i += kCta) {
-    if (i < n) {
-      sk_store<W>(sm.key, kSortSmall, i, load_plane<W>(ar.x, off + i));
-      sm.val[i] = ar.c[off + i];
-    } else {
-      sk_store<W>(sm.key, kSortSmall, i, plane_max<W>());
-      sm.val[i] = 0.0;
+  const uint32_t tid = threadIdx.x;
+  constexpr uint32_t kPer = kSortSmall / kCta;  // strings per thread in the blocked passes
+  unsigned long long removed_pk = 0;
+  for (uint32_t c0 = blockIdx.x * kCta; c0 < G; c0 += gridDim.x * kCta) {
+    __syncthreads();
+    const uint32_t gi = c0 + tid;
+    const uint32_t nt = gi < G ? g.cnt[gi] : 0u;
+    const bool small = nt > 0 && nt <= kSortPackGroup;
+    const bool single = nt > kSortPackGroup && nt <= kSortSmall;
+    uint32_t nsmall, tsz, nsingle;
+    const uint32_t r = block_excl_scan(small ? 1u : 0u, sm.scan, &nsmall);
+    const uint32_t P = block_excl_scan(small ? nt : 0u, sm.scan, &tsz);
+    const uint32_t rs = block_excl_scan(single ? 1u : 0u, sm.scan, &nsingle);
+    if (small) {
+      sm.plist[r] = gi;
+      sm.pp[r] = P;
+    }
+    if (single) sm.mlist[rs] = gi;
+    if (tid == 0) sm.pp[nsmall] = tsz;
+    __syncthreads();
+    const bool start = tid < nsmall && (tid == 0 || sm.pp[tid] / kSortPackGroup != sm.pp[tid - 1] / kSortPackGroup);
+    uint32_t npk;
+    const uint32_t q = block_excl_scan(start ? 1u : 0u, sm.scan, &npk);
+    if (start) sm.pfirst[q] = tid;
+    if (tid == 0) sm.pfirst[npk] = nsmall;
+    __syncthreads();
+    for (uint32_t pj = 0; pj < npk; ++pj) {
+      const uint32_t a = sm.pfirst[pj], b = sm.pfirst[pj + 1];
+      const uint32_t m = b - a, base = sm.pp[a], total = sm.pp[b] - base;
+      __syncthreads();
+      if (tid < m) {
+        const uint32_t gid = sm.plist[a + tid];
+        sm.pgid[tid] = gid;
+        sm.poff[tid] = g.off[gid];
+        sm.gstart[tid] = sm.pp[a + tid] - base;
+      }
+      if (tid == 0) sm.gstart[m] = total;
+      __syncthreads();
+      uint32_t np2 = 1;
+      while (np2 < total) np2 <<= 1;
+      for (uint32_t i = tid; i < np2; i += kCta) {
+        if (i < total) {
+          uint32_t lo = 0, hi = m;  // group of string i
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (sm.gstart[mid] <= i) lo = mid;
+            else hi = mid;
+          }
+          const uint64_t src = sm.poff[lo] + (i - sm.gstart[lo]);
+          sk_store<W>(sm.key, kSortSmall, i, load_plane<W>(ar.x, src));
+          sm.val[i] = ar.c[src];
+          sm.gk[i] = (uint16_t)lo;
+        } else {
+          sk_store<W>(sm.key, kSortSmall, i, plane_max<W>());
+          sm.val[i] = 0.0;
+          sm.gk[i] = 0xffff;
+        }
+      }
+      __syncthreads();
+      if (np2 > 1) smem_bitonic_pack<W>(sm.key, sm.val, sm.gk, kSortSmall, np2);
+      // combine equal (group, x) neighbours (at most two per key: one
+      // scaled parent and one record, or two records of one gate)
+      double cv[kPer];
+      uint32_t emask = 0, cnt = 0;
+#pragma unroll
+      for (uint32_t v = 0; v < kPer; ++v) {
+        const uint32_t p = tid * kPer + v;
+        cv[v] = 0.0;
+        if (p < total) {
+          const uint16_t k = sm.gk[p];
+          const Plane<W> key = sk_load<W>(sm.key, kSortSmall, p);
+          const bool head = p == 0 || sm.gk[p - 1] != k || !plane_eq<W>(sk_load<W>(sm.key, kSortSmall, p - 1), key);
+          if (head) {
+            double x = sm.val[p];
+            if (p + 1 < total && sm.gk[p + 1] == k && plane_eq<W>(sk_load<W>(sm.key, kSortSmall, p + 1), key))
+              x = __dadd_rn(x, sm.val[p + 1]);
+            cv[v] = x;
+            if (keep_zeros || x != 0.0) {
+              emask |= 1u << v;
+              ++cnt;
+            } else {
+              ++removed_pk;
+            }
+          }
+        }
+      }
+      uint32_t etot;
+      uint32_t e = block_excl_scan(cnt, sm.scan, &etot);  // barrier: all neighbour reads are done
+#pragma unroll
+      for (uint32_t v = 0; v < kPer; ++v) {
+        const uint32_t p = tid * kPer + v;
+        if (p < total) {
+          sm.val[p] = cv[v];
+          sm.em[p] = (emask >> v) & 1u;
+          if (p == sm.gstart[sm.gk[p]]) sm.estart[sm.gk[p]] = e;  // a group's first string is a head
+        }
+        e += (emask >> v) & 1u;
+      }
+      if (tid == 0) sm.estart[m] = etot;
+      __syncthreads();
+      // write back each group in place (its region was fully read above)
+      e -= cnt;
+#pragma unroll
+      for (uint32_t v = 0; v < kPer; ++v) {
+        const uint32_t p = tid * kPer + v;
+        if ((emask >> v) & 1u) {
+          const uint16_t k = sm.gk[p];
+          const uint64_t d = sm.poff[k] + (e - sm.estart[k]);
+          store_plane<W>(ar.x, d, sk_load<W>(sm.key, kSortSmall, p));
+          ar.c[d] = cv[v];
+          ++e;
+        }
+      }
+      // per-group statistics: one warp per group
+      const uint32_t lane = tid & 31;
+      for (uint32_t k = tid >> 5; k < m; k += kWarps) {
+        double gx = 0.0, gn = __longlong_as_double(0x7ff0000000000000ll);
+        uint32_t nf = 0;
+        for (uint32_t p = sm.gstart[k] + lane; p < sm.gstart[k + 1]; p += 32) {
+          if (!sm.em[p]) continue;
+          const double av = fabs(sm.val[p]);
+          if (!(av <= 1.7976931348623157e308)) nf = 1;
+          gx = fmax(gx, av);
+          gn = fmin(gn, av);
+        }
+        gx = warp_max(gx);
+        gn = warp_min(gn);
+        nf = __any_sync(0xffffffffu, nf);
+        if (lane == 0) {
+          const uint32_t gid = sm.pgid[k];
+          const uint32_t c = sm.estart[k + 1] - sm.estart[k];
+          g.cnt[gid] = c;
+          g.gmax[gid] = c ? gx : 0.0;
+          g.gmin[gid] = c ? gn : __longlong_as_double(0x7ff0000000000000ll);
+          g.flags[gid] = nf;
+        }
+      }
+    }
+    // groups between kSortPackGroup and kSortSmall strings: one by one
+    for (uint32_t mi = 0; mi < nsingle; ++mi) {
+      __syncthreads();
+      const uint32_t gid = sm.mlist[mi];
+      const uint32_t n = g.cnt[gid];
+      const uint64_t off = g.off[gid];
+      uint32_t np2 = 1;
+      while (np2 < n) np2 <<= 1;
+      for (uint32_t i = tid; i < np2; i += kCta) {
+        if (i < n) {
+          sk_store<W>(sm.key, kSortSmall, i, load_plane<W>(ar.x, off + i));
+          sm.val[i] = ar.c[off + i];
+        } else {
+          sk_store<W>(sm.key, kSortSmall, i, plane_max<W>());
+          sm.val[i] = 0.0;
+        }
+      }
+      __syncthreads();
+      if (np2 > 1) smem_bitonic<W>(sm.key, sm.val, kSortSmall, np2);
+      double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);
+      uint32_t nf = 0;
+      unsigned long long removed = 0;
+      auto getk = [&](uint32_t p) { return sk_load<W>(sm.key, kSortSmall, p); };
+      auto getv = [&](uint32_t p) { return sm.val[p]; };
+      uint32_t w = combine_stream<W>(n, getk, getv, ar, off, keep_zeros, sm.scan, vmax, vmin, nf, removed);
+      finish_group_stats<W>(g, gid, w, vmax, vmin, nf, removed, st);
     }
   }
-  __syncthreads();
-  if (np2 > 1) smem_bitonic<W>(sm.key, sm.val, kSortSmall, np2);
-  double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll);
-  uint32_t nf = 0;
-  unsigned long long removed = 0;
-  auto getk = [&](uint32_t p) { return sk_load<W>(sm.key, kSortSmall, p); };
-  auto getv = [&](uint32_t p) { return sm.val[p]; };
-  uint32_t w = combine_stream<W>(n, getk, getv, ar, off, keep_zeros, sm.scan, vmax, vmin, nf, removed);
-  finish_group_stats<W>(g, gid, w, vmax, vmin, nf, removed, st);
-  }
+  removed_pk = warp_sum64(removed_pk);
+  if ((tid & 31) == 0 && removed_pk) atomicAdd(&st->removed, removed_pk);
 }
 
 // two-run merge of sorted runs a=[0,na) and b=[0,nb) (global) into out,
