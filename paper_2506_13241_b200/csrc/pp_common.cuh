@@ -145,6 +145,21 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratc
   return out;
 }
 
+// max / min over a warp of non-negative doubles (or +inf) as their bit
+// patterns, which order like the values: two 32-bit REDUX steps each
+__device__ __forceinline__ unsigned long long warp_max_bits(unsigned long long v) {
+  const uint32_t hi = (uint32_t)(v >> 32);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? (uint32_t)v : 0u);
+  return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned long long warp_min_bits(unsigned long long v) {
+  const uint32_t hi = (uint32_t)(v >> 32);
+  const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? (uint32_t)v : 0xffffffffu);
+  return ((unsigned long long)mh << 32) | ml;
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

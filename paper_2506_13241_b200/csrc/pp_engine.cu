@@ -166,6 +166,12 @@ class DevicePool {
     std::lock_guard<std::mutex> lk(mu_);
     free_[dev].emplace(bytes, p);
   }
+  size_t cached_bytes(int dev) {
+    std::lock_guard<std::mutex> lk(mu_);
+    size_t b = 0;
+    for (auto& kv : free_[dev]) b += kv.first;
+    return b;
+  }
   void trim(int dev) {
     std::lock_guard<std::mutex> lk(mu_);
     for (auto& [b, p] : free_[dev]) cudaFree(p);
@@ -282,15 +288,8 @@ class EngineImpl final : public EngineBase {
     }
     keep_zeros_ = cfg.cadence == PP_CADENCE_LAYER;
     seed_ = 0x5eed5eed12345678ull;
-    // Memory plan: two arenas (current + compaction/regroup target) of at
-    // most arena_max_ strings each, plus ~8 B per string of regroup slots
-    // and a fixed reserve for tables and scratch.
-    size_t free_b = 0, total_b = 0;
-    PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const double frac = cfg.mem_fraction > 0 && cfg.mem_fraction <= 1 ? cfg.mem_fraction : 0.92;
-    const double budget = (double)free_b * frac - (double)(3ull << 30);
-    arena_max_ = budget > 0 ? (uint64_t)(budget / (double)(2 * R + 16)) : (1ull << 20);
     tight_arena_ = std::getenv("PP_TIGHT_ARENA") != nullptr;
+    update_arena_max();
   }
   ~EngineImpl() override {
     cudaStreamSynchronize(stream_);
@@ -735,14 +734,30 @@ class EngineImpl final : public EngineBase {
     return exec;
   }
 
+  // Memory plan: two arenas (current + compaction/regroup target) of at
+  // most arena_max_ strings each, plus ~16 B per string of regroup slots and
+  // group tables and a fixed reserve.  Re-planned before every arena
+  // allocation from what is free now, the pool's cached blocks and this
+  // engine's own arenas.
+  void update_arena_max() {
+    size_t free_b = 0, total_b = 0;
+    PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t avail = free_b + DevicePool::get().cached_bytes(cfg_.device) + arena_[0].buf.bytes +
+                         arena_[1].buf.bytes;
+    const double frac = cfg_.mem_fraction > 0 && cfg_.mem_fraction <= 1 ? cfg_.mem_fraction : 0.92;
+    const double budget = (double)avail * frac - (double)(3ull << 30);
+    arena_max_ = budget > 0 ? (uint64_t)(budget / (double)(2 * R + 16)) : (1ull << 20);
+  }
+
   // arena capacity for the next compaction: room to grow ~2x without
   // another compaction, generous for small states, never above the memory
   // plan's arena_max_ (the other arena must fit too)
   uint64_t next_arena_target() {
     if (tight_arena_) return live_ + live_ / 8 + 1024;  // test hook: exercise overflow and resume
+    if (8 * live_ + 1024 > arena_max_) update_arena_max();  // re-plan only when it matters
     const uint64_t lo = live_ + live_ / 8 + (1u << 16);
-    // 8x while two such arenas take at most half the plan, else 3x
-    const uint64_t want = std::max<uint64_t>(3 * live_ + 1024, std::min<uint64_t>(8 * live_, arena_max_ / 2));
+    // 8x while the plan allows (fewer compactions), at least 3x
+    const uint64_t want = std::max<uint64_t>(3 * live_ + 1024, std::min<uint64_t>(8 * live_, arena_max_));
     uint64_t t = std::min<uint64_t>(std::max<uint64_t>(want, arena_[cur_].cap), arena_max_);
     if (t < lo) {
       if (lo > arena_max_)
@@ -756,6 +771,7 @@ class EngineImpl final : public EngineBase {
 
   // regroup target arena: the exact output plus slack, within the plan
   uint64_t regroup_arena(uint64_t total) {
+    if (2 * total + (1u << 16) > arena_max_) update_arena_max();
     if (total + 1 > arena_max_)
       throw EngineError(PP_ERR_RESOURCE, "device memory exhausted: " + std::to_string(total) +
                                              " strings after regroup exceed the arena plan of " +
@@ -1520,7 +1536,7 @@ class EngineImpl final : public EngineBase {
       const bool source_kept = arena_[cur_].cap >= total_bound + 1;
       ensure_arena(cur_, std::min<uint64_t>(total_bound + 1, arena_max_));
       const uint32_t sort_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 16u));
-      const uint32_t small_grid = std::max<uint32_t>(1u, std::min<uint32_t>((groups_bound + kCta - 1) / kCta, 148u * 4u));
+      const uint32_t small_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 4u));
       k_sort_small<W><<<small_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o), keep_zeros_,
                                                                            d_stats_);
       k_sort_big<W><<<std::min<uint32_t>(sort_grid, 148u * 2u), kCta, big_sort_smem(), stream_>>>(

@@ -446,8 +446,10 @@ struct SegSmem {
   uint32_t bmid[kSeg];           // first class-1 string of each block
   uint32_t bobase[kSeg];         // output slot base of each block
   alignas(16) uint32_t pre[kSeg + 4];  // exclusive prefixes: pairs << 16 | unpaired class-1
-  uint32_t lbv[kSeg];            // partner search result per string
-  uint16_t cpos[2 * kSeg];       // compacted output position per slot
+  union {
+    uint32_t lbv[kSeg];          // partner search result per string (until the values pass)
+    uint16_t cpos[2 * kSeg];     // compacted output position per slot (from the compaction on)
+  };
   alignas(16) uint8_t f[kSeg];   // bit0 block start, bit1 class-0 with partner, bit2 unpaired class-1
   uint64_t okey[W * 2 * kSeg];
   double oval[2 * kSeg];
@@ -780,21 +782,24 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     const uint32_t lane = tid & 31;
     for (uint32_t k = tid >> 5; k < m; k += kWarps) {
       const uint32_t o0 = pk->ostart[k], o1 = k + 1 < m ? pk->ostart[k + 1] : ecnt;
-      double gx = 0.0, gn = __longlong_as_double(0x7ff0000000000000ll);
+      unsigned long long gx = 0ull, gn = 0x7ff0000000000000ull;  // bits of |c|: 0 and +inf
       uint32_t nf = 0;
       for (uint32_t j = o0 + lane; j < o1; j += 32) {
-        const double av = fabs(sm.oval[dense ? j : sm.cpos[j]]);
-        if (!(av <= 1.7976931348623157e308)) nf = 1;
-        gx = fmax(gx, av);
-        gn = fmin(gn, av);
+        const unsigned long long ab = (unsigned long long)__double_as_longlong(sm.oval[dense ? j : sm.cpos[j]]) &
+                                      0x7fffffffffffffffull;
+        if (ab >= 0x7ff0000000000000ull) nf = 1;  // NaN or Inf
+        if (ab <= 0x7ff0000000000000ull) {        // NaN takes no part in max/min (like fmax/fmin)
+          gx = ab > gx ? ab : gx;
+          gn = ab < gn ? ab : gn;
+        }
       }
-      gx = warp_max(gx);
-      gn = warp_min(gn);
+      gx = warp_max_bits(gx);
+      gn = warp_min_bits(gn);
       nf = __any_sync(0xffffffffu, nf);
       if (lane == 0) {
         pk->cnt[k] = o1 - o0;
-        pk->mx[k] = gx;
-        pk->mn[k] = gn;
+        pk->mx[k] = __longlong_as_double((long long)gx);
+        pk->mn[k] = __longlong_as_double((long long)gn);
         pk->nf[k] = nf;
       }
     }
@@ -866,6 +871,8 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   __shared__ uint32_t gscan[40];
   __shared__ uint32_t s_chunk, s_nlist;
   __shared__ uint32_t s_pp[kCta + 1], s_pfirst[kCta + 1];
+  __shared__ uint64_t s_off[kCta];  // small groups of the chunk: arena offset
+  __shared__ double s_tin[kCta];    // and deferred-truncation threshold
   __shared__ PackSmem pk;
   unsigned long long pk_records = 0, pk_removed = 0, pk_out = 0;
   // fused epilogue reduction (red_out): live count, max |c| over live strings
@@ -885,7 +892,12 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   if (g0 >= G) break;
   {
     const uint32_t gi = g0 + tid;
-    const bool take = tid < chunk && gi < G && (zq[gi] & mq) && g.cnt[gi] != 0 && g.stamp[gi] != seq;
+    bool take = false;
+    if (tid < chunk && gi < G) {  // three independent loads in flight
+      const uint64_t zw = zq[gi];
+      const uint32_t cn = g.cnt[gi], sp = g.stamp[gi];
+      take = (zw & mq) && cn != 0 && sp != seq;
+    }
     uint32_t tot;
     const uint32_t o = block_excl_scan(take ? 1u : 0u, gscan, &tot);
     if (take) glist[o] = gi;
@@ -900,25 +912,44 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   {
     const bool in = tid < nlist;
     const uint32_t gi = in ? glist[tid] : 0u;
-    const uint32_t nt = in ? g.cnt[gi] : 0u;
+    uint32_t nt = 0, sp = 0;
+    uint64_t go = 0;
+    if (in) {  // independent loads in flight together
+      nt = g.cnt[gi];
+      go = g.off[gi];
+      sp = g.stamp[gi];
+    }
     const bool small = in && nt <= kPackMaxGroup;
+    const double tg = (small && thr) ? thr[pending_index(sp, seq_base, seq_rel)] : -1.0;
     uint32_t tsz;
     const uint32_t r = block_excl_scan(small ? 1u : 0u, gscan, &nsmall);
     const uint32_t P = block_excl_scan(small ? nt : 0u, gscan, &tsz);
     if (small) {
       glist[r] = gi;
       s_pp[r] = P;
+      s_off[r] = go;
+      s_tin[r] = tg;
     } else if (in) {
       glist[nsmall + (tid - r)] = gi;  // the larger groups follow, in order
     }
-    if (tid == 0) s_pp[nsmall] = tsz;
+    if (tid == 0) {
+      s_pp[nsmall] = tsz;
+      // one allocation for every small group of the chunk
+      dst_s = tsz ? atomicAdd(&st->bump, 2ull * tsz) : 0ull;
+      if (tsz && dst_s + 2ull * tsz > cap) {  // no room: they stay untouched, the host compacts and resumes
+        atomicOr(&st->err_arena, 1u);
+        atomicMin(&st->err_seq, (unsigned long long)seq);
+      }
+    }
     __syncthreads();
-    const bool start = tid < nsmall && (tid % kMaxPack == 0 || s_pp[tid] / kPackMaxGroup !=
-                                                                  s_pp[tid - 1] / kPackMaxGroup);
+    const uint64_t chunk_dst = dst_s;
+    const uint32_t npack_groups = (tsz && chunk_dst + 2ull * tsz > cap) ? 0u : nsmall;  // no room: skip (uniform)
+    const bool start = tid < npack_groups && (tid % kMaxPack == 0 || s_pp[tid] / kPackMaxGroup !=
+                                                                         s_pp[tid - 1] / kPackMaxGroup);
     uint32_t npk;
     const uint32_t q = block_excl_scan(start ? 1u : 0u, gscan, &npk);
     if (start) s_pfirst[q] = tid;
-    if (tid == 0) s_pfirst[npk] = nsmall;
+    if (tid == 0) s_pfirst[npk] = npack_groups;
     __syncthreads();
     for (uint32_t pj = 0; pj < npk; ++pj) {
       const uint32_t a = s_pfirst[pj], b = s_pfirst[pj + 1];
@@ -926,24 +957,17 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
       const uint32_t base = s_pp[a], total = s_pp[b] - base;
       __syncthreads();  // the previous pack is written back
       if (tid < m) {
-        const uint32_t gid = glist[a + tid];
-        pk.gid[tid] = gid;
+        pk.gid[tid] = glist[a + tid];
         pk.gstart[tid] = s_pp[a + tid] - base;
-        pk.src[tid] = g.off[gid];
-        pk.tin[tid] = thr ? thr[pending_index(g.stamp[gid], seq_base, seq_rel)] : -1.0;
+        pk.src[tid] = s_off[a + tid];
+        pk.tin[tid] = s_tin[a + tid];
       }
       if (tid == 0) {
         pk.m = m;
         pk.gstart[m] = total;
-        dst_s = atomicAdd(&st->bump, 2ull * total);
-        if (dst_s + 2ull * total > cap) {  // no room: the pack stays untouched, the host compacts and resumes
-          atomicOr(&st->err_arena, 1u);
-          atomicMin(&st->err_seq, (unsigned long long)seq);
-        }
       }
       __syncthreads();
-      const uint64_t dst = dst_s;
-      if (dst + 2ull * total > cap) continue;
+      const uint64_t dst = chunk_dst + 2ull * base;
       aff_elems += total;
       uint32_t out_n = 0;
       double dmax = 0.0, dmin = 0.0, dall = 0.0;
@@ -1046,12 +1070,13 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
     const uint32_t gi = g0 + tid;
     if (tid < chunk && gi < G) {
       const uint32_t c = g.cnt[gi];
+      const double gm = g.gmax[gi];
+      const uint32_t fl = g.flags[gi];
       if (c) {
         r_live += c;
-        const double gm = g.gmax[gi];
         // deferred truncation: a group whose max is pending removal is empty
         if (!thr || gm > thr0 || gm > thr[pending_index(g.stamp[gi], seq_base, seq_rel)]) r_max = fmax(r_max, gm);
-        r_nf |= g.flags[gi] & 1u;
+        r_nf |= fl & 1u;
       }
     }
   }
@@ -1698,6 +1723,8 @@ __global__ void k_diag(GroupView<W> g, uint32_t G, ArenaView<W> ar, uint64_t* ou
 // ---------------------------------------------------------------------------
 // compaction of the arena into the other buffer (garbage collection)
 // ---------------------------------------------------------------------------
+constexpr uint32_t kGcWarpMax = 2048;  // k_gc: groups up to this size are copied by a warp
+
 template <int W>
 __global__ void __launch_bounds__(kCta) k_gc(GroupView<W> g, uint32_t G, ArenaView<W> src, ArenaView<W> dst,
                                              DevStats* st) {
@@ -1707,7 +1734,8 @@ __global__ void __launch_bounds__(kCta) k_gc(GroupView<W> g, uint32_t G, ArenaVi
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t base = warp * 32; base < G; base += nw * 32) {
     const uint32_t gid = base + lane;
-    const uint32_t n = gid < G ? g.cnt[gid] : 0u;
+    const uint32_t n0 = gid < G ? g.cnt[gid] : 0u;
+    const uint32_t n = n0 <= kGcWarpMax ? n0 : 0u;  // larger groups: whole CTAs, below
     const uint64_t so = gid < G ? g.off[gid] : 0ull;
     uint32_t inc = n;
 #pragma unroll
@@ -1719,7 +1747,7 @@ __global__ void __launch_bounds__(kCta) k_gc(GroupView<W> g, uint32_t G, ArenaVi
     if (lane == 31 && inc) d0 = atomicAdd(&st->bump, (unsigned long long)inc);
     d0 = __shfl_sync(0xffffffffu, d0, 31);
     const uint64_t d = d0 + (inc - n);
-    if (gid < G) {
+    if (gid < G && n0 <= kGcWarpMax) {
       g.off[gid] = n ? d : 0ull;
       g.cap[gid] = n;
     }
@@ -1733,6 +1761,26 @@ __global__ void __launch_bounds__(kCta) k_gc(GroupView<W> g, uint32_t G, ArenaVi
         for (int k = 0; k < W; ++k) dst.x[k][dj + p] = src.x[k][sj + p];
         dst.c[dj + p] = src.c[sj + p];
       }
+    }
+  }
+  // groups above kGcWarpMax strings: one CTA each
+  __shared__ unsigned long long d_s;
+  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
+    const uint32_t n = g.cnt[gid];
+    if (n <= kGcWarpMax) continue;  // uniform per CTA
+    const uint64_t so = g.off[gid];
+    __syncthreads();
+    if (threadIdx.x == 0) d_s = atomicAdd(&st->bump, (unsigned long long)n);
+    __syncthreads();
+    const uint64_t d = d_s;
+    for (uint32_t p = threadIdx.x; p < n; p += kCta) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) dst.x[k][d + p] = src.x[k][so + p];
+      dst.c[d + p] = src.c[so + p];
+    }
+    if (threadIdx.x == 0) {
+      g.off[gid] = d;
+      g.cap[gid] = n;
     }
   }
 }

@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(kCta) k_scatter(const Item* items, GroupView<W
 // ---------------------------------------------------------------------------
 constexpr uint32_t kSortSmall = 2048;
 
-constexpr uint32_t kSortPackGroup = kSortSmall / 2;  // groups up to this size are sorted in packs
+constexpr uint32_t kSortPackGroup = 256;  // groups up to this size are sorted in packs
 
 template <int W>
 struct SortSmem {
@@ -673,10 +673,12 @@ __global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W
   const uint32_t tid = threadIdx.x;
   constexpr uint32_t kPer = kSortSmall / kCta;  // strings per thread in the blocked passes
   unsigned long long removed_pk = 0;
-  for (uint32_t c0 = blockIdx.x * kCta; c0 < G; c0 += gridDim.x * kCta) {
+  // chunks of consecutive groups, sized so every CTA gets work when G is small
+  const uint32_t chunk = max(1u, min(kCta, (G + gridDim.x - 1) / gridDim.x));
+  for (uint32_t c0 = blockIdx.x * chunk; c0 < G; c0 += gridDim.x * chunk) {
     __syncthreads();
     const uint32_t gi = c0 + tid;
-    const uint32_t nt = gi < G ? g.cnt[gi] : 0u;
+    const uint32_t nt = (tid < chunk && gi < G) ? g.cnt[gi] : 0u;
     const bool small = nt > 0 && nt <= kSortPackGroup;
     const bool single = nt > kSortPackGroup && nt <= kSortSmall;
     uint32_t nsmall, tsz, nsingle;
@@ -690,7 +692,9 @@ __global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W
     if (single) sm.mlist[rs] = gi;
     if (tid == 0) sm.pp[nsmall] = tsz;
     __syncthreads();
-    const bool start = tid < nsmall && (tid == 0 || sm.pp[tid] / kSortPackGroup != sm.pp[tid - 1] / kSortPackGroup);
+    // a pack: groups whose start prefix shares one window of kSortSmall - kSortPackGroup strings
+    constexpr uint32_t kWin = kSortSmall - kSortPackGroup;
+    const bool start = tid < nsmall && (tid == 0 || sm.pp[tid] / kWin != sm.pp[tid - 1] / kWin);
     uint32_t npk;
     const uint32_t q = block_excl_scan(start ? 1u : 0u, sm.scan, &npk);
     if (start) sm.pfirst[q] = tid;

@@ -18,5 +18,6 @@ print(max(vals)[1])
 PY
 )
 echo "top launch index $IDX"
-ncu --set full --clock-control none --import-source on -k regex:${KRE:-k_branch_x} -s $IDX -c 1 \
+# --kernel-id invocation numbers count launches of the matching kernel, 1-based
+ncu --set full --clock-control none --import-source on --kernel-id ::regex:${KRE:-k_branch_x}:$((IDX + 1)) \
     -o gpurun_out/${OUT} python tools/profile_run.py $W > /dev/null 2>&1
