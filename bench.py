@@ -204,8 +204,10 @@ def run_sharded(args, pp, circ, wl, sg, final_terms, init, rank, world, local):
     from paper_2506_13241_b200.sharded import GpuShard, ShardedEngine, TorchComm
 
     n, eps = wl[1], wl[5]
-    gloo = dist.new_group(backend="gloo")  # host-staged exchange
-    comm = TorchComm(gloo)
+    gloo = dist.new_group(backend="gloo")  # scalars (and the host-staged fallback)
+    nccl = os.environ.get("PP_BENCH_PG") != "gloo" and os.environ.get("PP_HOST_EXCHANGE") is None
+    # strings move device-to-device: one NCCL all-to-all per z-changing step over NVLink
+    comm = TorchComm(gloo, data_group=dist.group.WORLD if nccl else None)
 
     def one_step():
         shard = GpuShard(n, eps, "gate", device=local)
@@ -247,7 +249,8 @@ def run_sharded(args, pp, circ, wl, sg, final_terms, init, rank, world, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic kicked-Ising circuit, BASELINE config)",
             "config": {"workload": args.workload, "string_gates_per_step": sg, "final_terms": final_terms,
-                       "parallelism": f"z-hash shards x{world}", "exchange": "host-staged (gloo)",
+                       "parallelism": f"z-hash shards x{world}",
+                       "exchange": "device all-to-all (NCCL)" if nccl else "host-staged (gloo)",
                        "records_exchanged_per_step": float(mv[0]) / args.steps},
             "e2e": {"value": sg / wall_per_step, "unit": "string-gates/s", "h2d_bytes_per_step": 40,
                     "d2h_bytes_per_step": 8 * 4 * circ.num_layers(), "api": "ShardedEngine.run_circuit"},

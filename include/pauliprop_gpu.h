@@ -150,6 +150,15 @@ int pp_shard_evict(pp_engine* engine, uint32_t world, uint32_t rank, uint64_t se
 int pp_shard_ingest(pp_engine* engine, const uint64_t* records, uint64_t count);
 uint32_t pp_shard_owner(const uint64_t* words, int n, uint64_t seed, uint32_t world);
 
+/* Device-resident exchange (NCCL / NVLink): pp_shard_evict_device leaves the
+ * records in an engine-owned device buffer (*records, valid until the next
+ * call on this engine) grouped by destination; pp_shard_ingest_device takes
+ * records from device memory on the engine's device (e.g. an NCCL all-to-all
+ * receive buffer), with the stream work that produced them complete. */
+int pp_shard_evict_device(pp_engine* engine, uint32_t world, uint32_t rank, uint64_t seed, const uint64_t** records,
+                          uint64_t* counts);
+int pp_shard_ingest_device(pp_engine* engine, const uint64_t* records, uint64_t count);
+
 /* Sum of squared coefficients (conserved at epsilon0 = 0; property checks at
  * sizes the oracle cannot reach). */
 int pp_norm2(pp_engine* engine, double* out);

@@ -248,7 +248,8 @@ class EngineBase {
   virtual int record_words() const = 0;
   virtual void shard_evict(uint32_t world, uint32_t rank, uint64_t seed, uint64_t* out, uint64_t cap,
                            uint64_t* counts) = 0;
-  virtual void shard_ingest(const uint64_t* rec, uint64_t count) = 0;
+  virtual void shard_ingest(const uint64_t* rec, uint64_t count, bool device) = 0;
+  virtual const uint64_t* device_records() const = 0;
   virtual double norm2() = 0;
   virtual void histogram(int bins, double gmax, double epsilon0, uint64_t* pos, uint64_t* neg) = 0;
 };
@@ -1005,20 +1006,24 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaMemcpyAsync(dcnt + world, off.data(), world * 8, cudaMemcpyHostToDevice, stream_));
     k_evict_write<W><<<G_, kCta, 0, stream_>>>(gview(gcur_), aview(cur_), world, rank, seed, dcnt + world,
                                                evict_buf_.as<uint64_t>());
-    PP_CUDA(cudaMemcpyAsync(out, evict_buf_.p, total * rw * 8, cudaMemcpyDeviceToHost, stream_));
+    if (out)  // host-staged exchange; otherwise the records stay in evict_buf_ (device_records())
+      PP_CUDA(cudaMemcpyAsync(out, evict_buf_.p, total * rw * 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
     launches_ += 2;
     dirty_ = true;
     sync_state();
   }
 
-  void shard_ingest(const uint64_t* rec, uint64_t count) override {
+  const uint64_t* device_records() const override { return evict_buf_.as<uint64_t>(); }
+
+  void shard_ingest(const uint64_t* rec, uint64_t count, bool device) override {
     sync_state();
     if (count == 0) return;
     const int rw = 2 * W + 1;
     if (bump_ + count > arena_[cur_].cap) gc_into_other(std::max<uint64_t>(next_arena_target(), live_ + 2 * count));
     evict_buf_.ensure(count * rw * 8);
-    PP_CUDA(cudaMemcpyAsync(evict_buf_.p, rec, count * rw * 8, cudaMemcpyHostToDevice, stream_));
+    PP_CUDA(cudaMemcpyAsync(evict_buf_.p, rec, count * rw * 8,
+                            device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
     rec_slot_.ensure(count * 4);
     uint32_t* flags = rec_slot_.as<uint32_t>();
     k_run_starts<<<(uint32_t)((count + kCta - 1) / kCta), kCta, 0, stream_>>>(evict_buf_.as<uint64_t>(), count, W, W,
@@ -1813,7 +1818,21 @@ int pp_shard_evict(pp_engine* e, uint32_t world, uint32_t rank, uint64_t seed, u
 
 int pp_shard_ingest(pp_engine* e, const uint64_t* records, uint64_t count) {
   if (!e || (!records && count)) return PP_ERR_INVALID;
-  return guarded(e, [&] { e->impl->shard_ingest(records, count); });
+  return guarded(e, [&] { e->impl->shard_ingest(records, count, false); });
+}
+
+int pp_shard_evict_device(pp_engine* e, uint32_t world, uint32_t rank, uint64_t seed, const uint64_t** records,
+                          uint64_t* counts) {
+  if (!e || !counts || !records || world == 0 || rank >= world) return PP_ERR_INVALID;
+  return guarded(e, [&] {
+    e->impl->shard_evict(world, rank, seed, nullptr, ~0ull, counts);
+    *records = e->impl->device_records();
+  });
+}
+
+int pp_shard_ingest_device(pp_engine* e, const uint64_t* records, uint64_t count) {
+  if (!e || (!records && count)) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->shard_ingest(records, count, true); });
 }
 
 uint32_t pp_shard_owner(const uint64_t* words, int n, uint64_t seed, uint32_t world) {

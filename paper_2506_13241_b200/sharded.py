@@ -45,15 +45,34 @@ class Comm:
 
 
 class TorchComm(Comm):
-    """torch.distributed on an existing process group (CPU tensors; use a
-    gloo group for the host-staged exchange)."""
+    """torch.distributed: scalars and the host-staged exchange on `group`
+    (CPU tensors, a gloo group); with `data_group` (an NCCL group) the string
+    exchange stays on the device: one NCCL all-to-all over NVLink between the
+    engines' device buffers (device_exchange)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, data_group=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
+        self.data_group = data_group
+        self.device_exchange = data_group is not None
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+
+    def alltoallv_device(self, send, counts):
+        """send: flat int64 CUDA tensor grouped by destination, counts: int64
+        words per destination.  Returns (recv tensor, recv word counts)."""
+        import torch
+        dev = send.device
+        c = torch.tensor(counts, dtype=torch.int64, device=dev)
+        rc = torch.empty_like(c)
+        self.dist.all_to_all_single(rc, c, group=self.data_group)
+        rcl = rc.tolist()
+        recv = torch.empty(int(sum(rcl)), dtype=torch.int64, device=dev)
+        self.dist.all_to_all_single(recv, send, output_split_sizes=rcl, input_split_sizes=list(counts),
+                                    group=self.data_group)
+        torch.cuda.current_stream(dev).synchronize()
+        return recv, rcl
 
     def allreduce(self, values, op):
         import torch
@@ -92,18 +111,31 @@ class _ThreadHub:
 
 
 class ThreadComm(Comm):
-    """Ranks as threads of one process (emulates a multi-GPU run on one GPU:
-    the exchange is host-staged, so no kernel ever waits on another rank)."""
+    """Ranks as threads of one process (emulates a multi-GPU run on one GPU;
+    no kernel ever waits on another rank).  device=True exchanges device
+    buffers (the NCCL path's data flow, with device-to-device copies standing
+    in for the all-to-all)."""
 
-    def __init__(self, hub: _ThreadHub, rank: int):
+    def __init__(self, hub: _ThreadHub, rank: int, device: bool = False):
         self.hub = hub
         self.rank = rank
         self.world = hub.world
+        self.device_exchange = device
 
     @staticmethod
-    def make(world):
+    def make(world, device=False):
         hub = _ThreadHub(world)
-        return [ThreadComm(hub, r) for r in range(world)]
+        return [ThreadComm(hub, r, device) for r in range(world)]
+
+    def alltoallv_device(self, send, counts):
+        import torch
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        allv = self._exchange((send, offs))
+        parts = [allv[s][0][int(allv[s][1][self.rank]):int(allv[s][1][self.rank + 1])] for s in range(self.world)]
+        recv = torch.cat(parts) if parts else send[:0]
+        torch.cuda.current_stream(send.device).synchronize()
+        self.hub.barrier.wait()  # every rank holds its copy before any source buffer is reused
+        return recv, [int(allv[s][1][self.rank + 1] - allv[s][1][self.rank]) for s in range(self.world)]
 
     def _exchange(self, obj):
         self.hub.slots[self.rank] = obj
@@ -127,6 +159,13 @@ class ThreadComm(Comm):
 # ---------------------------------------------------------------------------
 # the GPU backend
 # ---------------------------------------------------------------------------
+class _DeviceWords:
+    """__cuda_array_interface__ over an engine-owned device buffer (zero copy)."""
+
+    def __init__(self, ptr, words):
+        self.__cuda_array_interface__ = {"shape": (words,), "typestr": "<i8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
 class GpuShard:
     """One rank's local engine: the CUDA engine with external truncation."""
 
@@ -134,6 +173,7 @@ class GpuShard:
         from . import _pauliprop as _impl
         self.impl = _impl
         self.n = n
+        self.device = device
         self.engine = _impl.Engine(n, epsilon0, cadence, device=device, external_truncation=True)
 
     def owner(self, words, world):
@@ -154,6 +194,20 @@ class GpuShard:
     def evict(self, world, rank):
         rec, counts = self.engine.shard_evict(world, rank, SHARD_SEED)
         return np.ascontiguousarray(rec), counts
+
+    def evict_device(self, world, rank):
+        """Records stay on the device: (flat int64 CUDA tensor view of the
+        engine's buffer, records per destination)."""
+        import torch
+        ptr, counts = self.engine.shard_evict_device(world, rank, SHARD_SEED)
+        words = int(sum(counts)) * self.engine.record_words()
+        if words == 0:
+            return torch.zeros(0, dtype=torch.int64, device=f"cuda:{self.device}"), counts
+        return torch.as_tensor(_DeviceWords(ptr, words), device=f"cuda:{self.device}"), counts
+
+    def ingest_device(self, recv, nrec):
+        if nrec:
+            self.engine.shard_ingest_device(recv.data_ptr(), nrec)
 
     def ingest(self, rec):
         rw = self.engine.record_words()
@@ -221,6 +275,13 @@ class ShardedEngine:
 
     # -- collectives
     def _exchange(self):
+        if getattr(self.comm, "device_exchange", False) and hasattr(self.b, "evict_device"):
+            rw = self.b.record_words()
+            send, counts = self.b.evict_device(self.comm.world, self.comm.rank)
+            recv, rwords = self.comm.alltoallv_device(send, [int(c) * rw for c in counts])
+            self.exchanged_records += int(sum(int(c) for c in counts))
+            self.b.ingest_device(recv, int(sum(rwords)) // rw)
+            return
         rec, counts = self.b.evict(self.comm.world, self.comm.rank)
         rw = self.b.record_words()
         send, pos = [], 0

@@ -1,6 +1,8 @@
 """Sharded GPU engines (one per emulated rank, threads on one B200) against a
-single engine: same string set and coefficients bit for bit.  The exchange is
-host-staged, so no kernel waits on another rank."""
+single engine: same string set and coefficients bit for bit.  The exchange
+runs host-staged or device-resident (engine device buffers exchanged by
+device copies, the data flow of the NCCL all-to-all); either way no kernel
+waits on another rank."""
 import math
 import threading
 
@@ -12,10 +14,10 @@ from conftest import assert_same_terms
 pytestmark = pytest.mark.gpu
 
 
-def run_sharded(pp, n, circ, init_words, init_coeffs, eps, cadence, world):
+def run_sharded(pp, n, circ, init_words, init_coeffs, eps, cadence, world, device=False):
     from paper_2506_13241_b200.sharded import GpuShard, ShardedEngine, ThreadComm
 
-    comms = ThreadComm.make(world)
+    comms = ThreadComm.make(world, device=device)
     results, errors = [None] * world, []
 
     def rank_main(r):
@@ -38,6 +40,7 @@ def run_sharded(pp, n, circ, init_words, init_coeffs, eps, cadence, world):
     return results
 
 
+@pytest.mark.parametrize("device", [False, True], ids=["host_staged", "device_exchange"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("case", [
     ("hh_pi4_eps0", 127, "0.25pi", "-0.5pi", 0.0, "gate", 5),
@@ -45,7 +48,7 @@ def run_sharded(pp, n, circ, init_words, init_coeffs, eps, cadence, world):
     ("hh_0.3_eps1e-3_layer", 127, 0.3, "-0.5pi", 1e-3, "layer", 4),
     ("hh_noncliff_zz", 127, 0.4, -math.pi / 2 + 0.2, 1e-4, "gate", 3),
 ], ids=lambda c: c[0] if isinstance(c, tuple) else str(c))
-def test_sharded_gpu_matches_single(pp, O, case, world):
+def test_sharded_gpu_matches_single(pp, O, case, world, device):
     name, n, thx, thzz, eps, cadence, layers = case
     geom = pp.heavy_hex_127()
     circ = pp.build_kicked_ising(geom, thx, thzz, layers)
@@ -59,7 +62,7 @@ def test_sharded_gpu_matches_single(pp, O, case, world):
     single.set_initial(words, coeffs)
     srows = single.run_circuit(circ)
     sw, sc = single.export()
-    res = run_sharded(pp, n, circ, words, coeffs, eps, cadence, world)
+    res = run_sharded(pp, n, circ, words, coeffs, eps, cadence, world, device)
     for r in range(world):
         rows, w, c, _ = res[r]
         assert_same_terms(w, c, sw, sc, f"{name} world={world} rank={r}")
