@@ -113,6 +113,11 @@ void pp_destroy(pp_engine* engine);
 int pp_set_initial(pp_engine* engine, const uint64_t* words, const double* coeffs, size_t count);
 int pp_apply_gate(pp_engine* engine, const pp_gate* gate);
 int pp_apply_gates(pp_engine* engine, const pp_gate* gates, size_t count);
+
+/* One layer of run_circuit (engine.cpp:394-446) with a zero-state readout:
+ * pp_apply_gates followed by pp_expectation_zero_state, sharing one device
+ * round trip (errors surface here exactly as from pp_apply_gates). */
+int pp_apply_layer(pp_engine* engine, const pp_gate* gates, size_t count, double* observable);
 int pp_truncate_now(pp_engine* engine);
 int pp_term_count(const pp_engine* engine, uint64_t* out);
 int pp_global_max(const pp_engine* engine, double* out);

@@ -621,6 +621,13 @@ void Engine::apply_gates(const std::vector<Gate>& gates) {
   for (size_t i = 0; i < gates.size(); ++i) g[i] = to_pp(gates[i]);
   check(pp_apply_gates(handle_, g.data(), g.size()));
 }
+double Engine::apply_layer(const std::vector<Gate>& gates) {
+  std::vector<pp_gate> g(gates.size());
+  for (size_t i = 0; i < gates.size(); ++i) g[i] = to_pp(gates[i]);
+  double obs = 0.0;
+  check(pp_apply_layer(handle_, g.data(), g.size(), &obs));
+  return obs;
+}
 void Engine::truncate_now() { check(pp_truncate_now(handle_)); }
 uint64_t Engine::term_count() const {
   uint64_t n = 0;
@@ -686,6 +693,8 @@ RunLedger run_circuit(Engine& engine, const Circuit& circuit, const RunOptions& 
     engine.set_layer_context(t);
     const auto& layer = circuit.layers[L - t];
     auto t0 = std::chrono::steady_clock::now();
+    double fused = 0.0;
+    bool have_fused = false;
     if (options.on_gate_readout) {
       size_t gi = 0;
       for (auto g = layer.rbegin(); g != layer.rend(); ++g, ++gi) {
@@ -694,7 +703,13 @@ RunLedger run_circuit(Engine& engine, const Circuit& circuit, const RunOptions& 
       }
     } else {
       std::vector<Gate> rev(layer.rbegin(), layer.rend());
-      engine.apply_gates(rev);
+      if (options.readout == ReadoutMode::ZeroState &&
+          engine.config().policy.cadence == TruncationCadence::PerGate) {
+        fused = engine.apply_layer(rev);  // gates + readout in one device round trip
+        have_fused = true;
+      } else {
+        engine.apply_gates(rev);
+      }
     }
     if (engine.config().policy.cadence == TruncationCadence::PerLayer) engine.truncate_now();
     double wall_ns =
@@ -702,7 +717,7 @@ RunLedger run_circuit(Engine& engine, const Circuit& circuit, const RunOptions& 
     Engine::Counters c = engine.take_counters();
     LayerRecord row;
     row.t = t;
-    row.observable = read();
+    row.observable = have_fused ? fused : read();
     row.term_count = engine.term_count();
     row.global_max = engine.global_max();
     row.removed = c.removed;

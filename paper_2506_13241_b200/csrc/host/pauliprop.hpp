@@ -196,6 +196,7 @@ class Engine {
   void set_initial(const std::vector<std::pair<PauliString, double>>& terms);
   void apply_gate(const Gate& gate);
   void apply_gates(const std::vector<Gate>& gates);  // in order; fuses Clifford runs
+  double apply_layer(const std::vector<Gate>& gates);  // apply_gates + expectation_zero_state, one round trip
   void truncate_now();
 
   uint64_t term_count() const;

@@ -224,6 +224,31 @@ static void release_pinned_stats(DevStats* p) {
   std::lock_guard<std::mutex> lk(g_pinned_mu);
   g_pinned_free.push_back(p);
 }
+// pinned staging for the diagonal readout, recycled across engines
+constexpr size_t kDiagCap = 4096;  // diagonal strings fetched with the readout's single round trip
+struct DiagPinned {
+  uint64_t z[2 * kDiagCap];
+  double c[kDiagCap];
+};
+static std::vector<DiagPinned*> g_diag_free;
+static DiagPinned* pinned_diag() {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_diag_free.empty()) {
+      DiagPinned* p = g_diag_free.back();
+      g_diag_free.pop_back();
+      return p;
+    }
+  }
+  DiagPinned* p = nullptr;
+  PP_CUDA(cudaMallocHost(&p, sizeof(DiagPinned)));
+  return p;
+}
+static void release_pinned_diag(DiagPinned* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_diag_free.push_back(p);
+}
 
 static std::mutex g_graph_mu;
 static std::map<std::string, cudaGraphExec_t> g_graphs;
@@ -233,6 +258,7 @@ class EngineBase {
   virtual ~EngineBase() = default;
   virtual void set_initial(const uint64_t* words, const double* c, size_t count) = 0;
   virtual void apply_gates(const pp_gate* gates, size_t count) = 0;
+  virtual double apply_layer(const pp_gate* gates, size_t count) = 0;
   virtual void truncate_now() = 0;
   virtual uint64_t term_count() = 0;
   virtual double global_max() = 0;
@@ -297,6 +323,7 @@ class EngineImpl final : public EngineBase {
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     release_pinned_stats(h_stats_);
+    release_pinned_diag(h_diag_);
     cudaStreamDestroy(stream_);
   }
 
@@ -401,6 +428,13 @@ class EngineImpl final : public EngineBase {
     apply_gates_async(gates, count);
     sync_state();  // errors surface at the call, as Engine::apply_gate throws
   }
+  // one layer of run_circuit: the gates, then the <0|O|0> readout; errors
+  // surface at the readout's sync, inside this call
+  double apply_layer(const pp_gate* gates, size_t count) override {
+    apply_gates_async(gates, count);
+    return expectation();
+  }
+
   void apply_gates_async(const pp_gate* gates, size_t count) {
     size_t i = 0;
     while (i < count) {
@@ -800,22 +834,20 @@ class EngineImpl final : public EngineBase {
   double expectation() override {
     // expectation_zero_state (sparse_operator.cpp:89-97): sum over strings
     // with no X/Y.  Summed on the host in ascending z order with Neumaier
-    // compensation, so the value is deterministic.
-    sync_state();
+    // compensation, so the value is deterministic.  The diagonal pass shares
+    // the sync's round trip (sync_state(true)).
+    sync_state(true);
     if (G_ == 0) return 0.0;
-    diag_z_.ensure((size_t)G_ * W * 8);
-    diag_c_.ensure((size_t)G_ * 8);
-    reset_stats(bump_);
-    k_diag<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, aview(cur_), diag_z_.as<uint64_t>(),
-                                                 diag_c_.as<double>(), d_stats_);
-    ++launches_;
-    fetch_stats();
-    uint64_t nd = h_stats_->diag_count;
+    const uint64_t nd = diag_n_;
     std::vector<uint64_t> z(nd * W);
     std::vector<double> c(nd);
-    if (nd) {
-      PP_CUDA(cudaMemcpy(z.data(), diag_z_.p, nd * W * 8, cudaMemcpyDeviceToHost));
-      PP_CUDA(cudaMemcpy(c.data(), diag_c_.p, nd * 8, cudaMemcpyDeviceToHost));
+    if (nd <= diag_copied_) {
+      std::memcpy(z.data(), h_diag_->z, nd * W * 8);
+      std::memcpy(c.data(), h_diag_->c, nd * 8);
+    } else {
+      PP_CUDA(cudaMemcpyAsync(z.data(), diag_z_.p, nd * W * 8, cudaMemcpyDeviceToHost, stream_));
+      PP_CUDA(cudaMemcpyAsync(c.data(), diag_c_.p, nd * 8, cudaMemcpyDeviceToHost, stream_));
+      PP_CUDA(cudaStreamSynchronize(stream_));
     }
     std::vector<uint64_t> order(nd);
     for (uint64_t i = 0; i < nd; ++i) order[i] = i;
@@ -1224,8 +1256,31 @@ class EngineImpl final : public EngineBase {
     ++counters_.gates;
     epilogue(cfg_.cadence == PP_CADENCE_GATE, true);
   }
-  void sync_state() {
-    if (!dirty_) return;
+  // the diagonal pass of the readout, folded into a sync's single round trip
+  void launch_diag() {
+    PP_CUDA(cudaMemsetAsync(&d_stats_->diag_count, 0, sizeof(unsigned long long), stream_));
+    diag_copied_ = 0;
+    if (!G_) return;
+    diag_z_.ensure((size_t)G_ * W * 8);
+    diag_c_.ensure((size_t)G_ * 8);
+    k_diag<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, aview(cur_), diag_z_.as<uint64_t>(),
+                                                 diag_c_.as<double>(), d_stats_);
+    ++launches_;
+    if (!h_diag_) h_diag_ = pinned_diag();
+    diag_copied_ = std::min<uint64_t>(G_, kDiagCap);
+    PP_CUDA(cudaMemcpyAsync(h_diag_->z, diag_z_.p, diag_copied_ * W * 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaMemcpyAsync(h_diag_->c, diag_c_.p, diag_copied_ * 8, cudaMemcpyDeviceToHost, stream_));
+  }
+
+  void sync_state(bool diag = false) {
+    if (!dirty_) {
+      if (!diag) return;
+      launch_diag();  // clean store: the diagonal pass alone
+      fetch_stats();
+      PP_CUDA(cudaGetLastError());
+      diag_n_ = h_stats_->diag_count;
+      return;
+    }
     if (lazy_open_) {  // apply the deferred truncations of the last launch window
       if (G_) {
         k_flush<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), aview(cur_), thr_.as<double>(),
@@ -1238,9 +1293,11 @@ class EngineImpl final : public EngineBase {
     k_red_reset<<<1, 1, 0, stream_>>>(&d_stats_->red[2]);
     if (G_) k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, &d_stats_->red[2]);
     launches_ += 3;
+    if (diag) launch_diag();
     fetch_stats();
     PP_CUDA(cudaGetLastError());
     const DevStats& st = *h_stats_;
+    diag_n_ = st.diag_count;
     counters_.records_sent += st.records;
     counters_.removed += st.removed;
     if (st.err_budget) {
@@ -1616,6 +1673,8 @@ class EngineImpl final : public EngineBase {
   int cur_ = 0, gcur_ = 0;
   uint32_t G_ = 0;
   uint64_t bump_ = 0, live_ = 0;
+  DiagPinned* h_diag_ = nullptr;
+  uint64_t diag_n_ = 0, diag_copied_ = 0;
   uint64_t arena_max_ = 0;  // per-arena capacity of the memory plan (strings)
   bool tight_arena_ = false;  // PP_TIGHT_ARENA: minimal arenas (tests of the resume paths)
   static constexpr size_t kLazyWindow = 4096;  // gates per deferred-truncation window
@@ -1732,6 +1791,11 @@ int pp_apply_gate(pp_engine* e, const pp_gate* gate) {
 int pp_apply_gates(pp_engine* e, const pp_gate* gates, size_t count) {
   if (!e || (!gates && count)) return PP_ERR_INVALID;
   return guarded(e, [&] { e->impl->apply_gates(gates, count); });
+}
+
+int pp_apply_layer(pp_engine* e, const pp_gate* gates, size_t count, double* observable) {
+  if (!e || (!gates && count) || !observable) return PP_ERR_INVALID;
+  return guarded(e, [&] { *observable = e->impl->apply_layer(gates, count); });
 }
 
 int pp_truncate_now(pp_engine* e) {
