@@ -1173,21 +1173,43 @@ struct GroupStatsSmem {
 __device__ __forceinline__ void reduce_group_stats(GroupStatsSmem& r, double& vmax, double& vmin, double& vall,
                                                    uint32_t& nonfinite, unsigned long long& records,
                                                    unsigned long long& removed) {
-  vmax = warp_max(vmax);
-  vmin = warp_min(vmin);
-  vall = warp_max(vall);
-  records = warp_sum64(records);
-  removed = warp_sum64(removed);
+  // |c| statistics are non-negative and never NaN (fmax/fmin drop NaN), so
+  // their bit patterns reduce with REDUX; per-thread counts fit 32 bits
+  const unsigned long long bmax = warp_max_bits((unsigned long long)__double_as_longlong(vmax));
+  const unsigned long long bmin = warp_min_bits((unsigned long long)__double_as_longlong(vmin));
+  const unsigned long long ball = warp_max_bits((unsigned long long)__double_as_longlong(vall));
+  const uint32_t rec = __reduce_add_sync(0xffffffffu, (uint32_t)records);
+  const uint32_t rem = __reduce_add_sync(0xffffffffu, (uint32_t)removed);
   nonfinite = __any_sync(0xffffffffu, nonfinite);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();
   if (lane == 0) {
-    r.mx[warp] = vmax;
-    r.mn[warp] = vmin;
-    r.all[warp] = vall;
-    r.rec[warp] = records;
-    r.rem[warp] = removed;
+    r.mx[warp] = __longlong_as_double((long long)bmax);
+    r.mn[warp] = __longlong_as_double((long long)bmin);
+    r.all[warp] = __longlong_as_double((long long)ball);
+    r.rec[warp] = rec;
+    r.rem[warp] = rem;
     r.nf[warp] = nonfinite;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one thread folds the warps, every thread reads the result
+    double a = r.mx[0], b = r.mn[0], c = r.all[0];
+    unsigned long long d = r.rec[0], e = r.rem[0];
+    uint32_t f = r.nf[0];
+    for (uint32_t w = 1; w < kWarps; ++w) {
+      a = fmax(a, r.mx[w]);
+      b = fmin(b, r.mn[w]);
+      c = fmax(c, r.all[w]);
+      d += r.rec[w];
+      e += r.rem[w];
+      f |= r.nf[w];
+    }
+    r.mx[0] = a;
+    r.mn[0] = b;
+    r.all[0] = c;
+    r.rec[0] = d;
+    r.rem[0] = e;
+    r.nf[0] = f;
   }
   __syncthreads();
   vmax = r.mx[0];
@@ -1196,14 +1218,6 @@ __device__ __forceinline__ void reduce_group_stats(GroupStatsSmem& r, double& vm
   records = r.rec[0];
   removed = r.rem[0];
   nonfinite = r.nf[0];
-  for (uint32_t w = 1; w < kWarps; ++w) {
-    vmax = fmax(vmax, r.mx[w]);
-    vmin = fmin(vmin, r.mn[w]);
-    vall = fmax(vall, r.all[w]);
-    records += r.rec[w];
-    removed += r.rem[w];
-    nonfinite |= r.nf[w];
-  }
   __syncthreads();
 }
 
@@ -1221,6 +1235,7 @@ template <int W>
 __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
                                                            int keep_zeros, unsigned int* work, const double* tpred,
                                                            unsigned long long* gmax_out, DevStats* st) {
+  __shared__ uint32_t s_touch[kMaxSubGates / 32];
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
@@ -1285,9 +1300,27 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
       k0 = (stamp - seq0 < (uint32_t)gates.ng) ? (int)(stamp - seq0) + 1 : 0;  // resume after the stamp
     }
     int last = -1;  // last gate applied to this group (spec: truncations after it are pending)
-    for (int k = k0; k <= gates.ng; ++k) {
+    // the gates that touch this group, as a bit mask built by one ballot per warp
+    {
+      const int k = (int)tid;
+      const bool t = k < gates.ng && (z.w[gates.wq[k < kMaxSubGates ? k : 0]] & gates.mq[k < kMaxSubGates ? k : 0]);
+      const uint32_t b = __ballot_sync(0xffffffffu, t);
+      __syncthreads();  // the previous group's readers of s_touch are done
+      if ((tid & 31) == 0 && tid < kMaxSubGates) s_touch[tid >> 5] = b;
+      __syncthreads();
+    }
+    // next touching gate at or after k (gates.ng: the end step; ng + 1: done)
+    auto next_touch = [&](int k) {
+      if (k >= gates.ng) return k;
+      for (int w = k >> 5; w < kMaxSubGates / 32; ++w) {
+        uint32_t bits = s_touch[w];
+        if (w == (k >> 5)) bits &= ~0u << (k & 31);
+        if (bits) return min((w << 5) + __ffs(bits) - 1, gates.ng);
+      }
+      return gates.ng;
+    };
+    for (int k = next_touch(k0); k <= gates.ng; k = next_touch(k + 1)) {
       const bool end = k == gates.ng;
-      if (!end && !(z.w[gates.wq[k]] & gates.mq[k])) continue;
       if (spec) {
         // gates (last, k) did not touch the group: it held its values, each
         // of those gates' truncations applied to it
