@@ -443,7 +443,7 @@ struct SegSmem {
   double val[kSeg];
   alignas(16) uint32_t blk[kSeg];  // block id per string (stored as uint4)
   uint32_t bstart[kSeg + 1];     // first string of each block (+ end)
-  uint32_t bmid[kSeg];           // first class-1 string of each block
+  uint32_t bys[kSeg];            // |Y| (cosets) of each block
   uint32_t bobase[kSeg];         // output slot base of each block
   alignas(16) uint32_t pre[kSeg + 4];  // exclusive prefixes: pairs << 16 | unpaired class-1
   union {
@@ -525,7 +525,6 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
   const uint32_t has_next = (!PACK && p + L < n) ? 1u : 0u;
   const bool lazy = PACK ? pk->tin[0] >= 0.0 : tin >= 0.0;  // deferred truncation (uniform per launch)
   const double nsin = -sinv;
-  const uint64_t* kq = sm.key + wq * (kSeg + 1);  // the plane word holding bit q
   __syncthreads();  // previous users of the shared buffers are done
   for (uint32_t i = tid; i < L + has_next; i += kCta) {
     uint64_t a;
@@ -585,29 +584,22 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
   }
   const uint32_t nbc = sm.nbc, Lc = sm.lc;
   if (nbc == 0) return 0;
-  // mid of each block: its first class-1 string (class-1 strings close the block)
-  for (uint32_t b = tid; b < nbc; b += kCta) sm.bmid[b] = sm.bstart[b + 1];
-  __syncthreads();
-  for (uint32_t i = tid; i < Lc; i += kCta)
-    if ((kq[i] & mq) && ((sm.f[i] & 1u) || !(kq[i - 1] & mq))) sm.bmid[sm.blk[i]] = i;
-  __syncthreads();
-  // partners: class-0 x pairs with x | e_q in [mid, end), class-1 x with x &~e_q in [start, mid)
+  // partners: inside a block (equal bits above q) every class-1 key exceeds
+  // every class-0 key, so the lower bound of x | e_q (class 0) lands in the
+  // class-1 part and that of x &~e_q (class 1) in the class-0 part: one search
+  // over the whole block, no split point needed
   for (uint32_t i = tid; i < kSeg; i += kCta) {
     uint8_t fl = i < kSeg ? sm.f[i] : 0;
     if (i < Lc) {
-      const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1], m = sm.bmid[b];
+      const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1];
       Plane<W> k = sk_load<W>(sm.key, kSeg + 1, i);
-      if (!(k.w[wq] & mq)) {
-        k.w[wq] |= mq;
-        uint32_t lb = seg_lower_bound<W>(sm.key, m, be, k);
-        if (lb < be && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), k)) fl |= 2;
-        sm.lbv[i] = lb;
-      } else {
-        k.w[wq] &= ~mq;
-        uint32_t lb = seg_lower_bound<W>(sm.key, bs, m, k);
-        if (!(lb < m && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), k))) fl |= 4;
-        sm.lbv[i] = lb;
-      }
+      const bool c1 = (k.w[wq] & mq) != 0;
+      k.w[wq] ^= mq;
+      const uint32_t lb = seg_lower_bound<W>(sm.key, bs, be, k);
+      const bool found = lb < be && plane_eq<W>(sk_load<W>(sm.key, kSeg + 1, lb), k);
+      if (!c1 && found) fl |= 2;
+      if (c1 && !found) fl |= 4;
+      sm.lbv[i] = lb;
     }
     sm.f[i] = fl;
   }
@@ -639,6 +631,7 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
       if (b < nbc) {
         const uint32_t bs = sm.bstart[b], be = sm.bstart[b + 1];
         ys[v] = (be - bs) - ((sm.pre[be] >> 16) - (sm.pre[bs] >> 16));
+        sm.bys[b] = ys[v];
       }
       bsum += 2 * ys[v];
     }
@@ -667,11 +660,12 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     const bool pc = lazy && is_pending(c);
     if (pc) ++removed;
     if (cls1 && !(fl & 4)) continue;  // paired class-1: its class-0 partner owns the coset
-    const uint32_t b = sm.blk[i], bs = sm.bstart[b], be = sm.bstart[b + 1], m = sm.bmid[b];
+    const uint32_t b = sm.blk[i], bs = sm.bstart[b];
     const uint32_t lb = sm.lbv[i];
-    const uint32_t um = sm.pre[m] & 0xffffu;
+    // unpaired class-1 strings below the block's class-1 part = below its start
+    const uint32_t um = sm.pre[bs] & 0xffffu;
     const uint32_t ry = cls1 ? (lb - bs) + ((sm.pre[i] & 0xffffu) - um) : (i - bs) + ((sm.pre[lb] & 0xffffu) - um);
-    const uint32_t ysz = (be - bs) - ((sm.pre[be] >> 16) - (sm.pre[bs] >> 16));
+    const uint32_t ysz = sm.bys[b];
     const uint32_t s0 = sm.bobase[b] + ry, s1 = s0 + ysz;
     Plane<W> y = k, y1 = k;
     y.w[wq] &= ~mq;
