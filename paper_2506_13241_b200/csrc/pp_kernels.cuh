@@ -647,6 +647,7 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
   }
   __syncthreads();
   const uint32_t s2 = sm.scan[33];
+  bool hole = false;  // this thread left a slot unemitted
   // values: Rx rule (engine.cpp:218-227 + term_map.hpp:77-79); the owner of
   // a coset (its class-0 string, or an unpaired class-1 string) fills both
   // output slots.  Rank in Y = class-0 keys below + unpaired class-1 keys below.
@@ -713,14 +714,15 @@ __device__ uint32_t seg_branch(SegSmem<W>& sm, ArenaView<W> ar, uint64_t src, ui
     sk_store<W>(sm.okey, 2 * kSeg, s1, y1);
     sm.oval[s1] = v1;
     sm.oemit[s1] = e1;
+    hole |= !(e0 && e1);
   }
-  __syncthreads();
   // compaction: holes are exact zeros (removed strings); one blocked scan
   // over the emit bytes gives every slot its output position, then a
-  // coalesced store reads the slots in position order
+  // coalesced store reads the slots in position order.  Without holes (the
+  // common case at epsilon0 = 0) the slots are the output as they stand.
   constexpr uint32_t kSV = 2 * kSeg / kCta;
-  uint32_t ecnt;
-  {
+  uint32_t ecnt = s2;
+  if (__syncthreads_count(hole)) {
     const uint2 eb = reinterpret_cast<const uint2*>(sm.oemit)[tid];  // slots kSV tid .. kSV tid + 7
     const uint32_t base = tid * kSV;
     uint32_t m0 = 0;
