@@ -23,6 +23,7 @@
 
 #include "../../include/pauliprop_gpu.h"
 #include "pp_regroup.cuh"
+#include "pp_zz.cuh"
 
 namespace ppgpu {
 
@@ -301,6 +302,14 @@ class EngineImpl final : public EngineBase {
                                  (int)big_sort_smem()));
     PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    PP_CUDA(cudaFuncSetAttribute(k_branch_zz<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(ZzSmem<W>)));
+    {
+      int sms = 148, occ = 1;
+      PP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
+      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_branch_zz<W>, kCta, sizeof(ZzSmem<W>)));
+      zz_grid_ = (uint32_t)(sms * std::max(occ, 1));
+    }
     {  // persistent branch grids: every resident CTA slot of the device
       int sms = 148, occ_x = 1, occ_s = 1;
       PP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
@@ -1320,6 +1329,7 @@ class EngineImpl final : public EngineBase {
     }
     live_ = live_bound_ = st.red[2].live;
     bump_ = bump_bound_ = st.bump;
+    maxcnt_ = G_ ? st.red[2].maxcnt : 0u;
     if (truncated_since_sync_) gmax_ = __builtin_bit_cast(double, st.last_gmax_bits);
     // epsilon0 == 0 fast path: the skipped truncations would have used the
     // max after the last gate, which survives its own truncation
@@ -1364,6 +1374,73 @@ class EngineImpl final : public EngineBase {
   }
   uint32_t reduce_grid() const { return 148u * 4u; }
 
+  // ----- Z-type generator (x_J = 0): pairs of z-groups (pp_zz.cuh).  Returns
+  // false when a pair could exceed one segment; the caller then regroups.
+  bool apply_zz(const pp_gate& gate, const uint64_t* jzw) {
+    auto t0 = Clock::now();
+    sync_state();
+    if (2ull * maxcnt_ > kZSeg) return false;
+    const bool budget = cfg_.max_terms != 0 && !external();
+    const bool do_trunc = cfg_.cadence == PP_CADENCE_GATE;
+    const bool epi = !external() && !(cfg_.epsilon0 == 0.0 && !budget && !may_hold_zeros_);
+    const bool lazy = epi && do_trunc && !budget && cfg_.epsilon0 > 0.0 && !keep_zeros_ &&
+                      std::getenv("PP_EAGER_TRUNCATION") == nullptr;
+    Plane<W> jz;
+    for (int k = 0; k < W; ++k) jz.w[k] = jzw[k];
+    if (lazy) thr_.ensure(kLazyWindow * sizeof(double));
+    for (int attempt = 0; G_ > 0; ++attempt) {
+      if (attempt > 64) throw EngineError(PP_ERR_RESOURCE, "arena cannot hold the Z-type gate");
+      grow_groups_preserving(2 * G_ + 1024);  // room for a partner per group
+      if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
+      uint64_t tc = 1024;
+      while (tc < 2ull * G_) tc <<= 1;
+      ztab_.ensure(tc * (8 + 8 * W + 4));
+      ZTable<W> t;
+      char* tb = ztab_.as<char>();
+      t.fp = reinterpret_cast<unsigned long long*>(tb);
+      for (int k = 0; k < W; ++k) t.z[k] = reinterpret_cast<uint64_t*>(tb + tc * 8 * (1 + k));
+      t.gid = reinterpret_cast<uint32_t*>(tb + tc * 8 * (1 + W));
+      t.mask = tc - 1;
+      push_scalars(bseq_);
+      PP_CUDA(cudaMemsetAsync(&d_stats_->zz_newg, 0, 4 * sizeof(unsigned int), stream_));
+      PP_CUDA(cudaMemsetAsync(t.fp, 0, tc * 8, stream_));
+      if (lazy) {
+        PP_CUDA(cudaMemsetAsync(thr_.p, 0, 2 * sizeof(double), stream_));
+        lazy_open_ = true;
+        lazy_base_ = bseq_;
+        lazy_len_ = 1;
+      }
+      k_ztab_build<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, t);
+      k_branch_zz<W><<<zz_grid_, kCta, sizeof(ZzSmem<W>), stream_>>>(
+          gview(gcur_), G_, aview(cur_), jz, gate.cos_theta, gate.sin_theta, keep_zeros_, t, &d_stats_->work[0],
+          &d_stats_->work[1], 0, d_stats_, lazy ? thr_.as<double>() : nullptr, lazy ? &d_stats_->red[0] : nullptr);
+      launches_ += 2;
+      ++branch_launches_;
+      if (epi) launch_epilogue(0, do_trunc, budget, lazy);
+      dirty_ = true;
+      fetch_stats();  // the gate's one round trip: new groups, arena fault
+      PP_CUDA(cudaGetLastError());
+      if (h_stats_->zz_err) throw EngineError(PP_ERR_INTERNAL, "Z-type gate: pair larger than a segment");
+      G_ += h_stats_->zz_newg;
+      maxcnt_ = std::max<uint32_t>(maxcnt_, h_stats_->zz_maxcnt);
+      if (!h_stats_->err_arena) break;
+      k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);  // done pairs carry this gate's stamp
+      ++launches_;
+      lazy_open_ = false;  // the faulted launch set no threshold
+      gc_into_other(next_arena_target());
+    }
+    if (epi && do_trunc) truncated_since_sync_ = true;
+    if (!epi && do_trunc && !external()) gmax_stale_ = true;
+    if (keep_zeros_) may_hold_zeros_ = true;
+    dirty_ = true;
+    bseq_ += 1;
+    ++gates_applied_;
+    ++counters_.gates;
+    ++counters_.batches_sent;
+    counters_.branch_ns += ns_since(t0);
+    return true;
+  }
+
   // ----- one gate
   void apply_one(const pp_gate& gate) {
     uint64_t jx[2], jz[2];
@@ -1376,6 +1453,8 @@ class EngineImpl final : public EngineBase {
       // identity generator: commutes with everything, no records
     } else if (zfree && nx == 1) {
       run_rx(&gate, 1);
+      return;
+    } else if (nx == 0 && std::getenv("PP_ZZ_REGROUP") == nullptr && apply_zz(gate, jz)) {
       return;
     } else {
       GateProducer<W> p;
@@ -1694,6 +1773,9 @@ class EngineImpl final : public EngineBase {
 
   uint32_t branch_grid_ = 148u * 2u;
   uint32_t sub_grid_ = 148u * 2u;
+  uint32_t zz_grid_ = 148u * 2u;
+  uint32_t maxcnt_ = 0x7fffffffu;  // largest group at the last full sync (bounds Z-type pair sizes)
+  DevBuf ztab_;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_events_, free_events_;
   unsigned long long seed_;
   unsigned long long h_records_ = 0;

@@ -58,7 +58,7 @@ struct RedSlot {            // group reduction of one epilogue
   unsigned long long gmax_bits;
   unsigned long long gmin_bits;
   unsigned int nonfinite;
-  unsigned int pad;
+  unsigned int maxcnt;      // largest group (k_reduce)
 };
 struct SelSlot {            // affected-group selection of one X-type gate
   unsigned long long aff_elems;
@@ -71,6 +71,7 @@ __device__ __forceinline__ void clear_red(RedSlot* r) {
   r->gmax_bits = 0;
   r->gmin_bits = 0x7ff0000000000000ull;
   r->nonfinite = 0;
+  r->maxcnt = 0;
 }
 
 struct DevStats {
@@ -102,6 +103,10 @@ struct DevStats {
   unsigned int err_arena;          // sticky: a branch allocation did not fit; run must resume
   unsigned long long err_seq;      // first gate sequence number that overflowed
   unsigned long long scan_total;   // regroup: total records (copied from the scan)
+  unsigned int zz_newg;            // Z-type gate: groups created for missing partners
+  unsigned int zz_maxcnt;          // Z-type gate: largest group written
+  unsigned int zz_err;             // Z-type gate: a pair exceeded the segment (host pre-check failed)
+  unsigned int zz_pad;
 };
 
 // Scalars a launch run reads from device memory, so that a captured CUDA
@@ -1451,7 +1456,7 @@ __global__ void __launch_bounds__(kCta) k_reduce(GroupView<W> g, const DevStats*
   // every warp serialise in L2)
   unsigned long long live = 0;
   double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
-  uint32_t nf = 0;
+  uint32_t nf = 0, mc = 0;
   if (thr) {
     // deferred truncation: a group whose max is pending removal holds no live
     // string (every other value is smaller).  thr[0] bounds every slot, so
@@ -1474,9 +1479,12 @@ __global__ void __launch_bounds__(kCta) k_reduce(GroupView<W> g, const DevStats*
         mx = fmax(mx, g.gmax[i]);
         mn = fmin(mn, g.gmin[i]);
         nf |= g.flags[i] & 1u;
+        mc = max(mc, c);
       }
     }
   }
+  mc = __reduce_max_sync(0xffffffffu, mc);
+  if ((threadIdx.x & 31) == 0 && mc) atomicMax(&out->maxcnt, mc);
   live = warp_sum64(live);
   mx = warp_max(mx);
   mn = warp_min(mn);
