@@ -173,6 +173,11 @@ class DevicePool {
     for (auto& kv : free_[dev]) b += kv.first;
     return b;
   }
+  size_t largest_cached(int dev) {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = free_.find(dev);
+    return it == free_.end() || it->second.empty() ? 0 : it->second.rbegin()->first;
+  }
   void trim(int dev) {
     std::lock_guard<std::mutex> lk(mu_);
     for (auto& [b, p] : free_[dev]) cudaFree(p);
@@ -393,6 +398,12 @@ class EngineImpl final : public EngineBase {
     const uint32_t G = (uint32_t)gcnt.size();
     // fresh buffers
     cur_ = 0;
+    // a fresh engine starts on the largest block a previous engine left in
+    // the pool (simulate() creates one engine per call), else at 1 Mi strings
+    if (arena_[0].cap == 0 && !tight_arena_) {
+      const uint64_t warm = DevicePool::get().largest_cached(cfg_.device) / R;
+      ensure_arena(0, std::min<uint64_t>(std::max<uint64_t>(warm, 1u << 20), std::max<uint64_t>(arena_max_, 1u << 16)));
+    }
     ensure_arena(0, std::max<uint64_t>(1u << 16, 4 * n));
     ensure_groups(0, std::max<uint32_t>(G, 1024));
     gcur_ = 0;
@@ -517,29 +528,26 @@ class EngineImpl final : public EngineBase {
         sgates.sinv[i] = prm[i].sinv;
         sgates.any[prm[i].wq] |= prm[i].mq;
       }
-      for (int attempt = 0;; ++attempt) {
-        sync_state();
-        if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
-        push_scalars(seq0);
-        std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
-        PP_CUDA(cudaEventRecord(ev.first, stream_));
-        k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
-            gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], nullptr, nullptr, d_stats_);
-        PP_CUDA(cudaEventRecord(ev.second, stream_));
-        pending_events_.push_back(ev);
-        ++launches_;
-        ++branch_launches_;
-        if (keep_zeros_) may_hold_zeros_ = true;
-        if (do_trunc && !external()) gmax_stale_ = true;
-        dirty_ = true;
-        sync_state();
-        if (!arena_fault_) break;
-        if (attempt > 64) throw EngineError(PP_ERR_RESOURCE, "arena cannot hold the sublayer");
-        k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
-        ++launches_;
-        arena_fault_ = false;
-        gc_into_other(next_arena_target());  // groups resume after their stamps
+      // dense path (k_branch_sublayer / dense_group): zeros dropped, every
+      // gate of the run on its own qubit
+      {
+        bool distinct = true;
+        for (size_t i = 0; i < count && distinct; ++i)
+          for (size_t j = 0; j < i; ++j)
+            if (prm[i].wq == prm[j].wq && prm[i].mq == prm[j].mq) {
+              distinct = false;
+              break;
+            }
+        sgates.dense = distinct && !keep_zeros_ && !may_hold_zeros_ && std::getenv("PP_NO_DENSE") == nullptr;
       }
+      sync_state();
+      if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
+      // launched without a round trip: an arena overflow is found and
+      // resumed by the next sync_state (resume_sublayer)
+      sub_gates_ = sgates;
+      sub_seq0_ = seq0;
+      launch_sublayer();
+      sub_pending_ = true;
       bseq_ = seq0 + count;
       gates_applied_ += count;
       counters_.gates += count;
@@ -726,6 +734,38 @@ class EngineImpl final : public EngineBase {
     return false;  // did not converge: the caller runs the gates one by one
   }
 
+  void launch_sublayer() {
+    push_scalars(sub_seq0_);
+    std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
+    PP_CUDA(cudaEventRecord(ev.first, stream_));
+    k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+        gview(gcur_), aview(cur_), sub_gates_, keep_zeros_, &d_stats_->work[0], nullptr, nullptr, d_stats_);
+    PP_CUDA(cudaEventRecord(ev.second, stream_));
+    pending_events_.push_back(ev);
+    ++launches_;
+    ++branch_launches_;
+    if (keep_zeros_) may_hold_zeros_ = true;
+    if (cfg_.cadence == PP_CADENCE_GATE && !external()) gmax_stale_ = true;
+    dirty_ = true;
+  }
+  // a sublayer stopped on an arena overflow: compact into a larger arena and
+  // relaunch; groups that finished carry the run's stamps and are skipped
+  void resume_sublayer(bool diag) {
+    sub_pending_ = false;
+    for (int attempt = 0; arena_fault_; ++attempt) {
+      if (attempt > 64) throw EngineError(PP_ERR_RESOURCE, "arena cannot hold the sublayer");
+      k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
+      ++launches_;
+      arena_fault_ = false;
+      // repeated overflows (a dense block larger than the usual growth):
+      // at least double the arena
+      gc_into_other(attempt >= 2 ? std::max<uint64_t>(next_arena_target(), std::min<uint64_t>(2 * arena_[cur_].cap, arena_max_))
+                                 : next_arena_target());
+      launch_sublayer();
+      sync_state(diag);
+    }
+  }
+
   void launch_branch(const RxParam& p, uint32_t rel, bool lazy) {
     k_branch_x<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
         gview(gcur_), aview(cur_), p.wq, p.mq, p.cosv, p.sinv, keep_zeros_, gview(gcur_).z[p.wq],
@@ -882,6 +922,7 @@ class EngineImpl final : public EngineBase {
     words_to_planes(words, x, z);
     if (W == 1 && (x[1] | z[1])) return 0.0;
     if (G_ == 0) return 0.0;
+    PP_CUDA(cudaStreamSynchronize(stream_));  // legacy-stream copies below
     GroupView<W> g = gview(gcur_);
     std::vector<uint64_t> gz(G_);
     std::vector<uint32_t> match(G_, 1);
@@ -915,6 +956,9 @@ class EngineImpl final : public EngineBase {
     sync_state();
     if (live_ > cap) throw EngineError(PP_ERR_INVALID, "export capacity too small");
     compact();  // one contiguous live range in the current arena
+    // the copies below run on the legacy stream, which does not order with
+    // the engine's non-blocking stream
+    PP_CUDA(cudaStreamSynchronize(stream_));
     const uint64_t n = live_;
     std::vector<uint64_t> xs(n * W), zs;
     std::vector<double> cs(n);
@@ -1218,13 +1262,26 @@ class EngineImpl final : public EngineBase {
     mem_report("gc ->", new_cap);
     const int o = 1 - cur_;
     ensure_arena(o, new_cap);
-    reset_stats(0);
+    uint64_t total = 0;
     if (G_) {
-      k_gc<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), G_, aview(cur_), aview(o), d_stats_);
+      const uint64_t ntiles = (G_ + kScanTile - 1) / kScanTile;
+      scan_tmp_.ensure((ntiles + 1) * 8);
+      scan_off_.ensure((size_t)G_ * 8);
+      unsigned long long* noff = scan_off_.as<unsigned long long>();
+      device_scan(gview(gcur_).cnt, G_, 0, noff, ntiles);
+      total = live_;  // sync_state above: live_ = sum of the group counts
+      if (total) {
+        const uint64_t tiles = (total + kGcTile - 1) / kGcTile;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(tiles, 148ull * 8ull);
+        k_gc_copy<W><<<grid, kCta, 0, stream_>>>(gview(gcur_), G_, noff, total, aview(cur_), aview(o));
+        ++launches_;
+      }
+      k_gc_finish<W><<<std::min<uint32_t>(blocks(G_), 148u * 8u), kCta, 0, stream_>>>(gview(gcur_), G_, noff);
       ++launches_;
     }
-    fetch_stats();
-    bump_ = bump_bound_ = h_stats_->bump;
+    reset_stats(total);
+    PP_CUDA(cudaGetLastError());
+    bump_ = bump_bound_ = total;
     cur_ = o;
   }
   void compact() {
@@ -1238,6 +1295,7 @@ class EngineImpl final : public EngineBase {
   // when it needs exact sizes (sync_state).
   bool external() const { return (cfg_.flags & PP_FLAG_EXTERNAL_TRUNCATION) != 0; }
   void epilogue(bool do_truncate, bool check_budget) {
+    if (sub_pending_) sync_state();  // a sublayer must be complete before the epilogue reads the store
     if (external()) {  // the orchestrator truncates with a global threshold
       dirty_ = true;
       return;
@@ -1350,6 +1408,10 @@ class EngineImpl final : public EngineBase {
     k_clear_cumulative<<<1, 1, 0, stream_>>>(d_stats_);
     ++launches_;
     dirty_ = false;
+    if (sub_pending_) {
+      if (arena_fault_) resume_sublayer(diag);
+      sub_pending_ = false;
+    }
   }
   uint32_t persistent_grid() const { return 148u * 8u; }
 
@@ -1578,7 +1640,11 @@ class EngineImpl final : public EngineBase {
     gates_applied_ += count;
     counters_.gates += count;
     auto t1 = Clock::now();
-    epilogue(cfg_.cadence == PP_CADENCE_GATE, false);
+    // A Clifford run is a signed permutation of the strings: |c| values,
+    // hence the global max, are unchanged and no zero or NaN appears, so at
+    // epsilon0 = 0 (threshold 0, no zeros held) the truncation is a no-op and
+    // the regroup left the store exactly known (no sync needed).
+    if (!(cfg_.epsilon0 == 0.0 && !may_hold_zeros_ && !external())) epilogue(cfg_.cadence == PP_CADENCE_GATE, false);
     counters_.truncate_ns += ns_since(t1);
   }
 
@@ -1769,6 +1835,9 @@ class EngineImpl final : public EngineBase {
   bool dirty_ = false, truncated_since_sync_ = false, gmax_stale_ = false, may_hold_zeros_ = false;
   uint64_t eseq_ = 0, bseq_ = 0;
   bool arena_fault_ = false;
+  bool sub_pending_ = false;  // a sublayer launch not yet checked for an arena overflow
+  SubGates sub_gates_{};
+  uint64_t sub_seq0_ = 0;
   uint64_t arena_fault_seq_ = 0;
 
   uint32_t branch_grid_ = 148u * 2u;

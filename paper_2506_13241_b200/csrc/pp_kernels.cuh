@@ -1132,6 +1132,7 @@ struct SubGates {
   double cosv[kMaxSubGates];
   double sinv[kMaxSubGates];
   uint64_t any[2];  // union of the gate masks per plane word
+  int dense;        // dense path allowed: distinct qubits, zeros dropped (k_branch_sublayer)
 };
 
 // copy group region [src, src+n) to dst keeping |c| > T (truncation into
@@ -1222,6 +1223,318 @@ __device__ __forceinline__ void reduce_group_stats(GroupStatsSmem& r, double& vm
   __syncthreads();
 }
 
+
+// ---------------------------------------------------------------------------
+// Dense sublayer path (zeros dropped, distinct qubits, one x-class per group).
+//
+// A run of Rx gates on distinct qubits acts on a z-group as a tensor product
+// of 2x2 rotations over the x bits T = {q : z_q = 1, gate on q in the run}.
+// When every string of the group agrees on x outside T (one class, F), the
+// group is a vector over the 2^m points of T (m = |T|): string x sits at
+// b = pext(x, T) (T bits in ascending position, so b order is x order) and
+// every other point is zero.  Gate q is a butterfly over bit rank(q) of b
+// with the reference's per-string arithmetic (engine.cpp:218-227,
+// term_map.hpp:77-79)
+//   v0 = c0 cos [+ d0 = -sin c1 if d0 != 0],  v1 = c1 cos [+ d1 = sin c0 if d1 != 0]
+// A zero point is an absent string: zero times cos and a zero delta leave
+// every nonzero value unchanged, so the nonzero points after the run are
+// the reference's strings bit for bit.  Records (nonzero deltas) and removed
+// strings (points present after a gate -- nonzero before it or hit by a
+// nonzero delta -- whose value is zero) are counted per point as the
+// reference counts them per key.
+//
+// The group is read once and its output written once, already sorted.  The
+// stages run in shared memory when 2^m <= kDenseSmem; larger blocks live in
+// the output region's coefficient plane and pass through shared memory
+// kDenseSmemLog stages at a time (each pass: the cosets of those stages'
+// bits, one shared-memory tile each).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kDenseSmemLog = 13;
+constexpr uint32_t kDenseSmem = 1u << kDenseSmemLog;  // doubles of the dynamic buffer
+constexpr int kDenseMaxLog = 24;                      // larger blocks take the per-gate path
+
+template <int W>
+struct DenseCtl {
+  Plane<W> T;                   // touched x bits
+  Plane<W> F;                   // the group's x bits outside T
+  double scos[kMaxSubGates], ssin[kMaxSubGates];  // per stage
+  uint32_t tw[kMaxSubGates / 32];                 // touching gates of the run (from k0)
+  uint8_t sbit[kMaxSubGates];   // b bit of each stage, in gate order
+  uint8_t sgate[kMaxSubGates];  // gate of each stage
+  int m, klast;
+  uint32_t P;                   // pass: b bits of its stages
+  uint32_t deplo[128], dephi[64];  // pass: tile index -> b offset (low 7 / high 6 index bits)
+  uint8_t tpos[32];             // b bit j -> x bit position (ascending)
+  unsigned long long dst;
+  uint32_t fail;
+};
+
+template <int W>
+__device__ __forceinline__ uint32_t dense_pext(const Plane<W>& x, const Plane<W>& T) {
+  uint32_t b = 0, j = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+    for (uint64_t t = T.w[k]; t; t &= t - 1, ++j)
+      if (x.w[k] & t & (~t + 1)) b |= 1u << j;
+  return b;
+}
+template <int W>
+__device__ __forceinline__ Plane<W> dense_pdep(uint32_t b, const Plane<W>& T, Plane<W> x) {
+  uint32_t j = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+    for (uint64_t t = T.w[k]; t; t &= t - 1, ++j)
+      if ((b >> j) & 1u) x.w[k] |= t & (~t + 1);
+  return x;
+}
+// deposit the low bits of i into the set bits of mask (32-bit index space)
+__device__ __forceinline__ uint32_t dense_dep32(uint32_t i, uint32_t mask) {
+  uint32_t r = 0;
+  for (uint32_t t = mask; t; t &= t - 1, i >>= 1)
+    if (i & 1u) r |= t & (~t + 1);
+  return r;
+}
+
+__device__ __forceinline__ void dense_bfly(double& a, double& b, double cosv, double sinv, double nsin,
+                                           unsigned long long& records, unsigned long long& removed) {
+  const double c0 = a, c1 = b;
+  const double d1 = __dmul_rn(sinv, c0);  // child of the Z parent (x_q = 0), lands at x_q = 1
+  const double d0 = __dmul_rn(nsin, c1);  // child of the Y parent (x_q = 1), lands at x_q = 0
+  double v0 = __dmul_rn(c0, cosv), v1 = __dmul_rn(c1, cosv);
+  if (d0 != 0.0) {
+    v0 = __dadd_rn(v0, d0);
+    ++records;
+  }
+  if (d1 != 0.0) {
+    v1 = __dadd_rn(v1, d1);
+    ++records;
+  }
+  if ((c0 != 0.0 || d0 != 0.0) && v0 == 0.0) ++removed;
+  if ((c1 != 0.0 || d1 != 0.0) && v1 == 0.0) ++removed;
+  a = v0;
+  b = v1;
+}
+
+// butterflies of stages [j0, j1) over a tile of 2^u doubles in shared memory;
+// P: the b bits of the tile (stage bit p is tile bit popc(P & (2^p - 1)))
+template <int W>
+__device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, int j0, int j1, const DenseCtl<W>& dc,
+                                             const SubGates& gates, unsigned long long& records,
+                                             unsigned long long& removed) {
+  const uint32_t half = (1u << u) >> 1;
+  for (int j = j0; j < j1; ++j) {
+    const uint32_t p = __popc(P & ((1u << dc.sbit[j]) - 1u));
+    const double cosv = dc.scos[j], sinv = dc.ssin[j], nsin = -sinv;
+    const uint32_t lo = (1u << p) - 1u;
+    for (uint32_t t = threadIdx.x; t < half; t += kCta) {
+      const uint32_t b0 = ((t & ~lo) << 1) | (t & lo);
+      dense_bfly(d[b0], d[b0 | (1u << p)], cosv, sinv, nsin, records, removed);
+    }
+    __syncthreads();
+  }
+}
+
+// Returns 1 when the group was applied, 0 when it is not eligible (the
+// caller takes the per-gate path), -1 when its output did not fit the arena
+// (the group is untouched and resumes in the next launch).
+template <int W>
+__device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, uint32_t* scan, GroupView<W> g,
+                           ArenaView<W> ar, const SubGates& gates, const SubGates& gp, uint32_t gid, uint32_t n, uint64_t src, int k0,
+                           const uint32_t* s_touch, uint32_t seq0, unsigned long long cap, DevStats* st,
+                           unsigned long long& aff_elems) {
+  const uint32_t tid = threadIdx.x;
+  // stage list, in parallel: thread k owns gate k (parameters read from the
+  // kernel's parameter block once per gate, not serially per group)
+  __syncthreads();
+  if (tid < W) dc.T.w[tid] = 0;
+  if (tid < kMaxSubGates / 32) {
+    const uint32_t w0 = (uint32_t)k0 >> 5;
+    uint32_t t = tid < w0 ? 0u : s_touch[tid];
+    if (tid == w0) t &= ~0u << (k0 & 31);
+    dc.tw[tid] = t;
+  }
+  __syncthreads();
+  const int k = (int)tid;
+  const bool touch = k < gates.ng && ((dc.tw[k >> 5] >> (k & 31)) & 1u);
+  int wq = 0;
+  uint64_t mq = 0;
+  if (touch) {
+    wq = gp.wq[k];
+    mq = gp.mq[k];
+    atomicOr(reinterpret_cast<unsigned long long*>(&dc.T.w[wq]), (unsigned long long)mq);
+  }
+  __syncthreads();
+  if (touch) {
+    const Plane<W> T = dc.T;
+    uint32_t r = __popcll(T.w[wq] & (mq - 1));
+    for (int w = 0; w < wq; ++w) r += __popcll(T.w[w]);
+    uint32_t j = __popc(dc.tw[k >> 5] & ((1u << (k & 31)) - 1u));
+    for (int w = 0; w < (k >> 5); ++w) j += __popc(dc.tw[w]);
+    if (j < kMaxSubGates) {
+      dc.sbit[j] = (uint8_t)r;
+      dc.sgate[j] = (uint8_t)k;
+      dc.scos[j] = gp.cosv[k];
+      dc.ssin[j] = gp.sinv[k];
+    }
+  }
+  if (tid == 0) {
+    int m = 0, klast = -1;
+    for (int w = 0; w < kMaxSubGates / 32; ++w) {
+      m += __popc(dc.tw[w]);
+      if (dc.tw[w]) klast = 32 * w + 31 - __clz(dc.tw[w]);
+    }
+    dc.m = m;
+    dc.klast = klast;
+    Plane<W> F = load_plane<W>(ar.x, src);
+#pragma unroll
+    for (int w = 0; w < W; ++w) F.w[w] &= ~dc.T.w[w];
+    dc.F = F;
+    uint32_t j = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      for (uint64_t t = dc.T.w[w]; t && j < 32; t &= t - 1, ++j) dc.tpos[j] = (uint8_t)(64 * w + __ffsll((long long)t) - 1);
+  }
+  __syncthreads();
+  const int m = dc.m;
+  if (m == 0 || m > kDenseMaxLog) return 0;
+  const Plane<W> T = dc.T, F = dc.F;
+  // one class: every string agrees with the first outside T
+  bool one = true;
+  for (uint32_t i = tid; i < n; i += kCta) {
+    const Plane<W> x = load_plane<W>(ar.x, src + i);
+#pragma unroll
+    for (int k = 0; k < W; ++k) one &= (x.w[k] & ~T.w[k]) == F.w[k];
+  }
+  if (!__syncthreads_and(one)) return 0;
+  const uint32_t S = 1u << m;
+  if (tid == 0) {
+    const unsigned long long d = atomicAdd(&st->bump, (unsigned long long)S);
+    dc.dst = d;
+    dc.fail = d + S > cap;
+    if (dc.fail) {
+      atomicOr(&st->err_arena, 1u);
+      atomicMin(&st->err_seq, (unsigned long long)(seq0 + dc.sgate[0]));
+    }
+  }
+  __syncthreads();
+  if (dc.fail) return -1;
+  const uint64_t dst = dc.dst;
+  const bool in_smem = S <= kDenseSmem;
+  double* blk = in_smem ? dbuf : ar.c + dst;  // the dense block
+  // b -> x bits outside F, one table per byte of b (behind the dense tile)
+  Plane<W>* xt = reinterpret_cast<Plane<W>*>(dbuf + kDenseSmem);
+  for (uint32_t e = tid; e < 3 * 256; e += kCta) {
+    Plane<W> p;
+#pragma unroll
+    for (int w = 0; w < W; ++w) p.w[w] = 0;
+    const uint32_t j0 = 8 * (e >> 8);
+    for (uint32_t bit = 0; bit < 8; ++bit)
+      if (j0 + bit < (uint32_t)m && ((e >> bit) & 1u)) {
+        const uint32_t q = dc.tpos[j0 + bit];
+        p.w[q >> 6] |= 1ull << (q & 63);
+      }
+    xt[e] = p;
+  }
+  unsigned long long records = 0, removed = 0;
+  for (uint32_t i = tid; i < S; i += kCta) blk[i] = 0.0;
+  __syncthreads();
+  for (uint32_t i = tid; i < n; i += kCta) blk[dense_pext<W>(load_plane<W>(ar.x, src + i), T)] = ar.c[src + i];
+  __syncthreads();
+  if (in_smem) {
+    dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, gates, records, removed);
+  } else {
+    for (int j0 = 0; j0 < m; j0 += (int)kDenseSmemLog) {
+      const int j1 = min(m, j0 + (int)kDenseSmemLog);
+      if (tid == 0) {
+        // tile bits: this pass's stage bits, padded with the lowest other
+        // bits to a full tile (coalesced gathers, several cosets per tile)
+        uint32_t P = 0;
+        for (int j = j0; j < j1; ++j) P |= 1u << dc.sbit[j];
+        for (uint32_t b = 0; __popc(P) < (int)kDenseSmemLog; ++b) P |= 1u << b;
+        dc.P = P;
+      }
+      __syncthreads();
+      const uint32_t P = dc.P, u = kDenseSmemLog, Q = (S - 1u) & ~P;
+      {  // deposit tables: tile index bits 0-6 and 7-12 into P
+        uint32_t plo = P;
+        for (int c = 0; c < 7; ++c) plo &= plo - 1;
+        const uint32_t lo_mask = P & ~plo;
+        if (tid < 128) dc.deplo[tid] = dense_dep32(tid, lo_mask);
+        else if (tid < 192) dc.dephi[tid - 128] = dense_dep32(tid - 128, plo);
+      }
+      __syncthreads();
+      for (uint32_t sp = 0; sp < (S >> u); ++sp) {
+        const uint32_t base = dense_dep32(sp, Q);
+        for (uint32_t i = tid; i < (1u << u); i += kCta) dbuf[i] = blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]];
+        __syncthreads();
+        dense_stages<W>(dbuf, u, P, j0, j1, dc, gates, records, removed);
+        for (uint32_t i = tid; i < (1u << u); i += kCta) blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]] = dbuf[i];
+        __syncthreads();
+      }
+    }
+  }
+  // nonzero points in b (= x) order, compacted into the output region (in
+  // place for a block in global memory: a tile's writes land at or below its
+  // own positions, after all of its reads)
+  constexpr uint32_t kPer = 4;
+  double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll), vall = 0.0;
+  uint32_t nonfinite = 0;
+  uint32_t out = 0;
+  const uint32_t lane = tid & 31, warp = tid >> 5;
+  for (uint32_t base = 0; base < S; base += kCta * kPer) {
+    double v[kPer];
+    uint32_t bal[kPer];
+#pragma unroll
+    for (uint32_t e = 0; e < kPer; ++e) {  // striped: slot e covers [base + e kCta, base + (e+1) kCta)
+      const uint32_t b = base + e * kCta + tid;
+      v[e] = b < S ? blk[b] : 0.0;
+      bal[e] = __ballot_sync(0xffffffffu, v[e] != 0.0);
+      if (lane == 0) scan[e * kWarps + warp] = __popc(bal[e]);
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the kPer x kWarps counts, in b order
+      const uint32_t c = lane < kPer * kWarps ? scan[lane] : 0u;
+      const uint32_t inc = warp_incl_scan(c);
+      if (lane < kPer * kWarps) scan[lane] = inc - c;
+      if (lane == kPer * kWarps - 1) scan[kPer * kWarps] = inc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t e = 0; e < kPer; ++e) {
+      if (v[e] == 0.0) continue;
+      const uint32_t b = base + e * kCta + tid;
+      const uint32_t o = out + scan[e * kWarps + warp] + __popc(bal[e] & ((1u << lane) - 1u));
+      Plane<W> x = F;
+      const Plane<W> a0 = xt[b & 255u], a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
+#pragma unroll
+      for (int w = 0; w < W; ++w) x.w[w] |= a0.w[w] | a1.w[w] | a2.w[w];
+      store_plane<W>(ar.x, dst + o, x);
+      ar.c[dst + o] = v[e];
+      const double av = fabs(v[e]);
+      if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
+      vmax = fmax(vmax, av);
+      vmin = fmin(vmin, av);
+    }
+    out += scan[kPer * kWarps];
+    __syncthreads();
+  }
+  reduce_group_stats(gs, vmax, vmin, vall, nonfinite, records, removed);
+  if (tid == 0) {
+    g.off[gid] = dst;
+    g.cnt[gid] = out;
+    g.cap[gid] = S;
+    g.gmax[gid] = out ? vmax : 0.0;
+    g.gmin[gid] = out ? vmin : __longlong_as_double(0x7ff0000000000000ll);
+    g.flags[gid] = nonfinite;
+    g.stamp[gid] = seq0 + (uint32_t)dc.klast;
+    if (records) atomicAdd(&st->records, records);
+    if (removed) atomicAdd(&st->removed, removed);
+    atomicAdd(&st->out_elems, (unsigned long long)out);
+  }
+  aff_elems += n;
+  return 1;
+}
+
 // Modes:
 //  tpred == nullptr  (epsilon0 = 0, or per-layer cadence): only groups some
 //    gate touches; no truncation inside the run; resumable via stamps.
@@ -1251,7 +1564,17 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
   __shared__ GroupStatsSmem gs;
   __shared__ unsigned long long smax[kMaxSubGates];  // per-CTA per-gate max (bits)
   __shared__ uint32_t tscan[40];
-  for (int k = tid; k < gates.ng; k += kCta) smax[k] = 0ull;
+  __shared__ DenseCtl<W> dc;
+  __shared__ SubGates s_gp;  // the run's gates, read from the parameter block once per CTA
+  for (int k = tid; k < gates.ng; k += kCta) {
+    smax[k] = 0ull;
+    s_gp.wq[k] = gates.wq[k];
+    s_gp.mq[k] = gates.mq[k];
+    s_gp.cosv[k] = gates.cosv[k];
+    s_gp.sinv[k] = gates.sinv[k];
+  }
+  if (tid == 0) s_gp.ng = gates.ng;
+  __syncthreads();
   unsigned long long aff_elems = 0;
   bool failed = false;
   // contribute the group's current max to gates [a, b)
@@ -1277,8 +1600,12 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
     __syncthreads();
     if (tid == 0) s_gid = atomicAdd(work, 1u);
     __syncthreads();
-    const uint32_t gid = s_gid;
-    if (gid >= G || failed) break;
+    // dense runs: two sweeps over the table, groups with a large output
+    // (n 2^m >= one dense tile) first, so the longest groups start early
+    const bool lpt = !spec && gates.dense;
+    const uint32_t idx = s_gid;
+    if (idx >= (lpt ? 2 * G : G) || failed) break;
+    const uint32_t gid = idx < G ? idx : idx - G;
     Plane<W> z;
 #pragma unroll
     for (int k = 0; k < W; ++k) z.w[k] = g.z[k][gid];
@@ -1286,9 +1613,17 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
     if (n == 0) continue;
     if (!spec) {
       bool touched = false;
+      uint32_t mt = 0;
 #pragma unroll
-      for (int k = 0; k < W; ++k) touched |= (z.w[k] & gates.any[k]) != 0;
+      for (int k = 0; k < W; ++k) {
+        touched |= (z.w[k] & gates.any[k]) != 0;
+        mt += __popcll(z.w[k] & gates.any[k]);
+      }
       if (!touched) continue;
+      if (lpt) {
+        const bool big = mt >= kDenseSmemLog || ((unsigned long long)n << mt) >= kDenseSmem;
+        if (big != (idx < G)) continue;
+      }
     }
     uint64_t src = g.off[gid];
     uint32_t cap_g = g.cap[gid];
@@ -1309,6 +1644,15 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
       __syncthreads();  // the previous group's readers of s_touch are done
       if ((tid & 31) == 0 && tid < kMaxSubGates) s_touch[tid >> 5] = b;
       __syncthreads();
+    }
+    if (!spec && gates.dense) {
+      const int r = dense_group<W>(reinterpret_cast<double*>(smem_raw), dc, gs, tscan, g, ar, gates, s_gp, gid, n, src, k0,
+                                   s_touch, seq0, cap, st, aff_elems);
+      if (r < 0) {
+        failed = true;
+        break;
+      }
+      if (r > 0) continue;
     }
     // next touching gate at or after k (gates.ng: the end step; ng + 1: done)
     auto next_touch = [&](int k) {
@@ -1442,6 +1786,8 @@ template <int W>
 constexpr size_t branch_smem_bytes() {
   return sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
 }
+static_assert(branch_smem_bytes<1>() >= kDenseSmem * sizeof(double) + 3 * 256 * 8, "dense tile must fit the branch buffer");
+static_assert(branch_smem_bytes<2>() >= kDenseSmem * sizeof(double) + 3 * 256 * 16, "dense tile must fit the branch buffer");
 
 // ---------------------------------------------------------------------------
 // group-level reductions: live count, max |c|, min over group minima, NaN
@@ -1758,67 +2104,56 @@ __global__ void k_diag(GroupView<W> g, uint32_t G, ArenaView<W> ar, uint64_t* ou
 }
 
 // ---------------------------------------------------------------------------
-// compaction of the arena into the other buffer (garbage collection)
+// compaction of the arena into the other buffer (garbage collection).
+// Destination offsets are the exclusive scan of the group counts (group
+// order, deterministic); the copy is load-balanced over the output: each
+// CTA takes kGcTile consecutive output strings and every thread finds its
+// group by binary search among the groups overlapping the tile, so a few
+// huge groups and many tiny ones cost the same per string.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kGcWarpMax = 2048;  // k_gc: groups up to this size are copied by a warp
+constexpr uint32_t kGcTile = 4 * kCta;
+
+__device__ __forceinline__ uint32_t gc_find(const unsigned long long* off, uint32_t lo, uint32_t hi,
+                                            unsigned long long i) {
+  // last group in [lo, hi] with off <= i
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo + 1) / 2;
+    if (off[mid] <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
 
 template <int W>
-__global__ void __launch_bounds__(kCta) k_gc(GroupView<W> g, uint32_t G, ArenaView<W> src, ArenaView<W> dst,
-                                             DevStats* st) {
-  // warp per 32 consecutive groups: one bump allocation per warp batch, then
-  // the warp copies the groups one after another (coalesced per group)
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t base = warp * 32; base < G; base += nw * 32) {
-    const uint32_t gid = base + lane;
-    const uint32_t n0 = gid < G ? g.cnt[gid] : 0u;
-    const uint32_t n = n0 <= kGcWarpMax ? n0 : 0u;  // larger groups: whole CTAs, below
-    const uint64_t so = gid < G ? g.off[gid] : 0ull;
-    uint32_t inc = n;
+__global__ void __launch_bounds__(kCta) k_gc_copy(GroupView<W> g, uint32_t G, const unsigned long long* new_off,
+                                                  unsigned long long total, ArenaView<W> src, ArenaView<W> dst) {
+  __shared__ uint32_t range_s[2];
+  for (unsigned long long t0 = (unsigned long long)blockIdx.x * kGcTile; t0 < total;
+       t0 += (unsigned long long)gridDim.x * kGcTile) {
+    const unsigned long long t1 = t0 + kGcTile < total ? t0 + kGcTile : total;
+    __syncthreads();
+    if (threadIdx.x < 2) range_s[threadIdx.x] = gc_find(new_off, 0, G - 1, threadIdx.x ? t1 - 1 : t0);
+    __syncthreads();
+    const uint32_t lo = range_s[0], hi = range_s[1];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    unsigned long long d0 = 0;
-    if (lane == 31 && inc) d0 = atomicAdd(&st->bump, (unsigned long long)inc);
-    d0 = __shfl_sync(0xffffffffu, d0, 31);
-    const uint64_t d = d0 + (inc - n);
-    if (gid < G && n0 <= kGcWarpMax) {
-      g.off[gid] = n ? d : 0ull;
-      g.cap[gid] = n;
-    }
-    for (uint32_t j = 0; j < 32; ++j) {
-      const uint32_t nj = __shfl_sync(0xffffffffu, n, j);
-      if (!nj) continue;
-      const uint64_t sj = __shfl_sync(0xffffffffu, so, j);
-      const uint64_t dj = __shfl_sync(0xffffffffu, d, j);
-      for (uint32_t p = lane; p < nj; p += 32) {
+    for (uint32_t k = 0; k < kGcTile / kCta; ++k) {
+      const unsigned long long i = t0 + k * kCta + threadIdx.x;
+      if (i >= t1) break;
+      const uint32_t gid = gc_find(new_off, lo, hi, i);
+      const unsigned long long s = g.off[gid] + (i - new_off[gid]);
 #pragma unroll
-        for (int k = 0; k < W; ++k) dst.x[k][dj + p] = src.x[k][sj + p];
-        dst.c[dj + p] = src.c[sj + p];
-      }
+      for (int w = 0; w < W; ++w) dst.x[w][i] = src.x[w][s];
+      dst.c[i] = src.c[s];
     }
   }
-  // groups above kGcWarpMax strings: one CTA each
-  __shared__ unsigned long long d_s;
-  for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
-    const uint32_t n = g.cnt[gid];
-    if (n <= kGcWarpMax) continue;  // uniform per CTA
-    const uint64_t so = g.off[gid];
-    __syncthreads();
-    if (threadIdx.x == 0) d_s = atomicAdd(&st->bump, (unsigned long long)n);
-    __syncthreads();
-    const uint64_t d = d_s;
-    for (uint32_t p = threadIdx.x; p < n; p += kCta) {
-#pragma unroll
-      for (int k = 0; k < W; ++k) dst.x[k][d + p] = src.x[k][so + p];
-      dst.c[d + p] = src.c[so + p];
-    }
-    if (threadIdx.x == 0) {
-      g.off[gid] = d;
-      g.cap[gid] = n;
-    }
+}
+
+// after the copy: the table points into the new arena, capacity = count
+template <int W>
+__global__ void k_gc_finish(GroupView<W> g, uint32_t G, const unsigned long long* new_off) {
+  for (uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x; gid < G; gid += gridDim.x * blockDim.x) {
+    g.off[gid] = new_off[gid];
+    g.cap[gid] = g.cnt[gid];
   }
 }
 

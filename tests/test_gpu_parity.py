@@ -234,7 +234,12 @@ def test_fusion_matches_unfused(pp, O):
     ra, rb = a.run_circuit(circ), b.run_circuit(circ)
     wa, ca = a.export()
     wb, cb = b.export()
-    assert_same_terms(wa, ca, wb, cb, "fused vs unfused")
+    ora = O.OracleEngine(127, 0.0)
+    ora.set_initial(O.site_word(62, 3)[None], [1.0])
+    ora.run_layers([(np.asarray(g.generator.words), g.cos_theta, g.sin_theta) for g in circ.layers[0]], 4)
+    ow, oc = ora.export()
+    assert_same_terms(wa, ca, ow, oc, "fused vs oracle")
+    assert_same_terms(wb, cb, ow, oc, "unfused vs oracle")
     for x, y in zip(ra, rb):
         for k in ("term_count", "removed", "records_sent"):
             assert x[k] == y[k], (k, x, y)
@@ -267,3 +272,21 @@ def test_deferred_truncation_is_exact(pp, O, monkeypatch, mode):
     circ = pp.build_kicked_ising(geom, 0.4, -math.pi / 2 + 0.2, 3)
     init = [(O.site_word(q, 3), 1.0 / 127) for q in range(127)]
     run_both(pp, O, 127, list(circ.layers), init, 3e-4, "gate")
+
+
+@pytest.mark.parametrize("mode", ["per_gate", "dense_tight"])
+def test_sublayer_paths_match_oracle(pp, O, monkeypatch, mode):
+    """epsilon0 = 0 Rx runs: the dense sublayer (default, dense_group) and
+    the per-gate segment/stream path (PP_NO_DENSE) both equal the oracle bit
+    for bit, also when the arena overflows mid-run and resumes
+    (PP_TIGHT_ARENA: dense blocks in global memory and in shared memory)."""
+    if mode == "per_gate":
+        monkeypatch.setenv("PP_NO_DENSE", "1")
+    else:
+        monkeypatch.setenv("PP_TIGHT_ARENA", "1")
+    geom = pp.heavy_hex_127()
+    circ = _kicked(pp, geom, "0.25pi", 5)
+    run_both(pp, O, 127, list(circ.layers), [(O.site_word(62, 3), 1.0)], 0.0, "gate", check_each=True)
+    text = "\n".join(f"{i} {i + 1} {i % 2}" for i in range(63))
+    circ = pp.build_kicked_ising(pp.load_geometry(text), 0.3, "-0.5pi", 6)
+    run_both(pp, O, 64, list(circ.layers), [(O.site_word(32, 3), 1.0)], 0.0, "gate", check_each=True)
