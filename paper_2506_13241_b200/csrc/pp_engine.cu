@@ -330,10 +330,15 @@ class EngineImpl final : public EngineBase {
     keep_zeros_ = cfg.cadence == PP_CADENCE_LAYER;
     seed_ = 0x5eed5eed12345678ull;
     tight_arena_ = std::getenv("PP_TIGHT_ARENA") != nullptr;
+    no_dense_ = std::getenv("PP_NO_DENSE") != nullptr;
     update_arena_max();
   }
   ~EngineImpl() override {
     cudaStreamSynchronize(stream_);
+    if (std::getenv("PP_TRACE"))
+      std::fprintf(stderr, "[pp] trace: layers %.3f ms, %llu syncs waiting %.3f ms, launches %llu\n",
+                   tr_layer_ns_ * 1e-6, (unsigned long long)tr_syncs_, tr_sync_ns_ * 1e-6,
+                   (unsigned long long)launches_);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     release_pinned_stats(h_stats_);
@@ -451,8 +456,11 @@ class EngineImpl final : public EngineBase {
   // one layer of run_circuit: the gates, then the <0|O|0> readout; errors
   // surface at the readout's sync, inside this call
   double apply_layer(const pp_gate* gates, size_t count) override {
+    auto t0 = Clock::now();
     apply_gates_async(gates, count);
-    return expectation();
+    const double v = expectation();
+    tr_layer_ns_ += ns_since(t0);
+    return v;
   }
 
   void apply_gates_async(const pp_gate* gates, size_t count) {
@@ -494,22 +502,43 @@ class EngineImpl final : public EngineBase {
   // compacts and resumes at the failing gate, whose finished groups carry
   // its stamp and are skipped.
   void run_rx(const pp_gate* gates, size_t count) {
-    if (W == 1)
+    auto t0 = Clock::now();
+    // run_circuit passes the same gate list every layer: the host-side plan
+    // (parameters, sublayer descriptor, qubit distinctness) is cached
+    if (!(rx_key_.size() == count && std::memcmp(rx_key_.data(), gates, count * sizeof(pp_gate)) == 0)) {
+      rx_key_.clear();
+      if (W == 1)
+        for (size_t i = 0; i < count; ++i) {
+          uint64_t jx[2], jz[2];
+          words_to_planes(gates[i].words, jx, jz);
+          if (jx[1]) throw EngineError(PP_ERR_INVALID, "generator has sites beyond the engine width");
+        }
+      rx_prm_.assign(count, RxParam{});
       for (size_t i = 0; i < count; ++i) {
         uint64_t jx[2], jz[2];
         words_to_planes(gates[i].words, jx, jz);
-        if (jx[1]) throw EngineError(PP_ERR_INVALID, "generator has sites beyond the engine width");
+        rx_prm_[i].wq = jx[0] ? 0 : 1;
+        rx_prm_[i].mq = jx[0] ? jx[0] : jx[1];
+        rx_prm_[i].cosv = gates[i].cos_theta;
+        rx_prm_[i].sinv = gates[i].sin_theta;
       }
-    auto t0 = Clock::now();
-    std::vector<RxParam> prm(count);
-    for (size_t i = 0; i < count; ++i) {
-      uint64_t jx[2], jz[2];
-      words_to_planes(gates[i].words, jx, jz);
-      prm[i].wq = jx[0] ? 0 : 1;
-      prm[i].mq = jx[0] ? jx[0] : jx[1];
-      prm[i].cosv = gates[i].cos_theta;
-      prm[i].sinv = gates[i].sin_theta;
+      rx_sg_ = SubGates{};
+      rx_distinct_ = true;
+      if (count <= (size_t)kMaxSubGates) {
+        rx_sg_.ng = (int)count;
+        for (size_t i = 0; i < count; ++i) {
+          rx_sg_.wq[i] = (int8_t)rx_prm_[i].wq;
+          rx_sg_.mq[i] = rx_prm_[i].mq;
+          rx_sg_.cosv[i] = rx_prm_[i].cosv;
+          rx_sg_.sinv[i] = rx_prm_[i].sinv;
+          rx_sg_.any[rx_prm_[i].wq] |= rx_prm_[i].mq;
+          for (size_t j = 0; j < i && rx_distinct_; ++j)
+            if (rx_prm_[i].wq == rx_prm_[j].wq && rx_prm_[i].mq == rx_prm_[j].mq) rx_distinct_ = false;
+        }
+      }
+      rx_key_.assign(gates, gates + count);
     }
+    const std::vector<RxParam>& prm = rx_prm_;
     const bool budget = cfg_.max_terms != 0 && !external();
     const bool epi = !external() && !(cfg_.epsilon0 == 0.0 && !budget && !may_hold_zeros_);
     const bool do_trunc = cfg_.cadence == PP_CADENCE_GATE;
@@ -519,27 +548,10 @@ class EngineImpl final : public EngineBase {
     const bool no_budget = !budget;
     const bool independent = no_budget && (external() || !do_trunc || (cfg_.epsilon0 == 0.0 && !may_hold_zeros_));
     if (independent && count <= (size_t)kMaxSubGates && G_) {
-      SubGates sgates{};
-      sgates.ng = (int)count;
-      for (size_t i = 0; i < count; ++i) {
-        sgates.wq[i] = (int8_t)prm[i].wq;
-        sgates.mq[i] = prm[i].mq;
-        sgates.cosv[i] = prm[i].cosv;
-        sgates.sinv[i] = prm[i].sinv;
-        sgates.any[prm[i].wq] |= prm[i].mq;
-      }
+      SubGates sgates = rx_sg_;
       // dense path (k_branch_sublayer / dense_group): zeros dropped, every
       // gate of the run on its own qubit
-      {
-        bool distinct = true;
-        for (size_t i = 0; i < count && distinct; ++i)
-          for (size_t j = 0; j < i; ++j)
-            if (prm[i].wq == prm[j].wq && prm[i].mq == prm[j].mq) {
-              distinct = false;
-              break;
-            }
-        sgates.dense = distinct && !keep_zeros_ && !may_hold_zeros_ && std::getenv("PP_NO_DENSE") == nullptr;
-      }
+      sgates.dense = rx_distinct_ && !keep_zeros_ && !may_hold_zeros_ && !no_dense_;
       sync_state();
       if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
       // launched without a round trip: an arena overflow is found and
@@ -1243,8 +1255,11 @@ class EngineImpl final : public EngineBase {
     ++launches_;
   }
   void fetch_stats() {
+    auto t0 = Clock::now();
     PP_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, sizeof(DevStats), cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
+    tr_sync_ns_ += ns_since(t0);
+    ++tr_syncs_;
   }
 
   // ----- garbage collection: compact the current arena into the other one
@@ -1552,11 +1567,18 @@ class EngineImpl final : public EngineBase {
   // A run of Clifford Z_i Z_j gates (i != j, no X/Y): split into matchings,
   // then into equal-offset groups, and regroup with ZZRunProducer.
   bool try_zz_run(const pp_gate* gates, size_t count) {
+    if (zz_key_.size() == count && std::memcmp(zz_key_.data(), gates, count * sizeof(pp_gate)) == 0) {
+      if (!zz_ok_) return false;
+      regroup(zz_prod_);  // the same run as last time (run_circuit layers)
+      return true;
+    }
+    zz_key_.clear();
     std::vector<std::pair<int, int>> edges(count);
     std::vector<int> neg(count);
     for (size_t g = 0; g < count; ++g) {
       uint64_t jx[2], jz[2];
       words_to_planes(gates[g].words, jx, jz);
+      if (W == 1 && (jx[1] | jz[1])) throw EngineError(PP_ERR_INVALID, "generator has sites beyond the engine width");
       if (jx[0] | jx[1]) return false;
       int sites[3], ns = 0;
       for (int w = 0; w < 2; ++w)
@@ -1591,13 +1613,20 @@ class EngineImpl final : public EngineBase {
         if (neg[g]) e.second |= (T)1 << i;
       }
       for (auto& [d, mm] : by_d) {
-        if (p.ng >= kMaxZZGroups) return false;
+        if (p.ng >= kMaxZZGroups) {
+          zz_key_.assign(gates, gates + count);
+          zz_ok_ = false;
+          return false;
+        }
         p.grp[p.ng].m = mm.first;
         p.grp[p.ng].neg = mm.second;
         p.grp[p.ng].d = d;
         ++p.ng;
       }
     }
+    zz_key_.assign(gates, gates + count);
+    zz_prod_ = p;
+    zz_ok_ = true;
     regroup(p);
     return true;
   }
@@ -1605,30 +1634,30 @@ class EngineImpl final : public EngineBase {
   // ----- fused Clifford run
   void apply_clifford_run(const pp_gate* gates, size_t count) {
     auto t0 = Clock::now();
-    std::vector<uint64_t> gx(count * W), gz(count * W);
-    std::vector<double> gs(count);
-    for (size_t i = 0; i < count; ++i) {
-      uint64_t jx[2], jz[2];
-      words_to_planes(gates[i].words, jx, jz);
-      if (W == 1 && (jx[1] | jz[1])) throw EngineError(PP_ERR_INVALID, "generator has sites beyond the engine width");
-      for (int k = 0; k < W; ++k) {
-        gx[i * W + k] = jx[k];
-        gz[i * W + k] = jz[k];
-      }
-      gs[i] = gates[i].sin_theta;
-    }
     if (G_ && try_zz_run(gates, count)) {
       // handled by the bit-parallel ZZ producer
-    } else {
-    cliff_.ensure(count * (2 * W + 1) * 8);
-    uint64_t* dgx = cliff_.as<uint64_t>();
-    uint64_t* dgz = dgx + count * W;
-    double* dgs = reinterpret_cast<double*>(dgz + count * W);
-    PP_CUDA(cudaMemcpyAsync(dgx, gx.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(dgz, gz.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(dgs, gs.data(), count * 8, cudaMemcpyHostToDevice, stream_));
-    CliffordProducer<W> p{dgx, dgz, dgs, (int)count};
-    if (G_) regroup(p);
+    } else if (G_) {
+      std::vector<uint64_t> gx(count * W), gz(count * W);
+      std::vector<double> gs(count);
+      for (size_t i = 0; i < count; ++i) {
+        uint64_t jx[2], jz[2];
+        words_to_planes(gates[i].words, jx, jz);
+        if (W == 1 && (jx[1] | jz[1])) throw EngineError(PP_ERR_INVALID, "generator has sites beyond the engine width");
+        for (int k = 0; k < W; ++k) {
+          gx[i * W + k] = jx[k];
+          gz[i * W + k] = jz[k];
+        }
+        gs[i] = gates[i].sin_theta;
+      }
+      cliff_.ensure(count * (2 * W + 1) * 8);
+      uint64_t* dgx = cliff_.as<uint64_t>();
+      uint64_t* dgz = dgx + count * W;
+      double* dgs = reinterpret_cast<double*>(dgz + count * W);
+      PP_CUDA(cudaMemcpyAsync(dgx, gx.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemcpyAsync(dgz, gz.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(cudaMemcpyAsync(dgs, gs.data(), count * 8, cudaMemcpyHostToDevice, stream_));
+      CliffordProducer<W> p{dgx, dgz, dgs, (int)count};
+      regroup(p);
     }
     // Clifford gates zero each moved parent and re-insert it at I xor J;
     // absent a partner pair the reference removes one zero per record.
@@ -1834,6 +1863,15 @@ class EngineImpl final : public EngineBase {
   uint64_t bump_bound_ = 0, live_bound_ = 0;
   bool dirty_ = false, truncated_since_sync_ = false, gmax_stale_ = false, may_hold_zeros_ = false;
   uint64_t eseq_ = 0, bseq_ = 0;
+  uint64_t tr_layer_ns_ = 0, tr_sync_ns_ = 0, tr_syncs_ = 0;  // PP_TRACE host timeline
+  std::vector<pp_gate> rx_key_;  // run_rx plan cache
+  std::vector<RxParam> rx_prm_;
+  SubGates rx_sg_{};
+  bool rx_distinct_ = true;
+  bool no_dense_ = false;
+  std::vector<pp_gate> zz_key_;  // try_zz_run plan cache
+  ZZRunProducer<W> zz_prod_{};
+  bool zz_ok_ = false;
   bool arena_fault_ = false;
   bool sub_pending_ = false;  // a sublayer launch not yet checked for an arena overflow
   SubGates sub_gates_{};

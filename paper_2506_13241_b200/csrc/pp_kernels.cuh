@@ -1465,7 +1465,17 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       __syncthreads();
       for (uint32_t sp = 0; sp < (S >> u); ++sp) {
         const uint32_t base = dense_dep32(sp, Q);
-        for (uint32_t i = tid; i < (1u << u); i += kCta) dbuf[i] = blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]];
+        // 8 loads in flight per thread (the block sits in L2)
+        for (uint32_t i0 = 0; i0 < (1u << u); i0 += 8 * kCta) {
+          double t[8];
+#pragma unroll
+          for (uint32_t e = 0; e < 8; ++e) {
+            const uint32_t i = i0 + e * kCta + tid;
+            t[e] = blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]];
+          }
+#pragma unroll
+          for (uint32_t e = 0; e < 8; ++e) dbuf[i0 + e * kCta + tid] = t[e];
+        }
         __syncthreads();
         dense_stages<W>(dbuf, u, P, j0, j1, dc, gates, records, removed);
         for (uint32_t i = tid; i < (1u << u); i += kCta) blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]] = dbuf[i];
@@ -1476,11 +1486,12 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   // nonzero points in b (= x) order, compacted into the output region (in
   // place for a block in global memory: a tile's writes land at or below its
   // own positions, after all of its reads)
-  constexpr uint32_t kPer = 4;
+  constexpr uint32_t kPer = 8;  // 8 loads in flight per thread per tile
   double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll), vall = 0.0;
   uint32_t nonfinite = 0;
   uint32_t out = 0;
   const uint32_t lane = tid & 31, warp = tid >> 5;
+  uint32_t* ocnt = reinterpret_cast<uint32_t*>(dc.deplo);  // kPer x kWarps counts (+ total); passes are done
   for (uint32_t base = 0; base < S; base += kCta * kPer) {
     double v[kPer];
     uint32_t bal[kPer];
@@ -1488,22 +1499,27 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     for (uint32_t e = 0; e < kPer; ++e) {  // striped: slot e covers [base + e kCta, base + (e+1) kCta)
       const uint32_t b = base + e * kCta + tid;
       v[e] = b < S ? blk[b] : 0.0;
+    }
+#pragma unroll
+    for (uint32_t e = 0; e < kPer; ++e) {
       bal[e] = __ballot_sync(0xffffffffu, v[e] != 0.0);
-      if (lane == 0) scan[e * kWarps + warp] = __popc(bal[e]);
+      if (lane == 0) ocnt[e * kWarps + warp] = __popc(bal[e]);
     }
     __syncthreads();
-    if (warp == 0) {  // exclusive scan of the kPer x kWarps counts, in b order
-      const uint32_t c = lane < kPer * kWarps ? scan[lane] : 0u;
-      const uint32_t inc = warp_incl_scan(c);
-      if (lane < kPer * kWarps) scan[lane] = inc - c;
-      if (lane == kPer * kWarps - 1) scan[kPer * kWarps] = inc;
+    if (warp == 0) {  // exclusive scan of the kPer x kWarps counts (b order), 2 per lane
+      static_assert(kPer * kWarps == 64, "two counts per lane");
+      const uint32_t c0 = ocnt[2 * lane], c1 = ocnt[2 * lane + 1];
+      const uint32_t inc = warp_incl_scan(c0 + c1);
+      ocnt[2 * lane] = inc - c0 - c1;
+      ocnt[2 * lane + 1] = inc - c1;
+      if (lane == 31) ocnt[64] = inc;
     }
     __syncthreads();
 #pragma unroll
     for (uint32_t e = 0; e < kPer; ++e) {
       if (v[e] == 0.0) continue;
       const uint32_t b = base + e * kCta + tid;
-      const uint32_t o = out + scan[e * kWarps + warp] + __popc(bal[e] & ((1u << lane) - 1u));
+      const uint32_t o = out + ocnt[e * kWarps + warp] + __popc(bal[e] & ((1u << lane) - 1u));
       Plane<W> x = F;
       const Plane<W> a0 = xt[b & 255u], a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
 #pragma unroll
@@ -1515,7 +1531,7 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       vmax = fmax(vmax, av);
       vmin = fmin(vmin, av);
     }
-    out += scan[kPer * kWarps];
+    out += ocnt[kPer * kWarps];
     __syncthreads();
   }
   reduce_group_stats(gs, vmax, vmin, vall, nonfinite, records, removed);
@@ -1786,6 +1802,7 @@ template <int W>
 constexpr size_t branch_smem_bytes() {
   return sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
 }
+static_assert(kDenseSmem % (8 * kCta) == 0, "dense tile gathers in steps of 8 kCta");
 static_assert(branch_smem_bytes<1>() >= kDenseSmem * sizeof(double) + 3 * 256 * 8, "dense tile must fit the branch buffer");
 static_assert(branch_smem_bytes<2>() >= kDenseSmem * sizeof(double) + 3 * 256 * 16, "dense tile must fit the branch buffer");
 
