@@ -1252,6 +1252,9 @@ __device__ __forceinline__ void reduce_group_stats(GroupStatsSmem& r, double& vm
 constexpr uint32_t kDenseSmemLog = 13;
 constexpr uint32_t kDenseSmem = 1u << kDenseSmemLog;  // doubles of the dynamic buffer
 constexpr int kDenseMaxLog = 24;                      // larger blocks take the per-gate path
+constexpr uint32_t kDenseMaxK = 64;                   // x classes per group on the dense path
+constexpr uint32_t kDenseMaxIn = 32 * kCta;           // input strings per group (one match bit each per thread)
+constexpr uint32_t kDenseMaxOut = 1u << 26;           // K 2^m points per group
 
 template <int W>
 struct DenseCtl {
@@ -1267,6 +1270,8 @@ struct DenseCtl {
   uint8_t tpos[32];             // b bit j -> x bit position (ascending)
   unsigned long long dst;
   uint32_t fail;
+  uint32_t next;                // class discovery: first unmatched string
+  uint32_t zeros;               // multi-class: zero points written (holes to compact)
 };
 
 template <int W>
@@ -1319,9 +1324,10 @@ __device__ __forceinline__ void dense_bfly(double& a, double& b, double cosv, do
 // P: the b bits of the tile (stage bit p is tile bit popc(P & (2^p - 1)))
 template <int W>
 __device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, int j0, int j1, const DenseCtl<W>& dc,
-                                             const SubGates& gates, unsigned long long& records,
-                                             unsigned long long& removed) {
-  const uint32_t half = (1u << u) >> 1;
+                                             unsigned long long& records, unsigned long long& removed,
+                                             uint32_t count = 0) {
+  // count: points in the tile (a multiple of 2^(p+1) for every stage), default 2^u
+  const uint32_t half = (count ? count : (1u << u)) >> 1;
   for (int j = j0; j < j1; ++j) {
     const uint32_t p = __popc(P & ((1u << dc.sbit[j]) - 1u));
     const double cosv = dc.scos[j], sinv = dc.ssin[j], nsin = -sinv;
@@ -1332,6 +1338,239 @@ __device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, 
     }
     __syncthreads();
   }
+}
+
+
+// Stages of a block of S > kDenseSmem points in global memory (L2): passes
+// of up to kDenseSmemLog stages, each over full shared-memory tiles (the
+// cosets of the pass's stage bits, padded with low bits).
+template <int W>
+__device__ void dense_passes(double* dbuf, double* blk, uint32_t S, DenseCtl<W>& dc, unsigned long long& records,
+                             unsigned long long& removed) {
+  const uint32_t tid = threadIdx.x;
+  const int m = dc.m;
+  for (int j0 = 0; j0 < m; j0 += (int)kDenseSmemLog) {
+    const int j1 = min(m, j0 + (int)kDenseSmemLog);
+    if (tid == 0) {
+      // tile bits: this pass's stage bits, padded with the lowest other
+      // bits to a full tile (coalesced gathers, several cosets per tile)
+      uint32_t P = 0;
+      for (int j = j0; j < j1; ++j) P |= 1u << dc.sbit[j];
+      for (uint32_t b = 0; __popc(P) < (int)kDenseSmemLog; ++b) P |= 1u << b;
+      dc.P = P;
+    }
+    __syncthreads();
+    const uint32_t P = dc.P, u = kDenseSmemLog, Q = (S - 1u) & ~P;
+    {  // deposit tables: tile index bits 0-6 and 7-12 into P
+      uint32_t plo = P;
+      for (int c = 0; c < 7; ++c) plo &= plo - 1;
+      const uint32_t lo_mask = P & ~plo;
+      if (tid < 128) dc.deplo[tid] = dense_dep32(tid, lo_mask);
+      else if (tid < 192) dc.dephi[tid - 128] = dense_dep32(tid - 128, plo);
+    }
+    __syncthreads();
+    for (uint32_t sp = 0; sp < (S >> u); ++sp) {
+      const uint32_t base = dense_dep32(sp, Q);
+      // 8 loads in flight per thread (the block sits in L2)
+      for (uint32_t i0 = 0; i0 < (1u << u); i0 += 8 * kCta) {
+        double t[8];
+#pragma unroll
+        for (uint32_t e = 0; e < 8; ++e) {
+          const uint32_t i = i0 + e * kCta + tid;
+          t[e] = blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]];
+        }
+#pragma unroll
+        for (uint32_t e = 0; e < 8; ++e) dbuf[i0 + e * kCta + tid] = t[e];
+      }
+      __syncthreads();
+      dense_stages<W>(dbuf, u, P, j0, j1, dc, records, removed);
+      for (uint32_t i = tid; i < (1u << u); i += kCta) blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]] = dbuf[i];
+      __syncthreads();
+    }
+  }
+}
+
+// Several x classes F_1 < ... < F_K (sorted as planes): one 2^m block each.
+// The group's x order interleaves the blocks; point b of class i goes to
+//   rank(i, b) = b + sum_{j != i} (((b >> t_ij) + [j < i]) << t_ij),
+// t_ij = number of T bits below the highest bit where F_i and F_j differ
+// (above it both agree outside T, so order is decided by the T bits above
+// it, i.e. b >> t_ij, then by F at that bit).  Points are written at their
+// ranks (zeros included), then holes are compacted out in place.
+template <int W>
+__device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, uint32_t* scan, GroupView<W> g,
+                           ArenaView<W> ar, uint32_t gid, uint32_t n, uint64_t src, uint32_t K, uint32_t seq0,
+                           unsigned long long cap, DevStats* st, unsigned long long& aff_elems) {
+  const uint32_t tid = threadIdx.x;
+  const int m = dc.m;
+  const Plane<W> T = dc.T;
+  unsigned char* tail = reinterpret_cast<unsigned char*>(dbuf) + kDenseSmem * sizeof(double);
+  const Plane<W>* xt = reinterpret_cast<const Plane<W>*>(tail);
+  uint8_t* tij = tail + 3 * 256 * sizeof(Plane<W>);
+  Plane<W>* cF = reinterpret_cast<Plane<W>*>(tij + kDenseMaxK * kDenseMaxK);
+  Plane<W>* sF = cF + kDenseMaxK;
+  const uint32_t S = 1u << m;
+  const unsigned long long KS = (unsigned long long)K * S;
+  if (KS > kDenseMaxOut) return 0;
+  // classes in ascending order
+  if (tid < K) {
+    const Plane<W> f = cF[tid];
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < K; ++j) r += plane_lt<W>(cF[j], f);
+    sF[r] = f;
+  }
+  __syncthreads();
+  for (uint32_t p = tid; p < K * K; p += kCta) {
+    const uint32_t i = p / K, j = p % K;
+    uint32_t t = 0xff;
+    if (i != j) {
+      int hw = W - 1;
+      while (hw > 0 && sF[i].w[hw] == sF[j].w[hw]) --hw;
+      const uint64_t d = sF[i].w[hw] ^ sF[j].w[hw];
+      const int h = 63 - __clzll((long long)d);
+      t = __popcll(T.w[hw] & ((1ull << h) - 1ull));
+      for (int w = 0; w < hw; ++w) t += __popcll(T.w[w]);
+    }
+    tij[p] = (uint8_t)t;
+  }
+  // region: K 2^m output slots, plus a 2^m scratch block for blocks larger
+  // than a shared-memory tile
+  const bool big = S > kDenseSmem;
+  const unsigned long long need = KS + (big ? S : 0);
+  if (tid == 0) {
+    const unsigned long long d = atomicAdd(&st->bump, need);
+    dc.dst = d;
+    dc.fail = d + need > cap;
+    if (dc.fail) {
+      atomicOr(&st->err_arena, 1u);
+      atomicMin(&st->err_seq, (unsigned long long)(seq0 + dc.sgate[0]));
+    }
+    dc.zeros = 0;
+  }
+  __syncthreads();
+  if (dc.fail) return -1;
+  const uint64_t dst = dc.dst;
+  unsigned long long records = 0, removed = 0;
+  double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll), vall = 0.0;
+  uint32_t nonfinite = 0, zeros = 0;
+  // class of string i: binary search over the sorted classes
+  auto class_of = [&](const Plane<W>& x) -> uint32_t {
+    Plane<W> f = x;
+#pragma unroll
+    for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+    uint32_t lo = 0, hi = K;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (plane_lt<W>(f, sF[mid])) hi = mid;
+      else lo = mid;
+    }
+    return lo;
+  };
+  // point (i, b) -> its rank and x; value written there
+  auto emit = [&](uint32_t i, uint32_t b, double v) {
+    uint32_t r = b;
+    const uint8_t* ti = tij + i * K;
+    for (uint32_t j = 0; j < K; ++j) {
+      const uint32_t t = ti[j];
+      if (t == 0xff) continue;
+      r += ((b >> t) + (j < i ? 1u : 0u)) << t;
+    }
+    Plane<W> x = sF[i];
+    const Plane<W> a0 = xt[b & 255u], a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
+#pragma unroll
+    for (int w = 0; w < W; ++w) x.w[w] |= a0.w[w] | a1.w[w] | a2.w[w];
+    store_plane<W>(ar.x, dst + r, x);
+    ar.c[dst + r] = v;
+    if (v == 0.0) {
+      ++zeros;
+    } else {
+      const double av = fabs(v);
+      if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
+      vmax = fmax(vmax, av);
+      vmin = fmin(vmin, av);
+    }
+  };
+  if (!big) {
+    // batches of whole class blocks in one shared-memory tile
+    const uint32_t per = kDenseSmem / S;
+    for (uint32_t c0 = 0; c0 < K; c0 += per) {
+      const uint32_t c1 = min(K, c0 + per), cnt = (c1 - c0) * S;
+      for (uint32_t e = tid; e < cnt; e += kCta) dbuf[e] = 0.0;
+      __syncthreads();
+      for (uint32_t i = tid; i < n; i += kCta) {
+        const Plane<W> x = load_plane<W>(ar.x, src + i);
+        const uint32_t c = class_of(x);
+        if (c >= c0 && c < c1) dbuf[(c - c0) * S + dense_pext<W>(x, T)] = ar.c[src + i];
+      }
+      __syncthreads();
+      dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed, cnt);
+      for (uint32_t e = tid; e < cnt; e += kCta) emit(c0 + e / S, e % S, dbuf[e]);
+      __syncthreads();
+    }
+  } else {
+    double* blk = ar.c + dst + KS;  // scratch block (coefficient plane past the output)
+    for (uint32_t ci = 0; ci < K; ++ci) {
+      for (uint32_t e = tid; e < S; e += kCta) blk[e] = 0.0;
+      __syncthreads();
+      for (uint32_t i = tid; i < n; i += kCta) {
+        const Plane<W> x = load_plane<W>(ar.x, src + i);
+        if (class_of(x) == ci) blk[dense_pext<W>(x, T)] = ar.c[src + i];
+      }
+      __syncthreads();
+      dense_passes<W>(dbuf, blk, S, dc, records, removed);
+      for (uint32_t e = tid; e < S; e += kCta) emit(ci, e, blk[e]);
+      __syncthreads();
+    }
+  }
+  // holes (zero points): compact [dst, dst + KS) in place, in rank order
+  if (zeros) atomicAdd(&dc.zeros, zeros);
+  __syncthreads();
+  uint32_t out = (uint32_t)KS;
+  if (dc.zeros) {
+    out = 0;
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    for (unsigned long long base = 0; base < KS; base += kCta) {
+      const unsigned long long r = base + tid;
+      double v = 0.0;
+      Plane<W> x;
+      if (r < KS) {
+        v = ar.c[dst + r];
+        x = load_plane<W>(ar.x, dst + r);
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, v != 0.0);
+      if (lane == 0) scan[warp] = __popc(bal);
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t c = lane < kWarps ? scan[lane] : 0u;
+        const uint32_t inc = warp_incl_scan(c);
+        if (lane < kWarps) scan[lane] = inc - c;
+        if (lane == kWarps - 1) scan[kWarps] = inc;
+      }
+      __syncthreads();
+      if (v != 0.0) {
+        const uint32_t o = out + scan[warp] + __popc(bal & ((1u << lane) - 1u));
+        store_plane<W>(ar.x, dst + o, x);
+        ar.c[dst + o] = v;
+      }
+      out += scan[kWarps];
+      __syncthreads();
+    }
+  }
+  reduce_group_stats(gs, vmax, vmin, vall, nonfinite, records, removed);
+  if (tid == 0) {
+    g.off[gid] = dst;
+    g.cnt[gid] = out;
+    g.cap[gid] = (uint32_t)KS;
+    g.gmax[gid] = out ? vmax : 0.0;
+    g.gmin[gid] = out ? vmin : __longlong_as_double(0x7ff0000000000000ll);
+    g.flags[gid] = nonfinite;
+    g.stamp[gid] = seq0 + (uint32_t)dc.klast;
+    if (records) atomicAdd(&st->records, records);
+    if (removed) atomicAdd(&st->removed, removed);
+    atomicAdd(&st->out_elems, (unsigned long long)out);
+  }
+  aff_elems += n;
+  return 1;
 }
 
 // Returns 1 when the group was applied, 0 when it is not eligible (the
@@ -1398,14 +1637,60 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   const int m = dc.m;
   if (m == 0 || m > kDenseMaxLog) return 0;
   const Plane<W> T = dc.T, F = dc.F;
-  // one class: every string agrees with the first outside T
-  bool one = true;
-  for (uint32_t i = tid; i < n; i += kCta) {
-    const Plane<W> x = load_plane<W>(ar.x, src + i);
+  // x classes (the distinct x parts outside T), one round per class: every
+  // string compares with the first string no earlier class matched
+  if (n > kDenseMaxIn) return 0;
+  Plane<W>* cF = reinterpret_cast<Plane<W>*>(reinterpret_cast<unsigned char*>(dbuf) + kDenseSmem * sizeof(double) +
+                                             3 * 256 * sizeof(Plane<W>) + kDenseMaxK * kDenseMaxK);
+  uint32_t K = 0;
+  {
+    uint32_t matched = 0, cand = 0;
+    for (;;) {
+      if (tid == 0) {
+        Plane<W> x = load_plane<W>(ar.x, src + cand);
 #pragma unroll
-    for (int k = 0; k < W; ++k) one &= (x.w[k] & ~T.w[k]) == F.w[k];
+        for (int k = 0; k < W; ++k) x.w[k] &= ~T.w[k];
+        cF[K] = x;
+        dc.next = kNone;
+      }
+      __syncthreads();
+      const Plane<W> Fc = cF[K];
+      uint32_t first = kNone;
+      for (uint32_t k = 0, i = tid; i < n; ++k, i += kCta) {
+        if ((matched >> k) & 1u) continue;
+        const Plane<W> x = load_plane<W>(ar.x, src + i);
+        bool eq = true;
+#pragma unroll
+        for (int w = 0; w < W; ++w) eq &= (x.w[w] & ~T.w[w]) == Fc.w[w];
+        if (eq) matched |= 1u << k;
+        else if (first == kNone) first = i;
+      }
+      ++K;
+      if (first != kNone) atomicMin(&dc.next, first);
+      __syncthreads();
+      const uint32_t nx = dc.next;
+      __syncthreads();  // everyone read dc.next before the next round resets it
+      if (nx == kNone) break;
+      if (K == kDenseMaxK) return 0;
+      cand = nx;
+    }
   }
-  if (!__syncthreads_and(one)) return 0;
+  // b -> x bits outside F, one table per byte of b (behind the dense tile)
+  Plane<W>* xt = reinterpret_cast<Plane<W>*>(dbuf + kDenseSmem);
+  for (uint32_t e = tid; e < 3 * 256; e += kCta) {
+    Plane<W> p;
+#pragma unroll
+    for (int w = 0; w < W; ++w) p.w[w] = 0;
+    const uint32_t j0 = 8 * (e >> 8);
+    for (uint32_t bit = 0; bit < 8; ++bit)
+      if (j0 + bit < (uint32_t)m && ((e >> bit) & 1u)) {
+        const uint32_t q = dc.tpos[j0 + bit];
+        p.w[q >> 6] |= 1ull << (q & 63);
+      }
+    xt[e] = p;
+  }
+  __syncthreads();
+  if (K > 1) return dense_multi<W>(dbuf, dc, gs, scan, g, ar, gid, n, src, K, seq0, cap, st, aff_elems);
   const uint32_t S = 1u << m;
   if (tid == 0) {
     const unsigned long long d = atomicAdd(&st->bump, (unsigned long long)S);
@@ -1421,67 +1706,15 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   const uint64_t dst = dc.dst;
   const bool in_smem = S <= kDenseSmem;
   double* blk = in_smem ? dbuf : ar.c + dst;  // the dense block
-  // b -> x bits outside F, one table per byte of b (behind the dense tile)
-  Plane<W>* xt = reinterpret_cast<Plane<W>*>(dbuf + kDenseSmem);
-  for (uint32_t e = tid; e < 3 * 256; e += kCta) {
-    Plane<W> p;
-#pragma unroll
-    for (int w = 0; w < W; ++w) p.w[w] = 0;
-    const uint32_t j0 = 8 * (e >> 8);
-    for (uint32_t bit = 0; bit < 8; ++bit)
-      if (j0 + bit < (uint32_t)m && ((e >> bit) & 1u)) {
-        const uint32_t q = dc.tpos[j0 + bit];
-        p.w[q >> 6] |= 1ull << (q & 63);
-      }
-    xt[e] = p;
-  }
   unsigned long long records = 0, removed = 0;
   for (uint32_t i = tid; i < S; i += kCta) blk[i] = 0.0;
   __syncthreads();
   for (uint32_t i = tid; i < n; i += kCta) blk[dense_pext<W>(load_plane<W>(ar.x, src + i), T)] = ar.c[src + i];
   __syncthreads();
   if (in_smem) {
-    dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, gates, records, removed);
+    dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed);
   } else {
-    for (int j0 = 0; j0 < m; j0 += (int)kDenseSmemLog) {
-      const int j1 = min(m, j0 + (int)kDenseSmemLog);
-      if (tid == 0) {
-        // tile bits: this pass's stage bits, padded with the lowest other
-        // bits to a full tile (coalesced gathers, several cosets per tile)
-        uint32_t P = 0;
-        for (int j = j0; j < j1; ++j) P |= 1u << dc.sbit[j];
-        for (uint32_t b = 0; __popc(P) < (int)kDenseSmemLog; ++b) P |= 1u << b;
-        dc.P = P;
-      }
-      __syncthreads();
-      const uint32_t P = dc.P, u = kDenseSmemLog, Q = (S - 1u) & ~P;
-      {  // deposit tables: tile index bits 0-6 and 7-12 into P
-        uint32_t plo = P;
-        for (int c = 0; c < 7; ++c) plo &= plo - 1;
-        const uint32_t lo_mask = P & ~plo;
-        if (tid < 128) dc.deplo[tid] = dense_dep32(tid, lo_mask);
-        else if (tid < 192) dc.dephi[tid - 128] = dense_dep32(tid - 128, plo);
-      }
-      __syncthreads();
-      for (uint32_t sp = 0; sp < (S >> u); ++sp) {
-        const uint32_t base = dense_dep32(sp, Q);
-        // 8 loads in flight per thread (the block sits in L2)
-        for (uint32_t i0 = 0; i0 < (1u << u); i0 += 8 * kCta) {
-          double t[8];
-#pragma unroll
-          for (uint32_t e = 0; e < 8; ++e) {
-            const uint32_t i = i0 + e * kCta + tid;
-            t[e] = blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]];
-          }
-#pragma unroll
-          for (uint32_t e = 0; e < 8; ++e) dbuf[i0 + e * kCta + tid] = t[e];
-        }
-        __syncthreads();
-        dense_stages<W>(dbuf, u, P, j0, j1, dc, gates, records, removed);
-        for (uint32_t i = tid; i < (1u << u); i += kCta) blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]] = dbuf[i];
-        __syncthreads();
-      }
-    }
+    dense_passes<W>(dbuf, blk, S, dc, records, removed);
   }
   // nonzero points in b (= x) order, compacted into the output region (in
   // place for a block in global memory: a tile's writes land at or below its
