@@ -55,6 +55,8 @@ __global__ void k_clear_cumulative(DevStats* st) {
   st->out_elems = 0;
   st->aff_total = 0;
   st->stream_elems = 0;
+  st->dense_groups = 0;
+  st->dense_out = 0;
 }
 
 __global__ void k_reset_stats(DevStats* st, unsigned long long bump) {
@@ -1176,6 +1178,9 @@ class EngineImpl final : public EngineBase {
     *ms = branch_ms_;
     *bytes = branch_bytes_;
     last_stream_frac_ = branch_in_ ? (double)branch_stream_ / (double)branch_in_ : 0.0;
+    if (std::getenv("PP_DEBUG"))
+      std::fprintf(stderr, "[pp] dense sublayer: %llu groups, %llu strings written\n",
+                   (unsigned long long)dense_groups_, (unsigned long long)dense_out_);
     if (std::getenv("PP_DEBUG")) std::fprintf(stderr, "[pp] branch strings %llu, via long-block stream path %.3f\n",
                                               (unsigned long long)branch_in_, last_stream_frac_);
     branch_in_ = branch_stream_ = 0;
@@ -1420,6 +1425,8 @@ class EngineImpl final : public EngineBase {
     branch_bytes_ += (double)(st.aff_total + st.out_elems) * R;
     branch_in_ += st.aff_total;
     branch_stream_ += st.stream_elems;
+    dense_groups_ += st.dense_groups;
+    dense_out_ += st.dense_out;
     k_clear_cumulative<<<1, 1, 0, stream_>>>(d_stats_);
     ++launches_;
     dirty_ = false;
@@ -1864,6 +1871,7 @@ class EngineImpl final : public EngineBase {
   bool dirty_ = false, truncated_since_sync_ = false, gmax_stale_ = false, may_hold_zeros_ = false;
   uint64_t eseq_ = 0, bseq_ = 0;
   uint64_t tr_layer_ns_ = 0, tr_sync_ns_ = 0, tr_syncs_ = 0;  // PP_TRACE host timeline
+  uint64_t dense_groups_ = 0, dense_out_ = 0;
   std::vector<pp_gate> rx_key_;  // run_rx plan cache
   std::vector<RxParam> rx_prm_;
   SubGates rx_sg_{};

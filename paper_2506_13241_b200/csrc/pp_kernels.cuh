@@ -107,6 +107,8 @@ struct DevStats {
   unsigned int zz_maxcnt;          // Z-type gate: largest group written
   unsigned int zz_err;             // Z-type gate: a pair exceeded the segment (host pre-check failed)
   unsigned int zz_pad;
+  unsigned long long dense_groups;  // groups applied by the dense sublayer path (cumulative)
+  unsigned long long dense_out;     // strings those groups wrote
 };
 
 // Scalars a launch run reads from device memory, so that a captured CUDA
@@ -1256,6 +1258,21 @@ constexpr uint32_t kDenseMaxK = 64;                   // x classes per group on 
 constexpr uint32_t kDenseMaxIn = 32 * kCta;           // input strings per group (one match bit each per thread)
 constexpr uint32_t kDenseMaxOut = 1u << 26;           // K 2^m points per group
 
+// Behind the dense tile in the dynamic buffer: output tables and the x-class
+// bookkeeping of the group being processed.
+constexpr uint32_t kDenseSlots = 2 * kDenseMaxK;  // class hash set (load <= 1/2)
+template <int W>
+struct DenseTail {
+  Plane<W> xt[3 * 256];                 // b byte k -> x bits (T positions)
+  unsigned long long hfp[kDenseSlots];  // class hash set: fingerprint (0 = empty)
+  Plane<W> hF[kDenseSlots];             //   its class F
+  uint8_t hcls[kDenseSlots];            //   its class index (ascending F)
+  Plane<W> sF[kDenseMaxK];              // classes in ascending order
+  uint8_t lvl[kDenseMaxK][kDenseMaxLog + 1];  // rank terms: #classes j with t_ij = t
+  uint32_t lmask[kDenseMaxK];           //   levels t present
+  uint32_t C[kDenseMaxK];               //   sum over j < i of 2^t_ij
+};
+
 template <int W>
 struct DenseCtl {
   Plane<W> T;                   // touched x bits
@@ -1404,35 +1421,32 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   const uint32_t tid = threadIdx.x;
   const int m = dc.m;
   const Plane<W> T = dc.T;
-  unsigned char* tail = reinterpret_cast<unsigned char*>(dbuf) + kDenseSmem * sizeof(double);
-  const Plane<W>* xt = reinterpret_cast<const Plane<W>*>(tail);
-  uint8_t* tij = tail + 3 * 256 * sizeof(Plane<W>);
-  Plane<W>* cF = reinterpret_cast<Plane<W>*>(tij + kDenseMaxK * kDenseMaxK);
-  Plane<W>* sF = cF + kDenseMaxK;
+  DenseTail<W>& tl = *reinterpret_cast<DenseTail<W>*>(dbuf + kDenseSmem);
+  const Plane<W>* xt = tl.xt;
   const uint32_t S = 1u << m;
   const unsigned long long KS = (unsigned long long)K * S;
   if (KS > kDenseMaxOut) return 0;
-  // classes in ascending order
+  // rank terms of class i: lvl[i][t] = #{j != i : t_ij = t}, C_i = sum_{j<i} 2^t_ij
   if (tid < K) {
-    const Plane<W> f = cF[tid];
-    uint32_t r = 0;
-    for (uint32_t j = 0; j < K; ++j) r += plane_lt<W>(cF[j], f);
-    sF[r] = f;
+    for (int t = 0; t <= m; ++t) tl.lvl[tid][t] = 0;
+    uint32_t mask = 0, c = 0;
+    const Plane<W> fi = tl.sF[tid];
+    for (uint32_t j = 0; j < K; ++j) {
+      if (j == tid) continue;
+      int hw = W - 1;
+      while (hw > 0 && fi.w[hw] == tl.sF[j].w[hw]) --hw;
+      const uint64_t d = fi.w[hw] ^ tl.sF[j].w[hw];
+      const int h = 63 - __clzll((long long)d);
+      uint32_t t = __popcll(T.w[hw] & ((1ull << h) - 1ull));
+      for (int w = 0; w < hw; ++w) t += __popcll(T.w[w]);
+      tl.lvl[tid][t] += 1;
+      mask |= 1u << t;
+      if (j < tid) c += 1u << t;
+    }
+    tl.lmask[tid] = mask;
+    tl.C[tid] = c;
   }
   __syncthreads();
-  for (uint32_t p = tid; p < K * K; p += kCta) {
-    const uint32_t i = p / K, j = p % K;
-    uint32_t t = 0xff;
-    if (i != j) {
-      int hw = W - 1;
-      while (hw > 0 && sF[i].w[hw] == sF[j].w[hw]) --hw;
-      const uint64_t d = sF[i].w[hw] ^ sF[j].w[hw];
-      const int h = 63 - __clzll((long long)d);
-      t = __popcll(T.w[hw] & ((1ull << h) - 1ull));
-      for (int w = 0; w < hw; ++w) t += __popcll(T.w[w]);
-    }
-    tij[p] = (uint8_t)t;
-  }
   // region: K 2^m output slots, plus a 2^m scratch block for blocks larger
   // than a shared-memory tile
   const bool big = S > kDenseSmem;
@@ -1453,29 +1467,24 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   unsigned long long records = 0, removed = 0;
   double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll), vall = 0.0;
   uint32_t nonfinite = 0, zeros = 0;
-  // class of string i: binary search over the sorted classes
+  // class of a string: its slot in the class hash set
   auto class_of = [&](const Plane<W>& x) -> uint32_t {
     Plane<W> f = x;
 #pragma unroll
     for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
-    uint32_t lo = 0, hi = K;
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (plane_lt<W>(f, sF[mid])) hi = mid;
-      else lo = mid;
-    }
-    return lo;
+    const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+    uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+    while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
+    return tl.hcls[h];
   };
   // point (i, b) -> its rank and x; value written there
   auto emit = [&](uint32_t i, uint32_t b, double v) {
-    uint32_t r = b;
-    const uint8_t* ti = tij + i * K;
-    for (uint32_t j = 0; j < K; ++j) {
-      const uint32_t t = ti[j];
-      if (t == 0xff) continue;
-      r += ((b >> t) + (j < i ? 1u : 0u)) << t;
+    uint32_t r = b + tl.C[i];
+    for (uint32_t mk = tl.lmask[i]; mk; mk &= mk - 1) {
+      const uint32_t t = __ffs(mk) - 1;
+      r += (uint32_t)tl.lvl[i][t] * ((b >> t) << t);
     }
-    Plane<W> x = sF[i];
+    Plane<W> x = tl.sF[i];
     const Plane<W> a0 = xt[b & 255u], a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
 #pragma unroll
     for (int w = 0; w < W; ++w) x.w[w] |= a0.w[w] | a1.w[w] | a2.w[w];
@@ -1568,6 +1577,8 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     if (records) atomicAdd(&st->records, records);
     if (removed) atomicAdd(&st->removed, removed);
     atomicAdd(&st->out_elems, (unsigned long long)out);
+    atomicAdd(&st->dense_groups, 1ull);
+    atomicAdd(&st->dense_out, (unsigned long long)out);
   }
   aff_elems += n;
   return 1;
@@ -1636,47 +1647,63 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   __syncthreads();
   const int m = dc.m;
   if (m == 0 || m > kDenseMaxLog) return 0;
-  const Plane<W> T = dc.T, F = dc.F;
-  // x classes (the distinct x parts outside T), one round per class: every
-  // string compares with the first string no earlier class matched
+  const Plane<W> T = dc.T;
+  // x classes (the distinct x parts F outside T): a shared-memory hash set
+  // keyed by a fingerprint of F, verified against the stored F afterwards
+  // (a fingerprint collision sends the group to the per-gate path)
   if (n > kDenseMaxIn) return 0;
-  Plane<W>* cF = reinterpret_cast<Plane<W>*>(reinterpret_cast<unsigned char*>(dbuf) + kDenseSmem * sizeof(double) +
-                                             3 * 256 * sizeof(Plane<W>) + kDenseMaxK * kDenseMaxK);
-  uint32_t K = 0;
-  {
-    uint32_t matched = 0, cand = 0;
-    for (;;) {
-      if (tid == 0) {
-        Plane<W> x = load_plane<W>(ar.x, src + cand);
+  DenseTail<W>& tl = *reinterpret_cast<DenseTail<W>*>(dbuf + kDenseSmem);
+  for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) tl.hfp[sl] = 0ull;
+  __syncthreads();
+  bool ok = true;
+  for (uint32_t i = tid; i < n; i += kCta) {
+    Plane<W> f = load_plane<W>(ar.x, src + i);
 #pragma unroll
-        for (int k = 0; k < W; ++k) x.w[k] &= ~T.w[k];
-        cF[K] = x;
-        dc.next = kNone;
+    for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+    const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+    uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+    for (uint32_t probe = 0;; ++probe, h = (h + 1) & (kDenseSlots - 1)) {
+      if (probe == kDenseSlots) {
+        ok = false;  // more than kDenseSlots classes
+        break;
       }
-      __syncthreads();
-      const Plane<W> Fc = cF[K];
-      uint32_t first = kNone;
-      for (uint32_t k = 0, i = tid; i < n; ++k, i += kCta) {
-        if ((matched >> k) & 1u) continue;
-        const Plane<W> x = load_plane<W>(ar.x, src + i);
-        bool eq = true;
-#pragma unroll
-        for (int w = 0; w < W; ++w) eq &= (x.w[w] & ~T.w[w]) == Fc.w[w];
-        if (eq) matched |= 1u << k;
-        else if (first == kNone) first = i;
-      }
-      ++K;
-      if (first != kNone) atomicMin(&dc.next, first);
-      __syncthreads();
-      const uint32_t nx = dc.next;
-      __syncthreads();  // everyone read dc.next before the next round resets it
-      if (nx == kNone) break;
-      if (K == kDenseMaxK) return 0;
-      cand = nx;
+      const unsigned long long old = atomicCAS(&tl.hfp[h], 0ull, fp);
+      if (old == 0ull) tl.hF[h] = f;
+      if (old == 0ull || old == fp) break;
     }
   }
-  // b -> x bits outside F, one table per byte of b (behind the dense tile)
-  Plane<W>* xt = reinterpret_cast<Plane<W>*>(dbuf + kDenseSmem);
+  __syncthreads();
+  // verify (every string's F equals its slot's), count the classes
+  for (uint32_t i = tid; i < n && ok; i += kCta) {
+    Plane<W> f = load_plane<W>(ar.x, src + i);
+#pragma unroll
+    for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+    const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+    uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+    while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
+    ok = plane_eq<W>(tl.hF[h], f);
+  }
+  uint32_t used = 0;
+  for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) used += tl.hfp[sl] != 0ull;
+  if (tid == 0) dc.next = 0;
+  if (!__syncthreads_and(ok)) return 0;
+  if (used) atomicAdd(&dc.next, used);
+  __syncthreads();
+  const uint32_t K = dc.next;
+  if (K > kDenseMaxK) return 0;
+  // classes in ascending F order; class index per slot
+  for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) {
+    if (tl.hfp[sl] == 0ull) continue;
+    const Plane<W> f = tl.hF[sl];
+    uint32_t r = 0;
+    for (uint32_t s2 = 0; s2 < kDenseSlots; ++s2) r += tl.hfp[s2] != 0ull && plane_lt<W>(tl.hF[s2], f);
+    tl.hcls[sl] = (uint8_t)r;
+    tl.sF[r] = f;
+  }
+  __syncthreads();
+  const Plane<W> F = tl.sF[0];
+  // b -> x bits outside F, one table per byte of b
+  Plane<W>* xt = tl.xt;
   for (uint32_t e = tid; e < 3 * 256; e += kCta) {
     Plane<W> p;
 #pragma unroll
@@ -1779,6 +1806,8 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     if (records) atomicAdd(&st->records, records);
     if (removed) atomicAdd(&st->removed, removed);
     atomicAdd(&st->out_elems, (unsigned long long)out);
+    atomicAdd(&st->dense_groups, 1ull);
+    atomicAdd(&st->dense_out, (unsigned long long)out);
   }
   aff_elems += n;
   return 1;
@@ -2036,6 +2065,8 @@ constexpr size_t branch_smem_bytes() {
   return sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
 }
 static_assert(kDenseSmem % (8 * kCta) == 0, "dense tile gathers in steps of 8 kCta");
+static_assert(branch_smem_bytes<1>() >= kDenseSmem * sizeof(double) + sizeof(DenseTail<1>), "dense tail must fit");
+static_assert(branch_smem_bytes<2>() >= kDenseSmem * sizeof(double) + sizeof(DenseTail<2>), "dense tail must fit");
 static_assert(branch_smem_bytes<1>() >= kDenseSmem * sizeof(double) + 3 * 256 * 8, "dense tile must fit the branch buffer");
 static_assert(branch_smem_bytes<2>() >= kDenseSmem * sizeof(double) + 3 * 256 * 16, "dense tile must fit the branch buffer");
 
