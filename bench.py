@@ -388,11 +388,15 @@ def main():
     achieved = pks["branch_bytes"] / (pks["branch_ms"] / 1e3) / 1e9 if pks["branch_ms"] > 0 else 0.0
     launches_per_step = ks["launches"] / args.steps
     traffic = None
+    traffic_src = None
     prof = os.path.join(ROOT, "profiles", "branch_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(args.workload)
+                tr = json.load(f).get(args.workload)
+            if tr:  # ncu DRAM bytes per launch of the same kernel (tools/traffic.py)
+                traffic = tr["dram_bytes_per_launch"]
+                traffic_src = tr
         except Exception:
             traffic = None
 
@@ -422,12 +426,18 @@ def main():
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "api": "simulate()"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": "k_branch_x", "peak_kind": peak_kind,
-                         "bytes_model": "touched: (strings read + strings written) x (8W+8) B per launch",
+                         "traffic_unit": "DRAM bytes per launch (ncu)",
+                         "algorithmic_bytes_per_launch": (pks["branch_bytes"] / pks["branch_launches"]
+                                                          if pks["branch_launches"] else None),
+                         "traffic_detail": traffic_src,
+                         "kernel": "k_branch_sublayer", "peak_kind": peak_kind,
+                         "bytes_model": "(strings read + strings written) x (8W+8) B per launch; the dense "
+                                        "sublayer reads each input string once and writes each output "
+                                        "string once per Rx run",
                          "branch_ms_per_step": pks["branch_ms"],
                          "branch_bytes_per_step": pks["branch_bytes"],
                          "branch_launches_per_step": pks["branch_launches"],
-                         "how": "separate untimed pass, CUDA events around each k_branch_x launch",
+                         "how": "separate untimed pass, CUDA events around each branch launch",
                          # SURVEY.md 8d streaming model: R(n) (|O_in| + |O_out|) bytes per
                          # branching gate ~ 2 R(n) per string-gate, R(n) = 16 ceil(n/64) + 8
                          "streaming_model": {
