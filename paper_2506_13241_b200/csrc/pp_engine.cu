@@ -70,6 +70,7 @@ __global__ void k_reset_stats(DevStats* st, unsigned long long bump) {
 
 __global__ void k_clear_arena_error(DevStats* st) {
   st->err_arena = 0;
+  st->err_unsorted = 0;
   st->err_seq = ~0ull;
 }
 
@@ -333,14 +334,17 @@ class EngineImpl final : public EngineBase {
     seed_ = 0x5eed5eed12345678ull;
     tight_arena_ = std::getenv("PP_TIGHT_ARENA") != nullptr;
     no_dense_ = std::getenv("PP_NO_DENSE") != nullptr;
+    if (const char* mk = std::getenv("PP_DENSE_MAXK")) dense_maxk_ = std::max(1, std::atoi(mk));  // test hook
     update_arena_max();
   }
   ~EngineImpl() override {
     cudaStreamSynchronize(stream_);
     if (std::getenv("PP_TRACE"))
-      std::fprintf(stderr, "[pp] trace: layers %.3f ms, %llu syncs waiting %.3f ms, launches %llu\n",
-                   tr_layer_ns_ * 1e-6, (unsigned long long)tr_syncs_, tr_sync_ns_ * 1e-6,
-                   (unsigned long long)launches_);
+      std::fprintf(stderr,
+                   "[pp] trace: layers %.3f ms (clifford runs %.3f, rx runs %.3f), %llu syncs waiting %.3f ms, "
+                   "launches %llu\n",
+                   tr_layer_ns_ * 1e-6, tr_cliff_ns_ * 1e-6, tr_rx_ns_ * 1e-6, (unsigned long long)tr_syncs_,
+                   tr_sync_ns_ * 1e-6, (unsigned long long)launches_);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     release_pinned_stats(h_stats_);
@@ -466,24 +470,84 @@ class EngineImpl final : public EngineBase {
   }
 
   void apply_gates_async(const pp_gate* gates, size_t count) {
-    size_t i = 0;
-    while (i < count) {
-      if (fusion_allowed() && is_clifford(gates[i])) {
-        size_t j = i;
-        while (j < count && is_clifford(gates[j])) ++j;
-        apply_clifford_run(gates + i, j - i);
-        i = j;
-      } else if (is_x_type(gates[i])) {
-        size_t j = i;
-        while (j < count && is_x_type(gates[j]) && !(fusion_allowed() && is_clifford(gates[j]))) ++j;
-        run_rx(gates + i, j - i);
-        i = j;
+    // the partition of a gate list into runs is cached (run_circuit applies
+    // the same layer every step); with a term budget, fusion depends on |O|
+    const bool cacheable = cfg_.max_terms == 0;
+    if (!(cacheable && plan_key_.size() == count &&
+          std::memcmp(plan_key_.data(), gates, count * sizeof(pp_gate)) == 0)) {
+      plan_key_.clear();
+      plan_.clear();
+      size_t i = 0;
+      while (i < count) {
+        if (fusion_allowed() && is_clifford(gates[i])) {
+          size_t j = i;
+          while (j < count && is_clifford(gates[j])) ++j;
+          plan_.push_back({0, i, j});
+          i = j;
+        } else if (is_x_type(gates[i])) {
+          size_t j = i;
+          while (j < count && is_x_type(gates[j]) && !(fusion_allowed() && is_clifford(gates[j]))) ++j;
+          plan_.push_back({1, i, j});
+          i = j;
+        } else {
+          plan_.push_back({2, i, i + 1});
+          ++i;
+        }
+      }
+      if (cacheable) plan_key_.assign(gates, gates + count);
+    }
+    const std::vector<PlanRun> plan = plan_;  // a nested call may replace plan_
+    for (size_t pi = 0; pi < plan.size(); ++pi) {
+      const PlanRun& r = plan[pi];
+      auto t0 = Clock::now();
+      if (r.kind == 0) {
+        // a Clifford run feeding a dense Rx run leaves its groups unsorted
+        const bool next_dense = pi + 1 < plan.size() && plan[pi + 1].kind == 1 &&
+                                dense_capable(gates + plan[pi + 1].i, plan[pi + 1].j - plan[pi + 1].i);
+        apply_clifford_run(gates + r.i, r.j - r.i, !next_dense);
+        tr_cliff_ns_ += ns_since(t0);
+      } else if (r.kind == 1) {
+        run_rx(gates + r.i, r.j - r.i);
+        tr_rx_ns_ += ns_since(t0);
       } else {
-        apply_one(gates[i]);
-        ++i;
+        apply_one(gates[r.i]);
       }
     }
   }
+  // would run_rx take the dense sublayer for this X-type run (after a
+  // Clifford run, which changes neither zeros nor the budget state)?
+  bool dense_capable(const pp_gate* gates, size_t count) {
+    if (no_dense_ || keep_zeros_ || may_hold_zeros_ || cfg_.max_terms != 0 || count > (size_t)kMaxSubGates) return false;
+    if (!(external() || cfg_.epsilon0 == 0.0)) return false;
+    if (rx_key_.size() == count && std::memcmp(rx_key_.data(), gates, count * sizeof(pp_gate)) == 0)
+      return rx_distinct_;
+    for (size_t i = 0; i < count; ++i)
+      for (size_t j = 0; j < i; ++j)
+        if (std::memcmp(gates[i].words, gates[j].words, sizeof(gates[i].words)) == 0) return false;
+    return true;
+  }
+  // sort the groups a regroup left unsorted (before any consumer that needs
+  // x order: the per-gate branch kernels, Z-type pairs, shard eviction)
+  void ensure_sorted() {
+    if (!unsorted_) return;
+    sync_state();
+    unsorted_ = false;
+    if (!G_) return;
+    ensure_arena(1 - cur_, std::max<uint64_t>(live_ + 1, 1024));  // merge scratch for big groups
+    k_set_distinct<<<1, 1, 0, stream_>>>(d_stats_, G_);
+    const uint32_t small_grid = std::max<uint32_t>(1u, std::min<uint32_t>(G_, 148u * 4u));
+    const uint32_t big_grid = std::max<uint32_t>(1u, std::min<uint32_t>(G_, 148u * 2u));
+    k_sort_small<W><<<small_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(gcur_), aview(cur_), keep_zeros_, d_stats_,
+                                                                         1);
+    k_sort_big<W><<<big_grid, kCta, big_sort_smem(), stream_>>>(gview(gcur_), aview(cur_), aview(1 - cur_), keep_zeros_,
+                                                                 d_stats_, 1);
+    launches_ += 3;
+    dirty_ = true;
+  }
+  struct PlanRun {
+    int kind;  // 0 Clifford run, 1 X-type run, 2 single gate
+    size_t i, j;
+  };
 
   // single-qubit X generator: the z-group preserving branch kernel applies
   static bool is_x_type(const pp_gate& g) {
@@ -554,6 +618,7 @@ class EngineImpl final : public EngineBase {
       // dense path (k_branch_sublayer / dense_group): zeros dropped, every
       // gate of the run on its own qubit
       sgates.dense = rx_distinct_ && !keep_zeros_ && !may_hold_zeros_ && !no_dense_;
+      sgates.maxk = dense_maxk_;
       sync_state();
       if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
       // launched without a round trip: an arena overflow is found and
@@ -569,6 +634,7 @@ class EngineImpl final : public EngineBase {
       counters_.branch_ns += ns_since(t0);
       return;
     }
+    ensure_sorted();  // the per-gate kernels pair strings by x order
     // speculative fused run for epsilon0 > 0 (exact, but two passes per run on
     // these workloads: opt-in until the first prediction is right more often)
     const bool speculate = std::getenv("PP_SPECULATE") != nullptr;
@@ -749,6 +815,7 @@ class EngineImpl final : public EngineBase {
   }
 
   void launch_sublayer() {
+    sub_gates_.sorted = unsorted_ ? 0 : 1;
     push_scalars(sub_seq0_);
     std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
     PP_CUDA(cudaEventRecord(ev.first, stream_));
@@ -766,15 +833,22 @@ class EngineImpl final : public EngineBase {
   // relaunch; groups that finished carry the run's stamps and are skipped
   void resume_sublayer(bool diag) {
     sub_pending_ = false;
-    for (int attempt = 0; arena_fault_; ++attempt) {
+    for (int attempt = 0; arena_fault_ || unsorted_fault_; ++attempt) {
       if (attempt > 64) throw EngineError(PP_ERR_RESOURCE, "arena cannot hold the sublayer");
       k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
       ++launches_;
-      arena_fault_ = false;
-      // repeated overflows (a dense block larger than the usual growth):
-      // at least double the arena
-      gc_into_other(attempt >= 2 ? std::max<uint64_t>(next_arena_target(), std::min<uint64_t>(2 * arena_[cur_].cap, arena_max_))
-                                 : next_arena_target());
+      if (arena_fault_) {
+        arena_fault_ = false;
+        // repeated overflows (a dense block larger than the usual growth):
+        // at least double the arena
+        gc_into_other(attempt >= 2 ? std::max<uint64_t>(next_arena_target(),
+                                                        std::min<uint64_t>(2 * arena_[cur_].cap, arena_max_))
+                                   : next_arena_target());
+      }
+      if (unsorted_fault_) {  // groups the per-gate path needs sorted
+        unsorted_fault_ = false;
+        ensure_sorted();
+      }
       launch_sublayer();
       sync_state(diag);
     }
@@ -1350,7 +1424,7 @@ class EngineImpl final : public EngineBase {
     if (!G_) return;
     diag_z_.ensure((size_t)G_ * W * 8);
     diag_c_.ensure((size_t)G_ * 8);
-    k_diag<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, aview(cur_), diag_z_.as<uint64_t>(),
+    k_diag<W><<<blocks(32ull * G_), kCta, 0, stream_>>>(gview(gcur_), G_, aview(cur_), diag_z_.as<uint64_t>(),
                                                  diag_c_.as<double>(), d_stats_);
     ++launches_;
     if (!h_diag_) h_diag_ = pinned_diag();
@@ -1399,6 +1473,7 @@ class EngineImpl final : public EngineBase {
                                               ", |O|=" + std::to_string(st.err_live));
     }
     arena_fault_ = st.err_arena != 0;
+    unsorted_fault_ = st.err_unsorted != 0;
     arena_fault_seq_ = st.err_seq;
     if (st.red[2].nonfinite && gmax_stale_ && !external()) {
       dirty_ = false;
@@ -1431,7 +1506,7 @@ class EngineImpl final : public EngineBase {
     ++launches_;
     dirty_ = false;
     if (sub_pending_) {
-      if (arena_fault_) resume_sublayer(diag);
+      if (arena_fault_ || unsorted_fault_) resume_sublayer(diag);
       sub_pending_ = false;
     }
   }
@@ -1462,6 +1537,7 @@ class EngineImpl final : public EngineBase {
   // false when a pair could exceed one segment; the caller then regroups.
   bool apply_zz(const pp_gate& gate, const uint64_t* jzw) {
     auto t0 = Clock::now();
+    ensure_sorted();
     sync_state();
     if (2ull * maxcnt_ > kZSeg) return false;
     const bool budget = cfg_.max_terms != 0 && !external();
@@ -1573,10 +1649,10 @@ class EngineImpl final : public EngineBase {
 
   // A run of Clifford Z_i Z_j gates (i != j, no X/Y): split into matchings,
   // then into equal-offset groups, and regroup with ZZRunProducer.
-  bool try_zz_run(const pp_gate* gates, size_t count) {
+  bool try_zz_run(const pp_gate* gates, size_t count, bool sort) {
     if (zz_key_.size() == count && std::memcmp(zz_key_.data(), gates, count * sizeof(pp_gate)) == 0) {
       if (!zz_ok_) return false;
-      regroup(zz_prod_);  // the same run as last time (run_circuit layers)
+      regroup(zz_prod_, sort);  // the same run as last time (run_circuit layers)
       return true;
     }
     zz_key_.clear();
@@ -1634,14 +1710,14 @@ class EngineImpl final : public EngineBase {
     zz_key_.assign(gates, gates + count);
     zz_prod_ = p;
     zz_ok_ = true;
-    regroup(p);
+    regroup(p, sort);
     return true;
   }
 
   // ----- fused Clifford run
-  void apply_clifford_run(const pp_gate* gates, size_t count) {
+  void apply_clifford_run(const pp_gate* gates, size_t count, bool sort = true) {
     auto t0 = Clock::now();
-    if (G_ && try_zz_run(gates, count)) {
+    if (G_ && try_zz_run(gates, count, sort)) {
       // handled by the bit-parallel ZZ producer
     } else if (G_) {
       std::vector<uint64_t> gx(count * W), gz(count * W);
@@ -1664,7 +1740,7 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(cudaMemcpyAsync(dgz, gz.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemcpyAsync(dgs, gs.data(), count * 8, cudaMemcpyHostToDevice, stream_));
       CliffordProducer<W> p{dgx, dgz, dgs, (int)count};
-      regroup(p);
+      regroup(p, sort);
     }
     // Clifford gates zero each moved parent and re-insert it at I xor J;
     // absent a partner pair the reference removes one zero per record.
@@ -1686,7 +1762,7 @@ class EngineImpl final : public EngineBase {
 
   // ----- regroup: records -> new z-grouped store
   template <class P>
-  void regroup(const P& prod) {
+  void regroup(const P& prod, bool sort = true) {
     const int maxrec = P::kMaxRec;
     sync_state();
     const uint64_t live = live_;
@@ -1759,7 +1835,10 @@ class EngineImpl final : public EngineBase {
         groups_bound = distinct;
       }
       ensure_groups(1 - gcur_, std::max<uint32_t>(groups_bound, 1024));
-      ensure_arena(o, regroup_arena(total_bound));
+      // the two arenas alternate between regroups: keep the target as large
+      // as the current one (the Rx run after a regroup grows into it; a
+      // smaller target would overflow there and compact)
+      ensure_arena(o, std::max<uint64_t>(regroup_arena(total_bound), std::min<uint64_t>(arena_[cur_].cap, arena_max_)));
       k_table_emit<W><<<(uint32_t)((tc + kCta - 1) / kCta), kCta, 0, stream_>>>(
           t, scan_gid_.as<unsigned long long>(), scan_off_.as<unsigned long long>(), gview(1 - gcur_), 0);
       k_scatter<W, P><<<(uint32_t)n_items, kCta, 0, stream_>>>(items_.as<Item>(), gview(gcur_), aview(cur_), prod, t,
@@ -1776,15 +1855,24 @@ class EngineImpl final : public EngineBase {
       }
       // sort inside groups; the source arena is free now and serves as
       // scratch for the big-group merge passes
-      const bool source_kept = arena_[cur_].cap >= total_bound + 1;
-      ensure_arena(cur_, std::min<uint64_t>(total_bound + 1, arena_max_));
-      const uint32_t sort_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 16u));
-      const uint32_t small_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 4u));
-      k_sort_small<W><<<small_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o), keep_zeros_,
-                                                                           d_stats_);
-      k_sort_big<W><<<std::min<uint32_t>(sort_grid, 148u * 2u), kCta, big_sort_smem(), stream_>>>(
-          gview(1 - gcur_), aview(o), aview(cur_), keep_zeros_, d_stats_);
-      launches_ += 2;
+      bool source_kept = true;
+      if (sort) {
+        source_kept = arena_[cur_].cap >= total_bound + 1;
+        ensure_arena(cur_, std::min<uint64_t>(total_bound + 1, arena_max_));
+        const uint32_t sort_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 16u));
+        const uint32_t small_grid = std::max<uint32_t>(1u, std::min<uint32_t>(groups_bound, 148u * 4u));
+        k_sort_small<W><<<small_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(1 - gcur_), aview(o),
+                                                                             keep_zeros_, d_stats_);
+        k_sort_big<W><<<std::min<uint32_t>(sort_grid, 148u * 2u), kCta, big_sort_smem(), stream_>>>(
+            gview(1 - gcur_), aview(o), aview(cur_), keep_zeros_, d_stats_);
+        launches_ += 2;
+      } else {
+        // a bijection feeding a dense Rx run: statistics only, groups left
+        // unsorted (kFlagUnsorted)
+        k_group_stats<W><<<std::max<uint32_t>(1u, std::min<uint32_t>((groups_bound + 7) / 8, 148u * 8u)), kCta, 0,
+                           stream_>>>(gview(1 - gcur_), aview(o), d_stats_);
+        ++launches_;
+      }
       fetch_stats();
       PP_CUDA(cudaGetLastError());
       if (small && (h_stats_->overflow || h_stats_->collision)) {  // not expected: redo on the careful path
@@ -1801,6 +1889,7 @@ class EngineImpl final : public EngineBase {
       cur_ = o;
       gcur_ = 1 - gcur_;
       G_ = distinct;
+      unsorted_ = !sort;
       bump_ = bump_bound_ = total;
       live_ = live_bound_ = total - h_stats_->removed;
       reset_stats(bump_);  // cumulative counters were harvested above
@@ -1871,16 +1960,22 @@ class EngineImpl final : public EngineBase {
   bool dirty_ = false, truncated_since_sync_ = false, gmax_stale_ = false, may_hold_zeros_ = false;
   uint64_t eseq_ = 0, bseq_ = 0;
   uint64_t tr_layer_ns_ = 0, tr_sync_ns_ = 0, tr_syncs_ = 0;  // PP_TRACE host timeline
+  uint64_t tr_cliff_ns_ = 0, tr_rx_ns_ = 0;
+  std::vector<pp_gate> plan_key_;  // apply_gates_async run partition cache
+  std::vector<PlanRun> plan_;
   uint64_t dense_groups_ = 0, dense_out_ = 0;
   std::vector<pp_gate> rx_key_;  // run_rx plan cache
   std::vector<RxParam> rx_prm_;
   SubGates rx_sg_{};
   bool rx_distinct_ = true;
   bool no_dense_ = false;
+  int dense_maxk_ = (int)kDenseMaxK;
   std::vector<pp_gate> zz_key_;  // try_zz_run plan cache
   ZZRunProducer<W> zz_prod_{};
   bool zz_ok_ = false;
   bool arena_fault_ = false;
+  bool unsorted_fault_ = false;  // a sublayer left unsorted groups for the per-gate path
+  bool unsorted_ = false;        // the table holds kFlagUnsorted groups
   bool sub_pending_ = false;  // a sublayer launch not yet checked for an arena overflow
   SubGates sub_gates_{};
   uint64_t sub_seq0_ = 0;

@@ -35,9 +35,14 @@ struct GroupView {
   uint32_t* cap;
   double* gmax;
   double* gmin;
-  uint32_t* flags;  // bit0: non-finite coefficient present
+  uint32_t* flags;  // bit0: non-finite coefficient present; bit1 (kFlagUnsorted): strings not sorted by x
   uint32_t* stamp;  // sequence number of the last X-type gate applied (makes gates resumable)
 };
+// A regroup that feeds a dense Rx run skips the per-group sort (the dense
+// path scatters by x and writes sorted output); such groups carry this flag
+// until the dense path or a sort pass (k_sort_small/k_sort_big with
+// only_unsorted) rewrites them.
+constexpr uint32_t kFlagUnsorted = 2u;
 
 // deferred truncation helpers (see k_thresh): a pending string is held as
 // -0.0 in shared memory (stored values are never zero when truncating per
@@ -107,6 +112,8 @@ struct DevStats {
   unsigned int zz_maxcnt;          // Z-type gate: largest group written
   unsigned int zz_err;             // Z-type gate: a pair exceeded the segment (host pre-check failed)
   unsigned int zz_pad;
+  unsigned int err_unsorted;        // sticky: a sublayer skipped an unsorted group it could not apply densely
+  unsigned int pad2;
   unsigned long long dense_groups;  // groups applied by the dense sublayer path (cumulative)
   unsigned long long dense_out;     // strings those groups wrote
 };
@@ -1135,6 +1142,8 @@ struct SubGates {
   double sinv[kMaxSubGates];
   uint64_t any[2];  // union of the gate masks per plane word
   int dense;        // dense path allowed: distinct qubits, zeros dropped (k_branch_sublayer)
+  int sorted;       // every group is sorted by x (no kFlagUnsorted group in the table)
+  int maxk;         // x classes allowed per group on the dense path (<= kDenseMaxK; test hook)
 };
 
 // copy group region [src, src+n) to dst keeping |c| > T (truncation into
@@ -1254,8 +1263,7 @@ __device__ __forceinline__ void reduce_group_stats(GroupStatsSmem& r, double& vm
 constexpr uint32_t kDenseSmemLog = 13;
 constexpr uint32_t kDenseSmem = 1u << kDenseSmemLog;  // doubles of the dynamic buffer
 constexpr int kDenseMaxLog = 24;                      // larger blocks take the per-gate path
-constexpr uint32_t kDenseMaxK = 64;                   // x classes per group on the dense path
-constexpr uint32_t kDenseMaxIn = 32 * kCta;           // input strings per group (one match bit each per thread)
+constexpr uint32_t kDenseMaxK = 256;                  // x classes per group on the dense path
 constexpr uint32_t kDenseMaxOut = 1u << 26;           // K 2^m points per group
 
 // Behind the dense tile in the dynamic buffer: output tables and the x-class
@@ -1267,6 +1275,7 @@ struct DenseTail {
   unsigned long long hfp[kDenseSlots];  // class hash set: fingerprint (0 = empty)
   Plane<W> hF[kDenseSlots];             //   its class F
   uint8_t hcls[kDenseSlots];            //   its class index (ascending F)
+  uint16_t used[kDenseSlots];           // occupied slots, compacted
   Plane<W> sF[kDenseMaxK];              // classes in ascending order
   uint8_t lvl[kDenseMaxK][kDenseMaxLog + 1];  // rank terms: #classes j with t_ij = t
   uint32_t lmask[kDenseMaxK];           //   levels t present
@@ -1651,7 +1660,6 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   // x classes (the distinct x parts F outside T): a shared-memory hash set
   // keyed by a fingerprint of F, verified against the stored F afterwards
   // (a fingerprint collision sends the group to the per-gate path)
-  if (n > kDenseMaxIn) return 0;
   DenseTail<W>& tl = *reinterpret_cast<DenseTail<W>*>(dbuf + kDenseSmem);
   for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) tl.hfp[sl] = 0ull;
   __syncthreads();
@@ -1683,20 +1691,23 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
     ok = plane_eq<W>(tl.hF[h], f);
   }
-  uint32_t used = 0;
-  for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) used += tl.hfp[sl] != 0ull;
-  if (tid == 0) dc.next = 0;
+  static_assert(kDenseSlots == 2 * kCta, "two hash slots per thread");
+  const bool u0 = tl.hfp[2 * tid] != 0ull, u1 = tl.hfp[2 * tid + 1] != 0ull;
   if (!__syncthreads_and(ok)) return 0;
-  if (used) atomicAdd(&dc.next, used);
+  uint32_t K;
+  {
+    const uint32_t pos = block_excl_scan((uint32_t)u0 + (uint32_t)u1, scan, &K);
+    if (u0) tl.used[pos] = (uint16_t)(2 * tid);
+    if (u1) tl.used[pos + u0] = (uint16_t)(2 * tid + 1);
+  }
+  if (K > kDenseMaxK || K > (uint32_t)gates.maxk) return 0;
   __syncthreads();
-  const uint32_t K = dc.next;
-  if (K > kDenseMaxK) return 0;
   // classes in ascending F order; class index per slot
-  for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) {
-    if (tl.hfp[sl] == 0ull) continue;
+  for (uint32_t c = tid; c < K; c += kCta) {
+    const uint32_t sl = tl.used[c];
     const Plane<W> f = tl.hF[sl];
     uint32_t r = 0;
-    for (uint32_t s2 = 0; s2 < kDenseSlots; ++s2) r += tl.hfp[s2] != 0ull && plane_lt<W>(tl.hF[s2], f);
+    for (uint32_t j = 0; j < K; ++j) r += plane_lt<W>(tl.hF[tl.used[j]], f);
     tl.hcls[sl] = (uint8_t)r;
     tl.sF[r] = f;
   }
@@ -1932,6 +1943,12 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
       }
       if (r > 0) continue;
     }
+    if (!gates.sorted && (g.flags[gid] & kFlagUnsorted)) {
+      // the per-gate path needs the group sorted: leave it (stamp unchanged)
+      // for a relaunch after the host's sort pass
+      if (tid == 0) atomicOr(&st->err_unsorted, 1u);
+      continue;
+    }
     // next touching gate at or after k (gates.ng: the end step; ng + 1: done)
     auto next_touch = [&](int k) {
       if (k >= gates.ng) return k;
@@ -2062,7 +2079,11 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
 
 template <int W>
 constexpr size_t branch_smem_bytes() {
-  return sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
+  // the segment / stream buffers of the per-gate path, or the dense tile and
+  // its tables, whichever is larger
+  constexpr size_t a = sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
+  constexpr size_t d = kDenseSmem * sizeof(double) + sizeof(DenseTail<W>);
+  return a > d ? a : d;
 }
 static_assert(kDenseSmem % (8 * kCta) == 0, "dense tile gathers in steps of 8 kCta");
 static_assert(branch_smem_bytes<1>() >= kDenseSmem * sizeof(double) + sizeof(DenseTail<1>), "dense tail must fit");
@@ -2374,14 +2395,32 @@ __global__ void __launch_bounds__(kCta) k_histogram(GroupView<W> g, ArenaView<W>
 template <int W>
 __global__ void k_diag(GroupView<W> g, uint32_t G, ArenaView<W> ar, uint64_t* out_z, double* out_c,
                        DevStats* st) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= G || g.cnt[i] == 0) return;
-  uint64_t o = g.off[i];
-  if (!plane_zero<W>(load_plane<W>(ar.x, o))) return;
+  // warp per group: a sorted group holds x = 0 first; an unsorted one
+  // (kFlagUnsorted) is searched by the warp
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= G) return;
+  const uint32_t n = g.cnt[i];
+  if (n == 0) return;
+  const uint64_t o = g.off[i];
+  uint64_t hit = ~0ull;
+  if (g.flags[i] & kFlagUnsorted) {
+    for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+      const bool z = j0 + lane < n && plane_zero<W>(load_plane<W>(ar.x, o + j0 + lane));
+      const uint32_t b = __ballot_sync(0xffffffffu, z);
+      if (b) {
+        hit = o + j0 + __ffs(b) - 1;
+        break;
+      }
+    }
+  } else if (plane_zero<W>(load_plane<W>(ar.x, o))) {
+    hit = o;
+  }
+  if (lane != 0 || hit == ~0ull) return;
   unsigned long long d = atomicAdd(&st->diag_count, 1ull);
 #pragma unroll
   for (int k = 0; k < W; ++k) out_z[d * W + k] = g.z[k][i];
-  out_c[d] = ar.c[o];
+  out_c[d] = ar.c[hit];
 }
 
 // ---------------------------------------------------------------------------

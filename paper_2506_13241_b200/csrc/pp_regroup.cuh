@@ -666,7 +666,8 @@ __device__ void smem_bitonic_pack(uint64_t* key, double* val, uint16_t* gk, uint
 // kSortPackGroup strings are sorted together in packs of <= kSortSmall
 // strings (one bitonic pass on (group, x)), larger ones one by one.
 template <int W>
-__global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W> ar, int keep_zeros, DevStats* st) {
+__global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W> ar, int keep_zeros, DevStats* st,
+                                                     int only_unsorted = 0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<W>& sm = *reinterpret_cast<SortSmem<W>*>(smem_raw);
   const uint32_t G = *(volatile const unsigned int*)&st->distinct;
@@ -678,7 +679,8 @@ __global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W
   for (uint32_t c0 = blockIdx.x * chunk; c0 < G; c0 += gridDim.x * chunk) {
     __syncthreads();
     const uint32_t gi = c0 + tid;
-    const uint32_t nt = (tid < chunk && gi < G) ? g.cnt[gi] : 0u;
+    const uint32_t nt =
+        (tid < chunk && gi < G && (!only_unsorted || (g.flags[gi] & kFlagUnsorted))) ? g.cnt[gi] : 0u;
     const bool small = nt > 0 && nt <= kSortPackGroup;
     const bool single = nt > kSortPackGroup && nt <= kSortSmall;
     uint32_t nsmall, tsz, nsingle;
@@ -950,13 +952,14 @@ __device__ void cta_merge_runs(MergeSmem<W>& sm, ArenaView<W> ar, uint64_t a, ui
 // combine pass back into the region.  One CTA per group.
 template <int W>
 __global__ void __launch_bounds__(kCta) k_sort_big(GroupView<W> g, ArenaView<W> ar, ArenaView<W> scratch,
-                                                   int keep_zeros, DevStats* st) {
+                                                   int keep_zeros, DevStats* st, int only_unsorted = 0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t G = *(volatile const unsigned int*)&st->distinct;
   for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
   __syncthreads();
   const uint32_t n = g.cnt[gid];
   if (n <= kSortSmall) continue;
+  if (only_unsorted && !(g.flags[gid] & kFlagUnsorted)) continue;
   const uint64_t off = g.off[gid];
   __shared__ unsigned long long so_s;
   if (threadIdx.x == 0) so_s = atomicAdd(&st->scratch_bump, (unsigned long long)n);
@@ -1018,6 +1021,43 @@ __global__ void __launch_bounds__(kCta) k_sort_big(GroupView<W> g, ArenaView<W> 
   uint32_t w = combine_stream<W>(n, getk, getv, ar, off, keep_zeros, scan, vmax, vmin, nf, removed);
   finish_group_stats<W>(g, gid, w, vmax, vmin, nf, removed, st);
   }
+}
+
+// Group statistics of a regroup that skipped the sort (a Clifford run is a
+// signed permutation: no equal keys to combine, no zeros): max / min |c| and
+// the non-finite flag per group, marked unsorted.  Warp per group.
+template <int W>
+__global__ void __launch_bounds__(kCta) k_group_stats(GroupView<W> g, ArenaView<W> ar, const DevStats* st) {
+  const uint32_t G = *(volatile const unsigned int*)&st->distinct;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t gid = warp; gid < G; gid += nw) {
+    const uint64_t o = g.off[gid];
+    const uint32_t n = g.cnt[gid];
+    unsigned long long gx = 0ull, gn = 0x7ff0000000000000ull;
+    uint32_t nf = 0;
+    for (uint32_t j = lane; j < n; j += 32) {
+      const unsigned long long ab = (unsigned long long)__double_as_longlong(ar.c[o + j]) & 0x7fffffffffffffffull;
+      if (ab >= 0x7ff0000000000000ull) nf = 1;
+      if (ab <= 0x7ff0000000000000ull) {
+        gx = ab > gx ? ab : gx;
+        gn = ab < gn ? ab : gn;
+      }
+    }
+    gx = warp_max_bits(gx);
+    gn = warp_min_bits(gn);
+    nf = __any_sync(0xffffffffu, nf);
+    if (lane == 0) {
+      g.gmax[gid] = n ? __longlong_as_double((long long)gx) : 0.0;
+      g.gmin[gid] = n ? __longlong_as_double((long long)gn) : __longlong_as_double(0x7ff0000000000000ll);
+      g.flags[gid] = nf | kFlagUnsorted;
+    }
+  }
+}
+
+__global__ void k_set_distinct(DevStats* st, unsigned int G) {
+  st->distinct = G;
+  st->scratch_bump = 0;
 }
 
 }  // namespace ppgpu

@@ -274,16 +274,21 @@ def test_deferred_truncation_is_exact(pp, O, monkeypatch, mode):
     run_both(pp, O, 127, list(circ.layers), init, 3e-4, "gate")
 
 
-@pytest.mark.parametrize("mode", ["per_gate", "dense_tight"])
+@pytest.mark.parametrize("mode", ["per_gate", "dense_tight", "unsorted_fallback"])
 def test_sublayer_paths_match_oracle(pp, O, monkeypatch, mode):
     """epsilon0 = 0 Rx runs: the dense sublayer (default, dense_group) and
     the per-gate segment/stream path (PP_NO_DENSE) both equal the oracle bit
     for bit, also when the arena overflows mid-run and resumes
-    (PP_TIGHT_ARENA: dense blocks in global memory and in shared memory)."""
+    (PP_TIGHT_ARENA: dense blocks in global memory and in shared memory), and
+    when groups a regroup left unsorted must take the per-gate path."""
     if mode == "per_gate":
         monkeypatch.setenv("PP_NO_DENSE", "1")
-    else:
+    elif mode == "dense_tight":
         monkeypatch.setenv("PP_TIGHT_ARENA", "1")
+    else:
+        # multi-class groups leave the dense path after a regroup that skipped
+        # its sort: the sublayer defers them, the host sorts, the run resumes
+        monkeypatch.setenv("PP_DENSE_MAXK", "1")
     geom = pp.heavy_hex_127()
     circ = _kicked(pp, geom, "0.25pi", 5)
     run_both(pp, O, 127, list(circ.layers), [(O.site_word(62, 3), 1.0)], 0.0, "gate", check_each=True)
