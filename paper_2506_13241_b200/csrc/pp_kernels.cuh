@@ -1742,68 +1742,110 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   __syncthreads();
   if (dc.fail) return -1;
   const uint64_t dst = dc.dst;
-  const bool in_smem = S <= kDenseSmem;
-  double* blk = in_smem ? dbuf : ar.c + dst;  // the dense block
   unsigned long long records = 0, removed = 0;
-  for (uint32_t i = tid; i < S; i += kCta) blk[i] = 0.0;
-  __syncthreads();
-  for (uint32_t i = tid; i < n; i += kCta) blk[dense_pext<W>(load_plane<W>(ar.x, src + i), T)] = ar.c[src + i];
-  __syncthreads();
-  if (in_smem) {
-    dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed);
-  } else {
-    dense_passes<W>(dbuf, blk, S, dc, records, removed);
-  }
-  // nonzero points in b (= x) order, compacted into the output region (in
-  // place for a block in global memory: a tile's writes land at or below its
-  // own positions, after all of its reads)
-  constexpr uint32_t kPer = 8;  // 8 loads in flight per thread per tile
   double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll), vall = 0.0;
   uint32_t nonfinite = 0;
   uint32_t out = 0;
-  const uint32_t lane = tid & 31, warp = tid >> 5;
-  uint32_t* ocnt = reinterpret_cast<uint32_t*>(dc.deplo);  // kPer x kWarps counts (+ total); passes are done
-  for (uint32_t base = 0; base < S; base += kCta * kPer) {
-    double v[kPer];
-    uint32_t bal[kPer];
-#pragma unroll
-    for (uint32_t e = 0; e < kPer; ++e) {  // striped: slot e covers [base + e kCta, base + (e+1) kCta)
-      const uint32_t b = base + e * kCta + tid;
-      v[e] = b < S ? blk[b] : 0.0;
-    }
-#pragma unroll
-    for (uint32_t e = 0; e < kPer; ++e) {
-      bal[e] = __ballot_sync(0xffffffffu, v[e] != 0.0);
-      if (lane == 0) ocnt[e * kWarps + warp] = __popc(bal[e]);
-    }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of the kPer x kWarps counts (b order), 2 per lane
-      static_assert(kPer * kWarps == 64, "two counts per lane");
-      const uint32_t c0 = ocnt[2 * lane], c1 = ocnt[2 * lane + 1];
-      const uint32_t inc = warp_incl_scan(c0 + c1);
-      ocnt[2 * lane] = inc - c0 - c1;
-      ocnt[2 * lane + 1] = inc - c1;
-      if (lane == 31) ocnt[64] = inc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (uint32_t e = 0; e < kPer; ++e) {
-      if (v[e] == 0.0) continue;
-      const uint32_t b = base + e * kCta + tid;
-      const uint32_t o = out + ocnt[e * kWarps + warp] + __popc(bal[e] & ((1u << lane) - 1u));
+  bool done = false;
+  if (n == 1) {
+    // One string: output point b is the input coefficient times one factor
+    // per stage -- cos where b keeps the string's bit, the signed sin where it
+    // flips it (+sin from a Z, -sin from a Y) -- multiplied in gate order,
+    // exactly the products the butterflies form (no point ever receives two
+    // contributions).  Valid when no point ends at zero; then every stage's
+    // deltas are nonzero: records = 2^m - 1, nothing removed.
+    const double c0 = ar.c[src];
+    const uint32_t b0 = dense_pext<W>(load_plane<W>(ar.x, src), T);
+    bool zero = false;
+    for (uint32_t b = tid; b < S; b += kCta) {
+      double v = c0;
+      for (int j = 0; j < m; ++j) {
+        const uint32_t bit = 1u << dc.sbit[j];
+        const double f = ((b ^ b0) & bit) ? ((b0 & bit) ? -dc.ssin[j] : dc.ssin[j]) : dc.scos[j];
+        v = __dmul_rn(v, f);
+      }
+      zero |= v == 0.0;
       Plane<W> x = F;
       const Plane<W> a0 = xt[b & 255u], a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
 #pragma unroll
       for (int w = 0; w < W; ++w) x.w[w] |= a0.w[w] | a1.w[w] | a2.w[w];
-      store_plane<W>(ar.x, dst + o, x);
-      ar.c[dst + o] = v[e];
-      const double av = fabs(v[e]);
+      store_plane<W>(ar.x, dst + b, x);
+      ar.c[dst + b] = v;
+      const double av = fabs(v);
       if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
       vmax = fmax(vmax, av);
       vmin = fmin(vmin, av);
     }
-    out += ocnt[kPer * kWarps];
+    if (!__syncthreads_or(zero)) {
+      done = true;
+      out = S;
+      if (tid == 0) records = S - 1;
+    } else {  // an underflow or a zero angle: the general path below
+      vmax = 0.0;
+      vmin = __longlong_as_double(0x7ff0000000000000ll);
+      nonfinite = 0;
+    }
+  }
+  if (!done) {
+    const bool in_smem = S <= kDenseSmem;
+    double* blk = in_smem ? dbuf : ar.c + dst;  // the dense block
+    for (uint32_t i = tid; i < S; i += kCta) blk[i] = 0.0;
     __syncthreads();
+    for (uint32_t i = tid; i < n; i += kCta) blk[dense_pext<W>(load_plane<W>(ar.x, src + i), T)] = ar.c[src + i];
+    __syncthreads();
+    if (in_smem) {
+      dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed);
+    } else {
+      dense_passes<W>(dbuf, blk, S, dc, records, removed);
+    }
+    // nonzero points in b (= x) order, compacted into the output region (in
+    // place for a block in global memory: a tile's writes land at or below its
+    // own positions, after all of its reads)
+    constexpr uint32_t kPer = 8;  // 8 loads in flight per thread per tile
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    uint32_t* ocnt = reinterpret_cast<uint32_t*>(dc.deplo);  // kPer x kWarps counts (+ total); passes are done
+    for (uint32_t base = 0; base < S; base += kCta * kPer) {
+      double v[kPer];
+      uint32_t bal[kPer];
+  #pragma unroll
+      for (uint32_t e = 0; e < kPer; ++e) {  // striped: slot e covers [base + e kCta, base + (e+1) kCta)
+        const uint32_t b = base + e * kCta + tid;
+        v[e] = b < S ? blk[b] : 0.0;
+      }
+  #pragma unroll
+      for (uint32_t e = 0; e < kPer; ++e) {
+        bal[e] = __ballot_sync(0xffffffffu, v[e] != 0.0);
+        if (lane == 0) ocnt[e * kWarps + warp] = __popc(bal[e]);
+      }
+      __syncthreads();
+      if (warp == 0) {  // exclusive scan of the kPer x kWarps counts (b order), 2 per lane
+        static_assert(kPer * kWarps == 64, "two counts per lane");
+        const uint32_t c0 = ocnt[2 * lane], c1 = ocnt[2 * lane + 1];
+        const uint32_t inc = warp_incl_scan(c0 + c1);
+        ocnt[2 * lane] = inc - c0 - c1;
+        ocnt[2 * lane + 1] = inc - c1;
+        if (lane == 31) ocnt[64] = inc;
+      }
+      __syncthreads();
+  #pragma unroll
+      for (uint32_t e = 0; e < kPer; ++e) {
+        if (v[e] == 0.0) continue;
+        const uint32_t b = base + e * kCta + tid;
+        const uint32_t o = out + ocnt[e * kWarps + warp] + __popc(bal[e] & ((1u << lane) - 1u));
+        Plane<W> x = F;
+        const Plane<W> a0 = xt[b & 255u], a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
+  #pragma unroll
+        for (int w = 0; w < W; ++w) x.w[w] |= a0.w[w] | a1.w[w] | a2.w[w];
+        store_plane<W>(ar.x, dst + o, x);
+        ar.c[dst + o] = v[e];
+        const double av = fabs(v[e]);
+        if (!(av <= 1.7976931348623157e308)) nonfinite = 1;
+        vmax = fmax(vmax, av);
+        vmin = fmin(vmin, av);
+      }
+      out += ocnt[kPer * kWarps];
+      __syncthreads();
+    }
   }
   reduce_group_stats(gs, vmax, vmin, vall, nonfinite, records, removed);
   if (tid == 0) {
