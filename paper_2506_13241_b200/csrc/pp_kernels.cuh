@@ -1754,14 +1754,47 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     // exactly the products the butterflies form (no point ever receives two
     // contributions).  Valid when no point ends at zero; then every stage's
     // deltas are nonzero: records = 2^m - 1, nothing removed.
+    // The products share prefixes: with c the point's bits in stage order,
+    // P_{j+1}[c mod 2^{j+1}] = P_j[c mod 2^j] * f_j(bit j of c).  The first
+    // L = min(m, 13) stages build P_L in shared memory (2^{L+1} products);
+    // each output point multiplies its P_L by its remaining m - L factors.
     const double c0 = ar.c[src];
     const uint32_t b0 = dense_pext<W>(load_plane<W>(ar.x, src), T);
+    const int L = m < (int)kDenseSmemLog ? m : (int)kDenseSmemLog;
+    // b (x order) -> c (stage order), one table per byte of b; the class hash
+    // storage is free on this path
+    uint32_t* cperm = reinterpret_cast<uint32_t*>(tl.hF);
+    static_assert(sizeof(DenseTail<1>::hF) >= 3 * 256 * sizeof(uint32_t), "cperm fits the class hash keys");
+    for (uint32_t e = tid; e < 3 * 256; e += kCta) {
+      uint32_t c = 0;
+      const uint32_t t0 = 8 * (e >> 8);
+      for (int j = 0; j < m; ++j) {
+        const uint32_t t = dc.sbit[j];
+        if (t >= t0 && t < t0 + 8 && ((e >> (t - t0)) & 1u)) c |= 1u << j;
+      }
+      cperm[e] = c;
+    }
+    if (tid == 0) dbuf[0] = c0;
+    __syncthreads();
+    for (int j = 0; j < L; ++j) {
+      const uint32_t bit = 1u << dc.sbit[j];
+      const double fk = dc.scos[j], ff = (b0 & bit) ? -dc.ssin[j] : dc.ssin[j];  // keep / flip the string's bit
+      const double f0 = (b0 & bit) ? ff : fk, f1 = (b0 & bit) ? fk : ff;           // stage bit 0 / 1
+      for (uint32_t p = tid; p < (1u << j); p += kCta) {
+        const double v = dbuf[p];
+        dbuf[p + (1u << j)] = __dmul_rn(v, f1);
+        dbuf[p] = __dmul_rn(v, f0);
+      }
+      __syncthreads();
+    }
     bool zero = false;
     for (uint32_t b = tid; b < S; b += kCta) {
-      double v = c0;
-      for (int j = 0; j < m; ++j) {
+      const uint32_t c = cperm[b & 255u] | cperm[256 + ((b >> 8) & 255u)] | cperm[512 + (b >> 16)];
+      double v = dbuf[c & ((1u << L) - 1u)];
+      for (int j = L; j < m; ++j) {
         const uint32_t bit = 1u << dc.sbit[j];
-        const double f = ((b ^ b0) & bit) ? ((b0 & bit) ? -dc.ssin[j] : dc.ssin[j]) : dc.scos[j];
+        const double f = ((c >> j) & 1u) != ((b0 & bit) != 0u) ? ((b0 & bit) ? -dc.ssin[j] : dc.ssin[j])
+                                                                : dc.scos[j];
         v = __dmul_rn(v, f);
       }
       zero |= v == 0.0;
