@@ -1451,9 +1451,8 @@ class EngineImpl final : public EngineBase {
       lazy_open_ = false;
     }
     push_scalars(bseq_);
-    k_red_reset<<<1, 1, 0, stream_>>>(&d_stats_->red[2]);
     if (G_) k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, &d_stats_->red[2]);
-    launches_ += 3;
+    launches_ += G_ ? 1 : 0;
     if (diag) launch_diag();
     fetch_stats();
     PP_CUDA(cudaGetLastError());
@@ -1823,10 +1822,16 @@ class EngineImpl final : public EngineBase {
       scan_tmp_.ensure((ntiles + 1) * 8);
       scan_gid_.ensure(tc * 8);
       scan_off_.ensure(tc * 8);
-      device_scan(t.count, tc, 1, scan_gid_.as<unsigned long long>(), ntiles);
-      device_scan(t.count, tc, 0, scan_off_.as<unsigned long long>(), ntiles);
-      PP_CUDA(cudaMemcpyAsync(&d_stats_->scan_total, scan_tmp_.as<unsigned long long>() + ntiles, 8,
-                              cudaMemcpyDeviceToDevice, stream_));
+      if (tc <= kScanPairMax) {
+        k_scan_pair_small<<<1, kCta, 0, stream_>>>(t.count, (uint32_t)tc, scan_gid_.as<unsigned long long>(),
+                                                   scan_off_.as<unsigned long long>(), d_stats_);
+        ++launches_;
+      } else {
+        device_scan(t.count, tc, 1, scan_gid_.as<unsigned long long>(), ntiles);
+        device_scan(t.count, tc, 0, scan_off_.as<unsigned long long>(), ntiles);
+        PP_CUDA(cudaMemcpyAsync(&d_stats_->scan_total, scan_tmp_.as<unsigned long long>() + ntiles, 8,
+                                cudaMemcpyDeviceToDevice, stream_));
+      }
       uint64_t total_bound = records_upper;
       uint32_t groups_bound = (uint32_t)std::min<uint64_t>(records_upper, 0xffffffffu);
       if (!small) {

@@ -127,6 +127,7 @@ __global__ void k_set_scalars(DevStats* st, unsigned int G, unsigned long long c
   st->work[0] = st->work[1] = 0;
   clear_red(&st->red[0]);
   clear_red(&st->red[1]);
+  clear_red(&st->red[2]);  // the host-sync slot (only sync_state's k_reduce fills it)
 }
 
 // Reset of one reduction slot (cumulative counters and sticky errors stay).

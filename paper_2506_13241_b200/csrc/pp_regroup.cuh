@@ -1023,6 +1023,35 @@ __global__ void __launch_bounds__(kCta) k_sort_big(GroupView<W> g, ArenaView<W> 
   }
 }
 
+// Both exclusive scans of the regroup's slot counts (as flags: group ids;
+// as values: string offsets) for a small table, in one single-CTA launch:
+// each thread owns a contiguous chunk, one block scan of the chunk sums.
+constexpr uint32_t kScanPairMax = 1u << 16;
+__global__ void __launch_bounds__(kCta) k_scan_pair_small(const uint32_t* in, uint32_t n, unsigned long long* out_flag,
+                                                          unsigned long long* out_cnt, DevStats* st) {
+  __shared__ uint32_t scr[40];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t per = (n + kCta - 1) / kCta;
+  const uint32_t b0 = min(n, tid * per), b1 = min(n, b0 + per);
+  uint32_t f = 0, c = 0;
+  for (uint32_t i = b0; i < b1; ++i) {
+    const uint32_t v = in[i];
+    f += v != 0;
+    c += v;
+  }
+  uint32_t ft, ct;
+  uint32_t fe = block_excl_scan(f, scr, &ft);
+  uint32_t ce = block_excl_scan(c, scr, &ct);
+  for (uint32_t i = b0; i < b1; ++i) {
+    const uint32_t v = in[i];
+    out_flag[i] = fe;
+    out_cnt[i] = ce;
+    fe += v != 0;
+    ce += v;
+  }
+  if (tid == 0) st->scan_total = ct;
+}
+
 // Group statistics of a regroup that skipped the sort (a Clifford run is a
 // signed permutation: no equal keys to combine, no zeros): max / min |c| and
 // the non-finite flag per group, marked unsorted.  Warp per group.
