@@ -55,6 +55,7 @@ __global__ void k_clear_cumulative(DevStats* st) {
   st->out_elems = 0;
   st->aff_total = 0;
   st->stream_elems = 0;
+  st->cliff_records = 0;
   st->dense_groups = 0;
   st->dense_out = 0;
 }
@@ -300,6 +301,9 @@ class EngineImpl final : public EngineBase {
     h_stats_ = pinned_stats();
     PP_CUDA(cudaEventCreate(&ev0_));
     PP_CUDA(cudaEventCreate(&ev1_));
+    PP_CUDA(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming));
+    spin_sync_ = std::getenv("PP_BLOCKING_SYNC") == nullptr;
+    defer_ok_ = std::getenv("PP_NO_DEFER") == nullptr;
     PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)branch_smem_bytes<W>()));
     PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -347,6 +351,7 @@ class EngineImpl final : public EngineBase {
                    tr_sync_ns_ * 1e-6, (unsigned long long)launches_);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
+    cudaEventDestroy(ev_sync_);
     release_pinned_stats(h_stats_);
     release_pinned_diag(h_diag_);
     cudaStreamDestroy(stream_);
@@ -619,7 +624,7 @@ class EngineImpl final : public EngineBase {
       // gate of the run on its own qubit
       sgates.dense = rx_distinct_ && !keep_zeros_ && !may_hold_zeros_ && !no_dense_;
       sgates.maxk = dense_maxk_;
-      sync_state();
+      if (!g_pending_) sync_state();  // after a deferred regroup |O| and the bump are exact already
       if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
       // launched without a round trip: an arena overflow is found and
       // resumed by the next sync_state (resume_sublayer)
@@ -1333,10 +1338,20 @@ class EngineImpl final : public EngineBase {
     k_reset_stats<<<1, 1, 0, stream_>>>(d_stats_, bump);
     ++launches_;
   }
+  // The engine's round trips: spin on an event (lower wake-up latency than a
+  // blocking stream sync; the waits are short and frequent)
+  void wait_stream() {
+    PP_CUDA(cudaEventRecord(ev_sync_, stream_));
+    cudaError_t e;
+    while ((e = cudaEventQuery(ev_sync_)) == cudaErrorNotReady) {
+    }
+    PP_CUDA(e);
+  }
   void fetch_stats() {
     auto t0 = Clock::now();
     PP_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, sizeof(DevStats), cudaMemcpyDeviceToHost, stream_));
-    PP_CUDA(cudaStreamSynchronize(stream_));
+    if (spin_sync_) wait_stream();
+    else PP_CUDA(cudaStreamSynchronize(stream_));
     tr_sync_ns_ += ns_since(t0);
     ++tr_syncs_;
   }
@@ -1424,7 +1439,8 @@ class EngineImpl final : public EngineBase {
     if (!G_) return;
     diag_z_.ensure((size_t)G_ * W * 8);
     diag_c_.ensure((size_t)G_ * 8);
-    k_diag<W><<<blocks(32ull * G_), kCta, 0, stream_>>>(gview(gcur_), G_, aview(cur_), diag_z_.as<uint64_t>(),
+    k_diag<W><<<blocks(32ull * G_), kCta, 0, stream_>>>(gview(gcur_), g_pending_ ? kKeepG : G_, aview(cur_),
+                                                         diag_z_.as<uint64_t>(),
                                                  diag_c_.as<double>(), d_stats_);
     ++launches_;
     if (!h_diag_) h_diag_ = pinned_diag();
@@ -1457,6 +1473,18 @@ class EngineImpl final : public EngineBase {
     fetch_stats();
     PP_CUDA(cudaGetLastError());
     const DevStats& st = *h_stats_;
+    if (g_pending_) {
+      if (st.overflow || st.collision)
+        throw EngineError(PP_ERR_INTERNAL, "regroup: slot table overflow or fingerprint collision (deferred check)");
+      G_ = st.G_dev;
+      g_pending_ = false;
+    }
+    if (st.cliff_records) {  // Clifford records of a deferred regroup (apply_clifford_run's accounting)
+      counters_.records_sent += st.cliff_records;
+      counters_.removed += st.cliff_records;
+      counters_.batches_sent += pending_cliff_count_;
+    }
+    pending_cliff_count_ = 0;
     diag_n_ = st.diag_count;
     counters_.records_sent += st.records;
     counters_.removed += st.removed;
@@ -1512,7 +1540,7 @@ class EngineImpl final : public EngineBase {
   uint32_t persistent_grid() const { return 148u * 8u; }
 
   void push_scalars(uint64_t seq_base) {
-    k_set_scalars<<<1, 1, 0, stream_>>>(d_stats_, G_, arena_[cur_].cap, seq_base);
+    k_set_scalars<<<1, 1, 0, stream_>>>(d_stats_, g_pending_ ? kKeepG : G_, arena_[cur_].cap, seq_base);
     ++launches_;
   }
   // per-gate epilogue kernels for gate `rel` of a launch run (red slots by parity)
@@ -1743,6 +1771,7 @@ class EngineImpl final : public EngineBase {
     }
     // Clifford gates zero each moved parent and re-insert it at I xor J;
     // absent a partner pair the reference removes one zero per record.
+    if (g_pending_) pending_cliff_count_ = count;  // accounted at the next sync
     counters_.records_sent += h_records_;
     counters_.removed += h_records_;
     counters_.batches_sent += h_records_ ? count : 0;
@@ -1878,6 +1907,25 @@ class EngineImpl final : public EngineBase {
                            stream_>>>(gview(1 - gcur_), aview(o), d_stats_);
         ++launches_;
       }
+      if (small && !sort && defer_ok_) {
+        // a small Clifford regroup feeding a dense Rx run: no round trip.  A
+        // bijection keeps |O| (no merges, no zeros); the group count stays on
+        // the device (kernels read st->G_dev) until the next sync, which also
+        // checks the overflow / collision flags and accounts the records.
+        k_regroup_commit<<<1, 1, 0, stream_>>>(d_stats_);
+        ++launches_;
+        PP_CUDA(cudaGetLastError());
+        cur_ = o;
+        gcur_ = 1 - gcur_;
+        G_ = groups_bound;  // upper bound until the sync
+        g_pending_ = true;
+        unsorted_ = true;
+        bump_ = bump_bound_ = live;
+        live_ = live_bound_ = live;
+        h_records_ = 0;
+        dirty_ = true;
+        return;
+      }
       fetch_stats();
       PP_CUDA(cudaGetLastError());
       if (small && (h_stats_->overflow || h_stats_->collision)) {  // not expected: redo on the careful path
@@ -1978,6 +2026,11 @@ class EngineImpl final : public EngineBase {
   std::vector<pp_gate> zz_key_;  // try_zz_run plan cache
   ZZRunProducer<W> zz_prod_{};
   bool zz_ok_ = false;
+  cudaEvent_t ev_sync_ = nullptr;
+  bool g_pending_ = false;        // G_ is an upper bound; the exact count is st->G_dev
+  bool defer_ok_ = true;          // PP_NO_DEFER turns the deferred regroup off (test hook)
+  size_t pending_cliff_count_ = 0;
+  bool spin_sync_ = true;
   bool arena_fault_ = false;
   bool unsorted_fault_ = false;  // a sublayer left unsorted groups for the per-gate path
   bool unsorted_ = false;        // the table holds kFlagUnsorted groups

@@ -114,14 +114,16 @@ struct DevStats {
   unsigned int zz_pad;
   unsigned int err_unsorted;        // sticky: a sublayer skipped an unsorted group it could not apply densely
   unsigned int pad2;
+  unsigned long long cliff_records; // records of a regroup whose sizes the host reads later (deferred)
   unsigned long long dense_groups;  // groups applied by the dense sublayer path (cumulative)
   unsigned long long dense_out;     // strings those groups wrote
 };
 
 // Scalars a launch run reads from device memory, so that a captured CUDA
 // graph can be replayed for every layer.
+constexpr unsigned int kKeepG = 0xffffffffu;  // k_set_scalars / k_diag: the group count is on the device
 __global__ void k_set_scalars(DevStats* st, unsigned int G, unsigned long long cap, unsigned long long seq_base) {
-  st->G_dev = G;
+  if (G != kKeepG) st->G_dev = G;
   st->arena_cap = cap;
   st->seq_base = seq_base;
   st->work[0] = st->work[1] = 0;
@@ -2475,7 +2477,7 @@ __global__ void k_diag(GroupView<W> g, uint32_t G, ArenaView<W> ar, uint64_t* ou
   // (kFlagUnsorted) is searched by the warp
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= G) return;
+  if (i >= (G != kKeepG ? G : *(volatile const unsigned int*)&st->G_dev)) return;
   const uint32_t n = g.cnt[i];
   if (n == 0) return;
   const uint64_t o = g.off[i];

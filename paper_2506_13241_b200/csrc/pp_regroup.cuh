@@ -1084,6 +1084,16 @@ __global__ void __launch_bounds__(kCta) k_group_stats(GroupView<W> g, ArenaView<
   }
 }
 
+// End of a regroup whose sizes the host does not wait for: the new table's
+// group count and bump pointer become the device's, and the run's records
+// move aside for the next sync to account (records_sent and removed).
+__global__ void k_regroup_commit(DevStats* st) {
+  st->G_dev = st->distinct;
+  st->bump = st->scan_total;
+  st->cliff_records += st->records;
+  st->records = 0;
+}
+
 __global__ void k_set_distinct(DevStats* st, unsigned int G) {
   st->distinct = G;
   st->scratch_bump = 0;
