@@ -60,13 +60,37 @@ __global__ void k_clear_cumulative(DevStats* st) {
   st->dense_out = 0;
 }
 
-__global__ void k_reset_stats(DevStats* st, unsigned long long bump) {
+__device__ __forceinline__ void k_reset_stats_body(DevStats* st, unsigned long long bump);
+__global__ void k_reset_stats(DevStats* st, unsigned long long bump) { k_reset_stats_body(st, bump); }
+__device__ __forceinline__ void k_reset_stats_body(DevStats* st, unsigned long long bump) {
   DevStats s;
   memset(&s, 0, sizeof(s));
   s.bump = bump;
   for (int i = 0; i < 3; ++i) s.red[i].gmin_bits = 0x7ff0000000000000ull;
   s.err_seq = ~0ull;
   *st = s;
+}
+
+template <int W>
+__global__ void k_init_small(ArenaView<W> a, GroupView<W> g, const InitSmall<W> in, DevStats* st) {
+  const uint32_t t = threadIdx.x;
+  if (t < in.n) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) a.x[w][t] = in.x[t][w];
+    a.c[t] = in.c[t];
+  }
+  if (t < in.G) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) g.z[w][t] = in.z[t][w];
+    g.off[t] = in.off[t];
+    g.cnt[t] = in.cnt[t];
+    g.cap[t] = in.cnt[t];
+    g.gmax[t] = in.gmax[t];
+    g.gmin[t] = in.gmin[t];
+    g.flags[t] = in.flags[t];
+    g.stamp[t] = 0xffffffffu;
+  }
+  if (t == 0) k_reset_stats_body(st, in.n);
 }
 
 __global__ void k_clear_arena_error(DevStats* st) {
@@ -260,6 +284,44 @@ static void release_pinned_diag(DiagPinned* p) {
   g_diag_free.push_back(p);
 }
 
+// Streams and events outlive engines (simulate() creates one engine per
+// call): recycled per device, like the device memory pool.
+struct StreamSet {
+  cudaStream_t stream;
+  cudaEvent_t ev0, ev1, ev_sync;
+};
+static std::mutex g_streams_mu;
+static std::map<int, std::vector<StreamSet>> g_streams;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_event_pairs;
+static StreamSet acquire_stream_set(int dev) {
+  {
+    std::lock_guard<std::mutex> lk(g_streams_mu);
+    auto& v = g_streams[dev];
+    if (!v.empty()) {
+      StreamSet s = v.back();
+      v.pop_back();
+      return s;
+    }
+  }
+  StreamSet s;
+  PP_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  PP_CUDA(cudaEventCreate(&s.ev0));
+  PP_CUDA(cudaEventCreate(&s.ev1));
+  PP_CUDA(cudaEventCreateWithFlags(&s.ev_sync, cudaEventDisableTiming));
+  return s;
+}
+static void release_stream_set(int dev, const StreamSet& s) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  g_streams[dev].push_back(s);
+}
+// launch configuration of one (device, W): attributes set once, grids from
+// the occupancy calculator
+struct LaunchSetup {
+  uint32_t zz_grid = 0, branch_grid = 0, sub_grid = 0;
+};
+static std::mutex g_setup_mu;
+static std::map<std::pair<int, int>, LaunchSetup> g_setup;
+
 static std::mutex g_graph_mu;
 static std::map<std::string, cudaGraphExec_t> g_graphs;
 
@@ -295,44 +357,51 @@ class EngineImpl final : public EngineBase {
  public:
   explicit EngineImpl(const pp_config& cfg) : cfg_(cfg) {
     PP_CUDA(cudaSetDevice(cfg.device));
-    PP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    {
+      const StreamSet ss = acquire_stream_set(cfg.device);
+      stream_ = ss.stream;
+      ev0_ = ss.ev0;
+      ev1_ = ss.ev1;
+      ev_sync_ = ss.ev_sync;
+    }
     stats_buf_.ensure(sizeof(DevStats));
     d_stats_ = stats_buf_.as<DevStats>();
     h_stats_ = pinned_stats();
-    PP_CUDA(cudaEventCreate(&ev0_));
-    PP_CUDA(cudaEventCreate(&ev1_));
-    PP_CUDA(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming));
     spin_sync_ = std::getenv("PP_BLOCKING_SYNC") == nullptr;
     defer_ok_ = std::getenv("PP_NO_DEFER") == nullptr;
-    PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)branch_smem_bytes<W>()));
-    PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)branch_smem_bytes<W>()));
-    PP_CUDA(cudaFuncSetAttribute(k_sort_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(SortSmem<W>)));
-    PP_CUDA(cudaFuncSetAttribute(k_sort_big<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)big_sort_smem()));
-    PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    PP_CUDA(cudaFuncSetAttribute(k_branch_zz<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(ZzSmem<W>)));
     {
-      int sms = 148, occ = 1;
-      PP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
-      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_branch_zz<W>, kCta, sizeof(ZzSmem<W>)));
-      zz_grid_ = (uint32_t)(sms * std::max(occ, 1));
-    }
-    {  // persistent branch grids: every resident CTA slot of the device
-      int sms = 148, occ_x = 1, occ_s = 1;
-      PP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
-      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_branch_x<W>, kCta, branch_smem_bytes<W>()));
-      PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_branch_sublayer<W>, kCta,
-                                                            branch_smem_bytes<W>()));
-      branch_grid_ = (uint32_t)(sms * std::max(occ_x, 1));
-      sub_grid_ = (uint32_t)(sms * std::max(occ_s, 1));
-      if (std::getenv("PP_DEBUG"))
-        std::fprintf(stderr, "[pp] W=%d branch CTAs/SM %d, sublayer CTAs/SM %d, smem %zu\n", W, occ_x, occ_s,
-                     branch_smem_bytes<W>());
+      std::lock_guard<std::mutex> lk(g_setup_mu);
+      LaunchSetup& ls = g_setup[{cfg.device, W}];
+      if (!ls.sub_grid) {
+        PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)branch_smem_bytes<W>()));
+        PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)branch_smem_bytes<W>()));
+        PP_CUDA(cudaFuncSetAttribute(k_sort_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(SortSmem<W>)));
+        PP_CUDA(cudaFuncSetAttribute(k_sort_big<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)big_sort_smem()));
+        PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        PP_CUDA(cudaFuncSetAttribute(k_branch_zz<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(ZzSmem<W>)));
+        int sms = 148, occ = 1, occ_x = 1, occ_s = 1;
+        PP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
+        PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_branch_zz<W>, kCta, sizeof(ZzSmem<W>)));
+        // persistent branch grids: every resident CTA slot of the device
+        PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_branch_x<W>, kCta, branch_smem_bytes<W>()));
+        PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_branch_sublayer<W>, kCta,
+                                                              branch_smem_bytes<W>()));
+        ls.zz_grid = (uint32_t)(sms * std::max(occ, 1));
+        ls.branch_grid = (uint32_t)(sms * std::max(occ_x, 1));
+        ls.sub_grid = (uint32_t)(sms * std::max(occ_s, 1));
+        if (std::getenv("PP_DEBUG"))
+          std::fprintf(stderr, "[pp] W=%d branch CTAs/SM %d, sublayer CTAs/SM %d, smem %zu\n", W, occ_x, occ_s,
+                       branch_smem_bytes<W>());
+      }
+      zz_grid_ = ls.zz_grid;
+      branch_grid_ = ls.branch_grid;
+      sub_grid_ = ls.sub_grid;
     }
     keep_zeros_ = cfg.cadence == PP_CADENCE_LAYER;
     seed_ = 0x5eed5eed12345678ull;
@@ -349,12 +418,14 @@ class EngineImpl final : public EngineBase {
                    "launches %llu\n",
                    tr_layer_ns_ * 1e-6, tr_cliff_ns_ * 1e-6, tr_rx_ns_ * 1e-6, (unsigned long long)tr_syncs_,
                    tr_sync_ns_ * 1e-6, (unsigned long long)launches_);
-    cudaEventDestroy(ev0_);
-    cudaEventDestroy(ev1_);
-    cudaEventDestroy(ev_sync_);
+    release_stream_set(cfg_.device, StreamSet{stream_, ev0_, ev1_, ev_sync_});
+    {
+      std::lock_guard<std::mutex> lk(g_streams_mu);
+      for (auto& e : free_events_) g_event_pairs.push_back(e);
+      for (auto& e : pending_events_) g_event_pairs.push_back(e);
+    }
     release_pinned_stats(h_stats_);
     release_pinned_diag(h_diag_);
-    cudaStreamDestroy(stream_);
   }
 
   // ---------------------------------------------------------------- set_initial
@@ -424,13 +495,40 @@ class EngineImpl final : public EngineBase {
     ensure_groups(0, std::max<uint32_t>(G, 1024));
     gcur_ = 0;
     G_ = G;
-    if (n) {
+    sub_pending_ = false;
+    g_pending_ = false;
+    unsorted_ = false;
+    pending_cliff_count_ = 0;
+    if (n <= kInitSmall && G <= kInitSmall) {
+      InitSmall<W> in{};
+      in.n = (uint32_t)n;
+      in.G = G;
+      for (uint64_t i = 0; i < n; ++i) {
+        for (int j = 0; j < W; ++j) in.x[i][j] = hx[j * n + i];
+        in.c[i] = hc[i];
+      }
+      for (uint32_t q = 0; q < G; ++q) {
+        for (int j = 0; j < W; ++j) in.z[q][j] = gz[q * W + j];
+        in.off[q] = goff[q];
+        in.cnt[q] = gcnt[q];
+        in.flags[q] = gfl[q];
+        in.gmax[q] = gmx[q];
+        in.gmin[q] = gmn[q];
+      }
+      k_init_small<W><<<1, 32, 0, stream_>>>(aview(0), gview(0), in, d_stats_);
+      ++launches_;
+      PP_CUDA(cudaGetLastError());
+      n_small_init_ = true;
+    } else {
+      n_small_init_ = false;
+    }
+    if (n && !n_small_init_) {
       ArenaView<W> a = aview(0);
       for (int j = 0; j < W; ++j)
         PP_CUDA(cudaMemcpyAsync(a.x[j], hx.data() + j * n, n * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemcpyAsync(a.c, hc.data(), n * 8, cudaMemcpyHostToDevice, stream_));
     }
-    if (G) {
+    if (G && !n_small_init_) {
       GroupView<W> g = gview(0);
       std::vector<uint64_t> zt(G);
       for (int j = 0; j < W; ++j) {
@@ -445,8 +543,10 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(cudaMemcpyAsync(g.flags, gfl.data(), G * 4, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemsetAsync(g.stamp, 0xff, G * 4, stream_));
     }
-    reset_stats(n);
-    PP_CUDA(cudaStreamSynchronize(stream_));
+    if (!n_small_init_) {
+      reset_stats(n);
+      PP_CUDA(cudaStreamSynchronize(stream_));
+    }
     bump_ = bump_bound_ = n;
     live_ = live_bound_ = n;
     dirty_ = false;
@@ -1666,6 +1766,14 @@ class EngineImpl final : public EngineBase {
       free_events_.pop_back();
       return e;
     }
+    {
+      std::lock_guard<std::mutex> lk(g_streams_mu);
+      if (!g_event_pairs.empty()) {
+        auto e = g_event_pairs.back();
+        g_event_pairs.pop_back();
+        return e;
+      }
+    }
     std::pair<cudaEvent_t, cudaEvent_t> e;
     PP_CUDA(cudaEventCreate(&e.first));
     PP_CUDA(cudaEventCreate(&e.second));
@@ -2027,6 +2135,7 @@ class EngineImpl final : public EngineBase {
   ZZRunProducer<W> zz_prod_{};
   bool zz_ok_ = false;
   cudaEvent_t ev_sync_ = nullptr;
+  bool n_small_init_ = false;
   bool g_pending_ = false;        // G_ is an upper bound; the exact count is st->G_dev
   bool defer_ok_ = true;          // PP_NO_DEFER turns the deferred regroup off (test hook)
   size_t pending_cliff_count_ = 0;

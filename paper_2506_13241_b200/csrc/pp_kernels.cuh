@@ -132,6 +132,20 @@ __global__ void k_set_scalars(DevStats* st, unsigned int G, unsigned long long c
   clear_red(&st->red[2]);  // the host-sync slot (only sync_state's k_reduce fills it)
 }
 
+// set_initial for a handful of terms (the usual single observable string):
+// everything travels as kernel parameters, no copies and no round trip.
+constexpr uint32_t kInitSmall = 4;
+template <int W>
+struct InitSmall {
+  uint32_t n, G;
+  uint64_t x[kInitSmall][W];
+  double c[kInitSmall];
+  uint64_t z[kInitSmall][W];
+  uint64_t off[kInitSmall];
+  uint32_t cnt[kInitSmall], flags[kInitSmall];
+  double gmax[kInitSmall], gmin[kInitSmall];
+};
+
 // Reset of one reduction slot (cumulative counters and sticky errors stay).
 __global__ void k_red_reset(RedSlot* r) { clear_red(r); }
 
