@@ -374,7 +374,7 @@ class EngineImpl final : public EngineBase {
       LaunchSetup& ls = g_setup[{cfg.device, W}];
       if (!ls.sub_grid) {
         PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)branch_smem_bytes<W>()));
+                                     (int)branch_x_smem_bytes<W>()));
         PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)branch_smem_bytes<W>()));
         PP_CUDA(cudaFuncSetAttribute(k_sort_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -389,7 +389,7 @@ class EngineImpl final : public EngineBase {
         PP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
         PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_branch_zz<W>, kCta, sizeof(ZzSmem<W>)));
         // persistent branch grids: every resident CTA slot of the device
-        PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_branch_x<W>, kCta, branch_smem_bytes<W>()));
+        PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_branch_x<W>, kCta, branch_x_smem_bytes<W>()));
         PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_branch_sublayer<W>, kCta,
                                                               branch_smem_bytes<W>()));
         ls.zz_grid = (uint32_t)(sms * std::max(occ, 1));
@@ -960,7 +960,7 @@ class EngineImpl final : public EngineBase {
   }
 
   void launch_branch(const RxParam& p, uint32_t rel, bool lazy) {
-    k_branch_x<W><<<branch_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+    k_branch_x<W><<<branch_grid_, kCta, branch_x_smem_bytes<W>(), stream_>>>(
         gview(gcur_), aview(cur_), p.wq, p.mq, p.cosv, p.sinv, keep_zeros_, gview(gcur_).z[p.wq],
         &d_stats_->work[rel & 1], &d_stats_->work[(rel + 1) & 1], rel, d_stats_,
         lazy ? thr_.as<double>() : nullptr, lazy ? &d_stats_->red[rel & 1] : nullptr);

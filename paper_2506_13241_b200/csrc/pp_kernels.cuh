@@ -2169,11 +2169,15 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
 }
 
+// k_branch_x: the segment / stream buffers of the per-gate path
+template <int W>
+constexpr size_t branch_x_smem_bytes() {
+  return sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
+}
+// k_branch_sublayer: those, or the dense tile and its tables, whichever is larger
 template <int W>
 constexpr size_t branch_smem_bytes() {
-  // the segment / stream buffers of the per-gate path, or the dense tile and
-  // its tables, whichever is larger
-  constexpr size_t a = sizeof(BranchSmem<W>) > sizeof(SegSmem<W>) ? sizeof(BranchSmem<W>) : sizeof(SegSmem<W>);
+  constexpr size_t a = branch_x_smem_bytes<W>();
   constexpr size_t d = kDenseSmem * sizeof(double) + sizeof(DenseTail<W>);
   return a > d ? a : d;
 }
