@@ -742,6 +742,10 @@ class EngineImpl final : public EngineBase {
     ensure_sorted();  // the per-gate kernels pair strings by x order
     // speculative fused run for epsilon0 > 0 (exact, but two passes per run on
     // these workloads: opt-in until the first prediction is right more often)
+    // epsilon0 > 0 at per-gate cadence: the whole run in one launch with
+    // predicted thresholds (verified bit-exactly, rolled back otherwise),
+    // opt-in (PP_SPECULATE): under truncation the dense blocks of a run are
+    // far larger than what survives, so the per-gate launches win here
     const bool speculate = std::getenv("PP_SPECULATE") != nullptr;
     if (speculate && no_budget && do_trunc && !external() && cfg_.epsilon0 > 0.0 && count <= (size_t)kMaxSubGates &&
         G_ && !(cfg_.flags & PP_FLAG_PROFILE) && run_rx_speculative(prm, seq0, t0))
@@ -810,15 +814,10 @@ class EngineImpl final : public EngineBase {
   // predicted thresholds, verified bit-exactly against epsilon0 * gmax_k.
   bool run_rx_speculative(const std::vector<RxParam>& prm, uint64_t seq0, Clock::time_point t0) {
     const size_t count = prm.size();
-    SubGates sgates{};
-    sgates.ng = (int)count;
-    for (size_t i = 0; i < count; ++i) {
-      sgates.wq[i] = (int8_t)prm[i].wq;
-      sgates.mq[i] = prm[i].mq;
-      sgates.cosv[i] = prm[i].cosv;
-      sgates.sinv[i] = prm[i].sinv;
-      sgates.any[prm[i].wq] |= prm[i].mq;
-    }
+    SubGates sgates = rx_sg_;  // the cached descriptor of this run (run_rx)
+    sgates.dense = rx_distinct_ && !keep_zeros_ && !may_hold_zeros_ && !no_dense_;
+    sgates.maxk = dense_maxk_;
+    sgates.sorted = unsorted_ ? 0 : 1;
     sync_state();
     std::vector<double> tpred(count, cfg_.epsilon0 * gmax_);
     spec_buf_.ensure(count * 16 + 64);

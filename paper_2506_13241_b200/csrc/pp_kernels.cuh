@@ -1314,6 +1314,13 @@ struct DenseCtl {
   unsigned long long dst;
   uint32_t fail;
   uint32_t next;                // class discovery: first unmatched string
+  // speculative truncation (epsilon0 > 0, per-gate cadence; tpred != nullptr)
+  const double* tpred;          // predicted threshold per gate (shared copy), nullptr: none
+  unsigned long long* smax;     // per-CTA max |c| after each gate's apply (bits)
+  int ng;
+  double tin;                   // threshold of the gates before the first stage (-1: none)
+  double strunc[kMaxSubGates];  // threshold of the window after stage s (its gate .. the next stage's)
+  unsigned long long wmax[2][kWarps];  // per-warp stage max, by stage parity
   uint32_t zeros;               // multi-class: zero points written (holes to compact)
 };
 
@@ -1365,24 +1372,75 @@ __device__ __forceinline__ void dense_bfly(double& a, double& b, double cosv, do
 
 // butterflies of stages [j0, j1) over a tile of 2^u doubles in shared memory;
 // P: the b bits of the tile (stage bit p is tile bit popc(P & (2^p - 1)))
+// max |c| of a group after gate k's apply was M: gate k and the following
+// gates up to `next` (which do not touch the group; their truncations apply
+// to it) see M until a threshold empties the group (engine.cpp:318-351 per
+// gate; the old path's `contribute`).
 template <int W>
-__device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, int j0, int j1, const DenseCtl<W>& dc,
-                                             unsigned long long& records, unsigned long long& removed,
-                                             uint32_t count = 0) {
-  // count: points in the tile (a multiple of 2^(p+1) for every stage), default 2^u
-  const uint32_t half = (count ? count : (1u << u)) >> 1;
-  for (int j = j0; j < j1; ++j) {
-    const uint32_t p = __popc(P & ((1u << dc.sbit[j]) - 1u));
-    const double cosv = dc.scos[j], sinv = dc.ssin[j], nsin = -sinv;
-    const uint32_t lo = (1u << p) - 1u;
-    for (uint32_t t = threadIdx.x; t < half; t += kCta) {
-      const uint32_t b0 = ((t & ~lo) << 1) | (t & lo);
-      dense_bfly(d[b0], d[b0 | (1u << p)], cosv, sinv, nsin, records, removed);
-    }
-    __syncthreads();
+__device__ __forceinline__ void dense_contribute(const DenseCtl<W>& dc, int k, int next, double M) {
+  if (!(M > 0.0)) return;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(M);
+  atomicMax(&dc.smax[k], bits);
+  for (int jj = k + 1; jj < next; ++jj) {
+    if (M <= dc.tpred[jj - 1]) break;
+    atomicMax(&dc.smax[jj], bits);
   }
 }
 
+template <int W, bool SPEC>
+__device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P, int j0, int j1, DenseCtl<W>& dc,
+                                               unsigned long long& records, unsigned long long& removed,
+                                               uint32_t count) {
+  // count: points in the tile (a multiple of 2^(p+1) for every stage), default 2^u
+  const uint32_t half = (count ? count : (1u << u)) >> 1;
+  constexpr bool spec = SPEC;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = j0; j < j1; ++j) {
+    const uint32_t p = __popc(P & ((1u << dc.sbit[j]) - 1u));
+    const double cosv = dc.scos[j], sinv = dc.ssin[j], nsin = -sinv;
+    // speculative mode: the inputs carry the truncations of the previous
+    // stage's window; the outputs' max feeds this gate's gmax
+    const double tprev = (spec && j > 0) ? dc.strunc[j - 1] : -1.0;
+    const uint32_t lo = (1u << p) - 1u;
+    double mx = 0.0;
+    for (uint32_t t = threadIdx.x; t < half; t += kCta) {
+      const uint32_t b0 = ((t & ~lo) << 1) | (t & lo);
+      double a = d[b0], b = d[b0 | (1u << p)];
+      if (tprev >= 0.0) {
+        if (a != 0.0 && fabs(a) <= tprev) {  // remove_below: |c| <= T
+          a = 0.0;
+          ++removed;
+        }
+        if (b != 0.0 && fabs(b) <= tprev) {
+          b = 0.0;
+          ++removed;
+        }
+      }
+      dense_bfly(a, b, cosv, sinv, nsin, records, removed);
+      if (spec) mx = fmax(mx, fmax(fabs(a), fabs(b)));
+      d[b0] = a;
+      d[b0 | (1u << p)] = b;
+    }
+    if (spec) {
+      mx = __longlong_as_double((long long)warp_max_bits((unsigned long long)__double_as_longlong(mx)));
+      if (lane == 0) dc.wmax[j & 1][warp] = (unsigned long long)__double_as_longlong(mx);
+    }
+    __syncthreads();
+    if (spec && threadIdx.x == 0) {
+      unsigned long long m = 0;
+      for (uint32_t w = 0; w < kWarps; ++w) m = dc.wmax[j & 1][w] > m ? dc.wmax[j & 1][w] : m;
+      dense_contribute<W>(dc, dc.sgate[j], j + 1 < dc.m ? dc.sgate[j + 1] : dc.ng, __longlong_as_double((long long)m));
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, int j0, int j1, DenseCtl<W>& dc,
+                                             unsigned long long& records, unsigned long long& removed,
+                                             uint32_t count = 0) {
+  if (dc.tpred) dense_stages_t<W, true>(d, u, P, j0, j1, dc, records, removed, count);
+  else dense_stages_t<W, false>(d, u, P, j0, j1, dc, records, removed, count);
+}
 
 // Stages of a block of S > kDenseSmem points in global memory (L2): passes
 // of up to kDenseSmemLog stages, each over full shared-memory tiles (the
@@ -1504,7 +1562,12 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     return tl.hcls[h];
   };
   // point (i, b) -> its rank and x; value written there
+  const bool spec = dc.tpred != nullptr;
   auto emit = [&](uint32_t i, uint32_t b, double v) {
+    if (spec && v != 0.0 && fabs(v) <= dc.strunc[m - 1]) {  // the last window's truncation
+      v = 0.0;
+      ++removed;
+    }
     uint32_t r = b + tl.C[i];
     for (uint32_t mk = tl.lmask[i]; mk; mk &= mk - 1) {
       const uint32_t t = __ffs(mk) - 1;
@@ -1535,7 +1598,14 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       for (uint32_t i = tid; i < n; i += kCta) {
         const Plane<W> x = load_plane<W>(ar.x, src + i);
         const uint32_t c = class_of(x);
-        if (c >= c0 && c < c1) dbuf[(c - c0) * S + dense_pext<W>(x, T)] = ar.c[src + i];
+        if (c >= c0 && c < c1) {
+          const double v = ar.c[src + i];
+          if (spec && v != 0.0 && fabs(v) <= dc.tin) {
+            ++removed;
+            continue;
+          }
+          dbuf[(c - c0) * S + dense_pext<W>(x, T)] = v;
+        }
       }
       __syncthreads();
       dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed, cnt);
@@ -1549,7 +1619,14 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       __syncthreads();
       for (uint32_t i = tid; i < n; i += kCta) {
         const Plane<W> x = load_plane<W>(ar.x, src + i);
-        if (class_of(x) == ci) blk[dense_pext<W>(x, T)] = ar.c[src + i];
+        if (class_of(x) == ci) {
+          const double v = ar.c[src + i];
+          if (spec && v != 0.0 && fabs(v) <= dc.tin) {
+            ++removed;
+            continue;
+          }
+          blk[dense_pext<W>(x, T)] = v;
+        }
       }
       __syncthreads();
       dense_passes<W>(dbuf, blk, S, dc, records, removed);
@@ -1674,6 +1751,29 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   const int m = dc.m;
   if (m == 0 || m > kDenseMaxLog) return 0;
   const Plane<W> T = dc.T;
+  const bool spec = dc.tpred != nullptr;
+  if (spec) {
+    // truncation windows: after stage s, the gates from its own to the next
+    // stage's (exclusive); before stage 0, the gates from k0 to its
+    if (tid < (uint32_t)m) {
+      const int k = dc.sgate[tid], next = (int)tid + 1 < m ? dc.sgate[tid + 1] : dc.ng;
+      double t = -1.0;
+      for (int jj = k; jj < next; ++jj) t = fmax(t, dc.tpred[jj]);
+      dc.strunc[tid] = t;
+    }
+    if (tid == 0) {
+      double t = -1.0;
+      const int first = dc.sgate[0];
+      const double M = g.gmax[gid];  // the group held its values through those gates
+      for (int jj = k0; jj < first; ++jj) {
+        t = fmax(t, dc.tpred[jj]);
+        if (M > 0.0) atomicMax(&dc.smax[jj], (unsigned long long)__double_as_longlong(M));
+        if (M <= dc.tpred[jj]) break;  // emptied: later gates see nothing (t already covers M)
+      }
+      dc.tin = t;
+    }
+    __syncthreads();
+  }
   // x classes (the distinct x parts F outside T): a shared-memory hash set
   // keyed by a fingerprint of F, verified against the stored F afterwards
   // (a fingerprint collision sends the group to the per-gate path)
@@ -1764,7 +1864,7 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   uint32_t nonfinite = 0;
   uint32_t out = 0;
   bool done = false;
-  if (n == 1) {
+  if (n == 1 && !spec) {
     // One string: output point b is the input coefficient times one factor
     // per stage -- cos where b keeps the string's bit, the signed sin where it
     // flips it (+sin from a Z, -sin from a Y) -- multiplied in gate order,
@@ -1841,7 +1941,14 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     double* blk = in_smem ? dbuf : ar.c + dst;  // the dense block
     for (uint32_t i = tid; i < S; i += kCta) blk[i] = 0.0;
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += kCta) blk[dense_pext<W>(load_plane<W>(ar.x, src + i), T)] = ar.c[src + i];
+    for (uint32_t i = tid; i < n; i += kCta) {
+      const double c = ar.c[src + i];
+      if (spec && c != 0.0 && fabs(c) <= dc.tin) {  // truncated before the first stage
+        ++removed;
+        continue;
+      }
+      blk[dense_pext<W>(load_plane<W>(ar.x, src + i), T)] = c;
+    }
     __syncthreads();
     if (in_smem) {
       dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed);
@@ -1861,6 +1968,10 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       for (uint32_t e = 0; e < kPer; ++e) {  // striped: slot e covers [base + e kCta, base + (e+1) kCta)
         const uint32_t b = base + e * kCta + tid;
         v[e] = b < S ? blk[b] : 0.0;
+        if (spec && v[e] != 0.0 && fabs(v[e]) <= dc.strunc[m - 1]) {  // the last window's truncation
+          v[e] = 0.0;
+          ++removed;
+        }
       }
   #pragma unroll
       for (uint32_t e = 0; e < kPer; ++e) {
@@ -1954,7 +2065,15 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
     s_gp.cosv[k] = gates.cosv[k];
     s_gp.sinv[k] = gates.sinv[k];
   }
-  if (tid == 0) s_gp.ng = gates.ng;
+  __shared__ double s_tpred[kMaxSubGates];
+  if (tpred)
+    for (int k = tid; k < gates.ng; k += kCta) s_tpred[k] = tpred[k];
+  if (tid == 0) {
+    s_gp.ng = gates.ng;
+    dc.tpred = tpred ? s_tpred : nullptr;
+    dc.smax = smax;
+    dc.ng = gates.ng;
+  }
   __syncthreads();
   unsigned long long aff_elems = 0;
   bool failed = false;
@@ -2026,7 +2145,7 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
       if ((tid & 31) == 0 && tid < kMaxSubGates) s_touch[tid >> 5] = b;
       __syncthreads();
     }
-    if (!spec && gates.dense) {
+    if (gates.dense) {
       const int r = dense_group<W>(reinterpret_cast<double*>(smem_raw), dc, gs, tscan, g, ar, gates, s_gp, gid, n, src, k0,
                                    s_touch, seq0, cap, st, aff_elems);
       if (r < 0) {

@@ -245,10 +245,14 @@ def test_fusion_matches_unfused(pp, O):
             assert x[k] == y[k], (k, x, y)
 
 
-def test_speculative_sublayer_is_exact(pp, O, monkeypatch):
-    # the opt-in fused run for epsilon0 > 0 (predicted thresholds, verified and
-    # rolled back on mismatch) must give the per-gate result bit for bit
+@pytest.mark.parametrize("mode", ["dense", "per_gate_groups"])
+def test_speculative_sublayer_is_exact(pp, O, monkeypatch, mode):
+    # the fused run for epsilon0 > 0 (predicted thresholds, verified and
+    # rolled back on mismatch; dense groups truncate inside the butterfly
+    # network) must give the per-gate result bit for bit
     monkeypatch.setenv("PP_SPECULATE", "1")
+    if mode == "per_gate_groups":
+        monkeypatch.setenv("PP_NO_DENSE", "1")
     geom = pp.heavy_hex_127()
     for thx, eps in (("0.25pi", 1e-4), (0.3, 1e-5)):
         circ = _kicked(pp, geom, thx, 6)
@@ -261,6 +265,7 @@ def test_deferred_truncation_is_exact(pp, O, monkeypatch, mode):
     epsilon0 > 0) equals the eager per-gate compaction and the oracle: string
     sets, coefficient bits, records and removed counts per layer, also when
     the arena overflows mid-run and the run resumes (PP_TIGHT_ARENA)."""
+    monkeypatch.delenv("PP_SPECULATE", raising=False)  # the per-gate launches
     if mode == "eager":
         monkeypatch.setenv("PP_EAGER_TRUNCATION", "1")
     if mode == "deferred_tight":
