@@ -1903,6 +1903,38 @@ class EngineImpl final : public EngineBase {
     const uint64_t live = live_;
     if (G_ == 0 || live == 0) return;
     mem_report("regroup maxrec", maxrec);
+    if (!sort && defer_ok_ && P::kMaxRec == 1 && live <= kSmallRegroupMax) {
+      // a small store feeding a dense Rx run: the whole regroup in one CTA,
+      // sizes committed on the device (no round trip, as below)
+      uint32_t tc = 1024;
+      while (tc < live + live / 2) tc <<= 1;
+      const size_t smem = small_regroup_smem<W>(tc, (uint32_t)live);
+      static bool attr_set = false;  // per producer type
+      if (!attr_set) {
+        PP_CUDA(cudaFuncSetAttribute(k_regroup_small<W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)small_regroup_smem<W>(4096, kSmallRegroupMax)));
+        attr_set = true;
+      }
+      const int o = 1 - cur_;
+      ensure_groups(1 - gcur_, std::max<uint32_t>((uint32_t)live, 1024));
+      ensure_arena(o, std::max<uint64_t>(regroup_arena(live), std::min<uint64_t>(arena_[cur_].cap, arena_max_)));
+      reset_stats(bump_);
+      k_regroup_small<W, P><<<1, kSmallRegroupThreads, smem, stream_>>>(gview(gcur_), G_, aview(cur_), prod,
+                                                                       gview(1 - gcur_), aview(o), (uint32_t)live,
+                                                                       tc, d_stats_);
+      ++launches_;
+      PP_CUDA(cudaGetLastError());
+      cur_ = o;
+      gcur_ = 1 - gcur_;
+      G_ = (uint32_t)live;  // upper bound until the sync
+      g_pending_ = true;
+      unsorted_ = true;
+      bump_ = bump_bound_ = live;
+      live_ = live_bound_ = live;
+      h_records_ = 0;
+      dirty_ = true;
+      return;
+    }
     const uint64_t max_items = (uint64_t)G_ + live / kItem + 1;
     items_.ensure(max_items * sizeof(Item));
     rec_slot_.ensure(live * maxrec * 4);

@@ -1052,6 +1052,188 @@ __global__ void __launch_bounds__(kCta) k_scan_pair_small(const uint32_t* in, ui
   if (tid == 0) st->scan_total = ct;
 }
 
+// Whole regroup of a small store in one CTA (a Clifford run feeding a dense
+// Rx run: no x order needed).  Strings are mapped by the producer, grouped by
+// their new z in a shared-memory hash table (open addressing, a state word per
+// slot: empty / being written / ready), counted, given group ids and offsets
+// by two block scans in slot order, scattered into the target arena, and the
+// new table is filled (statistics by a warp per group, kFlagUnsorted).  The
+// device takes the new group count and bump pointer (as k_regroup_commit).
+constexpr uint32_t kSmallRegroupThreads = 1024;
+constexpr uint32_t kSmallRegroupMax = 1024;  // strings: larger stores run faster through the multi-CTA pipeline
+template <int W>
+constexpr size_t small_regroup_smem(uint32_t tc, uint32_t n) {
+  // table (key, state, count, offset per slot), slot per string, group prefix
+  return (size_t)tc * (12 + 8 * W) + (size_t)n * 2 + 16 + (size_t)(n + 1) * 4 + 64;
+}
+
+template <int W, class P>
+__global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupView<W> gi, uint32_t Gi, ArenaView<W> ai,
+                                                                        P prod, GroupView<W> go, ArenaView<W> ao,
+                                                                        uint32_t n, uint32_t tc, DevStats* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* key = reinterpret_cast<uint64_t*>(smem_raw);         // [W][tc]
+  uint32_t* state = reinterpret_cast<uint32_t*>(key + W * tc);   // 0 empty, 1 writing, 2 ready; later: cursor
+  uint32_t* cnt = state + tc;
+  uint32_t* off = cnt + tc;
+  uint16_t* slot = reinterpret_cast<uint16_t*>(off + tc);        // per string, in flattened order
+  uint32_t* gpre = reinterpret_cast<uint32_t*>(slot + ((n + 7) & ~7u));  // input group prefix (Gi + 1; Gi <= n)
+  __shared__ uint32_t scr[40];
+  __shared__ unsigned long long s_rec;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kSmallRegroupThreads / 32;
+  for (uint32_t h = tid; h < tc; h += kSmallRegroupThreads) {
+    state[h] = 0;
+    cnt[h] = 0;
+  }
+  if (tid == 0) s_rec = 0;
+  __syncthreads();
+  // input group prefix (strings flattened in group order)
+  {
+    constexpr uint32_t kG = (kSmallRegroupMax + kSmallRegroupThreads - 1) / kSmallRegroupThreads;
+    uint32_t c[kG], sum = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < kG; ++e) {
+      const uint32_t q = tid * kG + e;
+      c[e] = q < Gi ? gi.cnt[q] : 0u;
+      sum += c[e];
+    }
+    uint32_t tot;
+    uint32_t p = block_excl_scan(sum, scr, &tot);
+#pragma unroll
+    for (uint32_t e = 0; e < kG; ++e) {
+      const uint32_t q = tid * kG + e;
+      if (q < Gi) gpre[q] = p;
+      p += c[e];
+    }
+    if (tid == 0) gpre[Gi] = tot;
+  }
+  __syncthreads();
+  auto group_of = [&](uint32_t i) -> uint32_t {  // last group with gpre <= i
+    uint32_t lo = 0, hi = Gi;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (gpre[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  };
+  // map + insert, a thread per string
+  unsigned long long rec = 0;
+  for (uint32_t i = tid; i < n; i += kSmallRegroupThreads) {
+    const uint32_t gg = group_of(i);
+    const uint64_t a = gi.off[gg] + (i - gpre[gg]);
+    Plane<W> z;
+#pragma unroll
+    for (int k = 0; k < W; ++k) z.w[k] = gi.z[k][gg];
+    Record<W> r;
+    uint32_t nrec = 0;
+    prod.emit(load_plane<W>(ai.x, a), z, ai.c[a], &r, &nrec);
+    rec += nrec;
+    uint32_t h = (uint32_t)(plane_hash<W>(r.z, 0x5eedull) >> 40) & (tc - 1);
+    for (;;) {
+      const uint32_t sv = atomicCAS(&state[h], 0u, 1u);
+      if (sv == 0u) {
+#pragma unroll
+        for (int k = 0; k < W; ++k) key[k * tc + h] = r.z.w[k];
+        __threadfence_block();
+        atomicExch(&state[h], 2u);
+        break;
+      }
+      while (*(volatile uint32_t*)&state[h] != 2u) {
+      }
+      bool eq = true;
+#pragma unroll
+      for (int k = 0; k < W; ++k) eq &= *(volatile uint64_t*)&key[k * tc + h] == r.z.w[k];
+      if (eq) break;
+      h = (h + 1) & (tc - 1);
+    }
+    atomicAdd(&cnt[h], 1u);
+    slot[i] = (uint16_t)h;
+  }
+  rec = warp_sum64(rec);
+  if (lane == 0 && rec) atomicAdd(&s_rec, rec);
+  __syncthreads();
+  // group ids and offsets in slot order
+  constexpr uint32_t kPerT = 4;  // tc <= kPerT * threads
+  uint32_t used = 0, sum = 0;
+#pragma unroll
+  for (uint32_t e = 0; e < kPerT; ++e) {
+    const uint32_t h = tid * kPerT + e;
+    if (h < tc) {
+      used += state[h] == 2u;
+      sum += cnt[h];
+    }
+  }
+  uint32_t G, total;
+  uint32_t gid = block_excl_scan(used, scr, &G);
+  uint32_t o = block_excl_scan(sum, scr, &total);
+#pragma unroll
+  for (uint32_t e = 0; e < kPerT; ++e) {
+    const uint32_t h = tid * kPerT + e;
+    if (h < tc && state[h] == 2u) {
+      go.off[gid] = o;
+      go.cnt[gid] = cnt[h];
+      go.cap[gid] = cnt[h];
+#pragma unroll
+      for (int k = 0; k < W; ++k) go.z[k][gid] = key[k * tc + h];
+      go.stamp[gid] = 0xffffffffu;
+      off[h] = o;
+      cnt[h] = gid;  // slot -> group id from here on
+      o += go.cnt[gid];
+      ++gid;
+    }
+  }
+  __syncthreads();
+  for (uint32_t h = tid; h < tc; h += kSmallRegroupThreads) state[h] = 0;  // cursors
+  __syncthreads();
+  // scatter (recomputing the producer's record; order inside a group is free)
+  for (uint32_t i = tid; i < n; i += kSmallRegroupThreads) {
+    const uint32_t gg = group_of(i);
+    const uint64_t a = gi.off[gg] + (i - gpre[gg]);
+    Plane<W> z;
+#pragma unroll
+    for (int k = 0; k < W; ++k) z.w[k] = gi.z[k][gg];
+    Record<W> r;
+    uint32_t nrec = 0;
+    prod.emit(load_plane<W>(ai.x, a), z, ai.c[a], &r, &nrec);
+    const uint32_t h = slot[i];
+    const uint64_t d = off[h] + atomicAdd(&state[h], 1u);
+    store_plane<W>(ao.x, d, r.x);
+    ao.c[d] = r.c;
+  }
+  __syncthreads();
+  // statistics, a warp per new group
+  for (uint32_t q = warp; q < G; q += nw) {
+    const uint64_t go_ = go.off[q];
+    const uint32_t nq = go.cnt[q];
+    unsigned long long gx = 0ull, gn = 0x7ff0000000000000ull;
+    uint32_t nf = 0;
+    for (uint32_t j = lane; j < nq; j += 32) {
+      const unsigned long long ab = (unsigned long long)__double_as_longlong(ao.c[go_ + j]) & 0x7fffffffffffffffull;
+      if (ab >= 0x7ff0000000000000ull) nf = 1;
+      if (ab <= 0x7ff0000000000000ull) {
+        gx = ab > gx ? ab : gx;
+        gn = ab < gn ? ab : gn;
+      }
+    }
+    gx = warp_max_bits(gx);
+    gn = warp_min_bits(gn);
+    nf = __any_sync(0xffffffffu, nf);
+    if (lane == 0) {
+      go.gmax[q] = nq ? __longlong_as_double((long long)gx) : 0.0;
+      go.gmin[q] = nq ? __longlong_as_double((long long)gn) : __longlong_as_double(0x7ff0000000000000ll);
+      go.flags[q] = nf | kFlagUnsorted;
+    }
+  }
+  if (tid == 0) {
+    st->distinct = G;
+    st->scan_total = total;
+    st->G_dev = G;
+    st->bump = total;
+    st->cliff_records += s_rec;
+  }
+}
+
 // Group statistics of a regroup that skipped the sort (a Clifford run is a
 // signed permutation: no equal keys to combine, no zeros): max / min |c| and
 // the non-finite flag per group, marked unsorted.  Warp per group.
