@@ -1991,7 +1991,7 @@ class EngineImpl final : public EngineBase {
       scan_gid_.ensure(tc * 8);
       scan_off_.ensure(tc * 8);
       if (tc <= kScanPairMax) {
-        k_scan_pair_small<<<1, kCta, 0, stream_>>>(t.count, (uint32_t)tc, scan_gid_.as<unsigned long long>(),
+        k_scan_pair_small<<<1, kScanPairThreads, 0, stream_>>>(t.count, (uint32_t)tc, scan_gid_.as<unsigned long long>(),
                                                    scan_off_.as<unsigned long long>(), d_stats_);
         ++launches_;
       } else {

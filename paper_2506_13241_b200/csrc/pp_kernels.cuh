@@ -1774,65 +1774,68 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     }
     __syncthreads();
   }
-  // x classes (the distinct x parts F outside T): a shared-memory hash set
-  // keyed by a fingerprint of F, verified against the stored F afterwards
-  // (a fingerprint collision sends the group to the per-gate path)
   DenseTail<W>& tl = *reinterpret_cast<DenseTail<W>*>(dbuf + kDenseSmem);
-  for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) tl.hfp[sl] = 0ull;
-  __syncthreads();
-  bool ok = true;
-  for (uint32_t i = tid; i < n; i += kCta) {
-    Plane<W> f = load_plane<W>(ar.x, src + i);
-#pragma unroll
-    for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
-    const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
-    uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
-    for (uint32_t probe = 0;; ++probe, h = (h + 1) & (kDenseSlots - 1)) {
-      if (probe == kDenseSlots) {
-        ok = false;  // more than kDenseSlots classes
-        break;
+  uint32_t K = 1;
+  Plane<W> F = dc.F;  // one string: one class, its x outside T
+  if (n > 1) {
+    // x classes (the distinct x parts F outside T): a shared-memory hash set
+    // keyed by a fingerprint of F, verified against the stored F afterwards
+    // (a fingerprint collision sends the group to the per-gate path)
+    for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) tl.hfp[sl] = 0ull;
+    __syncthreads();
+    bool ok = true;
+    for (uint32_t i = tid; i < n; i += kCta) {
+      Plane<W> f = load_plane<W>(ar.x, src + i);
+  #pragma unroll
+      for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+      const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+      uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+      for (uint32_t probe = 0;; ++probe, h = (h + 1) & (kDenseSlots - 1)) {
+        if (probe == kDenseSlots) {
+          ok = false;  // more than kDenseSlots classes
+          break;
+        }
+        const unsigned long long old = atomicCAS(&tl.hfp[h], 0ull, fp);
+        if (old == 0ull) tl.hF[h] = f;
+        if (old == 0ull || old == fp) break;
       }
-      const unsigned long long old = atomicCAS(&tl.hfp[h], 0ull, fp);
-      if (old == 0ull) tl.hF[h] = f;
-      if (old == 0ull || old == fp) break;
     }
+    __syncthreads();
+    // verify (every string's F equals its slot's), count the classes
+    for (uint32_t i = tid; i < n && ok; i += kCta) {
+      Plane<W> f = load_plane<W>(ar.x, src + i);
+  #pragma unroll
+      for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+      const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+      uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+      while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
+      ok = plane_eq<W>(tl.hF[h], f);
+    }
+    static_assert(kDenseSlots == 2 * kCta, "two hash slots per thread");
+    const bool u0 = tl.hfp[2 * tid] != 0ull, u1 = tl.hfp[2 * tid + 1] != 0ull;
+    if (!__syncthreads_and(ok)) return 0;
+    {
+      const uint32_t pos = block_excl_scan((uint32_t)u0 + (uint32_t)u1, scan, &K);
+      if (u0) tl.used[pos] = (uint16_t)(2 * tid);
+      if (u1) tl.used[pos + u0] = (uint16_t)(2 * tid + 1);
+    }
+    if (K > kDenseMaxK || K > (uint32_t)gates.maxk) return 0;
+    __syncthreads();
+    // classes in ascending F order; class index per slot
+    for (uint32_t c = tid; c < K; c += kCta) {
+      const uint32_t sl = tl.used[c];
+      const Plane<W> f = tl.hF[sl];
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < K; ++j) r += plane_lt<W>(tl.hF[tl.used[j]], f);
+      tl.hcls[sl] = (uint8_t)r;
+      tl.sF[r] = f;
+    }
+    __syncthreads();
+    F = tl.sF[0];
   }
-  __syncthreads();
-  // verify (every string's F equals its slot's), count the classes
-  for (uint32_t i = tid; i < n && ok; i += kCta) {
-    Plane<W> f = load_plane<W>(ar.x, src + i);
-#pragma unroll
-    for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
-    const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
-    uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
-    while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
-    ok = plane_eq<W>(tl.hF[h], f);
-  }
-  static_assert(kDenseSlots == 2 * kCta, "two hash slots per thread");
-  const bool u0 = tl.hfp[2 * tid] != 0ull, u1 = tl.hfp[2 * tid + 1] != 0ull;
-  if (!__syncthreads_and(ok)) return 0;
-  uint32_t K;
-  {
-    const uint32_t pos = block_excl_scan((uint32_t)u0 + (uint32_t)u1, scan, &K);
-    if (u0) tl.used[pos] = (uint16_t)(2 * tid);
-    if (u1) tl.used[pos + u0] = (uint16_t)(2 * tid + 1);
-  }
-  if (K > kDenseMaxK || K > (uint32_t)gates.maxk) return 0;
-  __syncthreads();
-  // classes in ascending F order; class index per slot
-  for (uint32_t c = tid; c < K; c += kCta) {
-    const uint32_t sl = tl.used[c];
-    const Plane<W> f = tl.hF[sl];
-    uint32_t r = 0;
-    for (uint32_t j = 0; j < K; ++j) r += plane_lt<W>(tl.hF[tl.used[j]], f);
-    tl.hcls[sl] = (uint8_t)r;
-    tl.sF[r] = f;
-  }
-  __syncthreads();
-  const Plane<W> F = tl.sF[0];
   // b -> x bits outside F, one table per byte of b
   Plane<W>* xt = tl.xt;
-  for (uint32_t e = tid; e < 3 * 256; e += kCta) {
+  for (uint32_t e = tid; e < (uint32_t)((m + 7) / 8) * 256u; e += kCta) {
     Plane<W> p;
 #pragma unroll
     for (int w = 0; w < W; ++w) p.w[w] = 0;
@@ -1843,6 +1846,12 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
         p.w[q >> 6] |= 1ull << (q & 63);
       }
     xt[e] = p;
+  }
+  if (tid < 3 && tid >= (uint32_t)((m + 7) / 8)) {  // tables past b's bytes: only entry 0 is read
+    Plane<W> z0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) z0.w[w] = 0;
+    xt[256 * tid] = z0;
   }
   __syncthreads();
   if (K > 1) return dense_multi<W>(dbuf, dc, gs, scan, g, ar, gid, n, src, K, seq0, cap, st, aff_elems);
@@ -1883,6 +1892,7 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     uint32_t* cperm = reinterpret_cast<uint32_t*>(tl.hF);
     static_assert(sizeof(DenseTail<1>::hF) >= 3 * 256 * sizeof(uint32_t), "cperm fits the class hash keys");
     for (uint32_t e = tid; e < 3 * 256; e += kCta) {
+      if ((e & 255u) && (e >> 8) >= (uint32_t)((m + 7) / 8)) continue;  // only entry 0 of unused tables
       uint32_t c = 0;
       const uint32_t t0 = 8 * (e >> 8);
       for (int j = 0; j < m; ++j) {

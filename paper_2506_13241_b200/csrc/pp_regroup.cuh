@@ -1027,11 +1027,13 @@ __global__ void __launch_bounds__(kCta) k_sort_big(GroupView<W> g, ArenaView<W> 
 // as values: string offsets) for a small table, in one single-CTA launch:
 // each thread owns a contiguous chunk, one block scan of the chunk sums.
 constexpr uint32_t kScanPairMax = 1u << 16;
-__global__ void __launch_bounds__(kCta) k_scan_pair_small(const uint32_t* in, uint32_t n, unsigned long long* out_flag,
-                                                          unsigned long long* out_cnt, DevStats* st) {
+constexpr uint32_t kScanPairThreads = 1024;
+__global__ void __launch_bounds__(kScanPairThreads) k_scan_pair_small(const uint32_t* in, uint32_t n,
+                                                                      unsigned long long* out_flag,
+                                                                      unsigned long long* out_cnt, DevStats* st) {
   __shared__ uint32_t scr[40];
   const uint32_t tid = threadIdx.x;
-  const uint32_t per = (n + kCta - 1) / kCta;
+  const uint32_t per = (n + kScanPairThreads - 1) / kScanPairThreads;
   const uint32_t b0 = min(n, tid * per), b1 = min(n, b0 + per);
   uint32_t f = 0, c = 0;
   for (uint32_t i = b0; i < b1; ++i) {
