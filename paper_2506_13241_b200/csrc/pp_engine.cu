@@ -923,7 +923,9 @@ class EngineImpl final : public EngineBase {
     push_scalars(sub_seq0_);
     std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
     PP_CUDA(cudaEventRecord(ev.first, stream_));
-    k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+    // persistent grid, but no more CTAs than a few per group (tiny layers)
+    const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(sub_grid_, 4u * G_));
+    k_branch_sublayer<W><<<grid, kCta, branch_smem_bytes<W>(), stream_>>>(
         gview(gcur_), aview(cur_), sub_gates_, keep_zeros_, &d_stats_->work[0], nullptr, nullptr, d_stats_);
     PP_CUDA(cudaEventRecord(ev.second, stream_));
     pending_events_.push_back(ev);
@@ -1566,7 +1568,9 @@ class EngineImpl final : public EngineBase {
       lazy_open_ = false;
     }
     push_scalars(bseq_);
-    if (G_) k_reduce<W><<<reduce_grid(), kCta, 0, stream_>>>(gview(gcur_), d_stats_, &d_stats_->red[2]);
+    if (G_)
+      k_reduce<W><<<std::min<uint32_t>(reduce_grid(), blocks(G_)), kCta, 0, stream_>>>(gview(gcur_), d_stats_,
+                                                                                       &d_stats_->red[2]);
     launches_ += G_ ? 1 : 0;
     if (diag) launch_diag();
     fetch_stats();
@@ -1657,7 +1661,7 @@ class EngineImpl final : public EngineBase {
                                                            rn, d_stats_);
     launches_ += 2;
   }
-  uint32_t reduce_grid() const { return 148u * 4u; }
+  uint32_t reduce_grid() const { return 148u * 4u; }  // fixed: graphs capture it
 
   // ----- Z-type generator (x_J = 0): pairs of z-groups (pp_zz.cuh).  Returns
   // false when a pair could exceed one segment; the caller then regroups.
