@@ -1396,6 +1396,33 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
   constexpr bool spec = SPEC;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int j = j0; j < j1; ++j) {
+    if (!SPEC && j + 1 < j1) {
+      // two stages per pass (radix 4): each thread takes the four points a
+      // pair of stage bits spans through both butterflies in registers --
+      // the same operations in the same order per point, half the shared
+      // memory round trips and barriers
+      const uint32_t p1 = __popc(P & ((1u << dc.sbit[j]) - 1u)), p2 = __popc(P & ((1u << dc.sbit[j + 1]) - 1u));
+      const uint32_t plo = p1 < p2 ? p1 : p2, phi = p1 < p2 ? p2 : p1;
+      const uint32_t m1 = 1u << p1, m2 = 1u << p2;
+      const double c1 = dc.scos[j], s1 = dc.ssin[j], c2 = dc.scos[j + 1], s2 = dc.ssin[j + 1];
+      const uint32_t quarter = half >> 1;
+      for (uint32_t t = threadIdx.x; t < quarter; t += kCta) {
+        uint32_t b = ((t >> plo) << (plo + 1)) | (t & ((1u << plo) - 1u));
+        b = ((b >> phi) << (phi + 1)) | (b & ((1u << phi) - 1u));
+        double a00 = d[b], a10 = d[b | m1], a01 = d[b | m2], a11 = d[b | m1 | m2];
+        dense_bfly(a00, a10, c1, s1, -s1, records, removed);
+        dense_bfly(a01, a11, c1, s1, -s1, records, removed);
+        dense_bfly(a00, a01, c2, s2, -s2, records, removed);
+        dense_bfly(a10, a11, c2, s2, -s2, records, removed);
+        d[b] = a00;
+        d[b | m1] = a10;
+        d[b | m2] = a01;
+        d[b | m1 | m2] = a11;
+      }
+      __syncthreads();
+      ++j;
+      continue;
+    }
     const uint32_t p = __popc(P & ((1u << dc.sbit[j]) - 1u));
     const double cosv = dc.scos[j], sinv = dc.ssin[j], nsin = -sinv;
     // speculative mode: the inputs carry the truncations of the previous
