@@ -2158,7 +2158,9 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
       }
       if (!touched) continue;
       if (lpt) {
-        const bool big = mt >= kDenseSmemLog || ((unsigned long long)n << mt) >= kDenseSmem;
+        // the sweep follows from z alone: the count changes when another CTA
+        // applies the group (it must not move the group to the other sweep)
+        const bool big = mt >= kDenseSmemLog;
         if (big != (idx < G)) continue;
       }
     }
