@@ -335,6 +335,47 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
   const uint64_t off = g.off[it.g] + it.start;
   const Plane<W> z = load_plane<W>(g.z, it.g);
   unsigned long long records = 0;
+  if constexpr (P::kMaxRec == 1) {
+    // one record per string: slot counts aggregated per warp (strings of one
+    // item share their old z, so a warp's records fall into few new groups)
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t i0 = 0; i0 < it.len; i0 += kCta) {
+      const uint32_t i = i0 + threadIdx.x;
+      uint32_t slot_out = 0xffffffffu;
+      if (i < it.len) {
+        Record<W> rec[1];
+        uint32_t nr = 0;
+        const int nrec = prod.emit(load_plane<W>(src.x, off + i), z, src.c[off + i], rec, &nr);
+        records += nr;
+        if (nrec) {
+          const unsigned long long f = z_fingerprint<W>(rec[0].z, seed);
+          unsigned long long sl = f & t.mask;
+          for (unsigned long long probe = 0;; ++probe) {
+            unsigned long long cur = t.fp[sl];
+            if (cur == 0) {
+              cur = atomicCAS(&t.fp[sl], 0ull, f);
+              if (cur == 0) {
+                uint32_t d = atomicAdd(&st->distinct, 1u);
+                if (d >= max_distinct) atomicOr(&st->overflow, 1u);
+                store_plane<W>(t.z, sl, rec[0].z);
+                cur = f;
+              }
+            }
+            if (cur == f) break;
+            sl = (sl + 1) & t.mask;
+            if (probe > t.mask) {
+              atomicOr(&st->overflow, 1u);
+              break;
+            }
+          }
+          slot_out = (uint32_t)sl;
+        }
+        rec_slot[it.rbase + i] = slot_out;
+      }
+      const uint32_t mm = __match_any_sync(0xffffffffu, slot_out);
+      if (slot_out != 0xffffffffu && lane == (uint32_t)(__ffs(mm) - 1)) atomicAdd(&t.count[slot_out], __popc(mm));
+    }
+  } else {
   for (uint32_t i = threadIdx.x; i < it.len; i += kCta) {
     Record<W> rec[P::kMaxRec];
     uint32_t nr = 0;
@@ -369,6 +410,7 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
       }
       rec_slot[it.rbase + (unsigned long long)i * P::kMaxRec + r] = slot_out;
     }
+  }
   }
   records = warp_sum64(records);
   if ((threadIdx.x & 31) == 0 && records) atomicAdd(&st->records, records);
@@ -495,6 +537,34 @@ __global__ void __launch_bounds__(kCta) k_scatter(const Item* items, GroupView<W
   const Item it = items[blockIdx.x];
   const uint64_t off = g.off[it.g] + it.start;
   const Plane<W> z = load_plane<W>(g.z, it.g);
+  if constexpr (P::kMaxRec == 1) {
+    // positions reserved per warp and new group (one atomic per group per warp)
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t i0 = 0; i0 < it.len; i0 += kCta) {
+      const uint32_t i = i0 + threadIdx.x;
+      uint32_t gid = 0xffffffffu;
+      Record<W> rec[1];
+      if (i < it.len) {
+        uint32_t nr;
+        const int nrec = prod.emit(load_plane<W>(src.x, off + i), z, src.c[off + i], rec, &nr);
+        if (nrec) {
+          const uint32_t sl = rec_slot[it.rbase + i];
+          if (!plane_eq<W>(load_plane<W>(t.z, sl), rec[0].z)) atomicOr(&st->collision, 1u);  // fingerprint collision
+          else gid = t.gid[sl];
+        }
+      }
+      const uint32_t mm = __match_any_sync(0xffffffffu, gid);
+      if (gid != 0xffffffffu) {
+        const uint32_t leader = __ffs(mm) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&ng.cnt[gid], (unsigned)__popc(mm));
+        base = __shfl_sync(mm, base, leader);
+        const uint64_t pos = ng.off[gid] + base + __popc(mm & ((1u << lane) - 1u));
+        store_plane<W>(dst.x, pos, rec[0].x);
+        dst.c[pos] = rec[0].c;
+      }
+    }
+  } else {
   for (uint32_t i = threadIdx.x; i < it.len; i += kCta) {
     Record<W> rec[P::kMaxRec];
     uint32_t nr;
@@ -512,6 +582,7 @@ __global__ void __launch_bounds__(kCta) k_scatter(const Item* items, GroupView<W
       store_plane<W>(dst.x, pos, rec[r].x);
       dst.c[pos] = rec[r].c;
     }
+  }
   }
 }
 
