@@ -19,8 +19,11 @@ layer, exactly what the reference's run_circuit does.
            (oracle/_ref), on this box's host cores
 
 ``--impl reference`` times the reference CPU engine on the same workload.
-Under torchrun (N > 1) every rank runs an independent replica (weak
-scaling; the sharded exchange is not built yet -- DESIGN.md section 6).
+Under torchrun (N > 1) the operator is sharded over the ranks by z-plane
+hash (paper_2506_13241_b200/sharded.py): Rx runs are rank-local, strings
+move with one NCCL all-to-all after each Clifford run, scalars (global max,
+counts, <0|O|0>) are all-reduced -- total work fixed, strong scaling
+(DESIGN.md section 6).
 """
 from __future__ import annotations
 

@@ -1928,9 +1928,25 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       }
       cperm[e] = c;
     }
-    if (tid == 0) dbuf[0] = c0;
+    // the first stages (<= 256 products) by warp 0 alone, the rest by the CTA
+    const int Lw = L < 8 ? L : 8;
+    if (tid < 32) {
+      if (tid == 0) dbuf[0] = c0;
+      __syncwarp();
+      for (int j = 0; j < Lw; ++j) {
+        const uint32_t bit = 1u << dc.sbit[j];
+        const double fk = dc.scos[j], ff = (b0 & bit) ? -dc.ssin[j] : dc.ssin[j];  // keep / flip the string's bit
+        const double f0 = (b0 & bit) ? ff : fk, f1 = (b0 & bit) ? fk : ff;           // stage bit 0 / 1
+        for (uint32_t p = tid; p < (1u << j); p += 32) {
+          const double v = dbuf[p];
+          dbuf[p + (1u << j)] = __dmul_rn(v, f1);
+          dbuf[p] = __dmul_rn(v, f0);
+        }
+        __syncwarp();
+      }
+    }
     __syncthreads();
-    for (int j = 0; j < L; ++j) {
+    for (int j = Lw; j < L; ++j) {
       const uint32_t bit = 1u << dc.sbit[j];
       const double fk = dc.scos[j], ff = (b0 & bit) ? -dc.ssin[j] : dc.ssin[j];  // keep / flip the string's bit
       const double f0 = (b0 & bit) ? ff : fk, f1 = (b0 & bit) ? fk : ff;           // stage bit 0 / 1
