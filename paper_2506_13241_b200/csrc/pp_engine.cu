@@ -350,6 +350,10 @@ class EngineBase {
   virtual const uint64_t* device_records() const = 0;
   virtual double norm2() = 0;
   virtual void histogram(int bins, double gmax, double epsilon0, uint64_t* pos, uint64_t* neg) = 0;
+  // engine reuse across pp_create/pp_destroy (simulate() makes one per call)
+  virtual bool reusable() const = 0;
+  virtual void on_reuse() = 0;
+  virtual void poison() = 0;
 };
 
 template <int W>
@@ -427,6 +431,25 @@ class EngineImpl final : public EngineBase {
     release_pinned_stats(h_stats_);
     release_pinned_diag(h_diag_);
   }
+
+  bool reusable() const override {
+    return !poisoned_ && !sub_pending_ && !g_pending_ && !lazy_open_ &&
+           arena_[0].buf.bytes + arena_[1].buf.bytes <= (size_t(4) << 30);
+  }
+  void on_reuse() override {  // set_initial resets the operator; this resets the statistics
+    cudaStreamSynchronize(stream_);
+    for (auto& pr : pending_events_) free_events_.push_back(pr);
+    pending_events_.clear();
+    branch_ms_ = 0.0;
+    branch_bytes_ = 0.0;
+    branch_launches_ = launches_ = 0;
+    branch_in_ = branch_stream_ = 0;
+    dense_groups_ = dense_out_ = 0;
+    tr_layer_ns_ = tr_sync_ns_ = tr_syncs_ = tr_cliff_ns_ = tr_rx_ns_ = 0;
+    set_initial(nullptr, nullptr, 0);  // the empty operator of a fresh engine
+    counters_ = pp_counters{};
+  }
+  void poison() override { poisoned_ = true; }
 
   // ---------------------------------------------------------------- set_initial
   void set_initial(const uint64_t* words, const double* c, size_t count) override {
@@ -2171,6 +2194,7 @@ class EngineImpl final : public EngineBase {
   bool zz_ok_ = false;
   cudaEvent_t ev_sync_ = nullptr;
   bool n_small_init_ = false;
+  bool poisoned_ = false;  // an operation failed: not reused
   bool g_pending_ = false;        // G_ is an upper bound; the exact count is st->G_dev
   bool defer_ok_ = true;          // PP_NO_DEFER turns the deferred regroup off (test hook)
   size_t pending_cliff_count_ = 0;
@@ -2210,7 +2234,37 @@ class EngineImpl final : public EngineBase {
 struct pp_engine {
   std::unique_ptr<ppgpu::EngineBase> impl;
   std::string error;
+  std::string key;  // configuration + construction-time environment (engine pool)
 };
+
+namespace {
+// Released engines are kept (a few, small ones) and handed to the next
+// pp_create with the same configuration: creating an engine costs stream,
+// event and launch-setup work comparable to a small propagation.  The pool
+// is never destroyed (no CUDA calls during process teardown).
+std::mutex g_engine_pool_mu;
+std::vector<std::pair<std::string, ppgpu::EngineBase*>>* g_engine_pool = new std::vector<std::pair<std::string, ppgpu::EngineBase*>>();
+constexpr size_t kEnginePoolMax = 4;
+
+std::string engine_key(const pp_config& c) {
+  std::string k;
+  auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+  put(&c.n, sizeof c.n);
+  put(&c.epsilon0, sizeof c.epsilon0);
+  put(&c.cadence, sizeof c.cadence);
+  put(&c.max_terms, sizeof c.max_terms);
+  put(&c.workers, sizeof c.workers);
+  put(&c.device, sizeof c.device);
+  put(&c.flags, sizeof c.flags);
+  put(&c.mem_fraction, sizeof c.mem_fraction);
+  for (const char* v : {"PP_TIGHT_ARENA", "PP_NO_DENSE", "PP_DENSE_MAXK", "PP_NO_DEFER", "PP_BLOCKING_SYNC", "PP_TRACE"}) {
+    const char* x = std::getenv(v);
+    k += '|';
+    if (x) k += x;
+  }
+  return k;
+}
+}  // namespace
 
 namespace {
 thread_local std::string g_create_error;
@@ -2221,13 +2275,22 @@ int guarded(pp_engine* e, F&& f) {
     f();
     return PP_OK;
   } catch (const ppgpu::EngineError& x) {
-    if (e) e->error = x.what();
+    if (e) {
+      e->error = x.what();
+      if (e->impl) e->impl->poison();
+    }
     return x.code;
   } catch (const std::bad_alloc&) {
-    if (e) e->error = "host memory exhausted";
+    if (e) {
+      e->error = "host memory exhausted";
+      if (e->impl) e->impl->poison();
+    }
     return PP_ERR_RESOURCE;
   } catch (const std::exception& x) {
-    if (e) e->error = x.what();
+    if (e) {
+      e->error = x.what();
+      if (e->impl) e->impl->poison();
+    }
     return PP_ERR_INTERNAL;
   }
 }
@@ -2251,6 +2314,24 @@ int pp_create(const pp_config* config, pp_engine** out) {
     return PP_ERR_INVALID;
   }
   auto e = std::make_unique<pp_engine>();
+  e->key = engine_key(*config);
+  {
+    std::lock_guard<std::mutex> lk(g_engine_pool_mu);
+    for (auto it = g_engine_pool->begin(); it != g_engine_pool->end(); ++it)
+      if (it->first == e->key) {
+        e->impl.reset(it->second);
+        g_engine_pool->erase(it);
+        break;
+      }
+  }
+  if (e->impl) {
+    int rc = guarded(e.get(), [&] { e->impl->on_reuse(); });
+    if (rc == PP_OK) {
+      *out = e.release();
+      return PP_OK;
+    }
+    e->impl.reset();
+  }
   int rc = guarded(e.get(), [&] {
     int ndev = 0;
     cudaError_t err = cudaGetDeviceCount(&ndev);
@@ -2270,7 +2351,22 @@ int pp_create(const pp_config* config, pp_engine** out) {
   return PP_OK;
 }
 
-void pp_destroy(pp_engine* e) { delete e; }
+void pp_destroy(pp_engine* e) {
+  if (!e) return;
+  if (e->impl && e->impl->reusable()) {
+    ppgpu::EngineBase* victim = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_engine_pool_mu);
+      if (g_engine_pool->size() >= kEnginePoolMax) {
+        victim = g_engine_pool->front().second;
+        g_engine_pool->erase(g_engine_pool->begin());
+      }
+      g_engine_pool->emplace_back(e->key, e->impl.release());
+    }
+    delete victim;
+  }
+  delete e;
+}
 
 int pp_set_initial(pp_engine* e, const uint64_t* words, const double* coeffs, size_t count) {
   if (!e) return PP_ERR_INVALID;
