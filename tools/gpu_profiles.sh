@@ -1,4 +1,5 @@
 # round profile refresh: bench lines, reference arm, launch lists, traffic, full captures
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/prof_smoke.log 2>&1; echo "smoke rc=$?"; cat gpurun_out/prof_smoke.log | tail -2
 mkdir -p gpurun_out/prof
 P=gpurun_out/prof
 nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv > $P/gpu.txt
