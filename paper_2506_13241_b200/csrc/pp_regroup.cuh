@@ -1136,8 +1136,9 @@ constexpr uint32_t kSmallRegroupThreads = 1024;
 constexpr uint32_t kSmallRegroupMax = 1024;  // strings: larger stores run faster through the multi-CTA pipeline
 template <int W>
 constexpr size_t small_regroup_smem(uint32_t tc, uint32_t n) {
-  // table (key, state, count, offset per slot), slot per string, group prefix
-  return (size_t)tc * (12 + 8 * W) + (size_t)n * 2 + 16 + (size_t)(n + 1) * 4 + 64;
+  // table (key, state, count, offset, max / min |c| bits, non-finite per
+  // slot), slot per string, group prefix
+  return (size_t)tc * (12 + 8 * W + 16 + 4) + (size_t)n * 2 + 16 + (size_t)(n + 1) * 4 + 64;
 }
 
 template <int W, class P>
@@ -1149,14 +1150,20 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
   uint32_t* state = reinterpret_cast<uint32_t*>(key + W * tc);   // 0 empty, 1 writing, 2 ready; later: cursor
   uint32_t* cnt = state + tc;
   uint32_t* off = cnt + tc;
-  uint16_t* slot = reinterpret_cast<uint16_t*>(off + tc);        // per string, in flattened order
+  unsigned long long* smx = reinterpret_cast<unsigned long long*>(off + tc);  // max |c| bits per slot
+  unsigned long long* smn = smx + tc;                                          // min |c| bits per slot
+  uint32_t* snf = reinterpret_cast<uint32_t*>(smn + tc);                       // non-finite per slot
+  uint16_t* slot = reinterpret_cast<uint16_t*>(snf + tc);        // per string, in flattened order
   uint32_t* gpre = reinterpret_cast<uint32_t*>(slot + ((n + 7) & ~7u));  // input group prefix (Gi + 1; Gi <= n)
   __shared__ uint32_t scr[40];
   __shared__ unsigned long long s_rec;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kSmallRegroupThreads / 32;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
   for (uint32_t h = tid; h < tc; h += kSmallRegroupThreads) {
     state[h] = 0;
     cnt[h] = 0;
+    smx[h] = 0ull;
+    smn[h] = 0x7ff0000000000000ull;
+    snf[h] = 0;
   }
   if (tid == 0) s_rec = 0;
   __syncthreads();
@@ -1222,6 +1229,14 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
     }
     atomicAdd(&cnt[h], 1u);
     slot[i] = (uint16_t)h;
+    // group statistics as the strings arrive (|c| bit patterns order like
+    // the values; NaN takes no part in max / min, like fmax / fmin)
+    const unsigned long long ab = (unsigned long long)__double_as_longlong(r.c) & 0x7fffffffffffffffull;
+    if (ab >= 0x7ff0000000000000ull) snf[h] = 1;
+    if (ab <= 0x7ff0000000000000ull) {
+      atomicMax(&smx[h], ab);
+      atomicMin(&smn[h], ab);
+    }
   }
   rec = warp_sum64(rec);
   if (lane == 0 && rec) atomicAdd(&s_rec, rec);
@@ -1250,6 +1265,9 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
 #pragma unroll
       for (int k = 0; k < W; ++k) go.z[k][gid] = key[k * tc + h];
       go.stamp[gid] = 0xffffffffu;
+      go.gmax[gid] = __longlong_as_double((long long)smx[h]);
+      go.gmin[gid] = __longlong_as_double((long long)smn[h]);
+      go.flags[gid] = snf[h] | kFlagUnsorted;
       off[h] = o;
       cnt[h] = gid;  // slot -> group id from here on
       o += go.cnt[gid];
@@ -1275,29 +1293,6 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
     ao.c[d] = r.c;
   }
   __syncthreads();
-  // statistics, a warp per new group
-  for (uint32_t q = warp; q < G; q += nw) {
-    const uint64_t go_ = go.off[q];
-    const uint32_t nq = go.cnt[q];
-    unsigned long long gx = 0ull, gn = 0x7ff0000000000000ull;
-    uint32_t nf = 0;
-    for (uint32_t j = lane; j < nq; j += 32) {
-      const unsigned long long ab = (unsigned long long)__double_as_longlong(ao.c[go_ + j]) & 0x7fffffffffffffffull;
-      if (ab >= 0x7ff0000000000000ull) nf = 1;
-      if (ab <= 0x7ff0000000000000ull) {
-        gx = ab > gx ? ab : gx;
-        gn = ab < gn ? ab : gn;
-      }
-    }
-    gx = warp_max_bits(gx);
-    gn = warp_min_bits(gn);
-    nf = __any_sync(0xffffffffu, nf);
-    if (lane == 0) {
-      go.gmax[q] = nq ? __longlong_as_double((long long)gx) : 0.0;
-      go.gmin[q] = nq ? __longlong_as_double((long long)gn) : __longlong_as_double(0x7ff0000000000000ll);
-      go.flags[q] = nf | kFlagUnsorted;
-    }
-  }
   if (tid == 0) {
     st->distinct = G;
     st->scan_total = total;
