@@ -437,6 +437,7 @@ class EngineImpl final : public EngineBase {
            arena_[0].buf.bytes + arena_[1].buf.bytes <= (size_t(4) << 30);
   }
   void on_reuse() override {  // set_initial resets the operator; this resets the statistics
+    PP_CUDA(cudaSetDevice(cfg_.device));  // as a fresh engine's constructor does
     cudaStreamSynchronize(stream_);
     for (auto& pr : pending_events_) free_events_.push_back(pr);
     pending_events_.clear();

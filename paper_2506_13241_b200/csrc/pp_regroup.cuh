@@ -1102,27 +1102,45 @@ constexpr uint32_t kScanPairThreads = 1024;
 __global__ void __launch_bounds__(kScanPairThreads) k_scan_pair_small(const uint32_t* in, uint32_t n,
                                                                       unsigned long long* out_flag,
                                                                       unsigned long long* out_cnt, DevStats* st) {
-  __shared__ uint32_t scr[40];
-  const uint32_t tid = threadIdx.x;
-  const uint32_t per = (n + kScanPairThreads - 1) / kScanPairThreads;
-  const uint32_t b0 = min(n, tid * per), b1 = min(n, b0 + per);
+  // a warp per contiguous segment, lanes striped (coalesced): warp totals,
+  // one scan over the 32 warps, then per-chunk warp scans with a carry
+  __shared__ uint32_t wf[32], wc[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t seg = (n + 31) / 32;
+  const uint32_t s0 = min(n, warp * seg), s1 = min(n, s0 + seg);
   uint32_t f = 0, c = 0;
-  for (uint32_t i = b0; i < b1; ++i) {
+  for (uint32_t i = s0 + lane; i < s1; i += 32) {
     const uint32_t v = in[i];
     f += v != 0;
     c += v;
   }
-  uint32_t ft, ct;
-  uint32_t fe = block_excl_scan(f, scr, &ft);
-  uint32_t ce = block_excl_scan(c, scr, &ct);
-  for (uint32_t i = b0; i < b1; ++i) {
-    const uint32_t v = in[i];
-    out_flag[i] = fe;
-    out_cnt[i] = ce;
-    fe += v != 0;
-    ce += v;
+  f = __reduce_add_sync(0xffffffffu, f);
+  c = __reduce_add_sync(0xffffffffu, c);
+  if (lane == 0) {
+    wf[warp] = f;
+    wc[warp] = c;
   }
-  if (tid == 0) st->scan_total = ct;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t a = wf[lane], b = wc[lane];
+    const uint32_t ia = warp_incl_scan(a), ib = warp_incl_scan(b);
+    wf[lane] = ia - a;
+    wc[lane] = ib - b;
+    if (lane == 31) st->scan_total = ib;
+  }
+  __syncthreads();
+  uint32_t bf = wf[warp], bc = wc[warp];
+  for (uint32_t i0 = s0; i0 < s1; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t v = i < s1 ? in[i] : 0u, fv = v != 0;
+    const uint32_t ifl = warp_incl_scan(fv), icn = warp_incl_scan(v);
+    if (i < s1) {
+      out_flag[i] = bf + ifl - fv;
+      out_cnt[i] = bc + icn - v;
+    }
+    bf += __shfl_sync(0xffffffffu, ifl, 31);
+    bc += __shfl_sync(0xffffffffu, icn, 31);
+  }
 }
 
 // Whole regroup of a small store in one CTA (a Clifford run feeding a dense
