@@ -1934,13 +1934,12 @@ class EngineImpl final : public EngineBase {
     if (!sort && defer_ok_ && P::kMaxRec == 1 && live <= kSmallRegroupMax) {
       // a small store feeding a dense Rx run: the whole regroup in one CTA,
       // sizes committed on the device (no round trip, as below)
-      uint32_t tc = 1024;
-      while (tc < live + live / 2) tc <<= 1;
+      const uint32_t tc = small_regroup_tc((uint32_t)live);
       const size_t smem = small_regroup_smem<W>(tc, (uint32_t)live);
       static bool attr_set = false;  // per producer type
       if (!attr_set) {
         PP_CUDA(cudaFuncSetAttribute(k_regroup_small<W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)small_regroup_smem<W>(4096, kSmallRegroupMax)));
+                                     (int)small_regroup_smem<W>(small_regroup_tc(kSmallRegroupMax), kSmallRegroupMax)));
         attr_set = true;
       }
       const int o = 1 - cur_;

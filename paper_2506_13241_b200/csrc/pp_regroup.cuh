@@ -1152,11 +1152,16 @@ __global__ void __launch_bounds__(kScanPairThreads) k_scan_pair_small(const uint
 // device takes the new group count and bump pointer (as k_regroup_commit).
 constexpr uint32_t kSmallRegroupThreads = 1024;
 constexpr uint32_t kSmallRegroupMax = 1024;  // strings: larger stores run faster through the multi-CTA pipeline
+constexpr uint32_t small_regroup_tc(uint32_t n) {  // table slots: load <= 2/3
+  uint32_t tc = 1024;
+  while (tc < n + n / 2) tc <<= 1;
+  return tc;
+}
 template <int W>
 constexpr size_t small_regroup_smem(uint32_t tc, uint32_t n) {
   // table (key, state, count, offset, max / min |c| bits, non-finite per
   // slot), slot per string, group prefix
-  return (size_t)tc * (12 + 8 * W + 16 + 4) + (size_t)n * 2 + 16 + (size_t)(n + 1) * 4 + 64;
+  return (size_t)tc * (8 + 12 + 8 * W + 16 + 4) + (size_t)n * 2 + 16 + (size_t)(n + 1) * 4 + 64;
 }
 
 template <int W, class P>
@@ -1164,8 +1169,9 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
                                                                         P prod, GroupView<W> go, ArenaView<W> ao,
                                                                         uint32_t n, uint32_t tc, DevStats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* key = reinterpret_cast<uint64_t*>(smem_raw);         // [W][tc]
-  uint32_t* state = reinterpret_cast<uint32_t*>(key + W * tc);   // 0 empty, 1 writing, 2 ready; later: cursor
+  unsigned long long* kfp = reinterpret_cast<unsigned long long*>(smem_raw);  // fingerprint of the slot's z (0: empty)
+  uint64_t* key = reinterpret_cast<uint64_t*>(kfp + tc);         // [W][tc] the slot's z
+  uint32_t* state = reinterpret_cast<uint32_t*>(key + W * tc);   // scatter cursor
   uint32_t* cnt = state + tc;
   uint32_t* off = cnt + tc;
   unsigned long long* smx = reinterpret_cast<unsigned long long*>(off + tc);  // max |c| bits per slot
@@ -1177,6 +1183,7 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
   __shared__ unsigned long long s_rec;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   for (uint32_t h = tid; h < tc; h += kSmallRegroupThreads) {
+    kfp[h] = 0ull;
     state[h] = 0;
     cnt[h] = 0;
     smx[h] = 0ull;
@@ -1227,22 +1234,18 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
     uint32_t nrec = 0;
     prod.emit(load_plane<W>(ai.x, a), z, ai.c[a], &r, &nrec);
     rec += nrec;
-    uint32_t h = (uint32_t)(plane_hash<W>(r.z, 0x5eedull) >> 40) & (tc - 1);
+    // slots by a 64-bit fingerprint (no waiting on another thread's key);
+    // the scatter verifies the full z (a collision fails the deferred check)
+    const unsigned long long fp = plane_hash<W>(r.z, 0x5eedull) | 1ull;
+    uint32_t h = (uint32_t)(fp >> 40) & (tc - 1);
     for (;;) {
-      const uint32_t sv = atomicCAS(&state[h], 0u, 1u);
-      if (sv == 0u) {
+      const unsigned long long old = atomicCAS(&kfp[h], 0ull, fp);
+      if (old == 0ull) {
 #pragma unroll
         for (int k = 0; k < W; ++k) key[k * tc + h] = r.z.w[k];
-        __threadfence_block();
-        atomicExch(&state[h], 2u);
         break;
       }
-      while (*(volatile uint32_t*)&state[h] != 2u) {
-      }
-      bool eq = true;
-#pragma unroll
-      for (int k = 0; k < W; ++k) eq &= *(volatile uint64_t*)&key[k * tc + h] == r.z.w[k];
-      if (eq) break;
+      if (old == fp) break;
       h = (h + 1) & (tc - 1);
     }
     atomicAdd(&cnt[h], 1u);
@@ -1266,7 +1269,7 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
   for (uint32_t e = 0; e < kPerT; ++e) {
     const uint32_t h = tid * kPerT + e;
     if (h < tc) {
-      used += state[h] == 2u;
+      used += kfp[h] != 0ull;
       sum += cnt[h];
     }
   }
@@ -1276,7 +1279,7 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
 #pragma unroll
   for (uint32_t e = 0; e < kPerT; ++e) {
     const uint32_t h = tid * kPerT + e;
-    if (h < tc && state[h] == 2u) {
+    if (h < tc && kfp[h] != 0ull) {
       go.off[gid] = o;
       go.cnt[gid] = cnt[h];
       go.cap[gid] = cnt[h];
@@ -1293,7 +1296,7 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
     }
   }
   __syncthreads();
-  for (uint32_t h = tid; h < tc; h += kSmallRegroupThreads) state[h] = 0;  // cursors
+  for (uint32_t h = tid; h < tc; h += kSmallRegroupThreads) state[h] = 0;  // cursors (already zero; kept explicit)
   __syncthreads();
   // scatter (recomputing the producer's record; order inside a group is free)
   for (uint32_t i = tid; i < n; i += kSmallRegroupThreads) {
@@ -1306,6 +1309,10 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
     uint32_t nrec = 0;
     prod.emit(load_plane<W>(ai.x, a), z, ai.c[a], &r, &nrec);
     const uint32_t h = slot[i];
+    bool same = true;
+#pragma unroll
+    for (int k = 0; k < W; ++k) same &= key[k * tc + h] == r.z.w[k];
+    if (!same) atomicOr(&st->collision, 1u);
     const uint64_t d = off[h] + atomicAdd(&state[h], 1u);
     store_plane<W>(ao.x, d, r.x);
     ao.c[d] = r.c;
