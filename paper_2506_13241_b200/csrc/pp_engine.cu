@@ -1558,15 +1558,20 @@ class EngineImpl final : public EngineBase {
     epilogue(cfg_.cadence == PP_CADENCE_GATE, true);
   }
   // the diagonal pass of the readout, folded into a sync's single round trip
-  void launch_diag() {
+  // red != nullptr: the group reduction of sync_state in the same launch
+  void launch_diag(RedSlot* red = nullptr) {
     PP_CUDA(cudaMemsetAsync(&d_stats_->diag_count, 0, sizeof(unsigned long long), stream_));
     diag_copied_ = 0;
     if (!G_) return;
     diag_z_.ensure((size_t)G_ * W * 8);
     diag_c_.ensure((size_t)G_ * 8);
-    k_diag<W><<<blocks(32ull * G_), kCta, 0, stream_>>>(gview(gcur_), g_pending_ ? kKeepG : G_, aview(cur_),
-                                                         diag_z_.as<uint64_t>(),
-                                                 diag_c_.as<double>(), d_stats_);
+    if (red)
+      k_readout<W><<<blocks(32ull * G_), kCta, 0, stream_>>>(gview(gcur_), g_pending_ ? kKeepG : G_, aview(cur_),
+                                                              diag_z_.as<uint64_t>(), diag_c_.as<double>(), d_stats_,
+                                                              red);
+    else
+      k_diag<W><<<blocks(32ull * G_), kCta, 0, stream_>>>(gview(gcur_), g_pending_ ? kKeepG : G_, aview(cur_),
+                                                           diag_z_.as<uint64_t>(), diag_c_.as<double>(), d_stats_);
     ++launches_;
     if (!h_diag_) h_diag_ = pinned_diag();
     diag_copied_ = std::min<uint64_t>(G_, kDiagCap);
@@ -1592,11 +1597,14 @@ class EngineImpl final : public EngineBase {
       lazy_open_ = false;
     }
     push_scalars(bseq_);
-    if (G_)
-      k_reduce<W><<<std::min<uint32_t>(reduce_grid(), blocks(G_)), kCta, 0, stream_>>>(gview(gcur_), d_stats_,
-                                                                                       &d_stats_->red[2]);
-    launches_ += G_ ? 1 : 0;
-    if (diag) launch_diag();
+    if (diag) {
+      launch_diag(&d_stats_->red[2]);  // group reduction and diagonal search in one launch
+    } else {
+      if (G_)
+        k_reduce<W><<<std::min<uint32_t>(reduce_grid(), blocks(G_)), kCta, 0, stream_>>>(gview(gcur_), d_stats_,
+                                                                                         &d_stats_->red[2]);
+      launches_ += G_ ? 1 : 0;
+    }
     fetch_stats();
     PP_CUDA(cudaGetLastError());
     const DevStats& st = *h_stats_;

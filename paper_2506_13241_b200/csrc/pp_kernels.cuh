@@ -2662,6 +2662,78 @@ __global__ void __launch_bounds__(kCta) k_histogram(GroupView<W> g, ArenaView<W>
 // diagonal strings (x == 0 is the smallest key of a group, so it can only be
 // the first element): <0|O|0> terms (sparse_operator.cpp:32-36, 89-97)
 // ---------------------------------------------------------------------------
+// The per-layer readout in one launch: the group reduction of k_reduce
+// (live count, max / min |c|, NaN flag, largest group) and the diagonal
+// search of k_diag, a warp per group.
+template <int W>
+__global__ void __launch_bounds__(kCta) k_readout(GroupView<W> g, uint32_t Gp, ArenaView<W> ar, uint64_t* out_z,
+                                                  double* out_c, DevStats* st, RedSlot* out) {
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t G = Gp != kKeepG ? Gp : *(volatile const unsigned int*)&st->G_dev;
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t n = i < G ? g.cnt[i] : 0u;
+  unsigned long long live = 0;
+  double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
+  uint32_t nf = 0;
+  if (n) {
+    const uint64_t o = g.off[i];
+    const uint32_t fl = g.flags[i];
+    if (lane == 0) {
+      live = n;
+      mx = g.gmax[i];
+      mn = g.gmin[i];
+      nf = fl & 1u;
+    }
+    uint64_t hit = ~0ull;
+    if (fl & kFlagUnsorted) {
+      for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+        const bool z = j0 + lane < n && plane_zero<W>(load_plane<W>(ar.x, o + j0 + lane));
+        const uint32_t b = __ballot_sync(0xffffffffu, z);
+        if (b) {
+          hit = o + j0 + __ffs(b) - 1;
+          break;
+        }
+      }
+    } else if (plane_zero<W>(load_plane<W>(ar.x, o))) {
+      hit = o;
+    }
+    if (lane == 0 && hit != ~0ull) {
+      const unsigned long long d = atomicAdd(&st->diag_count, 1ull);
+#pragma unroll
+      for (int k = 0; k < W; ++k) out_z[d * W + k] = g.z[k][i];
+      out_c[d] = ar.c[hit];
+    }
+  }
+  __shared__ unsigned long long sl[kWarps];
+  __shared__ double smx[kWarps], smn[kWarps];
+  __shared__ uint32_t snf[kWarps], smc[kWarps];
+  if (lane == 0) {
+    sl[w] = live;
+    smx[w] = mx;
+    smn[w] = mn;
+    snf[w] = nf;
+    smc[w] = n;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t mc = 0;
+    for (uint32_t k = 0; k < kWarps; ++k) {
+      if (k) {
+        live += sl[k];
+        mx = fmax(mx, smx[k]);
+        mn = fmin(mn, smn[k]);
+        nf |= snf[k];
+      }
+      mc = max(mc, smc[k]);
+    }
+    if (live) atomicAdd(&out->live, live);
+    atomic_max_nonneg(reinterpret_cast<double*>(&out->gmax_bits), mx);
+    atomic_min_nonneg(reinterpret_cast<double*>(&out->gmin_bits), mn);
+    if (nf) atomicOr(&out->nonfinite, 1u);
+    if (mc) atomicMax(&out->maxcnt, mc);
+  }
+}
+
 template <int W>
 __global__ void k_diag(GroupView<W> g, uint32_t G, ArenaView<W> ar, uint64_t* out_z, double* out_c,
                        DevStats* st) {
