@@ -50,6 +50,11 @@ static uint64_t ns_since(Clock::time_point t) {
 }
 
 __global__ void k_clear_cumulative(DevStats* st) {
+  st->red[2].live = 0;  // the sync slot, ready for the next readout
+  st->red[2].gmax_bits = 0;
+  st->red[2].gmin_bits = 0x7ff0000000000000ull;
+  st->red[2].nonfinite = 0;
+  st->red[2].maxcnt = 0;
   st->records = 0;
   st->removed = 0;
   st->out_elems = 0;
@@ -1596,10 +1601,13 @@ class EngineImpl final : public EngineBase {
       }
       lazy_open_ = false;
     }
-    push_scalars(bseq_);
     if (diag) {
-      launch_diag(&d_stats_->red[2]);  // group reduction and diagonal search in one launch
+      // group reduction and diagonal search in one launch; k_readout takes the
+      // group count as a parameter (or st->G_dev, committed on the device), and
+      // red[2] is clean (cleared after every sync and by every reset)
+      launch_diag(&d_stats_->red[2]);
     } else {
+      push_scalars(bseq_);
       if (G_)
         k_reduce<W><<<std::min<uint32_t>(reduce_grid(), blocks(G_)), kCta, 0, stream_>>>(gview(gcur_), d_stats_,
                                                                                          &d_stats_->red[2]);
