@@ -65,16 +65,7 @@ __global__ void k_clear_cumulative(DevStats* st) {
   st->dense_out = 0;
 }
 
-__device__ __forceinline__ void k_reset_stats_body(DevStats* st, unsigned long long bump);
 __global__ void k_reset_stats(DevStats* st, unsigned long long bump) { k_reset_stats_body(st, bump); }
-__device__ __forceinline__ void k_reset_stats_body(DevStats* st, unsigned long long bump) {
-  DevStats s;
-  memset(&s, 0, sizeof(s));
-  s.bump = bump;
-  for (int i = 0; i < 3; ++i) s.red[i].gmin_bits = 0x7ff0000000000000ull;
-  s.err_seq = ~0ull;
-  *st = s;
-}
 
 template <int W>
 __global__ void k_init_small(ArenaView<W> a, GroupView<W> g, const InitSmall<W> in, DevStats* st) {
@@ -1961,10 +1952,10 @@ class EngineImpl final : public EngineBase {
       const int o = 1 - cur_;
       ensure_groups(1 - gcur_, std::max<uint32_t>((uint32_t)live, 1024));
       ensure_arena(o, std::max<uint64_t>(regroup_arena(live), std::min<uint64_t>(arena_[cur_].cap, arena_max_)));
-      reset_stats(bump_);
+      // (the kernel resets the statistics itself: no k_reset_stats launch)
       k_regroup_small<W, P><<<1, kSmallRegroupThreads, smem, stream_>>>(gview(gcur_), G_, aview(cur_), prod,
                                                                        gview(1 - gcur_), aview(o), (uint32_t)live,
-                                                                       tc, d_stats_);
+                                                                       tc, d_stats_, bump_);
       ++launches_;
       PP_CUDA(cudaGetLastError());
       cur_ = o;

@@ -146,6 +146,16 @@ struct InitSmall {
   double gmax[kInitSmall], gmin[kInitSmall];
 };
 
+// Full reset of the statistics block (bump pointer of the target arena).
+__device__ __forceinline__ void k_reset_stats_body(DevStats* st, unsigned long long bump) {
+  DevStats s;
+  memset(&s, 0, sizeof(s));
+  s.bump = bump;
+  for (int i = 0; i < 3; ++i) s.red[i].gmin_bits = 0x7ff0000000000000ull;
+  s.err_seq = ~0ull;
+  *st = s;
+}
+
 // Reset of one reduction slot (cumulative counters and sticky errors stay).
 __global__ void k_red_reset(RedSlot* r) { clear_red(r); }
 

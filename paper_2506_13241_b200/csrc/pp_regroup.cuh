@@ -1167,7 +1167,8 @@ constexpr size_t small_regroup_smem(uint32_t tc, uint32_t n) {
 template <int W, class P>
 __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupView<W> gi, uint32_t Gi, ArenaView<W> ai,
                                                                         P prod, GroupView<W> go, ArenaView<W> ao,
-                                                                        uint32_t n, uint32_t tc, DevStats* st) {
+                                                                        uint32_t n, uint32_t tc, DevStats* st,
+                                                                        unsigned long long bump0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* kfp = reinterpret_cast<unsigned long long*>(smem_raw);  // fingerprint of the slot's z (0: empty)
   uint64_t* key = reinterpret_cast<uint64_t*>(kfp + tc);         // [W][tc] the slot's z
@@ -1190,7 +1191,10 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
     smn[h] = 0x7ff0000000000000ull;
     snf[h] = 0;
   }
-  if (tid == 0) s_rec = 0;
+  if (tid == 0) {
+    s_rec = 0;
+    k_reset_stats_body(st, bump0);  // as reset_stats() before a regroup
+  }
   __syncthreads();
   // input group prefix (strings flattened in group order)
   {
