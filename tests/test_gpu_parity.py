@@ -300,3 +300,27 @@ def test_sublayer_paths_match_oracle(pp, O, monkeypatch, mode):
     text = "\n".join(f"{i} {i + 1} {i % 2}" for i in range(63))
     circ = pp.build_kicked_ising(pp.load_geometry(text), 0.3, "-0.5pi", 6)
     run_both(pp, O, 64, list(circ.layers), [(O.site_word(32, 3), 1.0)], 0.0, "gate", check_each=True)
+
+
+def test_engine_pool_reuse_is_fresh(pp, O):
+    """Released engines are pooled and handed to the next creation with the
+    same configuration (pp_create / pp_destroy): the reused engine starts as
+    an empty operator with zeroed counters, and a run on it equals the
+    oracle bit for bit."""
+    import gc
+
+    geom = pp.heavy_hex_127()
+    circ = _kicked(pp, geom, "0.25pi", 4)
+    a = pp.Engine(127, 0.0)
+    a.set_initial(O.site_word(62, 3)[None], np.array([1.0]))
+    a.run_circuit(circ)
+    del a
+    gc.collect()
+    b = pp.Engine(127, 0.0)  # the pooled engine
+    assert b.term_count() == 0
+    assert b.take_counters()["records_sent"] == 0
+    del b
+    gc.collect()
+    # run_both's engine is the pooled one again; a different observable
+    run_both(pp, O, 127, list(circ.layers), [(O.site_word(61, 3), 1.0), (O.site_word(63, 1), 0.5)], 0.0, "gate",
+             check_each=True)
