@@ -324,3 +324,44 @@ def test_engine_pool_reuse_is_fresh(pp, O):
     # run_both's engine is the pooled one again; a different observable
     run_both(pp, O, 127, list(circ.layers), [(O.site_word(61, 3), 1.0), (O.site_word(63, 1), 0.5)], 0.0, "gate",
              check_each=True)
+
+
+def test_chain_config0_t8_dense_big_blocks(pp, O):
+    """BASELINE config 0 to t = 8 (6,952,660 strings): the last Rx run has
+    groups of several x classes with 2^m > one shared-memory tile (the dense
+    path's global-memory passes, rank interleave and hole compaction) --
+    bit-exact against the oracle."""
+    text = "\n".join(f"{i} {i + 1} {i % 2}" for i in range(63))
+    circ = pp.build_kicked_ising(pp.load_geometry(text), 0.3, "-0.5pi", 8)
+    eng, _ = run_both(pp, O, 64, list(circ.layers), [(O.site_word(32, 3), 1.0)], 0.0, "gate", check_each=False)
+    assert eng.term_count() == 6952660
+
+
+@pytest.mark.parametrize("n", [64, 127])
+def test_dense_big_and_multiclass_blocks(pp, O, n):
+    """Groups built to take every dense sub-path in one Rx layer: several x
+    classes with 2^m above a shared-memory tile (global passes, rank
+    interleave), several classes batched through one tile, and one class of
+    several strings with 2^m above a tile -- bit-exact against the oracle."""
+    rng = np.random.default_rng(n)
+
+    def word(label):
+        return np.asarray(pp.PauliString(label, n).words, np.uint64)
+
+    def zs(sites, ys=()):
+        return " ".join(("Y" if q in ys else "Z") + str(q) for q in sites)
+
+    base = 40 if n == 64 else 100
+    big = list(range(14))                 # m = 14: 2^14 points > one tile
+    mid = list(range(base - 20, base - 8))  # m = 12
+    init = []
+    for j, extra in enumerate([f"X{base}", f"X{base + 1}", f"X{base} X{base + 1}"]):  # K = 3 classes
+        init.append((word(zs(big, ys=(j,)) + " " + extra), float(rng.uniform(-1, 1))))
+    for a, b in [(0, 0), (0, 1), (1, 0), (1, 1)]:  # K = 4 classes, batched two per tile
+        extra = " ".join(s for s, on in ((f"X{base + 2}", a), (f"X{base + 3}", b)) if on)
+        init.append((word(zs(mid) + (" " + extra if extra else "")), float(rng.uniform(-1, 1))))
+    for ys in [(20,), (21, 22), (23,)]:  # one class, several strings, m = 14
+        sites = list(range(16, 30))
+        init.append((word(zs(sites, ys=ys)), float(rng.uniform(-1, 1))))
+    layer = [pp.Gate(pp.PauliString(f"X{q}", n), float(rng.uniform(-3, 3))) for q in range(n)]
+    run_both(pp, O, n, [layer], init, 0.0, "gate", check_each=True)
