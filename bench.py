@@ -385,8 +385,12 @@ def main():
     e2e_value = sg * world / e2e_s
     L = circ.num_layers()
     n_zz_runs = L
-    h2d = 40 + n_zz_runs * 144 * (16 * (1 if n <= 64 else 2) + 8)  # initial term + Clifford-run gate planes
-    d2h = L * (8 * 40)  # per-layer ledger scalars and diagonal readout
+    # the initial term, and per layer the gate descriptors of the Rx run and
+    # the Clifford run (kernel parameters, ~ (8W + 16) B per gate)
+    h2d = 40 + n_zz_runs * circ.total_gates() // max(L, 1) * (8 * (1 if n <= 64 else 2) + 16)
+    # per layer: the statistics block of the readout round trip (~1 KiB) and
+    # the diagonal-string prefix (256 strings of 8W + 8 bytes)
+    d2h = L * (1024 + 256 * (8 * (1 if n <= 64 else 2) + 8))
 
     peak, peak_kind = load_peaks()
     achieved = pks["branch_bytes"] / (pks["branch_ms"] / 1e3) / 1e9 if pks["branch_ms"] > 0 else 0.0

@@ -255,7 +255,8 @@ static void release_pinned_stats(DevStats* p) {
   g_pinned_free.push_back(p);
 }
 // pinned staging for the diagonal readout, recycled across engines
-constexpr size_t kDiagCap = 4096;  // diagonal strings fetched with the readout's single round trip
+constexpr size_t kDiagCap = 4096;  // pinned room for diagonal strings
+constexpr size_t kDiagSpec = 256;  // fetched with the readout's single round trip
 struct DiagPinned {
   uint64_t z[2 * kDiagCap];
   double c[kDiagCap];
@@ -1570,7 +1571,9 @@ class EngineImpl final : public EngineBase {
                                                            diag_z_.as<uint64_t>(), diag_c_.as<double>(), d_stats_);
     ++launches_;
     if (!h_diag_) h_diag_ = pinned_diag();
-    diag_copied_ = std::min<uint64_t>(G_, kDiagCap);
+    // diagonal strings are few (at most one per group): fetch a short prefix
+    // with the readout's round trip, the rest only if there are more
+    diag_copied_ = std::min<uint64_t>(G_, kDiagSpec);
     PP_CUDA(cudaMemcpyAsync(h_diag_->z, diag_z_.p, diag_copied_ * W * 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaMemcpyAsync(h_diag_->c, diag_c_.p, diag_copied_ * 8, cudaMemcpyDeviceToHost, stream_));
   }
