@@ -142,6 +142,10 @@ static inline bool is_clifford(const pp_gate& g) {
 // per simulate() call, like the reference) does not pay cudaMalloc/cudaFree
 // every time.  Blocks are reused when they fit within 25 % slack.
 // ---------------------------------------------------------------------------
+// Called before the pool gives up on an allocation: releases engines parked
+// in the engine pool (their buffers come back here), set below.
+static void (*g_release_parked_engines)() = nullptr;
+
 class DevicePool {
  public:
   static DevicePool& get() {
@@ -167,6 +171,7 @@ class DevicePool {
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
+      if (g_release_parked_engines) g_release_parked_engines();
       trim(dev);
       e = cudaMalloc(&p, bytes);
     }
@@ -2255,6 +2260,21 @@ namespace {
 std::mutex g_engine_pool_mu;
 std::vector<std::pair<std::string, ppgpu::EngineBase*>>* g_engine_pool = new std::vector<std::pair<std::string, ppgpu::EngineBase*>>();
 constexpr size_t kEnginePoolMax = 4;
+
+// device memory is short: parked engines go (their buffers return to the
+// device pool, which then frees its cache)
+void release_parked_engines() {
+  std::vector<ppgpu::EngineBase*> victims;
+  {
+    std::lock_guard<std::mutex> lk(g_engine_pool_mu);
+    for (auto& kv : *g_engine_pool) victims.push_back(kv.second);
+    g_engine_pool->clear();
+  }
+  for (auto* v : victims) delete v;
+}
+struct ParkedEnginesHook {
+  ParkedEnginesHook() { ppgpu::g_release_parked_engines = &release_parked_engines; }
+} g_parked_engines_hook;
 
 std::string engine_key(const pp_config& c) {
   std::string k;
