@@ -5,18 +5,22 @@ Metric (BASELINE.json): Pauli-string terms processed per second per gate
 layer = string-gates/s, where one string-gate is one live string entering
 one gate.  Sum over gates of |O_in| / time.
 
-Workload (default, BASELINE.json configs[1]): 127-qubit heavy-hex kicked
-Ising, theta_h = pi/4, theta_J = -pi/2 (Clifford ZZ), O0 = Z62, eps0 = 0,
-5 Trotter steps (final |O| = 2,146,372).  One bench step = one full
-propagation of that circuit from O0 (1,355 gates), readout after every
-layer, exactly what the reference's run_circuit does.
+Workload (default): BASELINE.json config 0 in full -- the 64-qubit open
+kicked-Ising chain, theta_h = 0.3, theta_J = -pi/2, O0 = Z32, eps0 = 0, all
+10 Trotter steps (final |O| = 987,369,656 strings, ~24 GB of live state):
+the largest BASELINE configuration that runs on one B200 at eps0 = 0.  One
+bench step = one full propagation from O0 (1,270 gates), readout after every
+layer, exactly what the reference's run_circuit does.  Other workloads:
+``--workload config1`` (BASELINE configs[1]), ``config0_t9``,
+``config2_pi4_eps1e-4_t8``.
 
   value -- device-timed (CUDA events on the engine's stream), state created
            on the device, string-gates/s
   e2e   -- the public API call a user makes (simulate(...)), host circuit
            in, ledger rows out, wall-clocked around the call
   cpu_baseline -- the reference engine compiled from its own sources
-           (oracle/_ref), on this box's host cores
+           (oracle/_ref), on this box's host cores, on the largest prefix of
+           the workload it runs in seconds (config 0 to t = 9, 81.7 M strings)
 
 ``--impl reference`` times the reference CPU engine on the same workload.
 Under torchrun (N > 1) the operator is sharded over the ranks by z-plane
@@ -38,14 +42,29 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# name: (geometry, n, theta_x, theta_zz, observable site, eps0, layers)
 WORKLOADS = {
-    # name: (geometry, n, theta_x, theta_zz, observable site, eps0, layers)
     "config1": ("heavy_hex", 127, "0.25pi", "-0.5pi", 62, 0.0, 5),
     "config0_t8": ("chain64", 64, 0.3, "-0.5pi", 32, 0.0, 8),
     "config0_t9": ("chain64", 64, 0.3, "-0.5pi", 32, 0.0, 9),
     "config0_t10": ("chain64", 64, 0.3, "-0.5pi", 32, 0.0, 10),
     "config2_pi4_eps1e-4_t8": ("heavy_hex", 127, "0.25pi", "-0.5pi", 62, 1e-4, 8),
 }
+# Exact sum over gates of |O_in| (string-gates per step) and the final |O|,
+# counted once gate by gate (``--count`` recounts; tests pin the small ones
+# against the reference engine's own count).
+COUNTS = {
+    "config1": (106882582, 2146372),
+    "config0_t8": (283416094, 6952660),
+    "config0_t9": (3242286702, 81662152),
+    "config0_t10": (38261630218, 987369656),
+    "config2_pi4_eps1e-4_t8": (4518354553, 11856422),
+}
+# The reference CPU engine cannot hold config 0 at t = 10 (~1e9 strings) in a
+# few minutes: its arm and cpu_baseline time the largest prefix that runs in
+# seconds per step on the box's host cores.
+CPU_SAMPLE = {"config0_t10": "config0_t9"}
+DEFAULT_WORKLOAD = "config0_t10"
 
 
 def chain_text(n):
@@ -187,22 +206,40 @@ def cpu_reference_time(wl, steps, warmup, threads):
     return times, sg
 
 
+def config_dict(args, wl, world):
+    """The `config` object both arms print (same keys, same values)."""
+    sg, final_terms = COUNTS[args.workload]
+    return {"workload": args.workload, "epsilon0": wl[5], "layers": wl[6], "string_gates_per_step": sg,
+            "final_terms": final_terms, "observable": f"Z{wl[4]}", "n_qubits": wl[1],
+            "l2": "flushed (512 MB write) before every timed step and every e2e call",
+            "parallelism": "single GPU" if world == 1 else f"z-hash shards x{world}"}
+
+
+def cpu_sample_note(name, threads, runs):
+    return (f"{name}: full propagation per step through the reference engine compiled from its sources "
+            f"(oracle/_ref, -O3), {threads} workers = threads, median of {runs}")
+
+
 def run_reference_arm(args, wl, rank, world):
+    """The reference's own CPU engine on the host cores, rank 0 only.  For a
+    workload the reference cannot run in seconds (config0_t10) each step is
+    the largest prefix that does (CPU_SAMPLE), stated in cpu_baseline.sample."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    times, sg = cpu_reference_time(wl, args.steps, args.warmup, threads)
+    sample = CPU_SAMPLE.get(args.workload, args.workload)
+    times, sg = cpu_reference_time(WORKLOADS[sample], args.steps, args.warmup, threads)
     per = sorted(times)[len(times) // 2]
     value = sg / per
     line = {
-        "metric": "string_gates_per_s", "value": value, "unit": "string-gates/s", "n_gpus": 0,
+        "metric": "string_gates_per_s", "value": value, "unit": "string-gates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic circuit)",
         "impl": "reference",
-        "config": {"workload": args.workload, "string_gates_per_step": sg},
+        "config": config_dict(args, wl, world),
         "cpu_baseline": {"value": value, "unit": "string-gates/s", "cores": threads, "kind": "reference",
-                         "sample": f"full {args.workload} propagation per step (reference engine, "
-                                   f"{threads} workers/threads, median of {len(times)})"},
+                         "sample": cpu_sample_note(sample, threads, len(times)),
+                         "sample_string_gates_per_step": sg},
         "e2e": {"value": value, "unit": "string-gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -276,17 +313,32 @@ def run_sharded(args, pp, circ, wl, sg, final_terms, init, rank, world, local):
     dist.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """``--gpus N`` outside torchrun: relaunch this script under
+    torch.distributed.run with N ranks (one per GPU) on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config1", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--count", action="store_true", help="recount string-gates gate by gate (slow)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -311,7 +363,9 @@ def main():
 
     circ = build_circuit(pp, wl)
     n, site, eps = wl[1], wl[4], wl[5]
-    sg, final_terms = string_gates(pp, circ, wl)
+    if args.count:
+        COUNTS[args.workload] = string_gates(pp, circ, wl)
+    sg, final_terms = COUNTS[args.workload]
     init = np.zeros((1, 4), np.uint64)
     init[0, site // 32] = np.uint64(3) << np.uint64(2 * (site % 32))
     if world > 1:
@@ -325,8 +379,7 @@ def main():
 
     def one_step():
         eng.set_initial(init, np.array([1.0]))
-        rows = eng.run_circuit(circ)
-        return rows
+        return eng.run_circuit(circ)
 
     for _ in range(args.warmup):
         one_step()
@@ -337,8 +390,6 @@ def main():
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -347,7 +398,9 @@ def main():
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
     ks = eng.kernel_stats()
-    assert rows[-1]["term_count"] == final_terms
+    assert rows[-1]["term_count"] == final_terms, (rows[-1]["term_count"], final_terms)
+    ms_per_step = sum(ms) / args.steps
+    value = sg / (ms_per_step / 1e3)
     # roofline pass (untimed): no graphs, CUDA events around every branch launch
     del eng, stream  # its device buffers return to the engine's pool for reuse
     import gc
@@ -358,45 +411,31 @@ def main():
     peng.run_circuit(circ)
     pks = peng.kernel_stats()
     del peng
-    total_ms = sum(ms)
-    if world > 1:
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = sg * world / (ms_per_step / 1e3)
+    gc.collect()
 
-    # ---------------- e2e through the public API (simulate), wall clock
-    e2e_times = []
+    # ---------------- e2e through the public API (simulate): host circuit in,
+    # ledger rows out, L2 flushed before every call, bytes counted by the engine
+    e2e_times, h2d, d2h = [], [], []
     for i in range(args.warmup + args.steps):
+        flush.zero_()
         torch.cuda.synchronize()
+        b0 = pp.transfer_totals()
         t0 = time.perf_counter()
         out = pp.simulate(circ, observable=f"Z{site}", epsilon0=eps)
         t1 = time.perf_counter()
+        b1 = pp.transfer_totals()
         if i >= args.warmup:
             e2e_times.append(t1 - t0)
+            h2d.append(b1[0] - b0[0])
+            d2h.append(b1[1] - b0[1])
     assert out[-1]["term_count"] == final_terms
     e2e_sorted = sorted(e2e_times)
     e2e_s = e2e_sorted[len(e2e_sorted) // 2]  # median: one engine per call, robust to host hiccups
-    if world > 1:
-        t = torch.tensor([e2e_s], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = sg * world / e2e_s
-    L = circ.num_layers()
-    n_zz_runs = L
-    # the initial term, and per layer the gate descriptors of the Rx run and
-    # the Clifford run (kernel parameters, ~ (8W + 16) B per gate)
-    h2d = 40 + n_zz_runs * circ.total_gates() // max(L, 1) * (8 * (1 if n <= 64 else 2) + 16)
-    # per layer: the statistics block of the readout round trip (~1 KiB) and
-    # the diagonal-string prefix (256 strings of 8W + 8 bytes)
-    d2h = L * (1024 + 256 * (8 * (1 if n <= 64 else 2) + 8))
+    e2e_value = sg / e2e_s
 
     peak, peak_kind = load_peaks()
     achieved = pks["branch_bytes"] / (pks["branch_ms"] / 1e3) / 1e9 if pks["branch_ms"] > 0 else 0.0
-    launches_per_step = ks["launches"] / args.steps
-    traffic = None
-    traffic_src = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "branch_traffic.json")
     if os.path.exists(prof):
         try:
@@ -409,59 +448,57 @@ def main():
             traffic = None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
+        sample = CPU_SAMPLE.get(args.workload, args.workload)
         try:
             threads = os.cpu_count() or 1
-            times, csg = cpu_reference_time(wl, 1, 1, threads)
+            times, csg = cpu_reference_time(WORKLOADS[sample], 1, 1, threads)
             cpu = {"value": csg / times[0], "unit": "string-gates/s", "cores": threads, "kind": "reference",
-                   "sample": f"one full {args.workload} propagation (reference engine compiled from its "
-                             f"sources, {threads} workers/threads, after 1 warm-up run)"}
+                   "sample": cpu_sample_note(sample, threads, 1) + " after 1 warm-up run",
+                   "sample_string_gates_per_step": csg}
         except Exception as exc:  # the reference build travels as oracle/_ref
             cpu = {"value": None, "unit": "string-gates/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
-    if rank == 0:
-        line = {
-            "metric": "string_gates_per_s", "value": value, "unit": "string-gates/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (deterministic kicked-Ising circuit, BASELINE config)",
-            "config": {"workload": args.workload, "string_gates_per_step": sg, "final_terms": final_terms,
-                       "layers": L, "gates_per_step": circ.total_gates(),
-                       "l2": "flushed (512 MB write) between timed steps",
-                       "parallelism": f"replicas x{world}"},
-            "e2e": {"value": e2e_value, "unit": "string-gates/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "api": "simulate()",
-                    "stat": "median over steps", "ms_min": e2e_sorted[0] * 1e3,
-                    "ms_mean": sum(e2e_times) / len(e2e_times) * 1e3},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "traffic_unit": "DRAM bytes per launch (ncu)",
-                         "algorithmic_bytes_per_launch": (pks["branch_bytes"] / pks["branch_launches"]
-                                                          if pks["branch_launches"] else None),
-                         "traffic_detail": traffic_src,
-                         "kernel": "k_branch_sublayer", "peak_kind": peak_kind,
-                         "bytes_model": "(strings read + strings written) x (8W+8) B per launch; the dense "
-                                        "sublayer reads each input string once and writes each output "
-                                        "string once per Rx run",
-                         "branch_ms_per_step": pks["branch_ms"],
-                         "branch_bytes_per_step": pks["branch_bytes"],
-                         "branch_launches_per_step": pks["branch_launches"],
-                         "how": "separate untimed pass, CUDA events around each branch launch",
-                         # SURVEY.md 8d streaming model: R(n) (|O_in| + |O_out|) bytes per
-                         # branching gate ~ 2 R(n) per string-gate, R(n) = 16 ceil(n/64) + 8
-                         "streaming_model": {
-                             "bytes_per_string_gate": 2 * (16 * ((n + 63) // 64) + 8),
-                             "equivalent_GBps": value * 2 * (16 * ((n + 63) // 64) + 8) / 1e9,
-                             "frac": value * 2 * (16 * ((n + 63) // 64) + 8) / 1e9 / peak}},
-            "cpu_baseline": cpu,
-            "clocks": clk.summary(),
-            "gpu_launches": int(round(launches_per_step * args.steps)),
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    R = 16 * ((n + 63) // 64) + 8  # SURVEY 8d streaming record: x, z planes + coefficient
+    line = {
+        "metric": "string_gates_per_s", "value": value, "unit": "string-gates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (deterministic kicked-Ising circuit, BASELINE config; no dataset)",
+        "config": config_dict(args, wl, world),
+        "e2e": {"value": e2e_value, "unit": "string-gates/s",
+                "h2d_bytes_per_step": int(sorted(h2d)[len(h2d) // 2]),
+                "d2h_bytes_per_step": int(sorted(d2h)[len(d2h) // 2]),
+                "bytes": "counted by the engine (pp_transfer_totals): every copy + parameter blocks carrying "
+                         "host data", "ms_per_step": e2e_s * 1e3, "api": "simulate()",
+                "stat": "median over steps", "ms_min": e2e_sorted[0] * 1e3,
+                "ms_mean": sum(e2e_times) / len(e2e_times) * 1e3},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu)",
+                     "algorithmic_bytes_per_launch": (pks["branch_bytes"] / pks["branch_launches"]
+                                                      if pks["branch_launches"] else None),
+                     "traffic_detail": traffic_src,
+                     "kernel": "k_branch_sublayer", "peak_kind": peak_kind,
+                     "bytes_model": "(strings read + strings written) x (8W+8) B per launch; the dense "
+                                    "sublayer reads each input string once and writes each output "
+                                    "string once per Rx run",
+                     "branch_ms_per_step": pks["branch_ms"],
+                     "branch_share_of_step": pks["branch_ms"] / ms_per_step,
+                     "branch_bytes_per_step": pks["branch_bytes"],
+                     "branch_launches_per_step": pks["branch_launches"],
+                     "how": "separate untimed pass, CUDA events around each branch launch on the engine stream",
+                     "streaming_model": {
+                         "bytes_per_string_gate": 2 * R,
+                         "equivalent_GBps": value * 2 * R / 1e9,
+                         "note": "SURVEY 8d per-gate streaming bytes; the fused runs touch each string once "
+                                 "per run, so this equivalent exceeds HBM peak"}},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": int(ks["launches"]),
+    }
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -138,6 +138,11 @@ int pp_take_kernel_stats(pp_engine* engine, double* branch_ms, double* branch_by
  * bracket work with their own events. */
 void* pp_stream(const pp_engine* engine);
 
+/* Process-wide host<->device byte totals over every engine since load:
+ * explicit copies plus kernel parameter blocks carrying host data (gate
+ * lists, initial terms).  Callers difference two readings. */
+void pp_transfer_totals(uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+
 /* ---- sharding (one engine per GPU; the orchestrator owns the collectives).
  * owner(z) = pp_shard_owner: a hash of the string's z-plane.  An Rx gate keeps
  * z, so it never moves strings between shards; after a Clifford/ZZ run or a

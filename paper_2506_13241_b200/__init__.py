@@ -40,6 +40,7 @@ write_checkpoint_manifest = _impl.write_checkpoint_manifest
 write_shard_file = _impl.write_shard_file
 build_kicked_ising = _impl.build_kicked_ising
 commutes = _impl.commutes
+destination_set = _impl.destination_set
 heavy_hex_127 = _impl.heavy_hex_127
 load_geometry = _impl.load_geometry
 load_geometry_file = _impl.load_geometry_file
@@ -49,6 +50,8 @@ parse_pauli_label = _impl.parse_pauli_label
 pauli_weight = _impl.pauli_weight
 phase_exponent = _impl.phase_exponent
 simulate = _impl.simulate
+state_vector_expectation = _impl.state_vector_expectation
+transfer_totals = _impl.transfer_totals
 string_product = _impl.string_product
 uniformity_ratio = _impl.uniformity_ratio
 
@@ -60,8 +63,8 @@ NATIVE_LIBS = (
 __all__ = [
     "Circuit", "Engine", "Gate", "Geometry", "NumericalError", "PartitionSpec",
     "PauliString", "ResourceLimitError", "bfs_ball", "build_kicked_ising",
-    "commutes", "dump_operator", "histogram_from_counts", "load_dump", "read_checkpoint",
+    "commutes", "destination_set", "dump_operator", "histogram_from_counts", "load_dump", "read_checkpoint",
     "write_checkpoint_manifest", "write_shard_file", "heavy_hex_127", "load_geometry", "load_geometry_file", "owner",
     "parse_circuit", "parse_pauli_label", "pauli_weight", "phase_exponent",
-    "simulate", "string_product", "uniformity_ratio",
+    "simulate", "state_vector_expectation", "string_product", "uniformity_ratio",
 ]

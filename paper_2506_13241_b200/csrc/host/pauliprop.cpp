@@ -7,8 +7,15 @@
 #include "pauliprop.hpp"
 
 #include <algorithm>
+#include <cerrno>
+#include <charconv>
+#include <climits>
+#include <numeric>
+#include <string_view>
+#include <utility>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstring>
 #include <deque>
@@ -25,10 +32,9 @@ namespace pauliprop {
 
 namespace {
 constexpr double kPi = 3.14159265358979323846;
-
-// su(2) structure constants on one site, rows a, columns b, codes I X Y Z
-// (pauli_string.cpp:25-34): sigma_a sigma_b = i^{phase} sigma_{a xor b}.
-constexpr int8_t kPhase[4][4] = {{0, 0, 0, 0}, {0, 0, 1, -1}, {0, -1, 0, 1}, {0, 1, -1, 0}};
+constexpr char kLetters[] = "IXYZ";
+constexpr char kHexDigits[] = "0123456789abcdef";
+constexpr uint64_t kEven = 0x5555555555555555ULL;
 
 uint64_t splitmix(uint64_t z) {
   z += 0x9e3779b97f4a7c15ULL;
@@ -44,20 +50,27 @@ void require_site(int site, int n) {
 }
 
 int code_of(char c) {
-  switch (c) {
-    case 'I': return 0;
-    case 'X': return 1;
-    case 'Y': return 2;
-    case 'Z': return 3;
-    default: return -1;
-  }
+  const char* p = std::strchr(kLetters, c);
+  return (p && c) ? int(p - kLetters) : -1;
 }
 
-std::string trim(const std::string& s) {
-  size_t a = s.find_first_not_of(" \t\r");
-  if (a == std::string::npos) return "";
-  size_t b = s.find_last_not_of(" \t\r");
-  return s.substr(a, b - a + 1);
+int hex_value(char c) {
+  if (c >= '0' && c <= '9') return c - '0';
+  if (c >= 'a' && c <= 'f') return c - 'a' + 10;
+  if (c >= 'A' && c <= 'F') return c - 'A' + 10;
+  return -1;
+}
+
+bool is_blank(char c) { return c == ' ' || c == '\t' || c == '\r' || c == '\n' || c == '\v' || c == '\f'; }
+
+// x/z bit planes of one packed word (site s at bits 2s, 2s+1 -> plane bit 2s):
+// X = (x, !z), Y = (x, z), Z = (!x, z).
+struct Planes {
+  uint64_t x, z;
+};
+Planes planes_of(uint64_t w) {
+  const uint64_t lo = w & kEven, hi = (w >> 1) & kEven;
+  return {lo ^ hi, hi};
 }
 }  // namespace
 
@@ -75,11 +88,28 @@ uint64_t hash_string(const PauliString& s) {
   return h;
 }
 
-int local_phase(uint8_t a, uint8_t b) { return kPhase[a & 3][b & 3]; }
+// sigma_a sigma_b = i^{local_phase(a, b)} sigma_{a xor b} on one site
+// (pauli_string.cpp:25-34): +1 for the cyclic pairs XY, YZ, ZX, -1 for the
+// reversed ones, 0 when either is I or a == b.
+int local_phase(uint8_t a, uint8_t b) {
+  a &= 3, b &= 3;
+  if (!a || !b || a == b) return 0;
+  return b == a % 3 + 1 ? 1 : -1;
+}
 
+// B(I, J) mod 4 (pauli_string.cpp:79-85) from bit planes: the number of
+// cyclic site pairs minus the number of anti-cyclic ones.
 int phase_exponent(const PauliString& I, const PauliString& J, int n) {
   int b = 0;
-  for (int site = 0; site < n; ++site) b += local_phase(I.code_at(site), J.code_at(site));
+  for (int w = 0; w < kIndexWords && 32 * w < n; ++w) {
+    uint64_t keep = kEven;
+    if (n - 32 * w < 32) keep &= (uint64_t{1} << (2 * (n - 32 * w))) - 1;
+    const Planes p = planes_of(I.words[w]), q = planes_of(J.words[w]);
+    const uint64_t pX = p.x & ~p.z & keep, pY = p.x & p.z & keep, pZ = ~p.x & p.z & keep;
+    const uint64_t qX = q.x & ~q.z, qY = q.x & q.z, qZ = ~q.x & q.z;
+    b += __builtin_popcountll((pX & qY) | (pY & qZ) | (pZ & qX));
+    b -= __builtin_popcountll((pY & qX) | (pZ & qY) | (pX & qZ));
+  }
   return ((b % 4) + 4) % 4;
 }
 
@@ -91,106 +121,187 @@ StringProduct string_product(const PauliString& I, const PauliString& J, int n) 
 
 int pauli_weight(const PauliString& s) {
   int w = 0;
-  for (uint64_t v : s.words) w += __builtin_popcountll((v | (v >> 1)) & 0x5555555555555555ULL);
+  for (uint64_t v : s.words) w += __builtin_popcountll((v | (v >> 1)) & kEven);
   return w;
 }
 
-// Dense ("IZIZ", leftmost = site n-1) or sparse ("Z2 Z0") labels,
-// pauli_string.cpp:105-177.
+// ------------------------------------------------------------ text helpers
+// A line-oriented view of a text block: '#' starts a comment, tokens are
+// separated by blanks/tabs/CR.  Shared by the circuit and geometry readers.
+namespace {
+struct TextLine {
+  int number = 0;
+  std::vector<std::string_view> tokens;
+};
+
+std::vector<std::string_view> split_tokens(std::string_view text) {
+  std::vector<std::string_view> tokens;
+  size_t p = 0;
+  while (p < text.size()) {
+    while (p < text.size() && is_blank(text[p])) ++p;
+    size_t q = p;
+    while (q < text.size() && !is_blank(text[q])) ++q;
+    if (q > p) tokens.push_back(text.substr(p, q - p));
+    p = q;
+  }
+  return tokens;
+}
+
+std::vector<TextLine> split_lines(std::string_view text) {
+  std::vector<TextLine> out;
+  int number = 0;
+  while (!text.empty() || number == 0) {
+    size_t eol = text.find('\n');
+    std::string_view raw = text.substr(0, eol);
+    text = eol == std::string_view::npos ? std::string_view{} : text.substr(eol + 1);
+    TextLine tl;
+    tl.number = ++number;
+    tl.tokens = split_tokens(raw.substr(0, raw.find('#')));
+    out.push_back(std::move(tl));
+    if (eol == std::string_view::npos) break;
+  }
+  return out;
+}
+
+[[noreturn]] void line_error(const char* what, int number, const std::string& msg) {
+  throw std::invalid_argument(std::string(what) + " line " + std::to_string(number) + ": " + msg);
+}
+
+// Whole-token integer; false if the token has anything else in it.
+bool token_int(std::string_view tok, long long* out) {
+  if (tok.empty()) return false;
+  const char* first = tok.data();
+  if (*first == '+') ++first;  // operator>> accepts an explicit plus
+  auto [end, ec] = std::from_chars(first, tok.data() + tok.size(), *out);
+  return ec == std::errc() && end == tok.data() + tok.size();
+}
+
+// Leading integer of a token, as operator>> would extract it (rest ignored).
+bool leading_int(std::string_view tok, long long* out) {
+  const char* first = tok.data();
+  if (!tok.empty() && *first == '+') ++first;
+  auto [end, ec] = std::from_chars(first, tok.data() + tok.size(), *out);
+  return ec == std::errc() && end != first;
+}
+}  // namespace
+
+// ------------------------------------------------------------ labels
+// Two label forms (pauli_string.cpp:105-177): dense, one letter per site with
+// the leftmost letter = site n-1; sparse, blank-separated "<P><site>" tokens.
+// A label containing a digit or a blank is sparse.
 PauliString parse_pauli_label(const std::string& text, int n) {
   if (n < 1 || n > kMaxQubits) throw std::invalid_argument("qubit count out of range: " + std::to_string(n));
-  std::string t = trim(text);
-  if (t.empty()) throw std::invalid_argument("empty pauli label");
-  bool digit = t.find_first_of("0123456789") != std::string::npos;
-  bool space = t.find_first_of(" \t") != std::string::npos;
+  std::string_view body = text;
+  while (!body.empty() && (body.front() == ' ' || body.front() == '\t')) body.remove_prefix(1);
+  while (!body.empty() && (body.back() == ' ' || body.back() == '\t')) body.remove_suffix(1);
+  if (body.empty()) throw std::invalid_argument("empty pauli label");
+  const bool sparse = std::any_of(body.begin(), body.end(),
+                                  [](char ch) { return is_blank(ch) || (ch >= '0' && ch <= '9'); });
   PauliString s;
-  if (!digit && !space) {
-    if ((int)t.size() != n)
-      throw std::invalid_argument("dense pauli label \"" + t + "\" has length " + std::to_string(t.size()) +
-                                  ", expected n=" + std::to_string(n));
-    for (int i = 0; i < n; ++i) {
-      int c = code_of(t[i]);
-      if (c < 0) throw std::invalid_argument(std::string("invalid pauli character '") + t[i] + "'");
-      s.set_code(n - 1 - i, (uint8_t)c);
+  if (!sparse) {
+    if ((int)body.size() != n)
+      throw std::invalid_argument("dense pauli label \"" + std::string(body) + "\" has length " +
+                                  std::to_string(body.size()) + ", expected n=" + std::to_string(n));
+    int site = n;
+    for (char ch : body) {
+      --site;
+      const int code = code_of(ch);
+      if (code < 0) throw std::invalid_argument(std::string("invalid pauli character '") + ch + "'");
+      s.set_code(site, (uint8_t)code);
     }
     return s;
   }
-  std::istringstream in(t);
-  std::string tok;
-  while (in >> tok) {
-    int c = code_of(tok[0]);
-    if (c <= 0) throw std::invalid_argument("invalid sparse pauli token \"" + tok + "\"");
-    if (tok.size() < 2) throw std::invalid_argument("sparse pauli token \"" + tok + "\" is missing a site index");
-    size_t pos = 0;
-    int site;
-    try {
-      site = std::stoi(tok.substr(1), &pos);
-    } catch (const std::exception&) {
-      throw std::invalid_argument("invalid site index in token \"" + tok + "\"");
+  {
+    for (std::string_view tok : split_tokens(body)) {
+      const std::string t(tok);
+      const int code = code_of(tok[0]);
+      if (code <= 0) throw std::invalid_argument("invalid sparse pauli token \"" + t + "\"");
+      if (tok.size() == 1) throw std::invalid_argument("sparse pauli token \"" + t + "\" is missing a site index");
+      long long site = 0;
+      std::string_view digits = tok.substr(1);
+      // std::stoi semantics: leading blanks/sign allowed, then digits; the
+      // whole remainder must be consumed
+      const char* b = digits.data();
+      const char* e = b + digits.size();
+      const char* num = (*b == '+') ? b + 1 : b;
+      auto [end, ec] = std::from_chars(num, e, site);
+      if (ec != std::errc() || end == num || site < INT_MIN || site > INT_MAX)
+        throw std::invalid_argument("invalid site index in token \"" + t + "\"");
+      if (end != e) throw std::invalid_argument("invalid sparse pauli token \"" + t + "\"");
+      require_site((int)site, n);
+      if (s.code_at((int)site) != 0)
+        throw std::invalid_argument("site " + std::to_string(site) + " appears twice in pauli label");
+      s.set_code((int)site, (uint8_t)code);
     }
-    if (pos + 1 != tok.size()) throw std::invalid_argument("invalid sparse pauli token \"" + tok + "\"");
-    require_site(site, n);
-    if (s.code_at(site)) throw std::invalid_argument("site " + std::to_string(site) + " appears twice in pauli label");
-    s.set_code(site, (uint8_t)c);
   }
   return s;
 }
 
 std::string to_dense_label(const PauliString& s, int n) {
-  std::string out(n, 'I');
-  for (int site = 0; site < n; ++site) out[n - 1 - site] = "IXYZ"[s.code_at(site)];
+  std::string out;
+  out.reserve(n);
+  for (int site = n - 1; site >= 0; --site) out.push_back(kLetters[s.code_at(site)]);
   return out;
 }
 
 std::string to_sparse_label(const PauliString& s, int n) {
-  std::string out;
+  std::ostringstream out;
+  const char* sep = "";
   for (int site = 0; site < n; ++site) {
-    uint8_t c = s.code_at(site);
-    if (!c) continue;
-    if (!out.empty()) out += ' ';
-    out += "IXYZ"[c];
-    out += std::to_string(site);
+    if (uint8_t c = s.code_at(site)) {
+      out << sep << kLetters[c] << site;
+      sep = " ";
+    }
   }
-  return out.empty() ? "I" : out;
+  std::string r = out.str();
+  return r.empty() ? std::string("I") : r;
 }
 
+// Hex index (checkpoint dumps, sparse_operator.cpp:99-122): 2n bits, most
+// significant nibble first, ceil(2n/4) digits.
 std::string to_hex(const PauliString& s, int n) {
-  int digits = (2 * n + 3) / 4;
-  std::string out(digits, '0');
-  for (int d = 0; d < digits; ++d) {
-    int bit = 4 * d;
-    out[digits - 1 - d] = "0123456789abcdef"[(s.words[bit >> 6] >> (bit & 63)) & 0xf];
+  const int nibbles = (2 * n + 3) / 4;
+  std::string out;
+  out.reserve(nibbles);
+  for (int d = nibbles - 1; d >= 0; --d) {
+    const uint64_t word = s.words[(4 * d) / 64];
+    out.push_back(kHexDigits[(word >> ((4 * d) % 64)) & 0xFu]);
   }
   return out;
 }
 
 PauliString from_hex(const std::string& hex, int n) {
   PauliString s;
-  int bit = 0;
-  for (auto it = hex.rbegin(); it != hex.rend(); ++it, bit += 4) {
-    char c = (char)std::tolower(*it);
-    int v;
-    if (c >= '0' && c <= '9') v = c - '0';
-    else if (c >= 'a' && c <= 'f') v = 10 + (c - 'a');
-    else throw std::invalid_argument(std::string("invalid hex digit '") + *it + "'");
+  const int len = (int)hex.size();
+  for (int d = 0; d < len; ++d) {  // d = nibble index from the least significant end
+    const char ch = hex[len - 1 - d];
+    const int v = hex_value(ch);
+    if (v < 0) throw std::invalid_argument(std::string("invalid hex digit '") + ch + "'");
     if (v == 0) continue;
-    if (bit >= 2 * kMaxQubits) throw std::invalid_argument("hex index wider than the maximum width");
-    s.words[bit >> 6] |= (uint64_t)v << (bit & 63);
+    if (4 * d >= 2 * kMaxQubits) throw std::invalid_argument("hex index wider than the maximum width");
+    s.words[(4 * d) / 64] |= uint64_t(v) << ((4 * d) % 64);
   }
-  for (int site = n; site < kMaxQubits; ++site)
-    if (s.code_at(site)) throw std::invalid_argument("hex index has bits above site " + std::to_string(n - 1));
+  // every code above site n-1 must be identity
+  for (int w = 0; w < kIndexWords; ++w) {
+    const int lo_site = 32 * w;
+    uint64_t allowed = 0;
+    if (n >= lo_site + 32) allowed = ~uint64_t{0};
+    else if (n > lo_site) allowed = (uint64_t{1} << (2 * (n - lo_site))) - 1;
+    if (s.words[w] & ~allowed) throw std::invalid_argument("hex index has bits above site " + std::to_string(n - 1));
+  }
   return s;
 }
 
 // ------------------------------------------------------------ angles
-// Exact trig at half-integer multiples of pi (circuit.cpp:28-40).
+// Exact trig at half-integer multiples of pi (circuit.cpp:28-40): the
+// quarter-turn grid is looked up, everything else goes to libm.
 static double cos_pi(double r) {
   double f = std::fmod(r, 2.0);
   if (f < 0) f += 2.0;
-  double twice = 2.0 * f;
-  if (twice == std::floor(twice)) {
-    static constexpr double table[4] = {1.0, 0.0, -1.0, 0.0};
-    return table[static_cast<int>(twice) & 3];
+  const double quarter = 2.0 * f;
+  if (quarter == std::floor(quarter)) {
+    static constexpr double kGrid[4] = {1.0, 0.0, -1.0, 0.0};
+    return kGrid[static_cast<int>(quarter) & 3];
   }
   return std::cos(r * kPi);
 }
@@ -210,134 +321,135 @@ Angle Angle::from_pi_units(double r) {
 double Angle::cosine() const { return in_pi_units ? cos_pi(pi_units) : std::cos(radians); }
 double Angle::sine() const { return in_pi_units ? cos_pi(pi_units - 0.5) : std::sin(radians); }
 
+// "<number>" radians or "<number>pi" / "pi" / "-pi" pi units (circuit.cpp:65-87).
 Angle parse_angle(const std::string& text) {
-  std::string t = text;
-  bool pi = false;
-  if (t.size() >= 2 && (t.ends_with("pi") || t.ends_with("PI"))) {
-    pi = true;
-    t = t.substr(0, t.size() - 2);
-    if (t.empty() || t == "-" || t == "+") t += "1";
+  std::string number = text;
+  const bool pi_units = text.size() >= 2 && (text.compare(text.size() - 2, 2, "pi") == 0 ||
+                                             text.compare(text.size() - 2, 2, "PI") == 0);
+  if (pi_units) {
+    number.resize(number.size() - 2);
+    if (number.empty() || number == "+" || number == "-") number.push_back('1');  // "pi", "-pi"
   }
-  size_t pos = 0;
-  double v;
-  try {
-    v = std::stod(t, &pos);
-  } catch (const std::exception&) {
-    throw std::invalid_argument("invalid angle \"" + text + "\"");
-  }
-  if (pos != t.size()) throw std::invalid_argument("invalid angle \"" + text + "\"");
+  const char* begin = number.c_str();
+  char* end = nullptr;
+  errno = 0;
+  const double v = std::strtod(begin, &end);
+  if (end == begin || *end != '\0' || errno == ERANGE) throw std::invalid_argument("invalid angle \"" + text + "\"");
   if (!std::isfinite(v)) throw std::invalid_argument("angle must be finite: \"" + text + "\"");
-  return pi ? Angle::from_pi_units(v) : Angle::from_radians(v);
+  return pi_units ? Angle::from_pi_units(v) : Angle::from_radians(v);
 }
 
 Gate::Gate(const PauliString& g, Angle a)
     : generator(g), theta(a.radians), cos_theta(a.cosine()), sin_theta(a.sine()) {}
 
 size_t Circuit::total_gates() const {
-  size_t t = 0;
-  for (const auto& l : layers) t += l.size();
-  return t;
+  return std::accumulate(layers.begin(), layers.end(), size_t{0},
+                         [](size_t acc, const std::vector<Gate>& l) { return acc + l.size(); });
 }
 
-// "label angle" per line, blank line = layer break, '#' comments
-// (circuit.cpp:101-137).
+// Circuit text (circuit.cpp:101-137): one "<label> <angle>" gate per line;
+// the angle is the last token, everything before it is the label; blank
+// (or comment-only) lines close the current layer.
 Circuit parse_circuit_text(const std::string& text, int n) {
   Circuit c;
   c.n = n;
-  std::vector<Gate> layer;
-  std::istringstream in(text);
-  std::string line;
-  int lineno = 0;
-  while (std::getline(in, line)) {
-    ++lineno;
-    size_t h = line.find('#');
-    if (h != std::string::npos) line = line.substr(0, h);
-    size_t last = line.find_last_not_of(" \t\r");
-    if (last == std::string::npos) {
-      if (!layer.empty()) {
-        c.layers.push_back(std::move(layer));
-        layer.clear();
-      }
+  std::vector<Gate> open;
+  auto close_layer = [&] {
+    if (!open.empty()) c.layers.push_back(std::exchange(open, {}));
+  };
+  for (const TextLine& tl : split_lines(text)) {
+    if (tl.tokens.empty()) {
+      close_layer();
       continue;
     }
-    line = line.substr(0, last + 1);
-    size_t split = line.find_last_of(" \t");
-    if (split == std::string::npos)
-      throw std::invalid_argument("circuit line " + std::to_string(lineno) + ": expected \"pauli-label angle\"");
+    if (tl.tokens.size() < 2) line_error("circuit", tl.number, "expected \"pauli-label angle\"");
+    std::string label;
+    for (size_t k = 0; k + 1 < tl.tokens.size(); ++k) {
+      if (k) label.push_back(' ');
+      label.append(tl.tokens[k]);
+    }
     try {
-      layer.emplace_back(parse_pauli_label(line.substr(0, split), n), parse_angle(line.substr(split + 1)));
+      open.emplace_back(parse_pauli_label(label, n), parse_angle(std::string(tl.tokens.back())));
     } catch (const std::invalid_argument& e) {
-      throw std::invalid_argument("circuit line " + std::to_string(lineno) + ": " + e.what());
+      line_error("circuit", tl.number, e.what());
     }
   }
-  if (!layer.empty()) c.layers.push_back(std::move(layer));
+  close_layer();
   return c;
 }
 
 std::string format_circuit(const Circuit& c) {
-  std::ostringstream out;
-  char buf[32];
-  for (size_t l = 0; l < c.layers.size(); ++l) {
-    if (l) out << '\n';
-    for (const Gate& g : c.layers[l]) {
-      std::snprintf(buf, sizeof(buf), "%.17g", g.theta);
-      out << to_sparse_label(g.generator, c.n) << ' ' << buf << '\n';
+  std::string out;
+  char theta[40];
+  bool first_layer = true;
+  for (const auto& layer : c.layers) {
+    if (!first_layer) out.push_back('\n');
+    first_layer = false;
+    for (const Gate& g : layer) {
+      std::snprintf(theta, sizeof(theta), "%.17g", g.theta);
+      out += to_sparse_label(g.generator, c.n);
+      out.push_back(' ');
+      out += theta;
+      out.push_back('\n');
     }
   }
-  return out.str();
+  return out;
 }
 
 // ------------------------------------------------------------ geometry
-// "i j [color]" lines (models.cpp:27-105): same validation rules.
+// Edge-list text (models.cpp:27-105): "i j" or "i j color" per line, the
+// file either fully coloured or not at all, no self loops or repeated
+// edges, and each colour class a matching.  A line whose first token is not
+// an integer carries no edge.
 Geometry load_geometry_text(const std::string& text) {
-  Geometry g;
-  std::set<std::pair<int, int>> seen;
-  std::istringstream in(text);
-  std::string line;
-  int lineno = 0;
-  bool any_color = false, any_plain = false;
-  while (std::getline(in, line)) {
-    ++lineno;
-    size_t h = line.find('#');
-    if (h != std::string::npos) line = line.substr(0, h);
-    std::istringstream ls(line);
-    int i, j;
-    if (!(ls >> i)) continue;
-    if (!(ls >> j)) throw std::invalid_argument("geometry line " + std::to_string(lineno) + ": expected \"i j [color]\"");
-    int color = -1;
-    if (ls >> color) {
-      if (color < 0) throw std::invalid_argument("geometry line " + std::to_string(lineno) + ": negative color");
-      any_color = true;
-    } else {
-      any_plain = true;
+  struct Row {
+    int line, i, j, color;
+  };
+  std::vector<Row> rows;
+  for (const TextLine& tl : split_lines(text)) {
+    long long i = 0, j = 0, color = -1;
+    if (tl.tokens.empty() || !leading_int(tl.tokens[0], &i)) continue;
+    if (!token_int(tl.tokens[0], &i) || tl.tokens.size() < 2 || !leading_int(tl.tokens[1], &j))
+      line_error("geometry", tl.number, "expected \"i j [color]\"");
+    if (!token_int(tl.tokens[1], &j))
+      line_error("geometry", tl.number, "expected \"i j [color]\"");
+    size_t used = 2;
+    if (tl.tokens.size() > 2 && token_int(tl.tokens[2], &color)) {
+      if (color < 0) line_error("geometry", tl.number, "negative color");
+      used = 3;
     }
-    std::string trailing;
-    ls.clear();
-    if (ls >> trailing)
-      throw std::invalid_argument("geometry line " + std::to_string(lineno) + ": trailing content \"" + trailing + "\"");
-    if (i < 0 || j < 0) throw std::invalid_argument("geometry line " + std::to_string(lineno) + ": negative qubit index");
-    if (i == j) throw std::invalid_argument("geometry line " + std::to_string(lineno) + ": self loop on qubit " + std::to_string(i));
-    if (!seen.insert(std::minmax(i, j)).second)
-      throw std::invalid_argument("geometry line " + std::to_string(lineno) + ": duplicate edge " + std::to_string(i) +
-                                  "-" + std::to_string(j));
-    g.edges.emplace_back(i, j);
-    g.edge_colors.push_back(color);
-    g.n = std::max({g.n, i + 1, j + 1});
+    if (tl.tokens.size() > used)
+      line_error("geometry", tl.number, "trailing content \"" + std::string(tl.tokens[used]) + "\"");
+    if (i < 0 || j < 0) line_error("geometry", tl.number, "negative qubit index");
+    if (i == j) line_error("geometry", tl.number, "self loop on qubit " + std::to_string(i));
+    rows.push_back({tl.number, (int)i, (int)j, (int)color});
   }
-  if (g.edges.empty()) throw std::invalid_argument("geometry file has no edges");
-  if (any_color && any_plain) throw std::invalid_argument("geometry file mixes colored and uncolored edges");
-  if (!any_color) {
+  if (rows.empty()) throw std::invalid_argument("geometry file has no edges");
+
+  Geometry g;
+  std::set<std::pair<int, int>> undirected;
+  for (const Row& r : rows) {
+    if (!undirected.emplace(std::min(r.i, r.j), std::max(r.i, r.j)).second)
+      line_error("geometry", r.line, "duplicate edge " + std::to_string(r.i) + "-" + std::to_string(r.j));
+    g.edges.emplace_back(r.i, r.j);
+    g.edge_colors.push_back(r.color);
+    g.n = std::max(g.n, std::max(r.i, r.j) + 1);
+  }
+  const size_t coloured = (size_t)std::count_if(rows.begin(), rows.end(), [](const Row& r) { return r.color >= 0; });
+  if (coloured != 0 && coloured != rows.size())
+    throw std::invalid_argument("geometry file mixes colored and uncolored edges");
+  if (coloured == 0) {
     g.edge_colors.clear();
     return g;
   }
   g.color_count = 1 + *std::max_element(g.edge_colors.begin(), g.edge_colors.end());
-  std::vector<std::set<int>> used(g.color_count);
+  // (qubit, colour) pairs must be unique: every colour class is a matching
+  std::set<std::pair<int, int>> incident;
   for (size_t e = 0; e < g.edges.size(); ++e) {
-    auto [i, j] = g.edges[e];
-    auto& q = used[g.edge_colors[e]];
-    if (!q.insert(i).second || !q.insert(j).second)
-      throw std::invalid_argument("edges overlap within color " + std::to_string(g.edge_colors[e]) + " at edge " +
-                                  std::to_string(i) + "-" + std::to_string(j));
+    const int col = g.edge_colors[e];
+    if (!incident.emplace(g.edges[e].first, col).second || !incident.emplace(g.edges[e].second, col).second)
+      throw std::invalid_argument("edges overlap within color " + std::to_string(col) + " at edge " +
+                                  std::to_string(g.edges[e].first) + "-" + std::to_string(g.edges[e].second));
   }
   return g;
 }
@@ -350,115 +462,62 @@ Geometry load_geometry_file(const std::string& path) {
   return load_geometry_text(ss.str());
 }
 
-// Heavy-hex, 127 qubits, following the construction of BASELINE.json
-// config 1: rows are numbered row-major with each gap's 4 bridge qubits
-// interleaved after the row above it; row 0 has cols 0-13, rows 1-5 cols
-// 0-14, row 6 cols 1-14; bridges sit at cols {0,4,8,12} below even rows and
-// {2,6,10,14} below odd rows.  Edges are coloured by a deterministic
-// backtracking 3-edge-colouring (no two edges of a colour share a qubit).
+#include "heavy_hex_127.inc"
+
+// The reference's bundled 127-qubit heavy-hex map, same edges, colours and
+// edge order (models.cpp:120 loads data/heavy_hex_127.txt through
+// heavy_hex_data.cpp:21), so build_kicked_ising produces the reference's gate
+// order.  It equals the BASELINE.json config-1 row/bridge construction.
 Geometry heavy_hex_127() {
-  std::vector<std::vector<int>> row_q(7, std::vector<int>(15, -1));
-  std::vector<std::array<int, 4>> bridge_q(6);
-  int q = 0;
-  for (int r = 0; r < 7; ++r) {
-    int c0 = r == 6 ? 1 : 0, c1 = r == 0 ? 13 : 14;
-    for (int c = c0; c <= c1; ++c) row_q[r][c] = q++;
-    if (r < 6)
-      for (int b = 0; b < 4; ++b) bridge_q[r][b] = q++;
+  Geometry g;
+  g.n = 127;
+  g.color_count = 3;
+  for (const auto& e : kHeavyHex127) {
+    g.edges.emplace_back(e[0], e[1]);
+    g.edge_colors.push_back(e[2]);
   }
-  std::vector<std::pair<int, int>> edges;
-  for (int r = 0; r < 7; ++r)
-    for (int c = 0; c < 14; ++c)
-      if (row_q[r][c] >= 0 && row_q[r][c + 1] >= 0) edges.emplace_back(row_q[r][c], row_q[r][c + 1]);
-  for (int r = 0; r < 6; ++r)
-    for (int b = 0; b < 4; ++b) {
-      int col = (r % 2 == 0 ? 0 : 2) + 4 * b;
-      edges.emplace_back(row_q[r][col], bridge_q[r][b]);
-      edges.emplace_back(bridge_q[r][b], row_q[r + 1][col]);
-    }
-  // 3-edge-colouring of this bipartite (all cycles have length 12), degree-3
-  // graph by alternating-path recolouring (Koenig): colour edges in order;
-  // if no colour is free at both ends, swap the (a, b) path from v.
-  const int E = (int)edges.size();
-  std::vector<int> color(E, -1);
-  std::vector<std::array<int, 3>> at(q, {-1, -1, -1});  // at[v][c] = edge of colour c at v
-  for (int e = 0; e < E; ++e) {
-    auto [u, v] = edges[e];
-    int a = -1, b = -1;
-    for (int c = 0; c < 3 && a < 0; ++c)
-      if (at[u][c] < 0) a = c;
-    for (int c = 0; c < 3 && b < 0; ++c)
-      if (at[v][c] < 0) b = c;
-    if (at[v][a] >= 0) {
-      // walk the path from v alternating colours a, b and swap them
-      std::vector<int> path;
-      int x = v, col = a;
-      while (at[x][col] >= 0) {
-        int pe = at[x][col];
-        path.push_back(pe);
-        x = edges[pe].first == x ? edges[pe].second : edges[pe].first;
-        col = col == a ? b : a;
-      }
-      for (int pe : path) {
-        at[edges[pe].first][color[pe]] = -1;
-        at[edges[pe].second][color[pe]] = -1;
-      }
-      for (int pe : path) {
-        color[pe] = color[pe] == a ? b : a;
-        at[edges[pe].first][color[pe]] = pe;
-        at[edges[pe].second][color[pe]] = pe;
-      }
-    }
-    if (at[u][a] >= 0 || at[v][a] >= 0) throw std::logic_error("heavy-hex colouring failed");
-    color[e] = a;
-    at[u][a] = at[v][a] = e;
-  }
-  std::ostringstream text;
-  for (int e = 0; e < E; ++e) text << edges[e].first << ' ' << edges[e].second << ' ' << color[e] << '\n';
-  return load_geometry_text(text.str());
+  return g;
 }
 
+// Qubits within graph distance `radius` of `start`, ascending
+// (models.cpp:122-147), by frontier expansion over a CSR adjacency.
 std::vector<int> bfs_ball(const Geometry& geom, int start, int radius) {
-  std::vector<std::vector<int>> adj(geom.n);
-  for (auto [i, j] : geom.edges) {
-    adj[i].push_back(j);
-    adj[j].push_back(i);
-  }
-  std::vector<int> dist(geom.n, -1);
-  std::deque<int> qu{start};
-  dist[start] = 0;
-  while (!qu.empty()) {
-    int u = qu.front();
-    qu.pop_front();
-    if (dist[u] == radius) continue;
-    for (int v : adj[u])
-      if (dist[v] < 0) {
-        dist[v] = dist[u] + 1;
-        qu.push_back(v);
-      }
+  std::vector<int> offset(geom.n + 1, 0), nbr(2 * geom.edges.size());
+  for (auto [a, b] : geom.edges) ++offset[a + 1], ++offset[b + 1];
+  std::partial_sum(offset.begin(), offset.end(), offset.begin());
+  std::vector<int> fill(offset.begin(), offset.end() - 1);
+  for (auto [a, b] : geom.edges) nbr[fill[a]++] = b, nbr[fill[b]++] = a;
+  std::vector<char> in_ball(geom.n, 0);
+  std::vector<int> frontier{start}, next;
+  in_ball[start] = 1;
+  for (int d = 0; d < radius && !frontier.empty(); ++d) {
+    next.clear();
+    for (int u : frontier)
+      for (int k = offset[u]; k < offset[u + 1]; ++k)
+        if (!in_ball[nbr[k]]) in_ball[nbr[k]] = 1, next.push_back(nbr[k]);
+    frontier.swap(next);
   }
   std::vector<int> ball;
-  for (int i = 0; i < geom.n; ++i)
-    if (dist[i] >= 0) ball.push_back(i);
+  for (int q = 0; q < geom.n; ++q)
+    if (in_ball[q]) ball.push_back(q);
   return ball;
 }
 
-// One Trotter step: X rotations on qubits 0..n-1 ascending, then ZZ
-// rotations colour by colour in edge-list order (models.cpp:149-171).
+// One Trotter step (models.cpp:149-171): X on every qubit in index order,
+// then the ZZ bonds colour class by colour class, each class in edge-list
+// order (a stable sort of the edges by colour).
 std::vector<Gate> kicked_ising_layer(const Geometry& geom, Angle theta_x, Angle theta_zz) {
+  std::vector<size_t> order(geom.edges.size());
+  std::iota(order.begin(), order.end(), size_t{0});
+  if (geom.has_coloring())
+    std::stable_sort(order.begin(), order.end(),
+                     [&](size_t a, size_t b) { return geom.edge_colors[a] < geom.edge_colors[b]; });
   std::vector<Gate> layer;
-  layer.reserve(geom.n + geom.edges.size());
+  layer.reserve(geom.n + order.size());
   for (int q = 0; q < geom.n; ++q) layer.emplace_back(single_site(q, Pauli::X), theta_x);
-  auto add = [&](size_t e) {
-    auto [i, j] = geom.edges[e];
-    layer.emplace_back(single_site(i, Pauli::Z) ^ single_site(j, Pauli::Z), theta_zz);
-  };
-  if (geom.has_coloring()) {
-    for (int c = 0; c < geom.color_count; ++c)
-      for (size_t e = 0; e < geom.edges.size(); ++e)
-        if (geom.edge_colors[e] == c) add(e);
-  } else {
-    for (size_t e = 0; e < geom.edges.size(); ++e) add(e);
+  for (size_t e : order) {
+    const auto [a, b] = geom.edges[e];
+    layer.emplace_back(single_site(a, Pauli::Z) ^ single_site(b, Pauli::Z), theta_zz);
   }
   return layer;
 }
@@ -467,14 +526,18 @@ Circuit build_kicked_ising(const Geometry& geom, Angle theta_x, Angle theta_zz, 
   if (layers < 1) throw std::invalid_argument("layer count must be >= 1");
   Circuit c;
   c.n = geom.n;
-  c.layers.assign(layers, kicked_ising_layer(geom, theta_x, theta_zz));
+  c.layers = std::vector<std::vector<Gate>>(layers, kicked_ising_layer(geom, theta_x, theta_zz));
   return c;
 }
 
 // ------------------------------------------------------------ partition
+// The paper's block-sum owner map (partition.cpp:35-59),
+// kept for the ledger's worker accounting: owner = (sum over the k-bit blocks
+// of the packed 2n-bit index [+ hash % s]) mod workers.  Summing k-bit blocks
+// weighs bit i by 2^(i mod k), which is how it is evaluated here.
 uint32_t PartitionSpec::default_block_size(uint32_t workers) {
   uint32_t k = 1;
-  while ((uint64_t{1} << k) < workers) ++k;
+  while (k < 32 && (uint64_t{1} << k) < workers) ++k;
   return k;
 }
 PartitionSpec PartitionSpec::make(uint32_t workers, uint32_t k, uint32_t s) {
@@ -483,28 +546,118 @@ PartitionSpec PartitionSpec::make(uint32_t workers, uint32_t k, uint32_t s) {
   if (s < 1) throw std::invalid_argument("perturbation_s must be >= 1");
   return PartitionSpec{workers, k, s};
 }
-// Block-sum owner map, paper Eq. 9 (partition.cpp:53-59).
-uint32_t owner(const PartitionSpec& spec, const PauliString& index, int n) {
-  const uint32_t k = spec.block_size_bits;
-  const uint32_t blocks = (2 * (uint32_t)n + k - 1) / k;
+uint64_t block_sum(const PauliString& index, int n, uint32_t k) {
+  const uint32_t span = (2u * (uint32_t)n + k - 1) / k * k;  // whole blocks cover the 2n bits
   uint64_t sum = 0;
-  for (uint32_t j = 0; j < blocks; ++j) {
-    uint64_t lo = (uint64_t)j * k;
-    size_t w = lo >> 6;
-    if (w >= index.words.size()) continue;
-    int sh = (int)(lo & 63);
-    uint64_t v = index.words[w] >> sh;
-    if (sh + (int)k > 64 && w + 1 < index.words.size()) v |= index.words[w + 1] << (64 - sh);
-    sum += v & ((uint64_t{1} << k) - 1);
+  for (int w = 0; w < kIndexWords; ++w) {
+    for (uint64_t v = index.words[w]; v; v &= v - 1) {
+      const uint32_t bit = 64u * w + (uint32_t)__builtin_ctzll(v);
+      if (bit < span) sum += uint64_t{1} << (bit % k);
+    }
   }
+  return sum;
+}
+uint32_t owner(const PartitionSpec& spec, const PauliString& index, int n) {
+  uint64_t sum = block_sum(index, n, spec.block_size_bits);
   if (spec.perturbation_s > 1) sum += hash_string(index) % spec.perturbation_s;
   return (uint32_t)(sum % spec.worker_count);
 }
 double uniformity_ratio(const std::vector<size_t>& sizes) {
   if (sizes.empty()) throw std::invalid_argument("uniformity_ratio needs at least one shard");
-  auto [lo, hi] = std::minmax_element(sizes.begin(), sizes.end());
-  if (*lo == 0) return std::numeric_limits<double>::infinity();
-  return double(*hi) / double(*lo);
+  const auto [lo, hi] = std::minmax_element(sizes.begin(), sizes.end());
+  return *lo == 0 ? std::numeric_limits<double>::infinity() : double(*hi) / double(*lo);
+}
+
+
+std::vector<uint32_t> destination_set(const PartitionSpec& spec, uint32_t m, const PauliString& J, int n) {
+  const uint32_t N = spec.worker_count;
+  std::vector<uint32_t> out;
+  if (spec.perturbation_s > 1) {  // the perturbed map bounds nothing
+    for (uint32_t r = 0; r < N; ++r) out.push_back(r);
+    return out;
+  }
+  // XOR-ing a k-bit block j of J into a source block b moves the block sum by
+  // jb - 2 (b & jb) for some subset of jb's bits; the residues mod N reachable
+  // by summing one such move per block of J are the possible owner shifts.
+  const uint32_t k = spec.block_size_bits;
+  const uint32_t span = (2u * (uint32_t)n + k - 1) / k * k;
+  std::vector<uint64_t> jblocks;
+  for (uint32_t lo = 0; lo < span; lo += k) {
+    uint64_t v = 0;
+    for (uint32_t b = 0; b < k && lo + b < 64u * kIndexWords; ++b)
+      v |= ((J.words[(lo + b) / 64] >> ((lo + b) % 64)) & 1u) << b;
+    if (v) jblocks.push_back(v);
+  }
+  std::vector<char> reach(N, 0), next(N);
+  reach[0] = 1;
+  for (uint64_t jb : jblocks) {
+    std::fill(next.begin(), next.end(), 0);
+    for (uint64_t sub = jb;; sub = (sub - 1) & jb) {  // every subset of jb's bits
+      const int64_t d = (int64_t)jb - 2 * (int64_t)sub;
+      const uint32_t dm = (uint32_t)(((d % (int64_t)N) + (int64_t)N) % (int64_t)N);
+      for (uint32_t r = 0; r < N; ++r)
+        if (reach[r]) next[(r + dm) % N] = 1;
+      if (sub == 0) break;
+    }
+    reach.swap(next);
+  }
+  for (uint32_t r = 0; r < N; ++r)
+    if (reach[r]) out.push_back((m + r) % N);
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+// ------------------------------------------------------------ dense check
+// A Pauli string on the computational basis: P|b> = i^ny (-1)^popc(b & z) |b ^ x>
+// with x, z its bit planes (site q -> bit q) and ny its number of Y sites.
+namespace {
+struct BasisAction {
+  uint64_t x = 0, z = 0;
+  int ny = 0;
+};
+BasisAction basis_action(const PauliString& s, int n) {
+  BasisAction a;
+  for (int q = 0; q < n; ++q) {
+    const uint8_t c = s.code_at(q);
+    if (c == 1 || c == 2) a.x |= uint64_t{1} << q;
+    if (c == 2 || c == 3) a.z |= uint64_t{1} << q;
+    if (c == 2) ++a.ny;
+  }
+  return a;
+}
+std::complex<double> basis_phase(const BasisAction& a, uint64_t b) {
+  static const std::complex<double> ipow[4] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+  std::complex<double> p = ipow[a.ny & 3];
+  return (__builtin_popcountll(b & a.z) & 1) ? -p : p;
+}
+}  // namespace
+
+double state_vector_expectation(const Circuit& circuit, const PauliString& observable) {
+  const int n = circuit.n;
+  if (n < 1 || n > 26) throw std::invalid_argument("state_vector_expectation supports 1 <= n <= 26, got " + std::to_string(n));
+  std::vector<std::complex<double>> psi(size_t{1} << n);
+  psi[0] = 1.0;
+  for (const auto& layer : circuit.layers) {
+    for (const Gate& g : layer) {  // psi <- (cos(t/2) - i sin(t/2) P) psi, forward in time
+      const BasisAction a = basis_action(g.generator, n);
+      const std::complex<double> c(std::cos(0.5 * g.theta), 0.0), ms(0.0, -std::sin(0.5 * g.theta));
+      for (uint64_t b = 0; b < psi.size(); ++b) {
+        const uint64_t p = b ^ a.x;
+        if (p < b) continue;
+        if (p == b) {  // diagonal generator: a phase per basis state
+          psi[b] *= c + ms * basis_phase(a, b);
+          continue;
+        }
+        const std::complex<double> vb = psi[b], vp = psi[p];
+        psi[b] = c * vb + ms * basis_phase(a, p) * vp;  // <b|P|p> = phase(p)
+        psi[p] = c * vp + ms * basis_phase(a, b) * vb;
+      }
+    }
+  }
+  const BasisAction o = basis_action(observable, n);
+  std::complex<double> acc = 0.0;
+  for (uint64_t b = 0; b < psi.size(); ++b) acc += std::conj(psi[b ^ o.x]) * basis_phase(o, b) * psi[b];
+  return acc.real();
 }
 
 // ------------------------------------------------------------ ledger

@@ -106,8 +106,8 @@ struct Geometry {
 };
 Geometry load_geometry_text(const std::string& text);
 Geometry load_geometry_file(const std::string& path);
-// 127-qubit heavy-hex lattice built from the row/bridge rule of
-// BASELINE.json config 1, 3-edge-coloured deterministically.
+// The reference's bundled 127-qubit heavy-hex map (models.cpp:120): same
+// edges, colours and edge order, hence the same kicked-Ising gate order.
 Geometry heavy_hex_127();
 std::vector<int> bfs_ball(const Geometry& geom, int start, int radius);
 std::vector<Gate> kicked_ising_layer(const Geometry& geom, Angle theta_x, Angle theta_zz);
@@ -123,8 +123,16 @@ struct PartitionSpec {
   static uint32_t default_block_size(uint32_t workers);
   static PartitionSpec make(uint32_t workers, uint32_t block_size_bits, uint32_t perturbation_s = 1);
 };
+uint64_t block_sum(const PauliString& index, int n, uint32_t block_size_bits);
 uint32_t owner(const PartitionSpec& spec, const PauliString& index, int n);
 double uniformity_ratio(const std::vector<size_t>& shard_sizes);
+// Owners that can receive a record from worker m for generator J
+// (partition.cpp:61-108): every worker when the map is perturbed.
+std::vector<uint32_t> destination_set(const PartitionSpec& spec, uint32_t m, const PauliString& J, int n);
+
+// Dense check: <0|U^dag O U|0> by forward state-vector evolution from |0..0>
+// (the reference's oracle::evolve_state / expectation, n <= 26).
+double state_vector_expectation(const Circuit& circuit, const PauliString& observable);
 
 // ---------------------------------------------------------------- engine
 enum class TruncationCadence { PerGate, PerLayer };

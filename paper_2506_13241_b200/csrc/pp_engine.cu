@@ -9,6 +9,7 @@
 // threshold epsilon0 * gmax, remove |c| <= threshold).
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -131,6 +132,25 @@ static void planes_to_words(const uint64_t* x, const uint64_t* z, uint64_t* w) {
     w[2 * pw] = spread_even(lo) | (spread_even(hi) << 1);
     w[2 * pw + 1] = spread_even(lo >> 32) | (spread_even(hi >> 32) << 1);
   }
+}
+
+// Host<->device transfer accounting (process-wide, every engine): the bytes
+// of every explicit copy plus the kernel parameter blocks that carry host
+// data (gate lists, initial terms).  bench.py reads the totals around the
+// public call to report e2e h2d/d2h bytes as counted, not modelled.
+static std::atomic<unsigned long long> g_h2d_bytes{0}, g_d2h_bytes{0};
+static inline void count_xfer(cudaMemcpyKind k, size_t n) {
+  if (k == cudaMemcpyHostToDevice) g_h2d_bytes.fetch_add(n, std::memory_order_relaxed);
+  else if (k == cudaMemcpyDeviceToHost) g_d2h_bytes.fetch_add(n, std::memory_order_relaxed);
+}
+static inline void count_param_h2d(size_t n) { g_h2d_bytes.fetch_add(n, std::memory_order_relaxed); }
+static inline cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k, cudaStream_t s) {
+  count_xfer(k, n);
+  return cudaMemcpyAsync(dst, src, n, k, s);
+}
+static inline cudaError_t copy_sync(void* dst, const void* src, size_t n, cudaMemcpyKind k) {
+  count_xfer(k, n);
+  return cudaMemcpy(dst, src, n, k);
 }
 
 static inline bool is_clifford(const pp_gate& g) {
@@ -541,6 +561,7 @@ class EngineImpl final : public EngineBase {
         in.gmax[q] = gmx[q];
         in.gmin[q] = gmn[q];
       }
+      count_param_h2d(sizeof(in));  // the initial terms travel in the parameter block
       k_init_small<W><<<1, 32, 0, stream_>>>(aview(0), gview(0), in, d_stats_);
       ++launches_;
       PP_CUDA(cudaGetLastError());
@@ -551,22 +572,22 @@ class EngineImpl final : public EngineBase {
     if (n && !n_small_init_) {
       ArenaView<W> a = aview(0);
       for (int j = 0; j < W; ++j)
-        PP_CUDA(cudaMemcpyAsync(a.x[j], hx.data() + j * n, n * 8, cudaMemcpyHostToDevice, stream_));
-      PP_CUDA(cudaMemcpyAsync(a.c, hc.data(), n * 8, cudaMemcpyHostToDevice, stream_));
+        PP_CUDA(copy_async(a.x[j], hx.data() + j * n, n * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(a.c, hc.data(), n * 8, cudaMemcpyHostToDevice, stream_));
     }
     if (G && !n_small_init_) {
       GroupView<W> g = gview(0);
       std::vector<uint64_t> zt(G);
       for (int j = 0; j < W; ++j) {
         for (uint32_t q = 0; q < G; ++q) zt[q] = gz[q * W + j];
-        PP_CUDA(cudaMemcpyAsync(g.z[j], zt.data(), G * 8, cudaMemcpyHostToDevice, stream_));
+        PP_CUDA(copy_async(g.z[j], zt.data(), G * 8, cudaMemcpyHostToDevice, stream_));
       }
-      PP_CUDA(cudaMemcpyAsync(g.off, goff.data(), G * 8, cudaMemcpyHostToDevice, stream_));
-      PP_CUDA(cudaMemcpyAsync(g.cnt, gcnt.data(), G * 4, cudaMemcpyHostToDevice, stream_));
-      PP_CUDA(cudaMemcpyAsync(g.cap, gcnt.data(), G * 4, cudaMemcpyHostToDevice, stream_));
-      PP_CUDA(cudaMemcpyAsync(g.gmax, gmx.data(), G * 8, cudaMemcpyHostToDevice, stream_));
-      PP_CUDA(cudaMemcpyAsync(g.gmin, gmn.data(), G * 8, cudaMemcpyHostToDevice, stream_));
-      PP_CUDA(cudaMemcpyAsync(g.flags, gfl.data(), G * 4, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(g.off, goff.data(), G * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(g.cnt, gcnt.data(), G * 4, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(g.cap, gcnt.data(), G * 4, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(g.gmax, gmx.data(), G * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(g.gmin, gmn.data(), G * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(g.flags, gfl.data(), G * 4, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemsetAsync(g.stamp, 0xff, G * 4, stream_));
     }
     if (!n_small_init_) {
@@ -796,6 +817,7 @@ class EngineImpl final : public EngineBase {
         cudaGraphExec_t exec = rx_graph(prm, epi, do_trunc, budget, lazy);
         std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
         PP_CUDA(cudaEventRecord(ev.first, stream_));
+        count_param_h2d(count * sizeof(RxParam));  // the gate parameters baked into the graph
         PP_CUDA(cudaGraphLaunch(exec, stream_));
         PP_CUDA(cudaEventRecord(ev.second, stream_));
         pending_events_.push_back(ev);
@@ -865,14 +887,15 @@ class EngineImpl final : public EngineBase {
       // snapshot of the group table: the rollback point
       const size_t gbytes = (size_t)groups_[gcur_].cap * (8 * W + 8 + 8 + 8 + 4 + 4 + 4 + 4);
       backup_.ensure(gbytes);
-      PP_CUDA(cudaMemcpyAsync(backup_.p, groups_[gcur_].buf.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
+      PP_CUDA(copy_async(backup_.p, groups_[gcur_].buf.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
       const uint32_t G_saved = G_;
       const pp_counters saved = counters_;
-      PP_CUDA(cudaMemcpyAsync(d_tpred, tpred.data(), count * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(d_tpred, tpred.data(), count * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemsetAsync(d_gmax, 0, count * 8, stream_));
       push_scalars(seq0);
       std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
       PP_CUDA(cudaEventRecord(ev.first, stream_));
+      count_param_h2d(sizeof(sgates));
       k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
           gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_tpred, d_gmax, d_stats_);
       PP_CUDA(cudaEventRecord(ev.second, stream_));
@@ -880,7 +903,7 @@ class EngineImpl final : public EngineBase {
       ++launches_;
       ++branch_launches_;
       std::vector<unsigned long long> gm(count);
-      PP_CUDA(cudaMemcpyAsync(gm.data(), d_gmax, count * 8, cudaMemcpyDeviceToHost, stream_));
+      PP_CUDA(copy_async(gm.data(), d_gmax, count * 8, cudaMemcpyDeviceToHost, stream_));
       dirty_ = true;
       sync_state();  // harvests counters, reads the arena fault flag
       bool exact = !arena_fault_;
@@ -906,7 +929,7 @@ class EngineImpl final : public EngineBase {
         return true;
       }
       // roll back: restore the table (the old regions are untouched)
-      PP_CUDA(cudaMemcpyAsync(groups_[gcur_].buf.p, backup_.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
+      PP_CUDA(copy_async(groups_[gcur_].buf.p, backup_.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
       G_ = G_saved;
       counters_ = saved;
       if (std::getenv("PP_DEBUG")) {
@@ -951,6 +974,7 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaEventRecord(ev.first, stream_));
     // persistent grid, but no more CTAs than a few per group (tiny layers)
     const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(sub_grid_, 4u * G_));
+    count_param_h2d(sizeof(sub_gates_));  // the run's gate list
     k_branch_sublayer<W><<<grid, kCta, branch_smem_bytes<W>(), stream_>>>(
         gview(gcur_), aview(cur_), sub_gates_, keep_zeros_, &d_stats_->work[0], nullptr, nullptr, d_stats_);
     PP_CUDA(cudaEventRecord(ev.second, stream_));
@@ -987,6 +1011,7 @@ class EngineImpl final : public EngineBase {
   }
 
   void launch_branch(const RxParam& p, uint32_t rel, bool lazy) {
+    count_param_h2d(sizeof(RxParam));
     k_branch_x<W><<<branch_grid_, kCta, branch_x_smem_bytes<W>(), stream_>>>(
         gview(gcur_), aview(cur_), p.wq, p.mq, p.cosv, p.sinv, keep_zeros_, gview(gcur_).z[p.wq],
         &d_stats_->work[rel & 1], &d_stats_->work[(rel + 1) & 1], rel, d_stats_,
@@ -1114,8 +1139,8 @@ class EngineImpl final : public EngineBase {
       std::memcpy(z.data(), h_diag_->z, nd * W * 8);
       std::memcpy(c.data(), h_diag_->c, nd * 8);
     } else {
-      PP_CUDA(cudaMemcpyAsync(z.data(), diag_z_.p, nd * W * 8, cudaMemcpyDeviceToHost, stream_));
-      PP_CUDA(cudaMemcpyAsync(c.data(), diag_c_.p, nd * 8, cudaMemcpyDeviceToHost, stream_));
+      PP_CUDA(copy_async(z.data(), diag_z_.p, nd * W * 8, cudaMemcpyDeviceToHost, stream_));
+      PP_CUDA(copy_async(c.data(), diag_c_.p, nd * 8, cudaMemcpyDeviceToHost, stream_));
       PP_CUDA(cudaStreamSynchronize(stream_));
     }
     std::vector<uint64_t> order(nd);
@@ -1147,22 +1172,22 @@ class EngineImpl final : public EngineBase {
     std::vector<uint64_t> gz(G_);
     std::vector<uint32_t> match(G_, 1);
     for (int k = 0; k < W; ++k) {
-      PP_CUDA(cudaMemcpy(gz.data(), g.z[k], G_ * 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(copy_sync(gz.data(), g.z[k], G_ * 8, cudaMemcpyDeviceToHost));
       for (uint32_t i = 0; i < G_; ++i) match[i] &= gz[i] == z[k];
     }
     for (uint32_t i = 0; i < G_; ++i) {
       if (!match[i]) continue;
       uint64_t off;
       uint32_t cnt;
-      PP_CUDA(cudaMemcpy(&off, g.off + i, 8, cudaMemcpyDeviceToHost));
-      PP_CUDA(cudaMemcpy(&cnt, g.cnt + i, 4, cudaMemcpyDeviceToHost));
+      PP_CUDA(copy_sync(&off, g.off + i, 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(copy_sync(&cnt, g.cnt + i, 4, cudaMemcpyDeviceToHost));
       if (!cnt) continue;
       ArenaView<W> a = aview(cur_);
       std::vector<uint64_t> xs(cnt * W);
       std::vector<double> cs(cnt);
       for (int k = 0; k < W; ++k)
-        PP_CUDA(cudaMemcpy(xs.data() + k * cnt, a.x[k] + off, cnt * 8, cudaMemcpyDeviceToHost));
-      PP_CUDA(cudaMemcpy(cs.data(), a.c + off, cnt * 8, cudaMemcpyDeviceToHost));
+        PP_CUDA(copy_sync(xs.data() + k * cnt, a.x[k] + off, cnt * 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(copy_sync(cs.data(), a.c + off, cnt * 8, cudaMemcpyDeviceToHost));
       for (uint32_t e = 0; e < cnt; ++e) {
         bool eq = true;
         for (int k = 0; k < W; ++k) eq &= xs[k * cnt + e] == x[k];
@@ -1187,15 +1212,15 @@ class EngineImpl final : public EngineBase {
     if (n) {
       ArenaView<W> a = aview(cur_);
       for (int k = 0; k < W; ++k)
-        PP_CUDA(cudaMemcpy(xs.data() + k * n, a.x[k], n * 8, cudaMemcpyDeviceToHost));
-      PP_CUDA(cudaMemcpy(cs.data(), a.c, n * 8, cudaMemcpyDeviceToHost));
+        PP_CUDA(copy_sync(xs.data() + k * n, a.x[k], n * 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(copy_sync(cs.data(), a.c, n * 8, cudaMemcpyDeviceToHost));
     }
     if (G_) {
       GroupView<W> g = gview(gcur_);
-      PP_CUDA(cudaMemcpy(goff.data(), g.off, G_ * 8, cudaMemcpyDeviceToHost));
-      PP_CUDA(cudaMemcpy(gcnt.data(), g.cnt, G_ * 4, cudaMemcpyDeviceToHost));
+      PP_CUDA(copy_sync(goff.data(), g.off, G_ * 8, cudaMemcpyDeviceToHost));
+      PP_CUDA(copy_sync(gcnt.data(), g.cnt, G_ * 4, cudaMemcpyDeviceToHost));
       for (int k = 0; k < W; ++k)
-        PP_CUDA(cudaMemcpy(gz.data() + k * G_, g.z[k], G_ * 8, cudaMemcpyDeviceToHost));
+        PP_CUDA(copy_sync(gz.data() + k * G_, g.z[k], G_ * 8, cudaMemcpyDeviceToHost));
     }
     std::vector<std::array<uint64_t, 4>> out;
     std::vector<double> outc;
@@ -1262,7 +1287,7 @@ class EngineImpl final : public EngineBase {
     push_scalars(bseq_);
     k_norm2<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), aview(cur_), d_stats_, acc);
     double h = 0.0;
-    PP_CUDA(cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(copy_async(&h, acc, 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
     return h;
   }
@@ -1280,8 +1305,8 @@ class EngineImpl final : public EngineBase {
     k_histogram<W><<<persistent_grid(), kCta, smem, stream_>>>(gview(gcur_), aview(cur_), d_stats_, bins, gmax,
                                                                lower, std::log(lower), d, d + bins);
     ++launches_;
-    PP_CUDA(cudaMemcpyAsync(pos, d, 8 * (size_t)bins, cudaMemcpyDeviceToHost, stream_));
-    PP_CUDA(cudaMemcpyAsync(neg, d + bins, 8 * (size_t)bins, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(copy_async(pos, d, 8 * (size_t)bins, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(copy_async(neg, d + bins, 8 * (size_t)bins, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
   }
 
@@ -1295,7 +1320,7 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(cudaMemsetAsync(dcnt, 0, world * 8, stream_));
     k_evict_count<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, world, rank, seed, dcnt);
     std::vector<unsigned long long> hc(world);
-    PP_CUDA(cudaMemcpyAsync(hc.data(), dcnt, world * 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(copy_async(hc.data(), dcnt, world * 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
     uint64_t total = 0;
     std::vector<unsigned long long> off(world);
@@ -1308,11 +1333,11 @@ class EngineImpl final : public EngineBase {
     if (total == 0) return;
     const int rw = 2 * W + 1;
     evict_buf_.ensure(total * rw * 8);
-    PP_CUDA(cudaMemcpyAsync(dcnt + world, off.data(), world * 8, cudaMemcpyHostToDevice, stream_));
+    PP_CUDA(copy_async(dcnt + world, off.data(), world * 8, cudaMemcpyHostToDevice, stream_));
     k_evict_write<W><<<G_, kCta, 0, stream_>>>(gview(gcur_), aview(cur_), world, rank, seed, dcnt + world,
                                                evict_buf_.as<uint64_t>());
     if (out)  // host-staged exchange; otherwise the records stay in evict_buf_ (device_records())
-      PP_CUDA(cudaMemcpyAsync(out, evict_buf_.p, total * rw * 8, cudaMemcpyDeviceToHost, stream_));
+      PP_CUDA(copy_async(out, evict_buf_.p, total * rw * 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
     launches_ += 2;
     dirty_ = true;
@@ -1327,7 +1352,7 @@ class EngineImpl final : public EngineBase {
     const int rw = 2 * W + 1;
     if (bump_ + count > arena_[cur_].cap) gc_into_other(std::max<uint64_t>(next_arena_target(), live_ + 2 * count));
     evict_buf_.ensure(count * rw * 8);
-    PP_CUDA(cudaMemcpyAsync(evict_buf_.p, rec, count * rw * 8,
+    PP_CUDA(copy_async(evict_buf_.p, rec, count * rw * 8,
                             device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
     rec_slot_.ensure(count * 4);
     uint32_t* flags = rec_slot_.as<uint32_t>();
@@ -1338,7 +1363,7 @@ class EngineImpl final : public EngineBase {
     scan_gid_.ensure(count * 8);
     device_scan(flags, count, 1, scan_gid_.as<unsigned long long>(), ntiles);
     unsigned long long nruns = 0;
-    PP_CUDA(cudaMemcpyAsync(&nruns, scan_tmp_.as<unsigned long long>() + ntiles, 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(copy_async(&nruns, scan_tmp_.as<unsigned long long>() + ntiles, 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
     grow_groups_preserving(G_ + (uint32_t)nruns);
     k_ingest_append<W><<<(uint32_t)((count + kCta - 1) / kCta), kCta, 0, stream_>>>(
@@ -1361,14 +1386,14 @@ class EngineImpl final : public EngineBase {
     const int o = 1 - gcur_;
     ensure_groups(o, std::max<uint32_t>(cap, 2 * groups_[gcur_].cap));
     GroupView<W> a = gview(gcur_), b = gview(o);
-    for (int k = 0; k < W; ++k) PP_CUDA(cudaMemcpyAsync(b.z[k], a.z[k], G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(b.off, a.off, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(b.gmax, a.gmax, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(b.gmin, a.gmin, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(b.cnt, a.cnt, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(b.cap, a.cap, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(b.flags, a.flags, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
-    PP_CUDA(cudaMemcpyAsync(b.stamp, a.stamp, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
+    for (int k = 0; k < W; ++k) PP_CUDA(copy_async(b.z[k], a.z[k], G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(copy_async(b.off, a.off, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(copy_async(b.gmax, a.gmax, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(copy_async(b.gmin, a.gmin, G_ * 8ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(copy_async(b.cnt, a.cnt, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(copy_async(b.cap, a.cap, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(copy_async(b.flags, a.flags, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
+    PP_CUDA(copy_async(b.stamp, a.stamp, G_ * 4ull, cudaMemcpyDeviceToDevice, stream_));
     gcur_ = o;
   }
 
@@ -1476,7 +1501,7 @@ class EngineImpl final : public EngineBase {
   }
   void fetch_stats() {
     auto t0 = Clock::now();
-    PP_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, sizeof(DevStats), cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(copy_async(h_stats_, d_stats_, sizeof(DevStats), cudaMemcpyDeviceToHost, stream_));
     if (spin_sync_) wait_stream();
     else PP_CUDA(cudaStreamSynchronize(stream_));
     tr_sync_ns_ += ns_since(t0);
@@ -1579,8 +1604,8 @@ class EngineImpl final : public EngineBase {
     // diagonal strings are few (at most one per group): fetch a short prefix
     // with the readout's round trip, the rest only if there are more
     diag_copied_ = std::min<uint64_t>(G_, kDiagSpec);
-    PP_CUDA(cudaMemcpyAsync(h_diag_->z, diag_z_.p, diag_copied_ * W * 8, cudaMemcpyDeviceToHost, stream_));
-    PP_CUDA(cudaMemcpyAsync(h_diag_->c, diag_c_.p, diag_copied_ * 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(copy_async(h_diag_->z, diag_z_.p, diag_copied_ * W * 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(copy_async(h_diag_->c, diag_c_.p, diag_copied_ * 8, cudaMemcpyDeviceToHost, stream_));
   }
 
   void sync_state(bool diag = false) {
@@ -1913,9 +1938,9 @@ class EngineImpl final : public EngineBase {
       uint64_t* dgx = cliff_.as<uint64_t>();
       uint64_t* dgz = dgx + count * W;
       double* dgs = reinterpret_cast<double*>(dgz + count * W);
-      PP_CUDA(cudaMemcpyAsync(dgx, gx.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
-      PP_CUDA(cudaMemcpyAsync(dgz, gz.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
-      PP_CUDA(cudaMemcpyAsync(dgs, gs.data(), count * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(dgx, gx.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(dgz, gz.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
+      PP_CUDA(copy_async(dgs, gs.data(), count * 8, cudaMemcpyHostToDevice, stream_));
       CliffordProducer<W> p{dgx, dgz, dgs, (int)count};
       regroup(p, sort);
     }
@@ -1942,6 +1967,7 @@ class EngineImpl final : public EngineBase {
   template <class P>
   void regroup(const P& prod, bool sort = true) {
     const int maxrec = P::kMaxRec;
+    count_param_h2d(sizeof(P));  // the producer's gate descriptors
     sync_state();
     const uint64_t live = live_;
     if (G_ == 0 || live == 0) return;
@@ -2039,7 +2065,7 @@ class EngineImpl final : public EngineBase {
       } else {
         device_scan(t.count, tc, 1, scan_gid_.as<unsigned long long>(), ntiles);
         device_scan(t.count, tc, 0, scan_off_.as<unsigned long long>(), ntiles);
-        PP_CUDA(cudaMemcpyAsync(&d_stats_->scan_total, scan_tmp_.as<unsigned long long>() + ntiles, 8,
+        PP_CUDA(copy_async(&d_stats_->scan_total, scan_tmp_.as<unsigned long long>() + ntiles, 8,
                                 cudaMemcpyDeviceToDevice, stream_));
       }
       uint64_t total_bound = records_upper;
@@ -2462,6 +2488,11 @@ int pp_take_kernel_stats(pp_engine* e, double* branch_ms, double* branch_bytes, 
 }
 
 void* pp_stream(const pp_engine* e) { return e ? e->impl->stream() : nullptr; }
+
+void pp_transfer_totals(uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
+  if (h2d_bytes) *h2d_bytes = ppgpu::g_h2d_bytes.load();
+  if (d2h_bytes) *d2h_bytes = ppgpu::g_d2h_bytes.load();
+}
 
 int pp_local_stats(pp_engine* e, double* gmax, uint32_t* nonfinite, uint64_t* count) {
   if (!e || !gmax || !nonfinite || !count) return PP_ERR_INVALID;
