@@ -219,9 +219,10 @@ class OracleEngine:
         return self.L.ppo_coefficient(self.h, w.ctypes.data)
 
     def take_counters(self):
-        out = np.zeros(3, np.uint64)
+        out = np.zeros(4, np.uint64)
         self.L.ppo_take_counters(self.h, out.ctypes.data)
-        return {"removed": int(out[0]), "records_sent": int(out[1]), "gates": int(out[2])}
+        return {"removed": int(out[0]), "records_sent": int(out[1]), "gates": int(out[2]),
+                "batches_sent": int(out[3])}
 
     def export(self):
         n = self.term_count()
@@ -254,6 +255,7 @@ class OracleEngine:
                          "term_count": self.term_count(),
                          "global_max": self.global_max(),
                          "removed": cnt["removed"],
+                         "batches_sent": cnt["batches_sent"],
                          "records_sent": cnt["records_sent"]})
         return rows
 

@@ -168,7 +168,7 @@ typedef struct {
   ppo_store store;
   double last_global_max;
   /* counters drained per layer (engine.hpp:171-178) */
-  uint64_t removed, records, gates, gates_total;
+  uint64_t removed, records, gates, gates_total, batches;
   /* scratch for the records of one gate */
   ppo_key* rec_keys;
   double* rec_vals;
@@ -223,7 +223,7 @@ int ppo_set_initial(ppo_engine* e, const uint64_t* words, const double* c,
   }
   int nf;
   e->last_global_max = store_max_abs(&e->store, &nf);
-  e->removed = e->records = e->gates = e->gates_total = 0;
+  e->removed = e->records = e->gates = e->gates_total = e->batches = 0;
   return PPO_OK;
 }
 
@@ -296,6 +296,9 @@ int ppo_apply_gate(ppo_engine* e, const uint64_t* gen, double cos_t,
     if (rc) return rc;
   }
   e->records += nrec;
+  /* one worker: the (0, 0) outbox is one non-empty batch iff the gate sent a
+     record (engine.cpp:286-301) */
+  e->batches += nrec > 0;
   e->gates++;
   e->gates_total++;
   if (e->max_terms && s->size > e->max_terms) return PPO_RESOURCE;
@@ -365,12 +368,13 @@ int ppo_density_histogram(const ppo_engine* e, int bins, double gmax,
   return PPO_OK;
 }
 
-/* Counters since the last call: removed, records, gates. */
-void ppo_take_counters(ppo_engine* e, uint64_t* out3) {
-  out3[0] = e->removed;
-  out3[1] = e->records;
-  out3[2] = e->gates;
-  e->removed = e->records = e->gates = 0;
+/* Counters since the last call: removed, records, gates, batches. */
+void ppo_take_counters(ppo_engine* e, uint64_t* out4) {
+  out4[0] = e->removed;
+  out4[1] = e->records;
+  out4[2] = e->gates;
+  out4[3] = e->batches;
+  e->removed = e->records = e->gates = e->batches = 0;
 }
 
 /* cos_pi / sin_pi and Angle::cosine/sine, circuit.cpp:28-63. */

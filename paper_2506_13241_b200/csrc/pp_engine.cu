@@ -164,7 +164,9 @@ static inline bool is_clifford(const pp_gate& g) {
 // ---------------------------------------------------------------------------
 // Called before the pool gives up on an allocation: releases engines parked
 // in the engine pool (their buffers come back here), set below.
-static void (*g_release_parked_engines)() = nullptr;
+static void (*g_release_parked_engines)(int device) = nullptr;
+// device bytes held by engines parked in the engine pool on `device`
+static size_t (*g_parked_engine_bytes)(int device) = nullptr;
 
 class DevicePool {
  public:
@@ -191,7 +193,7 @@ class DevicePool {
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
-      if (g_release_parked_engines) g_release_parked_engines();
+      if (g_release_parked_engines) g_release_parked_engines(dev);
       trim(dev);
       e = cudaMalloc(&p, bytes);
     }
@@ -345,7 +347,15 @@ static std::mutex g_setup_mu;
 static std::map<std::pair<int, int>, LaunchSetup> g_setup;
 
 static std::mutex g_graph_mu;
-static std::map<std::string, cudaGraphExec_t> g_graphs;
+// Executable graphs of X-type runs, shared by engines with identical buffers
+// (pooled engines).  Entries are reference counted: an engine holds the ones
+// it launched until its stream has synchronised, so evicting the cache never
+// destroys an exec another thread is about to launch or has in flight.
+struct GraphExecDeleter {
+  void operator()(CUgraphExec_st* e) const { cudaGraphExecDestroy(e); }
+};
+using GraphExecPtr = std::shared_ptr<CUgraphExec_st>;
+static std::map<std::string, GraphExecPtr> g_graphs;
 
 class EngineBase {
  public:
@@ -374,6 +384,8 @@ class EngineBase {
   virtual void histogram(int bins, double gmax, double epsilon0, uint64_t* pos, uint64_t* neg) = 0;
   // engine reuse across pp_create/pp_destroy (simulate() makes one per call)
   virtual bool reusable() const = 0;
+  virtual size_t device_bytes() const = 0;
+  virtual int device() const = 0;
   virtual void on_reuse() = 0;
   virtual void poison() = 0;
 };
@@ -437,6 +449,11 @@ class EngineImpl final : public EngineBase {
     update_arena_max();
   }
   ~EngineImpl() override {
+    // buffers return to the pool of the device they came from: run the
+    // teardown on this engine's device whatever the caller's current one is
+    int prev_dev = -1;
+    cudaGetDevice(&prev_dev);
+    cudaSetDevice(cfg_.device);
     cudaStreamSynchronize(stream_);
     if (std::getenv("PP_TRACE"))
       std::fprintf(stderr,
@@ -452,11 +469,31 @@ class EngineImpl final : public EngineBase {
     }
     release_pinned_stats(h_stats_);
     release_pinned_diag(h_diag_);
+    release_all_buffers();  // while cfg_.device is current
+    if (prev_dev >= 0) cudaSetDevice(prev_dev);
+  }
+  // every device buffer the engine holds (the memory plan and the engine
+  // pool's size cap count them all)
+  template <class F>
+  void for_each_buf(F&& f) {
+    for (auto& a : arena_) f(a.buf);
+    for (auto& g : groups_) f(g.buf);
+    for (DevBuf* b : {&evict_cnt_, &evict_buf_, &spec_buf_, &backup_, &stats_buf_, &list_, &items_, &rec_slot_,
+                      &table_, &scan_tmp_, &scan_gid_, &scan_off_, &diag_z_, &diag_c_, &cliff_, &thr_, &ztab_})
+      f(*b);
+  }
+  size_t device_bytes() const override {
+    size_t b = 0;
+    const_cast<EngineImpl*>(this)->for_each_buf([&](DevBuf& d) { b += d.bytes; });
+    return b;
+  }
+  int device() const override { return cfg_.device; }
+  void release_all_buffers() {
+    for_each_buf([](DevBuf& d) { d.release(); });
   }
 
   bool reusable() const override {
-    return !poisoned_ && !sub_pending_ && !g_pending_ && !lazy_open_ &&
-           arena_[0].buf.bytes + arena_[1].buf.bytes <= (size_t(4) << 30);
+    return !poisoned_ && !sub_pending_ && !g_pending_ && !lazy_open_ && device_bytes() <= (size_t(4) << 30);
   }
   void on_reuse() override {  // set_initial resets the operator; this resets the statistics
     PP_CUDA(cudaSetDevice(cfg_.device));  // as a fresh engine's constructor does
@@ -596,6 +633,10 @@ class EngineImpl final : public EngineBase {
     }
     bump_ = bump_bound_ = n;
     live_ = live_bound_ = n;
+    // group statistics a fresh engine would start from (pooled engines and a
+    // second set_initial must not keep the previous operator's)
+    maxcnt_ = G ? *std::max_element(gcnt.begin(), gcnt.end()) : 0u;
+    zfactor_ = 4.0;
     dirty_ = false;
     truncated_since_sync_ = false;
     gmax_stale_ = false;
@@ -814,11 +855,12 @@ class EngineImpl final : public EngineBase {
         lazy_len_ = (uint32_t)(count - pos);
       }
       if (use_graph) {
-        cudaGraphExec_t exec = rx_graph(prm, epi, do_trunc, budget, lazy);
+        GraphExecPtr exec = rx_graph(prm, epi, do_trunc, budget, lazy);
+        held_graphs_.push_back(exec);  // alive until this stream has synchronised
         std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
         PP_CUDA(cudaEventRecord(ev.first, stream_));
         count_param_h2d(count * sizeof(RxParam));  // the gate parameters baked into the graph
-        PP_CUDA(cudaGraphLaunch(exec, stream_));
+        PP_CUDA(cudaGraphLaunch(exec.get(), stream_));
         PP_CUDA(cudaEventRecord(ev.second, stream_));
         pending_events_.push_back(ev);
         launches_ += count * (epi ? 3 : 1);
@@ -880,7 +922,10 @@ class EngineImpl final : public EngineBase {
       if (bump_ + want > arena_[cur_].cap) {
         size_t free_b = 0, total_b = 0;
         PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const uint64_t afford = (uint64_t)((free_b + arena_[1 - cur_].buf.bytes) * 0.8) / R;
+        const size_t parked = g_parked_engine_bytes ? g_parked_engine_bytes(cfg_.device) : 0;
+        const uint64_t afford =
+            (uint64_t)((free_b + DevicePool::get().cached_bytes(cfg_.device) + parked + arena_[1 - cur_].buf.bytes) *
+                       0.8) / R;
         if (live_ + want > afford && faults > 0) return false;
         gc_into_other(std::max<uint64_t>(std::min<uint64_t>(live_ + want, afford), next_arena_target()));
       }
@@ -1019,7 +1064,7 @@ class EngineImpl final : public EngineBase {
     ++launches_;
   }
 
-  cudaGraphExec_t rx_graph(const std::vector<RxParam>& prm, bool epi, bool do_trunc, bool budget, bool lazy) {
+  GraphExecPtr rx_graph(const std::vector<RxParam>& prm, bool epi, bool do_trunc, bool budget, bool lazy) {
     std::string key;
     auto put = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
     GroupView<W> gv = gview(gcur_);
@@ -1043,10 +1088,7 @@ class EngineImpl final : public EngineBase {
     std::lock_guard<std::mutex> lk(g_graph_mu);
     auto it = g_graphs.find(key);
     if (it != g_graphs.end()) return it->second;
-    if (g_graphs.size() > 64) {
-      for (auto& kv : g_graphs) cudaGraphExecDestroy(kv.second);
-      g_graphs.clear();
-    }
+    if (g_graphs.size() > 64) g_graphs.clear();  // holders keep their execs alive
     cudaGraph_t graph;
     PP_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     const uint64_t saved = launches_;
@@ -1056,9 +1098,10 @@ class EngineImpl final : public EngineBase {
     }
     launches_ = saved;
     PP_CUDA(cudaStreamEndCapture(stream_, &graph));
-    cudaGraphExec_t exec;
-    PP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphExec_t raw;
+    PP_CUDA(cudaGraphInstantiate(&raw, graph, 0));
     cudaGraphDestroy(graph);
+    GraphExecPtr exec(raw, GraphExecDeleter{});
     g_graphs.emplace(key, exec);
     return exec;
   }
@@ -1071,11 +1114,22 @@ class EngineImpl final : public EngineBase {
   void update_arena_max() {
     size_t free_b = 0, total_b = 0;
     PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const size_t avail = free_b + DevicePool::get().cached_bytes(cfg_.device) + arena_[0].buf.bytes +
+    // parked engines' buffers are released on demand (DevicePool::acquire),
+    // so they count as available
+    const size_t parked = g_parked_engine_bytes ? g_parked_engine_bytes(cfg_.device) : 0;
+    const size_t avail = free_b + DevicePool::get().cached_bytes(cfg_.device) + parked + arena_[0].buf.bytes +
                          arena_[1].buf.bytes;
     const double frac = cfg_.mem_fraction > 0 && cfg_.mem_fraction <= 1 ? cfg_.mem_fraction : 0.92;
     const double budget = (double)avail * frac - (double)(3ull << 30);
     arena_max_ = budget > 0 ? (uint64_t)(budget / (double)(2 * R + 16)) : (1ull << 20);
+  }
+
+  // memory is short: free this device's parked engines and the pool's cache,
+  // then plan again
+  void reclaim_parked() {
+    if (g_release_parked_engines) g_release_parked_engines(cfg_.device);
+    DevicePool::get().trim(cfg_.device);
+    update_arena_max();
   }
 
   // arena capacity for the next compaction: room to grow ~2x without
@@ -1089,6 +1143,7 @@ class EngineImpl final : public EngineBase {
     const uint64_t want = std::max<uint64_t>(3 * live_ + 1024, std::min<uint64_t>(8 * live_, arena_max_));
     uint64_t t = std::min<uint64_t>(std::max<uint64_t>(want, arena_[cur_].cap), arena_max_);
     if (t < lo) {
+      if (lo > arena_max_) reclaim_parked();
       if (lo > arena_max_)
         throw EngineError(PP_ERR_RESOURCE, "device memory exhausted: " + std::to_string(live_) +
                                                " live strings exceed the arena plan of " +
@@ -1101,6 +1156,7 @@ class EngineImpl final : public EngineBase {
   // regroup target arena: the exact output plus slack, within the plan
   uint64_t regroup_arena(uint64_t total) {
     if (2 * total + (1u << 16) > arena_max_) update_arena_max();
+    if (total + 1 > arena_max_) reclaim_parked();
     if (total + 1 > arena_max_)
       throw EngineError(PP_ERR_RESOURCE, "device memory exhausted: " + std::to_string(total) +
                                              " strings after regroup exceed the arena plan of " +
@@ -1504,6 +1560,7 @@ class EngineImpl final : public EngineBase {
     PP_CUDA(copy_async(h_stats_, d_stats_, sizeof(DevStats), cudaMemcpyDeviceToHost, stream_));
     if (spin_sync_) wait_stream();
     else PP_CUDA(cudaStreamSynchronize(stream_));
+    held_graphs_.clear();  // every launch so far has completed
     tr_sync_ns_ += ns_since(t0);
     ++tr_syncs_;
   }
@@ -2209,6 +2266,7 @@ class EngineImpl final : public EngineBase {
   bool tight_arena_ = false;  // PP_TIGHT_ARENA: minimal arenas (tests of the resume paths)
   static constexpr size_t kLazyWindow = 4096;  // gates per deferred-truncation window
   DevBuf thr_;                // thr[j] = max(T_j .. T_now) over the open window
+  std::vector<GraphExecPtr> held_graphs_;  // graphs launched since the last stream sync
   bool lazy_open_ = false;
   uint64_t lazy_base_ = 0;
   uint32_t lazy_len_ = 0;
@@ -2289,17 +2347,34 @@ constexpr size_t kEnginePoolMax = 4;
 
 // device memory is short: parked engines go (their buffers return to the
 // device pool, which then frees its cache)
-void release_parked_engines() {
+void release_parked_engines(int device) {
   std::vector<ppgpu::EngineBase*> victims;
   {
     std::lock_guard<std::mutex> lk(g_engine_pool_mu);
-    for (auto& kv : *g_engine_pool) victims.push_back(kv.second);
-    g_engine_pool->clear();
+    auto& pool = *g_engine_pool;
+    for (size_t i = 0; i < pool.size();) {
+      if (device < 0 || pool[i].second->device() == device) {
+        victims.push_back(pool[i].second);
+        pool.erase(pool.begin() + i);
+      } else {
+        ++i;
+      }
+    }
   }
-  for (auto* v : victims) delete v;
+  for (auto* v : victims) delete v;  // each destructor runs on its own device
+}
+size_t parked_engine_bytes(int device) {
+  std::lock_guard<std::mutex> lk(g_engine_pool_mu);
+  size_t b = 0;
+  for (auto& kv : *g_engine_pool)
+    if (kv.second->device() == device) b += kv.second->device_bytes();
+  return b;
 }
 struct ParkedEnginesHook {
-  ParkedEnginesHook() { ppgpu::g_release_parked_engines = &release_parked_engines; }
+  ParkedEnginesHook() {
+    ppgpu::g_release_parked_engines = &release_parked_engines;
+    ppgpu::g_parked_engine_bytes = &parked_engine_bytes;
+  }
 } g_parked_engines_hook;
 
 std::string engine_key(const pp_config& c) {

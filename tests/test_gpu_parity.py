@@ -365,3 +365,41 @@ def test_dense_big_and_multiclass_blocks(pp, O, n):
         init.append((word(zs(sites, ys=ys)), float(rng.uniform(-1, 1))))
     layer = [pp.Gate(pp.PauliString(f"X{q}", n), float(rng.uniform(-3, 3))) for q in range(n)]
     run_both(pp, O, n, [layer], init, 0.0, "gate", check_each=True)
+
+
+def test_reinitialised_engine_big_group_then_zz(pp, O):
+    """A pooled engine (and a second set_initial on one engine) starts from
+    the new operator's group statistics: a z-group of 1024 strings followed by
+    a non-Clifford ZZ as the first gate is exact (maxcnt_ was kept
+    from the previous operator)."""
+    n = 24
+    # z = Z on sites 0..9 plus 12, x free on 0..9: 1024 strings in one z-group
+    words, coeffs = [], []
+    rng = np.random.default_rng(3)
+    for xbits in range(1024):
+        w = np.zeros(4, np.uint64)
+        for q in range(10):
+            code = 2 if (xbits >> q) & 1 else 3  # Y (x=1, z=1) or Z (x=0, z=1)
+            w[0] |= np.uint64(code) << np.uint64(2 * q)
+        w[0] |= np.uint64(3) << np.uint64(24)
+        words.append(w)
+        coeffs.append(float(rng.uniform(-1, 1)))
+    words = np.stack(words)
+    coeffs = np.array(coeffs)
+    zz = pp.Gate(pp.PauliString("Z0 Z20", n), 0.37)
+    rx = pp.Gate(pp.PauliString("X3", n), 0.21)
+    for trial in range(3):
+        eng = pp.Engine(n, 0.0)
+        if trial == 0:  # a used engine re-initialised in place
+            eng.set_initial(O.site_word(5, 3)[None], np.array([1.0]))
+            eng.apply_gates([rx, zz])
+        eng.set_initial(words, coeffs)
+        eng.apply_gates([zz, rx, zz])
+        ora = O.OracleEngine(n, 0.0)
+        ora.set_initial(words, coeffs)
+        for g in (zz, rx, zz):
+            ora.apply_gate(np.asarray(g.generator.words, np.uint64), g.cos_theta, g.sin_theta)
+        w, c = eng.export()
+        ow, oc = ora.export()
+        assert_same_terms(w, c, ow, oc, f"trial {trial}")
+        del eng  # trial 1, 2: the next Engine is the pooled one

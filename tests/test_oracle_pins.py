@@ -70,6 +70,7 @@ def test_oracle_ledgers_match_reference(O, ledgers, name):
         assert np.float64(got["global_max"]).view(np.uint64) == want["global_max_bits"]
         assert got["removed"] == want["removed"]
         assert got["records_sent"] == want["records_sent"]
+        assert got["batches_sent"] == want["batches_sent"]
         assert abs(got["observable"] - want["observable"]) <= 1e-12 * max(1, abs(want["observable"]))
 
 

@@ -1,16 +1,11 @@
-set -x
+# One GPU pass (gpurun): the -m gpu suite, the default bench line, the
+# reference arm.  Outputs land in gpurun_out/.
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -4 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_config1.json 2> gpurun_out/bench_config1.err; echo "bench rc=$?"
-cat gpurun_out/bench_config1.json; tail -3 gpurun_out/bench_config1.err
-PP_TRACE=1 timeout 600 python tools/profile_run.py config1 --warm
-timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_config1_warm.csv python tools/profile_run.py config1 --warm > gpurun_out/ncu1.log 2>&1; echo "ncu rc=$?"
-python tools/launch_summary.py gpurun_out/launches_config1_warm.csv
-mkdir -p gpurun_out
-timeout 900 python bench.py --workload config0_t10 --no-cpu-baseline --steps 5 > gpurun_out/bench_c0t10.json 2> gpurun_out/bench_c0t10.err; echo "bench0 rc=$?"
-cat gpurun_out/bench_c0t10.json; tail -3 gpurun_out/bench_c0t10.err
-timeout 900 python bench.py --workload config2_pi4_eps1e-4_t8 --no-cpu-baseline --steps 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo "bench2 rc=$?"
-cat gpurun_out/bench_c2.json; tail -3 gpurun_out/bench_c2.err
-timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c0t10_warm.csv python tools/profile_run.py config0_t10 --warm > gpurun_out/ncu0.log 2>&1; echo "ncu rc=$?"
-python tools/launch_summary.py gpurun_out/launches_c0t10_warm.csv
+timeout 1800 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS:-} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -5 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+if [ -n "${REF_ARM:-}" ]; then
+  timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+  cat gpurun_out/bench_ref.json
+fi
