@@ -173,6 +173,11 @@ int pp_shard_ingest_device(pp_engine* engine, const uint64_t* records, uint64_t 
  * sizes the oracle cannot reach). */
 int pp_norm2(pp_engine* engine, double* out);
 
+/* Diagnostics: the operator's z-groups (strings sharing a z-plane) by size,
+ * log2 bins: groups[b] and strings[b] count groups of [2^b, 2^(b+1))
+ * strings (64 entries each). */
+int pp_group_sizes(pp_engine* engine, uint64_t* groups, uint64_t* strings);
+
 /* Log-binned coefficient density with a sign split, the reference's
  * density_histogram (sparse_operator.cpp:150-197, written per layer by
  * runner.cpp:173-179): edges exp(log(lower) * (1 - b/bins)), lower =

@@ -64,6 +64,8 @@ __global__ void k_clear_cumulative(DevStats* st) {
   st->cliff_records = 0;
   st->dense_groups = 0;
   st->dense_out = 0;
+  for (int w = 0; w < kSeenWords; ++w) st->seen[w] = 0;
+  for (int k = 0; k < kZZSeenGroups; ++k) st->zz_seen[k][0] = st->zz_seen[k][1] = 0;
 }
 
 __global__ void k_reset_stats(DevStats* st, unsigned long long bump) { k_reset_stats_body(st, bump); }
@@ -381,6 +383,7 @@ class EngineBase {
   virtual void shard_ingest(const uint64_t* rec, uint64_t count, bool device) = 0;
   virtual const uint64_t* device_records() const = 0;
   virtual double norm2() = 0;
+  virtual void group_sizes(uint64_t* groups, uint64_t* strings) = 0;
   virtual void histogram(int bins, double gmax, double epsilon0, uint64_t* pos, uint64_t* neg) = 0;
   // engine reuse across pp_create/pp_destroy (simulate() makes one per call)
   virtual bool reusable() const = 0;
@@ -581,7 +584,8 @@ class EngineImpl final : public EngineBase {
     sub_pending_ = false;
     g_pending_ = false;
     unsorted_ = false;
-    pending_cliff_count_ = 0;
+    seen_host_ = {};
+    zz_seen_pending_ = false;
     if (n <= kInitSmall && G <= kInitSmall) {
       InitSmall<W> in{};
       in.n = (uint32_t)n;
@@ -645,6 +649,7 @@ class EngineImpl final : public EngineBase {
     gmax_ = gmax;
     counters_ = pp_counters{};
     gates_applied_ = 0;
+    seen_w0_ = 0;
   }
 
   // ---------------------------------------------------------------- gates
@@ -671,15 +676,17 @@ class EngineImpl final : public EngineBase {
       plan_key_.clear();
       plan_.clear();
       size_t i = 0;
+      // runs are capped so one run always fits a batch window (reserve_window)
+      constexpr size_t kRunCap = kSeenGates / 2;
       while (i < count) {
         if (fusion_allowed() && is_clifford(gates[i])) {
           size_t j = i;
-          while (j < count && is_clifford(gates[j])) ++j;
+          while (j < count && j - i < kRunCap && is_clifford(gates[j])) ++j;
           plan_.push_back({0, i, j});
           i = j;
         } else if (is_x_type(gates[i])) {
           size_t j = i;
-          while (j < count && is_x_type(gates[j]) && !(fusion_allowed() && is_clifford(gates[j]))) ++j;
+          while (j < count && j - i < kRunCap && is_x_type(gates[j]) && !(fusion_allowed() && is_clifford(gates[j]))) ++j;
           plan_.push_back({1, i, j});
           i = j;
         } else {
@@ -692,6 +699,7 @@ class EngineImpl final : public EngineBase {
     const std::vector<PlanRun> plan = plan_;  // a nested call may replace plan_
     for (size_t pi = 0; pi < plan.size(); ++pi) {
       const PlanRun& r = plan[pi];
+      reserve_window(r.j - r.i);
       auto t0 = Clock::now();
       if (r.kind == 0) {
         // a Clifford run feeding a dense Rx run leaves its groups unsorted
@@ -823,7 +831,6 @@ class EngineImpl final : public EngineBase {
       bseq_ = seq0 + count;
       gates_applied_ += count;
       counters_.gates += count;
-      counters_.batches_sent += count;
       counters_.branch_ns += ns_since(t0);
       return;
     }
@@ -896,7 +903,6 @@ class EngineImpl final : public EngineBase {
     bseq_ = seq0 + count;
     gates_applied_ += count;
     counters_.gates += count;
-    counters_.batches_sent += count;
     counters_.branch_ns += ns_since(t0);
   }
 
@@ -905,7 +911,9 @@ class EngineImpl final : public EngineBase {
   bool run_rx_speculative(const std::vector<RxParam>& prm, uint64_t seq0, Clock::time_point t0) {
     const size_t count = prm.size();
     SubGates sgates = rx_sg_;  // the cached descriptor of this run (run_rx)
-    sgates.dense = rx_distinct_ && !keep_zeros_ && !may_hold_zeros_ && !no_dense_;
+    // per-gate path only: it marks every gate's records exactly (a truncation
+    // can empty a group in the middle of a dense run)
+    sgates.dense = false;
     sgates.maxk = dense_maxk_;
     sgates.sorted = unsorted_ ? 0 : 1;
     sync_state();
@@ -935,6 +943,7 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(copy_async(backup_.p, groups_[gcur_].buf.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
       const uint32_t G_saved = G_;
       const pp_counters saved = counters_;
+      const auto saved_seen = seen_host_;
       PP_CUDA(copy_async(d_tpred, tpred.data(), count * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemsetAsync(d_gmax, 0, count * 8, stream_));
       push_scalars(seq0);
@@ -966,7 +975,6 @@ class EngineImpl final : public EngineBase {
         bseq_ = seq0 + count;
         gates_applied_ += count;
         counters_.gates += count;
-        counters_.batches_sent += count;
         counters_.branch_ns += ns_since(t0);
         spec_attempts_ += attempt + 1;
         if (std::getenv("PP_DEBUG"))
@@ -977,6 +985,7 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(copy_async(groups_[gcur_].buf.p, backup_.p, gbytes, cudaMemcpyDeviceToDevice, stream_));
       G_ = G_saved;
       counters_ = saved;
+      seen_host_ = saved_seen;  // the rejected attempt's batch marks
       if (std::getenv("PP_DEBUG")) {
         size_t first = 0;
         while (first < count && __builtin_bit_cast(uint64_t, tobs[first]) == __builtin_bit_cast(uint64_t, tpred[first]))
@@ -1334,6 +1343,20 @@ class EngineImpl final : public EngineBase {
 
   int record_words() const override { return 2 * W + 1; }
 
+  // z-groups by size: groups[b] / strings[b] for sizes in [2^b, 2^(b+1))
+  void group_sizes(uint64_t* groups, uint64_t* strings) override {
+    sync_state();
+    for (int b = 0; b < 64; ++b) groups[b] = strings[b] = 0;
+    if (G_ == 0) return;
+    std::vector<uint32_t> cnt(G_);
+    PP_CUDA(copy_sync(cnt.data(), gview(gcur_).cnt, (size_t)G_ * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t c : cnt)
+      if (c) {
+        const int b = 31 - __builtin_clz(c);
+        ++groups[b];
+        strings[b] += c;
+      }
+  }
   double norm2() override {
     sync_state();
     if (G_ == 0) return 0.0;
@@ -1455,6 +1478,7 @@ class EngineImpl final : public EngineBase {
 
   pp_counters take_counters() override {
     sync_state();
+    close_window();
     pp_counters out = counters_;
     counters_ = pp_counters{};
     return out;
@@ -1706,9 +1730,8 @@ class EngineImpl final : public EngineBase {
     if (st.cliff_records) {  // Clifford records of a deferred regroup (apply_clifford_run's accounting)
       counters_.records_sent += st.cliff_records;
       counters_.removed += st.cliff_records;
-      counters_.batches_sent += pending_cliff_count_;
     }
-    pending_cliff_count_ = 0;
+    harvest_seen(st);
     diag_n_ = st.diag_count;
     counters_.records_sent += st.records;
     counters_.removed += st.removed;
@@ -1764,7 +1787,9 @@ class EngineImpl final : public EngineBase {
   uint32_t persistent_grid() const { return 148u * 8u; }
 
   void push_scalars(uint64_t seq_base) {
-    k_set_scalars<<<1, 1, 0, stream_>>>(d_stats_, g_pending_ ? kKeepG : G_, arena_[cur_].cap, seq_base);
+    // window index of gate seq_base: the current run starts at bseq_
+    const uint32_t seen_base = window_index() + (uint32_t)(seq_base - bseq_);
+    k_set_scalars<<<1, 1, 0, stream_>>>(d_stats_, g_pending_ ? kKeepG : G_, arena_[cur_].cap, seq_base, seen_base);
     ++launches_;
   }
   // per-gate epilogue kernels for gate `rel` of a launch run (red slots by parity)
@@ -1847,7 +1872,6 @@ class EngineImpl final : public EngineBase {
     bseq_ += 1;
     ++gates_applied_;
     ++counters_.gates;
-    ++counters_.batches_sent;
     counters_.branch_ns += ns_since(t0);
     return true;
   }
@@ -1875,11 +1899,11 @@ class EngineImpl final : public EngineBase {
       }
       p.cosv = gate.cos_theta;
       p.sinv = gate.sin_theta;
+      p.seen_base = window_index();
       regroup(p);
       counters_.records_sent += h_records_;
     }
     counters_.branch_ns += ns_since(t0);
-    counters_.batches_sent += 1;
     h_records_ = 0;
     post_gate();
   }
@@ -1911,6 +1935,7 @@ class EngineImpl final : public EngineBase {
   bool try_zz_run(const pp_gate* gates, size_t count, bool sort) {
     if (zz_key_.size() == count && std::memcmp(zz_key_.data(), gates, count * sizeof(pp_gate)) == 0) {
       if (!zz_ok_) return false;
+      note_zz_run();
       regroup(zz_prod_, sort);  // the same run as last time (run_circuit layers)
       return true;
     }
@@ -1945,14 +1970,17 @@ class EngineImpl final : public EngineBase {
     }
     ZZRunProducer<W> p;
     p.ng = 0;
+    std::vector<ZZEdge> zz_edges;
     using T = typename PlaneInt<W>::T;
     for (auto& mt : matchings) {
       std::map<int, std::pair<T, T>> by_d;
+      std::map<int, std::vector<std::pair<int, int>>> edge_gates;  // d -> (bit i, run gate)
       for (size_t g : mt) {
         int i = edges[g].first, d = edges[g].second - edges[g].first;  // first < second (ascending scan)
         auto& e = by_d[d];
         e.first |= (T)1 << i;
         if (neg[g]) e.second |= (T)1 << i;
+        edge_gates[d].push_back({i, (int)g});
       }
       for (auto& [d, mm] : by_d) {
         if (p.ng >= kMaxZZGroups) {
@@ -1963,12 +1991,15 @@ class EngineImpl final : public EngineBase {
         p.grp[p.ng].m = mm.first;
         p.grp[p.ng].neg = mm.second;
         p.grp[p.ng].d = d;
+        for (auto [i, g] : edge_gates[d]) zz_edges.push_back({p.ng, i, g});
         ++p.ng;
       }
     }
     zz_key_.assign(gates, gates + count);
     zz_prod_ = p;
+    zz_edges_ = zz_edges;
     zz_ok_ = true;
+    note_zz_run();
     regroup(p, sort);
     return true;
   }
@@ -1998,15 +2029,13 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(copy_async(dgx, gx.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(copy_async(dgz, gz.data(), count * W * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(copy_async(dgs, gs.data(), count * 8, cudaMemcpyHostToDevice, stream_));
-      CliffordProducer<W> p{dgx, dgz, dgs, (int)count};
+      CliffordProducer<W> p{dgx, dgz, dgs, (int)count, window_index()};
       regroup(p, sort);
     }
     // Clifford gates zero each moved parent and re-insert it at I xor J;
     // absent a partner pair the reference removes one zero per record.
-    if (g_pending_) pending_cliff_count_ = count;  // accounted at the next sync
     counters_.records_sent += h_records_;
     counters_.removed += h_records_;
-    counters_.batches_sent += h_records_ ? count : 0;
     h_records_ = 0;
     counters_.exchange_ns += ns_since(t0);
     gates_applied_ += count;
@@ -2203,6 +2232,7 @@ class EngineImpl final : public EngineBase {
       const uint64_t total = h_stats_->scan_total;
       counters_.removed += h_stats_->removed;
       h_records_ = h_stats_->records;
+      harvest_seen(*h_stats_);
       cur_ = o;
       gcur_ = 1 - gcur_;
       G_ = distinct;
@@ -2296,7 +2326,54 @@ class EngineImpl final : public EngineBase {
   bool poisoned_ = false;  // an operation failed: not reused
   bool g_pending_ = false;        // G_ is an upper bound; the exact count is st->G_dev
   bool defer_ok_ = true;          // PP_NO_DEFER turns the deferred regroup off (test hook)
-  size_t pending_cliff_count_ = 0;
+  // ---- batches_sent (engine.cpp:286-301 at one worker: gates that sent a
+  // record).  Gates are indexed from the start of the open window
+  // (seen_w0_ = gates_applied_ when it opened); kernels set device bits,
+  // every sync ORs them into seen_host_ (idempotent, so a relaunched run
+  // cannot count a gate twice), and take_counters closes the window.
+  struct ZZEdge {
+    int group, bit, gate;  // (group, bit) of the fused ZZ producer -> gate of the run
+  };
+  std::vector<ZZEdge> zz_edges_;
+  uint64_t seen_w0_ = 0;
+  std::array<unsigned long long, kSeenWords> seen_host_{};
+  bool zz_seen_pending_ = false;
+  uint32_t zz_seen_base_ = 0;
+  uint32_t window_index() const { return (uint32_t)(gates_applied_ - seen_w0_); }
+  void note_zz_run() {
+    if (zz_seen_pending_) sync_state();  // one fused ZZ run per harvest (its edge masks share one slot)
+    zz_seen_base_ = window_index();
+    zz_seen_pending_ = true;
+  }
+  void harvest_seen(const DevStats& st) {
+    for (int w = 0; w < kSeenWords; ++w) seen_host_[w] |= st.seen[w];
+    if (zz_seen_pending_) {
+      for (const ZZEdge& e : zz_edges_) {
+        if ((st.zz_seen[e.group][e.bit >> 6] >> (e.bit & 63)) & 1ull) {
+          const uint32_t b = zz_seen_base_ + (uint32_t)e.gate;
+          if (b < (uint32_t)kSeenGates) seen_host_[b >> 6] |= 1ull << (b & 63);
+        }
+      }
+      zz_seen_pending_ = false;
+    }
+  }
+  void close_window() {
+    uint64_t n = 0;
+    for (auto& w : seen_host_) {
+      n += (uint64_t)__builtin_popcountll(w);
+      w = 0;
+    }
+    counters_.batches_sent += n;
+    seen_w0_ = gates_applied_;
+  }
+  // before a run of `count` gates: the window must have room for all of them
+  void reserve_window(size_t count) {
+    if (window_index() + count <= (size_t)kSeenGates) return;
+    sync_state();
+    close_window();
+    if (count > (size_t)kSeenGates)
+      throw EngineError(PP_ERR_INTERNAL, "gate run longer than the batch window");
+  }
   bool spin_sync_ = true;
   bool arena_fault_ = false;
   bool unsorted_fault_ = false;  // a sublayer left unsorted groups for the per-gate path
@@ -2583,6 +2660,11 @@ int pp_truncate_threshold(pp_engine* e, double threshold, uint64_t* removed) {
 }
 
 int pp_record_words(const pp_engine* e) { return e ? e->impl->record_words() : 0; }
+
+int pp_group_sizes(pp_engine* e, uint64_t* groups, uint64_t* strings) {
+  if (!e || !groups || !strings) return PP_ERR_INVALID;
+  return guarded(e, [&] { e->impl->group_sizes(groups, strings); });
+}
 
 int pp_norm2(pp_engine* e, double* out) {
   if (!e || !out) return PP_ERR_INVALID;

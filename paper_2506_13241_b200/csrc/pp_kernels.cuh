@@ -79,6 +79,15 @@ __device__ __forceinline__ void clear_red(RedSlot* r) {
   r->maxcnt = 0;
 }
 
+// batches_sent (engine.cpp:286-301, one worker): a gate counts one batch iff
+// it sent at least one record.  Kernels set one bit per gate of the harvest
+// window (the gates applied since the host last read the statistics); fused
+// ZZ runs record their anticommuting-edge masks per edge group instead, which
+// the host maps back to gates.
+constexpr int kSeenWords = 16;          // gates per harvest window: 1024
+constexpr int kSeenGates = 64 * kSeenWords;
+constexpr int kZZSeenGroups = 64;       // = kMaxZZGroups (pp_regroup.cuh)
+
 struct DevStats {
   RedSlot red[3];                  // [0,1]: per-gate epilogues, [2]: host syncs
   SelSlot sel[2];
@@ -117,13 +126,26 @@ struct DevStats {
   unsigned long long cliff_records; // records of a regroup whose sizes the host reads later (deferred)
   unsigned long long dense_groups;  // groups applied by the dense sublayer path (cumulative)
   unsigned long long dense_out;     // strings those groups wrote
+  unsigned int seen_base;           // window index of gate 0 of the current launch run
+  unsigned int seen_pad;
+  unsigned long long seen[kSeenWords];            // bit g: window gate g sent a record
+  unsigned long long zz_seen[kZZSeenGroups][2];   // fused ZZ run: edges (bit i of group k) that sent one
 };
+
+__device__ __forceinline__ void mark_seen(DevStats* st, uint32_t bit) {
+  if (bit >= (uint32_t)kSeenGates) return;
+  const unsigned long long m = 1ull << (bit & 63);
+  unsigned long long* w = &st->seen[bit >> 6];
+  if (!(*(volatile unsigned long long*)w & m)) atomicOr(w, m);
+}
 
 // Scalars a launch run reads from device memory, so that a captured CUDA
 // graph can be replayed for every layer.
 constexpr unsigned int kKeepG = 0xffffffffu;  // k_set_scalars / k_diag: the group count is on the device
-__global__ void k_set_scalars(DevStats* st, unsigned int G, unsigned long long cap, unsigned long long seq_base) {
+__global__ void k_set_scalars(DevStats* st, unsigned int G, unsigned long long cap, unsigned long long seq_base,
+                              unsigned int seen_base) {
   if (G != kKeepG) st->G_dev = G;
+  st->seen_base = seen_base;
   st->arena_cap = cap;
   st->seq_base = seq_base;
   st->work[0] = st->work[1] = 0;
@@ -1100,6 +1122,7 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
       atomicAdd(&st->records, records);
       atomicAdd(&st->removed, removed);
       atomicAdd(&st->out_elems, (unsigned long long)out_n);
+      if (records) mark_seen(st, st->seen_base + seq_rel);
     }
   }  // groups of the chunk
   if (red_out) {
@@ -1144,7 +1167,10 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
   pk_records = warp_sum64(pk_records);
   pk_removed = warp_sum64(pk_removed);
   if ((tid & 31) == 0) {
-    if (pk_records) atomicAdd(&st->records, pk_records);
+    if (pk_records) {
+      atomicAdd(&st->records, pk_records);
+      mark_seen(st, st->seen_base + seq_rel);
+    }
     if (pk_removed) atomicAdd(&st->removed, pk_removed);
   }
   if (tid == 0 && pk_out) atomicAdd(&st->out_elems, pk_out);
@@ -1538,7 +1564,8 @@ __device__ void dense_passes(double* dbuf, double* blk, uint32_t S, DenseCtl<W>&
 template <int W>
 __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, uint32_t* scan, GroupView<W> g,
                            ArenaView<W> ar, uint32_t gid, uint32_t n, uint64_t src, uint32_t K, uint32_t seq0,
-                           unsigned long long cap, DevStats* st, unsigned long long& aff_elems) {
+                           unsigned long long cap, DevStats* st, unsigned long long& aff_elems,
+                           const uint32_t* s_touch, uint32_t* s_seen) {
   const uint32_t tid = threadIdx.x;
   const int m = dc.m;
   const Plane<W> T = dc.T;
@@ -1714,7 +1741,10 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     g.gmin[gid] = out ? vmin : __longlong_as_double(0x7ff0000000000000ll);
     g.flags[gid] = nonfinite;
     g.stamp[gid] = seq0 + (uint32_t)dc.klast;
-    if (records) atomicAdd(&st->records, records);
+    if (records) {
+      atomicAdd(&st->records, records);
+      for (int w = 0; w < kMaxSubGates / 32; ++w) atomicOr(&s_seen[w], s_touch[w]);
+    }
     if (removed) atomicAdd(&st->removed, removed);
     atomicAdd(&st->out_elems, (unsigned long long)out);
     atomicAdd(&st->dense_groups, 1ull);
@@ -1731,7 +1761,7 @@ template <int W>
 __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, uint32_t* scan, GroupView<W> g,
                            ArenaView<W> ar, const SubGates& gates, const SubGates& gp, uint32_t gid, uint32_t n, uint64_t src, int k0,
                            const uint32_t* s_touch, uint32_t seq0, unsigned long long cap, DevStats* st,
-                           unsigned long long& aff_elems) {
+                           unsigned long long& aff_elems, uint32_t* s_seen) {
   const uint32_t tid = threadIdx.x;
   // stage list, in parallel: thread k owns gate k (parameters read from the
   // kernel's parameter block once per gate, not serially per group)
@@ -1891,7 +1921,7 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     xt[256 * tid] = z0;
   }
   __syncthreads();
-  if (K > 1) return dense_multi<W>(dbuf, dc, gs, scan, g, ar, gid, n, src, K, seq0, cap, st, aff_elems);
+  if (K > 1) return dense_multi<W>(dbuf, dc, gs, scan, g, ar, gid, n, src, K, seq0, cap, st, aff_elems, s_touch, s_seen);
   const uint32_t S = 1u << m;
   if (tid == 0) {
     const unsigned long long d = atomicAdd(&st->bump, (unsigned long long)S);
@@ -2080,7 +2110,10 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     g.gmin[gid] = out ? vmin : __longlong_as_double(0x7ff0000000000000ll);
     g.flags[gid] = nonfinite;
     g.stamp[gid] = seq0 + (uint32_t)dc.klast;
-    if (records) atomicAdd(&st->records, records);
+    if (records) {
+      atomicAdd(&st->records, records);
+      for (int w = 0; w < kMaxSubGates / 32; ++w) atomicOr(&s_seen[w], s_touch[w]);
+    }
     if (removed) atomicAdd(&st->removed, removed);
     atomicAdd(&st->out_elems, (unsigned long long)out);
     atomicAdd(&st->dense_groups, 1ull);
@@ -2105,11 +2138,13 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
                                                            int keep_zeros, unsigned int* work, const double* tpred,
                                                            unsigned long long* gmax_out, DevStats* st) {
   __shared__ uint32_t s_touch[kMaxSubGates / 32];
+  __shared__ uint32_t s_seen[kMaxSubGates / 32];  // gates of the run that sent a record (batches_sent)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BranchSmem<W>& sm = *reinterpret_cast<BranchSmem<W>*>(smem_raw);
   SegSmem<W>& sg = *reinterpret_cast<SegSmem<W>*>(smem_raw);
   const uint32_t tid = threadIdx.x;
   if (engine_failed(st)) return;
+  if (tid < kMaxSubGates / 32) s_seen[tid] = 0;
   const bool spec = tpred != nullptr;
   const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
   const unsigned long long cap = *(volatile const unsigned long long*)&st->arena_cap;
@@ -2212,7 +2247,7 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
     }
     if (gates.dense) {
       const int r = dense_group<W>(reinterpret_cast<double*>(smem_raw), dc, gs, tscan, g, ar, gates, s_gp, gid, n, src, k0,
-                                   s_touch, seq0, cap, st, aff_elems);
+                                   s_touch, seq0, cap, st, aff_elems, s_seen);
       if (r < 0) {
         failed = true;
         break;
@@ -2310,6 +2345,7 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
         atomicAdd(&st->records, records);
         atomicAdd(&st->removed, removed);
         atomicAdd(&st->out_elems, (unsigned long long)out_n);
+        if (records) atomicOr(&s_seen[k >> 5], 1u << (k & 31));
       }
       if (spec) {
         if (tid == 0 && vall > 0.0) atomicMax(&smax[k], (unsigned long long)__double_as_longlong(vall));
@@ -2350,6 +2386,11 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
   if (spec)
     for (int k = tid; k < gates.ng; k += kCta)
       if (smax[k]) atomicMax(&gmax_out[k], smax[k]);
+  // a touched group with a nonzero string sends a record through every gate
+  // with sin != 0 that touches it (dense path: the group's vector stays
+  // nonzero through the run's rotations); the per-gate path marks exactly
+  for (int k = tid; k < gates.ng; k += kCta)
+    if (((s_seen[k >> 5] >> (k & 31)) & 1u) && s_gp.sinv[k] != 0.0) mark_seen(st, st->seen_base + k);
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
 }
 

@@ -48,6 +48,31 @@ struct CliffordProducer {
   const uint64_t* gz;  // [ng][W]
   const double* gsin;  // [ng], +-1
   int ng;
+  uint32_t seen_base;  // window index of gate 0 (batches_sent)
+  // batches_sent: bit i of acc = gate i moved a nonzero string (|c| never
+  // changes along the run, so a nonzero string stays nonzero)
+  static constexpr int kMarkWords = kSeenWords;
+  __device__ __forceinline__ void mark(Plane<W> x, Plane<W> z, double c, unsigned long long* acc) const {
+    if (c == 0.0) return;
+    for (int i = 0; i < ng && i < kSeenGates; ++i) {
+      Plane<W> jx, jz;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        jx.w[k] = gx[i * W + k];
+        jz.w[k] = gz[i * W + k];
+      }
+      if (plane_parity_and<W>(x, jz) ^ plane_parity_and<W>(z, jx)) {
+        const unsigned long long m = 1ull << (i & 63);
+        if (!(acc[i >> 6] & m)) atomicOr(&acc[i >> 6], m);
+        x = plane_xor<W>(x, jx);
+        z = plane_xor<W>(z, jz);
+      }
+    }
+  }
+  __device__ void flush(const unsigned long long* acc, DevStats* st) const {
+    for (int i = threadIdx.x; i < ng && i < kSeenGates; i += blockDim.x)
+      if ((acc[i >> 6] >> (i & 63)) & 1ull) mark_seen(st, seen_base + i);
+  }
   __device__ __forceinline__ int emit(Plane<W> x, Plane<W> z, double c, Record<W>* out, uint32_t* nrec) const {
     uint32_t moved = 0;
     for (int i = 0; i < ng; ++i) {
@@ -86,6 +111,7 @@ struct CliffordProducer {
 // Commuting Clifford rotations compose to the same signed permutation in any
 // order, so regrouping the run is exact.
 constexpr int kMaxZZGroups = 64;  // keeps the kernel parameter block under 4 KB
+static_assert(kMaxZZGroups == kZZSeenGroups, "DevStats::zz_seen holds one entry per ZZ group");
 
 template <int W>
 struct PlaneInt;
@@ -111,6 +137,27 @@ struct ZZRunProducer {
   using T = typename PlaneInt<W>::T;
   int ng;
   ZZGroup<W> grp[kMaxZZGroups];
+  // batches_sent: the anticommuting edges of every group (x never changes in
+  // a ZZ run, so edge (i, i + d) sends a record iff some nonzero string has
+  // x_i != x_{i+d}); the host maps (group, bit) back to gates
+  static constexpr int kMarkWords = 2 * kMaxZZGroups;
+  __device__ __forceinline__ void mark(Plane<W> xp, Plane<W> zp, double c, unsigned long long* acc) const {
+    if (c == 0.0) return;
+    const T x = pack(xp);
+    for (int k = 0; k < ng; ++k) {
+      const T a = (x ^ (x >> grp[k].d)) & grp[k].m;
+      const unsigned long long lo = (unsigned long long)a;
+      if (lo & ~acc[2 * k]) atomicOr(&acc[2 * k], lo);
+      if constexpr (W == 2) {
+        const unsigned long long hi = (unsigned long long)(a >> 64);
+        if (hi & ~acc[2 * k + 1]) atomicOr(&acc[2 * k + 1], hi);
+      }
+    }
+  }
+  __device__ void flush(const unsigned long long* acc, DevStats* st) const {
+    for (int w = threadIdx.x; w < 2 * ng; w += blockDim.x)
+      if (acc[w]) atomicOr(&st->zz_seen[w >> 1][w & 1], acc[w]);
+  }
   __device__ __forceinline__ static T pack(const Plane<W>& p) {
     if constexpr (W == 1) return p.w[0];
     else return (T)p.w[0] | ((T)p.w[1] << 64);
@@ -154,6 +201,9 @@ struct ZZRunProducer {
 template <int W>
 struct IdentityProducer {
   static constexpr int kMaxRec = 1;
+  static constexpr int kMarkWords = 0;
+  __device__ __forceinline__ void mark(Plane<W>, Plane<W>, double, unsigned long long*) const {}
+  __device__ void flush(const unsigned long long*, DevStats*) const {}
   __device__ __forceinline__ int emit(Plane<W> x, Plane<W> z, double c, Record<W>* out, uint32_t* nrec) const {
     out[0].x = x;
     out[0].z = z;
@@ -270,6 +320,16 @@ struct GateProducer {
   static constexpr int kMaxRec = 2;
   Plane<W> jx, jz;
   double cosv, sinv;
+  uint32_t seen_base;  // window index of the gate (batches_sent)
+  static constexpr int kMarkWords = 1;
+  __device__ __forceinline__ void mark(Plane<W> x, Plane<W> z, double c, unsigned long long* acc) const {
+    if (acc[0] || !(plane_parity_and<W>(x, jz) ^ plane_parity_and<W>(z, jx))) return;
+    const int b = phase_mod4<W>(x, z, jx, jz);
+    if (__dmul_rn(b == 1 ? sinv : -sinv, c) != 0.0) atomicOr(&acc[0], 1ull);  // emit's record condition
+  }
+  __device__ void flush(const unsigned long long* acc, DevStats* st) const {
+    if (threadIdx.x == 0 && acc[0]) mark_seen(st, seen_base);
+  }
   __device__ __forceinline__ int emit(Plane<W> x, Plane<W> z, double c, Record<W>* out, uint32_t* nrec) const {
     out[0].x = x;
     out[0].z = z;
@@ -335,6 +395,9 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
   const uint64_t off = g.off[it.g] + it.start;
   const Plane<W> z = load_plane<W>(g.z, it.g);
   unsigned long long records = 0;
+  __shared__ unsigned long long s_mark[P::kMarkWords > 0 ? P::kMarkWords : 1];  // batches_sent
+  for (int w = threadIdx.x; w < P::kMarkWords; w += kCta) s_mark[w] = 0;
+  __syncthreads();
   if constexpr (P::kMaxRec == 1) {
     // one record per string: slot counts aggregated per warp (strings of one
     // item share their old z, so a warp's records fall into few new groups)
@@ -345,7 +408,10 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
       if (i < it.len) {
         Record<W> rec[1];
         uint32_t nr = 0;
-        const int nrec = prod.emit(load_plane<W>(src.x, off + i), z, src.c[off + i], rec, &nr);
+        const Plane<W> xi = load_plane<W>(src.x, off + i);
+        const double ci = src.c[off + i];
+        const int nrec = prod.emit(xi, z, ci, rec, &nr);
+        if (nr) prod.mark(xi, z, ci, s_mark);
         records += nr;
         if (nrec) {
           const unsigned long long f = z_fingerprint<W>(rec[0].z, seed);
@@ -379,7 +445,10 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
   for (uint32_t i = threadIdx.x; i < it.len; i += kCta) {
     Record<W> rec[P::kMaxRec];
     uint32_t nr = 0;
-    int nrec = prod.emit(load_plane<W>(src.x, off + i), z, src.c[off + i], rec, &nr);
+    const Plane<W> xi = load_plane<W>(src.x, off + i);
+    const double ci = src.c[off + i];
+    int nrec = prod.emit(xi, z, ci, rec, &nr);
+    if (nr) prod.mark(xi, z, ci, s_mark);
     records += nr;
 #pragma unroll
     for (int r = 0; r < P::kMaxRec; ++r) {
@@ -414,6 +483,8 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
   }
   records = warp_sum64(records);
   if ((threadIdx.x & 31) == 0 && records) atomicAdd(&st->records, records);
+  __syncthreads();
+  prod.flush(s_mark, st);
 }
 
 // --------------------------- device-wide exclusive scan over uint32 -> u64
@@ -1182,7 +1253,9 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
   uint32_t* gpre = reinterpret_cast<uint32_t*>(slot + ((n + 7) & ~7u));  // input group prefix (Gi + 1; Gi <= n)
   __shared__ uint32_t scr[40];
   __shared__ unsigned long long s_rec;
+  __shared__ unsigned long long s_mark[P::kMarkWords > 0 ? P::kMarkWords : 1];  // batches_sent
   const uint32_t tid = threadIdx.x, lane = tid & 31;
+  for (int w = tid; w < P::kMarkWords; w += kSmallRegroupThreads) s_mark[w] = 0;
   for (uint32_t h = tid; h < tc; h += kSmallRegroupThreads) {
     kfp[h] = 0ull;
     state[h] = 0;
@@ -1236,7 +1309,9 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
     for (int k = 0; k < W; ++k) z.w[k] = gi.z[k][gg];
     Record<W> r;
     uint32_t nrec = 0;
-    prod.emit(load_plane<W>(ai.x, a), z, ai.c[a], &r, &nrec);
+    const Plane<W> xa = load_plane<W>(ai.x, a);
+    prod.emit(xa, z, ai.c[a], &r, &nrec);
+    if (nrec) prod.mark(xa, z, ai.c[a], s_mark);
     rec += nrec;
     // slots by a 64-bit fingerprint (no waiting on another thread's key);
     // the scatter verifies the full z (a collision fails the deferred check)
@@ -1322,6 +1397,7 @@ __global__ void __launch_bounds__(kSmallRegroupThreads) k_regroup_small(GroupVie
     ao.c[d] = r.c;
   }
   __syncthreads();
+  prod.flush(s_mark, st);
   if (tid == 0) {
     st->distinct = G;
     st->scan_total = total;

@@ -478,7 +478,10 @@ __global__ void __launch_bounds__(kCta) k_branch_zz(GroupView<W> g, uint32_t G, 
   const uint32_t rem32 = __reduce_add_sync(0xffffffffu, (uint32_t)removed);
   const uint32_t mc = __reduce_max_sync(0xffffffffu, r_mc);
   if ((tid & 31) == 0) {
-    if (rec32) atomicAdd(&st->records, (unsigned long long)rec32);
+    if (rec32) {
+      atomicAdd(&st->records, (unsigned long long)rec32);
+      mark_seen(st, st->seen_base + seq_rel);  // batches_sent: this gate sent a record
+    }
     if (rem32) atomicAdd(&st->removed, (unsigned long long)rem32);
     if (mc) atomicMax(&st->zz_maxcnt, mc);
   }

@@ -52,6 +52,7 @@ def run_both(pp, O, n, layers, initial, eps=0.0, cadence="gate", steps=None, che
             assert eng.global_max() == ora.global_max()
             assert ctr["records_sent"] == octr["records_sent"], (ctr, octr)
             assert ctr["removed"] == octr["removed"], (ctr, octr)
+            assert ctr["batches_sent"] == octr["batches_sent"], (ctr, octr)
     return eng, ora
 
 
@@ -241,7 +242,7 @@ def test_fusion_matches_unfused(pp, O):
     assert_same_terms(wa, ca, ow, oc, "fused vs oracle")
     assert_same_terms(wb, cb, ow, oc, "unfused vs oracle")
     for x, y in zip(ra, rb):
-        for k in ("term_count", "removed", "records_sent"):
+        for k in ("term_count", "removed", "records_sent", "batches_sent"):
             assert x[k] == y[k], (k, x, y)
 
 
