@@ -188,6 +188,50 @@ int pp_group_sizes(pp_engine* engine, uint64_t* groups, uint64_t* strings);
 int pp_density_histogram(pp_engine* engine, int bins, double global_max, double epsilon0, uint64_t* positive,
                          uint64_t* negative);
 
+/* ---- native sharded engine: one rank per GPU, SPMD, NCCL inside
+ * (the multi-GPU form of Engine).  Ownership is a
+ * z-plane hash into 4096 buckets, rebalanced from the global bucket
+ * histogram at every exchange; Rx runs are rank-local; strings move with one
+ * all-to-all after each Clifford/ZZ step; eps0 > 0 runs reduce their
+ * per-gate maxima over the ranks once per run.  Every rank calls every entry
+ * point in the same order (collective calls).
+ *
+ * Bootstrap: rank 0 calls pp_nccl_unique_id and hands the 128 bytes to every
+ * rank out of band (MPI, a store, a file); each rank then calls
+ * pp_sharded_create with its device in config->device.  pp_hub_create makes
+ * an in-process transport instead (ranks as threads of one process sharing
+ * one device; for tests). */
+typedef struct pp_sharded pp_sharded;
+typedef struct pp_hub pp_hub;
+typedef struct {
+  uint64_t exchanges;     /* string exchanges so far */
+  uint64_t records_moved; /* strings this rank sent */
+  uint64_t exchange_ns;   /* wall time in exchanges (rebalance + all-to-all + ingest) */
+  double balance;         /* max / min strings per rank after the last rebalance */
+} pp_shard_stats;
+
+int pp_nccl_unique_id(uint8_t id[128]);
+int pp_sharded_create(const pp_config* config, int world, int rank, const uint8_t id[128], pp_sharded** out);
+pp_hub* pp_hub_create(int world);
+void pp_hub_destroy(pp_hub* hub);
+int pp_sharded_create_hub(const pp_config* config, pp_hub* hub, int rank, pp_sharded** out);
+void pp_sharded_destroy(pp_sharded* s);
+/* every rank passes the same terms; each keeps those it owns */
+int pp_sharded_set_initial(pp_sharded* s, const uint64_t* words, const double* coeffs, size_t count);
+int pp_sharded_apply_gates(pp_sharded* s, const pp_gate* gates, size_t count);
+/* one run_circuit layer (gates in application order) + the global <0|O|0> */
+int pp_sharded_apply_layer(pp_sharded* s, const pp_gate* gates, size_t count, double* observable);
+int pp_sharded_truncate_now(pp_sharded* s);
+int pp_sharded_term_count(pp_sharded* s, uint64_t* out);
+int pp_sharded_global_max(pp_sharded* s, double* out);
+int pp_sharded_take_counters(pp_sharded* s, pp_counters* out); /* removed/batches/records summed over ranks */
+int pp_sharded_stats(pp_sharded* s, pp_shard_stats* out);
+/* this rank's strings (sorted), for checkpoints and tests */
+int pp_sharded_local_count(pp_sharded* s, uint64_t* out);
+int pp_sharded_local_export(pp_sharded* s, uint64_t* words, double* coeffs, uint64_t cap, uint64_t* count);
+void* pp_sharded_stream(const pp_sharded* s);
+const char* pp_sharded_last_error(const pp_sharded* s);
+
 #ifdef __cplusplus
 }
 #endif

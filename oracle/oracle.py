@@ -286,6 +286,8 @@ def _ref_lib():
         L.ppref_time_circuit.argtypes = [_vp, _int, _vp, _vp, _vp, _vp, _int, _vp, _vp]
         L.ppref_term_count.restype = _u64
         L.ppref_term_count.argtypes = [_vp]
+        L.ppref_shard_sizes.restype = _int
+        L.ppref_shard_sizes.argtypes = [_vp, _vp, _int]
         L.ppref_global_max.restype = _dbl
         L.ppref_global_max.argtypes = [_vp]
         L.ppref_expectation.restype = _dbl
@@ -411,6 +413,11 @@ class RefEngine:
 
     def term_count(self):
         return int(self.L.ppref_term_count(self.h))
+
+    def shard_sizes(self):
+        out = np.zeros(4096, np.uint64)
+        k = self.L.ppref_shard_sizes(self.h, out.ctypes.data, 4096)
+        return [int(v) for v in out[:k]]
 
     def global_max(self):
         return self.L.ppref_global_max(self.h)

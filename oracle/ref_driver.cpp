@@ -220,6 +220,14 @@ uint64_t ppref_term_count(void* h) {
   return static_cast<Handle*>(h)->engine.term_count();
 }
 
+// Engine::shard_sizes (engine.hpp:162): strings per worker shard.
+int ppref_shard_sizes(void* h, uint64_t* out, int cap) {
+  std::vector<size_t> sz = static_cast<Handle*>(h)->engine.shard_sizes();
+  int k = 0;
+  for (; k < cap && k < (int)sz.size(); ++k) out[k] = sz[k];
+  return k;
+}
+
 double ppref_global_max(void* h) {
   return static_cast<Handle*>(h)->engine.global_max();
 }

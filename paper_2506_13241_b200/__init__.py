@@ -25,6 +25,9 @@ except ImportError as exc:  # pragma: no cover - exercised only when unbuilt
 
 Circuit = _impl.Circuit
 Engine = _impl.Engine
+NativeShardedEngine = _impl.NativeShardedEngine
+ShardHub = _impl.ShardHub
+nccl_unique_id = _impl.nccl_unique_id
 Gate = _impl.Gate
 Geometry = _impl.Geometry
 NumericalError = _impl.NumericalError

@@ -751,6 +751,7 @@ Engine& Engine::operator=(Engine&& o) noexcept {
     config_ = o.config_;
     handle_ = o.handle_;
     layer_context_ = o.layer_context_;
+    mirror_valid_ = false;
     o.handle_ = nullptr;
   }
   return *this;
@@ -763,25 +764,52 @@ void Engine::set_initial(const std::vector<std::pair<PauliString, double>>& term
     for (int k = 0; k < 4; ++k) w[4 * i + k] = terms[i].first.words[k];
     c[i] = terms[i].second;
   }
+  invalidate();
   check(pp_set_initial(handle_, w.data(), c.data(), terms.size()));
 }
 void Engine::apply_gate(const Gate& gate) {
+  invalidate();
   pp_gate g = to_pp(gate);
   check(pp_apply_gate(handle_, &g));
 }
 void Engine::apply_gates(const std::vector<Gate>& gates) {
+  invalidate();
   std::vector<pp_gate> g(gates.size());
   for (size_t i = 0; i < gates.size(); ++i) g[i] = to_pp(gates[i]);
   check(pp_apply_gates(handle_, g.data(), g.size()));
 }
 double Engine::apply_layer(const std::vector<Gate>& gates) {
+  invalidate();
   std::vector<pp_gate> g(gates.size());
   for (size_t i = 0; i < gates.size(); ++i) g[i] = to_pp(gates[i]);
   double obs = 0.0;
   check(pp_apply_layer(handle_, g.data(), g.size(), &obs));
   return obs;
 }
-void Engine::truncate_now() { check(pp_truncate_now(handle_)); }
+void Engine::truncate_now() {
+  invalidate();
+  check(pp_truncate_now(handle_));
+}
+std::span<const SparseOperator> Engine::shards() const {
+  if (!mirror_valid_) {
+    const SparseOperator all = merged();
+    const PartitionSpec& spec = config_.partition;
+    shard_mirror_.assign(spec.worker_count, SparseOperator{});
+    for (auto& sh : shard_mirror_) sh.n = config_.n;
+    for (size_t i = 0; i < all.keys.size(); ++i) {  // merged() is sorted: every shard stays sorted
+      SparseOperator& sh = shard_mirror_[owner(spec, all.keys[i], config_.n)];
+      sh.keys.push_back(all.keys[i]);
+      sh.values.push_back(all.values[i]);
+    }
+    mirror_valid_ = true;
+  }
+  return shard_mirror_;
+}
+std::vector<size_t> Engine::shard_sizes() const {
+  std::vector<size_t> out;
+  for (const SparseOperator& sh : shards()) out.push_back(sh.term_count());
+  return out;
+}
 uint64_t Engine::term_count() const {
   uint64_t n = 0;
   check(pp_term_count(handle_, &n));
@@ -824,6 +852,10 @@ Engine::Counters Engine::take_counters() {
   out.records_sent = c.records_sent;
   out.gates = c.gates;
   out.total_ns = c.branch_ns + c.exchange_ns + c.truncate_ns + c.other_ns;
+  out.timers.generate_ns = c.branch_ns;
+  out.timers.exchange_ns = c.exchange_ns;
+  out.timers.apply_ns = c.other_ns;
+  out.timers.truncate_ns = c.truncate_ns;
   return out;
 }
 

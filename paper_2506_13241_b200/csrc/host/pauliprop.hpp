@@ -16,6 +16,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <span>
 #include <vector>
 
 struct pp_engine;
@@ -212,13 +213,30 @@ class Engine {
   double expectation_zero_state() const;
   double coefficient(const PauliString& index) const;
   SparseOperator merged() const;
+  // Host mirror of the reference's per-worker shards (engine.hpp:161-162):
+  // the operator split by the block-sum owner map of config().partition,
+  // each shard sorted.  Built on first use, invalidated by every change.
+  std::span<const SparseOperator> shards() const;
+  std::vector<size_t> shard_sizes() const;
 
+  // engine.hpp:109-118.  The GPU fuses generate and apply into one branch
+  // kernel: generate_ns carries the branch+merge time, exchange_ns the
+  // regroups after Clifford/ZZ runs, truncate_ns the reductions and
+  // truncation, apply_ns the rest of the device time.
+  struct PhaseTimers {
+    uint64_t generate_ns = 0;
+    uint64_t exchange_ns = 0;
+    uint64_t apply_ns = 0;
+    uint64_t truncate_ns = 0;
+    uint64_t total_ns() const { return generate_ns + exchange_ns + apply_ns + truncate_ns; }
+  };
   struct Counters {
     uint64_t removed = 0;
     uint64_t batches_sent = 0;
     uint64_t records_sent = 0;
     uint64_t gates = 0;
     uint64_t total_ns = 0;
+    PhaseTimers timers;
   };
   Counters take_counters();
   void set_layer_context(int t) { layer_context_ = t; }
@@ -229,6 +247,9 @@ class Engine {
  private:
   EngineConfig config_;
   pp_engine* handle_ = nullptr;
+  mutable std::vector<SparseOperator> shard_mirror_;
+  mutable bool mirror_valid_ = false;
+  void invalidate() const { mirror_valid_ = false; }
   int layer_context_ = 0;
 };
 

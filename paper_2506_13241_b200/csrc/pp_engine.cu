@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -382,6 +383,10 @@ class EngineBase {
                            uint64_t* counts) = 0;
   virtual void shard_ingest(const uint64_t* rec, uint64_t count, bool device) = 0;
   virtual const uint64_t* device_records() const = 0;
+  virtual void set_bucket_table(const uint16_t* table) = 0;
+  virtual void bucket_histogram(uint64_t seed, uint64_t* hist) = 0;
+  virtual void set_spec_reduce(std::function<void(std::vector<unsigned long long>&)> f) = 0;
+  virtual void set_global_max(double g) = 0;
   virtual double norm2() = 0;
   virtual void group_sizes(uint64_t* groups, uint64_t* strings) = 0;
   virtual void histogram(int bins, double gmax, double epsilon0, uint64_t* pos, uint64_t* neg) = 0;
@@ -482,7 +487,8 @@ class EngineImpl final : public EngineBase {
     for (auto& a : arena_) f(a.buf);
     for (auto& g : groups_) f(g.buf);
     for (DevBuf* b : {&evict_cnt_, &evict_buf_, &spec_buf_, &backup_, &stats_buf_, &list_, &items_, &rec_slot_,
-                      &table_, &scan_tmp_, &scan_gid_, &scan_off_, &diag_z_, &diag_c_, &cliff_, &thr_, &ztab_})
+                      &table_, &scan_tmp_, &scan_gid_, &scan_off_, &diag_z_, &diag_c_, &cliff_, &thr_, &ztab_,
+                      &norms_, &sub_groups_, &buckets_})
       f(*b);
   }
   size_t device_bytes() const override {
@@ -677,7 +683,9 @@ class EngineImpl final : public EngineBase {
       plan_.clear();
       size_t i = 0;
       // runs are capped so one run always fits a batch window (reserve_window)
+      // and an X-type run one sublayer launch
       constexpr size_t kRunCap = kSeenGates / 2;
+      static_assert(kMaxSubGates <= kRunCap, "an X-type run fits the window");
       while (i < count) {
         if (fusion_allowed() && is_clifford(gates[i])) {
           size_t j = i;
@@ -686,7 +694,9 @@ class EngineImpl final : public EngineBase {
           i = j;
         } else if (is_x_type(gates[i])) {
           size_t j = i;
-          while (j < count && j - i < kRunCap && is_x_type(gates[j]) && !(fusion_allowed() && is_clifford(gates[j]))) ++j;
+          while (j < count && j - i < (size_t)kMaxSubGates && is_x_type(gates[j]) &&
+                 !(fusion_allowed() && is_clifford(gates[j])))
+            ++j;
           plan_.push_back({1, i, j});
           i = j;
         } else {
@@ -813,6 +823,16 @@ class EngineImpl final : public EngineBase {
     // epsilon0 = 0 (no global threshold), no budget: the whole run in one
     // launch, every group through its gates (k_branch_sublayer)
     const bool no_budget = !budget;
+    // sharded eps0 > 0 (pp_sharded): the speculative run with every rank's
+    // per-gate maxima combined (spec_reduce_), on every rank whatever its size
+    const bool coordinated = external() && spec_reduce_ && cfg_.epsilon0 > 0.0 && do_trunc;
+    if (coordinated) {
+      if (count > (size_t)kMaxSubGates) throw EngineError(PP_ERR_INTERNAL, "sharded X-type run longer than a sublayer");
+      ensure_sorted();
+      if (!run_rx_speculative(prm, seq0, t0))
+        throw EngineError(PP_ERR_RESOURCE, "sharded run: the speculative sublayer did not fit the device");
+      return;
+    }
     const bool independent = no_budget && (external() || !do_trunc || (cfg_.epsilon0 == 0.0 && !may_hold_zeros_));
     if (independent && count <= (size_t)kMaxSubGates && G_) {
       SubGates sgates = rx_sg_;
@@ -835,15 +855,12 @@ class EngineImpl final : public EngineBase {
       return;
     }
     ensure_sorted();  // the per-gate kernels pair strings by x order
-    // speculative fused run for epsilon0 > 0 (exact, but two passes per run on
-    // these workloads: opt-in until the first prediction is right more often)
     // epsilon0 > 0 at per-gate cadence: the whole run in one launch with
-    // predicted thresholds (verified bit-exactly, rolled back otherwise),
-    // opt-in (PP_SPECULATE): under truncation the dense blocks of a run are
-    // far larger than what survives, so the per-gate launches win here
-    const bool speculate = std::getenv("PP_SPECULATE") != nullptr;
+    // predicted thresholds, verified bit-exactly and rolled back otherwise
+    // (PP_NO_SPECULATE: the per-gate launches below)
+    const bool speculate = std::getenv("PP_NO_SPECULATE") == nullptr;
     if (speculate && no_budget && do_trunc && !external() && cfg_.epsilon0 > 0.0 && count <= (size_t)kMaxSubGates &&
-        G_ && !(cfg_.flags & PP_FLAG_PROFILE) && run_rx_speculative(prm, seq0, t0))
+        G_ && run_rx_speculative(prm, seq0, t0))
       return;
     // per-gate truncation without a budget: deferred (k_thresh / k_flush)
     const bool lazy = epi && do_trunc && no_budget && !external() && cfg_.epsilon0 > 0.0 && !keep_zeros_ &&
@@ -921,12 +938,16 @@ class EngineImpl final : public EngineBase {
     spec_buf_.ensure(count * 16 + 64);
     double* d_tpred = spec_buf_.as<double>();
     unsigned long long* d_gmax = reinterpret_cast<unsigned long long*>(d_tpred + count);
+    if (std::getenv("PP_NO_DISCOVERY") == nullptr) discover_thresholds(sgates, seq0, tpred);
     int faults = 0;
     for (int attempt = 0; attempt < 8; ++attempt) {
+      bool give_up = false;
       sync_state();
       // every gate application writes fresh space (the pre-run regions are
       // the rollback point): reserve ~24 |O| when memory allows
-      const uint64_t want = 24 * live_ + (1u << 16);
+      // (groups keep their intermediate versions in the CTAs' L2 scratch;
+      // the arena takes the results and large groups' per-gate versions)
+      const uint64_t want = (faults ? 8 : 3) * live_ + (1u << 16);
       if (bump_ + want > arena_[cur_].cap) {
         size_t free_b = 0, total_b = 0;
         PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -934,9 +955,15 @@ class EngineImpl final : public EngineBase {
         const uint64_t afford =
             (uint64_t)((free_b + DevicePool::get().cached_bytes(cfg_.device) + parked + arena_[1 - cur_].buf.bytes) *
                        0.8) / R;
-        if (live_ + want > afford && faults > 0) return false;
-        gc_into_other(std::max<uint64_t>(std::min<uint64_t>(live_ + want, afford), next_arena_target()));
+        give_up = live_ + want > afford && faults > 0;
+        if (!give_up) gc_into_other(std::max<uint64_t>(std::min<uint64_t>(live_ + want, afford), next_arena_target()));
       }
+      if (spec_reduce_) {  // all ranks give up together
+        std::vector<unsigned long long> v{give_up ? 1ull : 0ull};
+        spec_reduce_(v);
+        give_up = v[0] != 0;
+      }
+      if (give_up) return false;
       // snapshot of the group table: the rollback point
       const size_t gbytes = (size_t)groups_[gcur_].cap * (8 * W + 8 + 8 + 8 + 4 + 4 + 4 + 4);
       backup_.ensure(gbytes);
@@ -960,13 +987,24 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(copy_async(gm.data(), d_gmax, count * 8, cudaMemcpyDeviceToHost, stream_));
       dirty_ = true;
       sync_state();  // harvests counters, reads the arena fault flag
-      bool exact = !arena_fault_;
+      bool any_fault = arena_fault_;
+      bool nonfinite = h_stats_->red[2].nonfinite != 0;
+      if (spec_reduce_) {
+        std::vector<unsigned long long> v(gm);
+        v.push_back(any_fault ? 1ull : 0ull);
+        v.push_back(nonfinite ? 1ull : 0ull);
+        spec_reduce_(v);
+        std::copy(v.begin(), v.begin() + count, gm.begin());
+        any_fault = v[count] != 0;
+        nonfinite = v[count + 1] != 0;
+      }
+      bool exact = !any_fault;
       std::vector<double> tobs(count);
       for (size_t k = 0; k < count; ++k) {
         tobs[k] = cfg_.epsilon0 * __builtin_bit_cast(double, gm[k]);  // engine.cpp:345
         if (__builtin_bit_cast(uint64_t, tobs[k]) != __builtin_bit_cast(uint64_t, tpred[k])) exact = false;
       }
-      if (exact && h_stats_->red[2].nonfinite)
+      if (exact && nonfinite)
         throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient in gates " + std::to_string(gates_applied_ + 1) +
                                                 ".." + std::to_string(gates_applied_ + count));
       if (exact) {
@@ -995,11 +1033,12 @@ class EngineImpl final : public EngineBase {
                        tpred[first], (unsigned long long)__builtin_bit_cast(uint64_t, tpred[first]), tobs[first],
                        (unsigned long long)gm[first], gmax_);
       }
-      const bool fault = arena_fault_;
-      if (fault) {
-        k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
-        ++launches_;
-        arena_fault_ = false;
+      if (any_fault) {
+        if (arena_fault_) {
+          k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
+          ++launches_;
+          arena_fault_ = false;
+        }
         if (++faults >= 2) {  // cannot hold a whole speculative run: gates one by one
           dirty_ = true;
           sync_state();
@@ -1019,6 +1058,108 @@ class EngineImpl final : public EngineBase {
       }
     }
     return false;  // did not converge: the caller runs the gates one by one
+  }
+
+  // The exact thresholds of the run from the groups that can hold its maxima
+  // (k_group_norms / k_select_groups): the speculative sublayer on that
+  // subset alone, iterated to a fixed point, outputs discarded (the bump
+  // pointer and the statistics are reset afterwards).  On success tpred holds
+  // epsilon0 * gmax_k for every gate; otherwise it is left as it was.
+  void discover_thresholds(const SubGates& sgates, uint64_t seq0, std::vector<double>& tpred) {
+    const size_t count = tpred.size();
+    // (sharded: every rank takes part in every collective, empty or not)
+    if (!(gmax_ > 0.0) || (G_ == 0 && !spec_reduce_)) return;
+    const uint64_t bump0 = bump_;
+    norms_.ensure((size_t)G_ * 8 + 64);
+    ensure_sub_groups(std::max<uint32_t>(G_, 1));
+    double* d_norm = norms_.as<double>();
+    unsigned int* d_count = reinterpret_cast<unsigned int*>(d_norm + G_);
+    double* d_tp = spec_buf_.as<double>();
+    unsigned long long* d_gm = reinterpret_cast<unsigned long long*>(d_tp + count);
+    push_scalars(seq0);
+    k_group_norms<W><<<persistent_grid(), kCta, 0, stream_>>>(gview(gcur_), aview(cur_), d_stats_, d_norm);
+    ++launches_;
+    std::vector<double> tp(count, cfg_.epsilon0 * gmax_), tobs(count);
+    std::vector<unsigned long long> gm(count);
+    double L = 0.25 * gmax_;
+    bool ok = false;
+    for (int round = 0; round < 4 && !ok; ++round) {
+      bool fixed = false;
+      for (int attempt = 0; attempt < 8 && !fixed; ++attempt) {
+        // a fresh copy of the subset's table entries (the run rewrites them)
+        PP_CUDA(cudaMemsetAsync(d_count, 0, 4, stream_));
+        k_set_scalars<<<1, 1, 0, stream_>>>(d_stats_, G_, arena_[cur_].cap, seq0, window_index());
+        k_select_groups<W><<<std::max<uint32_t>(1u, blocks(G_)), kCta, 0, stream_>>>(gview(gcur_), d_stats_, d_norm, L,
+                                                                                     sub_view(), d_count);
+        k_use_group_count<<<1, 1, 0, stream_>>>(d_stats_, d_count, bump0);
+        launches_ += 2;
+        PP_CUDA(copy_async(d_tp, tp.data(), count * 8, cudaMemcpyHostToDevice, stream_));
+        PP_CUDA(cudaMemsetAsync(d_gm, 0, count * 8, stream_));
+        k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
+            sub_view(), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_tp, d_gm, d_stats_);
+        launches_ += 2;
+        PP_CUDA(copy_async(gm.data(), d_gm, count * 8, cudaMemcpyDeviceToHost, stream_));
+        fetch_stats();
+        PP_CUDA(cudaGetLastError());
+        if (spec_reduce_) {
+          std::vector<unsigned long long> v(gm);
+          v.push_back(h_stats_->err_arena ? 1ull : 0ull);
+          spec_reduce_(v);
+          std::copy(v.begin(), v.begin() + count, gm.begin());
+          if (v[count]) break;
+        } else if (h_stats_->err_arena) {
+          break;  // no room for the subset's outputs: plain speculation
+        }
+        fixed = true;
+        for (size_t k = 0; k < count; ++k) {
+          tobs[k] = cfg_.epsilon0 * __builtin_bit_cast(double, gm[k]);  // engine.cpp:345
+          if (__builtin_bit_cast(uint64_t, tobs[k]) != __builtin_bit_cast(uint64_t, tp[k])) fixed = false;
+        }
+        tp = tobs;
+      }
+      if (!fixed) break;
+      double mn = INFINITY;
+      for (size_t k = 0; k < count; ++k) mn = std::min(mn, __builtin_bit_cast(double, gm[k]));
+      if (mn >= L) {
+        ok = true;
+      } else {
+        L = 0.5 * mn;  // a max fell below the bound: widen the subset
+      }
+      if (std::getenv("PP_DEBUG"))
+        std::fprintf(stderr, "[pp] discovery round %d: L=%.6g min gmax_k=%.6g subset %u groups -> %s\n", round, L,
+                     mn, h_stats_->G_dev, ok ? "ok" : "widen");
+    }
+    reset_stats(bump0);  // discard the subset runs' outputs and counters
+    if (ok) {
+      tpred = tp;
+      ++discoveries_;
+    }
+  }
+  GroupView<W> sub_view() const {
+    GroupView<W> v;
+    const uint64_t C = sub_cap_;
+    char* b = sub_groups_.template as<char>();
+    for (int k = 0; k < W; ++k) v.z[k] = reinterpret_cast<uint64_t*>(b) + k * C;
+    char* p = b + W * C * 8;
+    v.off = reinterpret_cast<uint64_t*>(p);
+    p += C * 8;
+    v.gmax = reinterpret_cast<double*>(p);
+    p += C * 8;
+    v.gmin = reinterpret_cast<double*>(p);
+    p += C * 8;
+    v.cnt = reinterpret_cast<uint32_t*>(p);
+    p += C * 4;
+    v.cap = reinterpret_cast<uint32_t*>(p);
+    p += C * 4;
+    v.flags = reinterpret_cast<uint32_t*>(p);
+    p += C * 4;
+    v.stamp = reinterpret_cast<uint32_t*>(p);
+    return v;
+  }
+  void ensure_sub_groups(uint32_t n) {
+    if (sub_cap_ >= n) return;
+    sub_groups_.ensure((size_t)n * (8 * W + 8 + 8 + 8 + 4 + 4 + 4 + 4));
+    sub_cap_ = n;
   }
 
   void launch_sublayer() {
@@ -1397,7 +1538,7 @@ class EngineImpl final : public EngineBase {
     evict_cnt_.ensure(world * 8 * 2);
     unsigned long long* dcnt = evict_cnt_.as<unsigned long long>();
     PP_CUDA(cudaMemsetAsync(dcnt, 0, world * 8, stream_));
-    k_evict_count<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, world, rank, seed, dcnt);
+    k_evict_count<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, world, rank, seed, dcnt, bucket_table());
     std::vector<unsigned long long> hc(world);
     PP_CUDA(copy_async(hc.data(), dcnt, world * 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
@@ -1414,7 +1555,7 @@ class EngineImpl final : public EngineBase {
     evict_buf_.ensure(total * rw * 8);
     PP_CUDA(copy_async(dcnt + world, off.data(), world * 8, cudaMemcpyHostToDevice, stream_));
     k_evict_write<W><<<G_, kCta, 0, stream_>>>(gview(gcur_), aview(cur_), world, rank, seed, dcnt + world,
-                                               evict_buf_.as<uint64_t>());
+                                               evict_buf_.as<uint64_t>(), bucket_table());
     if (out)  // host-staged exchange; otherwise the records stay in evict_buf_ (device_records())
       PP_CUDA(copy_async(out, evict_buf_.p, total * rw * 8, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(cudaStreamSynchronize(stream_));
@@ -1424,6 +1565,32 @@ class EngineImpl final : public EngineBase {
   }
 
   const uint64_t* device_records() const override { return evict_buf_.as<uint64_t>(); }
+
+  // ---- sharded use (pp_sharded.cuh)
+  void set_bucket_table(const uint16_t* table) override {  // kBuckets entries, or nullptr: hash mod world
+    if (!table) {
+      buckets_on_ = false;
+      return;
+    }
+    buckets_.ensure(kBuckets * sizeof(uint16_t));
+    PP_CUDA(copy_async(buckets_.p, table, kBuckets * sizeof(uint16_t), cudaMemcpyHostToDevice, stream_));
+    buckets_on_ = true;
+  }
+  const uint16_t* bucket_table() const { return buckets_on_ ? buckets_.as<uint16_t>() : nullptr; }
+  void bucket_histogram(uint64_t seed, uint64_t* hist) override {  // kBuckets strings-per-bucket counts
+    sync_state();
+    evict_cnt_.ensure(kBuckets * 8);
+    unsigned long long* d = evict_cnt_.as<unsigned long long>();
+    PP_CUDA(cudaMemsetAsync(d, 0, kBuckets * 8, stream_));
+    if (G_) {
+      k_bucket_hist<W><<<blocks(G_), kCta, 0, stream_>>>(gview(gcur_), G_, seed, d);
+      ++launches_;
+    }
+    PP_CUDA(copy_async(hist, d, kBuckets * 8, cudaMemcpyDeviceToHost, stream_));
+    PP_CUDA(cudaStreamSynchronize(stream_));
+  }
+  void set_spec_reduce(std::function<void(std::vector<unsigned long long>&)> f) override { spec_reduce_ = std::move(f); }
+  void set_global_max(double g) override { gmax_ = g; }
 
   void shard_ingest(const uint64_t* rec, uint64_t count, bool device) override {
     sync_state();
@@ -1509,6 +1676,9 @@ class EngineImpl final : public EngineBase {
 
   bool fusion_allowed() const {
     if (cfg_.flags & PP_FLAG_NO_CLIFFORD_FUSION) return false;
+    // per-layer cadence keeps each gate's zeroed parents until the layer's
+    // truncation, and a later gate may revive one: gate by gate is exact
+    if (keep_zeros_) return false;
     // a fused run never exceeds |O|, but the reference's transient count
     // inside a Clifford gate can reach 2|O| before truncation
     return cfg_.max_terms == 0 || 2 * live_ <= cfg_.max_terms;
@@ -1517,7 +1687,8 @@ class EngineImpl final : public EngineBase {
   // ----- buffers
   struct Arena {
     DevBuf buf;
-    uint64_t cap = 0;
+    uint64_t cap = 0;     // strings of bump space
+    uint64_t stride = 0;  // plane stride (cap + scratch tail)
   };
   struct Groups {
     DevBuf buf;
@@ -1526,8 +1697,8 @@ class EngineImpl final : public EngineBase {
   ArenaView<W> aview(int i) const {
     ArenaView<W> v;
     uint64_t* b = arena_[i].buf.template as<uint64_t>();
-    for (int k = 0; k < W; ++k) v.x[k] = b + k * arena_[i].cap;
-    v.c = reinterpret_cast<double*>(b + W * arena_[i].cap);
+    for (int k = 0; k < W; ++k) v.x[k] = b + k * arena_[i].stride;
+    v.c = reinterpret_cast<double*>(b + W * arena_[i].stride);
     return v;
   }
   GroupView<W> gview(int i) const {
@@ -1551,12 +1722,19 @@ class EngineImpl final : public EngineBase {
     v.stamp = reinterpret_cast<uint32_t*>(p);
     return v;
   }
+  // cap strings of bump space, plus (speculative eps0 > 0 runs) the per-CTA
+  // scratch tail of k_branch_sublayer (kSpecScratch)
   void ensure_arena(int i, uint64_t cap) {
     if (arena_[i].cap >= cap) return;
     arena_[i].buf.release();
-    arena_[i].cap = 0;
-    arena_[i].buf.ensure(cap * R);
+    arena_[i].cap = arena_[i].stride = 0;
+    const uint64_t tail = spec_capable() ? 2ull * kSpecScratch * sub_grid_ : 0;
+    arena_[i].buf.ensure((cap + tail) * R);
     arena_[i].cap = cap;
+    arena_[i].stride = cap + tail;
+  }
+  bool spec_capable() const {
+    return cfg_.epsilon0 > 0.0 && cfg_.cadence == PP_CADENCE_GATE && !external() && cfg_.max_terms == 0;
   }
   void ensure_groups(int i, uint32_t cap) {
     if (groups_[i].cap >= cap) return;
@@ -1933,6 +2111,9 @@ class EngineImpl final : public EngineBase {
   // A run of Clifford Z_i Z_j gates (i != j, no X/Y): split into matchings,
   // then into equal-offset groups, and regroup with ZZRunProducer.
   bool try_zz_run(const pp_gate* gates, size_t count, bool sort) {
+    // a previous fused ZZ run's edge masks are decoded with zz_edges_: harvest
+    // them before zz_edges_ can change
+    if (zz_seen_pending_) sync_state();
     if (zz_key_.size() == count && std::memcmp(zz_key_.data(), gates, count * sizeof(pp_gate)) == 0) {
       if (!zz_ok_) return false;
       note_zz_run();
@@ -2297,6 +2478,18 @@ class EngineImpl final : public EngineBase {
   static constexpr size_t kLazyWindow = 4096;  // gates per deferred-truncation window
   DevBuf thr_;                // thr[j] = max(T_j .. T_now) over the open window
   std::vector<GraphExecPtr> held_graphs_;  // graphs launched since the last stream sync
+  DevBuf norms_, sub_groups_;  // threshold discovery: group norms, the subset's table
+  DevBuf buckets_;             // sharded: bucket -> rank table (kBuckets uint16)
+  bool buckets_on_ = false;
+ public:
+  // Sharded runs (pp_sharded_*): every rank's observations of a speculative
+  // run -- the per-gate maxima and the fault / non-finite / give-up flags --
+  // are combined by an element-wise max over the ranks before any decision,
+  // so all ranks accept, roll back or give up together.
+  std::function<void(std::vector<unsigned long long>&)> spec_reduce_;
+ private:
+  uint32_t sub_cap_ = 0;
+  uint64_t discoveries_ = 0;
   bool lazy_open_ = false;
   uint64_t lazy_base_ = 0;
   uint32_t lazy_len_ = 0;
@@ -2341,7 +2534,9 @@ class EngineImpl final : public EngineBase {
   uint32_t zz_seen_base_ = 0;
   uint32_t window_index() const { return (uint32_t)(gates_applied_ - seen_w0_); }
   void note_zz_run() {
-    if (zz_seen_pending_) sync_state();  // one fused ZZ run per harvest (its edge masks share one slot)
+    // settle everything launched so far first: regroup's own sync_state must
+    // not harvest (and consume) this run's mask slot before the run exists
+    sync_state();
     zz_seen_base_ = window_index();
     zz_seen_pending_ = true;
   }
@@ -2404,6 +2599,8 @@ class EngineImpl final : public EngineBase {
 
 }  // namespace ppgpu
 
+#include "pp_sharded.cuh"
+
 // ===========================================================================
 // C-ABI
 // ===========================================================================
@@ -2465,7 +2662,8 @@ std::string engine_key(const pp_config& c) {
   put(&c.device, sizeof c.device);
   put(&c.flags, sizeof c.flags);
   put(&c.mem_fraction, sizeof c.mem_fraction);
-  for (const char* v : {"PP_TIGHT_ARENA", "PP_NO_DENSE", "PP_DENSE_MAXK", "PP_NO_DEFER", "PP_BLOCKING_SYNC", "PP_TRACE"}) {
+  for (const char* v : {"PP_TIGHT_ARENA", "PP_NO_DENSE", "PP_DENSE_MAXK", "PP_NO_DEFER", "PP_BLOCKING_SYNC", "PP_TRACE",
+                        "PP_NO_SPECULATE"}) {
     const char* x = std::getenv(v);
     k += '|';
     if (x) k += x;
@@ -2724,3 +2922,147 @@ uint32_t pp_shard_owner(const uint64_t* words, int n, uint64_t seed, uint32_t wo
 const char* pp_last_error(const pp_engine* e) { return e ? e->error.c_str() : g_create_error.c_str(); }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- sharded engine
+struct pp_sharded {
+  std::unique_ptr<ppgpu::ShardedDriver> d;
+  std::string error;
+};
+struct pp_hub {
+  explicit pp_hub(int w) : hub(w) {}
+  ppgpu::ThreadHub hub;
+};
+
+namespace {
+template <class F>
+int guarded_s(pp_sharded* s, F&& f) {
+  try {
+    f();
+    return PP_OK;
+  } catch (const ppgpu::EngineError& x) {
+    if (s) s->error = x.what();
+    return x.code;
+  } catch (const std::bad_alloc&) {
+    if (s) s->error = "host memory exhausted";
+    return PP_ERR_RESOURCE;
+  } catch (const std::exception& x) {
+    if (s) s->error = x.what();
+    return PP_ERR_INTERNAL;
+  }
+}
+int sharded_precheck(const pp_config* c) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    g_create_error = "no CUDA device available";
+    return PP_ERR_INTERNAL;
+  }
+  if (!c || c->n < 1 || c->n > 128 || !(c->epsilon0 >= 0.0) || c->device < 0 || c->device >= ndev) {
+    g_create_error = "invalid sharded engine configuration";
+    return PP_ERR_INVALID;
+  }
+  return PP_OK;
+}
+}  // namespace
+
+int pp_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return PP_ERR_INVALID;
+  try {
+    ncclUniqueId u;
+    ncclResult_t r = ppgpu::NcclApi::get().GetUniqueId(&u);
+    if (r != ncclSuccess) {
+      g_create_error = std::string("ncclGetUniqueId: ") + ppgpu::NcclApi::get().GetErrorString(r);
+      return PP_ERR_INTERNAL;
+    }
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+    return PP_OK;
+  } catch (const std::exception& x) {
+    g_create_error = x.what();
+    return PP_ERR_INTERNAL;
+  }
+}
+
+int pp_sharded_create(const pp_config* c, int world, int rank, const uint8_t id[128], pp_sharded** out) {
+  if (!out || !id || world < 1 || rank < 0 || rank >= world) return PP_ERR_INVALID;
+  *out = nullptr;
+  if (int rc = sharded_precheck(c)) return rc;
+  auto s = std::make_unique<pp_sharded>();
+  int rc = guarded_s(s.get(), [&] {
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    s->d = std::make_unique<ppgpu::ShardedDriver>(
+        *c, std::make_unique<ppgpu::NcclCollective>(world, rank, u, c->device));
+  });
+  if (rc != PP_OK) {
+    g_create_error = s->error;
+    return rc;
+  }
+  *out = s.release();
+  return PP_OK;
+}
+
+pp_hub* pp_hub_create(int world) { return world >= 1 ? new pp_hub(world) : nullptr; }
+void pp_hub_destroy(pp_hub* h) { delete h; }
+
+int pp_sharded_create_hub(const pp_config* c, pp_hub* hub, int rank, pp_sharded** out) {
+  if (!out || !hub || rank < 0 || rank >= hub->hub.world) return PP_ERR_INVALID;
+  *out = nullptr;
+  if (int rc = sharded_precheck(c)) return rc;
+  auto s = std::make_unique<pp_sharded>();
+  int rc = guarded_s(s.get(), [&] {
+    s->d = std::make_unique<ppgpu::ShardedDriver>(*c, std::make_unique<ppgpu::HubCollective>(&hub->hub, rank,
+                                                                                            c->device));
+  });
+  if (rc != PP_OK) {
+    g_create_error = s->error;
+    return rc;
+  }
+  *out = s.release();
+  return PP_OK;
+}
+
+void pp_sharded_destroy(pp_sharded* s) { delete s; }
+
+int pp_sharded_set_initial(pp_sharded* s, const uint64_t* words, const double* coeffs, size_t count) {
+  if (!s || (count && (!words || !coeffs))) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { s->d->set_initial(words, coeffs, count); });
+}
+int pp_sharded_apply_gates(pp_sharded* s, const pp_gate* gates, size_t count) {
+  if (!s || (count && !gates)) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { s->d->apply_gates(gates, count); });
+}
+int pp_sharded_apply_layer(pp_sharded* s, const pp_gate* gates, size_t count, double* observable) {
+  if (!s || !observable || (count && !gates)) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { *observable = s->d->apply_layer(gates, count); });
+}
+int pp_sharded_truncate_now(pp_sharded* s) {
+  if (!s) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { s->d->truncate_now(); });
+}
+int pp_sharded_term_count(pp_sharded* s, uint64_t* out) {
+  if (!s || !out) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { *out = s->d->term_count(); });
+}
+int pp_sharded_global_max(pp_sharded* s, double* out) {
+  if (!s || !out) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { *out = s->d->global_max(); });
+}
+int pp_sharded_take_counters(pp_sharded* s, pp_counters* out) {
+  if (!s || !out) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { *out = s->d->take_counters(); });
+}
+int pp_sharded_stats(pp_sharded* s, pp_shard_stats* out) {
+  if (!s || !out) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { s->d->stats(out); });
+}
+int pp_sharded_local_count(pp_sharded* s, uint64_t* out) {
+  if (!s || !out) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { *out = s->d->engine().term_count(); });
+}
+int pp_sharded_local_export(pp_sharded* s, uint64_t* words, double* coeffs, uint64_t cap, uint64_t* count) {
+  if (!s || !count || (cap && (!words || !coeffs))) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { *count = s->d->engine().export_terms(words, coeffs, cap); });
+}
+void* pp_sharded_stream(const pp_sharded* s) { return s ? s->d->engine().stream() : nullptr; }
+const char* pp_sharded_last_error(const pp_sharded* s) { return s ? s->error.c_str() : g_create_error.c_str(); }

@@ -1187,6 +1187,13 @@ __global__ void __launch_bounds__(kCta) k_branch_x(GroupView<W> g, ArenaView<W> 
 // resumes after its stamp.
 // ---------------------------------------------------------------------------
 constexpr int kMaxSubGates = 128;
+// Speculative (eps0 > 0) runs: each CTA of k_branch_sublayer ping-pongs a
+// group's intermediate versions through two halves of its own scratch
+// region in the arena tail ([cap + 2 kSpecScratch blockIdx, ...)), reused
+// gate after gate so they stay in L2; only the run's final strings are
+// written to fresh arena space.  Groups whose working set outgrows a half
+// take fresh arena space per gate.
+constexpr uint32_t kSpecScratch = 4096;
 struct SubGates {
   int ng;
   int8_t wq[kMaxSubGates];
@@ -1432,6 +1439,53 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
   constexpr bool spec = SPEC;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int j = j0; j < j1; ++j) {
+    if (!SPEC && j + 3 < j1 && half >= 8) {
+      // four stages per pass (radix 16): each thread takes the 16 points the
+      // four stage bits span and runs all four butterfly stages in registers
+      // -- per point the same operations in the same order as stage by
+      // stage, a quarter of the shared-memory round trips and barriers
+      uint32_t pm[4], q[4];
+      double cs[4], sn[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        pm[i] = __popc(P & ((1u << dc.sbit[j + i]) - 1u));
+        q[i] = pm[i];
+        cs[i] = dc.scos[j + i];
+        sn[i] = dc.ssin[j + i];
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a)  // ascending insertion positions
+#pragma unroll
+        for (int b2 = 0; b2 < 3 - a; ++b2)
+          if (q[b2] > q[b2 + 1]) {
+            const uint32_t t2 = q[b2];
+            q[b2] = q[b2 + 1];
+            q[b2 + 1] = t2;
+          }
+      const uint32_t sixteenth = half >> 3;
+      for (uint32_t t = threadIdx.x; t < sixteenth; t += kCta) {
+        uint32_t b = t;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) b = ((b >> q[i]) << (q[i] + 1)) | (b & ((1u << q[i]) - 1u));
+        double a[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          a[e] = d[b | ((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
+                   (((e >> 3) & 1) << pm[3])];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (!((e >> i) & 1)) dense_bfly(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed);
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          d[b | ((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
+            (((e >> 3) & 1) << pm[3])] = a[e];
+      }
+      __syncthreads();
+      j += 3;
+      continue;
+    }
     if (!SPEC && j + 1 < j1) {
       // two stages per pass (radix 4): each thread takes the four points a
       // pair of stage bits spans through both butterflies in registers --
@@ -2134,7 +2188,7 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
 //    eps * gmax_out[k] == tpred[k] for every k and otherwise roll the group
 //    table back and rerun with the observed thresholds.
 template <int W>
-__global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
+__global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
                                                            int keep_zeros, unsigned int* work, const double* tpred,
                                                            unsigned long long* gmax_out, DevStats* st) {
   __shared__ uint32_t s_touch[kMaxSubGates / 32];
@@ -2180,6 +2234,14 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
     if (!spec || m <= 0.0) return;
     const unsigned long long bits = (unsigned long long)__double_as_longlong(m);
     for (int j = a + (int)tid; j < b; j += kCta) atomicMax(&smax[j], bits);
+  };
+  const uint64_t scr0 = cap + 2ull * kSpecScratch * blockIdx.x;  // this CTA's scratch halves (spec mode)
+  auto in_scratch = [&](uint64_t a) { return a >= scr0 && a < scr0 + 2ull * kSpecScratch; };
+  // destination for n strings derived from src: the other scratch half when
+  // they fit, else fresh arena space
+  auto scratch_dst = [&](uint64_t from, uint32_t n) -> uint64_t {
+    if (n > kSpecScratch) return ~0ull;
+    return (in_scratch(from) && from == scr0) ? scr0 + kSpecScratch : scr0;
   };
   auto alloc = [&](uint32_t n, int k) -> bool {
     __syncthreads();
@@ -2285,15 +2347,23 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
               break;
             }
           contribute(last + 1, j_empty + 1 < k ? j_empty + 1 : k, curmax);
-          if (j_empty < k) n = 0;
+          if (j_empty < k) {  // every string is at or below that gate's threshold: all removed
+            if (tid == 0) atomicAdd(&st->removed, (unsigned long long)n);
+            n = 0;
+          }
         }
         if (n && curmin <= tp) {  // drop what those truncations removed, into fresh space
-          if (!alloc(n, k)) {
-            failed = true;
-            break;
+          // (the run's last truncation of a group goes straight to the arena)
+          uint64_t tdst = end ? ~0ull : scratch_dst(src, n);
+          if (tdst == ~0ull) {
+            if (!alloc(n, k)) {
+              failed = true;
+              break;
+            }
+            tdst = dst_s;
           }
           double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
-          const uint32_t w = copy_truncated<W>(ar, src, n, dst_s, tp, tscan, mx, mn);
+          const uint32_t w = copy_truncated<W>(ar, src, n, tdst, tp, tscan, mx, mn);
           mx = warp_max(mx);
           mn = warp_min(mn);
           double dv = 0.0;
@@ -2302,7 +2372,7 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
           if (tid != 0) rm = 0;
           reduce_group_stats(gs, mx, mn, dv, nf0, r0, rm);
           if (tid == 0 && rm) atomicAdd(&st->removed, rm);
-          src = dst_s;
+          src = tdst;
           cap_g = n;
           n = w;
           curmax = w ? mx : 0.0;
@@ -2313,11 +2383,14 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
       if (end || n == 0) break;
       const int wq = gates.wq[k];
       const uint64_t mq = gates.mq[k];
-      if (!alloc(2 * n, k)) {
-        failed = true;
-        break;
+      uint64_t dst = spec ? scratch_dst(src, 2 * n) : ~0ull;
+      if (dst == ~0ull) {
+        if (!alloc(2 * n, k)) {
+          failed = true;
+          break;
+        }
+        dst = dst_s;
       }
-      const uint64_t dst = dst_s;
       aff_elems += n;
       uint32_t out_n = 0;
       double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll), vall = 0.0;
@@ -2371,6 +2444,19 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
       __syncthreads();
     }
     if (failed) break;
+    if (spec && n && in_scratch(src)) {  // the run's result: out of the scratch, into fresh arena space
+      if (!alloc(n, gates.ng)) {
+        failed = true;
+        break;
+      }
+      const uint64_t o = dst_s;
+      for (uint32_t i = tid; i < n; i += kCta) {
+        store_plane<W>(ar.x, o + i, load_plane<W>(ar.x, src + i));
+        ar.c[o + i] = ar.c[src + i];
+      }
+      src = o;
+      cap_g = n;
+    }
     if (spec && changed && tid == 0) {
       g.off[gid] = src;
       g.cnt[gid] = n;
@@ -2392,6 +2478,68 @@ __global__ void __launch_bounds__(kCta) k_branch_sublayer(GroupView<W> g, ArenaV
   for (int k = tid; k < gates.ng; k += kCta)
     if (((s_seen[k >> 5] >> (k & 31)) & 1u) && s_gp.sinv[k] != 0.0) mark_seen(st, st->seen_base + k);
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
+}
+
+// ---------------------------------------------------------------------------
+// Threshold discovery for a speculative run (eps0 > 0, per-gate cadence).
+// Inside a run of X-type gates a group's strings only rotate among
+// themselves and lose strings to truncation, so the group's max |c| after
+// any of the run's gates is at most its L2 norm (up to rounding, covered by
+// a 1e-9 margin).  If L <= gmax_k for every gate k of the run, the groups
+// with norm < L cannot hold any gmax_k: the run's exact thresholds
+// epsilon0 * gmax_k follow from the groups with norm >= L alone.  The host
+// runs the speculative sublayer on that small subset (a copy of their table
+// entries, outputs discarded) until its thresholds are a fixed point, checks
+// min_k gmax_k >= L, and then runs the whole table once with them.
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(kCta) k_group_norms(GroupView<W> g, ArenaView<W> ar, const DevStats* st,
+                                                      double* norm) {
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < G; gi += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t n = g.cnt[gi];
+    const uint64_t o = g.off[gi];
+    double s = 0.0;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const double v = ar.c[o + i];
+      s = fma(v, v, s);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+    if (lane == 0) norm[gi] = s;
+  }
+}
+
+// Copies the table entries of the groups whose norm may reach L (or that
+// hold a non-finite value) into `sub`; the subset's group count lands in
+// *count.
+template <int W>
+__global__ void k_select_groups(GroupView<W> g, const DevStats* st, const double* norm, double L, GroupView<W> sub,
+                                unsigned int* count) {
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= G) return;
+  const uint32_t n = g.cnt[gi];
+  if (!n) return;
+  const double nrm = sqrt(norm[gi]) * (1.0 + 1e-9);  // summation and rotation rounding
+  if (!(nrm >= L) && !(g.flags[gi] & 1u)) return;
+  const uint32_t j = atomicAdd(count, 1u);
+#pragma unroll
+  for (int k = 0; k < W; ++k) sub.z[k][j] = g.z[k][gi];
+  sub.off[j] = g.off[gi];
+  sub.cnt[j] = n;
+  sub.cap[j] = g.cap[gi];
+  sub.gmax[j] = g.gmax[gi];
+  sub.gmin[j] = g.gmin[gi];
+  sub.flags[j] = g.flags[gi];
+  sub.stamp[j] = g.stamp[gi];
+}
+
+__global__ void k_use_group_count(DevStats* st, const unsigned int* count, unsigned long long bump) {
+  st->G_dev = *count;
+  st->bump = bump;
+  st->work[0] = 0;
 }
 
 // k_branch_x: the segment / stream buffers of the per-gate path

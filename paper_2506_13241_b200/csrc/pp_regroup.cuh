@@ -218,19 +218,38 @@ struct IdentityProducer {
 // (which keeps z) never moves a string between shards; Clifford/ZZ gates do,
 // and whole z-groups are evicted to their new owner after a regroup.
 // ---------------------------------------------------------------------------
+// Load balancing: the z-hash picks one of kBuckets virtual
+// buckets and a bucket table (rebalanced from the global bucket histogram at
+// every exchange, pp_sharded.cuh) maps buckets to ranks; without a table the
+// owner is the hash mod the rank count.
+constexpr uint32_t kBuckets = 4096;
 template <int W>
-__host__ __device__ __forceinline__ uint32_t shard_owner(const Plane<W>& z, uint64_t seed, uint32_t world) {
+__host__ __device__ __forceinline__ uint64_t shard_hash(const Plane<W>& z, uint64_t seed) {
   uint64_t h = mix64(z.w[0] ^ seed);
   if (W == 2) h = mix64(h ^ z.w[W - 1]);
-  return (uint32_t)(h % world);
+  return h;
+}
+template <int W>
+__host__ __device__ __forceinline__ uint32_t shard_owner(const Plane<W>& z, uint64_t seed, uint32_t world,
+                                                         const uint16_t* bucket_rank = nullptr) {
+  const uint64_t h = shard_hash<W>(z, seed);
+  return bucket_rank ? (uint32_t)bucket_rank[h % kBuckets] : (uint32_t)(h % world);
+}
+
+// strings per bucket of this rank's groups (the rebalance's local histogram)
+template <int W>
+__global__ void k_bucket_hist(GroupView<W> g, uint32_t G, uint64_t seed, unsigned long long* hist) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G || g.cnt[i] == 0) return;
+  atomicAdd(&hist[shard_hash<W>(load_plane<W>(g.z, i), seed) % kBuckets], (unsigned long long)g.cnt[i]);
 }
 
 template <int W>
 __global__ void k_evict_count(GroupView<W> g, uint32_t G, uint32_t world, uint32_t rank, uint64_t seed,
-                              unsigned long long* counts) {
+                              unsigned long long* counts, const uint16_t* bucket_rank) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= G || g.cnt[i] == 0) return;
-  uint32_t d = shard_owner<W>(load_plane<W>(g.z, i), seed, world);
+  uint32_t d = shard_owner<W>(load_plane<W>(g.z, i), seed, world, bucket_rank);
   if (d != rank) atomicAdd(&counts[d], (unsigned long long)g.cnt[i]);
 }
 
@@ -239,12 +258,13 @@ __global__ void k_evict_count(GroupView<W> g, uint32_t G, uint32_t world, uint32
 // empties the group
 template <int W>
 __global__ void __launch_bounds__(kCta) k_evict_write(GroupView<W> g, ArenaView<W> ar, uint32_t world, uint32_t rank,
-                                                      uint64_t seed, unsigned long long* cursor, uint64_t* out) {
+                                                      uint64_t seed, unsigned long long* cursor, uint64_t* out,
+                                                      const uint16_t* bucket_rank) {
   const uint32_t gid = blockIdx.x;
   const uint32_t n = g.cnt[gid];
   if (n == 0) return;
   const Plane<W> z = load_plane<W>(g.z, gid);
-  const uint32_t d = shard_owner<W>(z, seed, world);
+  const uint32_t d = shard_owner<W>(z, seed, world, bucket_rank);
   if (d == rank) return;
   __shared__ unsigned long long base_s;
   if (threadIdx.x == 0) base_s = atomicAdd(&cursor[d], (unsigned long long)n);

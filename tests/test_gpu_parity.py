@@ -246,14 +246,15 @@ def test_fusion_matches_unfused(pp, O):
             assert x[k] == y[k], (k, x, y)
 
 
-@pytest.mark.parametrize("mode", ["dense", "per_gate_groups"])
+@pytest.mark.parametrize("mode", ["default", "tight_arena"])
 def test_speculative_sublayer_is_exact(pp, O, monkeypatch, mode):
-    # the fused run for epsilon0 > 0 (predicted thresholds, verified and
-    # rolled back on mismatch; dense groups truncate inside the butterfly
-    # network) must give the per-gate result bit for bit
-    monkeypatch.setenv("PP_SPECULATE", "1")
-    if mode == "per_gate_groups":
-        monkeypatch.setenv("PP_NO_DENSE", "1")
+    # the fused run for epsilon0 > 0 (the default: predicted thresholds,
+    # verified and rolled back on mismatch, intermediate versions in the CTAs'
+    # scratch) must give the per-gate result bit for bit, also when the arena
+    # overflows inside a run (PP_TIGHT_ARENA)
+    monkeypatch.delenv("PP_NO_SPECULATE", raising=False)
+    if mode == "tight_arena":
+        monkeypatch.setenv("PP_TIGHT_ARENA", "1")
     geom = pp.heavy_hex_127()
     for thx, eps in (("0.25pi", 1e-4), (0.3, 1e-5)):
         circ = _kicked(pp, geom, thx, 6)
@@ -266,7 +267,7 @@ def test_deferred_truncation_is_exact(pp, O, monkeypatch, mode):
     epsilon0 > 0) equals the eager per-gate compaction and the oracle: string
     sets, coefficient bits, records and removed counts per layer, also when
     the arena overflows mid-run and the run resumes (PP_TIGHT_ARENA)."""
-    monkeypatch.delenv("PP_SPECULATE", raising=False)  # the per-gate launches
+    monkeypatch.setenv("PP_NO_SPECULATE", "1")  # the per-gate launches
     if mode == "eager":
         monkeypatch.setenv("PP_EAGER_TRUNCATION", "1")
     if mode == "deferred_tight":
@@ -404,3 +405,63 @@ def test_reinitialised_engine_big_group_then_zz(pp, O):
         ow, oc = ora.export()
         assert_same_terms(w, c, ow, oc, f"trial {trial}")
         del eng  # trial 1, 2: the next Engine is the pooled one
+
+
+def test_tracked_coefficient_and_gate_readout(pp, O):
+    """RunOptions readout modes (engine.hpp:203-213): TrackedCoefficient per
+    layer and the per-gate on_gate_readout trace, against the oracle."""
+    geom = pp.heavy_hex_127()
+    circ = _kicked(pp, geom, 0.3, 3)
+    z62 = pp.PauliString("Z62", 127)
+    tracked = pp.PauliString("Z62 X63", 127)
+    eng = pp.Engine(127, 1e-5)
+    eng.set_initial(O.site_word(62, 3)[None], np.array([1.0]))
+    trace = []
+    rows = eng.run_circuit(circ, readout="coefficient", tracked=tracked,
+                           on_gate_readout=lambda t, gi, v: trace.append((t, gi, v)))
+    ora = O.OracleEngine(127, 1e-5)
+    ora.set_initial(O.site_word(62, 3)[None], [1.0])
+    tw = np.asarray(tracked.words, np.uint64)
+    k = 0
+    L = circ.num_layers()
+    for t in range(1, L + 1):
+        for gi, g in enumerate(reversed(circ.layers[L - t])):
+            ora.apply_gate(np.asarray(g.generator.words, np.uint64), g.cos_theta, g.sin_theta)
+            tt, tgi, v = trace[k]
+            assert (tt, tgi) == (t, gi)
+            assert v == ora.coefficient(tw), (t, gi)  # a coefficient is one string's value: bit-exact
+            k += 1
+        assert rows[t - 1]["observable"] == ora.coefficient(tw)
+    assert k == len(trace) == circ.total_gates()
+    # the default readout and a tracked Z62 agree with <0|O|0>'s single-string case at t = 0
+    e2 = pp.Engine(127, 0.0)
+    e2.set_initial(O.site_word(62, 3)[None], np.array([1.0]))
+    assert e2.run_circuit(_kicked(pp, geom, "0.5pi", 1), readout="coefficient", tracked=z62)[0]["term_count"] == 1
+
+
+def test_shards_mirror_the_reference_partition(pp, O):
+    """Engine.shards()/shard_sizes() (engine.hpp:161-162): the operator split
+    by the reference's block-sum owner map, sizes equal to the reference's own
+    shards at the same worker count; PhaseTimers present in the counters."""
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    geom = pp.heavy_hex_127()
+    circ = _kicked(pp, geom, "0.25pi", 4)
+    for workers in (1, 4, 7):
+        eng = pp.Engine(127, 0.0, workers=workers)
+        eng.set_initial(O.site_word(62, 3)[None], np.array([1.0]))
+        eng.run_circuit(circ)
+        ref = O.RefEngine(127, 0.0, workers=workers, threads=workers)
+        ref.set_initial(O.site_word(62, 3)[None], [1.0])
+        gates = [(np.asarray(g.generator.words, np.uint64), 0.25 if i < 127 else -0.5, 1)
+                 for i, g in enumerate(circ.layers[0])]
+        ref.run_circuit(gates, 4)
+        assert eng.shard_sizes() == ref.shard_sizes(), workers
+        shards = eng.shards()
+        assert len(shards) == workers and sum(len(c) for _, c in shards) == eng.term_count()
+        spec = pp.PartitionSpec(workers=workers)  # block_size_bits 0: the default k
+        for m, (w, c) in enumerate(shards):
+            for row in w[:50]:
+                assert pp.owner(spec, pp.PauliString.from_words([int(v) for v in row]), 127) == m
+    t = eng.take_counters()["timers"]
+    assert set(t) == {"generate_ns", "exchange_ns", "apply_ns", "truncate_ns"}

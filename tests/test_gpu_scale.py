@@ -32,11 +32,25 @@ def chain_geometry(pp, n=64):
     return pp.load_geometry("\n".join(f"{i} {i + 1} {i % 2}" for i in range(n - 1)))
 
 
-def circuit_of(pp, case):
-    geom = pp.heavy_hex_127() if case["geometry"] == "heavy_hex_ref" else chain_geometry(pp, case["n"])
-    tx = f"{case['theta_x']!r}pi" if case["theta_x_pi"] else case["theta_x"]
-    tz = f"{case['theta_zz']!r}pi" if case["theta_zz_pi"] else case["theta_zz"]
-    return pp.build_kicked_ising(geom, tx, tz, case["layers"])
+def _angles(case):
+    """(theta_x, theta_zz) as build_kicked_ising takes them; ledgers.json and
+    scale.json spell the keys differently."""
+    tx, txp = case.get("theta_x", case.get("thx")), case.get("theta_x_pi", case.get("thx_pi"))
+    tz, tzp = case.get("theta_zz", case.get("thzz")), case.get("theta_zz_pi", case.get("thzz_pi"))
+    return (f"{tx!r}pi" if txp else tx), (f"{tz!r}pi" if tzp else tz)
+
+
+def _geometry(pp, case):
+    return pp.heavy_hex_127() if case["geometry"] == "heavy_hex_ref" else chain_geometry(pp, case["n"])
+
+
+def circuit_of(pp, case, layers=None):
+    tx, tz = _angles(case)
+    return pp.build_kicked_ising(_geometry(pp, case), tx, tz, layers or case["layers"])
+
+
+def _eps(case):
+    return case.get("epsilon0", case.get("eps"))
 
 
 def init_of(O, case):
@@ -61,16 +75,10 @@ def check_row(got, want, ctx):
 
 
 def run_case(pp, O, case, cadence="gate"):
-    """Layer by layer through Engine.run_circuit semantics; yields (t, row, engine)."""
-    circ = circuit_of(pp, case)
-    eng = pp.Engine(case["n"], case["epsilon0"], cadence)
-    w, c = init_of(O, case)
-    eng.set_initial(w, c)
-    one = pp.build_kicked_ising(
-        pp.heavy_hex_127() if case["geometry"] == "heavy_hex_ref" else chain_geometry(pp, case["n"]),
-        f"{case['theta_x']!r}pi" if case["theta_x_pi"] else case["theta_x"],
-        f"{case['theta_zz']!r}pi" if case["theta_zz_pi"] else case["theta_zz"], 1)
-    assert circ.num_layers() == case["layers"]
+    """Layer by layer through Engine.run_circuit; yields (t, row, engine)."""
+    eng = pp.Engine(case["n"], _eps(case), cadence)
+    eng.set_initial(*init_of(O, case))
+    one = circuit_of(pp, case, layers=1)
     for t in range(1, case["layers"] + 1):
         row = eng.run_circuit(one)[0]
         yield t, row, eng
@@ -94,10 +102,10 @@ def test_ledgers_through_public_api(pp, O, ledgers):
     for case in ledgers["cases"]:
         circ = circuit_of(pp, case)
         if len(case["init"]) == 1:
-            rows = pp.simulate(circ, observable=f"Z{case['init'][0][0]}", epsilon0=case["epsilon0"],
+            rows = pp.simulate(circ, observable=f"Z{case['init'][0][0]}", epsilon0=_eps(case),
                                cadence="layer" if case["cadence"] else "gate")
         else:
-            eng = pp.Engine(case["n"], case["epsilon0"], "layer" if case["cadence"] else "gate")
+            eng = pp.Engine(case["n"], _eps(case), "layer" if case["cadence"] else "gate")
             eng.set_initial(*init_of(O, case))
             rows = eng.run_circuit(circ)
         assert len(rows) == len(case["rows"])
