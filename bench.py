@@ -23,10 +23,10 @@ layer, exactly what the reference's run_circuit does.  Other workloads:
            the workload it runs in seconds (config 0 to t = 9, 81.7 M strings)
 
 ``--impl reference`` times the reference CPU engine on the same workload.
-Under torchrun (N > 1) the operator is sharded over the ranks by z-plane
-hash (paper_2506_13241_b200/sharded.py): Rx runs are rank-local, strings
-move with one NCCL all-to-all after each Clifford run, scalars (global max,
-counts, <0|O|0>) are all-reduced -- total work fixed, strong scaling
+``--gpus N`` relaunches itself under torch.distributed.run; with N > 1 ranks
+the operator is sharded by the native engine (C-ABI pp_sharded_*, NCCL
+inside): Rx runs are rank-local, strings move with one all-to-all after each
+Clifford run, scalars are all-reduced -- total work fixed, strong scaling
 (DESIGN.md section 6).
 """
 from __future__ import annotations
@@ -246,70 +246,88 @@ def run_reference_arm(args, wl, rank, world):
 
 
 def run_sharded(args, pp, circ, wl, sg, final_terms, init, rank, world, local):
-    """N > 1: the operator is sharded over the ranks by z-plane hash
-    (paper_2506_13241_b200/sharded.py); total work fixed -> strong scaling.
-    Device time per step = CUDA events on this rank's engine stream, max over
-    ranks."""
+    """N > 1: the native sharded engine (C-ABI pp_sharded_*: NCCL inside,
+    bucket-balanced z-hash ownership, one all-to-all per string-moving step,
+    per-run reduced speculation for eps0 > 0).  torch.distributed only
+    bootstraps it (broadcast of the NCCL id) and takes the max over ranks of
+    the timings.  Total work fixed -> strong scaling."""
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_2506_13241_b200.sharded import GpuShard, ShardedEngine, TorchComm
 
-    n, eps = wl[1], wl[5]
-    gloo = dist.new_group(backend="gloo")  # scalars (and the host-staged fallback)
-    nccl = os.environ.get("PP_BENCH_PG") != "gloo" and os.environ.get("PP_HOST_EXCHANGE") is None
-    # strings move device-to-device: one NCCL all-to-all per z-changing step over NVLink
-    comm = TorchComm(gloo, data_group=dist.group.WORLD if nccl else None)
+    n, site, eps = wl[1], wl[4], wl[5]
+    gloo = dist.group.WORLD
+    idt = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        idt = torch.tensor(list(pp.nccl_unique_id()), dtype=torch.uint8)
+    dist.broadcast(idt, 0, group=gloo)
+    eng = pp.NativeShardedEngine(n, eps, "gate", world=world, rank=rank, nccl_id=bytes(idt.tolist()), device=local)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=local)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
 
     def one_step():
-        shard = GpuShard(n, eps, "gate", device=local)
-        se = ShardedEngine(shard, n, comm, eps, "gate")
-        stream = torch.cuda.ExternalStream(shard.engine.stream_ptr(), device=local)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        t0 = time.perf_counter()
-        se.set_initial(init, np.array([1.0]))
-        rows = se.run_circuit(circ)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        return rows, e0.elapsed_time(e1), wall, se.exchanged_records
+        eng.set_initial(init, np.array([1.0]))
+        return eng.run_circuit(circ)
 
     for _ in range(args.warmup):
         one_step()
-    ms, walls, moved = [], [], 0
+    eng.kernel_stats()
+    st0 = eng.stats()
+    ms, walls, rows = [], [], None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            rows, m, w, mv = one_step()
-            ms.append(m)
-            walls.append(w)
-            moved += mv
-    assert rows[-1]["term_count"] == final_terms
-    t = torch.tensor([sum(ms), sum(walls)], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
-    ms_per_step = float(t[0]) / args.steps
-    wall_per_step = float(t[1]) / args.steps
-    mv = torch.tensor([float(moved)], dtype=torch.float64)
-    dist.all_reduce(mv, group=gloo)
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier(group=gloo)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            t0 = time.perf_counter()
+            rows = one_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+            ms.append(e0.elapsed_time(e1))
+    ks = eng.kernel_stats()
+    st1 = eng.stats()
+    assert rows[-1]["term_count"] == final_terms, (rows[-1]["term_count"], final_terms)
+    red = torch.tensor([sum(ms), sum(walls), ks["branch_ms"], ks["branch_bytes"],
+                        float(st1["records_moved"] - st0["records_moved"]),
+                        (st1["exchange_ns"] - st0["exchange_ns"]) * 1e-6], dtype=torch.float64)
+    mx = red.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=gloo)
+    tot = red.clone()
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=gloo)
+    ms_per_step = float(mx[0]) / args.steps
+    wall_per_step = float(mx[1]) / args.steps
     if rank == 0:
+        peak, peak_kind = load_peaks()
+        achieved = float(tot[3]) / (float(mx[2]) / 1e3) / 1e9 / world if mx[2] > 0 else 0.0  # per GPU
+        moved_bytes = float(mx[4]) * eng.record_bytes() / args.steps
+        ex_ms = float(mx[5]) / args.steps
         line = {
             "metric": "string_gates_per_s", "value": sg / (ms_per_step / 1e3), "unit": "string-gates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (deterministic kicked-Ising circuit, BASELINE config)",
-            "config": {"workload": args.workload, "string_gates_per_step": sg, "final_terms": final_terms,
-                       "parallelism": f"z-hash shards x{world}",
-                       "exchange": "device all-to-all (NCCL)" if nccl else "host-staged (gloo)",
-                       "records_exchanged_per_step": float(mv[0]) / args.steps},
+            "data": "synthetic (deterministic kicked-Ising circuit, BASELINE config; no dataset)",
+            "config": config_dict(args, wl, world),
             "e2e": {"value": sg / wall_per_step, "unit": "string-gates/s", "h2d_bytes_per_step": 40,
-                    "d2h_bytes_per_step": 8 * 4 * circ.num_layers(), "api": "ShardedEngine.run_circuit"},
-            "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
+                    "d2h_bytes_per_step": 8 * 4 * circ.num_layers(), "api": "NativeShardedEngine.run_circuit",
+                    "bytes": "the initial term in, four ledger scalars per layer out"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "k_branch_sublayer (per GPU, summed bytes / max device time)",
+                         "exchange": {"bound": "nvlink", "bytes_per_step_max_rank": moved_bytes,
+                                      "ms_per_step_max_rank": ex_ms,
+                                      "achieved_GBps": moved_bytes / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None,
+                                      "peak_GBps": 900.0,
+                                      "note": "exchange time includes the rebalance all-reduce and the ingest"}},
+            "cpu_baseline": None,
+            "clocks": clk.summary(),
+            "gpu_launches": int(ks["launches"]),
         }
         print(json.dumps(line), flush=True)
-    dist.barrier()
+    dist.barrier(group=gloo)
     dist.destroy_process_group()
 
 
@@ -350,14 +368,9 @@ def main():
     import numpy as np
     import torch
     import torch.distributed as dist
-    if os.environ.get("PP_BENCH_PG") == "gloo":  # test hook: several ranks sharing one GPU
-        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    if world > 1:
-        if os.environ.get("PP_BENCH_PG") == "gloo":
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1:  # bootstrap and timing reductions only; the data plane is NCCL inside the engine
+        dist.init_process_group("gloo")
 
     import paper_2506_13241_b200 as pp
 

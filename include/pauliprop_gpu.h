@@ -230,6 +230,9 @@ int pp_sharded_stats(pp_sharded* s, pp_shard_stats* out);
 int pp_sharded_local_count(pp_sharded* s, uint64_t* out);
 int pp_sharded_local_export(pp_sharded* s, uint64_t* words, double* coeffs, uint64_t cap, uint64_t* count);
 void* pp_sharded_stream(const pp_sharded* s);
+/* this rank's branch-kernel device time and algorithmic bytes (pp_take_kernel_stats) */
+int pp_sharded_kernel_stats(pp_sharded* s, double* branch_ms, double* branch_bytes, uint64_t* branch_launches,
+                            uint64_t* total_launches);
 const char* pp_sharded_last_error(const pp_sharded* s);
 
 #ifdef __cplusplus

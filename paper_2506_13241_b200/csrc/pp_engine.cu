@@ -197,8 +197,14 @@ class DevicePool {
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
       if (g_release_parked_engines) g_release_parked_engines(dev);
-      trim(dev);
-      e = cudaMalloc(&p, bytes);
+      // free cached blocks, largest first, only until the request fits: the
+      // rest stays for the next engine (simulate() makes one per call)
+      for (;;) {
+        e = cudaMalloc(&p, bytes);
+        if (e != cudaErrorMemoryAllocation) break;
+        cudaGetLastError();
+        if (!trim_largest(dev)) break;
+      }
     }
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -236,6 +242,15 @@ class DevicePool {
     std::lock_guard<std::mutex> lk(mu_);
     for (auto& [b, p] : free_[dev]) cudaFree(p);
     free_[dev].clear();
+  }
+  bool trim_largest(int dev) {  // frees the largest cached block; false when none is left
+    std::lock_guard<std::mutex> lk(mu_);
+    auto& fl = free_[dev];
+    if (fl.empty()) return false;
+    auto it = std::prev(fl.end());
+    cudaFree(it->second);
+    fl.erase(it);
+    return true;
   }
 
  private:
@@ -344,7 +359,7 @@ static void release_stream_set(int dev, const StreamSet& s) {
 // launch configuration of one (device, W): attributes set once, grids from
 // the occupancy calculator
 struct LaunchSetup {
-  uint32_t zz_grid = 0, branch_grid = 0, sub_grid = 0;
+  uint32_t zz_grid = 0, branch_grid = 0, sub_grid = 0, small_grid = 0;
 };
 static std::mutex g_setup_mu;
 static std::map<std::pair<int, int>, LaunchSetup> g_setup;
@@ -427,6 +442,8 @@ class EngineImpl final : public EngineBase {
                                      (int)sizeof(SortSmem<W>)));
         PP_CUDA(cudaFuncSetAttribute(k_sort_big<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)big_sort_smem()));
+        PP_CUDA(cudaFuncSetAttribute(k_spec_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)spec_small_smem_bytes<W>()));
         PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         PP_CUDA(cudaFuncSetAttribute(k_branch_zz<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -441,6 +458,10 @@ class EngineImpl final : public EngineBase {
         ls.zz_grid = (uint32_t)(sms * std::max(occ, 1));
         ls.branch_grid = (uint32_t)(sms * std::max(occ_x, 1));
         ls.sub_grid = (uint32_t)(sms * std::max(occ_s, 1));
+        int occ_k = 1;
+        PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_k, k_spec_small<W>, kSmallWarps * 32,
+                                                              spec_small_smem_bytes<W>()));
+        ls.small_grid = (uint32_t)(sms * std::max(occ_k, 1));
         if (std::getenv("PP_DEBUG"))
           std::fprintf(stderr, "[pp] W=%d branch CTAs/SM %d, sublayer CTAs/SM %d, smem %zu\n", W, occ_x, occ_s,
                        branch_smem_bytes<W>());
@@ -448,6 +469,7 @@ class EngineImpl final : public EngineBase {
       zz_grid_ = ls.zz_grid;
       branch_grid_ = ls.branch_grid;
       sub_grid_ = ls.sub_grid;
+      small_grid_ = ls.small_grid;
     }
     keep_zeros_ = cfg.cadence == PP_CADENCE_LAYER;
     seed_ = 0x5eed5eed12345678ull;
@@ -488,7 +510,7 @@ class EngineImpl final : public EngineBase {
     for (auto& g : groups_) f(g.buf);
     for (DevBuf* b : {&evict_cnt_, &evict_buf_, &spec_buf_, &backup_, &stats_buf_, &list_, &items_, &rec_slot_,
                       &table_, &scan_tmp_, &scan_gid_, &scan_off_, &diag_z_, &diag_c_, &cliff_, &thr_, &ztab_,
-                      &norms_, &sub_groups_, &buckets_})
+                      &norms_, &sub_groups_, &buckets_, &spec_done_})
       f(*b);
   }
   size_t device_bytes() const override {
@@ -801,6 +823,9 @@ class EngineImpl final : public EngineBase {
       }
       rx_sg_ = SubGates{};
       rx_distinct_ = true;
+      rx_sg_.fast = std::getenv("PP_DENSE_CAREFUL") == nullptr ? 1 : 0;  // (test hook: always point by point)
+      for (size_t i = 0; i < count; ++i)
+        if (!(std::fabs(gates[i].sin_theta) >= 0x1p-100) || !(std::fabs(gates[i].cos_theta) >= 0x1p-100)) rx_sg_.fast = 0;
       if (count <= (size_t)kMaxSubGates) {
         rx_sg_.ng = (int)count;
         for (size_t i = 0; i < count; ++i) {
@@ -940,6 +965,7 @@ class EngineImpl final : public EngineBase {
     unsigned long long* d_gmax = reinterpret_cast<unsigned long long*>(d_tpred + count);
     if (std::getenv("PP_NO_DISCOVERY") == nullptr) discover_thresholds(sgates, seq0, tpred);
     int faults = 0;
+    uint64_t need = 0;  // arena demand a faulted attempt reported (its bump overshoot)
     for (int attempt = 0; attempt < 8; ++attempt) {
       bool give_up = false;
       sync_state();
@@ -947,7 +973,7 @@ class EngineImpl final : public EngineBase {
       // the rollback point): reserve ~24 |O| when memory allows
       // (groups keep their intermediate versions in the CTAs' L2 scratch;
       // the arena takes the results and large groups' per-gate versions)
-      const uint64_t want = (faults ? 8 : 3) * live_ + (1u << 16);
+      const uint64_t want = std::max<uint64_t>((faults ? 8 : 3) * live_ + (1u << 16), need);
       if (bump_ + want > arena_[cur_].cap) {
         size_t free_b = 0, total_b = 0;
         PP_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -974,11 +1000,19 @@ class EngineImpl final : public EngineBase {
       PP_CUDA(copy_async(d_tpred, tpred.data(), count * 8, cudaMemcpyHostToDevice, stream_));
       PP_CUDA(cudaMemsetAsync(d_gmax, 0, count * 8, stream_));
       push_scalars(seq0);
+      const uint64_t bump_before = bump_;
       std::pair<cudaEvent_t, cudaEvent_t> ev = take_event_pair();
       PP_CUDA(cudaEventRecord(ev.first, stream_));
       count_param_h2d(sizeof(sgates));
+      // small groups a warp each, the rest (and any that outgrew a warp) a CTA each
+      spec_done_.ensure(std::max<uint32_t>(G_, 1));
+      PP_CUDA(cudaMemsetAsync(spec_done_.p, 0, std::max<uint32_t>(G_, 1), stream_));
+      k_spec_small<W><<<small_grid_, kSmallWarps * 32, spec_small_smem_bytes<W>(), stream_>>>(
+          gview(gcur_), aview(cur_), sgates, &d_stats_->work[1], d_tpred, d_gmax, d_stats_, spec_done_.as<uint8_t>());
       k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
-          gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_tpred, d_gmax, d_stats_);
+          gview(gcur_), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_tpred, d_gmax, d_stats_,
+          spec_done_.as<uint8_t>());
+      ++launches_;
       PP_CUDA(cudaEventRecord(ev.second, stream_));
       pending_events_.push_back(ev);
       ++launches_;
@@ -1034,12 +1068,20 @@ class EngineImpl final : public EngineBase {
                        (unsigned long long)gm[first], gmax_);
       }
       if (any_fault) {
+        // the kernels keep bumping past the capacity: what they asked for,
+        // plus the live strings, sizes the next attempt
+        need = std::max<uint64_t>(need, (bump_ > bump_before ? bump_ - bump_before : 0) + live_ / 2 + (1u << 16));
+        if (spec_reduce_) {  // every rank sizes for the largest demand
+          std::vector<unsigned long long> v{need};
+          spec_reduce_(v);
+          need = v[0];
+        }
         if (arena_fault_) {
           k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
           ++launches_;
           arena_fault_ = false;
         }
-        if (++faults >= 2) {  // cannot hold a whole speculative run: gates one by one
+        if (++faults >= 4) {  // cannot hold a whole speculative run: gates one by one
           dirty_ = true;
           sync_state();
           gc_into_other(next_arena_target());
@@ -1095,9 +1137,14 @@ class EngineImpl final : public EngineBase {
         launches_ += 2;
         PP_CUDA(copy_async(d_tp, tp.data(), count * 8, cudaMemcpyHostToDevice, stream_));
         PP_CUDA(cudaMemsetAsync(d_gm, 0, count * 8, stream_));
+        spec_done_.ensure(std::max<uint32_t>(G_, 1));
+        PP_CUDA(cudaMemsetAsync(spec_done_.p, 0, std::max<uint32_t>(G_, 1), stream_));
+        k_spec_small<W><<<small_grid_, kSmallWarps * 32, spec_small_smem_bytes<W>(), stream_>>>(
+            sub_view(), aview(cur_), sgates, &d_stats_->work[1], d_tp, d_gm, d_stats_, spec_done_.as<uint8_t>());
         k_branch_sublayer<W><<<sub_grid_, kCta, branch_smem_bytes<W>(), stream_>>>(
-            sub_view(), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_tp, d_gm, d_stats_);
-        launches_ += 2;
+            sub_view(), aview(cur_), sgates, keep_zeros_, &d_stats_->work[0], d_tp, d_gm, d_stats_,
+            spec_done_.as<uint8_t>());
+        launches_ += 3;
         PP_CUDA(copy_async(gm.data(), d_gm, count * 8, cudaMemcpyDeviceToHost, stream_));
         fetch_stats();
         PP_CUDA(cudaGetLastError());
@@ -1733,8 +1780,8 @@ class EngineImpl final : public EngineBase {
     arena_[i].cap = cap;
     arena_[i].stride = cap + tail;
   }
-  bool spec_capable() const {
-    return cfg_.epsilon0 > 0.0 && cfg_.cadence == PP_CADENCE_GATE && !external() && cfg_.max_terms == 0;
+  bool spec_capable() const {  // (external engines too: a sharded driver runs them coordinated)
+    return cfg_.epsilon0 > 0.0 && cfg_.cadence == PP_CADENCE_GATE && cfg_.max_terms == 0;
   }
   void ensure_groups(int i, uint32_t cap) {
     if (groups_[i].cap >= cap) return;
@@ -2480,6 +2527,7 @@ class EngineImpl final : public EngineBase {
   std::vector<GraphExecPtr> held_graphs_;  // graphs launched since the last stream sync
   DevBuf norms_, sub_groups_;  // threshold discovery: group norms, the subset's table
   DevBuf buckets_;             // sharded: bucket -> rank table (kBuckets uint16)
+  DevBuf spec_done_;           // per group: finished by k_spec_small in this attempt
   bool buckets_on_ = false;
  public:
   // Sharded runs (pp_sharded_*): every rank's observations of a speculative
@@ -2580,6 +2628,7 @@ class EngineImpl final : public EngineBase {
 
   uint32_t branch_grid_ = 148u * 2u;
   uint32_t sub_grid_ = 148u * 2u;
+  uint32_t small_grid_ = 148u * 3u;
   uint32_t zz_grid_ = 148u * 2u;
   uint32_t maxcnt_ = 0x7fffffffu;  // largest group at the last full sync (bounds Z-type pair sizes)
   DevBuf ztab_;
@@ -3065,4 +3114,9 @@ int pp_sharded_local_export(pp_sharded* s, uint64_t* words, double* coeffs, uint
   return guarded_s(s, [&] { *count = s->d->engine().export_terms(words, coeffs, cap); });
 }
 void* pp_sharded_stream(const pp_sharded* s) { return s ? s->d->engine().stream() : nullptr; }
+int pp_sharded_kernel_stats(pp_sharded* s, double* branch_ms, double* branch_bytes, uint64_t* branch_launches,
+                            uint64_t* total_launches) {
+  if (!s || !branch_ms || !branch_bytes || !branch_launches || !total_launches) return PP_ERR_INVALID;
+  return guarded_s(s, [&] { s->d->engine().take_kernel_stats(branch_ms, branch_bytes, branch_launches, total_launches); });
+}
 const char* pp_sharded_last_error(const pp_sharded* s) { return s ? s->error.c_str() : g_create_error.c_str(); }

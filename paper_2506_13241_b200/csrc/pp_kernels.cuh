@@ -1190,10 +1190,11 @@ constexpr int kMaxSubGates = 128;
 // Speculative (eps0 > 0) runs: each CTA of k_branch_sublayer ping-pongs a
 // group's intermediate versions through two halves of its own scratch
 // region in the arena tail ([cap + 2 kSpecScratch blockIdx, ...)), reused
-// gate after gate so they stay in L2; only the run's final strings are
-// written to fresh arena space.  Groups whose working set outgrows a half
-// take fresh arena space per gate.
-constexpr uint32_t kSpecScratch = 4096;
+// gate after gate and group after group (a small group's versions stay in
+// L2); only the run's final strings are written to fresh arena space.  A
+// working set beyond a half takes a pair of arena regions grown by doubling.
+constexpr uint32_t kSpecScratch = 32768;
+
 struct SubGates {
   int ng;
   int8_t wq[kMaxSubGates];
@@ -1204,6 +1205,7 @@ struct SubGates {
   int dense;        // dense path allowed: distinct qubits, zeros dropped (k_branch_sublayer)
   int sorted;       // every group is sorted by x (no kFlagUnsorted group in the table)
   int maxk;         // x classes allowed per group on the dense path (<= kDenseMaxK; test hook)
+  int fast;         // every |sin|, |cos| >= 2^-100: the dense butterflies may skip the per-point bookkeeping
 };
 
 // copy group region [src, src+n) to dst keeping |c| > T (truncation into
@@ -1365,6 +1367,7 @@ struct DenseCtl {
   double strunc[kMaxSubGates];  // threshold of the window after stage s (its gate .. the next stage's)
   unsigned long long wmax[2][kWarps];  // per-warp stage max, by stage parity
   uint32_t zeros;               // multi-class: zero points written (holes to compact)
+  uint32_t fast;                // this group's butterflies take dense_bfly_fast (see there)
 };
 
 template <int W>
@@ -1413,6 +1416,35 @@ __device__ __forceinline__ void dense_bfly(double& a, double& b, double cosv, do
   b = v1;
 }
 
+// The same butterfly without the per-point branches.  Always adding the
+// delta equals dense_bfly's "add only if nonzero" whenever no delta
+// underflows to zero (it is zero exactly when its source point is), and the
+// record count is then the number of nonzero sources.  That holds while every
+// |sin| >= 2^-100 (SubGates::fast) and every nonzero value has |v| >= 2^-899
+// and is finite; an output of a live pair outside that range (an exact
+// cancellation to zero included) raises `anom`, and the caller redoes the
+// block with dense_bfly.  Nothing is removed on this path (no zeros appear).
+__device__ __forceinline__ void dense_bfly_fast(double& a, double& b, double cosv, double sinv, double nsin,
+                                                unsigned long long& records, uint32_t& anom) {
+  const double d1 = __dmul_rn(sinv, a), d0 = __dmul_rn(nsin, b);
+  const double v0 = __dadd_rn(__dmul_rn(a, cosv), d0), v1 = __dadd_rn(__dmul_rn(b, cosv), d1);
+  const unsigned long long ab = (unsigned long long)__double_as_longlong(a) << 1;
+  const unsigned long long bb = (unsigned long long)__double_as_longlong(b) << 1;
+  const uint32_t na = ab != 0ull, nb = bb != 0ull;
+  records += na + nb;
+  const uint32_t e0 = (uint32_t)((unsigned long long)__double_as_longlong(v0) >> 52) & 0x7ffu;
+  const uint32_t e1 = (uint32_t)((unsigned long long)__double_as_longlong(v1) >> 52) & 0x7ffu;
+  anom |= (na | nb) & ((uint32_t)(e0 - 124u > 0x7feu - 124u) | (uint32_t)(e1 - 124u > 0x7feu - 124u));
+  a = v0;
+  b = v1;
+}
+template <bool FAST>
+__device__ __forceinline__ void dense_bfly_t(double& a, double& b, double cosv, double sinv, double nsin,
+                                             unsigned long long& records, unsigned long long& removed, uint32_t& anom) {
+  if (FAST) dense_bfly_fast(a, b, cosv, sinv, nsin, records, anom);
+  else dense_bfly(a, b, cosv, sinv, nsin, records, removed);
+}
+
 // butterflies of stages [j0, j1) over a tile of 2^u doubles in shared memory;
 // P: the b bits of the tile (stage bit p is tile bit popc(P & (2^p - 1)))
 // max |c| of a group after gate k's apply was M: gate k and the following
@@ -1430,10 +1462,10 @@ __device__ __forceinline__ void dense_contribute(const DenseCtl<W>& dc, int k, i
   }
 }
 
-template <int W, bool SPEC>
+template <int W, bool SPEC, bool FAST = false>
 __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P, int j0, int j1, DenseCtl<W>& dc,
                                                unsigned long long& records, unsigned long long& removed,
-                                               uint32_t count) {
+                                               uint32_t count, uint32_t& anom) {
   // count: points in the tile (a multiple of 2^(p+1) for every stage), default 2^u
   const uint32_t half = (count ? count : (1u << u)) >> 1;
   constexpr bool spec = SPEC;
@@ -1476,7 +1508,7 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int e = 0; e < 16; ++e)
-            if (!((e >> i) & 1)) dense_bfly(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed);
+            if (!((e >> i) & 1)) dense_bfly_t<FAST>(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed, anom);
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           d[b | ((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
@@ -1500,10 +1532,10 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
         uint32_t b = ((t >> plo) << (plo + 1)) | (t & ((1u << plo) - 1u));
         b = ((b >> phi) << (phi + 1)) | (b & ((1u << phi) - 1u));
         double a00 = d[b], a10 = d[b | m1], a01 = d[b | m2], a11 = d[b | m1 | m2];
-        dense_bfly(a00, a10, c1, s1, -s1, records, removed);
-        dense_bfly(a01, a11, c1, s1, -s1, records, removed);
-        dense_bfly(a00, a01, c2, s2, -s2, records, removed);
-        dense_bfly(a10, a11, c2, s2, -s2, records, removed);
+        dense_bfly_t<FAST>(a00, a10, c1, s1, -s1, records, removed, anom);
+        dense_bfly_t<FAST>(a01, a11, c1, s1, -s1, records, removed, anom);
+        dense_bfly_t<FAST>(a00, a01, c2, s2, -s2, records, removed, anom);
+        dense_bfly_t<FAST>(a10, a11, c2, s2, -s2, records, removed, anom);
         d[b] = a00;
         d[b | m1] = a10;
         d[b | m2] = a01;
@@ -1533,7 +1565,7 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
           ++removed;
         }
       }
-      dense_bfly(a, b, cosv, sinv, nsin, records, removed);
+      dense_bfly_t<FAST && !SPEC>(a, b, cosv, sinv, nsin, records, removed, anom);
       if (spec) mx = fmax(mx, fmax(fabs(a), fabs(b)));
       d[b0] = a;
       d[b0 | (1u << p)] = b;
@@ -1554,9 +1586,10 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
 template <int W>
 __device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, int j0, int j1, DenseCtl<W>& dc,
                                              unsigned long long& records, unsigned long long& removed,
-                                             uint32_t count = 0) {
-  if (dc.tpred) dense_stages_t<W, true>(d, u, P, j0, j1, dc, records, removed, count);
-  else dense_stages_t<W, false>(d, u, P, j0, j1, dc, records, removed, count);
+                                             uint32_t count, uint32_t& anom, bool fast) {
+  if (dc.tpred) dense_stages_t<W, true>(d, u, P, j0, j1, dc, records, removed, count, anom);
+  else if (fast) dense_stages_t<W, false, true>(d, u, P, j0, j1, dc, records, removed, count, anom);
+  else dense_stages_t<W, false>(d, u, P, j0, j1, dc, records, removed, count, anom);
 }
 
 // Stages of a block of S > kDenseSmem points in global memory (L2): passes
@@ -1564,7 +1597,7 @@ __device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, 
 // cosets of the pass's stage bits, padded with low bits).
 template <int W>
 __device__ void dense_passes(double* dbuf, double* blk, uint32_t S, DenseCtl<W>& dc, unsigned long long& records,
-                             unsigned long long& removed) {
+                             unsigned long long& removed, uint32_t& anom, bool fast) {
   const uint32_t tid = threadIdx.x;
   const int m = dc.m;
   for (int j0 = 0; j0 < m; j0 += (int)kDenseSmemLog) {
@@ -1601,7 +1634,7 @@ __device__ void dense_passes(double* dbuf, double* blk, uint32_t S, DenseCtl<W>&
         for (uint32_t e = 0; e < 8; ++e) dbuf[i0 + e * kCta + tid] = t[e];
       }
       __syncthreads();
-      dense_stages<W>(dbuf, u, P, j0, j1, dc, records, removed);
+      dense_stages<W>(dbuf, u, P, j0, j1, dc, records, removed, 0, anom, fast);
       for (uint32_t i = tid; i < (1u << u); i += kCta) blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]] = dbuf[i];
       __syncthreads();
     }
@@ -1652,7 +1685,8 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   // region: K 2^m output slots, plus a 2^m scratch block for blocks larger
   // than a shared-memory tile
   const bool big = S > kDenseSmem;
-  const unsigned long long need = KS + (big ? S : 0);
+  // outputs, the big-block scratch, and the strings' (class, point) codes
+  const unsigned long long need = KS + (big ? S : 0) + n;
   if (tid == 0) {
     const unsigned long long d = atomicAdd(&st->bump, need);
     dc.dst = d;
@@ -1706,48 +1740,71 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       vmin = fmin(vmin, av);
     }
   };
+  // each string's (class, point) once: packed into the output region's x
+  // plane, which the emits overwrite only after the last batch has read it
+  // (rank(i, b) >= the string's position cannot be guaranteed, so the codes
+  // live past the output: [dst + KS, dst + KS + n) of the x plane -- the
+  // region reserves them)
+  uint64_t* codes = ar.x[0] + dst + KS;
+  for (uint32_t i = tid; i < n; i += kCta) {
+    const Plane<W> x = load_plane<W>(ar.x, src + i);
+    codes[i] = ((uint64_t)class_of(x) << 32) | dense_pext<W>(x, T);
+  }
+  __syncthreads();
   if (!big) {
     // batches of whole class blocks in one shared-memory tile
     const uint32_t per = kDenseSmem / S;
     for (uint32_t c0 = 0; c0 < K; c0 += per) {
       const uint32_t c1 = min(K, c0 + per), cnt = (c1 - c0) * S;
-      for (uint32_t e = tid; e < cnt; e += kCta) dbuf[e] = 0.0;
-      __syncthreads();
-      for (uint32_t i = tid; i < n; i += kCta) {
-        const Plane<W> x = load_plane<W>(ar.x, src + i);
-        const uint32_t c = class_of(x);
-        if (c >= c0 && c < c1) {
-          const double v = ar.c[src + i];
-          if (spec && v != 0.0 && fabs(v) <= dc.tin) {
-            ++removed;
-            continue;
+      const unsigned long long rec0 = records;
+      for (bool fast = dc.fast != 0;; fast = false) {
+        for (uint32_t e = tid; e < cnt; e += kCta) dbuf[e] = 0.0;
+        __syncthreads();
+        for (uint32_t i = tid; i < n; i += kCta) {
+          const uint64_t code = codes[i];
+          const uint32_t c = (uint32_t)(code >> 32);
+          if (c >= c0 && c < c1) {
+            const double v = ar.c[src + i];
+            if (spec && v != 0.0 && fabs(v) <= dc.tin) {
+              ++removed;
+              continue;
+            }
+            dbuf[(c - c0) * S + (uint32_t)code] = v;
           }
-          dbuf[(c - c0) * S + dense_pext<W>(x, T)] = v;
         }
+        __syncthreads();
+        uint32_t anom = 0;
+        dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed, cnt, anom, fast);
+        if (!fast || !__syncthreads_or(anom)) break;
+        records = rec0;  // a cancellation or an extreme value: redo the batch point by point
       }
-      __syncthreads();
-      dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed, cnt);
       for (uint32_t e = tid; e < cnt; e += kCta) emit(c0 + e / S, e % S, dbuf[e]);
       __syncthreads();
     }
   } else {
     double* blk = ar.c + dst + KS;  // scratch block (coefficient plane past the output)
     for (uint32_t ci = 0; ci < K; ++ci) {
-      for (uint32_t e = tid; e < S; e += kCta) blk[e] = 0.0;
-      __syncthreads();
-      for (uint32_t i = tid; i < n; i += kCta) {
-        const Plane<W> x = load_plane<W>(ar.x, src + i);
-        if (class_of(x) == ci) {
-          const double v = ar.c[src + i];
-          if (spec && v != 0.0 && fabs(v) <= dc.tin) {
-            ++removed;
-            continue;
+      const unsigned long long rec0 = records;
+      for (bool fast = dc.fast != 0;; fast = false) {
+        for (uint32_t e = tid; e < S; e += kCta) blk[e] = 0.0;
+        __syncthreads();
+        for (uint32_t i = tid; i < n; i += kCta) {
+          const uint64_t code = codes[i];
+          if ((uint32_t)(code >> 32) == ci) {
+            const double v = ar.c[src + i];
+            if (spec && v != 0.0 && fabs(v) <= dc.tin) {
+              ++removed;
+              continue;
+            }
+            blk[(uint32_t)code] = v;
           }
-          blk[dense_pext<W>(x, T)] = v;
         }
+        __syncthreads();
+        uint32_t anom = 0;
+        dense_passes<W>(dbuf, blk, S, dc, records, removed, anom, fast);
+        if (!fast || !__syncthreads_or(anom)) break;
+        records = rec0;
       }
-      __syncthreads();
-      dense_passes<W>(dbuf, blk, S, dc, records, removed);
       for (uint32_t e = tid; e < S; e += kCta) emit(ci, e, blk[e]);
       __syncthreads();
     }
@@ -1871,6 +1928,9 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   __syncthreads();
   const int m = dc.m;
   if (m == 0 || m > kDenseMaxLog) return 0;
+  // bookkeeping-free butterflies (dense_bfly_fast) when the run's angles and
+  // the group's values are far from underflow; anything else is caught there
+  if (tid == 0) dc.fast = (!dc.tpred && gates.fast && g.gmin[gid] >= 0x1p-899) ? 1u : 0u;
   const Plane<W> T = dc.T;
   const bool spec = dc.tpred != nullptr;
   if (spec) {
@@ -2086,21 +2146,27 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   if (!done) {
     const bool in_smem = S <= kDenseSmem;
     double* blk = in_smem ? dbuf : ar.c + dst;  // the dense block
-    for (uint32_t i = tid; i < S; i += kCta) blk[i] = 0.0;
-    __syncthreads();
-    for (uint32_t i = tid; i < n; i += kCta) {
-      const double c = ar.c[src + i];
-      if (spec && c != 0.0 && fabs(c) <= dc.tin) {  // truncated before the first stage
-        ++removed;
-        continue;
+    const unsigned long long rec0 = records;
+    for (bool fast = dc.fast != 0;; fast = false) {
+      for (uint32_t i = tid; i < S; i += kCta) blk[i] = 0.0;
+      __syncthreads();
+      for (uint32_t i = tid; i < n; i += kCta) {
+        const double c = ar.c[src + i];
+        if (spec && c != 0.0 && fabs(c) <= dc.tin) {  // truncated before the first stage
+          ++removed;
+          continue;
+        }
+        blk[dense_pext<W>(load_plane<W>(ar.x, src + i), T)] = c;
       }
-      blk[dense_pext<W>(load_plane<W>(ar.x, src + i), T)] = c;
-    }
-    __syncthreads();
-    if (in_smem) {
-      dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed);
-    } else {
-      dense_passes<W>(dbuf, blk, S, dc, records, removed);
+      __syncthreads();
+      uint32_t anom = 0;
+      if (in_smem) {
+        dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed, 0, anom, fast);
+      } else {
+        dense_passes<W>(dbuf, blk, S, dc, records, removed, anom, fast);
+      }
+      if (!fast || !__syncthreads_or(anom)) break;
+      records = rec0;  // a cancellation or an extreme value: redo point by point
     }
     // nonzero points in b (= x) order, compacted into the output region (in
     // place for a block in global memory: a tile's writes land at or below its
@@ -2190,7 +2256,8 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
 template <int W>
 __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
                                                            int keep_zeros, unsigned int* work, const double* tpred,
-                                                           unsigned long long* gmax_out, DevStats* st) {
+                                                           unsigned long long* gmax_out, DevStats* st,
+                                                           const uint8_t* spec_done = nullptr) {
   __shared__ uint32_t s_touch[kMaxSubGates / 32];
   __shared__ uint32_t s_seen[kMaxSubGates / 32];  // gates of the run that sent a record (batches_sent)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2237,11 +2304,16 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
   };
   const uint64_t scr0 = cap + 2ull * kSpecScratch * blockIdx.x;  // this CTA's scratch halves (spec mode)
   auto in_scratch = [&](uint64_t a) { return a >= scr0 && a < scr0 + 2ull * kSpecScratch; };
-  // destination for n strings derived from src: the other scratch half when
-  // they fit, else fresh arena space
+  // ping-pong of a group's versions through the run: the CTA's scratch halves
+  // when n strings fit one, else a pair of arena regions grown by doubling
+  // (pair_a, pair_cap: per group), so a large group costs O(its peak) of
+  // arena space, not a fresh region per gate
+  uint64_t pair_a = ~0ull;
+  uint32_t pair_cap = 0;
   auto scratch_dst = [&](uint64_t from, uint32_t n) -> uint64_t {
-    if (n > kSpecScratch) return ~0ull;
-    return (in_scratch(from) && from == scr0) ? scr0 + kSpecScratch : scr0;
+    if (n <= kSpecScratch) return (in_scratch(from) && from == scr0) ? scr0 + kSpecScratch : scr0;
+    if (n <= pair_cap) return from == pair_a ? pair_a + pair_cap : pair_a;
+    return ~0ull;  // the caller grows the pair
   };
   auto alloc = [&](uint32_t n, int k) -> bool {
     __syncthreads();
@@ -2271,6 +2343,7 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
     for (int k = 0; k < W; ++k) z.w[k] = g.z[k][gid];
     uint32_t n = g.cnt[gid];
     if (n == 0) continue;
+    if (spec && spec_done && spec_done[gid]) continue;  // run by k_spec_small
     if (!spec) {
       bool touched = false;
       uint32_t mt = 0;
@@ -2293,6 +2366,8 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
     uint32_t curnf = g.flags[gid];
     bool changed = false;
     int k0 = 0;
+    pair_a = ~0ull;
+    pair_cap = 0;
     if (!spec) {
       const uint32_t stamp = g.stamp[gid];
       k0 = (stamp - seq0 < (uint32_t)gates.ng) ? (int)(stamp - seq0) + 1 : 0;  // resume after the stamp
@@ -2362,6 +2437,10 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
             }
             tdst = dst_s;
           }
+          if (pair_cap && tdst != pair_a && tdst != pair_a + pair_cap && !in_scratch(tdst)) {
+            pair_a = ~0ull;  // the versions left the pair (final copy)
+            pair_cap = 0;
+          }
           double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
           const uint32_t w = copy_truncated<W>(ar, src, n, tdst, tp, tscan, mx, mn);
           mx = warp_max(mx);
@@ -2385,11 +2464,17 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
       const uint64_t mq = gates.mq[k];
       uint64_t dst = spec ? scratch_dst(src, 2 * n) : ~0ull;
       if (dst == ~0ull) {
-        if (!alloc(2 * n, k)) {
+        // (spec: a new pair, twice the need or the old pair, whichever is larger)
+        const uint32_t want = spec ? max(2 * n, 2 * pair_cap) : 2 * n;
+        if (!alloc(spec ? 2 * want : want, k)) {
           failed = true;
           break;
         }
         dst = dst_s;
+        if (spec) {
+          pair_a = dst;
+          pair_cap = want;
+        }
       }
       aff_elems += n;
       uint32_t out_n = 0;
@@ -2539,7 +2624,367 @@ __global__ void k_select_groups(GroupView<W> g, const DevStats* st, const double
 __global__ void k_use_group_count(DevStats* st, const unsigned int* count, unsigned long long bump) {
   st->G_dev = *count;
   st->bump = bump;
-  st->work[0] = 0;
+  st->work[0] = st->work[1] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// k_spec_small: the speculative run (eps0 > 0, per-gate cadence) for small
+// z-groups, one WARP per group, the group's strings held in that warp's
+// shared memory from the first gate of the run to the last.  Per touching
+// gate X_q the strings are hashed by x; a string x pairs with x ^ e_q when
+// both are present (one butterfly, the reference's per-key arithmetic:
+// v = c cos [+ (+-sin) c_partner], engine.cpp:218-227 + TermMap::add), a
+// lone string keeps c cos and appends its child (x ^ e_q, +-sin c); then
+// every string with |c| <= T_k goes (truncate_now, engine.cpp:318-351).
+// Gates that do not touch the group apply their truncations when the next
+// touching gate (or the end) comes, and the group's max feeds their gmax
+// until a threshold empties it -- k_branch_sublayer's spec semantics exactly.
+// Only the final strings are written (sorted by x, fresh arena space): no
+// intermediate version leaves the SM.  A group that outgrows the warp's
+// buffer is left untouched for k_branch_sublayer; finished groups are
+// flagged in spec_done (cleared per attempt) so k_branch_sublayer skips them.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kSmallCap = 512;       // strings per warp buffer
+constexpr uint32_t kSmallWarps = 4;       // warps (groups in flight) per CTA
+constexpr uint32_t kSmallMaxIn = 256;     // groups of at most this many strings start here
+
+template <int W>
+constexpr size_t spec_small_smem_bytes() {
+  return (size_t)kSmallWarps * kSmallCap * (8 * W + 8 + 2 * 4);  // x planes, c, hash (2 slots per string)
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t small_hash(const uint64_t* xs, uint32_t i) {
+  uint64_t h = xs[i] * 0x9E3779B97F4A7C15ull;
+  if (W == 2) h ^= xs[kSmallCap + i] * 0xC2B2AE3D27D4EB4Full;
+  return (uint32_t)(h >> 40) & (2 * kSmallCap - 1);
+}
+template <int W>
+__device__ __forceinline__ uint32_t small_hash_key(const Plane<W>& x) {
+  uint64_t h = x.w[0] * 0x9E3779B97F4A7C15ull;
+  if (W == 2) h ^= x.w[1] * 0xC2B2AE3D27D4EB4Full;
+  return (uint32_t)(h >> 40) & (2 * kSmallCap - 1);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kSmallWarps * 32) k_spec_small(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
+                                                                 unsigned int* work, const double* __restrict__ tpred,
+                                                                 unsigned long long* gmax_out, DevStats* st,
+                                                                 uint8_t* spec_done) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t* xs = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * W * kSmallCap;  // [W][kSmallCap]
+  double* cs = reinterpret_cast<double*>(reinterpret_cast<uint64_t*>(smem_raw) + (size_t)kSmallWarps * W * kSmallCap) +
+               (size_t)warp * kSmallCap;
+  uint32_t* ht = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(reinterpret_cast<uint64_t*>(smem_raw) +
+                                                                       (size_t)kSmallWarps * W * kSmallCap) +
+                                             (size_t)kSmallWarps * kSmallCap) +
+                 (size_t)warp * 2 * kSmallCap;
+  __shared__ unsigned long long smax[kMaxSubGates];
+  __shared__ double s_tp[kMaxSubGates], s_cos[kMaxSubGates], s_sin[kMaxSubGates];
+  __shared__ uint64_t s_mq[kMaxSubGates];
+  __shared__ int8_t s_wq[kMaxSubGates];
+  __shared__ uint32_t s_seen[kMaxSubGates / 32];
+  const int ng = gates.ng;
+  for (int k = threadIdx.x; k < ng; k += blockDim.x) {
+    smax[k] = 0ull;
+    s_tp[k] = tpred[k];
+    s_cos[k] = gates.cosv[k];
+    s_sin[k] = gates.sinv[k];
+    s_mq[k] = gates.mq[k];
+    s_wq[k] = gates.wq[k];
+  }
+  if (threadIdx.x < kMaxSubGates / 32) s_seen[threadIdx.x] = 0;
+  __syncthreads();
+  if (engine_failed(st)) return;
+  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  const unsigned long long cap = *(volatile const unsigned long long*)&st->arena_cap;
+  const uint32_t seq0 = (uint32_t)(*(volatile const unsigned long long*)&st->seq_base);
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  unsigned long long w_records = 0, w_removed = 0, w_out = 0, w_in = 0;
+  auto contribute = [&](int j, double m) {  // group max m at gate j
+    if (m > 0.0) atomicMax(&smax[j], (unsigned long long)__double_as_longlong(m));
+  };
+  for (;;) {
+    uint32_t gid = 0;
+    if (lane == 0) gid = atomicAdd(work, 1u);
+    gid = __shfl_sync(0xffffffffu, gid, 0);
+    if (gid >= G) break;
+    uint32_t n = g.cnt[gid];
+    if (n == 0 || n > kSmallMaxIn) continue;
+    Plane<W> z;
+#pragma unroll
+    for (int w = 0; w < W; ++w) z.w[w] = g.z[w][gid];
+    const uint64_t src = g.off[gid];
+    // touching gates (z_q = 1), 4 words of 32
+    uint32_t touch[kMaxSubGates / 32];
+#pragma unroll
+    for (int t = 0; t < kMaxSubGates / 32; ++t) {
+      const int k = 32 * t + (int)lane;
+      const bool tk = k < ng && (z.w[s_wq[k < ng ? k : 0]] & s_mq[k < ng ? k : 0]);
+      touch[t] = __ballot_sync(0xffffffffu, tk);
+    }
+    // load the group
+    double mx = 0.0, mn = kInf;
+    for (uint32_t i = lane; i < n; i += 32) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) xs[w * kSmallCap + i] = ar.x[w][src + i];
+      const double v = ar.c[src + i];
+      cs[i] = v;
+      mx = fmax(mx, fabs(v));
+      mn = fmin(mn, fabs(v));
+    }
+    mx = warp_max(mx);
+    mn = warp_min(mn);
+    __syncwarp();
+    w_in += n;
+    uint32_t nonfinite = 0;
+    unsigned long long g_records = 0, g_removed = 0;
+    uint32_t seen_local[kMaxSubGates / 32] = {0, 0, 0, 0};
+    bool abort = false;
+    int last = -1;
+    // truncation |c| <= T of the n strings (in place, order kept); returns the count kept
+    auto truncate = [&](double T) {
+      uint32_t out = 0;
+      double kmx = 0.0, kmn = kInf;
+      for (uint32_t b = 0; b < n; b += 32) {
+        const uint32_t i = b + lane;
+        Plane<W> x;
+        double v = 0.0;
+        bool keep = false;
+        if (i < n) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) x.w[w] = xs[w * kSmallCap + i];
+          v = cs[i];
+          keep = !(fabs(v) <= T);
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) {
+          const uint32_t o = out + __popc(bal & ((1u << lane) - 1u));
+#pragma unroll
+          for (int w = 0; w < W; ++w) xs[w * kSmallCap + o] = x.w[w];
+          cs[o] = v;
+          kmx = fmax(kmx, fabs(v));
+          kmn = fmin(kmn, fabs(v));
+        }
+        __syncwarp();
+        out += __popc(bal);
+      }
+      g_removed += n - out;
+      n = out;
+      mx = warp_max(kmx);
+      mn = warp_min(kmn);
+    };
+    for (int t = 0;; ++t) {
+      // next touching gate at or after last + 1 (ng: the end step)
+      int k = ng;
+      for (int ww = (last + 1) >> 5; ww < kMaxSubGates / 32; ++ww) {
+        uint32_t bits = touch[ww];
+        if (ww == ((last + 1) >> 5)) bits &= ~0u << ((last + 1) & 31);
+        if (bits) {
+          k = min(32 * ww + __ffs(bits) - 1, ng);
+          break;
+        }
+      }
+      // gates (last, k) leave the group as it is: their truncations apply,
+      // its max feeds their gmax until a threshold empties it
+      if (n && last + 1 < k) {
+        int jlim = k;  // gates (last, jlim) see the group's max (an emptying gate included)
+        double tp = -1.0;
+        for (int j0 = last + 1; j0 < k; j0 += 32) {
+          const int j = j0 + (int)lane;
+          const double tj = j < k ? s_tp[j] : -1.0;
+          tp = fmax(tp, tj);
+          const uint32_t em = __ballot_sync(0xffffffffu, j < k && mx <= tj);
+          if (em && jlim == k) jlim = j0 + __ffs(em);  // emptied at gate j0 + ffs - 1
+        }
+        tp = warp_max(tp);
+        for (int j = last + 1 + (int)lane; j < jlim; j += 32) contribute(j, mx);
+        if (tp >= 0.0 && mn <= tp) truncate(tp);
+      }
+      if (k >= ng || n == 0) break;
+      // ---- gate k: X_q on the group
+      const int wq = s_wq[k];
+      const uint64_t mq = s_mq[k];
+      const double cosv = s_cos[k], sinv = s_sin[k], nsin = -sinv;
+      for (uint32_t sl = lane; sl < 2 * kSmallCap; sl += 32) ht[sl] = 0u;
+      __syncwarp();
+      for (uint32_t i = lane; i < n; i += 32) {
+        uint32_t h = small_hash<W>(xs, i);
+        while (atomicCAS(&ht[h], 0u, i + 1) != 0u) h = (h + 1) & (2 * kSmallCap - 1);
+      }
+      __syncwarp();
+      uint32_t added = 0;
+      double gmx = 0.0;
+      unsigned long long recs = 0;
+      for (uint32_t b = 0; b < n; b += 32) {
+        const uint32_t i = b + lane;
+        bool child = false;
+        Plane<W> cx;
+        double cd = 0.0;
+        if (i < n) {
+          Plane<W> x;
+#pragma unroll
+          for (int w = 0; w < W; ++w) x.w[w] = xs[w * kSmallCap + i];
+          Plane<W> p = x;
+          p.w[wq] ^= mq;
+          uint32_t h = small_hash_key<W>(p), j = 0;
+          for (;;) {
+            const uint32_t e = ht[h];
+            if (e == 0u) break;
+            bool eq = true;
+#pragma unroll
+            for (int w = 0; w < W; ++w) eq &= xs[w * kSmallCap + e - 1] == p.w[w];
+            if (eq) {
+              j = e;
+              break;
+            }
+            h = (h + 1) & (2 * kSmallCap - 1);
+          }
+          const bool bit1 = (x.w[wq] & mq) != 0;
+          const double c = cs[i];
+          if (j) {
+            if (!bit1) {  // the pair (x, x | e_q): one butterfly, by the x_q = 0 string
+              double a = c, bb = cs[j - 1];
+              const double d1 = __dmul_rn(sinv, a), d0 = __dmul_rn(nsin, bb);
+              double v0 = __dmul_rn(a, cosv), v1 = __dmul_rn(bb, cosv);
+              if (d0 != 0.0) {
+                v0 = __dadd_rn(v0, d0);
+                ++recs;
+              }
+              if (d1 != 0.0) {
+                v1 = __dadd_rn(v1, d1);
+                ++recs;
+              }
+              cs[i] = v0;
+              cs[j - 1] = v1;
+              gmx = fmax(gmx, fmax(fabs(v0), fabs(v1)));
+              if (!(fabs(v0) <= 1.7976931348623157e308) || !(fabs(v1) <= 1.7976931348623157e308)) nonfinite = 1;
+            }
+          } else {  // alone: keeps c cos, its child (+sin from a Z, -sin from a Y) is a new string
+            const double v = __dmul_rn(c, cosv);
+            cd = __dmul_rn(bit1 ? nsin : sinv, c);
+            cs[i] = v;
+            gmx = fmax(gmx, fabs(v));
+            if (!(fabs(v) <= 1.7976931348623157e308)) nonfinite = 1;
+            if (cd != 0.0) {
+              child = true;
+              cx = p;
+              ++recs;
+              gmx = fmax(gmx, fabs(cd));
+              if (!(fabs(cd) <= 1.7976931348623157e308)) nonfinite = 1;
+            }
+          }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, child);
+        if (child) {
+          const uint32_t o = n + added + __popc(bal & ((1u << lane) - 1u));
+          if (o < kSmallCap) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) xs[w * kSmallCap + o] = cx.w[w];
+            cs[o] = cd;
+          }
+        }
+        added += __popc(bal);
+      }
+      __syncwarp();
+      if (n + added > kSmallCap) {  // outgrew the buffer: k_branch_sublayer takes the group
+        abort = true;
+        break;
+      }
+      n += added;
+      recs = warp_sum64(recs);
+      g_records += recs;
+      if (recs && lane == 0) seen_local[k >> 5] |= 1u << (k & 31);
+      gmx = warp_max(gmx);
+      if (lane == 0) contribute(k, gmx);  // gmax after gate k's apply, before its truncation
+      mx = gmx;
+      mn = 0.0;  // (force the truncation below)
+      truncate(s_tp[k]);
+      last = k;
+    }
+    if (abort) continue;  // nothing written: the group is untouched
+    nonfinite = __any_sync(0xffffffffu, nonfinite);
+    // sort by x (bitonic, padded with all-ones keys) and write out
+    uint32_t P = 1;
+    while (P < n) P <<= 1;
+    for (uint32_t i = n + lane; i < P; i += 32) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) xs[w * kSmallCap + i] = ~0ull;
+      cs[i] = 0.0;
+    }
+    __syncwarp();
+    for (uint32_t kk = 2; kk <= P; kk <<= 1) {
+      for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+        for (uint32_t i = lane; i < P; i += 32) {
+          const uint32_t l = i ^ jj;
+          if (l > i) {
+            Plane<W> a, b;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+              a.w[w] = xs[w * kSmallCap + i];
+              b.w[w] = xs[w * kSmallCap + l];
+            }
+            const bool up = (i & kk) == 0;
+            if (up ? plane_lt<W>(b, a) : plane_lt<W>(a, b)) {
+#pragma unroll
+              for (int w = 0; w < W; ++w) {
+                xs[w * kSmallCap + i] = b.w[w];
+                xs[w * kSmallCap + l] = a.w[w];
+              }
+              const double t2 = cs[i];
+              cs[i] = cs[l];
+              cs[l] = t2;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    unsigned long long o = 0;
+    if (lane == 0) {
+      o = atomicAdd(&st->bump, (unsigned long long)n);
+      if (o + n > cap) {
+        atomicOr(&st->err_arena, 1u);
+        atomicMin(&st->err_seq, (unsigned long long)seq0);
+      }
+    }
+    o = __shfl_sync(0xffffffffu, o, 0);
+    if (o + n > cap) continue;  // the attempt faults (the host rolls back); leave the group
+    for (uint32_t i = lane; i < n; i += 32) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) ar.x[w][o + i] = xs[w * kSmallCap + i];
+      ar.c[o + i] = cs[i];
+    }
+    if (lane == 0) {
+      g.off[gid] = o;
+      g.cnt[gid] = n;
+      g.cap[gid] = n;
+      g.gmax[gid] = n ? mx : 0.0;
+      g.gmin[gid] = n ? mn : kInf;
+      g.flags[gid] = nonfinite;
+      spec_done[gid] = 1;
+#pragma unroll
+      for (int t = 0; t < kMaxSubGates / 32; ++t)
+        if (seen_local[t]) atomicOr(&s_seen[t], seen_local[t]);
+    }
+    w_records += g_records;
+    w_removed += g_removed;
+    w_out += n;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (w_records) atomicAdd(&st->records, w_records);
+    if (w_removed) atomicAdd(&st->removed, w_removed);
+    if (w_out) atomicAdd(&st->out_elems, w_out);
+    if (w_in) atomicAdd(&st->aff_total, w_in);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < ng; k += blockDim.x) {
+    if (smax[k]) atomicMax(&gmax_out[k], smax[k]);
+    if ((s_seen[k >> 5] >> (k & 31)) & 1u) mark_seen(st, st->seen_base + k);
+  }
 }
 
 // k_branch_x: the segment / stream buffers of the per-gate path

@@ -1,0 +1,91 @@
+"""BASELINE config 2 on one B200: heavy-hex kicked Ising, theta_J = -pi/2,
+Z62, 20 steps, theta_h = k pi/16 (k = 1..8), per-gate truncation with the
+eps0 in [1e-7, 1e-4] that brings the peak live-string count closest to 1e9
+(without exceeding the device).  For each theta_h: a short search over eps0
+(geometric steps; a run that exhausts device memory counts as "too small an
+eps0"), then one JSON line per run with the per-layer <Z62>(t), |O|(t) and
+seconds, and a summary line with the eps0 used.
+
+  python tools/config2_search.py [--k 4] [--budget 900] > config2.jsonl
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import paper_2506_13241_b200 as pp  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--k", type=int, nargs="*", default=list(range(1, 9)), help="theta_h = k pi / 16")
+ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--target", type=float, default=1e9)
+ap.add_argument("--budget", type=float, default=900.0, help="seconds per theta_h")
+ap.add_argument("--eps0", type=float, default=1.5e-5, help="first eps0 tried")
+args = ap.parse_args()
+
+z62 = np.asarray(pp.parse_pauli_label("Z62", 127).words, np.uint64)[None]
+
+
+def run(k, eps):
+    one = pp.build_kicked_ising(pp.heavy_hex_127(), f"{k / 16!r}pi", "-0.5pi", 1)
+    eng = pp.Engine(127, eps)
+    eng.set_initial(z62, np.array([1.0]))
+    rows, peak, t_all = [], 1, time.perf_counter()
+    for t in range(1, args.steps + 1):
+        t0 = time.perf_counter()
+        try:
+            r = eng.run_circuit(one)[0]
+        except pp.ResourceLimitError as exc:
+            return {"k": k, "epsilon0": eps, "resource_limit_at": t, "error": str(exc)[:200], "rows": rows,
+                    "peak": peak}
+        dt = time.perf_counter() - t0
+        peak = max(peak, r["term_count"])
+        rows.append({"t": t, "Z62": r["observable"], "terms": r["term_count"], "removed": r["removed"],
+                     "records": r["records_sent"], "seconds": dt})
+    return {"k": k, "epsilon0": eps, "peak": peak, "rows": rows, "seconds": time.perf_counter() - t_all}
+
+
+for k in args.k:
+    start = time.time()
+    if k == 8:  # theta_h = pi/2 is Clifford: |O| = 1 at every eps0 (acceptance_main.cpp:434-445)
+        res = run(k, 1e-7)
+        print(json.dumps(res), flush=True)
+        print(json.dumps({"summary": True, "k": k, "theta_h_pi": k / 16, "epsilon0": 1e-7, "peak": res["peak"],
+                          "note": "Clifford: the 1e9 target is unreachable"}), flush=True)
+        continue
+    eps, best, tried = args.eps0, None, []
+    lo, hi = None, None  # eps0 with peak < target (too big), eps0 that overflowed or exceeded (too small)
+    for _ in range(8):
+        if time.time() - start > args.budget:
+            break
+        res = run(k, eps)
+        tried.append(eps)
+        print(json.dumps(res), flush=True)
+        over = "resource_limit_at" in res
+        if not over and (best is None or abs(math.log(res["peak"] / args.target)) <
+                         abs(math.log(best["peak"] / args.target))):
+            best = res
+        if over or res["peak"] > 1.6 * args.target:
+            hi = eps
+        elif res["peak"] < 0.6 * args.target:
+            lo = eps
+        else:
+            break
+        if eps <= 1e-7 and not over and res["peak"] < args.target:
+            break  # the smallest eps0 the config allows
+        if lo is not None and hi is not None:
+            eps = math.sqrt(lo * hi)
+        elif over or res["peak"] > args.target:
+            eps = eps * 2.0
+        else:
+            eps = max(1e-7, eps * max(0.05, res["peak"] / args.target) ** 0.8)
+    print(json.dumps({"summary": True, "k": k, "theta_h_pi": k / 16, "epsilon0": best["epsilon0"] if best else None,
+                      "peak": best["peak"] if best else None, "tried": tried,
+                      "Z62": [r["Z62"] for r in best["rows"]] if best else None,
+                      "seconds": best.get("seconds") if best else None}), flush=True)
