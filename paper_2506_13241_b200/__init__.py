@@ -15,6 +15,24 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
+
+def _nccl_library():
+    """The libnccl.so.2 PyTorch links (the nvidia-nccl wheel), so the sharded
+    engine's run-time NCCL and a later ``import torch`` share one library."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(base, "nccl", "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            return cand
+    return None
+
+
+if "PP_NCCL_LIBRARY" not in os.environ:
+    _lib = _nccl_library()
+    if _lib:
+        os.environ["PP_NCCL_LIBRARY"] = _lib
+
 try:
     from . import _pauliprop as _impl
 except ImportError as exc:  # pragma: no cover - exercised only when unbuilt

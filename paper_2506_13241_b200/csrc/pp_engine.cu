@@ -1087,6 +1087,12 @@ class EngineImpl final : public EngineBase {
           gc_into_other(next_arena_target());
           return false;
         }
+        // the faulted run saw a subset of the groups: its maxima are lower
+        // bounds of the true ones, so they can only raise the prediction
+        // (a threshold predicted too low keeps too many strings -- the usual
+        // cause of the fault)
+        for (size_t k = 0; k < count; ++k)
+          if (tobs[k] > tpred[k]) tpred[k] = tobs[k];
       } else {
         tpred = tobs;
       }
@@ -1525,7 +1531,8 @@ class EngineImpl final : public EngineBase {
       dirty_ = true;
       sync_state();
     }
-    gmax_ = T;  // informational; the orchestrator keeps the global max
+    // gmax_ stays what the orchestrator set (pp_set_global_max): the
+    // speculative sharded run predicts its thresholds from it
     return counters_.removed - before;
   }
 

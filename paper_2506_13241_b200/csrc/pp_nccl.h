@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -41,10 +42,16 @@ struct NcclApi {
 
  private:
   void load() {
-    void* h = nullptr;
+    // one NCCL per process: the copy already loaded (e.g. PyTorch's), else
+    // PP_NCCL_LIBRARY (the Python package points it at the wheel PyTorch
+    // links, so a later `import torch` finds the same soname loaded), else
+    // the loader's search path
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    const char* env = std::getenv("PP_NCCL_LIBRARY");
+    if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
     for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
       if (h) break;
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
     }
     if (!h) {
       error = std::string("NCCL not found (dlopen libnccl.so.2): ") + dlerror();
