@@ -1571,13 +1571,45 @@ class EngineImpl final : public EngineBase {
     for (int b = 0; b < bins; ++b) pos[b] = neg[b] = 0;
     if (G_ == 0) return;
     const double lower = std::max(epsilon0, 1e-16);
-    evict_cnt_.ensure(16 * (size_t)bins);
+    // The reference bins ax = |c / gmax| in (lower, 1) by
+    // int(bins * (1 - std::log(ax) / log_lower)) (sparse_operator.cpp:177-186),
+    // with the host's libm log.  That map is monotone in ax, so it is fixed by
+    // its bin edges: edge[b] = the smallest double whose bin is >= b, found
+    // here by bisection over the ordered bit patterns with the very same host
+    // expression.  The kernel counts edges <= ax -- no device log, so a
+    // 1-ulp libm difference cannot move a string across a bin boundary.
+    const double log_lower = std::log(lower);
+    auto bin_of = [&](double ax) {
+      int b = static_cast<int>(bins * (1.0 - std::log(ax) / log_lower));
+      return std::clamp(b, 0, bins - 1);
+    };
+    std::vector<double> edges(bins > 1 ? bins - 1 : 1, 2.0);
+    for (int b = 1; b < bins; ++b) {
+      uint64_t lo = __builtin_bit_cast(uint64_t, lower), hi = __builtin_bit_cast(uint64_t, 1.0);
+      if (!(lower < 1.0) || bin_of(std::nextafter(1.0, 0.0)) < b) {
+        edges[b - 1] = 1.0;  // only ax >= 1 (the last bin) reaches it
+        continue;
+      }
+      // invariant: bin(lo) < b or lo == lower (excluded), bin(hi - 1ulp) >= b
+      while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (bin_of(__builtin_bit_cast(double, mid)) >= b) hi = mid;
+        else lo = mid;
+      }
+      edges[b - 1] = __builtin_bit_cast(double, hi);
+    }
+    const size_t ne = edges.size();
+    evict_cnt_.ensure(16 * (size_t)bins + 8 * ne);
     unsigned long long* d = evict_cnt_.as<unsigned long long>();
+    double* d_edges = reinterpret_cast<double*>(d + 2 * (size_t)bins);
     PP_CUDA(cudaMemsetAsync(d, 0, 16 * (size_t)bins, stream_));
+    PP_CUDA(copy_async(d_edges, edges.data(), 8 * ne, cudaMemcpyHostToDevice, stream_));
     push_scalars(bseq_);
-    const size_t smem = 8 * (size_t)bins;
+    const size_t smem = 8 * (size_t)((bins + 1) & ~1) + 8 * ne;
+    if (smem > 48 * 1024)
+      PP_CUDA(cudaFuncSetAttribute(k_histogram<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_histogram<W><<<persistent_grid(), kCta, smem, stream_>>>(gview(gcur_), aview(cur_), d_stats_, bins, gmax,
-                                                               lower, std::log(lower), d, d + bins);
+                                                               lower, d_edges, d, d + bins);
     ++launches_;
     PP_CUDA(copy_async(pos, d, 8 * (size_t)bins, cudaMemcpyDeviceToHost, stream_));
     PP_CUDA(copy_async(neg, d + bins, 8 * (size_t)bins, cudaMemcpyDeviceToHost, stream_));

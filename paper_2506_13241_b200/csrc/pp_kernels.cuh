@@ -3271,10 +3271,15 @@ constexpr int kMaxHistBins = 4096;
 
 template <int W>
 __global__ void __launch_bounds__(kCta) k_histogram(GroupView<W> g, ArenaView<W> ar, const DevStats* st, int bins,
-                                                   double gmax, double lower, double log_lower,
+                                                   double gmax, double lower, const double* __restrict__ edges_g,
                                                    unsigned long long* pos, unsigned long long* neg) {
-  extern __shared__ unsigned int hist[];  // [2 * bins]: positive then negative
+  // density_histogram (sparse_operator.cpp:150-196): the bin of a string in
+  // (lower, 1) is the number of host-computed edges <= |c / gmax|
+  extern __shared__ unsigned int hist[];  // [2 * bins]: positive then negative, then the edges
+  double* edges = reinterpret_cast<double*>(hist + 2 * ((bins + 1) & ~1));
+  const int ne = bins > 1 ? bins - 1 : 1;
   for (int b = threadIdx.x; b < 2 * bins; b += kCta) hist[b] = 0;
+  for (int b = threadIdx.x; b < ne; b += kCta) edges[b] = edges_g[b];
   __syncthreads();
   const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
   for (uint32_t gid = blockIdx.x; gid < G; gid += gridDim.x) {
@@ -3289,8 +3294,13 @@ __global__ void __launch_bounds__(kCta) k_histogram(GroupView<W> g, ArenaView<W>
       } else if (ax >= 1.0) {
         b = bins - 1;
       } else {
-        b = (int)((double)bins * (1.0 - log(ax) / log_lower));
-        b = b < 0 ? 0 : (b > bins - 1 ? bins - 1 : b);
+        int lo = 0, hi = bins - 1;  // number of edges <= ax, in [0, bins - 1]
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (edges[mid - 1] <= ax) lo = mid;
+          else hi = mid - 1;
+        }
+        b = lo;
       }
       atomicAdd(&hist[(x < 0 ? bins : 0) + b], 1u);
     }

@@ -66,6 +66,54 @@ def test_device_histogram_large_state(pp, O):
         assert got["total_terms"] == len(c)
 
 
+def _ref_bin(ax, bins, lower):
+    """sparse_operator.cpp:177-186 with the host libm (Python's math.log is
+    the same glibc log the reference calls)."""
+    import math
+    if ax <= lower:
+        return 0
+    if ax >= 1.0:
+        return bins - 1
+    return min(max(int(bins * (1.0 - math.log(ax) / math.log(lower))), 0), bins - 1)
+
+
+@pytest.mark.parametrize("bins,eps", [(64, 0.0), (37, 1e-5), (1000, 1e-12)])
+def test_device_histogram_bin_edges_exact(pp, O, bins, eps):
+    """Values one ulp either side of every bin boundary land in the
+    reference's bin: the kernel compares against host-computed edges, so a
+    device-vs-glibc log difference cannot move a string."""
+    import math
+    lower = max(eps, 1e-16)
+    vals = []
+    for b in range(1, bins):
+        # the nominal boundary, then walk to the exact first double of bin b
+        x = math.exp(math.log(lower) * (1.0 - b / bins))
+        for _ in range(64):
+            if _ref_bin(x, bins, lower) >= b and _ref_bin(math.nextafter(x, 0.0), bins, lower) < b:
+                break
+            x = math.nextafter(x, 0.0) if _ref_bin(x, bins, lower) >= b else math.nextafter(x, 2.0)
+        vals += [math.nextafter(x, 0.0), x, math.nextafter(x, 2.0)]
+    vals += [lower, math.nextafter(lower, 2.0), 1.0, math.nextafter(1.0, 0.0)]
+    n = len(vals)
+    sites = 12  # distinct strings: x patterns over 12 sites (4^12 > n)
+    words = np.zeros((n, 4), np.uint64)
+    for i in range(n):
+        v, w = i + 1, 0
+        for s in range(sites):
+            w |= (v % 4) << (2 * s)
+            v //= 4
+        words[i, 0] = w
+    coeffs = np.array([v if i % 2 else -v for i, v in enumerate(vals)])
+    e = pp.Engine(sites, 0.0)
+    e.set_initial(words, coeffs)
+    got = e.density_histogram(bins, eps, 1.0)
+    pos = [0] * bins
+    neg = [0] * bins
+    for c in coeffs:
+        (neg if c < 0 else pos)[_ref_bin(abs(c), bins, lower)] += 1
+    assert got["positive_counts"] == pos and got["negative_counts"] == neg
+
+
 def test_device_histogram_rejects_zero_max(pp, O):
     e = pp.Engine(2, 0.0)
     e.set_initial(O.site_word(0, 3)[None], [1.0])
