@@ -1462,6 +1462,29 @@ __device__ __forceinline__ void dense_contribute(const DenseCtl<W>& dc, int k, i
   }
 }
 
+// Shared-memory bank spreading for the register butterflies.  A thread owns
+// the 2^r points its r stage bits span, at b | dep(e) (b: its index with
+// zeros at the stage positions).  When stage positions fall among the low 4
+// tile bits, the lanes of a half-warp differ only above them and all hit one
+// bank (a 16-way conflict at stage bits {0..3}).  Thread t instead keeps
+// point b | dep(e ^ g) in register e, g taking the lane bits that land above
+// bit 3 onto the low stage positions: the 16 lanes then cover 16 distinct
+// banks.  The butterfly of stage i is symmetric under that relabelling up to
+// the sign of sin (registers e, e | 2^i hold the upper, lower point when bit
+// i of g is set), so each point sees the same products and sums.
+__device__ __forceinline__ uint32_t dense_bank_flip(const uint32_t* pm, int r, uint32_t lane) {
+  int s = 0;
+  for (int i = 0; i < r; ++i) s += pm[i] < 4u;
+  uint32_t g = 0;
+  for (int i = 0; i < r; ++i)
+    if (pm[i] < 4u) {
+      int rk = 0;  // rank of pm[i] among the low stage positions
+      for (int k = 0; k < r; ++k) rk += pm[k] < pm[i];
+      g |= ((lane >> (4 - s + rk)) & 1u) << i;
+    }
+  return g;
+}
+
 template <int W, bool SPEC, bool FAST = false>
 __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P, int j0, int j1, DenseCtl<W>& dc,
                                                unsigned long long& records, unsigned long long& removed,
@@ -1495,24 +1518,76 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
             q[b2 + 1] = t2;
           }
       const uint32_t sixteenth = half >> 3;
+      const uint32_t g = dense_bank_flip(pm, 4, lane);
+      uint32_t dg = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        dg |= ((g >> i) & 1u) << pm[i];
+        if ((g >> i) & 1u) sn[i] = -sn[i];
+      }
       for (uint32_t t = threadIdx.x; t < sixteenth; t += kCta) {
         uint32_t b = t;
 #pragma unroll
         for (int i = 0; i < 4; ++i) b = ((b >> q[i]) << (q[i] + 1)) | (b & ((1u << q[i]) - 1u));
+        b |= dg;
         double a[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          a[e] = d[b | ((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
-                   (((e >> 3) & 1) << pm[3])];
+          a[e] = d[b ^ (((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
+                        (((e >> 3) & 1) << pm[3]))];
+        if (FAST) {
+          // |v| >= 2^-899 for all 16 points (high words >= kLiveHi): no point
+          // is absent, so dense_bfly_fast's per-point bookkeeping reduces to
+          // constants -- every butterfly records both deltas (16 per stage)
+          // and removes nothing, provided every output stays >= 2^-899 (one
+          // min over the outputs' high words per stage; below it, an exact
+          // zero included, raises anom and the caller redoes the block point
+          // by point).  All 16 zero: nothing to do, nothing to store.
+          constexpr uint32_t kLiveHi = 124u << 20;
+          uint32_t mn = 0xffffffffu, any = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t h = (uint32_t)__double2hiint(a[e]) & 0x7fffffffu;
+            mn = min(mn, h);
+            any |= h | (uint32_t)__double2loint(a[e]);
+          }
+          if (!any) continue;
+          if (mn >= kLiveHi) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (!((e >> i) & 1)) dense_bfly_t<FAST>(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed, anom);
+            for (int i = 0; i < 4; ++i) {
+              uint32_t omn = 0xffffffffu;
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (!((e >> i) & 1)) {
+                  double& x0 = a[e];
+                  double& x1 = a[e | (1 << i)];
+                  const double d1 = __dmul_rn(sn[i], x0), d0 = __dmul_rn(-sn[i], x1);
+                  x0 = __dadd_rn(__dmul_rn(x0, cs[i]), d0);
+                  x1 = __dadd_rn(__dmul_rn(x1, cs[i]), d1);
+                  omn = min(omn, min((uint32_t)__double2hiint(x0) & 0x7fffffffu,
+                                     (uint32_t)__double2hiint(x1) & 0x7fffffffu));
+                }
+              anom |= omn < kLiveHi;
+            }
+            records += 64;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (!((e >> i) & 1)) dense_bfly_t<FAST>(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed, anom);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (!((e >> i) & 1)) dense_bfly_t<FAST>(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed, anom);
+        }
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          d[b | ((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
-            (((e >> 3) & 1) << pm[3])] = a[e];
+          d[b ^ (((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
+                 (((e >> 3) & 1) << pm[3]))] = a[e];
       }
       __syncthreads();
       j += 3;
@@ -1526,35 +1601,43 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
       const uint32_t p1 = __popc(P & ((1u << dc.sbit[j]) - 1u)), p2 = __popc(P & ((1u << dc.sbit[j + 1]) - 1u));
       const uint32_t plo = p1 < p2 ? p1 : p2, phi = p1 < p2 ? p2 : p1;
       const uint32_t m1 = 1u << p1, m2 = 1u << p2;
-      const double c1 = dc.scos[j], s1 = dc.ssin[j], c2 = dc.scos[j + 1], s2 = dc.ssin[j + 1];
+      const uint32_t pp[2] = {p1, p2};
+      const uint32_t g = dense_bank_flip(pp, 2, lane);  // see there
+      const uint32_t dg = ((g & 1u) << p1) | (((g >> 1) & 1u) << p2);
+      const double c1 = dc.scos[j], c2 = dc.scos[j + 1];
+      const double s1 = (g & 1u) ? -dc.ssin[j] : dc.ssin[j], s2 = (g & 2u) ? -dc.ssin[j + 1] : dc.ssin[j + 1];
       const uint32_t quarter = half >> 1;
       for (uint32_t t = threadIdx.x; t < quarter; t += kCta) {
         uint32_t b = ((t >> plo) << (plo + 1)) | (t & ((1u << plo) - 1u));
         b = ((b >> phi) << (phi + 1)) | (b & ((1u << phi) - 1u));
-        double a00 = d[b], a10 = d[b | m1], a01 = d[b | m2], a11 = d[b | m1 | m2];
+        b |= dg;
+        double a00 = d[b], a10 = d[b ^ m1], a01 = d[b ^ m2], a11 = d[b ^ m1 ^ m2];
         dense_bfly_t<FAST>(a00, a10, c1, s1, -s1, records, removed, anom);
         dense_bfly_t<FAST>(a01, a11, c1, s1, -s1, records, removed, anom);
         dense_bfly_t<FAST>(a00, a01, c2, s2, -s2, records, removed, anom);
         dense_bfly_t<FAST>(a10, a11, c2, s2, -s2, records, removed, anom);
         d[b] = a00;
-        d[b | m1] = a10;
-        d[b | m2] = a01;
-        d[b | m1 | m2] = a11;
+        d[b ^ m1] = a10;
+        d[b ^ m2] = a01;
+        d[b ^ m1 ^ m2] = a11;
       }
       __syncthreads();
       ++j;
       continue;
     }
     const uint32_t p = __popc(P & ((1u << dc.sbit[j]) - 1u));
-    const double cosv = dc.scos[j], sinv = dc.ssin[j], nsin = -sinv;
+    // bank spreading (dense_bank_flip): for p < 4 the lanes above bit 3 flip
+    // which register holds the lower point
+    const uint32_t gflip = p < 4u ? (lane >> 3) & 1u : 0u;
+    const double cosv = dc.scos[j], sinv = gflip ? -dc.ssin[j] : dc.ssin[j], nsin = -sinv;
     // speculative mode: the inputs carry the truncations of the previous
     // stage's window; the outputs' max feeds this gate's gmax
     const double tprev = (spec && j > 0) ? dc.strunc[j - 1] : -1.0;
     const uint32_t lo = (1u << p) - 1u;
     double mx = 0.0;
     for (uint32_t t = threadIdx.x; t < half; t += kCta) {
-      const uint32_t b0 = ((t & ~lo) << 1) | (t & lo);
-      double a = d[b0], b = d[b0 | (1u << p)];
+      const uint32_t b0 = (((t & ~lo) << 1) | (t & lo)) | (gflip << p);
+      double a = d[b0], b = d[b0 ^ (1u << p)];
       if (tprev >= 0.0) {
         if (a != 0.0 && fabs(a) <= tprev) {  // remove_below: |c| <= T
           a = 0.0;
@@ -1568,7 +1651,7 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
       dense_bfly_t<FAST && !SPEC>(a, b, cosv, sinv, nsin, records, removed, anom);
       if (spec) mx = fmax(mx, fmax(fabs(a), fabs(b)));
       d[b0] = a;
-      d[b0 | (1u << p)] = b;
+      d[b0 ^ (1u << p)] = b;
     }
     if (spec) {
       mx = __longlong_as_double((long long)warp_max_bits((unsigned long long)__double_as_longlong(mx)));
