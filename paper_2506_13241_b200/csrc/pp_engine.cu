@@ -26,6 +26,7 @@
 #include "../../include/pauliprop_gpu.h"
 #include "pp_regroup.cuh"
 #include "pp_zz.cuh"
+#include "pp_dense.cuh"
 
 namespace ppgpu {
 
@@ -359,7 +360,7 @@ static void release_stream_set(int dev, const StreamSet& s) {
 // launch configuration of one (device, W): attributes set once, grids from
 // the occupancy calculator
 struct LaunchSetup {
-  uint32_t zz_grid = 0, branch_grid = 0, sub_grid = 0, small_grid = 0;
+  uint32_t zz_grid = 0, branch_grid = 0, sub_grid = 0, small_grid = 0, dense_grid = 0;
 };
 static std::mutex g_setup_mu;
 static std::map<std::pair<int, int>, LaunchSetup> g_setup;
@@ -444,6 +445,9 @@ class EngineImpl final : public EngineBase {
                                      (int)big_sort_smem()));
         PP_CUDA(cudaFuncSetAttribute(k_spec_small<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)spec_small_smem_bytes<W>()));
+        PP_CUDA(cudaFuncSetAttribute(k_dense_sublayer<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)dense_smem_bytes<W>()));
+        PP_CUDA(cudaFuncSetAttribute(k_dense_sublayer<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         PP_CUDA(cudaFuncSetAttribute(k_branch_x<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         PP_CUDA(cudaFuncSetAttribute(k_branch_sublayer<W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         PP_CUDA(cudaFuncSetAttribute(k_branch_zz<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -458,17 +462,21 @@ class EngineImpl final : public EngineBase {
         ls.zz_grid = (uint32_t)(sms * std::max(occ, 1));
         ls.branch_grid = (uint32_t)(sms * std::max(occ_x, 1));
         ls.sub_grid = (uint32_t)(sms * std::max(occ_s, 1));
+        int occ_d = 1;
+        PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_dense_sublayer<W>, kCta, dense_smem_bytes<W>()));
+        ls.dense_grid = (uint32_t)(sms * std::max(occ_d, 1));
         int occ_k = 1;
         PP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_k, k_spec_small<W>, kSmallWarps * 32,
                                                               spec_small_smem_bytes<W>()));
         ls.small_grid = (uint32_t)(sms * std::max(occ_k, 1));
         if (std::getenv("PP_DEBUG"))
-          std::fprintf(stderr, "[pp] W=%d branch CTAs/SM %d, sublayer CTAs/SM %d, smem %zu\n", W, occ_x, occ_s,
-                       branch_smem_bytes<W>());
+          std::fprintf(stderr, "[pp] W=%d branch CTAs/SM %d, sublayer CTAs/SM %d, smem %zu; dense CTAs/SM %d, smem %zu\n",
+                       W, occ_x, occ_s, branch_smem_bytes<W>(), occ_d, dense_smem_bytes<W>());
       }
       zz_grid_ = ls.zz_grid;
       branch_grid_ = ls.branch_grid;
       sub_grid_ = ls.sub_grid;
+      dense_grid_ = ls.dense_grid;
       small_grid_ = ls.small_grid;
     }
     keep_zeros_ = cfg.cadence == PP_CADENCE_LAYER;
@@ -761,19 +769,23 @@ class EngineImpl final : public EngineBase {
   }
   // sort the groups a regroup left unsorted (before any consumer that needs
   // x order: the per-gate branch kernels, Z-type pairs, shard eviction)
-  void ensure_sorted() {
+  // pending_only (a sublayer's unsorted fault): only the groups a regroup
+  // left unsorted -- the ones still waiting for the run; the class-major
+  // output the run has written already stays as it is (and unsorted_ set)
+  void ensure_sorted(bool pending_only = false) {
     if (!unsorted_) return;
     sync_state();
-    unsorted_ = false;
+    unsorted_ = pending_only;
     if (!G_) return;
+    const int mode = pending_only ? 2 : 1;
     ensure_arena(1 - cur_, std::max<uint64_t>(live_ + 1, 1024));  // merge scratch for big groups
     k_set_distinct<<<1, 1, 0, stream_>>>(d_stats_, G_);
     const uint32_t small_grid = std::max<uint32_t>(1u, std::min<uint32_t>(G_, 148u * 4u));
     const uint32_t big_grid = std::max<uint32_t>(1u, std::min<uint32_t>(G_, 148u * 2u));
     k_sort_small<W><<<small_grid, kCta, sizeof(SortSmem<W>), stream_>>>(gview(gcur_), aview(cur_), keep_zeros_, d_stats_,
-                                                                         1);
+                                                                         mode);
     k_sort_big<W><<<big_grid, kCta, big_sort_smem(), stream_>>>(gview(gcur_), aview(cur_), aview(1 - cur_), keep_zeros_,
-                                                                 d_stats_, 1);
+                                                                 d_stats_, mode);
     launches_ += 3;
     dirty_ = true;
   }
@@ -1223,12 +1235,30 @@ class EngineImpl final : public EngineBase {
     // persistent grid, but no more CTAs than a few per group (tiny layers)
     const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(sub_grid_, 4u * G_));
     count_param_h2d(sizeof(sub_gates_));  // the run's gate list
-    k_branch_sublayer<W><<<grid, kCta, branch_smem_bytes<W>(), stream_>>>(
-        gview(gcur_), aview(cur_), sub_gates_, keep_zeros_, &d_stats_->work[0], nullptr, nullptr, d_stats_);
+    if (sub_gates_.dense && !no_dense_kernel_) {
+      // the dense path in its own kernel; what it leaves behind (left_list_,
+      // DevStats::left_n) goes through the per-gate path right after it
+      left_list_.ensure((size_t)std::max<uint32_t>(2u * G_, 4096u) * sizeof(uint32_t));
+      const uint32_t dgrid = std::max<uint32_t>(1u, std::min<uint32_t>(dense_grid_, 4u * G_));
+      k_dense_sublayer<W><<<dgrid, kCta, dense_smem_bytes<W>(), stream_>>>(
+          gview(gcur_), aview(cur_), sub_gates_, &d_stats_->work[0], d_stats_, left_list_.as<uint32_t>());
+      SubGates rest = sub_gates_;
+      rest.dense = 0;
+      k_branch_sublayer<W><<<grid, kCta, branch_smem_bytes<W>(), stream_>>>(
+          gview(gcur_), aview(cur_), rest, keep_zeros_, &d_stats_->work[1], nullptr, nullptr, d_stats_, nullptr,
+          left_list_.as<uint32_t>());
+      ++launches_;
+    } else {
+      k_branch_sublayer<W><<<grid, kCta, branch_smem_bytes<W>(), stream_>>>(
+          gview(gcur_), aview(cur_), sub_gates_, keep_zeros_, &d_stats_->work[0], nullptr, nullptr, d_stats_);
+    }
     PP_CUDA(cudaEventRecord(ev.second, stream_));
     pending_events_.push_back(ev);
     ++launches_;
     ++branch_launches_;
+    // a group with several x classes leaves the dense path class-major
+    // (kFlagUnsorted | kFlagMinFirst, dense_multi)
+    if (sub_gates_.dense && sub_gates_.maxk > 1) unsorted_ = true;
     if (keep_zeros_) may_hold_zeros_ = true;
     if (cfg_.cadence == PP_CADENCE_GATE && !external()) gmax_stale_ = true;
     dirty_ = true;
@@ -1237,6 +1267,7 @@ class EngineImpl final : public EngineBase {
   // relaunch; groups that finished carry the run's stamps and are skipped
   void resume_sublayer(bool diag) {
     sub_pending_ = false;
+    int unsorted_faults = 0;
     for (int attempt = 0; arena_fault_ || unsorted_fault_; ++attempt) {
       if (attempt > 64) throw EngineError(PP_ERR_RESOURCE, "arena cannot hold the sublayer");
       k_clear_arena_error<<<1, 1, 0, stream_>>>(d_stats_);
@@ -1251,7 +1282,9 @@ class EngineImpl final : public EngineBase {
       }
       if (unsorted_fault_) {  // groups the per-gate path needs sorted
         unsorted_fault_ = false;
-        ensure_sorted();
+        // (a second fault in a row: a group an earlier dense run left
+        // class-major is among them -- sort everything)
+        ensure_sorted(/*pending_only=*/unsorted_faults++ == 0);
       }
       launch_sublayer();
       sync_state(diag);
@@ -2667,6 +2700,9 @@ class EngineImpl final : public EngineBase {
 
   uint32_t branch_grid_ = 148u * 2u;
   uint32_t sub_grid_ = 148u * 2u;
+  uint32_t dense_grid_ = 148u * 2u;
+  DevBuf left_list_;             // groups the dense kernel left for the per-gate path
+  bool no_dense_kernel_ = std::getenv("PP_NO_DENSE_KERNEL") != nullptr;  // dense path inside k_branch_sublayer
   uint32_t small_grid_ = 148u * 3u;
   uint32_t zz_grid_ = 148u * 2u;
   uint32_t maxcnt_ = 0x7fffffffu;  // largest group at the last full sync (bounds Z-type pair sizes)
@@ -2751,7 +2787,7 @@ std::string engine_key(const pp_config& c) {
   put(&c.flags, sizeof c.flags);
   put(&c.mem_fraction, sizeof c.mem_fraction);
   for (const char* v : {"PP_TIGHT_ARENA", "PP_NO_DENSE", "PP_DENSE_MAXK", "PP_NO_DEFER", "PP_BLOCKING_SYNC", "PP_TRACE",
-                        "PP_NO_SPECULATE"}) {
+                        "PP_NO_SPECULATE", "PP_NO_DENSE_KERNEL", "PP_DENSE_CAREFUL"}) {
     const char* x = std::getenv(v);
     k += '|';
     if (x) k += x;

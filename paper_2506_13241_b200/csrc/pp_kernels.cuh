@@ -43,6 +43,16 @@ struct GroupView {
 // until the dense path or a sort pass (k_sort_small/k_sort_big with
 // only_unsorted) rewrites them.
 constexpr uint32_t kFlagUnsorted = 2u;
+// bit2: the smallest x of an unsorted group is its first string (dense_multi's class-major output)
+constexpr uint32_t kFlagMinFirst = 4u;
+// which groups a sort pass takes: only_unsorted = 0 all, 1 the unsorted ones,
+// 2 the unsorted ones that are not a dense run's class-major output (what a
+// regroup left, i.e. groups still waiting for the current run)
+__device__ __forceinline__ bool sort_wanted(uint32_t flags, int only_unsorted) {
+  if (only_unsorted == 0) return true;
+  if (!(flags & kFlagUnsorted)) return false;
+  return only_unsorted == 1 || !(flags & kFlagMinFirst);
+}
 
 // deferred truncation helpers (see k_thresh): a pending string is held as
 // -0.0 in shared memory (stored values are never zero when truncating per
@@ -127,7 +137,7 @@ struct DevStats {
   unsigned long long dense_groups;  // groups applied by the dense sublayer path (cumulative)
   unsigned long long dense_out;     // strings those groups wrote
   unsigned int seen_base;           // window index of gate 0 of the current launch run
-  unsigned int seen_pad;
+  unsigned int left_n;              // groups k_dense_sublayer left for the per-gate path (this launch)
   unsigned long long seen[kSeenWords];            // bit g: window gate g sent a record
   unsigned long long zz_seen[kZZSeenGroups][2];   // fused ZZ run: edges (bit i of group k) that sent one
 };
@@ -149,6 +159,7 @@ __global__ void k_set_scalars(DevStats* st, unsigned int G, unsigned long long c
   st->arena_cap = cap;
   st->seq_base = seq_base;
   st->work[0] = st->work[1] = 0;
+  st->left_n = 0;
   clear_red(&st->red[0]);
   clear_red(&st->red[1]);
   clear_red(&st->red[2]);  // the host-sync slot (only sync_state's k_reduce fills it)
@@ -1339,9 +1350,6 @@ struct DenseTail {
   uint8_t hcls[kDenseSlots];            //   its class index (ascending F)
   uint16_t used[kDenseSlots];           // occupied slots, compacted
   Plane<W> sF[kDenseMaxK];              // classes in ascending order
-  uint8_t lvl[kDenseMaxK][kDenseMaxLog + 1];  // rank terms: #classes j with t_ij = t
-  uint32_t lmask[kDenseMaxK];           //   levels t present
-  uint32_t C[kDenseMaxK];               //   sum over j < i of 2^t_ij
 };
 
 template <int W>
@@ -1416,35 +1424,6 @@ __device__ __forceinline__ void dense_bfly(double& a, double& b, double cosv, do
   b = v1;
 }
 
-// The same butterfly without the per-point branches.  Always adding the
-// delta equals dense_bfly's "add only if nonzero" whenever no delta
-// underflows to zero (it is zero exactly when its source point is), and the
-// record count is then the number of nonzero sources.  That holds while every
-// |sin| >= 2^-100 (SubGates::fast) and every nonzero value has |v| >= 2^-899
-// and is finite; an output of a live pair outside that range (an exact
-// cancellation to zero included) raises `anom`, and the caller redoes the
-// block with dense_bfly.  Nothing is removed on this path (no zeros appear).
-__device__ __forceinline__ void dense_bfly_fast(double& a, double& b, double cosv, double sinv, double nsin,
-                                                unsigned long long& records, uint32_t& anom) {
-  const double d1 = __dmul_rn(sinv, a), d0 = __dmul_rn(nsin, b);
-  const double v0 = __dadd_rn(__dmul_rn(a, cosv), d0), v1 = __dadd_rn(__dmul_rn(b, cosv), d1);
-  const unsigned long long ab = (unsigned long long)__double_as_longlong(a) << 1;
-  const unsigned long long bb = (unsigned long long)__double_as_longlong(b) << 1;
-  const uint32_t na = ab != 0ull, nb = bb != 0ull;
-  records += na + nb;
-  const uint32_t e0 = (uint32_t)((unsigned long long)__double_as_longlong(v0) >> 52) & 0x7ffu;
-  const uint32_t e1 = (uint32_t)((unsigned long long)__double_as_longlong(v1) >> 52) & 0x7ffu;
-  anom |= (na | nb) & ((uint32_t)(e0 - 124u > 0x7feu - 124u) | (uint32_t)(e1 - 124u > 0x7feu - 124u));
-  a = v0;
-  b = v1;
-}
-template <bool FAST>
-__device__ __forceinline__ void dense_bfly_t(double& a, double& b, double cosv, double sinv, double nsin,
-                                             unsigned long long& records, unsigned long long& removed, uint32_t& anom) {
-  if (FAST) dense_bfly_fast(a, b, cosv, sinv, nsin, records, anom);
-  else dense_bfly(a, b, cosv, sinv, nsin, records, removed);
-}
-
 // butterflies of stages [j0, j1) over a tile of 2^u doubles in shared memory;
 // P: the b bits of the tile (stage bit p is tile bit popc(P & (2^p - 1)))
 // max |c| of a group after gate k's apply was M: gate k and the following
@@ -1485,7 +1464,7 @@ __device__ __forceinline__ uint32_t dense_bank_flip(const uint32_t* pm, int r, u
   return g;
 }
 
-template <int W, bool SPEC, bool FAST = false>
+template <int W, bool SPEC>
 __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P, int j0, int j1, DenseCtl<W>& dc,
                                                unsigned long long& records, unsigned long long& removed,
                                                uint32_t count, uint32_t& anom) {
@@ -1535,55 +1514,11 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
         for (int e = 0; e < 16; ++e)
           a[e] = d[b ^ (((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
                         (((e >> 3) & 1) << pm[3]))];
-        if (FAST) {
-          // |v| >= 2^-899 for all 16 points (high words >= kLiveHi): no point
-          // is absent, so dense_bfly_fast's per-point bookkeeping reduces to
-          // constants -- every butterfly records both deltas (16 per stage)
-          // and removes nothing, provided every output stays >= 2^-899 (one
-          // min over the outputs' high words per stage; below it, an exact
-          // zero included, raises anom and the caller redoes the block point
-          // by point).  All 16 zero: nothing to do, nothing to store.
-          constexpr uint32_t kLiveHi = 124u << 20;
-          uint32_t mn = 0xffffffffu, any = 0;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const uint32_t h = (uint32_t)__double2hiint(a[e]) & 0x7fffffffu;
-            mn = min(mn, h);
-            any |= h | (uint32_t)__double2loint(a[e]);
-          }
-          if (!any) continue;
-          if (mn >= kLiveHi) {
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              uint32_t omn = 0xffffffffu;
-#pragma unroll
-              for (int e = 0; e < 16; ++e)
-                if (!((e >> i) & 1)) {
-                  double& x0 = a[e];
-                  double& x1 = a[e | (1 << i)];
-                  const double d1 = __dmul_rn(sn[i], x0), d0 = __dmul_rn(-sn[i], x1);
-                  x0 = __dadd_rn(__dmul_rn(x0, cs[i]), d0);
-                  x1 = __dadd_rn(__dmul_rn(x1, cs[i]), d1);
-                  omn = min(omn, min((uint32_t)__double2hiint(x0) & 0x7fffffffu,
-                                     (uint32_t)__double2hiint(x1) & 0x7fffffffu));
-                }
-              anom |= omn < kLiveHi;
-            }
-            records += 64;
-          } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-              for (int e = 0; e < 16; ++e)
-                if (!((e >> i) & 1)) dense_bfly_t<FAST>(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed, anom);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-              if (!((e >> i) & 1)) dense_bfly_t<FAST>(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed, anom);
-        }
+          for (int e = 0; e < 16; ++e)
+            if (!((e >> i) & 1)) dense_bfly(a[e], a[e | (1 << i)], cs[i], sn[i], -sn[i], records, removed);
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           d[b ^ (((e & 1) << pm[0]) | (((e >> 1) & 1) << pm[1]) | (((e >> 2) & 1) << pm[2]) |
@@ -1612,10 +1547,10 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
         b = ((b >> phi) << (phi + 1)) | (b & ((1u << phi) - 1u));
         b |= dg;
         double a00 = d[b], a10 = d[b ^ m1], a01 = d[b ^ m2], a11 = d[b ^ m1 ^ m2];
-        dense_bfly_t<FAST>(a00, a10, c1, s1, -s1, records, removed, anom);
-        dense_bfly_t<FAST>(a01, a11, c1, s1, -s1, records, removed, anom);
-        dense_bfly_t<FAST>(a00, a01, c2, s2, -s2, records, removed, anom);
-        dense_bfly_t<FAST>(a10, a11, c2, s2, -s2, records, removed, anom);
+        dense_bfly(a00, a10, c1, s1, -s1, records, removed);
+        dense_bfly(a01, a11, c1, s1, -s1, records, removed);
+        dense_bfly(a00, a01, c2, s2, -s2, records, removed);
+        dense_bfly(a10, a11, c2, s2, -s2, records, removed);
         d[b] = a00;
         d[b ^ m1] = a10;
         d[b ^ m2] = a01;
@@ -1648,7 +1583,7 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
           ++removed;
         }
       }
-      dense_bfly_t<FAST && !SPEC>(a, b, cosv, sinv, nsin, records, removed, anom);
+      dense_bfly(a, b, cosv, sinv, nsin, records, removed);
       if (spec) mx = fmax(mx, fmax(fabs(a), fabs(b)));
       d[b0] = a;
       d[b0 ^ (1u << p)] = b;
@@ -1666,12 +1601,142 @@ __device__ __forceinline__ void dense_stages_t(double* d, uint32_t u, uint32_t P
   }
 }
 
+// Bookkeeping-free butterflies (SubGates::fast, DenseCtl::fast).  Live values
+// entering a stage satisfy |v| >= 2^-890 (kFastLive; checked for the group's
+// input and for every stage's outputs) and every |sin|, |cos| >= 2^-100, so a
+// delta is zero exactly when its source point is, and "add the delta if it is
+// nonzero" (term_map.hpp:77-79) equals always adding it.  Each stage then
+// sends one record per live point (counted from the block's 2^R-bit live
+// mask: a point is live after a stage when it or its partner was) and removes
+// nothing, provided every live point still holds a value >= kFastLive after
+// the stage -- one integer min over the high words (sign shifted out) of the
+// live outputs.  A smaller value there, the zero of an exact cancellation
+// included (cos = sin at pi/4 produces them), raises `anom` and the caller
+// redoes the tile point by point (dense_bfly).
+constexpr uint32_t kFastLiveHi = (1023u - 890u) << 20;
+constexpr double kFastLive = 0x1p-890;
+
+// One pass of R stages (radix 2^R): each thread takes the 2^R points the R
+// stage bits span through all R butterfly stages in registers -- per point
+// the same operations in the same order as stage by stage.
+template <int R>
+__device__ __forceinline__ void dense_fast_pass(double* d, uint32_t npts, const uint32_t (&pm)[4],
+                                                const double (&cs0)[4], const double (&sn0)[4], uint32_t& records,
+                                                uint32_t& anom) {
+  constexpr int N = 1 << R;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t q[R];
+  double cs[R], sn[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) q[i] = pm[i];
+#pragma unroll
+  for (int a = 0; a < R - 1; ++a)  // ascending insertion positions
+#pragma unroll
+    for (int b2 = 0; b2 < R - 1 - a; ++b2)
+      if (q[b2] > q[b2 + 1]) {
+        const uint32_t t2 = q[b2];
+        q[b2] = q[b2 + 1];
+        q[b2 + 1] = t2;
+      }
+  const uint32_t g = dense_bank_flip(pm, R, lane);  // see there
+  uint32_t dg = 0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    dg |= ((g >> i) & 1u) << pm[i];
+    cs[i] = cs0[i];
+    sn[i] = ((g >> i) & 1u) ? -sn0[i] : sn0[i];
+  }
+  for (uint32_t t = threadIdx.x; t < (npts >> R); t += kCta) {
+    uint32_t b = t;
+#pragma unroll
+    for (int i = 0; i < R; ++i) b = ((b >> q[i]) << (q[i] + 1)) | (b & ((1u << q[i]) - 1u));
+    b |= dg;
+    double a[N];
+    uint32_t off[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      uint32_t o = 0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) o |= (uint32_t)((e >> i) & 1) << pm[i];
+      off[e] = b ^ o;
+      a[e] = d[off[e]];
+    }
+    uint32_t mask = 0;
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+      if ((uint32_t)__double2hiint(a[e]) << 1) mask |= 1u << e;
+    if (!mask) continue;  // nothing live: nothing to do, nothing to store
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      records += __popc(mask);
+#pragma unroll
+      for (int e = 0; e < N; ++e)
+        if (!((e >> i) & 1)) {
+          double& x0 = a[e];
+          double& x1 = a[e | (1 << i)];
+          const double d1 = __dmul_rn(sn[i], x0), d0 = __dmul_rn(-sn[i], x1);
+          x0 = __dadd_rn(__dmul_rn(x0, cs[i]), d0);
+          x1 = __dadd_rn(__dmul_rn(x1, cs[i]), d1);
+        }
+      // a point is live after the stage when it or its partner was; every
+      // live point must hold a value >= kFastLive (an exact cancellation
+      // leaves a zero there: caught like any other small value)
+      const uint32_t lowhalf = (i == 0 ? 0x5555u : i == 1 ? 0x3333u : i == 2 ? 0x0f0fu : 0x00ffu) & ((1u << N) - 1u);
+      mask |= ((mask & lowhalf) << (1 << i)) | ((mask >> (1 << i)) & lowhalf);
+      uint32_t umin = 0xffffffffu;
+      if (mask == (1u << N) - 1u) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) umin = min(umin, (uint32_t)__double2hiint(a[e]) << 1);
+      } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e)
+          if ((mask >> e) & 1u) umin = min(umin, (uint32_t)__double2hiint(a[e]) << 1);
+      }
+      anom |= umin < 2u * kFastLiveHi;
+    }
+#pragma unroll
+    for (int e = 0; e < N; ++e) d[off[e]] = a[e];
+  }
+  __syncthreads();
+}
+
+// Stages [j0, j1) over a tile of `count` (default 2^u) doubles in shared
+// memory, in ceil(n / 4) passes of near-equal radix.
+template <int W>
+__device__ __forceinline__ void dense_stages_fast(double* d, uint32_t u, uint32_t P, int j0, int j1, DenseCtl<W>& dc,
+                                                  unsigned long long& records, uint32_t count, uint32_t& anom) {
+  const uint32_t npts = count ? count : (1u << u);
+  const int ns = j1 - j0;
+  if (ns <= 0) return;
+  const int np = (ns + 3) >> 2, base = ns / np, extra = ns % np;
+  uint32_t rec = 0;
+  int j = j0;
+  for (int p = 0; p < np; ++p) {
+    const int r = base + (p < extra ? 1 : 0);
+    uint32_t pm[4];
+    double cs[4], sn[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int jj = i < r ? j + i : j;
+      pm[i] = __popc(P & ((1u << dc.sbit[jj]) - 1u));
+      cs[i] = dc.scos[jj];
+      sn[i] = dc.ssin[jj];
+    }
+    if (r == 4) dense_fast_pass<4>(d, npts, pm, cs, sn, rec, anom);
+    else if (r == 3) dense_fast_pass<3>(d, npts, pm, cs, sn, rec, anom);
+    else if (r == 2) dense_fast_pass<2>(d, npts, pm, cs, sn, rec, anom);
+    else dense_fast_pass<1>(d, npts, pm, cs, sn, rec, anom);
+    j += r;
+  }
+  records += rec;
+}
+
 template <int W>
 __device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, int j0, int j1, DenseCtl<W>& dc,
                                              unsigned long long& records, unsigned long long& removed,
                                              uint32_t count, uint32_t& anom, bool fast) {
   if (dc.tpred) dense_stages_t<W, true>(d, u, P, j0, j1, dc, records, removed, count, anom);
-  else if (fast) dense_stages_t<W, false, true>(d, u, P, j0, j1, dc, records, removed, count, anom);
+  else if (fast) dense_stages_fast<W>(d, u, P, j0, j1, dc, records, count, anom);
   else dense_stages_t<W, false>(d, u, P, j0, j1, dc, records, removed, count, anom);
 }
 
@@ -1724,13 +1789,15 @@ __device__ void dense_passes(double* dbuf, double* blk, uint32_t S, DenseCtl<W>&
   }
 }
 
-// Several x classes F_1 < ... < F_K (sorted as planes): one 2^m block each.
-// The group's x order interleaves the blocks; point b of class i goes to
-//   rank(i, b) = b + sum_{j != i} (((b >> t_ij) + [j < i]) << t_ij),
-// t_ij = number of T bits below the highest bit where F_i and F_j differ
-// (above it both agree outside T, so order is decided by the T bits above
-// it, i.e. b >> t_ij, then by F at that bit).  Points are written at their
-// ranks (zeros included), then holes are compacted out in place.
+// Several x classes F_1 < ... < F_K (sorted as planes): one 2^m block each,
+// written class-major -- block i holds class F_i in b (= x) order, at
+// [i 2^m, (i + 1) 2^m) of the group's region (zeros included, then holes are
+// compacted out in place).  The group's x order would interleave the blocks,
+// so the group is marked kFlagUnsorted like the output of a regroup (nothing
+// on the eps0 = 0 pipeline needs x order: the next regroup and the next dense
+// run scatter anyway; consumers that do sort first, EngineImpl::ensure_sorted)
+// plus kFlagMinFirst: the group's smallest x (class F_1 at b = 0, the only
+// place x = 0 can be) still comes first, which is all the readout needs.
 template <int W>
 __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, uint32_t* scan, GroupView<W> g,
                            ArenaView<W> ar, uint32_t gid, uint32_t n, uint64_t src, uint32_t K, uint32_t seq0,
@@ -1744,27 +1811,6 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   const uint32_t S = 1u << m;
   const unsigned long long KS = (unsigned long long)K * S;
   if (KS > kDenseMaxOut) return 0;
-  // rank terms of class i: lvl[i][t] = #{j != i : t_ij = t}, C_i = sum_{j<i} 2^t_ij
-  if (tid < K) {
-    for (int t = 0; t <= m; ++t) tl.lvl[tid][t] = 0;
-    uint32_t mask = 0, c = 0;
-    const Plane<W> fi = tl.sF[tid];
-    for (uint32_t j = 0; j < K; ++j) {
-      if (j == tid) continue;
-      int hw = W - 1;
-      while (hw > 0 && fi.w[hw] == tl.sF[j].w[hw]) --hw;
-      const uint64_t d = fi.w[hw] ^ tl.sF[j].w[hw];
-      const int h = 63 - __clzll((long long)d);
-      uint32_t t = __popcll(T.w[hw] & ((1ull << h) - 1ull));
-      for (int w = 0; w < hw; ++w) t += __popcll(T.w[w]);
-      tl.lvl[tid][t] += 1;
-      mask |= 1u << t;
-      if (j < tid) c += 1u << t;
-    }
-    tl.lmask[tid] = mask;
-    tl.C[tid] = c;
-  }
-  __syncthreads();
   // region: K 2^m output slots, plus a 2^m scratch block for blocks larger
   // than a shared-memory tile
   const bool big = S > kDenseSmem;
@@ -1803,11 +1849,7 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       v = 0.0;
       ++removed;
     }
-    uint32_t r = b + tl.C[i];
-    for (uint32_t mk = tl.lmask[i]; mk; mk &= mk - 1) {
-      const uint32_t t = __ffs(mk) - 1;
-      r += (uint32_t)tl.lvl[i][t] * ((b >> t) << t);
-    }
+    const uint32_t r = (i << m) + b;  // class-major: block i holds class F_i in b order
     Plane<W> x = tl.sF[i];
     const Plane<W> a0 = xt[b & 255u], a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
 #pragma unroll
@@ -1845,9 +1887,9 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
         __syncthreads();
         for (uint32_t i = tid; i < n; i += kCta) {
           const uint64_t code = codes[i];
+          const double v = ar.c[src + i];  // loaded with the code, not after it (one latency per string)
           const uint32_t c = (uint32_t)(code >> 32);
           if (c >= c0 && c < c1) {
-            const double v = ar.c[src + i];
             if (spec && v != 0.0 && fabs(v) <= dc.tin) {
               ++removed;
               continue;
@@ -1861,7 +1903,7 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
         if (!fast || !__syncthreads_or(anom)) break;
         records = rec0;  // a cancellation or an extreme value: redo the batch point by point
       }
-      for (uint32_t e = tid; e < cnt; e += kCta) emit(c0 + e / S, e % S, dbuf[e]);
+      for (uint32_t e = tid; e < cnt; e += kCta) emit(c0 + (e >> m), e & (S - 1u), dbuf[e]);
       __syncthreads();
     }
   } else {
@@ -1873,8 +1915,8 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
         __syncthreads();
         for (uint32_t i = tid; i < n; i += kCta) {
           const uint64_t code = codes[i];
+          const double v = ar.c[src + i];
           if ((uint32_t)(code >> 32) == ci) {
-            const double v = ar.c[src + i];
             if (spec && v != 0.0 && fabs(v) <= dc.tin) {
               ++removed;
               continue;
@@ -1933,7 +1975,7 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     g.cap[gid] = (uint32_t)KS;
     g.gmax[gid] = out ? vmax : 0.0;
     g.gmin[gid] = out ? vmin : __longlong_as_double(0x7ff0000000000000ll);
-    g.flags[gid] = nonfinite;
+    g.flags[gid] = nonfinite | kFlagUnsorted | kFlagMinFirst;
     g.stamp[gid] = seq0 + (uint32_t)dc.klast;
     if (records) {
       atomicAdd(&st->records, records);
@@ -1948,96 +1990,19 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   return 1;
 }
 
-// Returns 1 when the group was applied, 0 when it is not eligible (the
-// caller takes the per-gate path), -1 when its output did not fit the arena
-// (the group is untouched and resumes in the next launch).
+// The group's stage list is in dc (T, m, sbit/sgate/scos/ssin, tpos, klast,
+// fast, F of its first string; spec: tin, strunc): x classes, output tables,
+// then the butterflies and the output (dense_multi for several classes).
+// Returns like dense_group.
 template <int W>
-__device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, uint32_t* scan, GroupView<W> g,
-                           ArenaView<W> ar, const SubGates& gates, const SubGates& gp, uint32_t gid, uint32_t n, uint64_t src, int k0,
+__device__ int dense_apply(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, uint32_t* scan, GroupView<W> g,
+                           ArenaView<W> ar, const SubGates& gates, uint32_t gid, uint32_t n, uint64_t src,
                            const uint32_t* s_touch, uint32_t seq0, unsigned long long cap, DevStats* st,
                            unsigned long long& aff_elems, uint32_t* s_seen) {
   const uint32_t tid = threadIdx.x;
-  // stage list, in parallel: thread k owns gate k (parameters read from the
-  // kernel's parameter block once per gate, not serially per group)
-  __syncthreads();
-  if (tid < W) dc.T.w[tid] = 0;
-  if (tid < kMaxSubGates / 32) {
-    const uint32_t w0 = (uint32_t)k0 >> 5;
-    uint32_t t = tid < w0 ? 0u : s_touch[tid];
-    if (tid == w0) t &= ~0u << (k0 & 31);
-    dc.tw[tid] = t;
-  }
-  __syncthreads();
-  const int k = (int)tid;
-  const bool touch = k < gates.ng && ((dc.tw[k >> 5] >> (k & 31)) & 1u);
-  int wq = 0;
-  uint64_t mq = 0;
-  if (touch) {
-    wq = gp.wq[k];
-    mq = gp.mq[k];
-    atomicOr(reinterpret_cast<unsigned long long*>(&dc.T.w[wq]), (unsigned long long)mq);
-  }
-  __syncthreads();
-  if (touch) {
-    const Plane<W> T = dc.T;
-    uint32_t r = __popcll(T.w[wq] & (mq - 1));
-    for (int w = 0; w < wq; ++w) r += __popcll(T.w[w]);
-    uint32_t j = __popc(dc.tw[k >> 5] & ((1u << (k & 31)) - 1u));
-    for (int w = 0; w < (k >> 5); ++w) j += __popc(dc.tw[w]);
-    if (j < kMaxSubGates) {
-      dc.sbit[j] = (uint8_t)r;
-      dc.sgate[j] = (uint8_t)k;
-      dc.scos[j] = gp.cosv[k];
-      dc.ssin[j] = gp.sinv[k];
-    }
-  }
-  if (tid == 0) {
-    int m = 0, klast = -1;
-    for (int w = 0; w < kMaxSubGates / 32; ++w) {
-      m += __popc(dc.tw[w]);
-      if (dc.tw[w]) klast = 32 * w + 31 - __clz(dc.tw[w]);
-    }
-    dc.m = m;
-    dc.klast = klast;
-    Plane<W> F = load_plane<W>(ar.x, src);
-#pragma unroll
-    for (int w = 0; w < W; ++w) F.w[w] &= ~dc.T.w[w];
-    dc.F = F;
-    uint32_t j = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w)
-      for (uint64_t t = dc.T.w[w]; t && j < 32; t &= t - 1, ++j) dc.tpos[j] = (uint8_t)(64 * w + __ffsll((long long)t) - 1);
-  }
-  __syncthreads();
   const int m = dc.m;
-  if (m == 0 || m > kDenseMaxLog) return 0;
-  // bookkeeping-free butterflies (dense_bfly_fast) when the run's angles and
-  // the group's values are far from underflow; anything else is caught there
-  if (tid == 0) dc.fast = (!dc.tpred && gates.fast && g.gmin[gid] >= 0x1p-899) ? 1u : 0u;
   const Plane<W> T = dc.T;
   const bool spec = dc.tpred != nullptr;
-  if (spec) {
-    // truncation windows: after stage s, the gates from its own to the next
-    // stage's (exclusive); before stage 0, the gates from k0 to its
-    if (tid < (uint32_t)m) {
-      const int k = dc.sgate[tid], next = (int)tid + 1 < m ? dc.sgate[tid + 1] : dc.ng;
-      double t = -1.0;
-      for (int jj = k; jj < next; ++jj) t = fmax(t, dc.tpred[jj]);
-      dc.strunc[tid] = t;
-    }
-    if (tid == 0) {
-      double t = -1.0;
-      const int first = dc.sgate[0];
-      const double M = g.gmax[gid];  // the group held its values through those gates
-      for (int jj = k0; jj < first; ++jj) {
-        t = fmax(t, dc.tpred[jj]);
-        if (M > 0.0) atomicMax(&dc.smax[jj], (unsigned long long)__double_as_longlong(M));
-        if (M <= dc.tpred[jj]) break;  // emptied: later gates see nothing (t already covers M)
-      }
-      dc.tin = t;
-    }
-    __syncthreads();
-  }
   DenseTail<W>& tl = *reinterpret_cast<DenseTail<W>*>(dbuf + kDenseSmem);
   uint32_t K = 1;
   Plane<W> F = dc.F;  // one string: one class, its x outside T
@@ -2326,6 +2291,99 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   return 1;
 }
 
+// Returns 1 when the group was applied, 0 when it is not eligible (the
+// caller takes the per-gate path), -1 when its output did not fit the arena
+// (the group is untouched and resumes in the next launch).
+template <int W>
+__device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, uint32_t* scan, GroupView<W> g,
+                           ArenaView<W> ar, const SubGates& gates, const SubGates& gp, uint32_t gid, uint32_t n, uint64_t src, int k0,
+                           const uint32_t* s_touch, uint32_t seq0, unsigned long long cap, DevStats* st,
+                           unsigned long long& aff_elems, uint32_t* s_seen) {
+  const uint32_t tid = threadIdx.x;
+  // stage list, in parallel: thread k owns gate k (parameters read from the
+  // kernel's parameter block once per gate, not serially per group)
+  __syncthreads();
+  if (tid < W) dc.T.w[tid] = 0;
+  if (tid < kMaxSubGates / 32) {
+    const uint32_t w0 = (uint32_t)k0 >> 5;
+    uint32_t t = tid < w0 ? 0u : s_touch[tid];
+    if (tid == w0) t &= ~0u << (k0 & 31);
+    dc.tw[tid] = t;
+  }
+  __syncthreads();
+  const int k = (int)tid;
+  const bool touch = k < gates.ng && ((dc.tw[k >> 5] >> (k & 31)) & 1u);
+  int wq = 0;
+  uint64_t mq = 0;
+  if (touch) {
+    wq = gp.wq[k];
+    mq = gp.mq[k];
+    atomicOr(reinterpret_cast<unsigned long long*>(&dc.T.w[wq]), (unsigned long long)mq);
+  }
+  __syncthreads();
+  if (touch) {
+    const Plane<W> T = dc.T;
+    uint32_t r = __popcll(T.w[wq] & (mq - 1));
+    for (int w = 0; w < wq; ++w) r += __popcll(T.w[w]);
+    uint32_t j = __popc(dc.tw[k >> 5] & ((1u << (k & 31)) - 1u));
+    for (int w = 0; w < (k >> 5); ++w) j += __popc(dc.tw[w]);
+    if (j < kMaxSubGates) {
+      dc.sbit[j] = (uint8_t)r;
+      dc.sgate[j] = (uint8_t)k;
+      dc.scos[j] = gp.cosv[k];
+      dc.ssin[j] = gp.sinv[k];
+    }
+  }
+  if (tid == 0) {
+    int m = 0, klast = -1;
+    for (int w = 0; w < kMaxSubGates / 32; ++w) {
+      m += __popc(dc.tw[w]);
+      if (dc.tw[w]) klast = 32 * w + 31 - __clz(dc.tw[w]);
+    }
+    dc.m = m;
+    dc.klast = klast;
+    Plane<W> F = load_plane<W>(ar.x, src);
+#pragma unroll
+    for (int w = 0; w < W; ++w) F.w[w] &= ~dc.T.w[w];
+    dc.F = F;
+    uint32_t j = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      for (uint64_t t = dc.T.w[w]; t && j < 32; t &= t - 1, ++j) dc.tpos[j] = (uint8_t)(64 * w + __ffsll((long long)t) - 1);
+  }
+  __syncthreads();
+  const int m = dc.m;
+  if (m == 0 || m > kDenseMaxLog) return 0;
+  // bookkeeping-free butterflies (dense_bfly_fast) when the run's angles and
+  // the group's values are far from underflow; anything else is caught there
+  if (tid == 0) dc.fast = (!dc.tpred && gates.fast && g.gmin[gid] >= kFastLive) ? 1u : 0u;
+  const Plane<W> T = dc.T;
+  const bool spec = dc.tpred != nullptr;
+  if (spec) {
+    // truncation windows: after stage s, the gates from its own to the next
+    // stage's (exclusive); before stage 0, the gates from k0 to its
+    if (tid < (uint32_t)m) {
+      const int k = dc.sgate[tid], next = (int)tid + 1 < m ? dc.sgate[tid + 1] : dc.ng;
+      double t = -1.0;
+      for (int jj = k; jj < next; ++jj) t = fmax(t, dc.tpred[jj]);
+      dc.strunc[tid] = t;
+    }
+    if (tid == 0) {
+      double t = -1.0;
+      const int first = dc.sgate[0];
+      const double M = g.gmax[gid];  // the group held its values through those gates
+      for (int jj = k0; jj < first; ++jj) {
+        t = fmax(t, dc.tpred[jj]);
+        if (M > 0.0) atomicMax(&dc.smax[jj], (unsigned long long)__double_as_longlong(M));
+        if (M <= dc.tpred[jj]) break;  // emptied: later gates see nothing (t already covers M)
+      }
+      dc.tin = t;
+    }
+    __syncthreads();
+  }
+  return dense_apply<W>(dbuf, dc, gs, scan, g, ar, gates, gid, n, src, s_touch, seq0, cap, st, aff_elems, s_seen);
+}
+
 // Modes:
 //  tpred == nullptr  (epsilon0 = 0, or per-layer cadence): only groups some
 //    gate touches; no truncation inside the run; resumable via stamps.
@@ -2340,7 +2398,8 @@ template <int W>
 __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
                                                            int keep_zeros, unsigned int* work, const double* tpred,
                                                            unsigned long long* gmax_out, DevStats* st,
-                                                           const uint8_t* spec_done = nullptr) {
+                                                           const uint8_t* spec_done = nullptr,
+                                                           const uint32_t* list = nullptr) {
   __shared__ uint32_t s_touch[kMaxSubGates / 32];
   __shared__ uint32_t s_seen[kMaxSubGates / 32];  // gates of the run that sent a record (batches_sent)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2350,7 +2409,9 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
   if (engine_failed(st)) return;
   if (tid < kMaxSubGates / 32) s_seen[tid] = 0;
   const bool spec = tpred != nullptr;
-  const uint32_t G = *(volatile const unsigned int*)&st->G_dev;
+  // list != nullptr: only the groups k_dense_sublayer left behind (pp_dense.cuh)
+  const uint32_t G = list ? *(volatile const unsigned int*)&st->left_n : *(volatile const unsigned int*)&st->G_dev;
+  if (G == 0) return;
   const unsigned long long cap = *(volatile const unsigned long long*)&st->arena_cap;
   const uint32_t seq0 = (uint32_t)(*(volatile const unsigned long long*)&st->seq_base);
   __shared__ unsigned long long dst_s;
@@ -2420,7 +2481,7 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
     const bool lpt = !spec && gates.dense;
     const uint32_t idx = s_gid;
     if (idx >= (lpt ? 2 * G : G) || failed) break;
-    const uint32_t gid = idx < G ? idx : idx - G;
+    const uint32_t gid = list ? list[idx] : (idx < G ? idx : idx - G);
     Plane<W> z;
 #pragma unroll
     for (int k = 0; k < W; ++k) z.w[k] = g.z[k][gid];
@@ -3422,7 +3483,7 @@ __global__ void __launch_bounds__(kCta) k_readout(GroupView<W> g, uint32_t Gp, A
       nf = fl & 1u;
     }
     uint64_t hit = ~0ull;
-    if (fl & kFlagUnsorted) {
+    if ((fl & (kFlagUnsorted | kFlagMinFirst)) == kFlagUnsorted) {
       for (uint32_t j0 = 0; j0 < n; j0 += 32) {
         const bool z = j0 + lane < n && plane_zero<W>(load_plane<W>(ar.x, o + j0 + lane));
         const uint32_t b = __ballot_sync(0xffffffffu, z);
@@ -3483,7 +3544,7 @@ __global__ void k_diag(GroupView<W> g, uint32_t G, ArenaView<W> ar, uint64_t* ou
   if (n == 0) return;
   const uint64_t o = g.off[i];
   uint64_t hit = ~0ull;
-  if (g.flags[i] & kFlagUnsorted) {
+  if ((g.flags[i] & (kFlagUnsorted | kFlagMinFirst)) == kFlagUnsorted) {
     for (uint32_t j0 = 0; j0 < n; j0 += 32) {
       const bool z = j0 + lane < n && plane_zero<W>(load_plane<W>(ar.x, o + j0 + lane));
       const uint32_t b = __ballot_sync(0xffffffffu, z);

@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(kCta) k_sort_small(GroupView<W> g, ArenaView<W
     __syncthreads();
     const uint32_t gi = c0 + tid;
     const uint32_t nt =
-        (tid < chunk && gi < G && (!only_unsorted || (g.flags[gi] & kFlagUnsorted))) ? g.cnt[gi] : 0u;
+        (tid < chunk && gi < G && sort_wanted(g.flags[gi], only_unsorted)) ? g.cnt[gi] : 0u;
     const bool small = nt > 0 && nt <= kSortPackGroup;
     const bool single = nt > kSortPackGroup && nt <= kSortSmall;
     uint32_t nsmall, tsz, nsingle;
@@ -1121,7 +1121,7 @@ __global__ void __launch_bounds__(kCta) k_sort_big(GroupView<W> g, ArenaView<W> 
   __syncthreads();
   const uint32_t n = g.cnt[gid];
   if (n <= kSortSmall) continue;
-  if (only_unsorted && !(g.flags[gid] & kFlagUnsorted)) continue;
+  if (!sort_wanted(g.flags[gid], only_unsorted)) continue;
   const uint64_t off = g.off[gid];
   __shared__ unsigned long long so_s;
   if (threadIdx.x == 0) so_s = atomicAdd(&st->scratch_bump, (unsigned long long)n);

@@ -281,9 +281,11 @@ def test_deferred_truncation_is_exact(pp, O, monkeypatch, mode):
     run_both(pp, O, 127, list(circ.layers), init, 3e-4, "gate")
 
 
-@pytest.mark.parametrize("mode", ["per_gate", "dense_tight", "unsorted_fallback"])
+@pytest.mark.parametrize("mode", ["per_gate", "dense_tight", "unsorted_fallback", "dense_in_branch_kernel",
+                                  "dense_careful", "dense_kernel_tight_maxk"])
 def test_sublayer_paths_match_oracle(pp, O, monkeypatch, mode):
-    """epsilon0 = 0 Rx runs: the dense sublayer (default, dense_group) and
+    """epsilon0 = 0 Rx runs: the dense sublayer (default: k_dense_sublayer +
+    dense_apply, class-major multi-class output) and
     the per-gate segment/stream path (PP_NO_DENSE) both equal the oracle bit
     for bit, also when the arena overflows mid-run and resumes
     (PP_TIGHT_ARENA: dense blocks in global memory and in shared memory), and
@@ -291,6 +293,17 @@ def test_sublayer_paths_match_oracle(pp, O, monkeypatch, mode):
     if mode == "per_gate":
         monkeypatch.setenv("PP_NO_DENSE", "1")
     elif mode == "dense_tight":
+        monkeypatch.setenv("PP_TIGHT_ARENA", "1")
+    elif mode == "dense_in_branch_kernel":
+        # the dense path inside k_branch_sublayer instead of k_dense_sublayer
+        monkeypatch.setenv("PP_NO_DENSE_KERNEL", "1")
+    elif mode == "dense_careful":
+        # point-by-point butterflies (dense_bfly) instead of the bookkeeping-free passes
+        monkeypatch.setenv("PP_DENSE_CAREFUL", "1")
+    elif mode == "dense_kernel_tight_maxk":
+        # k_dense_sublayer leaves groups of more than 2 classes to the per-gate
+        # pass behind it, with arena overflows and resumes on top
+        monkeypatch.setenv("PP_DENSE_MAXK", "2")
         monkeypatch.setenv("PP_TIGHT_ARENA", "1")
     else:
         # multi-class groups leave the dense path after a regroup that skipped

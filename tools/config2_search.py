@@ -48,6 +48,7 @@ def run(k, eps):
         peak = max(peak, r["term_count"])
         rows.append({"t": t, "Z62": r["observable"], "terms": r["term_count"], "removed": r["removed"],
                      "records": r["records_sent"], "seconds": dt})
+        print(f"k={k} eps0={eps:.3e} t={t} terms={r['term_count']} {dt:.2f}s", file=sys.stderr, flush=True)
     return {"k": k, "epsilon0": eps, "peak": peak, "rows": rows, "seconds": time.perf_counter() - t_all}
 
 
