@@ -1844,6 +1844,7 @@ class EngineImpl final : public EngineBase {
   // cap strings of bump space, plus (speculative eps0 > 0 runs) the per-CTA
   // scratch tail of k_branch_sublayer (kSpecScratch)
   void ensure_arena(int i, uint64_t cap) {
+    cap = (cap + 1) & ~1ull;  // even plane strides: every plane starts 16-byte aligned (128-bit stores)
     if (arena_[i].cap >= cap) return;
     arena_[i].buf.release();
     arena_[i].cap = arena_[i].stride = 0;

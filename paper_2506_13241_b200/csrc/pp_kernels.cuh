@@ -1349,6 +1349,7 @@ struct DenseTail {
   Plane<W> hF[kDenseSlots];             //   its class F
   uint8_t hcls[kDenseSlots];            //   its class index (ascending F)
   uint16_t used[kDenseSlots];           // occupied slots, compacted
+  uint32_t ccnt[kDenseMaxK + 1];        // strings per class, then class start offsets
   Plane<W> sF[kDenseMaxK];              // classes in ascending order
 };
 
@@ -1811,14 +1812,16 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   const uint32_t S = 1u << m;
   const unsigned long long KS = (unsigned long long)K * S;
   if (KS > kDenseMaxOut) return 0;
-  // region: K 2^m output slots, plus a 2^m scratch block for blocks larger
-  // than a shared-memory tile
+  // region: K 2^m output slots (from an even offset: the output is written
+  // two points per 128-bit store), a 2^m scratch block for blocks larger than
+  // a shared-memory tile, and the strings' (class, point) codes: unsorted
+  // with their rank inside the class, then sorted by class with the values
   const bool big = S > kDenseSmem;
-  // outputs, the big-block scratch, and the strings' (class, point) codes
-  const unsigned long long need = KS + (big ? S : 0) + n;
+  const unsigned long long Sx = big ? S : 0;
+  const unsigned long long need = KS + Sx + 2ull * n + 1;
   if (tid == 0) {
     const unsigned long long d = atomicAdd(&st->bump, need);
-    dc.dst = d;
+    dc.dst = (d + 1) & ~1ull;
     dc.fail = d + need > cap;
     if (dc.fail) {
       atomicOr(&st->err_arena, 1u);
@@ -1826,36 +1829,17 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     }
     dc.zeros = 0;
   }
+  if (tid < K) tl.ccnt[tid] = 0;
   __syncthreads();
   if (dc.fail) return -1;
   const uint64_t dst = dc.dst;
   unsigned long long records = 0, removed = 0;
   double vmax = 0.0, vmin = __longlong_as_double(0x7ff0000000000000ll), vall = 0.0;
   uint32_t nonfinite = 0, zeros = 0;
-  // class of a string: its slot in the class hash set
-  auto class_of = [&](const Plane<W>& x) -> uint32_t {
-    Plane<W> f = x;
-#pragma unroll
-    for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
-    const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
-    uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
-    while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
-    return tl.hcls[h];
-  };
-  // point (i, b) -> its rank and x; value written there
   const bool spec = dc.tpred != nullptr;
-  auto emit = [&](uint32_t i, uint32_t b, double v) {
-    if (spec && v != 0.0 && fabs(v) <= dc.strunc[m - 1]) {  // the last window's truncation
-      v = 0.0;
-      ++removed;
-    }
-    const uint32_t r = (i << m) + b;  // class-major: block i holds class F_i in b order
-    Plane<W> x = tl.sF[i];
-    const Plane<W> a0 = xt[b & 255u], a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
-#pragma unroll
-    for (int w = 0; w < W; ++w) x.w[w] |= a0.w[w] | a1.w[w] | a2.w[w];
-    store_plane<W>(ar.x, dst + r, x);
-    ar.c[dst + r] = v;
+  // points (i, b) and (i, b + 1), b even -> [dst + i 2^m + b, + 2) as one
+  // 128-bit store per plane word and one for the coefficients
+  auto note = [&](double v) {
     if (v == 0.0) {
       ++zeros;
     } else {
@@ -1865,15 +1849,69 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       vmin = fmin(vmin, av);
     }
   };
-  // each string's (class, point) once: packed into the output region's x
-  // plane, which the emits overwrite only after the last batch has read it
-  // (rank(i, b) >= the string's position cannot be guaranteed, so the codes
-  // live past the output: [dst + KS, dst + KS + n) of the x plane -- the
-  // region reserves them)
-  uint64_t* codes = ar.x[0] + dst + KS;
+  auto emit2 = [&](uint32_t i, uint32_t b, double v0, double v1) {
+    if (spec) {  // the last window's truncation
+      if (v0 != 0.0 && fabs(v0) <= dc.strunc[m - 1]) {
+        v0 = 0.0;
+        ++removed;
+      }
+      if (v1 != 0.0 && fabs(v1) <= dc.strunc[m - 1]) {
+        v1 = 0.0;
+        ++removed;
+      }
+    }
+    const uint64_t r = dst + ((uint64_t)i << m) + b;  // class-major: block i holds class F_i in b order
+    Plane<W> hi = tl.sF[i];
+    const Plane<W> a1 = xt[256 + ((b >> 8) & 255u)], a2 = xt[512 + (b >> 16)];
+    const Plane<W> l0 = xt[b & 255u], l1 = xt[(b & 255u) + 1u];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      hi.w[w] |= a1.w[w] | a2.w[w];
+      *reinterpret_cast<ulonglong2*>(ar.x[w] + r) = make_ulonglong2(hi.w[w] | l0.w[w], hi.w[w] | l1.w[w]);
+    }
+    *reinterpret_cast<double2*>(ar.c + r) = make_double2(v0, v1);
+    note(v0);
+    note(v1);
+  };
+  // each string's class (its slot in the class hash set; the stored F is
+  // compared here, a fingerprint collision sends the group to the per-gate
+  // path), point and rank inside its class, once
+  uint64_t* codes = ar.x[0] + dst + KS;        // class << 56 | rank << 24 | point
+  uint64_t* scodes = codes + n;                // sorted by class: class << 32 | point
+  double* svals = ar.c + dst + KS + Sx + n;    //   and the values
+  {
+    bool bad = false;
+    for (uint32_t i = tid; i < n; i += kCta) {
+      const Plane<W> x = load_plane<W>(ar.x, src + i);
+      Plane<W> f = x;
+#pragma unroll
+      for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+      const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+      uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+      while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
+      bad |= !plane_eq<W>(tl.hF[h], f);
+      const uint32_t c = tl.hcls[h];
+      const uint32_t rk = atomicAdd(&tl.ccnt[c], 1u);
+      codes[i] = ((uint64_t)c << 56) | ((uint64_t)rk << 24) | dense_pext<W>(x, T);
+    }
+    if (__syncthreads_or(bad)) return 0;  // (the region is given up)
+  }
+  {  // class start offsets
+    uint32_t tot;
+    const uint32_t c = tid < K ? tl.ccnt[tid] : 0u;
+    const uint32_t o = block_excl_scan(c, scan, &tot);
+    __syncthreads();
+    if (tid < K) tl.ccnt[tid] = o;
+    if (tid == 0) tl.ccnt[K] = n;
+    __syncthreads();
+  }
   for (uint32_t i = tid; i < n; i += kCta) {
-    const Plane<W> x = load_plane<W>(ar.x, src + i);
-    codes[i] = ((uint64_t)class_of(x) << 32) | dense_pext<W>(x, T);
+    const uint64_t code = codes[i];
+    const double v = ar.c[src + i];
+    const uint32_t c = (uint32_t)(code >> 56);
+    const uint32_t pos = tl.ccnt[c] + (uint32_t)((code >> 24) & 0xffffffffu);
+    scodes[pos] = ((uint64_t)c << 32) | (code & 0xffffffu);
+    svals[pos] = v;
   }
   __syncthreads();
   if (!big) {
@@ -1881,21 +1919,19 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     const uint32_t per = kDenseSmem / S;
     for (uint32_t c0 = 0; c0 < K; c0 += per) {
       const uint32_t c1 = min(K, c0 + per), cnt = (c1 - c0) * S;
+      const uint32_t j0 = tl.ccnt[c0], j1 = tl.ccnt[c1];
       const unsigned long long rec0 = records;
       for (bool fast = dc.fast != 0;; fast = false) {
-        for (uint32_t e = tid; e < cnt; e += kCta) dbuf[e] = 0.0;
+        for (uint32_t e = 2 * tid; e < cnt; e += 2 * kCta) *reinterpret_cast<double2*>(dbuf + e) = make_double2(0.0, 0.0);
         __syncthreads();
-        for (uint32_t i = tid; i < n; i += kCta) {
-          const uint64_t code = codes[i];
-          const double v = ar.c[src + i];  // loaded with the code, not after it (one latency per string)
-          const uint32_t c = (uint32_t)(code >> 32);
-          if (c >= c0 && c < c1) {
-            if (spec && v != 0.0 && fabs(v) <= dc.tin) {
-              ++removed;
-              continue;
-            }
-            dbuf[(c - c0) * S + (uint32_t)code] = v;
+        for (uint32_t j = j0 + tid; j < j1; j += kCta) {
+          const uint64_t code = scodes[j];
+          const double v = svals[j];
+          if (spec && v != 0.0 && fabs(v) <= dc.tin) {
+            ++removed;
+            continue;
           }
+          dbuf[((uint32_t)(code >> 32) - c0) * S + (uint32_t)code] = v;
         }
         __syncthreads();
         uint32_t anom = 0;
@@ -1903,26 +1939,28 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
         if (!fast || !__syncthreads_or(anom)) break;
         records = rec0;  // a cancellation or an extreme value: redo the batch point by point
       }
-      for (uint32_t e = tid; e < cnt; e += kCta) emit(c0 + (e >> m), e & (S - 1u), dbuf[e]);
+      for (uint32_t e = 2 * tid; e < cnt; e += 2 * kCta) {
+        const double2 v = *reinterpret_cast<const double2*>(dbuf + e);
+        emit2(c0 + (e >> m), e & (S - 1u), v.x, v.y);
+      }
       __syncthreads();
     }
   } else {
     double* blk = ar.c + dst + KS;  // scratch block (coefficient plane past the output)
     for (uint32_t ci = 0; ci < K; ++ci) {
+      const uint32_t j0 = tl.ccnt[ci], j1 = tl.ccnt[ci + 1];
       const unsigned long long rec0 = records;
       for (bool fast = dc.fast != 0;; fast = false) {
-        for (uint32_t e = tid; e < S; e += kCta) blk[e] = 0.0;
+        for (uint32_t e = 2 * tid; e < S; e += 2 * kCta) *reinterpret_cast<double2*>(blk + e) = make_double2(0.0, 0.0);
         __syncthreads();
-        for (uint32_t i = tid; i < n; i += kCta) {
-          const uint64_t code = codes[i];
-          const double v = ar.c[src + i];
-          if ((uint32_t)(code >> 32) == ci) {
-            if (spec && v != 0.0 && fabs(v) <= dc.tin) {
-              ++removed;
-              continue;
-            }
-            blk[(uint32_t)code] = v;
+        for (uint32_t j = j0 + tid; j < j1; j += kCta) {
+          const uint64_t code = scodes[j];
+          const double v = svals[j];
+          if (spec && v != 0.0 && fabs(v) <= dc.tin) {
+            ++removed;
+            continue;
           }
+          blk[(uint32_t)code] = v;
         }
         __syncthreads();
         uint32_t anom = 0;
@@ -1930,7 +1968,10 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
         if (!fast || !__syncthreads_or(anom)) break;
         records = rec0;
       }
-      for (uint32_t e = tid; e < S; e += kCta) emit(ci, e, blk[e]);
+      for (uint32_t e = 2 * tid; e < S; e += 2 * kCta) {
+        const double2 v = *reinterpret_cast<const double2*>(blk + e);
+        emit2(ci, e, v.x, v.y);
+      }
       __syncthreads();
     }
   }
@@ -2030,16 +2071,8 @@ __device__ int dense_apply(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       }
     }
     __syncthreads();
-    // verify (every string's F equals its slot's), count the classes
-    for (uint32_t i = tid; i < n && ok; i += kCta) {
-      Plane<W> f = load_plane<W>(ar.x, src + i);
-  #pragma unroll
-      for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
-      const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
-      uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
-      while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
-      ok = plane_eq<W>(tl.hF[h], f);
-    }
+    // count the classes (dense_multi compares every string's F with its
+    // slot's when it codes the strings; one class: here)
     static_assert(kDenseSlots == 2 * kCta, "two hash slots per thread");
     const bool u0 = tl.hfp[2 * tid] != 0ull, u1 = tl.hfp[2 * tid + 1] != 0ull;
     if (!__syncthreads_and(ok)) return 0;
@@ -2049,6 +2082,18 @@ __device__ int dense_apply(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       if (u1) tl.used[pos + u0] = (uint16_t)(2 * tid + 1);
     }
     if (K > kDenseMaxK || K > (uint32_t)gates.maxk) return 0;
+    if (K == 1) {
+      for (uint32_t i = tid; i < n && ok; i += kCta) {
+        Plane<W> f = load_plane<W>(ar.x, src + i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+        const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+        uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+        while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
+        ok = plane_eq<W>(tl.hF[h], f);
+      }
+      if (!__syncthreads_and(ok)) return 0;
+    }
     __syncthreads();
     // classes in ascending F order; class index per slot
     for (uint32_t c = tid; c < K; c += kCta) {
