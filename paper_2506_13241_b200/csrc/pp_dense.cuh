@@ -42,7 +42,7 @@ constexpr size_t dense_smem_bytes() {
 }
 
 template <int W>
-__global__ void __launch_bounds__(kCta, 2) k_dense_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
+__global__ void __launch_bounds__(kCta, PP_DENSE_CTAS) k_dense_sublayer(GroupView<W> g, ArenaView<W> ar, const SubGates gates,
                                                           unsigned int* work, DevStats* st, uint32_t* left) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_touch[kMaxSubGates / 32];

@@ -1,4 +1,13 @@
 // pp_kernels.cuh -- sm_100a kernels of the Pauli-propagation hot path.
+#ifndef PP_DENSE_LOG
+#define PP_DENSE_LOG 13
+#endif
+#ifndef PP_DENSE_RADIX
+#define PP_DENSE_RADIX 4
+#endif
+#ifndef PP_DENSE_CTAS
+#define PP_DENSE_CTAS 2
+#endif
 //
 // Store layout: the operator is a set of
 // z-groups.  Every string of a group shares its z-plane, which is stored
@@ -1307,6 +1316,47 @@ __device__ __forceinline__ void reduce_group_stats(GroupStatsSmem& r, double& vm
   __syncthreads();
 }
 
+// The same reduction with the result valid in thread 0 only: one barrier.
+// (The caller's next writes to `r` come after further barriers.)
+__device__ __forceinline__ void reduce_group_stats_t0(GroupStatsSmem& r, double& vmax, double& vmin, double& vall,
+                                                      uint32_t& nonfinite, unsigned long long& records,
+                                                      unsigned long long& removed) {
+  const unsigned long long bmax = warp_max_bits((unsigned long long)__double_as_longlong(vmax));
+  const unsigned long long bmin = warp_min_bits((unsigned long long)__double_as_longlong(vmin));
+  const unsigned long long ball = warp_max_bits((unsigned long long)__double_as_longlong(vall));
+  const uint32_t rec = __reduce_add_sync(0xffffffffu, (uint32_t)records);
+  const uint32_t rem = __reduce_add_sync(0xffffffffu, (uint32_t)removed);
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    r.mx[warp] = __longlong_as_double((long long)bmax);
+    r.mn[warp] = __longlong_as_double((long long)bmin);
+    r.all[warp] = __longlong_as_double((long long)ball);
+    r.rec[warp] = rec;
+    r.rem[warp] = rem;
+    r.nf[warp] = nonfinite;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = r.mx[0], b = r.mn[0], c = r.all[0];
+    unsigned long long d = r.rec[0], e = r.rem[0];
+    uint32_t f = r.nf[0];
+    for (uint32_t w = 1; w < kWarps; ++w) {
+      a = fmax(a, r.mx[w]);
+      b = fmin(b, r.mn[w]);
+      c = fmax(c, r.all[w]);
+      d += r.rec[w];
+      e += r.rem[w];
+      f |= r.nf[w];
+    }
+    vmax = a;
+    vmin = b;
+    vall = c;
+    records = d;
+    removed = e;
+    nonfinite = f;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Dense sublayer path (zeros dropped, distinct qubits, one x-class per group).
@@ -1333,7 +1383,7 @@ __device__ __forceinline__ void reduce_group_stats(GroupStatsSmem& r, double& vm
 // kDenseSmemLog stages at a time (each pass: the cosets of those stages'
 // bits, one shared-memory tile each).
 // ---------------------------------------------------------------------------
-constexpr uint32_t kDenseSmemLog = 13;
+constexpr uint32_t kDenseSmemLog = PP_DENSE_LOG;
 constexpr uint32_t kDenseSmem = 1u << kDenseSmemLog;  // doubles of the dynamic buffer
 constexpr int kDenseMaxLog = 24;                      // larger blocks take the per-gate path
 constexpr uint32_t kDenseMaxK = 256;                  // x classes per group on the dense path
@@ -1709,7 +1759,7 @@ __device__ __forceinline__ void dense_stages_fast(double* d, uint32_t u, uint32_
   const uint32_t npts = count ? count : (1u << u);
   const int ns = j1 - j0;
   if (ns <= 0) return;
-  const int np = (ns + 3) >> 2, base = ns / np, extra = ns % np;
+  const int np = (ns + PP_DENSE_RADIX - 1) / PP_DENSE_RADIX, base = ns / np, extra = ns % np;
   uint32_t rec = 0;
   int j = j0;
   for (int p = 0; p < np; ++p) {
@@ -1817,8 +1867,9 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   // a shared-memory tile, and the strings' (class, point) codes: unsorted
   // with their rank inside the class, then sorted by class with the values
   const bool big = S > kDenseSmem;
+  const bool one_tile = KS <= kDenseSmem;  // every class block in one shared-memory tile: no codes, no sort
   const unsigned long long Sx = big ? S : 0;
-  const unsigned long long need = KS + Sx + 2ull * n + 1;
+  const unsigned long long need = KS + Sx + (one_tile ? 0ull : 2ull * n) + 1;
   if (tid == 0) {
     const unsigned long long d = atomicAdd(&st->bump, need);
     dc.dst = (d + 1) & ~1ull;
@@ -1879,6 +1930,41 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   uint64_t* codes = ar.x[0] + dst + KS;        // class << 56 | rank << 24 | point
   uint64_t* scodes = codes + n;                // sorted by class: class << 32 | point
   double* svals = ar.c + dst + KS + Sx + n;    //   and the values
+  if (one_tile) {
+    // the usual case: strings go straight to their points of the tile
+    const uint32_t cnt = (uint32_t)KS;
+    const unsigned long long rec0 = records;
+    for (bool fast = dc.fast != 0;; fast = false) {
+      for (uint32_t e = 2 * tid; e < cnt; e += 2 * kCta) *reinterpret_cast<double2*>(dbuf + e) = make_double2(0.0, 0.0);
+      __syncthreads();
+      bool bad = false;
+      for (uint32_t i = tid; i < n; i += kCta) {
+        const Plane<W> x = load_plane<W>(ar.x, src + i);
+        const double v = ar.c[src + i];
+        Plane<W> f = x;
+#pragma unroll
+        for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+        const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+        uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+        while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
+        bad |= !plane_eq<W>(tl.hF[h], f);
+        if (spec && v != 0.0 && fabs(v) <= dc.tin) {
+          ++removed;
+          continue;
+        }
+        dbuf[((uint32_t)tl.hcls[h] << m) + dense_pext<W>(x, T)] = v;
+      }
+      if (__syncthreads_or(bad)) return 0;  // a fingerprint collision (the region is given up)
+      uint32_t anom = 0;
+      dense_stages<W>(dbuf, (uint32_t)m, S - 1u, 0, m, dc, records, removed, cnt, anom, fast);
+      if (!fast || !__syncthreads_or(anom)) break;
+      records = rec0;  // a cancellation or an extreme value: redo point by point
+    }
+    for (uint32_t e = 2 * tid; e < cnt; e += 2 * kCta) {
+      const double2 v = *reinterpret_cast<const double2*>(dbuf + e);
+      emit2(e >> m, e & (S - 1u), v.x, v.y);
+    }
+  } else {
   {
     bool bad = false;
     for (uint32_t i = tid; i < n; i += kCta) {
@@ -1975,6 +2061,7 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       __syncthreads();
     }
   }
+  }
   // holes (zero points): compact [dst, dst + KS) in place, in rank order
   if (zeros) atomicAdd(&dc.zeros, zeros);
   __syncthreads();
@@ -2009,7 +2096,7 @@ __device__ int dense_multi(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       __syncthreads();
     }
   }
-  reduce_group_stats(gs, vmax, vmin, vall, nonfinite, records, removed);
+  reduce_group_stats_t0(gs, vmax, vmin, vall, nonfinite, records, removed);
   if (tid == 0) {
     g.off[gid] = dst;
     g.cnt[gid] = out;
@@ -2314,7 +2401,7 @@ __device__ int dense_apply(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
       __syncthreads();
     }
   }
-  reduce_group_stats(gs, vmax, vmin, vall, nonfinite, records, removed);
+  reduce_group_stats_t0(gs, vmax, vmin, vall, nonfinite, records, removed);
   if (tid == 0) {
     g.off[gid] = dst;
     g.cnt[gid] = out;
