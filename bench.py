@@ -316,7 +316,7 @@ def run_sharded(args, pp, circ, wl, sg, final_terms, init, rank, world, local):
                     "bytes": "the initial term in, four ledger scalars per layer out"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "k_branch_sublayer (per GPU, summed bytes / max device time)",
+                         "kernel": "k_dense_sublayer + k_branch_sublayer (per GPU, summed bytes / max device time)",
                          "exchange": {"bound": "nvlink", "bytes_per_step_max_rank": moved_bytes,
                                       "ms_per_step_max_rank": ex_ms,
                                       "achieved_GBps": moved_bytes / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None,
@@ -493,7 +493,7 @@ def main():
                      "algorithmic_bytes_per_launch": (pks["branch_bytes"] / pks["branch_launches"]
                                                       if pks["branch_launches"] else None),
                      "traffic_detail": traffic_src,
-                     "kernel": "k_branch_sublayer", "peak_kind": peak_kind,
+                     "kernel": "k_dense_sublayer (+ k_branch_sublayer for the groups it leaves; k_branch_x on per-gate launches)", "peak_kind": peak_kind,
                      "bytes_model": "(strings read + strings written) x (8W+8) B per launch; the dense "
                                     "sublayer reads each input string once and writes each output "
                                     "string once per Rx run",
@@ -501,7 +501,7 @@ def main():
                      "branch_share_of_step": pks["branch_ms"] / ms_per_step,
                      "branch_bytes_per_step": pks["branch_bytes"],
                      "branch_launches_per_step": pks["branch_launches"],
-                     "how": "separate untimed pass, CUDA events around each branch launch on the engine stream",
+                     "how": "separate untimed pass, CUDA events around each Rx-run launch (pair) on the engine stream",
                      "streaming_model": {
                          "bytes_per_string_gate": 2 * R,
                          "equivalent_GBps": value * 2 * R / 1e9,

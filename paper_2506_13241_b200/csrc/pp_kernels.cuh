@@ -1400,6 +1400,7 @@ struct DenseTail {
   uint8_t hcls[kDenseSlots];            //   its class index (ascending F)
   uint16_t used[kDenseSlots];           // occupied slots, compacted
   uint32_t ccnt[kDenseMaxK + 1];        // strings per class, then class start offsets
+  uint32_t nused;                       // occupied slots
   Plane<W> sF[kDenseMaxK];              // classes in ascending order
 };
 
@@ -1712,11 +1713,23 @@ __device__ __forceinline__ void dense_fast_pass(double* d, uint32_t npts, const 
       off[e] = b ^ o;
       a[e] = d[off[e]];
     }
-    uint32_t mask = 0;
+    // live mask of the block (a live value is >= kFastLive, anything else is
+    // an exact zero): all dead -- nothing to do, nothing to store -- and all
+    // live are the common cases, found with one OR / one min over the block
+    uint32_t orv = 0, imin = 0xffffffffu;
 #pragma unroll
-    for (int e = 0; e < N; ++e)
-      if ((uint32_t)__double2hiint(a[e]) << 1) mask |= 1u << e;
-    if (!mask) continue;  // nothing live: nothing to do, nothing to store
+    for (int e = 0; e < N; ++e) {
+      orv |= (uint32_t)__double2hiint(a[e]);
+      imin = min(imin, (uint32_t)__double2hiint(a[e]) << 1);
+    }
+    if (!(orv << 1)) continue;
+    uint32_t mask = (1u << N) - 1u;
+    if (imin < 2u * kFastLiveHi) {
+      mask = 0;
+#pragma unroll
+      for (int e = 0; e < N; ++e)
+        if ((uint32_t)__double2hiint(a[e]) << 1) mask |= 1u << e;
+    }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       records += __popc(mask);
@@ -2134,66 +2147,6 @@ __device__ int dense_apply(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   DenseTail<W>& tl = *reinterpret_cast<DenseTail<W>*>(dbuf + kDenseSmem);
   uint32_t K = 1;
   Plane<W> F = dc.F;  // one string: one class, its x outside T
-  if (n > 1) {
-    // x classes (the distinct x parts F outside T): a shared-memory hash set
-    // keyed by a fingerprint of F, verified against the stored F afterwards
-    // (a fingerprint collision sends the group to the per-gate path)
-    for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) tl.hfp[sl] = 0ull;
-    __syncthreads();
-    bool ok = true;
-    for (uint32_t i = tid; i < n; i += kCta) {
-      Plane<W> f = load_plane<W>(ar.x, src + i);
-  #pragma unroll
-      for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
-      const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
-      uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
-      for (uint32_t probe = 0;; ++probe, h = (h + 1) & (kDenseSlots - 1)) {
-        if (probe == kDenseSlots) {
-          ok = false;  // more than kDenseSlots classes
-          break;
-        }
-        const unsigned long long old = atomicCAS(&tl.hfp[h], 0ull, fp);
-        if (old == 0ull) tl.hF[h] = f;
-        if (old == 0ull || old == fp) break;
-      }
-    }
-    __syncthreads();
-    // count the classes (dense_multi compares every string's F with its
-    // slot's when it codes the strings; one class: here)
-    static_assert(kDenseSlots == 2 * kCta, "two hash slots per thread");
-    const bool u0 = tl.hfp[2 * tid] != 0ull, u1 = tl.hfp[2 * tid + 1] != 0ull;
-    if (!__syncthreads_and(ok)) return 0;
-    {
-      const uint32_t pos = block_excl_scan((uint32_t)u0 + (uint32_t)u1, scan, &K);
-      if (u0) tl.used[pos] = (uint16_t)(2 * tid);
-      if (u1) tl.used[pos + u0] = (uint16_t)(2 * tid + 1);
-    }
-    if (K > kDenseMaxK || K > (uint32_t)gates.maxk) return 0;
-    if (K == 1) {
-      for (uint32_t i = tid; i < n && ok; i += kCta) {
-        Plane<W> f = load_plane<W>(ar.x, src + i);
-#pragma unroll
-        for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
-        const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
-        uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
-        while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
-        ok = plane_eq<W>(tl.hF[h], f);
-      }
-      if (!__syncthreads_and(ok)) return 0;
-    }
-    __syncthreads();
-    // classes in ascending F order; class index per slot
-    for (uint32_t c = tid; c < K; c += kCta) {
-      const uint32_t sl = tl.used[c];
-      const Plane<W> f = tl.hF[sl];
-      uint32_t r = 0;
-      for (uint32_t j = 0; j < K; ++j) r += plane_lt<W>(tl.hF[tl.used[j]], f);
-      tl.hcls[sl] = (uint8_t)r;
-      tl.sF[r] = f;
-    }
-    __syncthreads();
-    F = tl.sF[0];
-  }
   // b -> x bits outside F, one table per byte of b
   Plane<W>* xt = tl.xt;
   for (uint32_t e = tid; e < (uint32_t)((m + 7) / 8) * 256u; e += kCta) {
@@ -2214,7 +2167,65 @@ __device__ int dense_apply(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
     for (int w = 0; w < W; ++w) z0.w[w] = 0;
     xt[256 * tid] = z0;
   }
-  __syncthreads();
+  if (n > 1) {
+    // x classes (the distinct x parts F outside T): a shared-memory hash set
+    // keyed by a fingerprint of F; the stored F is compared when the strings
+    // are placed (dense_multi; one class: below) -- a fingerprint collision
+    // sends the group to the per-gate path
+    for (uint32_t sl = tid; sl < kDenseSlots; sl += kCta) tl.hfp[sl] = 0ull;
+    if (tid == 0) tl.nused = 0;
+    __syncthreads();
+    bool ok = true;
+    for (uint32_t i = tid; i < n; i += kCta) {
+      Plane<W> f = load_plane<W>(ar.x, src + i);
+  #pragma unroll
+      for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+      const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+      uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+      for (uint32_t probe = 0;; ++probe, h = (h + 1) & (kDenseSlots - 1)) {
+        if (probe == kDenseSlots) {
+          ok = false;  // more than kDenseSlots classes
+          break;
+        }
+        const unsigned long long old = atomicCAS(&tl.hfp[h], 0ull, fp);
+        if (old == 0ull) tl.hF[h] = f;
+        if (old == 0ull || old == fp) break;
+      }
+    }
+    __syncthreads();
+    // the occupied slots, in any order (the classes are ranked by F below)
+    static_assert(kDenseSlots == 2 * kCta, "two hash slots per thread");
+    if (tl.hfp[2 * tid] != 0ull) tl.used[atomicAdd(&tl.nused, 1u)] = (uint16_t)(2 * tid);
+    if (tl.hfp[2 * tid + 1] != 0ull) tl.used[atomicAdd(&tl.nused, 1u)] = (uint16_t)(2 * tid + 1);
+    if (!__syncthreads_and(ok)) return 0;
+    K = tl.nused;
+    if (K > kDenseMaxK || K > (uint32_t)gates.maxk) return 0;
+    if (K == 1) {
+      for (uint32_t i = tid; i < n && ok; i += kCta) {
+        Plane<W> f = load_plane<W>(ar.x, src + i);
+#pragma unroll
+        for (int w = 0; w < W; ++w) f.w[w] &= ~T.w[w];
+        const unsigned long long fp = plane_hash<W>(f, 0x9e3779b97f4a7c15ull) | 1ull;
+        uint32_t h = (uint32_t)(fp >> 40) & (kDenseSlots - 1);
+        while (tl.hfp[h] != fp) h = (h + 1) & (kDenseSlots - 1);
+        ok = plane_eq<W>(tl.hF[h], f);
+      }
+      if (!__syncthreads_and(ok)) return 0;
+    }
+    // classes in ascending F order; class index per slot
+    for (uint32_t c = tid; c < K; c += kCta) {
+      const uint32_t sl = tl.used[c];
+      const Plane<W> f = tl.hF[sl];
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < K; ++j) r += plane_lt<W>(tl.hF[tl.used[j]], f);
+      tl.hcls[sl] = (uint8_t)r;
+      tl.sF[r] = f;
+    }
+    __syncthreads();
+    F = tl.sF[0];
+  } else {
+    __syncthreads();
+  }
   if (K > 1) return dense_multi<W>(dbuf, dc, gs, scan, g, ar, gid, n, src, K, seq0, cap, st, aff_elems, s_touch, s_seen);
   const uint32_t S = 1u << m;
   if (tid == 0) {

@@ -406,6 +406,10 @@ __device__ __forceinline__ unsigned long long z_fingerprint(const Plane<W>& z, u
   return f ? f : 1ull;
 }
 
+// Longest probe sequence before the table counts as too small (at load
+// <= 1/2 sequences stay far below this).
+constexpr uint32_t kMaxProbe = 4096;
+
 template <int W, class P>
 __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W> g, ArenaView<W> src, P prod,
                                                  HashTable<W> t, uint32_t* rec_slot, unsigned long long seed,
@@ -423,6 +427,9 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
     // item share their old z, so a warp's records fall into few new groups)
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t i0 = 0; i0 < it.len; i0 += kCta) {
+      // the table is too small (the host retries with a larger one): stop
+      // probing it -- a full table costs a whole probe sequence per string
+      if (__any_sync(0xffffffffu, *(volatile const unsigned int*)&st->overflow != 0u)) break;  // (warp-uniform)
       const uint32_t i = i0 + threadIdx.x;
       uint32_t slot_out = 0xffffffffu;
       if (i < it.len) {
@@ -449,7 +456,7 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
             }
             if (cur == f) break;
             sl = (sl + 1) & t.mask;
-            if (probe > t.mask) {
+            if (probe > min(t.mask, (unsigned long long)kMaxProbe)) {
               atomicOr(&st->overflow, 1u);
               break;
             }
@@ -463,6 +470,7 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
     }
   } else {
   for (uint32_t i = threadIdx.x; i < it.len; i += kCta) {
+    if (*(volatile const unsigned int*)&st->overflow) break;  // (as above)
     Record<W> rec[P::kMaxRec];
     uint32_t nr = 0;
     const Plane<W> xi = load_plane<W>(src.x, off + i);
@@ -489,7 +497,7 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
           }
           if (cur == f) break;
           s = (s + 1) & t.mask;
-          if (probe > t.mask) {
+          if (probe > min(t.mask, (unsigned long long)kMaxProbe)) {
             atomicOr(&st->overflow, 1u);
             break;
           }
