@@ -1713,23 +1713,11 @@ __device__ __forceinline__ void dense_fast_pass(double* d, uint32_t npts, const 
       off[e] = b ^ o;
       a[e] = d[off[e]];
     }
-    // live mask of the block (a live value is >= kFastLive, anything else is
-    // an exact zero): all dead -- nothing to do, nothing to store -- and all
-    // live are the common cases, found with one OR / one min over the block
-    uint32_t orv = 0, imin = 0xffffffffu;
+    uint32_t mask = 0;
 #pragma unroll
-    for (int e = 0; e < N; ++e) {
-      orv |= (uint32_t)__double2hiint(a[e]);
-      imin = min(imin, (uint32_t)__double2hiint(a[e]) << 1);
-    }
-    if (!(orv << 1)) continue;
-    uint32_t mask = (1u << N) - 1u;
-    if (imin < 2u * kFastLiveHi) {
-      mask = 0;
-#pragma unroll
-      for (int e = 0; e < N; ++e)
-        if ((uint32_t)__double2hiint(a[e]) << 1) mask |= 1u << e;
-    }
+    for (int e = 0; e < N; ++e)
+      if ((uint32_t)__double2hiint(a[e]) << 1) mask |= 1u << e;
+    if (!mask) continue;  // nothing live: nothing to do, nothing to store
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       records += __popc(mask);

@@ -427,9 +427,6 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
     // item share their old z, so a warp's records fall into few new groups)
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t i0 = 0; i0 < it.len; i0 += kCta) {
-      // the table is too small (the host retries with a larger one): stop
-      // probing it -- a full table costs a whole probe sequence per string
-      if (__any_sync(0xffffffffu, *(volatile const unsigned int*)&st->overflow != 0u)) break;  // (warp-uniform)
       const uint32_t i = i0 + threadIdx.x;
       uint32_t slot_out = 0xffffffffu;
       if (i < it.len) {
@@ -456,6 +453,9 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
             }
             if (cur == f) break;
             sl = (sl + 1) & t.mask;
+            // a table that is too small (the host retries with a larger one):
+            // stop probing it once anyone has found out
+            if ((probe & 63) == 63 && *(volatile const unsigned int*)&st->overflow) break;
             if (probe > min(t.mask, (unsigned long long)kMaxProbe)) {
               atomicOr(&st->overflow, 1u);
               break;
@@ -470,7 +470,6 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
     }
   } else {
   for (uint32_t i = threadIdx.x; i < it.len; i += kCta) {
-    if (*(volatile const unsigned int*)&st->overflow) break;  // (as above)
     Record<W> rec[P::kMaxRec];
     uint32_t nr = 0;
     const Plane<W> xi = load_plane<W>(src.x, off + i);
@@ -497,6 +496,7 @@ __global__ void __launch_bounds__(kCta) k_insert(const Item* items, GroupView<W>
           }
           if (cur == f) break;
           s = (s + 1) & t.mask;
+          if ((probe & 63) == 63 && *(volatile const unsigned int*)&st->overflow) break;
           if (probe > min(t.mask, (unsigned long long)kMaxProbe)) {
             atomicOr(&st->overflow, 1u);
             break;
