@@ -1713,10 +1713,11 @@ __device__ __forceinline__ void dense_fast_pass(double* d, uint32_t npts, const 
       off[e] = b ^ o;
       a[e] = d[off[e]];
     }
-    uint32_t mask = 0;
+    uint32_t mk[4] = {0, 0, 0, 0};  // (four short dependency chains instead of one long one)
 #pragma unroll
     for (int e = 0; e < N; ++e)
-      if ((uint32_t)__double2hiint(a[e]) << 1) mask |= 1u << e;
+      if ((uint32_t)__double2hiint(a[e]) << 1) mk[e & 3] |= 1u << e;
+    uint32_t mask = (mk[0] | mk[1]) | (mk[2] | mk[3]);
     if (!mask) continue;  // nothing live: nothing to do, nothing to store
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -1735,16 +1736,16 @@ __device__ __forceinline__ void dense_fast_pass(double* d, uint32_t npts, const 
       // leaves a zero there: caught like any other small value)
       const uint32_t lowhalf = (i == 0 ? 0x5555u : i == 1 ? 0x3333u : i == 2 ? 0x0f0fu : 0x00ffu) & ((1u << N) - 1u);
       mask |= ((mask & lowhalf) << (1 << i)) | ((mask >> (1 << i)) & lowhalf);
-      uint32_t umin = 0xffffffffu;
+      uint32_t um[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
       if (mask == (1u << N) - 1u) {
 #pragma unroll
-        for (int e = 0; e < N; ++e) umin = min(umin, (uint32_t)__double2hiint(a[e]) << 1);
+        for (int e = 0; e < N; ++e) um[e & 3] = min(um[e & 3], (uint32_t)__double2hiint(a[e]) << 1);
       } else {
 #pragma unroll
         for (int e = 0; e < N; ++e)
-          if ((mask >> e) & 1u) umin = min(umin, (uint32_t)__double2hiint(a[e]) << 1);
+          if ((mask >> e) & 1u) um[e & 3] = min(um[e & 3], (uint32_t)__double2hiint(a[e]) << 1);
       }
-      anom |= umin < 2u * kFastLiveHi;
+      anom |= min(min(um[0], um[1]), min(um[2], um[3])) < 2u * kFastLiveHi;
     }
 #pragma unroll
     for (int e = 0; e < N; ++e) d[off[e]] = a[e];
