@@ -2468,10 +2468,11 @@ class EngineImpl final : public EngineBase {
       // smaller target would overflow there and compact)
       ensure_arena(o, std::max<uint64_t>(regroup_arena(total_bound), std::min<uint64_t>(arena_[cur_].cap, arena_max_)));
       k_table_emit<W><<<(uint32_t)((tc + kCta - 1) / kCta), kCta, 0, stream_>>>(
-          t, scan_gid_.as<unsigned long long>(), scan_off_.as<unsigned long long>(), gview(1 - gcur_), 0);
+          t, scan_gid_.as<unsigned long long>(), scan_off_.as<unsigned long long>(), gview(1 - gcur_), 0,
+          P::kMaxRec == 1 ? 1 : 0);
       k_scatter<W, P><<<(uint32_t)n_items, kCta, 0, stream_>>>(items_.as<Item>(), gview(gcur_), aview(cur_), prod, t,
                                                                rec_slot_.as<uint32_t>(), gview(1 - gcur_), aview(o),
-                                                               d_stats_);
+                                                               d_stats_, scan_off_.as<unsigned long long>());
       launches_ += 2;
       if (!small) {
         fetch_stats();

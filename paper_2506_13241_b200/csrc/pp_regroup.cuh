@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kCta) k_scan_apply(const uint32_t* in, unsigne
 // new group table from the hash table (slot order => deterministic ids)
 template <int W>
 __global__ void k_table_emit(HashTable<W> t, const unsigned long long* gid_scan, const unsigned long long* off_scan,
-                             GroupView<W> ng, uint64_t arena_base) {
+                             GroupView<W> ng, uint64_t arena_base, int final_counts = 0) {
   unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (s > t.mask) return;
   uint32_t c = t.count[s];
@@ -623,7 +623,9 @@ __global__ void k_table_emit(HashTable<W> t, const unsigned long long* gid_scan,
   for (int k = 0; k < W; ++k) ng.z[k][gid] = t.z[k][s];
   ng.off[gid] = arena_base + off_scan[s];
   ng.cap[gid] = c;
-  ng.cnt[gid] = 0;  // scatter cursor
+  // scatter cursor; final_counts: the scatter takes its positions from the
+  // table's slot counts (one record per string) and the group count is final
+  ng.cnt[gid] = final_counts ? c : 0;
   ng.flags[gid] = 0;
   ng.stamp[gid] = 0xffffffffu;
 }
@@ -631,34 +633,45 @@ __global__ void k_table_emit(HashTable<W> t, const unsigned long long* gid_scan,
 template <int W, class P>
 __global__ void __launch_bounds__(kCta) k_scatter(const Item* items, GroupView<W> g, ArenaView<W> src, P prod,
                                                   HashTable<W> t, const uint32_t* rec_slot, GroupView<W> ng,
-                                                  ArenaView<W> dst, DevStats* st) {
+                                                  ArenaView<W> dst, DevStats* st,
+                                                  const unsigned long long* off_scan = nullptr) {
   if (blockIdx.x >= *(volatile const unsigned long long*)&st->items) return;
   const Item it = items[blockIdx.x];
   const uint64_t off = g.off[it.g] + it.start;
   const Plane<W> z = load_plane<W>(g.z, it.g);
   if constexpr (P::kMaxRec == 1) {
-    // positions reserved per warp and new group (one atomic per group per warp)
+    // positions reserved per warp and new group (one atomic per group per
+    // warp), straight from the table slot: the slot's record count (final
+    // after k_insert) is drawn down as the cursor and its offset comes from
+    // the scan -- slot verify, offset and cursor are independent loads, two
+    // dependent round trips per string instead of four (slot -> group id ->
+    // group offset -> cursor)
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t i0 = 0; i0 < it.len; i0 += kCta) {
       const uint32_t i = i0 + threadIdx.x;
-      uint32_t gid = 0xffffffffu;
+      uint32_t sl = 0xffffffffu;
       Record<W> rec[1];
+      unsigned long long so = 0;
       if (i < it.len) {
         uint32_t nr;
         const int nrec = prod.emit(load_plane<W>(src.x, off + i), z, src.c[off + i], rec, &nr);
         if (nrec) {
-          const uint32_t sl = rec_slot[it.rbase + i];
-          if (!plane_eq<W>(load_plane<W>(t.z, sl), rec[0].z)) atomicOr(&st->collision, 1u);  // fingerprint collision
-          else gid = t.gid[sl];
+          sl = rec_slot[it.rbase + i];
+          so = off_scan[sl];
+          if (!plane_eq<W>(load_plane<W>(t.z, sl), rec[0].z)) {  // fingerprint collision
+            atomicOr(&st->collision, 1u);
+            sl = 0xffffffffu;
+          }
         }
       }
-      const uint32_t mm = __match_any_sync(0xffffffffu, gid);
-      if (gid != 0xffffffffu) {
+      const uint32_t mm = __match_any_sync(0xffffffffu, sl);
+      if (sl != 0xffffffffu) {
         const uint32_t leader = __ffs(mm) - 1;
-        unsigned long long base = 0;
-        if (lane == leader) base = atomicAdd(&ng.cnt[gid], (unsigned)__popc(mm));
+        const uint32_t k = (uint32_t)__popc(mm);
+        uint32_t base = 0;
+        if (lane == leader) base = atomicSub(&t.count[sl], k) - k;
         base = __shfl_sync(mm, base, leader);
-        const uint64_t pos = ng.off[gid] + base + __popc(mm & ((1u << lane) - 1u));
+        const uint64_t pos = so + base + __popc(mm & ((1u << lane) - 1u));
         store_plane<W>(dst.x, pos, rec[0].x);
         dst.c[pos] = rec[0].c;
       }
