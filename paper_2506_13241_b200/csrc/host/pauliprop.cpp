@@ -710,6 +710,12 @@ static pp_gate to_pp(const Gate& g) {
 void Engine::check(int rc) const {
   if (rc == PP_OK) return;
   std::string msg = pp_last_error(handle_);
+  // the reference names the layer next to the gate (engine.cpp:269-273,
+  // 334-338: "... at layer L, gate G"); the device library knows the gate only
+  if (rc == PP_ERR_RESOURCE || rc == PP_ERR_NUMERICAL) {
+    const size_t at = msg.find(" at gate ");
+    if (at != std::string::npos) msg.replace(at, 9, " at layer " + std::to_string(layer_context_) + ", gate ");
+  }
   switch (rc) {
     case PP_ERR_INVALID: throw std::invalid_argument(msg);
     case PP_ERR_NUMERICAL: throw NumericalError(msg);

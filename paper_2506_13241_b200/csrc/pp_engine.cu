@@ -908,6 +908,7 @@ class EngineImpl final : public EngineBase {
       sync_state();
       if (bump_ + 2 * live_ > arena_[cur_].cap) gc_into_other(next_arena_target());
       const bool use_graph = pos == 0 && !(cfg_.flags & PP_FLAG_PROFILE);
+      err_base_ = gates_applied_ + pos;  // gates applied before this launch run's gate 0
       push_scalars(seq0 + pos);
       if (lazy) {
         PP_CUDA(cudaMemsetAsync(thr_.p, 0, 2 * sizeof(double), stream_));
@@ -1952,6 +1953,7 @@ class EngineImpl final : public EngineBase {
     }
     push_scalars(bseq_);
     if (G_) {
+      err_base_ = gates_applied_ ? gates_applied_ - 1 : 0;  // the gate(s) just applied are counted already
       launch_epilogue(0, do_truncate, budget);
       if (do_truncate) may_hold_zeros_ = false;
     }
@@ -2037,11 +2039,11 @@ class EngineImpl final : public EngineBase {
       dirty_ = false;
       throw EngineError(PP_ERR_RESOURCE, "term budget exhausted: |O|=" + std::to_string(st.err_live) +
                                              " exceeds max_terms=" + std::to_string(cfg_.max_terms) + " at gate " +
-                                             std::to_string(st.err_gate + 1));
+                                             std::to_string(err_base_ + st.err_gate + 1));
     }
     if (st.err_numerical) {
       dirty_ = false;
-      throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient at gate " + std::to_string(st.err_gate + 1) +
+      throw EngineError(PP_ERR_NUMERICAL, "non-finite coefficient at gate " + std::to_string(err_base_ + st.err_gate + 1) +
                                               ", |O|=" + std::to_string(st.err_live));
     }
     arena_fault_ = st.err_arena != 0;
@@ -2150,6 +2152,7 @@ class EngineImpl final : public EngineBase {
           &d_stats_->work[1], 0, d_stats_, lazy ? thr_.as<double>() : nullptr, lazy ? &d_stats_->red[0] : nullptr);
       launches_ += 2;
       ++branch_launches_;
+      err_base_ = gates_applied_;  // (this gate is counted after its launches)
       if (epi) launch_epilogue(0, do_trunc, budget, lazy);
       dirty_ = true;
       fetch_stats();  // the gate's one round trip: new groups, arena fault
@@ -2714,6 +2717,7 @@ class EngineImpl final : public EngineBase {
   unsigned long long h_records_ = 0;
   pp_counters counters_{};
   uint64_t gates_applied_ = 0;
+  uint64_t err_base_ = 0;  // gates applied before relative gate 0 of the launches in flight (error messages)
   int layer_ = 0;
   double branch_ms_ = 0.0, branch_bytes_ = 0.0;
   uint64_t branch_in_ = 0, branch_stream_ = 0;

@@ -216,6 +216,48 @@ def test_budget_and_nan(pp, O):
         eng.apply_gate(pp.Gate(pp.PauliString("X0", 2), 0.3))
 
 
+@pytest.mark.parametrize("eps,limit", [(0.0, 1000), (1e-3, 200), (0.0, 40)])
+def test_budget_error_fires_where_the_reference_fires(pp, O, eps, limit):
+    """check_budget (engine.cpp:266-275): the error comes after the same gate
+    of the same layer with the same |O| (counted before that gate's
+    truncation) as in the oracle, through run_circuit (fused Clifford runs,
+    Rx runs) and gate by gate."""
+    import re
+
+    geom = pp.heavy_hex_127()
+    circ = _kicked(pp, geom, "0.3pi", 6)
+    init = O.site_word(62, 3)[None]
+    ora = O.OracleEngine(127, eps, max_terms=limit)
+    ora.set_initial(init, [1.0])
+    expect = None
+    L = len(circ.layers)
+    for t in range(1, L + 1):
+        for k, g in enumerate(reversed(list(circ.layers[L - t]))):
+            try:
+                ora.apply_gate(np.asarray(g.generator.words), g.cos_theta, g.sin_theta)
+            except O.OracleError:
+                expect = (t, ora.take_counters()["gates"], ora.term_count())
+                break
+        if expect:
+            break
+    assert expect is not None, "the budget must be exceeded in this circuit"
+    for per_gate in (False, True):
+        eng = pp.Engine(127, eps, "gate", max_terms=limit)
+        eng.set_initial(init, np.array([1.0]))
+        with pytest.raises(pp.ResourceLimitError) as err:
+            if per_gate:
+                for t in range(1, L + 1):
+                    eng.set_layer_context(t)
+                    for g in reversed(list(circ.layers[L - t])):
+                        eng.apply_gate(g)
+            else:
+                eng.run_circuit(circ)
+        m = re.search(r"\|O\|=(\d+) exceeds max_terms=(\d+) at layer (\d+), gate (\d+)", str(err.value))
+        assert m, str(err.value)
+        assert (int(m.group(3)), int(m.group(4)), int(m.group(1))) == expect, (str(err.value), expect, per_gate)
+        assert int(m.group(2)) == limit
+
+
 def test_simulate_reference_smoke_values(pp):
     # tests/python/test_smoke.py:59-66 of the reference
     geom = pp.heavy_hex_127()

@@ -153,3 +153,37 @@ def test_plane_conversion_round_trip(O):
     for code, (ex, ez) in zip(range(4), [(0, 0), (1, 0), (1, 1), (0, 1)]):
         x, z = O.to_planes(O.site_word(5, code)[None])
         assert int(x[0][0]) == ex << 5 and int(z[0][0]) == ez << 5
+
+
+@pytest.mark.parametrize("eps,limit", [(0.0, 1000), (1e-3, 200), (0.0, 40)])
+def test_oracle_budget_error_matches_reference(O, eps, limit):
+    """check_budget (engine.cpp:266-275): the restatement refuses the same
+    gate with the same |O| as the reference engine (compiled from its sources,
+    oracle/_ref); the reference's message carries both."""
+    import re
+
+    if not O.ref_available():
+        pytest.skip("oracle/_ref is not built (needs /root/reference)")
+    layer = ref_order_layer(O, 127, 0.3, 1, -0.5, 1, "heavy_hex")
+    ref = O.RefEngine(127, eps, max_terms=limit)
+    ora = O.OracleEngine(127, eps, max_terms=limit)
+    init = O.site_word(62, 3)[None]
+    ref.set_initial(init, [1.0])
+    ora.set_initial(init, [1.0])
+    ref_gates = [(w, 0.3 if c != 0.0 and abs(s) != 1.0 else -0.5, 1) for (w, c, s) in layer]
+    with pytest.raises(O.OracleError) as err:
+        for _ in range(8):
+            ref.run_circuit(ref_gates)
+    m = re.search(r"\|O\|=(\d+) exceeds max_terms=(\d+) at layer (\d+), gate (\d+)", str(err.value))
+    assert m, str(err.value)
+    got = None
+    for _ in range(8):
+        for w, c, s in reversed(layer):
+            try:
+                ora.apply_gate(w, c, s)
+            except O.OracleError:
+                got = (ora.take_counters()["gates"], ora.term_count())
+                break
+        if got:
+            break
+    assert got == (int(m.group(4)), int(m.group(1))), (str(err.value), got)
