@@ -1359,6 +1359,10 @@ class EngineImpl final : public EngineBase {
     const double frac = cfg_.mem_fraction > 0 && cfg_.mem_fraction <= 1 ? cfg_.mem_fraction : 0.92;
     const double budget = (double)avail * frac - (double)(3ull << 30);
     arena_max_ = budget > 0 ? (uint64_t)(budget / (double)(2 * R + 16)) : (1ull << 20);
+    // a coarse grain: free memory wobbles by a few MB from call to call, and an
+    // engine that asks for a slightly larger arena than the last one released
+    // misses the pool's cached block (a fresh cudaMalloc of tens of GB)
+    if (arena_max_ > (1ull << 28)) arena_max_ &= ~((1ull << 26) - 1);
   }
 
   // memory is short: free this device's parked engines and the pool's cache,
