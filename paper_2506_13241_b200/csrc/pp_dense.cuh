@@ -72,6 +72,9 @@ __global__ void __launch_bounds__(kCta, PP_DENSE_CTAS) k_dense_sublayer(GroupVie
     dc.tpred = nullptr;
     dc.smax = nullptr;
     dc.ng = gates.ng;
+    mbar_init(&dc.mbar, 1);
+    dc.mphase = 0;
+    dc.bulk_tiles = 0;
   }
   __syncthreads();
   const int ng = gates.ng;
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(kCta, PP_DENSE_CTAS) k_dense_sublayer(GroupVie
   for (int k = tid; k < ng; k += kCta)
     if (((s_seen[k >> 5] >> (k & 31)) & 1u) && s_gp.sinv[k] != 0.0) mark_seen(st, st->seen_base + k);
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
+  if (tid == 0 && dc.bulk_tiles) atomicAdd(&st->bulk_tiles, (unsigned long long)dc.bulk_tiles);
 }
 
 }  // namespace ppgpu

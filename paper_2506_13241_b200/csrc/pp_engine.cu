@@ -66,6 +66,7 @@ __global__ void k_clear_cumulative(DevStats* st) {
   st->cliff_records = 0;
   st->dense_groups = 0;
   st->dense_out = 0;
+  st->bulk_tiles = 0;
   for (int w = 0; w < kSeenWords; ++w) st->seen[w] = 0;
   for (int k = 0; k < kZZSeenGroups; ++k) st->zz_seen[k][0] = st->zz_seen[k][1] = 0;
 }
@@ -543,7 +544,7 @@ class EngineImpl final : public EngineBase {
     branch_bytes_ = 0.0;
     branch_launches_ = launches_ = 0;
     branch_in_ = branch_stream_ = 0;
-    dense_groups_ = dense_out_ = 0;
+    dense_groups_ = dense_out_ = bulk_tiles_ = 0;
     tr_layer_ns_ = tr_sync_ns_ = tr_syncs_ = tr_cliff_ns_ = tr_rx_ns_ = 0;
     set_initial(nullptr, nullptr, 0);  // the empty operator of a fresh engine
     counters_ = pp_counters{};
@@ -1781,8 +1782,9 @@ class EngineImpl final : public EngineBase {
     *bytes = branch_bytes_;
     last_stream_frac_ = branch_in_ ? (double)branch_stream_ / (double)branch_in_ : 0.0;
     if (std::getenv("PP_DEBUG"))
-      std::fprintf(stderr, "[pp] dense sublayer: %llu groups, %llu strings written\n",
-                   (unsigned long long)dense_groups_, (unsigned long long)dense_out_);
+      std::fprintf(stderr, "[pp] dense sublayer: %llu groups, %llu strings written, %llu big-block tiles by bulk copies\n",
+                   (unsigned long long)dense_groups_, (unsigned long long)dense_out_,
+                   (unsigned long long)bulk_tiles_);
     if (std::getenv("PP_DEBUG")) std::fprintf(stderr, "[pp] branch strings %llu, via long-block stream path %.3f\n",
                                               (unsigned long long)branch_in_, last_stream_frac_);
     branch_in_ = branch_stream_ = 0;
@@ -2080,6 +2082,7 @@ class EngineImpl final : public EngineBase {
     branch_stream_ += st.stream_elems;
     dense_groups_ += st.dense_groups;
     dense_out_ += st.dense_out;
+    bulk_tiles_ += st.bulk_tiles;
     k_clear_cumulative<<<1, 1, 0, stream_>>>(d_stats_);
     ++launches_;
     dirty_ = false;
@@ -2633,7 +2636,7 @@ class EngineImpl final : public EngineBase {
   uint64_t tr_cliff_ns_ = 0, tr_rx_ns_ = 0;
   std::vector<pp_gate> plan_key_;  // apply_gates_async run partition cache
   std::vector<PlanRun> plan_;
-  uint64_t dense_groups_ = 0, dense_out_ = 0;
+  uint64_t dense_groups_ = 0, dense_out_ = 0, bulk_tiles_ = 0;
   std::vector<pp_gate> rx_key_;  // run_rx plan cache
   std::vector<RxParam> rx_prm_;
   SubGates rx_sg_{};

@@ -145,6 +145,7 @@ struct DevStats {
   unsigned long long cliff_records; // records of a regroup whose sizes the host reads later (deferred)
   unsigned long long dense_groups;  // groups applied by the dense sublayer path (cumulative)
   unsigned long long dense_out;     // strings those groups wrote
+  unsigned long long bulk_tiles;    // dense_passes tiles moved by bulk copies (cumulative)
   unsigned int seen_base;           // window index of gate 0 of the current launch run
   unsigned int left_n;              // groups k_dense_sublayer left for the per-gate path (this launch)
   unsigned long long seen[kSeenWords];            // bit g: window gate g sent a record
@@ -1428,6 +1429,9 @@ struct DenseCtl {
   unsigned long long wmax[2][kWarps];  // per-warp stage max, by stage parity
   uint32_t zeros;               // multi-class: zero points written (holes to compact)
   uint32_t fast;                // this group's butterflies take dense_bfly_fast (see there)
+  unsigned long long mbar;      // mbarrier of dense_passes' bulk tile loads (initialised once per CTA)
+  uint32_t mphase;              //   its phase parity
+  uint32_t bulk_tiles;          //   tiles it moved (diagnostics)
 };
 
 template <int W>
@@ -1793,6 +1797,47 @@ __device__ __forceinline__ void dense_stages(double* d, uint32_t u, uint32_t P, 
   else dense_stages_t<W, false>(d, u, P, j0, j1, dc, records, removed, count, anom);
 }
 
+// ---- bulk copies (TMA engine, cp.async.bulk) between a block in global
+// memory and the shared-memory tile, completion on an mbarrier: one
+// instruction moves a whole contiguous tile row, no registers, no LSU slots
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t arrivals) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(arrivals));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "PP_MBAR_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra PP_MBAR_DONE;\n"
+      "bra PP_MBAR_WAIT;\n"
+      "PP_MBAR_DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_global, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src_global), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst_global, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_global), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
 // Stages of a block of S > kDenseSmem points in global memory (L2): passes
 // of up to kDenseSmemLog stages, each over full shared-memory tiles (the
 // cosets of the pass's stage bits, padded with low bits).
@@ -1821,22 +1866,56 @@ __device__ void dense_passes(double* dbuf, double* blk, uint32_t S, DenseCtl<W>&
       else if (tid < 192) dc.dephi[tid - 128] = dense_dep32(tid - 128, plo);
     }
     __syncthreads();
+    // Tile rows: P's low bits up to its first gap are contiguous in the block,
+    // 2^L points per row.  Rows of at least 512 bytes move as bulk copies (one
+    // cp.async.bulk per row, completion on the CTA's mbarrier); shorter rows
+    // element by element.
+    const uint32_t L = (uint32_t)__ffs((int)~P) - 1u;
+    const bool bulk = L >= 6 && (reinterpret_cast<uintptr_t>(blk) & 15u) == 0;
+    const uint32_t rows = (1u << u) >> L, rbytes = 8u << L;
+    if (bulk) proxy_fence();  // this thread's earlier writes to the block, before the copy engine reads it
+    __syncthreads();
     for (uint32_t sp = 0; sp < (S >> u); ++sp) {
       const uint32_t base = dense_dep32(sp, Q);
-      // 8 loads in flight per thread (the block sits in L2)
-      for (uint32_t i0 = 0; i0 < (1u << u); i0 += 8 * kCta) {
-        double t[8];
-#pragma unroll
-        for (uint32_t e = 0; e < 8; ++e) {
-          const uint32_t i = i0 + e * kCta + tid;
-          t[e] = blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]];
+      if (bulk) {
+        if (tid == 0) {
+          mbar_expect_tx(&dc.mbar, 8u << u);
+          ++dc.bulk_tiles;
         }
+        for (uint32_t r = tid; r < rows; r += kCta) {
+          const uint32_t i = r << L;
+          bulk_g2s(dbuf + i, blk + (base | dc.deplo[i & 127] | dc.dephi[i >> 7]), rbytes, &dc.mbar);
+        }
+        mbar_wait(&dc.mbar, dc.mphase & 1u);
+        __syncthreads();
+        if (tid == 0) dc.mphase ^= 1u;
+      } else {
+        // 8 loads in flight per thread (the block sits in L2)
+        for (uint32_t i0 = 0; i0 < (1u << u); i0 += 8 * kCta) {
+          double t[8];
 #pragma unroll
-        for (uint32_t e = 0; e < 8; ++e) dbuf[i0 + e * kCta + tid] = t[e];
+          for (uint32_t e = 0; e < 8; ++e) {
+            const uint32_t i = i0 + e * kCta + tid;
+            t[e] = blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]];
+          }
+#pragma unroll
+          for (uint32_t e = 0; e < 8; ++e) dbuf[i0 + e * kCta + tid] = t[e];
+        }
+        __syncthreads();
       }
-      __syncthreads();
       dense_stages<W>(dbuf, u, P, j0, j1, dc, records, removed, 0, anom, fast);
-      for (uint32_t i = tid; i < (1u << u); i += kCta) blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]] = dbuf[i];
+      if (bulk) {
+        proxy_fence();  // the tile's generic-proxy writes, before the copy engine reads them
+        __syncthreads();
+        for (uint32_t r = tid; r < rows; r += kCta) {
+          const uint32_t i = r << L;
+          bulk_s2g(blk + (base | dc.deplo[i & 127] | dc.dephi[i >> 7]), dbuf + i, rbytes);
+        }
+        bulk_commit_wait();  // (threads without a row have nothing to wait for)
+        proxy_fence();       // the block is read with ordinary loads again afterwards
+      } else {
+        for (uint32_t i = tid; i < (1u << u); i += kCta) blk[base | dc.deplo[i & 127] | dc.dephi[i >> 7]] = dbuf[i];
+      }
       __syncthreads();
     }
   }
@@ -2568,6 +2647,9 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
     dc.tpred = tpred ? s_tpred : nullptr;
     dc.smax = smax;
     dc.ng = gates.ng;
+    mbar_init(&dc.mbar, 1);
+    dc.mphase = 0;
+    dc.bulk_tiles = 0;
   }
   __syncthreads();
   unsigned long long aff_elems = 0;
@@ -2839,6 +2921,7 @@ __global__ void __launch_bounds__(kCta, 2) k_branch_sublayer(GroupView<W> g, Are
   for (int k = tid; k < gates.ng; k += kCta)
     if (((s_seen[k >> 5] >> (k & 31)) & 1u) && s_gp.sinv[k] != 0.0) mark_seen(st, st->seen_base + k);
   if (tid == 0 && aff_elems) atomicAdd(&st->aff_total, aff_elems);
+  if (tid == 0 && dc.bulk_tiles) atomicAdd(&st->bulk_tiles, (unsigned long long)dc.bulk_tiles);
 }
 
 // ---------------------------------------------------------------------------
