@@ -160,6 +160,15 @@ __device__ __forceinline__ unsigned long long warp_min_bits(unsigned long long v
   return ((unsigned long long)mh << 32) | ml;
 }
 
+// the same for non-negative doubles (or +inf) held as doubles: |c| maxima and
+// minima (fmax / fmin never leave a NaN in them)
+__device__ __forceinline__ double warp_max_nn(double v) {
+  return __longlong_as_double((long long)warp_max_bits((unsigned long long)__double_as_longlong(v)));
+}
+__device__ __forceinline__ double warp_min_nn(double v) {
+  return __longlong_as_double((long long)warp_min_bits((unsigned long long)__double_as_longlong(v)));
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

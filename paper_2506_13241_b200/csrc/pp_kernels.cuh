@@ -3093,8 +3093,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_spec_small(GroupView<W> g,
       mx = fmax(mx, fabs(v));
       mn = fmin(mn, fabs(v));
     }
-    mx = warp_max(mx);
-    mn = warp_min(mn);
+    mx = warp_max_nn(mx);
+    mn = warp_min_nn(mn);
     __syncwarp();
     w_in += n;
     uint32_t nonfinite = 0;
@@ -3132,8 +3132,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_spec_small(GroupView<W> g,
       }
       g_removed += n - out;
       n = out;
-      mx = warp_max(kmx);
-      mn = warp_min(kmn);
+      mx = warp_max_nn(kmx);
+      mn = warp_min_nn(kmn);
     };
     for (int t = 0;; ++t) {
       // next touching gate at or after last + 1 (ng: the end step)
@@ -3256,7 +3256,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_spec_small(GroupView<W> g,
       recs = warp_sum64(recs);
       g_records += recs;
       if (recs && lane == 0) seen_local[k >> 5] |= 1u << (k & 31);
-      gmx = warp_max(gmx);
+      gmx = warp_max_nn(gmx);
       if (lane == 0) contribute(k, gmx);  // gmax after gate k's apply, before its truncation
       mx = gmx;
       mn = 0.0;  // (force the truncation below)
