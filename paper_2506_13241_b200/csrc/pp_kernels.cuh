@@ -3167,7 +3167,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_spec_small(GroupView<W> g,
       const int wq = s_wq[k];
       const uint64_t mq = s_mq[k];
       const double cosv = s_cos[k], sinv = s_sin[k], nsin = -sinv;
-      for (uint32_t sl = lane; sl < 2 * kSmallCap; sl += 32) ht[sl] = 0u;
+      for (uint32_t sl = lane; sl < 2 * kSmallCap / 4; sl += 32) reinterpret_cast<uint4*>(ht)[sl] = make_uint4(0u, 0u, 0u, 0u);
       __syncwarp();
       for (uint32_t i = lane; i < n; i += 32) {
         uint32_t h = small_hash<W>(xs, i);
@@ -3253,7 +3253,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_spec_small(GroupView<W> g,
         break;
       }
       n += added;
-      recs = warp_sum64(recs);
+      recs = __reduce_add_sync(0xffffffffu, (uint32_t)recs);  // (at most 2 per string and lane pass: far below 2^32)
       g_records += recs;
       if (recs && lane == 0) seen_local[k >> 5] |= 1u << (k & 31);
       gmx = warp_max_nn(gmx);
