@@ -3003,9 +3003,16 @@ __global__ void k_use_group_count(DevStats* st, const unsigned int* count, unsig
 // buffer is left untouched for k_branch_sublayer; finished groups are
 // flagged in spec_done (cleared per attempt) so k_branch_sublayer skips them.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kSmallCap = 512;       // strings per warp buffer
-constexpr uint32_t kSmallWarps = 4;       // warps (groups in flight) per CTA
-constexpr uint32_t kSmallMaxIn = 256;     // groups of at most this many strings start here
+// (measured on the config-2 shape: 256 strings x 8 warps 50.5 ms per step, 512 x 4 53.8, 128 x 8 57.4, 1024 x 2 83.3)
+#ifndef PP_SMALL_CAP
+#define PP_SMALL_CAP 256
+#endif
+#ifndef PP_SMALL_WARPS
+#define PP_SMALL_WARPS 8
+#endif
+constexpr uint32_t kSmallCap = PP_SMALL_CAP;       // strings per warp buffer
+constexpr uint32_t kSmallWarps = PP_SMALL_WARPS;   // warps (groups in flight) per CTA
+constexpr uint32_t kSmallMaxIn = kSmallCap / 2;    // groups of at most this many strings start here
 
 template <int W>
 constexpr size_t spec_small_smem_bytes() {
