@@ -3012,7 +3012,10 @@ __global__ void k_use_group_count(DevStats* st, const unsigned int* count, unsig
 #endif
 constexpr uint32_t kSmallCap = PP_SMALL_CAP;       // strings per warp buffer
 constexpr uint32_t kSmallWarps = PP_SMALL_WARPS;   // warps (groups in flight) per CTA
-constexpr uint32_t kSmallMaxIn = kSmallCap / 2;    // groups of at most this many strings start here
+#ifndef PP_SMALL_MAXIN
+#define PP_SMALL_MAXIN (PP_SMALL_CAP / 2)
+#endif
+constexpr uint32_t kSmallMaxIn = PP_SMALL_MAXIN;   // groups of at most this many strings start here
 
 template <int W>
 constexpr size_t spec_small_smem_bytes() {
