@@ -2416,6 +2416,7 @@ class EngineImpl final : public EngineBase {
       // overflow retries with a 4x larger table
       const double est = std::max(2.0, 1.5 * zfactor_) * (double)G_;
       while ((double)tc < 2.0 * std::min<double>((double)records_upper, est) + 1024) tc <<= 1;
+      if (std::getenv("PP_TINY_TABLE")) tc = 1024;  // test hook: overflow and the 4x retries
     }
     uint64_t tc_max = 1024;
     while (tc_max < 2 * records_upper + 1024) tc_max <<= 1;

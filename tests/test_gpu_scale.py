@@ -166,3 +166,26 @@ def test_config0_t10_properties(pp, O):
         assert abs(got - want) <= 1e-12, (i, got, want)
         nonzero += abs(want) > 1e-9
     assert nonzero >= 8, "sampled keys should mostly be live strings"
+
+
+def test_regroup_table_overflow_retries(pp, O, monkeypatch):
+    """A regroup whose hash table is far too small (PP_TINY_TABLE: 1024 slots
+    for 7e6 records) gives up probing early (k_insert's probe cap and overflow
+    flag), retries with tables 4x larger, and ends with the same operator:
+    config 0 to t = 9, ledgers and sum c^2 against the run with the planned
+    table."""
+    circ = pp.build_kicked_ising(chain_geometry(pp), 0.3, "-0.5pi", 9)
+    init = O.site_word(32, 3)[None]
+
+    def run():
+        eng = pp.Engine(64, 0.0)
+        eng.set_initial(init, np.array([1.0]))
+        rows = eng.run_circuit(circ)
+        return [{k: v for k, v in r.items() if k != "wall_ms_per_gate"} for r in rows], eng.norm2()
+
+    ref_rows, ref_norm = run()
+    monkeypatch.setenv("PP_TINY_TABLE", "1")
+    rows, norm = run()
+    assert rows == ref_rows
+    assert abs(norm - ref_norm) < 1e-12  # (summed in group order, which follows the table's slot order)
+    assert rows[-1]["term_count"] == 81662152
