@@ -1428,7 +1428,7 @@ struct DenseCtl {
   double strunc[kMaxSubGates];  // threshold of the window after stage s (its gate .. the next stage's)
   unsigned long long wmax[2][kWarps];  // per-warp stage max, by stage parity
   uint32_t zeros;               // multi-class: zero points written (holes to compact)
-  uint32_t fast;                // this group's butterflies take dense_bfly_fast (see there)
+  uint32_t fast;                // this group's butterflies take dense_stages_fast (see there)
   unsigned long long mbar;      // mbarrier of dense_passes' bulk tile loads (initialised once per CTA)
   uint32_t mphase;              //   its phase parity
   uint32_t bulk_tiles;          //   tiles it moved (diagnostics)
@@ -2565,7 +2565,7 @@ __device__ int dense_group(double* dbuf, DenseCtl<W>& dc, GroupStatsSmem& gs, ui
   __syncthreads();
   const int m = dc.m;
   if (m == 0 || m > kDenseMaxLog) return 0;
-  // bookkeeping-free butterflies (dense_bfly_fast) when the run's angles and
+  // bookkeeping-free butterflies (dense_stages_fast) when the run's angles and
   // the group's values are far from underflow; anything else is caught there
   if (tid == 0) dc.fast = (!dc.tpred && gates.fast && g.gmin[gid] >= kFastLive) ? 1u : 0u;
   const Plane<W> T = dc.T;

@@ -389,7 +389,7 @@ def test_engine_pool_reuse_is_fresh(pp, O):
 def test_chain_config0_t8_dense_big_blocks(pp, O):
     """BASELINE config 0 to t = 8 (6,952,660 strings): the last Rx run has
     groups of several x classes with 2^m > one shared-memory tile (the dense
-    path's global-memory passes, rank interleave and hole compaction) --
+    path's global-memory passes, class-major output and hole compaction) --
     bit-exact against the oracle."""
     text = "\n".join(f"{i} {i + 1} {i % 2}" for i in range(63))
     circ = pp.build_kicked_ising(pp.load_geometry(text), 0.3, "-0.5pi", 8)
@@ -400,8 +400,8 @@ def test_chain_config0_t8_dense_big_blocks(pp, O):
 @pytest.mark.parametrize("n", [64, 127])
 def test_dense_big_and_multiclass_blocks(pp, O, n):
     """Groups built to take every dense sub-path in one Rx layer: several x
-    classes with 2^m above a shared-memory tile (global passes, rank
-    interleave), several classes batched through one tile, and one class of
+    classes with 2^m above a shared-memory tile (global passes, bulk-copied
+    tile rows, class-major output), several classes batched through one tile, and one class of
     several strings with 2^m above a tile -- bit-exact against the oracle."""
     rng = np.random.default_rng(n)
 
